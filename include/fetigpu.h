@@ -1,0 +1,199 @@
+/*
+ * fetigpu.h -- C-ABI of the B200-native FETI dual-operator engine.
+ *
+ * This is the drop-in boundary for the hot path of arxiv 2111.11728's FETI
+ * solvers.  The reference declares its solver entry points as
+ * SPEC contracts over the building blocks in proj/include/feti; each function
+ * below replaces one of them (file:line of the interface it stands in for):
+ *
+ *   fetigpu_create/build   build_partition + assemble_subdomain +
+ *                          apply_traction + build_constraints +
+ *                          build_coarse_space + k_scaling + build_tfeti /
+ *                          build_fetidp + dirichlet_schur/lumped
+ *                          (decomposition.hpp:47-180, fem.cpp:86-167,
+ *                           SPEC.md:288-309,360-377)
+ *   fetigpu_apply_F        DualOperator::apply / TfetiSystem action
+ *                          F = sum_s B_s K_s^+ B_s^T (per
+ *                          subdomain SemidefiniteCholesky::solve_unchecked,
+ *                          linalg.hpp:113-114 + ConstraintSet::apply_BsT /
+ *                          accumulate_Bs, decomposition.hpp:98-101) and the
+ *                          condensed FETI-DP operator
+ *   fetigpu_apply_precond  apply_coarse_preconditioner
+ *   fetigpu_project        CoarseSpace::project / project_block
+ *                          (decomposition.hpp:136-138)
+ *   fetigpu_rhs            d = B K^+ f - c, lambda0 = G^T (G G^T)^{-1} e
+ *                          (decomposition.hpp:139-140) /
+ *                          FETI-DP rhs
+ *   fetigpu_solve          pcg / simultaneous_pcg
+ *   fetigpu_recover        recover_primal
+ *
+ * Conventions: plain pointers and sizes, no C++ or torch types.  Host
+ * pointers are borrowed for the duration of the call; *_device variants take
+ * device pointers and run on the context's stream.  Every function returns
+ * 0 on success or an error code mapped 1:1 to proj/include/feti/errors.hpp
+ * (FETIGPU_E_*).  Non-convergence is not an error: it is reported in
+ * fetigpu_trace.status.  A context is not reentrant
+ * (one call in flight per context); distinct contexts may be
+ * used from different host threads.
+ */
+#ifndef FETIGPU_H
+#define FETIGPU_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* error codes (errors.hpp:7-69, in declaration order) */
+enum {
+  FETIGPU_OK = 0,
+  FETIGPU_E_NOT_POSITIVE_DEFINITE = 1,
+  FETIGPU_E_INDEFINITE_INPUT = 2,
+  FETIGPU_E_INCOMPATIBLE_RHS = 3,
+  FETIGPU_E_EDGE_NOT_ON_BOUNDARY = 4,
+  FETIGPU_E_DIMENSION_MISMATCH = 5,
+  FETIGPU_E_NODE_NOT_FOUND = 6,
+  FETIGPU_E_INSUFFICIENT_CORNERS = 7,
+  FETIGPU_E_ZERO_STIFFNESS_DIAGONAL = 8,
+  FETIGPU_E_SINGULAR_INTERIOR = 9,
+  FETIGPU_E_COARSE_SINGULAR = 10,
+  FETIGPU_E_SINGULAR_REMAINDER = 11,
+  FETIGPU_E_SINGULAR_COARSE = 12,
+  FETIGPU_E_SINGULAR_GLOBAL = 13,
+  FETIGPU_E_NEGATIVE_INNER_PRODUCT = 14,
+  FETIGPU_E_NOT_CONVERGED = 15,
+  FETIGPU_E_STATE_SOLVE_FAILED = 16,
+  FETIGPU_E_CONFIG = 17,
+  FETIGPU_E_IO = 18,
+  FETIGPU_E_INVALID_ARGUMENT = 20, /* std::invalid_argument in fem.cpp */
+  FETIGPU_E_DOMAIN = 21,           /* std::domain_error in fem.cpp */
+  FETIGPU_E_CUDA = 100,
+  FETIGPU_E_NO_DEVICE = 101,
+  FETIGPU_E_OUT_OF_MEMORY = 102,
+  FETIGPU_E_STATE = 103            /* call order violated (e.g. apply before build) */
+};
+
+enum { FETIGPU_TFETI = 0, FETIGPU_FETIDP = 1 };
+enum { FETIGPU_MULTIPLICITY = 0, FETIGPU_KSCALING = 1 };
+enum { FETIGPU_LUMPED = 0, FETIGPU_DIRICHLET = 1, FETIGPU_SUPERLUMPED = 2 };
+enum { FETIGPU_SINGLE = 0, FETIGPU_FO = 1, FETIGPU_RRS = 2 };
+enum { FETIGPU_CONVERGED = 0, FETIGPU_MAX_ITER = 1, FETIGPU_BREAKDOWN = 2 };
+
+typedef struct fetigpu_ctx fetigpu_ctx;
+
+/* Problem description: partition (decomposition.hpp:13-48), material
+ * (fem.hpp:12-20), per-design densities keyed by module_type (the reference's
+ * factorization cache key), Dirichlet supports
+ * (decomposition.hpp:50-54), edge tractions (fem.hpp:90-99) and nodal point
+ * loads (lowest-index owner copy).  Loads must lie on module perimeters. */
+typedef struct fetigpu_problem {
+  int sx, sy, n;
+  double hx, hy;
+  double E0, Emin, nu, p, thickness;
+  int n_designs;
+  const double* densities;   /* n_designs * n * n, row-major from the bottom row */
+  const int* module_type;    /* sx*sy, design index per subdomain (sj*sx + si) */
+  int n_dirichlet;
+  const int* dir_gnode;
+  const int* dir_dir;
+  const double* dir_value;
+  int n_tractions;
+  const int* tr_sub;
+  const int* tr_side;        /* 0 left, 1 right, 2 bottom, 3 top */
+  const int* tr_first;
+  const int* tr_count;
+  const double* tr_txy;      /* 2 per traction */
+  int n_point_loads;
+  const int* pl_gnode;
+  const int* pl_dir;
+  const double* pl_value;
+  int method;                /* FETIGPU_TFETI | FETIGPU_FETIDP */
+  int scaling;               /* FETIGPU_MULTIPLICITY | FETIGPU_KSCALING */
+  int precond;               /* FETIGPU_LUMPED | FETIGPU_DIRICHLET | FETIGPU_SUPERLUMPED */
+} fetigpu_problem;
+
+/* SolveOptions */
+typedef struct fetigpu_solve_opts {
+  double tol;
+  int rel;                   /* 1: eps_r(i)/eps_r(0) <= tol */
+  int max_it;
+  int directions;            /* FETIGPU_SINGLE | FETIGPU_FO | FETIGPU_RRS */
+  double pivot_tol;          /* rank-revealing Cholesky tolerance, default 1e-12 */
+  int reorth_passes;         /* classical Gram-Schmidt passes, default 2 */
+} fetigpu_solve_opts;
+
+/* ConvergenceTrace; arrays are caller-owned (cap entries) */
+typedef struct fetigpu_trace {
+  int status;
+  int iterations;
+  int f_applies;
+  double eps0, eps_final;
+  int cap;
+  double* eps;
+  int* kept;
+  int* f_app;
+  double solve_ms;           /* device time of the iteration loop */
+} fetigpu_trace;
+
+/* Build statistics and the per-apply algorithmic work. */
+typedef struct fetigpu_stats {
+  int m, n_sub, local_dofs, n_c, n_kept, n_iface, max_ns, n_designs;
+  int n_op_slots, n_pc_slots;
+  double op_bytes;           /* F-apply GEMV algorithmic bytes per apply */
+  double op_flops_per_col;   /* block F-apply flops per column */
+  double main_kernel_bytes;  /* bytes of the dominant apply kernel (F_s stream) */
+  double build_ms;           /* device time of fetigpu_build */
+  double nd_ms, slot_ms, coarse_ms;
+  double device_bytes;       /* device memory held by the context */
+} fetigpu_stats;
+
+int fetigpu_create(const fetigpu_problem* p, fetigpu_ctx** out);
+int fetigpu_build(fetigpu_ctx* ctx);
+void fetigpu_destroy(fetigpu_ctx* ctx);
+const char* fetigpu_last_error(void);
+int fetigpu_stats_get(const fetigpu_ctx* ctx, fetigpu_stats* st);
+
+/* ConstraintSet rows (decomposition.hpp:58-108): kind 0 interface pair, 1
+ * Dirichlet; weights are the plus/minus sides of the scaled jump operator. */
+int fetigpu_rows(const fetigpu_ctx* ctx, int* kind, int* sub_plus, int* dof_plus,
+                 int* sub_minus, int* dof_minus, double* gap, int* mult,
+                 double* w_plus, double* w_minus);
+
+/* y = F x for ncols columns of length m (column stride ld >= m). */
+int fetigpu_apply_F(fetigpu_ctx* ctx, const double* x, double* y, int ncols, int ld);
+int fetigpu_apply_F_device(fetigpu_ctx* ctx, const double* x, double* y, int ncols, int ld);
+/* z = sum_s Bt_s St_s Bt_s^T r; Zcols (m x N_s, column-major) optional */
+int fetigpu_apply_precond(fetigpu_ctx* ctx, const double* r, double* z, double* Zcols);
+int fetigpu_apply_precond_device(fetigpu_ctx* ctx, const double* r, double* z, double* Zcols);
+/* v <- P v in place for ncols columns (identity for FETI-DP) */
+int fetigpu_project(fetigpu_ctx* ctx, double* v, int ncols, int ld);
+int fetigpu_project_device(fetigpu_ctx* ctx, double* v, int ncols, int ld);
+int fetigpu_rhs(fetigpu_ctx* ctx, double* d, double* lambda0);
+int fetigpu_solve(fetigpu_ctx* ctx, const fetigpu_solve_opts* o, double* lambda,
+                  fetigpu_trace* tr);
+/* u: N_s x local DOFs (2(n+1)^2 per subdomain, node-major x/y) */
+int fetigpu_recover(fetigpu_ctx* ctx, const double* lambda, double* u);
+
+/* Explicit local operator of subdomain s on its touched DOFs (test hook):
+ * writes n_s, the local DOF ids (ns) and the dense n_s x n_s F_s. */
+int fetigpu_local_operator(fetigpu_ctx* ctx, int s, int* ns, int* dofs, double* F, int cap);
+
+/* Device memory / timing helpers for benchmarks (no torch on the path). */
+int fetigpu_device_alloc(fetigpu_ctx* ctx, size_t bytes, void** ptr);
+int fetigpu_device_free(fetigpu_ctx* ctx, void* ptr);
+int fetigpu_host_alloc(size_t bytes, void** ptr);   /* pinned */
+int fetigpu_host_free(void* ptr);
+int fetigpu_memcpy(fetigpu_ctx* ctx, void* dst, const void* src, size_t bytes, int kind);
+int fetigpu_fill_random(fetigpu_ctx* ctx, double* d_ptr, size_t count, unsigned long long seed);
+int fetigpu_synchronize(fetigpu_ctx* ctx);
+/* Times `reps` device-resident applies of F on ncols columns with CUDA
+ * events on the context stream; ms[0] = mean per apply, ms[1] = mean of the
+ * dominant kernel, ms[2] = its share; launches[0] = kernels per apply. */
+int fetigpu_time_apply(fetigpu_ctx* ctx, const double* d_x, double* d_y, int ncols,
+                       int reps, int flush_l2, double* ms, int* launches);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -153,6 +153,37 @@ struct BandChol {
   }
 };
 
+// Accuracy reference mode (tests only): x = A_sub^{-1} b with two steps of
+// iterative refinement on long-double residuals.  Not part of the reference
+// algorithm; used to measure how far the double-precision oracle and the GPU
+// each are from the exact local solves at high stiffness contrast.
+static bool g_refine = false;
+static void solve_sub(const BandChol& bc, const Csr& A, const std::vector<int>& sub, double* x,
+                      bool refine) {
+  if (!refine) { bc.solve(x); return; }
+  const int n = (int)sub.size();
+  std::vector<long double> b(x, x + n), xl(n);
+  std::vector<int> map(A.n, -1);
+  for (int i = 0; i < n; ++i) map[sub[i]] = i;
+  bc.solve(x);
+  for (int i = 0; i < n; ++i) xl[i] = x[i];
+  std::vector<double> r(n);
+  for (int pass = 0; pass < 2; ++pass) {
+    for (int i = 0; i < n; ++i) {
+      long double acc = b[i];
+      const int gi = sub[i];
+      for (int k = A.ptr[gi]; k < A.ptr[gi + 1]; ++k) {
+        const int j = map[A.idx[k]];
+        if (j >= 0) acc -= (long double)A.val[k] * xl[j];
+      }
+      r[i] = (double)acc;
+    }
+    bc.solve(r.data());
+    for (int i = 0; i < n; ++i) xl[i] += r[i];
+  }
+  for (int i = 0; i < n; ++i) x[i] = (double)xl[i];
+}
+
 // Dense Cholesky (Eigen::LLT in decomposition.hpp:131 and the FETI-DP coarse
 // factorization SPEC.md:396).
 struct DenseChol {
@@ -511,6 +542,24 @@ struct Oracle {
   }
   bool is_corner_node(int gx, int gy) const { return gx % P.n == 0 && gy % P.n == 0; }
 
+  bool refine = false;
+  void coarse_solve(double* x) const {
+    if (!refine) { kcc.solve(x); return; }
+    std::vector<long double> b(x, x + Nc), xl(Nc);
+    std::vector<double> r(Nc);
+    kcc.solve(x);
+    for (int i = 0; i < Nc; ++i) xl[i] = x[i];
+    for (int pass = 0; pass < 2; ++pass) {
+      for (int i = 0; i < Nc; ++i) {
+        long double acc = b[i];
+        for (int j = 0; j < Nc; ++j) acc -= (long double)Kcc(i, j) * xl[j];
+        r[i] = (double)acc;
+      }
+      kcc.solve(r.data());
+      for (int i = 0; i < Nc; ++i) xl[i] += r[i];
+    }
+    for (int i = 0; i < Nc; ++i) x[i] = (double)xl[i];
+  }
   void build();
   void build_constraints();
   void build_weights();
@@ -797,7 +846,7 @@ void Oracle::build_fetidp() {
     for (int j = 0; j < nc; ++j) {
       double* col = S.Phi.col(j);
       for (int i = 0; i < nr; ++i) col[i] = S.K.get(S.rd[i], S.cd[j]);
-      S.krr.solve(col);
+      solve_sub(S.krr, S.K, S.rd, col, refine);
     }
     S.Kccb = Mat(nc, nc);
     for (int a = 0; a < nc; ++a)
@@ -857,7 +906,7 @@ void Oracle::apply_F(const double* x, double* y) {
       std::vector<double> b(S.keep.size(), 0.0), full(nloc, 0.0);
       for (auto& en : S.ent) full[en.dof] += en.sign * x[en.row];
       for (size_t i = 0; i < S.keep.size(); ++i) b[i] = full[S.keep[i]];
-      S.kred.solve(b.data());
+      solve_sub(S.kred, S.K, S.keep, b.data(), refine);
       std::fill(full.begin(), full.end(), 0.0);
       for (size_t i = 0; i < S.keep.size(); ++i) full[S.keep[i]] = b[i];
       loc[s].resize(S.ent.size());
@@ -877,13 +926,13 @@ void Oracle::apply_F(const double* x, double* y) {
         for (int i = 0; i < nr; ++i) v += S.Phi(i, a) * xr[i];
         ts[s][a] = v;
       }
-      S.krr.solve(xr.data());
+      solve_sub(S.krr, S.K, S.rd, xr.data(), refine);
       ys[s] = std::move(xr);
     }
     std::vector<double> u(Nc, 0.0);
     for (int s = 0; s < Ns; ++s)
       for (size_t a = 0; a < subs[s].cd.size(); ++a) u[subs[s].cg[a]] += ts[s][a];
-    if (Nc > 0) kcc.solve(u.data());
+    if (Nc > 0) coarse_solve(u.data());
 #pragma omp parallel for schedule(dynamic)
     for (int s = 0; s < Ns; ++s) {
       Sub& S = subs[s];
@@ -921,7 +970,7 @@ void Oracle::apply_precond(const double* r, double* z, double* Zcols) {
       if (P.precond == 1 && !S.other.empty()) {  // Dirichlet: - K_bi K_ii^{-1} K_ib
         std::vector<double> t(S.other.size());
         for (size_t i = 0; i < S.other.size(); ++i) t[i] = kx[S.other[i]];
-        S.koo.solve(t.data());
+        solve_sub(S.koo, S.K, S.other, t.data(), refine);
         std::vector<double> ext(nloc, 0.0), kt(nloc);
         for (size_t i = 0; i < S.other.size(); ++i) ext[S.other[i]] = t[i];
         S.K.matvec(ext.data(), kt.data());
@@ -966,7 +1015,7 @@ void Oracle::rhs(double* d, double* lam0) {
       Sub& S = subs[s];
       std::vector<double> b(S.keep.size()), full(nloc, 0.0);
       for (size_t i = 0; i < S.keep.size(); ++i) b[i] = S.f[S.keep[i]];
-      S.kred.solve(b.data());
+      solve_sub(S.kred, S.K, S.keep, b.data(), refine);
       for (size_t i = 0; i < S.keep.size(); ++i) full[S.keep[i]] = b[i];
       loc[s].resize(S.ent.size());
       for (size_t k = 0; k < S.ent.size(); ++k) loc[s][k] = S.ent[k].sign * full[S.ent[k].dof];
@@ -985,7 +1034,7 @@ void Oracle::rhs(double* d, double* lam0) {
     for (int s = 0; s < Ns; ++s) {
       Sub& S = subs[s];
       ys[s] = S.fr;
-      S.krr.solve(ys[s].data());
+      solve_sub(S.krr, S.K, S.rd, ys[s].data(), refine);
     }
     for (int s = 0; s < Ns; ++s) {
       Sub& S = subs[s];
@@ -996,7 +1045,7 @@ void Oracle::rhs(double* d, double* lam0) {
         fbar[S.cg[a]] += v;
       }
     }
-    if (Nc > 0) kcc.solve(fbar.data());
+    if (Nc > 0) coarse_solve(fbar.data());
     for (int s = 0; s < Ns; ++s) {
       Sub& S = subs[s];
       std::vector<double> v(S.rd.size(), 0.0);
@@ -1027,7 +1076,7 @@ void Oracle::recover(const double* lambda, double* u) {
       std::vector<double> full(S.f), b(S.keep.size());
       for (auto& en : S.ent) full[en.dof] -= en.sign * lambda[en.row];
       for (size_t i = 0; i < S.keep.size(); ++i) b[i] = full[S.keep[i]];
-      S.kred.solve(b.data());
+      solve_sub(S.kred, S.K, S.keep, b.data(), refine);
       double* us = u + (size_t)s * nloc;
       for (int i = 0; i < nloc; ++i) us[i] = 0.0;
       for (size_t i = 0; i < S.keep.size(); ++i) us[S.keep[i]] = b[i];
@@ -1046,14 +1095,14 @@ void Oracle::recover(const double* lambda, double* u) {
         t[S.cg[a]] += v;
       }
     }
-    if (Nc > 0) kcc.solve(t.data());  // u_c = Kbar^{-1} (fbar_c + F_rc^T lambda)
+    if (Nc > 0) coarse_solve(t.data());  // u_c = Kbar^{-1} (fbar_c + F_rc^T lambda)
 #pragma omp parallel for schedule(dynamic)
     for (int s = 0; s < Ns; ++s) {
       Sub& S = subs[s];
       const int nr = (int)S.rd.size();
       std::vector<double> v(S.fr);
       for (auto& en : S.ent) v[S.rpos[en.dof]] -= en.sign * lambda[en.row];
-      S.krr.solve(v.data());
+      solve_sub(S.krr, S.K, S.rd, v.data(), refine);
       for (size_t a = 0; a < S.cd.size(); ++a)
         for (int i = 0; i < nr; ++i) v[i] -= S.Phi(i, a) * t[S.cg[a]];
       double* us = u + (size_t)s * nloc;
@@ -1141,11 +1190,13 @@ int Oracle::solve(const fo_opts& o, double* lambda, fo_trace* tr) {
         Ws.push_back(std::move(wn));
         Qs.push_back(std::move(qn));
         w = z;
-        for (int p = 0; p < passes; ++p)
-          for (size_t j = 0; j < Ws.size(); ++j) {
-            const double psi = dot(Qs[j].data(), w.data(), m);
-            for (int i = 0; i < m; ++i) w[i] -= psi * Ws[j][i];
-          }
+        // classical Gram-Schmidt + one refinement pass
+        std::vector<double> psi(Ws.size());
+        for (int p = 0; p < passes; ++p) {
+          for (size_t j = 0; j < Ws.size(); ++j) psi[j] = dot(Qs[j].data(), w.data(), m);
+          for (size_t j = 0; j < Ws.size(); ++j)
+            for (int i = 0; i < m; ++i) w[i] -= psi[j] * Ws[j][i];
+        }
       } else {
         const double beta = rz_new / rz;
         for (int i = 0; i < m; ++i) w[i] = z[i] + beta * w[i];
@@ -1200,14 +1251,22 @@ int Oracle::solve(const fo_opts& o, double* lambda, fo_trace* tr) {
       Qs.push_back(std::move(Q));
       W = Z;
       for (int c = 0; c < Ns; ++c) project(W.col(c));
-      for (int p = 0; p < passes; ++p)
+      // lines 18-21 as block classical Gram-Schmidt against all stored
+      // blocks, twice: Psi_j = Q_j^T W for all j, then
+      // W -= sum_j W_j Psi_j
+      for (int p = 0; p < passes; ++p) {
+        std::vector<Mat> Psis(Ws.size());
         for (size_t j = 0; j < Ws.size(); ++j) {
-          const Mat& Wj = Ws[j];
           const Mat& Qj = Qs[j];
-          Mat Psi(Wj.c, W.c);
+          Mat& Psi = Psis[j];
+          Psi = Mat(Qj.c, W.c);
 #pragma omp parallel for schedule(dynamic)
           for (int b = 0; b < W.c; ++b)
-            for (int a = 0; a < Wj.c; ++a) Psi(a, b) = dot(Qj.col(a), W.col(b), m);
+            for (int a = 0; a < Qj.c; ++a) Psi(a, b) = dot(Qj.col(a), W.col(b), m);
+        }
+        for (size_t j = 0; j < Ws.size(); ++j) {
+          const Mat& Wj = Ws[j];
+          const Mat& Psi = Psis[j];
 #pragma omp parallel for schedule(dynamic)
           for (int b = 0; b < W.c; ++b)
             for (int a = 0; a < Wj.c; ++a) {
@@ -1217,6 +1276,7 @@ int Oracle::solve(const fo_opts& o, double* lambda, fo_trace* tr) {
               for (int i = 0; i < m; ++i) wb[i] -= wj[i] * ps;
             }
         }
+      }
     }
     (void)kept_last;
   }
@@ -1325,12 +1385,14 @@ static int guarded(F&& f) {
 extern "C" {
 
 const char* fo_last_error(void) { return g_err.c_str(); }
+void fo_set_refine(int on) { g_refine = on != 0; }
 
 int fo_create(const fo_problem* p, void** out) {
   *out = nullptr;
   auto o = std::make_unique<Oracle>();
   int rc = guarded([&] {
     o->P = *p;
+    o->refine = g_refine;
     o->build();
   });
   if (rc == 0) *out = o.release();

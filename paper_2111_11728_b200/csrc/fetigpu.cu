@@ -1,0 +1,1605 @@
+// fetigpu.cu -- context, build orchestration, operators, engine and C-ABI.
+//
+// One context = one FETI problem resident on one GPU.  fetigpu_build runs the
+// whole operator construction on the device (ND Schur tree -> per-slot dense
+// local operators -> FETI-DP coarse inverse); afterwards every operator
+// application, preconditioner, projection and the PCG/FO/RRS loop run on the
+// context's stream without host work beyond scalar read-back.
+#include <cublas_v2.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "fetigpu.h"
+#include "kernels_apply.cuh"
+#include "kernels_build.cuh"
+#include "setup.hpp"
+
+namespace fg {
+
+#define CK(x)                                                                                  \
+  do {                                                                                         \
+    cudaError_t e_ = (x);                                                                      \
+    if (e_ != cudaSuccess)                                                                     \
+      fail(e_ == cudaErrorMemoryAllocation ? FETIGPU_E_OUT_OF_MEMORY : FETIGPU_E_CUDA,         \
+           std::string(#x) + ": " + cudaGetErrorString(e_));                                   \
+  } while (0)
+#define CB(x)                                                                                  \
+  do {                                                                                         \
+    cublasStatus_t s_ = (x);                                                                   \
+    if (s_ != CUBLAS_STATUS_SUCCESS) fail(FETIGPU_E_CUDA, std::string(#x) + " failed");        \
+  } while (0)
+#define LAUNCH_CHECK() CK(cudaGetLastError())
+
+static size_t g_device_bytes = 0;
+
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  ~DBuf() { release(); }
+  void release() {
+    if (p) {
+      cudaFree(p);
+      g_device_bytes -= n * sizeof(T);
+    }
+    p = nullptr;
+    n = 0;
+  }
+  void alloc(size_t count) {
+    release();
+    if (count == 0) count = 1;
+    CK(cudaMalloc(&p, count * sizeof(T)));
+    n = count;
+    g_device_bytes += n * sizeof(T);
+  }
+  void upload(const std::vector<T>& v, cudaStream_t st) {
+    alloc(v.size());
+    if (!v.empty()) CK(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, st));
+  }
+  void zero(cudaStream_t st) { CK(cudaMemsetAsync(p, 0, n * sizeof(T), st)); }
+};
+
+static inline int round_up(int v, int a) { return (v + a - 1) / a * a; }
+static inline int grid_for(long long n, int threads = kThreads, int cap = 148 * 16) {
+  long long g = (n + threads - 1) / threads;
+  return (int)std::max<long long>(1, std::min<long long>(g, cap));
+}
+
+struct Ctx {
+  Setup su;
+  cudaStream_t st = nullptr;
+  cublasHandle_t cb = nullptr;
+  bool built = false;
+  DBuf<int> d_status;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr;
+  double build_ms = 0, nd_ms = 0, slot_ms = 0, coarse_ms = 0;
+  bool keep_factors = true;
+
+  // ND tree
+  DBuf<NdDev> d_nodes;
+  DBuf<int> d_elem_ids, d_emap, d_cmaps, d_nd_dofs, d_topdown, d_design;
+  DBuf<double> d_dens, d_S, d_ndfac;
+  // operator (F_s) per subdomain
+  int KR = 1;
+  DBuf<OpSub> d_op;
+  DBuf<double> d_opmat, d_opcoef, d_opfac;
+  DBuf<int> d_oprows, d_slot_of, d_fac_ne, d_top_pos, d_top_off;
+  DBuf<long long> d_fac_off;
+  std::vector<int> op_ns, op_ld;
+  std::vector<long long> op_moff, op_foff;
+  int max_ld = 0, max_ne = 0;
+  // slot src/ext lists
+  DBuf<int> d_op_src, d_op_ext, d_op_src_off, d_op_ext_off;
+  // preconditioner
+  int KRp = 1;
+  DBuf<OpSub> d_pc;
+  DBuf<double> d_pcmat, d_pccoef;
+  DBuf<int> d_pcrows;
+  int max_pc_ld = 0;
+  // projector (T-FETI)
+  DBuf<OpSub> d_pj;
+  DBuf<double> d_pjcoef, d_RT, d_H, d_e;
+  DBuf<int> d_rt_off;
+  // FETI-DP
+  DBuf<DpSub> d_dp;
+  DBuf<double> d_abc, d_kccs, d_Kinv, d_vbuf, d_tbuf, d_fbar_loc, d_fbar;
+  DBuf<int> d_cmap, d_voff, d_optr, d_oidx;
+  // boundary data for rhs / recovery
+  DBuf<double> d_fb, d_gD;
+  DBuf<int> d_D, d_D_off, d_D_cnt, d_c_pos, d_c_off, d_xoff;
+  DBuf<double> d_xb;
+  // scratch vectors
+  DBuf<double> d_v1, d_v2, d_v3, d_g, d_h, d_partial;
+  DBuf<double> d_d, d_lam0;
+  bool have_rhs = false;
+  // stats
+  double op_bytes = 0, op_flops = 0, main_bytes = 0;
+
+  ~Ctx() {
+    if (cb) cublasDestroy(cb);
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev1) cudaEventDestroy(ev1);
+    if (ev2) cudaEventDestroy(ev2);
+    if (st) cudaStreamDestroy(st);
+  }
+
+  void check_status() {
+    int h = 0;
+    CK(cudaMemcpyAsync(&h, d_status.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (h != 0) {
+      CK(cudaMemsetAsync(d_status.p, 0, sizeof(int), st));
+      fail(h, "device factorization failed (nonpositive pivot)");
+    }
+  }
+
+  void init_device() {
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+      fail(FETIGPU_E_NO_DEVICE, "no CUDA device available");
+    CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    CB(cublasCreate(&cb));
+    CB(cublasSetStream(cb, st));
+    CK(cudaEventCreate(&ev0));
+    CK(cudaEventCreate(&ev1));
+    CK(cudaEventCreate(&ev2));
+    d_status.alloc(1);
+    d_status.zero(st);
+    CK(cudaFuncSetAttribute(k_nd_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            kSmallFront * kSmallFront * 8));
+    CK(cudaFuncSetAttribute(k_front_elim_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            kSmallFront * kSmallFront * 8));
+  }
+
+  double elapsed(cudaEvent_t a, cudaEvent_t b) {
+    float ms = 0;
+    CK(cudaEventSynchronize(b));
+    CK(cudaEventElapsedTime(&ms, a, b));
+    return ms;
+  }
+
+  // ------------------------------------------------------------ build --
+  void eliminate(const std::vector<FrontDesc>& fds, double* base) {
+    std::vector<FrontDesc> small, large;
+    int nfmax = 0;
+    for (auto& f : fds) {
+      if (f.nf <= kSmallFront && f.ld == f.nf) { small.push_back(f); nfmax = std::max(nfmax, f.nf); }
+      else large.push_back(f);
+    }
+    DBuf<FrontDesc> ds, dl;
+    if (!small.empty()) {
+      ds.upload(small, st);
+      k_front_elim_small<<<(int)small.size(), kThreads, nfmax * nfmax * 8, st>>>(ds.p, base, d_status.p);
+      LAUNCH_CHECK();
+    }
+    if (!large.empty()) {
+      dl.upload(large, st);
+      k_front_elim_large<<<(int)large.size(), kThreads, 0, st>>>(dl.p, base, d_status.p);
+      LAUNCH_CHECK();
+    }
+    CK(cudaStreamSynchronize(st));
+  }
+
+  void build_nd() {
+    const NdPlan& P = su.nd;
+    const int nb = su.nb, n = su.n, D = su.n_designs;
+    std::vector<NdDev> nodes(P.nodes.size());
+    std::vector<int> elem_ids, emap, cmaps, dofs;
+    for (size_t i = 0; i < P.nodes.size(); ++i) {
+      const NdNode& s = P.nodes[i];
+      NdDev& d = nodes[i];
+      d.nf = s.nf; d.ne = s.ne; d.leaf = s.leaf; d.height = s.height;
+      d.off = s.off; d.foff = s.foff;
+      d.elem_off = (int)elem_ids.size();
+      d.elem_cnt = (int)s.elems.size();
+      elem_ids.insert(elem_ids.end(), s.elems.begin(), s.elems.end());
+      emap.insert(emap.end(), s.emap.begin(), s.emap.end());
+      for (int c = 0; c < 2; ++c) {
+        d.child[c] = s.child[c];
+        d.cmap_off[c] = (int)cmaps.size();
+        cmaps.insert(cmaps.end(), s.cmap[c].begin(), s.cmap[c].end());
+      }
+      d.dof_off = (int)dofs.size();
+      dofs.insert(dofs.end(), s.dofs.begin(), s.dofs.end());
+    }
+    d_nodes.upload(nodes, st);
+    d_elem_ids.upload(elem_ids, st);
+    d_emap.upload(emap, st);
+    d_cmaps.upload(cmaps, st);
+    d_nd_dofs.upload(dofs, st);
+    d_topdown.upload(P.topdown, st);
+    d_dens.upload(su.densities, st);
+    d_S.alloc((size_t)D * nb * nb);
+    if (keep_factors) d_ndfac.alloc((size_t)D * P.factor_stride);
+
+    long long per_design = 0;
+    for (long long s : P.height_stride) per_design += s;
+    size_t free_b = 0, tot_b = 0;
+    CK(cudaMemGetInfo(&free_b, &tot_b));
+    const long long budget = std::max<long long>(256ll << 20, (long long)(free_b * 0.3));
+    const int chunk = (int)std::max<long long>(1, std::min<long long>(D, budget / (per_design * 8)));
+    DBuf<double> ws;
+    ws.alloc((size_t)chunk * per_design);
+    // per-height node lists split by size
+    std::vector<std::vector<int>> hsmall(P.max_height + 1), hlarge(P.max_height + 1);
+    std::vector<int> hnfmax(P.max_height + 1, 0);
+    for (int h = 0; h <= P.max_height; ++h)
+      for (int t : P.by_height[h]) {
+        if (P.nodes[t].nf <= kSmallFront) { hsmall[h].push_back(t); hnfmax[h] = std::max(hnfmax[h], P.nodes[t].nf); }
+        else hlarge[h].push_back(t);
+      }
+    std::vector<DBuf<int>> dsm(P.max_height + 1), dlg(P.max_height + 1);
+    for (int h = 0; h <= P.max_height; ++h) {
+      dsm[h].upload(hsmall[h], st);
+      dlg[h].upload(hlarge[h], st);
+    }
+    DBuf<long long> d_hbase, d_hstride;
+    d_hstride.upload(P.height_stride, st);
+    for (int d0 = 0; d0 < D; d0 += chunk) {
+      const int dc = std::min(chunk, D - d0);
+      std::vector<long long> hbase(P.max_height + 1, 0);
+      long long acc = 0;
+      for (int h = 0; h <= P.max_height; ++h) { hbase[h] = acc; acc += (long long)dc * P.height_stride[h]; }
+      d_hbase.upload(hbase, st);
+      NdArgs a{d_nodes.p, nullptr, d_hbase.p, d_hstride.p, ws.p, d_elem_ids.p, d_emap.p, d_cmaps.p,
+               d_dens.p, n, d0, su.E0, su.Emin, su.p, keep_factors ? d_ndfac.p : nullptr,
+               P.factor_stride, d_status.p};
+      for (int h = 0; h <= P.max_height; ++h) {
+        if (!hsmall[h].empty()) {
+          a.level_nodes = dsm[h].p;
+          dim3 grid((unsigned)hsmall[h].size(), dc);
+          k_nd_small<<<grid, kThreads, hnfmax[h] * hnfmax[h] * 8, st>>>(a);
+          LAUNCH_CHECK();
+        }
+        if (!hlarge[h].empty()) {
+          a.level_nodes = dlg[h].p;
+          dim3 grid((unsigned)hlarge[h].size(), dc);
+          k_nd_assemble<<<grid, kThreads, 0, st>>>(a);
+          LAUNCH_CHECK();
+          std::vector<FrontDesc> fds;
+          for (int dl = 0; dl < dc; ++dl)
+            for (int t : hlarge[h]) {
+              const NdNode& nd = P.nodes[t];
+              fds.push_back({hbase[h] + (long long)dl * P.height_stride[h] + nd.off, nd.nf, nd.ne, nd.nf,
+                             FETIGPU_E_SINGULAR_INTERIOR});
+            }
+          DBuf<FrontDesc> dfd;
+          dfd.upload(fds, st);
+          k_front_elim_large<<<(int)fds.size(), kThreads, 0, st>>>(dfd.p, ws.p, d_status.p);
+          LAUNCH_CHECK();
+          if (keep_factors) {
+            k_nd_copy_factors<<<grid, kThreads, 0, st>>>(a);
+            LAUNCH_CHECK();
+          }
+          CK(cudaStreamSynchronize(st));
+        }
+      }
+      k_nd_extract_root<<<dim3(grid_for((long long)nb * nb), dc), kThreads, 0, st>>>(
+          d_nodes.p, P.root, d_hbase.p, d_hstride.p, ws.p, d_S.p, nb, d0);
+      LAUNCH_CHECK();
+      CK(cudaStreamSynchronize(st));
+    }
+    check_status();
+  }
+
+  // batched slot processing: assemble [[S[src,src],E],[E^T,0]], eliminate,
+  // extract; processed in chunks bounded by a workspace budget
+  struct SlotOut {
+    std::vector<long long> mat_off;
+    std::vector<int> mat_ld;
+    std::vector<long long> abc_off, kcc_off, fac_off;
+  };
+  void run_slots(const std::vector<SlotFront>& slots, const SlotOut& out, double* mats, double sign,
+                 bool nc_first, double* abc, double* kcc, double* fac, int errcode) {
+    std::vector<int> src_all, ext_all;
+    std::vector<SlotDev> sd(slots.size());
+    for (size_t i = 0; i < slots.size(); ++i) {
+      sd[i].design = slots[i].design;
+      sd[i].nsrc = (int)slots[i].src.size();
+      sd[i].ne = slots[i].ne;
+      sd[i].next = (int)slots[i].ext.size();
+      sd[i].src_off = (int)src_all.size();
+      sd[i].ext_off = (int)ext_all.size();
+      src_all.insert(src_all.end(), slots[i].src.begin(), slots[i].src.end());
+      ext_all.insert(ext_all.end(), slots[i].ext.begin(), slots[i].ext.end());
+    }
+    DBuf<int> dsrc, dext;
+    dsrc.upload(src_all, st);
+    dext.upload(ext_all, st);
+    size_t free_b = 0, tot_b = 0;
+    CK(cudaMemGetInfo(&free_b, &tot_b));
+    const long long budget = std::max<long long>(256ll << 20, (long long)(free_b * 0.3)) / 8;
+    size_t i0 = 0;
+    DBuf<double> ws;
+    while (i0 < slots.size()) {
+      long long used = 0;
+      size_t i1 = i0;
+      std::vector<SlotDev> chunk;
+      while (i1 < slots.size()) {
+        const long long nf = slots[i1].nf();
+        if (!chunk.empty() && used + nf * nf > budget) break;
+        SlotDev d = sd[i1];
+        d.woff = used;
+        used += nf * nf;
+        chunk.push_back(d);
+        ++i1;
+      }
+      ws.alloc(used);
+      DBuf<SlotDev> dchunk;
+      dchunk.upload(chunk, st);
+      const int nch = (int)chunk.size();
+      k_slot_assemble<<<dim3(64, nch), kThreads, 0, st>>>(dchunk.p, dsrc.p, dext.p, d_S.p, su.nb, ws.p);
+      LAUNCH_CHECK();
+      std::vector<FrontDesc> fds;
+      for (auto& c : chunk) fds.push_back({c.woff, c.nsrc + c.next, c.ne, c.nsrc + c.next, errcode});
+      eliminate(fds, ws.p);
+      auto sub = [&](const std::vector<long long>& v) {
+        return std::vector<long long>(v.begin() + i0, v.begin() + i1);
+      };
+      DBuf<long long> dmo, dao, dko, dfo;
+      DBuf<int> dml;
+      dmo.upload(sub(out.mat_off), st);
+      dml.upload(std::vector<int>(out.mat_ld.begin() + i0, out.mat_ld.begin() + i1), st);
+      if (abc) { dao.upload(sub(out.abc_off), st); dko.upload(sub(out.kcc_off), st); }
+      k_slot_extract<<<dim3(32, nch), kThreads, 0, st>>>(dchunk.p, ws.p, dmo.p, dml.p, mats,
+                                                         nc_first ? 1 : 0, sign, abc ? dao.p : nullptr,
+                                                         abc, abc ? dko.p : nullptr, kcc);
+      LAUNCH_CHECK();
+      if (fac) {
+        dfo.upload(sub(out.fac_off), st);
+        k_slot_factor<<<dim3(32, nch), kThreads, 0, st>>>(dchunk.p, ws.p, dfo.p, fac);
+        LAUNCH_CHECK();
+      }
+      CK(cudaStreamSynchronize(st));
+      i0 = i1;
+    }
+    check_status();
+  }
+
+  void build_ops() {
+    const int Ns = su.Ns, nb = su.nb;
+    const bool dp = su.method == FETIGPU_FETIDP;
+    // ---- operator slots
+    const int nslot = (int)su.op_slots.size();
+    SlotOut so;
+    long long mo = 0, ao = 0, ko = 0, fo = 0;
+    op_ns.resize(nslot); op_ld.resize(nslot); op_moff.resize(nslot); op_foff.resize(nslot);
+    for (int i = 0; i < nslot; ++i) {
+      const SlotFront& s = su.op_slots[i];
+      const int ns = (int)s.ext.size(), ld = round_up(ns, 4), nc = (int)s.src.size() - s.ne;
+      op_ns[i] = ns; op_ld[i] = ld; op_moff[i] = mo;
+      so.mat_off.push_back(mo); so.mat_ld.push_back(ld);
+      so.abc_off.push_back(ao); so.kcc_off.push_back(ko); so.fac_off.push_back(fo);
+      op_foff[i] = fo;
+      mo += (long long)ns * ld; ao += (long long)ns * nc; ko += (long long)nc * nc;
+      fo += (long long)s.ne * s.ne;
+      max_ld = std::max(max_ld, ld);
+      max_ne = std::max(max_ne, s.ne);
+    }
+    d_opmat.alloc(mo);
+    d_opfac.alloc(fo);
+    if (dp) { d_abc.alloc(ao); d_kccs.alloc(ko); }
+    run_slots(su.op_slots, so, d_opmat.p, -1.0, dp, dp ? d_abc.p : nullptr, dp ? d_kccs.p : nullptr,
+              d_opfac.p, dp ? FETIGPU_E_SINGULAR_REMAINDER : FETIGPU_E_NOT_POSITIVE_DEFINITE);
+    // slot src/ext lists for rhs / recovery
+    {
+      std::vector<int> src, ext, so_, eo_, fne;
+      for (auto& s : su.op_slots) {
+        so_.push_back((int)src.size());
+        eo_.push_back((int)ext.size());
+        src.insert(src.end(), s.src.begin(), s.src.end());
+        ext.insert(ext.end(), s.ext.begin(), s.ext.end());
+        fne.push_back(s.ne);
+      }
+      d_op_src.upload(src, st); d_op_ext.upload(ext, st);
+      d_op_src_off.upload(so_, st); d_op_ext_off.upload(eo_, st);
+      d_fac_ne.upload(fne, st);
+      d_fac_off.upload(so.fac_off, st);
+    }
+    // ---- per-subdomain operator maps
+    struct Ent { int row; double coef; double w; };
+    std::vector<std::vector<std::vector<Ent>>> ent(Ns);  // [s][perimeter pos] -> entries
+    for (int s = 0; s < Ns; ++s) ent[s].assign(nb, {});
+    for (int i = 0; i < su.m; ++i) {
+      const Row& r = su.rows[i];
+      ent[r.sp][su.dpos[r.dp]].push_back({i, 1.0, su.wplus[i]});
+      if (r.kind == 0) ent[r.sm][su.dpos[r.dm]].push_back({i, -1.0, su.wminus[i]});
+    }
+    KR = dp ? 1 : 3;
+    for (int s = 0; s < Ns; ++s)
+      for (int i = 0; i < nb; ++i)
+        if ((int)ent[s][i].size() > KR) fail(FETIGPU_E_STATE, "too many dual rows per DOF");
+    KRp = KR;
+    std::vector<OpSub> ops(Ns), pcs(Ns), pjs(Ns);
+    std::vector<int> rows, prow, slot_of(Ns), top_pos, top_off(Ns), design(Ns);
+    std::vector<double> coef, pcoef, pjcoef, RT;
+    std::vector<int> rt_off(Ns);
+    for (int s = 0; s < Ns; ++s) {
+      const SubPlan& S = su.subs[s];
+      const int sl = S.op_slot;
+      slot_of[s] = sl;
+      design[s] = S.design;
+      ops[s] = {op_moff[sl], op_ns[sl], op_ld[sl], (int)rows.size(), 0};
+      top_off[s] = (int)top_pos.size();
+      for (int t : S.Top) {
+        top_pos.push_back(t);
+        for (int k = 0; k < KR; ++k) {
+          if (k < (int)ent[s][t].size()) { rows.push_back(ent[s][t][k].row); coef.push_back(ent[s][t][k].coef); }
+          else { rows.push_back(-1); coef.push_back(0.0); }
+        }
+      }
+      // preconditioner / projector maps over T
+      pcs[s] = {0, (int)S.T.size(), 0, (int)prow.size(), 0};
+      pjs[s] = pcs[s];
+      rt_off[s] = (int)RT.size();
+      for (int t : S.T) {
+        for (int k = 0; k < KRp; ++k) {
+          if (k < (int)ent[s][t].size()) {
+            prow.push_back(ent[s][t][k].row);
+            pcoef.push_back(ent[s][t][k].coef * ent[s][t][k].w);
+            pjcoef.push_back(ent[s][t][k].coef);
+          } else { prow.push_back(-1); pcoef.push_back(0.0); pjcoef.push_back(0.0); }
+        }
+        for (int k = 0; k < 3; ++k) RT.push_back(su.Rb[(size_t)k * nb + t]);
+      }
+    }
+    d_oprows.upload(rows, st); d_opcoef.upload(coef, st);
+    d_slot_of.upload(slot_of, st); d_design.upload(design, st);
+    d_top_pos.upload(top_pos, st); d_top_off.upload(top_off, st);
+    d_pcrows.upload(prow, st); d_pccoef.upload(pcoef, st);
+
+    // ---- preconditioner matrices
+    std::vector<long long> pc_moff;
+    std::vector<int> pc_ld;
+    long long pm = 0;
+    const int npc = su.precond == FETIGPU_DIRICHLET ? (int)su.pc_slots.size() : (int)su.pc_lumped_T.size();
+    for (int i = 0; i < npc; ++i) {
+      const int nt = su.precond == FETIGPU_DIRICHLET ? (int)(su.pc_slots[i].src.size() - su.pc_slots[i].ne)
+                                                    : (int)su.pc_lumped_T[i].size();
+      const int ld = round_up(nt, 4);
+      pc_moff.push_back(pm); pc_ld.push_back(ld);
+      pm += (long long)nt * ld;
+      max_pc_ld = std::max(max_pc_ld, ld);
+    }
+    d_pcmat.alloc(pm);
+    if (su.precond == FETIGPU_DIRICHLET) {
+      SlotOut po;
+      po.mat_off = pc_moff; po.mat_ld = pc_ld;
+      run_slots(su.pc_slots, po, d_pcmat.p, 1.0, false, nullptr, nullptr, nullptr, FETIGPU_E_SINGULAR_INTERIOR);
+    } else {
+      // K_bb per design from element contributions
+      std::vector<int> pne(su.nb / 2 * 4, -1);
+      const int n = su.n, nn = n + 1;
+      for (int q = 0; q < su.nb / 2; ++q) {
+        const int v = su.perim_dof[2 * q] / 2, vx = v % nn, vy = v / nn;
+        int cnt = 0;
+        std::vector<std::pair<int, int>> el;
+        for (int ey = std::max(0, vy - 1); ey <= std::min(n - 1, vy); ++ey)
+          for (int ex = std::max(0, vx - 1); ex <= std::min(n - 1, vx); ++ex) {
+            const int n0 = ey * nn + ex;
+            const int en[4] = {n0, n0 + 1, n0 + nn + 1, n0 + nn};
+            for (int a = 0; a < 4; ++a)
+              if (en[a] == v) el.push_back({ey * n + ex, a});
+          }
+        std::sort(el.begin(), el.end());
+        for (auto& e : el) {
+          if (cnt < 2) { pne[q * 4 + 2 * cnt] = e.first; pne[q * 4 + 2 * cnt + 1] = e.second; }
+          ++cnt;
+        }
+        if (cnt > 2) fail(FETIGPU_E_STATE, "perimeter node with > 2 elements");
+      }
+      DBuf<int> dpne, dpd;
+      dpne.upload(pne, st);
+      dpd.upload(su.perim_dof, st);
+      DBuf<double> kbb;
+      kbb.alloc((size_t)su.n_designs * nb * nb);
+      k_kbb<<<dim3(grid_for((long long)nb * nb), su.n_designs), kThreads, 0, st>>>(
+          d_dens.p, n, su.E0, su.Emin, su.p, dpne.p, dpd.p, nb, kbb.p);
+      LAUNCH_CHECK();
+      std::vector<int> tall, toff, tcnt;
+      for (auto& T : su.pc_lumped_T) {
+        toff.push_back((int)tall.size());
+        tcnt.push_back((int)T.size());
+        tall.insert(tall.end(), T.begin(), T.end());
+      }
+      DBuf<int> dt, dto, dtc, dsd, dld;
+      DBuf<long long> dmo;
+      dt.upload(tall, st); dto.upload(toff, st); dtc.upload(tcnt, st);
+      dsd.upload(su.pc_lumped_design, st);
+      dmo.upload(pc_moff, st); dld.upload(pc_ld, st);
+      k_pc_lumped<<<dim3(16, npc), kThreads, 0, st>>>(dsd.p, dto.p, dtc.p, dt.p, kbb.p, nb, dmo.p, dld.p,
+                                                     d_pcmat.p, su.precond == FETIGPU_SUPERLUMPED);
+      LAUNCH_CHECK();
+      CK(cudaStreamSynchronize(st));
+    }
+    for (int s = 0; s < Ns; ++s) {
+      const int sl = su.subs[s].pc_slot;
+      pcs[s].moff = pc_moff[sl];
+      pcs[s].ld = pc_ld[sl];
+    }
+    d_pc.upload(pcs, st);
+    d_op.upload(ops, st);
+
+    // ---- T-FETI projector data
+    if (!dp) {
+      d_pj.upload(pjs, st);
+      d_pjcoef.upload(pjcoef, st);
+      d_RT.upload(RT, st);
+      d_rt_off.upload(rt_off, st);
+      d_H.upload(su.H, st);
+      std::vector<double> e(3 * Ns, 0.0);  // e = -R^T f (decomposition.hpp:127)
+      for (int s = 0; s < Ns; ++s)
+        for (int k = 0; k < 3; ++k) {
+          double v = 0.0;
+          for (int i = 0; i < nb; ++i) v += su.Rb[(size_t)k * nb + i] * su.subs[s].f[i];
+          e[3 * s + k] = -v;
+        }
+      d_e.upload(e, st);
+    }
+
+    // ---- boundary data for rhs / recovery
+    {
+      std::vector<double> fb, gD;
+      std::vector<int> Dl, Doff, Dcnt, cpos, coff, xoff;
+      int xo = 0;
+      for (int s = 0; s < Ns; ++s) {
+        const SubPlan& S = su.subs[s];
+        fb.insert(fb.end(), S.f.begin(), S.f.end());
+        Doff.push_back((int)Dl.size());
+        Dcnt.push_back((int)S.D.size());
+        Dl.insert(Dl.end(), S.D.begin(), S.D.end());
+        gD.insert(gD.end(), S.gD.begin(), S.gD.end());
+        coff.push_back((int)cpos.size());
+        cpos.insert(cpos.end(), S.c.begin(), S.c.end());
+        xoff.push_back(xo);
+        xo += su.op_slots[S.op_slot].ne;
+      }
+      d_fb.upload(fb, st); d_gD.upload(gD, st);
+      d_D.upload(Dl, st); d_D_off.upload(Doff, st); d_D_cnt.upload(Dcnt, st);
+      d_c_pos.upload(cpos, st); d_c_off.upload(coff, st);
+      d_xoff.upload(xoff, st);
+      d_xb.alloc(xo);
+    }
+
+    // ---- FETI-DP coarse problem
+    if (dp) {
+      std::vector<DpSub> dps(Ns);
+      std::vector<int> cmap, voff, optr{0}, oidx, osub, oloc;
+      int vo = 0, to = 0;
+      std::vector<int> toff(Ns);
+      for (int s = 0; s < Ns; ++s) {
+        const SubPlan& S = su.subs[s];
+        const int sl = S.op_slot;
+        dps[s].abc_off = so.abc_off[sl];
+        dps[s].nc = (int)S.c.size();
+        if (dps[s].nc > 8) fail(FETIGPU_E_STATE, "more than 8 primal DOFs per subdomain");
+        dps[s].cmap_off = (int)cmap.size();
+        cmap.insert(cmap.end(), S.cg.begin(), S.cg.end());
+        dps[s].v_off = vo;
+        voff.push_back(vo);
+        vo += (int)S.Top.size();
+        dps[s].t_off = to;
+        toff[s] = to;
+        to += (int)S.c.size();
+      }
+      for (int i = 0; i < su.Nc; ++i) {
+        for (auto& o : su.c_owners[i]) {
+          oidx.push_back(toff[o.first] + o.second);
+          osub.push_back(o.first);
+          oloc.push_back(o.second);
+        }
+        optr.push_back((int)oidx.size());
+      }
+      d_dp.upload(dps, st);
+      d_cmap.upload(cmap, st);
+      d_voff.upload(voff, st);
+      d_optr.upload(optr, st);
+      d_oidx.upload(oidx, st);
+      d_vbuf.alloc(vo);
+      d_tbuf.alloc(std::max(1, to));
+      d_fbar_loc.alloc(std::max(1, to));
+      d_fbar.alloc(std::max(1, su.Nc));
+      build_coarse(so, osub, oloc);
+    }
+    // ---- scratch
+    const size_t m = std::max(1, su.m);
+    d_v1.alloc(m); d_v2.alloc(m); d_v3.alloc(m);
+    d_g.alloc(3 * (size_t)Ns + 8); d_h.alloc(3 * (size_t)Ns + 8);
+    d_partial.alloc(4 * kDotBlocks);
+    d_d.alloc(m); d_lam0.alloc(m);
+
+    // ---- work per apply
+    double sn2 = 0, snc = 0, sns = 0;
+    for (int s = 0; s < Ns; ++s) {
+      const double ns = (double)su.subs[s].Top.size();
+      sn2 += ns * ns;
+      sns += ns;
+      if (dp) snc += ns * (double)su.subs[s].c.size();
+    }
+    double ld_bytes = 0;
+    for (int s = 0; s < Ns; ++s) ld_bytes += 8.0 * op_ns[su.subs[s].op_slot] * op_ld[su.subs[s].op_slot];
+    op_bytes = 8 * sn2 + (dp ? 16 * snc + 8.0 * su.Nc * su.Nc : 0) + 16.0 * su.m + 8 * sns;
+    op_flops = 2 * sn2 + (dp ? 4 * snc + 2.0 * su.Nc * su.Nc : 0);
+    main_bytes = 8 * sn2;
+    (void)ld_bytes;
+  }
+
+  void build_coarse(const SlotOut& so, const std::vector<int>& osub, const std::vector<int>& oloc) {
+    const int Nc = su.Nc;
+    if (Nc == 0) return;
+    // Kbar_cc = sum_s B_c^T Kbar_cc^s B_c, owners in ascending subdomain order
+    std::vector<long long> kco(su.Ns);
+    std::vector<int> ncs(su.Ns);
+    for (int s = 0; s < su.Ns; ++s) {
+      kco[s] = so.kcc_off[su.subs[s].op_slot];
+      ncs[s] = (int)su.subs[s].c.size();
+    }
+    DBuf<long long> dkco;
+    DBuf<int> dncs, dos, dol;
+    dkco.upload(kco, st); dncs.upload(ncs, st); dos.upload(osub, st); dol.upload(oloc, st);
+    DBuf<double> K;
+    K.alloc((size_t)Nc * Nc);
+    launch_kcc_assemble(d_optr.p, dos.p, dol.p, dkco.p, dncs.p, d_kccs.p, Nc, K.p);
+    // blocked Cholesky: diagonal blocks by k_front_elim_large, panels by cuBLAS
+    const int NBc = 256;
+    const double one = 1.0, mone = -1.0, zero = 0.0;
+    for (int k0 = 0; k0 < Nc; k0 += NBc) {
+      const int kb = std::min(NBc, Nc - k0);
+      std::vector<FrontDesc> f{{(long long)k0 * Nc + k0, kb, kb, Nc, FETIGPU_E_SINGULAR_COARSE}};
+      DBuf<FrontDesc> df;
+      df.upload(f, st);
+      k_front_elim_large<<<1, kThreads, 0, st>>>(df.p, K.p, d_status.p);
+      LAUNCH_CHECK();
+      CK(cudaStreamSynchronize(st));
+      const int rest = Nc - k0 - kb;
+      if (rest > 0) {
+        CB(cublasDtrsm(cb, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT,
+                       rest, kb, &one, K.p + (size_t)k0 * Nc + k0, Nc, K.p + (size_t)k0 * Nc + k0 + kb, Nc));
+        CB(cublasDsyrk(cb, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, rest, kb, &mone,
+                       K.p + (size_t)k0 * Nc + k0 + kb, Nc, &one, K.p + (size_t)(k0 + kb) * Nc + k0 + kb, Nc));
+      }
+    }
+    check_status();
+    // inverse: X = L^{-1}, Kinv = X^T X
+    DBuf<double> X;
+    X.alloc((size_t)Nc * Nc);
+    launch_identity(X.p, Nc);
+    CB(cublasDtrsm(cb, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, Nc, Nc,
+                   &one, K.p, Nc, X.p, Nc));
+    d_Kinv.alloc((size_t)Nc * Nc);
+    CB(cublasDsyrk(cb, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, Nc, Nc, &one, X.p, Nc, &zero, d_Kinv.p, Nc));
+    launch_symmetrize(d_Kinv.p, Nc);
+    CK(cudaStreamSynchronize(st));
+  }
+
+  void launch_kcc_assemble(const int* optr, const int* osub, const int* oloc, const long long* kco,
+                           const int* ncs, const double* kccs, int Nc, double* K);
+  void launch_identity(double* X, int n);
+  void launch_symmetrize(double* A, int n);
+
+  void build() {
+    CK(cudaEventRecord(ev0, st));
+    CK(cudaMemcpyToSymbolAsync(c_kunit, su.kunit, sizeof(su.kunit), 0, cudaMemcpyHostToDevice, st));
+    build_nd();
+    CK(cudaEventRecord(ev1, st));
+    nd_ms = elapsed(ev0, ev1);
+    build_ops();
+    CK(cudaEventRecord(ev2, st));
+    slot_ms = elapsed(ev1, ev2);
+    build_ms = elapsed(ev0, ev2);
+    built = true;
+  }
+
+  // -------------------------------------------------------- operators --
+  void apply_F(const double* x, double* y, int ncols, int ldx, int ldy) {
+    const int Ns = su.Ns;
+    if (su.method == FETIGPU_TFETI) {
+      for (int c = 0; c < ncols; ++c) CK(cudaMemsetAsync(y + (size_t)c * ldy, 0, su.m * 8, st));
+      dim3 grid(Ns, ncols);
+      k_gather_gemv_scatter<3, false><<<grid, kThreads, max_ld * 8, st>>>(
+          d_op.p, d_opmat.p, d_oprows.p, d_opcoef.p, x, y, nullptr, 0, nullptr, nullptr, ldx, ldy);
+      LAUNCH_CHECK();
+    } else {
+      for (int c = 0; c < ncols; ++c) {
+        const double* xc = x + (size_t)c * ldx;
+        double* yc = y + (size_t)c * ldy;
+        k_gather_gemv_scatter<1, true><<<Ns, kThreads, max_ld * 8, st>>>(
+            d_op.p, d_opmat.p, d_oprows.p, d_opcoef.p, xc, nullptr, nullptr, 0, d_vbuf.p, d_voff.p, ldx, 0);
+        k_dp_t<<<Ns, kThreads, 0, st>>>(d_op.p, d_dp.p, d_oprows.p, d_opcoef.p, d_abc.p, xc, d_tbuf.p);
+        k_coarse_gather<<<grid_for(su.Nc), kThreads, 0, st>>>(d_optr.p, d_oidx.p, d_tbuf.p, su.Nc, d_g.p,
+                                                             1.0, nullptr);
+        k_dense_gemv<<<grid_for((long long)su.Nc * 32), kThreads, 0, st>>>(d_Kinv.p, su.Nc, d_g.p, d_h.p);
+        CK(cudaMemsetAsync(yc, 0, su.m * 8, st));
+        k_dp_phase2<<<Ns, kThreads, 0, st>>>(d_op.p, d_dp.p, d_oprows.p, d_opcoef.p, d_abc.p, d_cmap.p,
+                                             d_h.p, d_vbuf.p, yc, 1.0);
+        LAUNCH_CHECK();
+      }
+    }
+  }
+
+  void apply_precond(const double* r, double* z, double* Zcols) {
+    CK(cudaMemsetAsync(z, 0, su.m * 8, st));
+    if (Zcols) CK(cudaMemsetAsync(Zcols, 0, (size_t)su.m * su.Ns * 8, st));
+    if (KRp == 1)
+      k_gather_gemv_scatter<1, false><<<su.Ns, kThreads, max_pc_ld * 8, st>>>(
+          d_pc.p, d_pcmat.p, d_pcrows.p, d_pccoef.p, r, z, Zcols, su.m, nullptr, nullptr, 0, 0);
+    else
+      k_gather_gemv_scatter<3, false><<<su.Ns, kThreads, max_pc_ld * 8, st>>>(
+          d_pc.p, d_pcmat.p, d_pcrows.p, d_pccoef.p, r, z, Zcols, su.m, nullptr, nullptr, 0, 0);
+    LAUNCH_CHECK();
+  }
+
+  // corr = P v - v for ncols columns (T-FETI); caller adds
+  void proj_corr(const double* v, int ldv, double* corr, int ldc, int ncols, double gsign = -1.0) {
+    const int nc = 3 * su.Ns;
+    DBuf<double> g, h;
+    double* gp = d_g.p;
+    double* hp = d_h.p;
+    if (ncols > 1) {
+      g.alloc((size_t)nc * ncols);
+      h.alloc((size_t)nc * ncols);
+      gp = g.p;
+      hp = h.p;
+    }
+    k_proj_gather<<<dim3(su.Ns, ncols), kThreads, 0, st>>>(d_pj.p, d_pcrows.p, d_pjcoef.p, d_RT.p,
+                                                          d_rt_off.p, v, ldv, gp, nc, gsign);
+    k_small_gemm<<<dim3(grid_for(nc), ncols), kThreads, 0, st>>>(d_H.p, nc, gp, nc, hp, nc);
+    for (int c = 0; c < ncols; ++c) CK(cudaMemsetAsync(corr + (size_t)c * ldc, 0, su.m * 8, st));
+    k_proj_scatter<<<dim3(su.Ns, ncols), kThreads, 0, st>>>(d_pj.p, d_pcrows.p, d_pjcoef.p, d_RT.p,
+                                                           d_rt_off.p, hp, nc, corr, ldc);
+    LAUNCH_CHECK();
+    if (ncols > 1) CK(cudaStreamSynchronize(st));
+  }
+
+  void project(double* v, int ncols, int ld) {
+    if (su.method != FETIGPU_TFETI) return;
+    DBuf<double> corr;
+    double* cp = d_v3.p;
+    if (ncols > 1) { corr.alloc((size_t)su.m * ncols); cp = corr.p; }
+    proj_corr(v, ld, cp, su.m, ncols);
+    k_add<<<dim3(grid_for(su.m), ncols), kThreads, 0, st>>>(su.m, cp, v, su.m, ld);
+    LAUNCH_CHECK();
+    if (ncols > 1) CK(cudaStreamSynchronize(st));
+  }
+
+  // per-subdomain boundary rhs b = (f - B^T lambda)[src] - S[src,D] gD - S[src,c] u_c
+  void launch_bnd_rhs(const double* lambda, const double* uc);
+  void launch_bnd_u(const double* uc, double* ub_all);
+  void launch_dp_fbar();
+  void launch_rhs_scatter(double* out);
+  void launch_add_rigid(double* u, const double* alpha);
+  void launch_scatter_perim(const double* ub_all, double* u);
+
+  void rhs() {
+    const int m = su.m;
+    // x_s = S_kk^{-1} f_k (T-FETI) or S_rr^{-1} (f_r - S_rD g) (FETI-DP)
+    launch_bnd_rhs(nullptr, nullptr);
+    k_chol_solve<<<su.Ns, kThreads, max_ne * 8, st>>>(d_opfac.p, d_fac_off.p, d_slot_of.p, d_fac_ne.p, d_xb.p,
+                                                       d_xoff.p);
+    LAUNCH_CHECK();
+    CK(cudaMemsetAsync(d_v1.p, 0, m * 8, st));
+    launch_rhs_scatter(d_v1.p);  // B K^+ f
+    if (su.method == FETIGPU_TFETI) {
+      DBuf<double> gap;
+      gap.upload(su.gap, st);
+      k_sub<<<grid_for(m), kThreads, 0, st>>>(m, d_v1.p, gap.p, d_d.p);
+      // lambda0 = G^T (G G^T)^{-1} e = -B R H e
+      k_small_gemm<<<grid_for(3 * su.Ns), kThreads, 0, st>>>(d_H.p, 3 * su.Ns, d_e.p, 3 * su.Ns, d_h.p, 3 * su.Ns);
+      CK(cudaMemsetAsync(d_v2.p, 0, m * 8, st));
+      k_proj_scatter<<<su.Ns, kThreads, 0, st>>>(d_pj.p, d_pcrows.p, d_pjcoef.p, d_RT.p, d_rt_off.p, d_h.p,
+                                                 3 * su.Ns, d_v2.p, m);
+      CK(cudaMemsetAsync(d_lam0.p, 0, m * 8, st));
+      k_axpy<<<grid_for(m), kThreads, 0, st>>>(m, -1.0, d_v2.p, d_lam0.p);
+      CK(cudaStreamSynchronize(st));
+      gap.release();
+    } else {
+      // fbar_c = sum B_c^T (f_c - S_cD g - S_cr x); d = d_r - F_rc Kbar^{-1} fbar_c
+      launch_dp_fbar();
+      k_coarse_gather<<<grid_for(su.Nc), kThreads, 0, st>>>(d_optr.p, d_oidx.p, d_fbar_loc.p, su.Nc, d_fbar.p,
+                                                           1.0, nullptr);
+      k_dense_gemv<<<grid_for((long long)su.Nc * 32), kThreads, 0, st>>>(d_Kinv.p, su.Nc, d_fbar.p, d_h.p);
+      CK(cudaMemsetAsync(d_v2.p, 0, m * 8, st));
+      k_dp_phase2<<<su.Ns, kThreads, 0, st>>>(d_op.p, d_dp.p, d_oprows.p, d_opcoef.p, d_abc.p, d_cmap.p, d_h.p,
+                                              nullptr, d_v2.p, 0.0);
+      k_sub<<<grid_for(m), kThreads, 0, st>>>(m, d_v1.p, d_v2.p, d_d.p);
+      CK(cudaMemsetAsync(d_lam0.p, 0, m * 8, st));
+      LAUNCH_CHECK();
+    }
+    CK(cudaStreamSynchronize(st));
+    have_rhs = true;
+  }
+
+  void recover(const double* lambda_dev, double* u_dev) {
+    const int m = su.m, Ns = su.Ns;
+    if (!have_rhs) rhs();
+    DBuf<double> ub, alpha, uc;
+    ub.alloc((size_t)Ns * su.nb);
+    if (su.method == FETIGPU_TFETI) {
+      // rho = d - F lambda; alpha = (G G^T)^{-1} G rho (least squares, decomposition.hpp:143)
+      apply_F(lambda_dev, d_v1.p, 1, m, m);
+      k_sub<<<grid_for(m), kThreads, 0, st>>>(m, d_d.p, d_v1.p, d_v2.p);
+      k_proj_gather<<<su.Ns, kThreads, 0, st>>>(d_pj.p, d_pcrows.p, d_pjcoef.p, d_RT.p, d_rt_off.p, d_v2.p, m,
+                                                d_g.p, 3 * Ns, -1.0);
+      alpha.alloc(3 * (size_t)Ns);
+      k_small_gemm<<<grid_for(3 * Ns), kThreads, 0, st>>>(d_H.p, 3 * Ns, d_g.p, 3 * Ns, alpha.p, 3 * Ns);
+      launch_bnd_rhs(lambda_dev, nullptr);
+    } else {
+      // u_c = Kbar^{-1} (fbar_c + F_rc^T lambda)
+      k_dp_t<<<Ns, kThreads, 0, st>>>(d_op.p, d_dp.p, d_oprows.p, d_opcoef.p, d_abc.p, lambda_dev, d_tbuf.p);
+      k_coarse_gather<<<grid_for(su.Nc), kThreads, 0, st>>>(d_optr.p, d_oidx.p, d_tbuf.p, su.Nc, d_g.p, 1.0,
+                                                           d_fbar.p);
+      uc.alloc(std::max(1, su.Nc));
+      k_dense_gemv<<<grid_for((long long)su.Nc * 32), kThreads, 0, st>>>(d_Kinv.p, su.Nc, d_g.p, uc.p);
+      launch_bnd_rhs(lambda_dev, uc.p);
+    }
+    k_chol_solve<<<Ns, kThreads, max_ne * 8, st>>>(d_opfac.p, d_fac_off.p, d_slot_of.p, d_fac_ne.p, d_xb.p,
+                                                    d_xoff.p);
+    launch_bnd_u(uc.p, ub.p);
+    CK(cudaMemsetAsync(u_dev, 0, (size_t)Ns * su.nloc * 8, st));
+    launch_scatter_perim(ub.p, u_dev);
+    if (!keep_factors) fail(FETIGPU_E_STATE, "recovery needs the ND factors");
+    int shm = 0;
+    for (auto& nd : su.nd.nodes) shm = std::max(shm, nd.nf);
+    k_nd_backsub<<<Ns, kThreads, shm * 8, st>>>(d_nodes.p, d_topdown.p, (int)su.nd.topdown.size(), d_nd_dofs.p,
+                                                d_ndfac.p, su.nd.factor_stride, d_design.p, u_dev, su.nloc);
+    LAUNCH_CHECK();
+    if (su.method == FETIGPU_TFETI) launch_add_rigid(u_dev, alpha.p);
+    CK(cudaStreamSynchronize(st));
+  }
+
+  // ------------------------------------------------------------ engine --
+  void dots(std::initializer_list<std::pair<const double*, const double*>> pairs, double* out) {
+    DotArgs a{};
+    int k = 0;
+    for (auto& p : pairs) { a.a[k] = p.first; a.b[k] = p.second; ++k; }
+    a.npairs = k;
+    a.n = su.m;
+    k_dot_partial<<<kDotBlocks, kThreads, 0, st>>>(a, d_partial.p);
+    k_dot_final<<<1, 32 * k, 0, st>>>(d_partial.p, k, out);
+    LAUNCH_CHECK();
+  }
+
+  void precond_projected(const double* r, double* z, double* Zcols) {
+    apply_precond(r, z, Zcols);
+    project(z, 1, su.m);
+  }
+
+  int solve(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_trace* tr);
+  int solve_rrs(const fetigpu_solve_opts& o, double* lam, fetigpu_trace* tr);
+};
+
+// ------------------------------------------------------- small kernels ----
+__global__ void k_kcc_assemble(const int* optr, const int* osub, const int* oloc, const long long* kco,
+                               const int* ncs, const double* kccs, int Nc, double* K) {
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < (long long)Nc * Nc;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int j = (int)(idx / Nc), i = (int)(idx - (long long)j * Nc);
+    double v = 0.0;
+    int a = optr[i], b = optr[j];
+    const int ae = optr[i + 1], be = optr[j + 1];
+    while (a < ae && b < be) {
+      const int sa = osub[a], sb = osub[b];
+      if (sa == sb) {
+        const int nc = ncs[sa];
+        v += kccs[kco[sa] + (long long)oloc[a] * nc + oloc[b]];
+        ++a; ++b;
+      } else if (sa < sb) ++a;
+      else ++b;
+    }
+    K[idx] = v;
+  }
+}
+__global__ void k_identity(double* X, int n) {
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < (long long)n * n;
+       idx += (long long)gridDim.x * blockDim.x)
+    X[idx] = (idx / n == idx % n) ? 1.0 : 0.0;
+}
+__global__ void k_symmetrize(double* A, int n) {
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < (long long)n * n;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int j = (int)(idx / n), i = (int)(idx % n);
+    if (i < j) A[idx] = A[(long long)i * n + j];
+  }
+}
+void Ctx::launch_kcc_assemble(const int* optr, const int* osub, const int* oloc, const long long* kco,
+                              const int* ncs, const double* kccs, int Nc, double* K) {
+  k_kcc_assemble<<<grid_for((long long)Nc * Nc), kThreads, 0, st>>>(optr, osub, oloc, kco, ncs, kccs, Nc, K);
+  LAUNCH_CHECK();
+}
+void Ctx::launch_identity(double* X, int n) {
+  k_identity<<<grid_for((long long)n * n), kThreads, 0, st>>>(X, n);
+  LAUNCH_CHECK();
+}
+void Ctx::launch_symmetrize(double* A, int n) {
+  k_symmetrize<<<grid_for((long long)n * n), kThreads, 0, st>>>(A, n);
+  LAUNCH_CHECK();
+}
+
+// b_i = p[src_i] - sum_D S[src_i, D] g - sum_c S[src_i, c] u_c  with
+// p = f - B_s^T lambda on the perimeter
+__global__ void k_bnd_rhs(int nb, const double* __restrict__ fb, const double* __restrict__ lambda,
+                          const OpSub* __restrict__ ops, const int* __restrict__ rows,
+                          const double* __restrict__ coefs, int KR, const int* __restrict__ top_pos,
+                          const int* __restrict__ top_off, const int* __restrict__ D,
+                          const int* __restrict__ D_off, const int* __restrict__ D_cnt,
+                          const double* __restrict__ gD, const int* __restrict__ c_pos,
+                          const int* __restrict__ c_off, const int* __restrict__ cmap,
+                          const DpSub* __restrict__ dps, const double* __restrict__ uc,
+                          const double* __restrict__ S, const int* __restrict__ design,
+                          const int* __restrict__ slot_of, const int* __restrict__ src,
+                          const int* __restrict__ src_off, const int* __restrict__ nes,
+                          double* __restrict__ xb, const int* __restrict__ xoff) {
+  extern __shared__ double p[];
+  const int s = blockIdx.x;
+  for (int i = threadIdx.x; i < nb; i += blockDim.x) p[i] = fb[(size_t)s * nb + i];
+  __syncthreads();
+  if (lambda) {
+    const OpSub d = ops[s];
+    for (int a = threadIdx.x; a < d.ns; a += blockDim.x) {
+      double v = 0.0;
+      for (int k = 0; k < KR; ++k) {
+        const int r = rows[d.map_off + a * KR + k];
+        if (r >= 0) v += coefs[d.map_off + a * KR + k] * lambda[r];
+      }
+      p[top_pos[top_off[s] + a]] -= v;
+    }
+    __syncthreads();
+  }
+  const int sl = slot_of[s];
+  const int ne = nes[sl];
+  const int* sr = src + src_off[sl];
+  const double* Sd = S + (size_t)design[s] * nb * nb;
+  const int nD = D_cnt[s];
+  const int nc = (uc && dps) ? dps[s].nc : 0;
+  for (int i = threadIdx.x; i < ne; i += blockDim.x) {
+    const int pi = sr[i];
+    double v = p[pi];
+    for (int k = 0; k < nD; ++k) v -= Sd[(size_t)D[D_off[s] + k] * nb + pi] * gD[D_off[s] + k];
+    for (int k = 0; k < nc; ++k)
+      v -= Sd[(size_t)c_pos[c_off[s] + k] * nb + pi] * uc[cmap[dps[s].cmap_off + k]];
+    xb[xoff[s] + i] = v;
+  }
+}
+void Ctx::launch_bnd_rhs(const double* lambda, const double* uc) {
+  k_bnd_rhs<<<su.Ns, kThreads, su.nb * 8, st>>>(
+      su.nb, d_fb.p, lambda, d_op.p, d_oprows.p, d_opcoef.p, KR, d_top_pos.p, d_top_off.p, d_D.p, d_D_off.p,
+      d_D_cnt.p, d_gD.p, d_c_pos.p, d_c_off.p, d_cmap.p, su.method == FETIGPU_FETIDP ? d_dp.p : nullptr, uc,
+      d_S.p, d_design.p, d_slot_of.p, d_op_src.p, d_op_src_off.p, d_fac_ne.p, d_xb.p, d_xoff.p);
+  LAUNCH_CHECK();
+}
+
+// d[row] += sign * x[ext[a]] over the operator support (B K^+ f)
+__global__ void k_rhs_scatter(const OpSub* __restrict__ ops, const int* __restrict__ rows,
+                              const double* __restrict__ coefs, int KR, const int* __restrict__ slot_of,
+                              const int* __restrict__ ext, const int* __restrict__ ext_off,
+                              const double* __restrict__ xb, const int* __restrict__ xoff,
+                              double* __restrict__ out) {
+  const int s = blockIdx.x;
+  const OpSub d = ops[s];
+  const int* e = ext + ext_off[slot_of[s]];
+  for (int a = threadIdx.x; a < d.ns; a += blockDim.x) {
+    const double v = xb[xoff[s] + e[a]];
+    for (int k = 0; k < KR; ++k) {
+      const int r = rows[d.map_off + a * KR + k];
+      if (r >= 0) atomicAdd(out + r, coefs[d.map_off + a * KR + k] * v);
+    }
+  }
+}
+void Ctx::launch_rhs_scatter(double* out) {
+  k_rhs_scatter<<<su.Ns, kThreads, 0, st>>>(d_op.p, d_oprows.p, d_opcoef.p, KR, d_slot_of.p, d_op_ext.p,
+                                            d_op_ext_off.p, d_xb.p, d_xoff.p, out);
+  LAUNCH_CHECK();
+}
+
+// fbar_c^s = f_c - S[c,D] g - S[c, r] x   (x = S_rr^{-1} b on r)
+__global__ void k_dp_fbar(int nb, const double* __restrict__ fb, const int* __restrict__ D,
+                          const int* __restrict__ D_off, const int* __restrict__ D_cnt,
+                          const double* __restrict__ gD, const int* __restrict__ c_pos,
+                          const int* __restrict__ c_off, const DpSub* __restrict__ dps,
+                          const double* __restrict__ S, const int* __restrict__ design,
+                          const int* __restrict__ slot_of, const int* __restrict__ src,
+                          const int* __restrict__ src_off, const int* __restrict__ nes,
+                          const double* __restrict__ xb, const int* __restrict__ xoff,
+                          double* __restrict__ fbar) {
+  const int s = blockIdx.x;
+  const DpSub dp = dps[s];
+  const int sl = slot_of[s];
+  const int ne = nes[sl];
+  const int* sr = src + src_off[sl];
+  const double* Sd = S + (size_t)design[s] * nb * nb;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int k = warp; k < dp.nc; k += blockDim.x >> 5) {
+    const int cp = c_pos[c_off[s] + k];
+    double v = 0.0;
+    for (int i = lane; i < ne; i += 32) v += Sd[(size_t)sr[i] * nb + cp] * xb[xoff[s] + i];
+    for (int q = lane; q < D_cnt[s]; q += 32) v += Sd[(size_t)D[D_off[s] + q] * nb + cp] * gD[D_off[s] + q];
+    v = warp_sum(v);
+    if (lane == 0) fbar[dp.t_off + k] = fb[(size_t)s * nb + cp] - v;
+  }
+}
+void Ctx::launch_dp_fbar() {
+  k_dp_fbar<<<su.Ns, kThreads, 0, st>>>(su.nb, d_fb.p, d_D.p, d_D_off.p, d_D_cnt.p, d_gD.p, d_c_pos.p,
+                                        d_c_off.p, d_dp.p, d_S.p, d_design.p, d_slot_of.p, d_op_src.p,
+                                        d_op_src_off.p, d_fac_ne.p, d_xb.p, d_xoff.p, d_fbar_loc.p);
+  LAUNCH_CHECK();
+}
+
+// perimeter displacement: ub[src_i] = x_i; FETI-DP adds corners and supports
+__global__ void k_bnd_u(int nb, const int* __restrict__ slot_of, const int* __restrict__ src,
+                        const int* __restrict__ src_off, const int* __restrict__ nes,
+                        const double* __restrict__ xb, const int* __restrict__ xoff,
+                        const int* __restrict__ D, const int* __restrict__ D_off,
+                        const int* __restrict__ D_cnt, const double* __restrict__ gD,
+                        const int* __restrict__ c_pos, const int* __restrict__ c_off,
+                        const DpSub* __restrict__ dps, const int* __restrict__ cmap,
+                        const double* __restrict__ uc, double* __restrict__ ub) {
+  const int s = blockIdx.x;
+  double* u = ub + (size_t)s * nb;
+  for (int i = threadIdx.x; i < nb; i += blockDim.x) u[i] = 0.0;
+  __syncthreads();
+  const int sl = slot_of[s];
+  const int* sr = src + src_off[sl];
+  for (int i = threadIdx.x; i < nes[sl]; i += blockDim.x) u[sr[i]] = xb[xoff[s] + i];
+  for (int k = threadIdx.x; k < D_cnt[s]; k += blockDim.x) u[D[D_off[s] + k]] = gD[D_off[s] + k];
+  if (dps && uc)
+    for (int k = threadIdx.x; k < dps[s].nc; k += blockDim.x)
+      u[c_pos[c_off[s] + k]] = uc[cmap[dps[s].cmap_off + k]];
+}
+void Ctx::launch_bnd_u(const double* uc, double* ub_all) {
+  k_bnd_u<<<su.Ns, kThreads, 0, st>>>(su.nb, d_slot_of.p, d_op_src.p, d_op_src_off.p, d_fac_ne.p, d_xb.p,
+                                      d_xoff.p, d_D.p, d_D_off.p, d_D_cnt.p, d_gD.p, d_c_pos.p, d_c_off.p,
+                                      su.method == FETIGPU_FETIDP ? d_dp.p : nullptr, d_cmap.p, uc, ub_all);
+  LAUNCH_CHECK();
+}
+__global__ void k_scatter_perim(int nb, int nloc, const int* __restrict__ pdof, const double* __restrict__ ub,
+                                double* __restrict__ u) {
+  const int s = blockIdx.x;
+  for (int i = threadIdx.x; i < nb; i += blockDim.x) u[(size_t)s * nloc + pdof[i]] = ub[(size_t)s * nb + i];
+}
+void Ctx::launch_scatter_perim(const double* ub_all, double* u) {
+  DBuf<int> pd;
+  pd.upload(su.perim_dof, st);
+  k_scatter_perim<<<su.Ns, kThreads, 0, st>>>(su.nb, su.nloc, pd.p, ub_all, u);
+  LAUNCH_CHECK();
+  CK(cudaStreamSynchronize(st));
+}
+__global__ void k_add_rigid(int nloc, const double* __restrict__ R, const double* __restrict__ alpha,
+                            double* __restrict__ u) {
+  const int s = blockIdx.x;
+  const double a0 = alpha[3 * s], a1 = alpha[3 * s + 1], a2 = alpha[3 * s + 2];
+  for (int i = threadIdx.x; i < nloc; i += blockDim.x)
+    u[(size_t)s * nloc + i] += R[i] * a0 + R[nloc + i] * a1 + R[2 * nloc + i] * a2;
+}
+void Ctx::launch_add_rigid(double* u, const double* alpha) {
+  DBuf<double> R;
+  R.upload(su.Rfull, st);
+  k_add_rigid<<<su.Ns, kThreads, 0, st>>>(su.nloc, R.p, alpha, u);
+  LAUNCH_CHECK();
+  CK(cudaStreamSynchronize(st));
+}
+
+// ----------------------------------------------------------- the engine ---
+// pcg single / FO: z = P Fbar^{-1} P r, eps_r = sqrt(r^T z)
+// (PAPER.md:384); FO keeps F-normalized directions and re-orthogonalizes by
+// classical Gram-Schmidt with `reorth_passes` passes.
+int Ctx::solve(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_trace* tr) {
+  if (o.directions == FETIGPU_RRS) return solve_rrs(o, lambda_host, tr);
+  const int m = su.m;
+  const bool fo = o.directions == FETIGPU_FO;
+  const int passes = std::max(1, o.reorth_passes);
+  rhs();
+  DBuf<double> lam, r, z, w, q, corr, Wst, Qst, psi;
+  DBuf<Scal> sc;
+  lam.alloc(m); r.alloc(m); z.alloc(m); w.alloc(m); q.alloc(m); corr.alloc(m);
+  sc.alloc(1);
+  sc.zero(st);
+  if (fo) {
+    Wst.alloc((size_t)m * std::max(1, o.max_it));
+    Qst.alloc((size_t)m * std::max(1, o.max_it));
+    psi.alloc(std::max(1, o.max_it));
+  }
+  Scal* hs = nullptr;
+  CK(cudaMallocHost(&hs, sizeof(Scal)));
+  std::unique_ptr<Scal, decltype(&cudaFreeHost)> hs_guard(hs, cudaFreeHost);
+  const bool tf = su.method == FETIGPU_TFETI;
+  CK(cudaEventRecord(ev0, st));
+  CK(cudaMemcpyAsync(lam.p, d_lam0.p, m * 8, cudaMemcpyDeviceToDevice, st));
+  apply_F(lam.p, q.p, 1, m, m);
+  int fapp = 1;
+  k_sub<<<grid_for(m), kThreads, 0, st>>>(m, d_d.p, q.p, r.p);
+  project(r.p, 1, m);
+  precond_projected(r.p, z.p, nullptr);
+  dots({{r.p, z.p}, {r.p, r.p}, {z.p, z.p}}, &sc.p->rz);
+  CK(cudaMemcpyAsync(hs, sc.p, sizeof(Scal), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  auto metric = [&](const Scal& s) {
+    if (s.rz < -1e-14 * std::sqrt(s.rr) * std::sqrt(s.zz))
+      fail(FETIGPU_E_NEGATIVE_INNER_PRODUCT, "r^T z < 0: preconditioner is not symmetric positive");
+    return std::sqrt(std::max(s.rz, 0.0));
+  };
+  const double eps0 = metric(*hs);
+  double eps = eps0, rz_old = hs->rz;
+  int it = 0, status = FETIGPU_MAX_ITER;
+  auto push = [&](double e, int kept) {
+    if (tr && it < tr->cap) {
+      if (tr->eps) tr->eps[it] = e;
+      if (tr->kept) tr->kept[it] = kept;
+      if (tr->f_app) tr->f_app[it] = fapp;
+    }
+  };
+  push(eps0, 1);
+  CK(cudaMemcpyAsync(w.p, z.p, m * 8, cudaMemcpyDeviceToDevice, st));
+  const double target = o.rel ? o.tol * eps0 : o.tol;
+  const double one = 1.0, mone = -1.0, zero = 0.0;
+  while (true) {
+    if (eps <= target) { status = FETIGPU_CONVERGED; break; }
+    if (it >= o.max_it) { status = FETIGPU_MAX_ITER; break; }
+    apply_F(w.p, q.p, 1, m, m);
+    ++fapp;
+    dots({{w.p, q.p}, {w.p, r.p}}, &sc.p->delta);
+    if (tf) proj_corr(q.p, m, corr.p, m, 1);
+    // breakdown check needs delta before the update
+    CK(cudaMemcpyAsync(hs, sc.p, sizeof(Scal), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (!(hs->delta > 0.0)) { status = FETIGPU_BREAKDOWN; break; }
+    k_pcg_update<<<grid_for(m), kThreads, 0, st>>>(m, sc.p, fo ? 1 : 0, w.p, q.p, tf ? corr.p : nullptr, lam.p,
+                                                   r.p);
+    precond_projected(r.p, z.p, nullptr);
+    dots({{r.p, z.p}, {r.p, r.p}, {z.p, z.p}}, &sc.p->rz);
+    if (fo) {
+      k_fo_store<<<grid_for(m), kThreads, 0, st>>>(m, sc.p, w.p, q.p, Wst.p + (size_t)it * m,
+                                                   Qst.p + (size_t)it * m);
+    }
+    CK(cudaMemcpyAsync(hs, sc.p, sizeof(Scal), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    eps = metric(*hs);
+    ++it;
+    push(eps, 1);
+    if (fo) {
+      CK(cudaMemcpyAsync(w.p, z.p, m * 8, cudaMemcpyDeviceToDevice, st));
+      for (int pss = 0; pss < passes; ++pss) {
+        CB(cublasDgemv(cb, CUBLAS_OP_T, m, it, &one, Qst.p, m, w.p, 1, &zero, psi.p, 1));
+        CB(cublasDgemv(cb, CUBLAS_OP_N, m, it, &mone, Wst.p, m, psi.p, 1, &one, w.p, 1));
+      }
+    } else {
+      const double beta = hs->rz / rz_old;
+      k_xpby<<<grid_for(m), kThreads, 0, st>>>(m, z.p, beta, w.p);
+    }
+    rz_old = hs->rz;
+    LAUNCH_CHECK();
+  }
+  CK(cudaEventRecord(ev1, st));
+  const double ms = elapsed(ev0, ev1);
+  CK(cudaMemcpyAsync(lambda_host, lam.p, m * 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (tr) {
+    tr->status = status;
+    tr->iterations = it;
+    tr->f_applies = fapp;
+    tr->eps0 = eps0;
+    tr->eps_final = eps;
+    tr->solve_ms = ms;
+  }
+  return 0;
+}
+
+// Rank-Revealing Simultaneous FETI, Alg. 1 of PAPER.md:302-351:
+// one search direction per subdomain, Delta = Q^T W factorized by the
+// rank-revealing Cholesky, W, Q compressed to F-orthonormal columns, and the
+// new block re-orthogonalized against all stored blocks (CGS, 2 passes).
+int Ctx::solve_rrs(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_trace* tr) {
+  const int m = su.m, Ns = su.Ns;
+  const int passes = std::max(1, o.reorth_passes);
+  rhs();
+  DBuf<double> lam, r, z, q, tmp, Z, W, Q, Wsel, Delta, gamma;
+  DBuf<int> perm, rank_d;
+  DBuf<Scal> sc;
+  lam.alloc(m); r.alloc(m); z.alloc(m); q.alloc(m); tmp.alloc(m);
+  Z.alloc((size_t)m * Ns); W.alloc((size_t)m * Ns); Wsel.alloc((size_t)m * Ns);
+  Delta.alloc((size_t)Ns * Ns); gamma.alloc(Ns);
+  perm.alloc(Ns); rank_d.alloc(1);
+  sc.alloc(1);
+  sc.zero(st);
+  std::vector<std::unique_ptr<DBuf<double>>> Ws, Qs, Psis;
+  std::vector<int> widths;
+  Scal* hs = nullptr;
+  CK(cudaMallocHost(&hs, sizeof(Scal)));
+  std::unique_ptr<Scal, decltype(&cudaFreeHost)> hs_guard(hs, cudaFreeHost);
+  const double one = 1.0, mone = -1.0, zero = 0.0;
+  CK(cudaEventRecord(ev0, st));
+  CK(cudaMemcpyAsync(lam.p, d_lam0.p, m * 8, cudaMemcpyDeviceToDevice, st));
+  apply_F(lam.p, q.p, 1, m, m);
+  int fapp = 1;
+  k_sub<<<grid_for(m), kThreads, 0, st>>>(m, d_d.p, q.p, r.p);
+  project(r.p, 1, m);
+  apply_precond(r.p, z.p, Z.p);  // Alg. 1 line 2 (columns) and z = Z 1
+  dots({{r.p, z.p}, {r.p, r.p}, {z.p, z.p}}, &sc.p->rz);
+  CK(cudaMemcpyAsync(hs, sc.p, sizeof(Scal), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  auto metric = [&](const Scal& s) {
+    if (s.rz < -1e-14 * std::sqrt(s.rr) * std::sqrt(s.zz))
+      fail(FETIGPU_E_NEGATIVE_INNER_PRODUCT, "r^T z < 0: preconditioner is not symmetric positive");
+    return std::sqrt(std::max(s.rz, 0.0));
+  };
+  const double eps0 = metric(*hs);
+  double eps = eps0;
+  int it = 0, status = FETIGPU_MAX_ITER, k = Ns;
+  auto push = [&](double e, int kept) {
+    if (tr && it < tr->cap) {
+      if (tr->eps) tr->eps[it] = e;
+      if (tr->kept) tr->kept[it] = kept;
+      if (tr->f_app) tr->f_app[it] = fapp;
+    }
+  };
+  push(eps0, Ns);
+  CK(cudaMemcpyAsync(W.p, Z.p, (size_t)m * Ns * 8, cudaMemcpyDeviceToDevice, st));
+  project(W.p, Ns, m);  // line 3
+  const double target = o.rel ? o.tol * eps0 : o.tol;
+  while (true) {
+    if (eps <= target) { status = FETIGPU_CONVERGED; break; }
+    if (it >= o.max_it) { status = FETIGPU_MAX_ITER; break; }
+    auto Qb = std::make_unique<DBuf<double>>();
+    Qb->alloc((size_t)m * k);
+    apply_F(W.p, Qb->p, k, m, m);  // line 7
+    fapp += k;
+    // line 8: Delta = Q^T W (lower triangle used)
+    CB(cublasDgemm(cb, CUBLAS_OP_T, CUBLAS_OP_N, k, k, m, &one, Qb->p, m, W.p, m, &zero, Delta.p, k));
+    k_mirror_lower<<<grid_for((long long)k * k), kThreads, 0, st>>>(Delta.p, k);
+    // line 9
+    k_pivchol<<<1, 1024, 0, st>>>(Delta.p, k, o.pivot_tol, perm.p, rank_d.p, d_status.p);
+    LAUNCH_CHECK();
+    int rank = 0;
+    CK(cudaMemcpyAsync(&rank, rank_d.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    int hstat = 0;
+    CK(cudaMemcpy(&hstat, d_status.p, sizeof(int), cudaMemcpyDeviceToHost));
+    if (hstat) { CK(cudaMemset(d_status.p, 0, sizeof(int))); fail(FETIGPU_E_INDEFINITE_INPUT, "pivoted Cholesky: negative pivot"); }
+    if (rank == 0) { status = FETIGPU_BREAKDOWN; break; }
+    // lines 10-11: W <- W N^T [L~^{-T}; 0], same for Q
+    auto Wb = std::make_unique<DBuf<double>>();
+    Wb->alloc((size_t)m * rank);
+    k_gather_cols<<<dim3(grid_for(m), rank), kThreads, 0, st>>>(W.p, m, perm.p, rank, Wb->p);
+    k_gather_cols<<<dim3(grid_for(m), rank), kThreads, 0, st>>>(Qb->p, m, perm.p, rank, Wsel.p);
+    CB(cublasDtrsm(cb, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, m, rank,
+                   &one, Delta.p, k, Wb->p, m));
+    CB(cublasDtrsm(cb, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, m, rank,
+                   &one, Delta.p, k, Wsel.p, m));
+    Qb->alloc((size_t)m * rank);
+    CK(cudaMemcpyAsync(Qb->p, Wsel.p, (size_t)m * rank * 8, cudaMemcpyDeviceToDevice, st));
+    // lines 13-15
+    CB(cublasDgemv(cb, CUBLAS_OP_T, m, rank, &one, Wb->p, m, r.p, 1, &zero, gamma.p, 1));
+    CB(cublasDgemv(cb, CUBLAS_OP_N, m, rank, &one, Wb->p, m, gamma.p, 1, &one, lam.p, 1));
+    CB(cublasDgemv(cb, CUBLAS_OP_N, m, rank, &one, Qb->p, m, gamma.p, 1, &zero, tmp.p, 1));
+    project(tmp.p, 1, m);
+    k_axpy<<<grid_for(m), kThreads, 0, st>>>(m, -1.0, tmp.p, r.p);
+    // line 16
+    apply_precond(r.p, z.p, Z.p);
+    dots({{r.p, z.p}, {r.p, r.p}, {z.p, z.p}}, &sc.p->rz);
+    CK(cudaMemcpyAsync(hs, sc.p, sizeof(Scal), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    eps = metric(*hs);
+    ++it;
+    push(eps, rank);
+    Ws.push_back(std::move(Wb));
+    Qs.push_back(std::move(Qb));
+    widths.push_back(rank);
+    // line 17
+    k = Ns;
+    CK(cudaMemcpyAsync(W.p, Z.p, (size_t)m * Ns * 8, cudaMemcpyDeviceToDevice, st));
+    project(W.p, Ns, m);
+    // lines 18-21: block classical Gram-Schmidt, `passes` passes
+    Psis.resize(Ws.size());
+    for (size_t j = 0; j < Ws.size(); ++j)
+      if (!Psis[j]) { Psis[j] = std::make_unique<DBuf<double>>(); Psis[j]->alloc((size_t)widths[j] * Ns); }
+    for (int p = 0; p < passes; ++p) {
+      for (size_t j = 0; j < Ws.size(); ++j)
+        CB(cublasDgemm(cb, CUBLAS_OP_T, CUBLAS_OP_N, widths[j], Ns, m, &one, Qs[j]->p, m, W.p, m, &zero,
+                       Psis[j]->p, widths[j]));
+      for (size_t j = 0; j < Ws.size(); ++j)
+        CB(cublasDgemm(cb, CUBLAS_OP_N, CUBLAS_OP_N, m, Ns, widths[j], &mone, Ws[j]->p, m, Psis[j]->p,
+                       widths[j], &one, W.p, m));
+    }
+  }
+  CK(cudaEventRecord(ev1, st));
+  const double ms = elapsed(ev0, ev1);
+  CK(cudaMemcpyAsync(lambda_host, lam.p, m * 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (tr) {
+    tr->status = status;
+    tr->iterations = it;
+    tr->f_applies = fapp;
+    tr->eps0 = eps0;
+    tr->eps_final = eps;
+    tr->solve_ms = ms;
+  }
+  return 0;
+}
+
+}  // namespace fg
+
+// ------------------------------------------------------------------ C-ABI --
+using namespace fg;
+struct fetigpu_ctx {
+  Ctx c;
+};
+static thread_local std::string g_err;
+
+template <class F>
+static int guarded(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const Error& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::bad_alloc& e) {
+    g_err = e.what();
+    return FETIGPU_E_OUT_OF_MEMORY;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return FETIGPU_E_INVALID_ARGUMENT;
+  }
+}
+#define NEED_BUILT(ctx) \
+  if (!(ctx) || !(ctx)->c.built) fail(FETIGPU_E_STATE, "context not built")
+
+extern "C" {
+
+const char* fetigpu_last_error(void) { return g_err.c_str(); }
+
+int fetigpu_create(const fetigpu_problem* p, fetigpu_ctx** out) {
+  *out = nullptr;
+  auto ctx = std::make_unique<fetigpu_ctx>();
+  int rc = guarded([&] {
+    if (!p) fail(FETIGPU_E_INVALID_ARGUMENT, "null problem");
+    ctx->c.su.load(*p);
+  });
+  if (rc == 0) *out = ctx.release();
+  return rc;
+}
+
+int fetigpu_build(fetigpu_ctx* ctx) {
+  return guarded([&] {
+    if (!ctx) fail(FETIGPU_E_INVALID_ARGUMENT, "null context");
+    if (ctx->c.built) fail(FETIGPU_E_STATE, "context already built");
+    if (!ctx->c.st) ctx->c.init_device();
+    ctx->c.build();
+  });
+}
+
+void fetigpu_destroy(fetigpu_ctx* ctx) { delete ctx; }
+
+int fetigpu_stats_get(const fetigpu_ctx* ctx, fetigpu_stats* s) {
+  return guarded([&] {
+    const Ctx& c = ctx->c;
+    int mx = 0;
+    for (auto& S : c.su.subs) mx = std::max(mx, (int)S.T.size());
+    s->m = c.su.m; s->n_sub = c.su.Ns; s->local_dofs = c.su.nloc; s->n_c = c.su.Nc;
+    s->n_kept = c.su.n_kept; s->n_iface = c.su.n_iface; s->max_ns = mx; s->n_designs = c.su.n_designs;
+    s->n_op_slots = (int)c.su.op_slots.size();
+    s->n_pc_slots = (int)(c.su.precond == FETIGPU_DIRICHLET ? c.su.pc_slots.size() : c.su.pc_lumped_T.size());
+    s->op_bytes = c.op_bytes; s->op_flops_per_col = c.op_flops; s->main_kernel_bytes = c.main_bytes;
+    s->build_ms = c.build_ms; s->nd_ms = c.nd_ms; s->slot_ms = c.slot_ms; s->coarse_ms = c.coarse_ms;
+    s->device_bytes = (double)g_device_bytes;
+  });
+}
+
+int fetigpu_rows(const fetigpu_ctx* ctx, int* kind, int* sp, int* dp, int* sm, int* dm, double* gap,
+                 int* mult, double* wp, double* wm) {
+  return guarded([&] {
+    const Setup& su = ctx->c.su;
+    for (int i = 0; i < su.m; ++i) {
+      const Row& r = su.rows[i];
+      kind[i] = r.kind; sp[i] = r.sp; dp[i] = r.dp; sm[i] = r.sm; dm[i] = r.dm;
+      gap[i] = r.gap; mult[i] = r.mult; wp[i] = su.wplus[i]; wm[i] = su.wminus[i];
+    }
+  });
+}
+
+int fetigpu_apply_F_device(fetigpu_ctx* ctx, const double* x, double* y, int ncols, int ld) {
+  return guarded([&] {
+    NEED_BUILT(ctx);
+    ctx->c.apply_F(x, y, ncols, ld, ld);
+  });
+}
+
+int fetigpu_apply_F(fetigpu_ctx* ctx, const double* x, double* y, int ncols, int ld) {
+  return guarded([&] {
+    NEED_BUILT(ctx);
+    Ctx& c = ctx->c;
+    const size_t bytes = (size_t)ld * ncols * 8;
+    DBuf<double> dx, dy;
+    dx.alloc((size_t)ld * ncols);
+    dy.alloc((size_t)ld * ncols);
+    CK(cudaMemcpyAsync(dx.p, x, bytes, cudaMemcpyHostToDevice, c.st));
+    c.apply_F(dx.p, dy.p, ncols, ld, ld);
+    CK(cudaMemcpyAsync(y, dy.p, bytes, cudaMemcpyDeviceToHost, c.st));
+    CK(cudaStreamSynchronize(c.st));
+  });
+}
+
+int fetigpu_apply_precond_device(fetigpu_ctx* ctx, const double* r, double* z, double* Z) {
+  return guarded([&] {
+    NEED_BUILT(ctx);
+    ctx->c.apply_precond(r, z, Z);
+  });
+}
+
+int fetigpu_apply_precond(fetigpu_ctx* ctx, const double* r, double* z, double* Zcols) {
+  return guarded([&] {
+    NEED_BUILT(ctx);
+    Ctx& c = ctx->c;
+    const int m = c.su.m;
+    DBuf<double> dr, dz, dZ;
+    dr.alloc(m);
+    dz.alloc(m);
+    if (Zcols) dZ.alloc((size_t)m * c.su.Ns);
+    CK(cudaMemcpyAsync(dr.p, r, m * 8, cudaMemcpyHostToDevice, c.st));
+    c.apply_precond(dr.p, dz.p, Zcols ? dZ.p : nullptr);
+    CK(cudaMemcpyAsync(z, dz.p, m * 8, cudaMemcpyDeviceToHost, c.st));
+    if (Zcols) CK(cudaMemcpyAsync(Zcols, dZ.p, (size_t)m * c.su.Ns * 8, cudaMemcpyDeviceToHost, c.st));
+    CK(cudaStreamSynchronize(c.st));
+  });
+}
+
+int fetigpu_project_device(fetigpu_ctx* ctx, double* v, int ncols, int ld) {
+  return guarded([&] {
+    NEED_BUILT(ctx);
+    ctx->c.project(v, ncols, ld);
+  });
+}
+
+int fetigpu_project(fetigpu_ctx* ctx, double* v, int ncols, int ld) {
+  return guarded([&] {
+    NEED_BUILT(ctx);
+    Ctx& c = ctx->c;
+    DBuf<double> dv;
+    dv.alloc((size_t)ld * ncols);
+    CK(cudaMemcpyAsync(dv.p, v, (size_t)ld * ncols * 8, cudaMemcpyHostToDevice, c.st));
+    c.project(dv.p, ncols, ld);
+    CK(cudaMemcpyAsync(v, dv.p, (size_t)ld * ncols * 8, cudaMemcpyDeviceToHost, c.st));
+    CK(cudaStreamSynchronize(c.st));
+  });
+}
+
+int fetigpu_rhs(fetigpu_ctx* ctx, double* d, double* l0) {
+  return guarded([&] {
+    NEED_BUILT(ctx);
+    Ctx& c = ctx->c;
+    c.rhs();
+    CK(cudaMemcpyAsync(d, c.d_d.p, c.su.m * 8, cudaMemcpyDeviceToHost, c.st));
+    CK(cudaMemcpyAsync(l0, c.d_lam0.p, c.su.m * 8, cudaMemcpyDeviceToHost, c.st));
+    CK(cudaStreamSynchronize(c.st));
+  });
+}
+
+int fetigpu_solve(fetigpu_ctx* ctx, const fetigpu_solve_opts* o, double* lambda, fetigpu_trace* tr) {
+  return guarded([&] {
+    NEED_BUILT(ctx);
+    ctx->c.solve(*o, lambda, tr);
+  });
+}
+
+int fetigpu_recover(fetigpu_ctx* ctx, const double* lambda, double* u) {
+  return guarded([&] {
+    NEED_BUILT(ctx);
+    Ctx& c = ctx->c;
+    DBuf<double> dl, du;
+    dl.alloc(c.su.m);
+    du.alloc((size_t)c.su.Ns * c.su.nloc);
+    CK(cudaMemcpyAsync(dl.p, lambda, c.su.m * 8, cudaMemcpyHostToDevice, c.st));
+    c.recover(dl.p, du.p);
+    CK(cudaMemcpyAsync(u, du.p, (size_t)c.su.Ns * c.su.nloc * 8, cudaMemcpyDeviceToHost, c.st));
+    CK(cudaStreamSynchronize(c.st));
+  });
+}
+
+int fetigpu_local_operator(fetigpu_ctx* ctx, int s, int* ns, int* dofs, double* F, int cap) {
+  return guarded([&] {
+    NEED_BUILT(ctx);
+    Ctx& c = ctx->c;
+    if (s < 0 || s >= c.su.Ns) fail(FETIGPU_E_INVALID_ARGUMENT, "subdomain out of range");
+    const SubPlan& S = c.su.subs[s];
+    const int sl = S.op_slot, n = c.op_ns[sl], ld = c.op_ld[sl];
+    *ns = n;
+    if (n > cap) return;
+    for (int a = 0; a < n; ++a) dofs[a] = c.su.perim_dof[S.Top[a]];
+    std::vector<double> tmp((size_t)n * ld);
+    CK(cudaMemcpyAsync(tmp.data(), c.d_opmat.p + c.op_moff[sl], tmp.size() * 8, cudaMemcpyDeviceToHost, c.st));
+    CK(cudaStreamSynchronize(c.st));
+    for (int a = 0; a < n; ++a)
+      for (int b = 0; b < n; ++b) F[(size_t)a * n + b] = tmp[(size_t)a * ld + b];
+  });
+}
+
+int fetigpu_device_alloc(fetigpu_ctx*, size_t bytes, void** ptr) {
+  return guarded([&] { CK(cudaMalloc(ptr, bytes)); });
+}
+int fetigpu_device_free(fetigpu_ctx*, void* ptr) {
+  return guarded([&] { CK(cudaFree(ptr)); });
+}
+int fetigpu_host_alloc(size_t bytes, void** ptr) {
+  return guarded([&] { CK(cudaMallocHost(ptr, bytes)); });
+}
+int fetigpu_host_free(void* ptr) {
+  return guarded([&] { CK(cudaFreeHost(ptr)); });
+}
+int fetigpu_memcpy(fetigpu_ctx* ctx, void* dst, const void* src, size_t bytes, int kind) {
+  return guarded([&] {
+    CK(cudaMemcpyAsync(dst, src, bytes, (cudaMemcpyKind)kind, ctx->c.st));
+  });
+}
+int fetigpu_fill_random(fetigpu_ctx* ctx, double* p, size_t count, unsigned long long seed) {
+  return guarded([&] {
+    k_fill_random<<<grid_for((long long)count), kThreads, 0, ctx->c.st>>>(p, count, seed);
+    LAUNCH_CHECK();
+  });
+}
+int fetigpu_synchronize(fetigpu_ctx* ctx) {
+  return guarded([&] { CK(cudaStreamSynchronize(ctx->c.st)); });
+}
+
+int fetigpu_time_apply(fetigpu_ctx* ctx, const double* x, double* y, int ncols, int reps, int flush_l2,
+                       double* ms, int* launches) {
+  return guarded([&] {
+    NEED_BUILT(ctx);
+    Ctx& c = ctx->c;
+    DBuf<double> fl;
+    const size_t fl_n = (size_t)(256u << 20) / 8;  // 256 MB > 126 MB L2
+    if (flush_l2) fl.alloc(fl_n);
+    std::vector<cudaEvent_t> ev(2 * reps + 2);
+    for (auto& e : ev) CK(cudaEventCreate(&e));
+    // dominant kernel alone, same launch configuration as inside apply_F
+    double tot = 0, tot_main = 0;
+    for (int r = 0; r < reps; ++r) {
+      if (flush_l2) k_flush<<<grid_for((long long)fl_n), kThreads, 0, c.st>>>(fl.p, fl_n, (double)r);
+      CK(cudaEventRecord(ev[2 * r], c.st));
+      c.apply_F(x, y, ncols, c.su.m, c.su.m);
+      CK(cudaEventRecord(ev[2 * r + 1], c.st));
+    }
+    CK(cudaStreamSynchronize(c.st));
+    for (int r = 0; r < reps; ++r) {
+      float t = 0;
+      CK(cudaEventElapsedTime(&t, ev[2 * r], ev[2 * r + 1]));
+      tot += t;
+    }
+    for (int r = 0; r < reps; ++r) {
+      if (flush_l2) k_flush<<<grid_for((long long)fl_n), kThreads, 0, c.st>>>(fl.p, fl_n, (double)r);
+      CK(cudaEventRecord(ev[2 * r], c.st));
+      for (int col = 0; col < ncols; ++col) {
+        if (c.su.method == FETIGPU_TFETI)
+          k_gather_gemv_scatter<3, false><<<dim3(c.su.Ns, 1), kThreads, c.max_ld * 8, c.st>>>(
+              c.d_op.p, c.d_opmat.p, c.d_oprows.p, c.d_opcoef.p, x + (size_t)col * c.su.m,
+              y + (size_t)col * c.su.m, nullptr, 0, nullptr, nullptr, c.su.m, c.su.m);
+        else
+          k_gather_gemv_scatter<1, true><<<c.su.Ns, kThreads, c.max_ld * 8, c.st>>>(
+              c.d_op.p, c.d_opmat.p, c.d_oprows.p, c.d_opcoef.p, x + (size_t)col * c.su.m, nullptr, nullptr, 0,
+              c.d_vbuf.p, c.d_voff.p, c.su.m, 0);
+      }
+      CK(cudaEventRecord(ev[2 * r + 1], c.st));
+    }
+    CK(cudaStreamSynchronize(c.st));
+    for (int r = 0; r < reps; ++r) {
+      float t = 0;
+      CK(cudaEventElapsedTime(&t, ev[2 * r], ev[2 * r + 1]));
+      tot_main += t;
+    }
+    for (auto& e : ev) cudaEventDestroy(e);
+    ms[0] = tot / reps;
+    ms[1] = tot_main / reps;
+    ms[2] = ms[1] / ms[0];
+    if (launches) *launches = (c.su.method == FETIGPU_TFETI ? 1 : 5) * ncols;
+  });
+}
+
+}  // extern "C"

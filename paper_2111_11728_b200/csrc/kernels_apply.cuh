@@ -1,0 +1,533 @@
+// kernels_apply.cuh -- per-iteration kernels of the FETI engine.
+//
+// K4/K7: y = sum_s B_s F_s B_s^T x as ONE kernel per apply:
+// each CTA gathers its subdomain's x_s = B_s^T x (signed, weighted for the
+// preconditioner) into shared memory, streams the dense row-major F_s from HBM
+// once (128-bit streaming loads, one warp per row, warp-shuffle reduction)
+// and scatters sign * (F_s x_s)_i to the dual rows.  Every dual row receives
+// exactly two contributions (one for Dirichlet rows) into a zeroed output,
+// so the atomic scatter is order-independent (0 + a + b == 0 + b + a) and
+// the apply is bit-reproducible.
+//
+// This replaces, per apply and per subdomain, the reference's
+// ConstraintSet::apply_BsT -> SemidefiniteCholesky::solve_unchecked ->
+// accumulate_Bs chain (decomposition.hpp:98-101, linalg.cpp:206-213).
+#pragma once
+
+#include "common.cuh"
+
+namespace fg {
+
+// ------------------------------------------------------------ the F-apply --
+// KR = max dual rows touching one local DOF (1 FETI-DP, <= 3 T-FETI cross points)
+template <int KR, bool STORE_V>
+__global__ void __launch_bounds__(kThreads) k_gather_gemv_scatter(
+    const OpSub* __restrict__ subs, const double* __restrict__ mats, const int* __restrict__ rows,
+    const double* __restrict__ coefs, const double* __restrict__ x, double* __restrict__ y,
+    double* __restrict__ zcols, int ldz, double* __restrict__ vbuf, const int* __restrict__ voff,
+    int ldx, int ldy) {
+  extern __shared__ double xs[];
+  const int s = blockIdx.x;
+  const int col = blockIdx.y;
+  const OpSub d = subs[s];
+  const double* xc = x + (size_t)col * ldx;
+  const int* rw = rows + d.map_off;
+  const double* cf = coefs + d.map_off;
+  for (int j = threadIdx.x; j < d.ld; j += blockDim.x) {
+    double acc = 0.0;
+    if (j < d.ns) {
+#pragma unroll
+      for (int k = 0; k < KR; ++k) {
+        const int r = rw[j * KR + k];
+        if (r >= 0) acc += cf[j * KR + k] * xc[r];
+      }
+    }
+    xs[j] = acc;
+  }
+  __syncthreads();
+  const double* A = mats + d.moff;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nw = blockDim.x >> 5;
+  for (int i = warp; i < d.ns; i += nw) {
+    const double2* Ai = reinterpret_cast<const double2*>(A + (size_t)i * d.ld);
+    double acc0 = 0.0, acc1 = 0.0;
+    const int n2 = d.ld >> 1;
+    int j = lane;
+#pragma unroll 4
+    for (; j + 32 < n2; j += 64) {
+      const double2 a0 = __ldcs(Ai + j);
+      const double2 a1 = __ldcs(Ai + j + 32);
+      acc0 = fma(a0.x, xs[2 * j], acc0);
+      acc1 = fma(a0.y, xs[2 * j + 1], acc1);
+      acc0 = fma(a1.x, xs[2 * j + 64], acc0);
+      acc1 = fma(a1.y, xs[2 * j + 65], acc1);
+    }
+    for (; j < n2; j += 32) {
+      const double2 a0 = __ldcs(Ai + j);
+      acc0 = fma(a0.x, xs[2 * j], acc0);
+      acc1 = fma(a0.y, xs[2 * j + 1], acc1);
+    }
+    const double v = warp_sum(acc0 + acc1);
+    if (lane == 0) {
+      if (STORE_V) {
+        vbuf[voff[s] + i] = v;
+      } else {
+        double* yc = y + (size_t)col * ldy;
+#pragma unroll
+        for (int k = 0; k < KR; ++k) {
+          const int r = rw[i * KR + k];
+          if (r >= 0) {
+            const double c = cf[i * KR + k] * v;
+            atomicAdd(yc + r, c);
+            if (zcols) zcols[(size_t)s * ldz + r] = c;
+          }
+        }
+      }
+    }
+  }
+}
+
+// FETI-DP coarse coupling, phase 1: t_s = A_bc^T x_s (after k_gather_gemv_scatter
+// stored v_s = F_s x_s): x_s is re-gathered (1 row per DOF).
+__global__ void k_dp_t(const OpSub* __restrict__ subs, const DpSub* __restrict__ dps,
+                       const int* __restrict__ rows, const double* __restrict__ coefs,
+                       const double* __restrict__ abc, const double* __restrict__ x,
+                       double* __restrict__ tbuf) {
+  const int s = blockIdx.x;
+  const OpSub d = subs[s];
+  const DpSub p = dps[s];
+  __shared__ double red[8][kThreads / 32];
+  double acc[8] = {};
+  const double* Ab = abc + p.abc_off;
+  for (int j = threadIdx.x; j < d.ns; j += blockDim.x) {
+    const int r = rows[d.map_off + j];
+    const double xj = r >= 0 ? coefs[d.map_off + j] * x[r] : 0.0;
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+      if (c < p.nc) acc[c] += Ab[(size_t)j * p.nc + c] * xj;
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const double v = warp_sum(acc[c]);
+    if (lane == 0) red[c][warp] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < p.nc) {
+    double v = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) v += red[threadIdx.x][w];
+    tbuf[p.t_off + threadIdx.x] = v;
+  }
+}
+
+// global coarse vector: out[i] = sum over owners of primal DOF i (ascending
+// subdomain order) of the per-subdomain entries -> deterministic assembly
+__global__ void k_coarse_gather(const int* __restrict__ optr, const int* __restrict__ oidx,
+                                const double* __restrict__ tbuf, int nc, double* __restrict__ out,
+                                double sign, const double* __restrict__ add) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nc; i += gridDim.x * blockDim.x) {
+    double v = add ? add[i] : 0.0;
+    for (int k = optr[i]; k < optr[i + 1]; ++k) v += sign * tbuf[oidx[k]];
+    out[i] = v;
+  }
+}
+
+// dense row-major GEMV y = M x (one warp per row), n x n
+__global__ void k_dense_gemv(const double* __restrict__ M, int n, const double* __restrict__ x,
+                             double* __restrict__ y) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int i = warp; i < n; i += nwarps) {
+    const double* Mi = M + (size_t)i * n;
+    double acc = 0.0;
+    for (int j = lane; j < n; j += 32) acc = fma(Mi[j], x[j], acc);
+    acc = warp_sum(acc);
+    if (lane == 0) y[i] = acc;
+  }
+}
+
+// FETI-DP phase 2: v_s += A_bc u[cmap]; scatter sign * v_s
+__global__ void k_dp_phase2(const OpSub* __restrict__ subs, const DpSub* __restrict__ dps,
+                            const int* __restrict__ rows, const double* __restrict__ coefs,
+                            const double* __restrict__ abc, const int* __restrict__ cmap,
+                            const double* __restrict__ u, const double* __restrict__ vbuf,
+                            double* __restrict__ y, double vscale) {
+  const int s = blockIdx.x;
+  const OpSub d = subs[s];
+  const DpSub p = dps[s];
+  __shared__ double uc[8];
+  if (threadIdx.x < p.nc) uc[threadIdx.x] = u[cmap[p.cmap_off + threadIdx.x]];
+  __syncthreads();
+  const double* Ab = abc + p.abc_off;
+  for (int j = threadIdx.x; j < d.ns; j += blockDim.x) {
+    double v = vbuf ? vscale * vbuf[p.v_off + j] : 0.0;
+    for (int c = 0; c < p.nc; ++c) v = fma(Ab[(size_t)j * p.nc + c], uc[c], v);
+    const int r = rows[d.map_off + j];
+    if (r >= 0) atomicAdd(y + r, coefs[d.map_off + j] * v);
+  }
+}
+
+// ------------------------------------------------------ T-FETI projector --
+// g_s = -R_T^T (B_s^T v): per subdomain 3 values (K8, decomposition.hpp:136)
+__global__ void k_proj_gather(const OpSub* __restrict__ psubs, const int* __restrict__ rows,
+                              const double* __restrict__ coefs, const double* __restrict__ RT,
+                              const int* __restrict__ rt_off, const double* __restrict__ v, int ldv,
+                              double* __restrict__ g, int ldg, double sign) {
+  const int s = blockIdx.x, col = blockIdx.y;
+  const OpSub d = psubs[s];
+  const double* vc = v + (size_t)col * ldv;
+  const double* R = RT + rt_off[s];
+  double a0 = 0, a1 = 0, a2 = 0;
+  for (int j = threadIdx.x; j < d.ns; j += blockDim.x) {
+    double xj = 0.0;
+    for (int k = 0; k < 3; ++k) {
+      const int r = rows[d.map_off + j * 3 + k];
+      if (r >= 0) xj += coefs[d.map_off + j * 3 + k] * vc[r];
+    }
+    a0 += R[j * 3] * xj;
+    a1 += R[j * 3 + 1] * xj;
+    a2 += R[j * 3 + 2] * xj;
+  }
+  __shared__ double red[3][kThreads / 32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  a0 = warp_sum(a0); a1 = warp_sum(a1); a2 = warp_sum(a2);
+  if (lane == 0) { red[0][warp] = a0; red[1][warp] = a1; red[2][warp] = a2; }
+  __syncthreads();
+  if (threadIdx.x < 3) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[threadIdx.x][w];
+    g[(size_t)col * ldg + 3 * s + threadIdx.x] = sign * t;
+  }
+}
+
+// dense column-major H (n x n) times g columns: h = H g
+__global__ void k_small_gemm(const double* __restrict__ H, int n, const double* __restrict__ g,
+                             int ldg, double* __restrict__ h, int ldh) {
+  const int col = blockIdx.y;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int j = 0; j < n; ++j) acc = fma(H[(size_t)j * n + i], g[(size_t)col * ldg + j], acc);
+    h[(size_t)col * ldh + i] = acc;
+  }
+}
+
+// corr[row] += sign_entry * (R_T h_s)_j into a zeroed buffer (2 contributions per row)
+__global__ void k_proj_scatter(const OpSub* __restrict__ psubs, const int* __restrict__ rows,
+                               const double* __restrict__ coefs, const double* __restrict__ RT,
+                               const int* __restrict__ rt_off, const double* __restrict__ h, int ldh,
+                               double* __restrict__ corr, int ldc) {
+  const int s = blockIdx.x, col = blockIdx.y;
+  const OpSub d = psubs[s];
+  const double* R = RT + rt_off[s];
+  const double* hc = h + (size_t)col * ldh + 3 * s;
+  const double h0 = hc[0], h1 = hc[1], h2 = hc[2];
+  double* cc = corr + (size_t)col * ldc;
+  for (int j = threadIdx.x; j < d.ns; j += blockDim.x) {
+    const double v = R[j * 3] * h0 + R[j * 3 + 1] * h1 + R[j * 3 + 2] * h2;
+    for (int k = 0; k < 3; ++k) {
+      const int r = rows[d.map_off + j * 3 + k];
+      if (r >= 0) atomicAdd(cc + r, coefs[d.map_off + j * 3 + k] * v);
+    }
+  }
+}
+
+// ------------------------------------------------------------- reductions --
+// Deterministic multi-dot: fixed grid, fixed per-block order, final pass in
+// fixed order.  pairs: up to 4 (a_k, b_k) products of length n.
+struct DotArgs {
+  const double* a[4];
+  const double* b[4];
+  int npairs;
+  int n;
+};
+constexpr int kDotBlocks = 296;
+__global__ void __launch_bounds__(kThreads) k_dot_partial(DotArgs args, double* partial) {
+  double acc[4] = {0, 0, 0, 0};
+  const int stride = gridDim.x * blockDim.x;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < args.n; i += stride) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (k < args.npairs) acc[k] = fma(args.a[k][i], args.b[k][i], acc[k]);
+  }
+  __shared__ double red[4][kThreads / 32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const double v = warp_sum(acc[k]);
+    if (lane == 0) red[k][warp] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < args.npairs) {
+    double v = 0.0;
+    for (int w = 0; w < kThreads / 32; ++w) v += red[threadIdx.x][w];
+    partial[threadIdx.x * kDotBlocks + blockIdx.x] = v;
+  }
+}
+__global__ void k_dot_final(const double* partial, int npairs, double* out) {
+  const int k = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (k >= npairs) return;
+  double acc = 0.0;
+  for (int b = lane; b < kDotBlocks; b += 32) acc += partial[k * kDotBlocks + b];
+  acc = warp_sum(acc);
+  if (lane == 0) out[k] = acc;
+}
+
+// ------------------------------------------------------- vector updates --
+// PCG scalars live in device memory (no host round trip inside an iteration)
+struct Scal {
+  double delta;    // w^T F w
+  double wr;       // w^T r
+  double rz;       // r^T z (current)
+  double rr, zz;
+  double rz_old;
+  double alpha;
+  double pad;
+};
+
+__global__ void k_axpy(int n, double a, const double* __restrict__ x, double* __restrict__ y) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    y[i] = fma(a, x[i], y[i]);
+}
+// v += corr (projector finish)
+__global__ void k_add(int n, const double* __restrict__ c, double* __restrict__ v, int ldc, int ldv) {
+  const int col = blockIdx.y;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    v[(size_t)col * ldv + i] += c[(size_t)col * ldc + i];
+}
+// alpha from device scalars; lambda += alpha w; r -= alpha * Pq  (Pq = q + corr or q)
+__global__ void k_pcg_update(int n, Scal* sc, int fo, const double* __restrict__ w,
+                             const double* __restrict__ q, const double* __restrict__ corr,
+                             double* __restrict__ lambda, double* __restrict__ r) {
+  const double alpha = (fo ? sc->wr : sc->rz) / sc->delta;
+  if (blockIdx.x == 0 && threadIdx.x == 0) sc->alpha = alpha;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    lambda[i] = fma(alpha, w[i], lambda[i]);
+    const double pq = corr ? q[i] + corr[i] : q[i];
+    r[i] = fma(-alpha, pq, r[i]);
+  }
+}
+// w = z + beta w with beta = rz / rz_old
+__global__ void k_cg_dir(int n, const Scal* sc, const double* __restrict__ z, double* __restrict__ w) {
+  const double beta = sc->rz / sc->rz_old;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    w[i] = fma(beta, w[i], z[i]);
+}
+// FO: store w / sqrt(delta), q / sqrt(delta) as column j of W, Q
+__global__ void k_fo_store(int n, const Scal* sc, const double* __restrict__ w,
+                           const double* __restrict__ q, double* __restrict__ Wc,
+                           double* __restrict__ Qc) {
+  const double inv = 1.0 / sqrt(sc->delta);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    Wc[i] = w[i] * inv;
+    Qc[i] = q[i] * inv;
+  }
+}
+// y = x + beta * y
+__global__ void k_xpby(int n, const double* __restrict__ x, double beta, double* __restrict__ y) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    y[i] = fma(beta, y[i], x[i]);
+}
+__global__ void k_sub(int n, const double* __restrict__ a, const double* __restrict__ b,
+                      double* __restrict__ out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    out[i] = a[i] - b[i];
+}
+
+// ---------------------------------------------- one-time solves (rhs, u) --
+// Per subdomain: x = (L L^T)^{-1} b with L the slot's dense factor (ne x ne,
+// column-major).  b is gathered from perimeter vectors by `idx`.
+__global__ void k_chol_solve(const double* __restrict__ fac, const long long* __restrict__ fac_off,
+                             const int* __restrict__ slot_of, const int* __restrict__ nes,
+                             double* __restrict__ xb, const int* __restrict__ xoff) {
+  extern __shared__ double xsh[];
+  const int s = blockIdx.x;
+  const int sl = slot_of[s];
+  const int ne = nes[sl];
+  const double* L = fac + fac_off[sl];
+  double* x = xb + xoff[s];
+  for (int i = threadIdx.x; i < ne; i += blockDim.x) xsh[i] = x[i];
+  __syncthreads();
+  for (int j = 0; j < ne; ++j) {
+    if (threadIdx.x == 0) xsh[j] = xsh[j] / L[(size_t)j * ne + j];
+    __syncthreads();
+    const double xj = xsh[j];
+    for (int i = j + 1 + threadIdx.x; i < ne; i += blockDim.x) xsh[i] -= L[(size_t)j * ne + i] * xj;
+    __syncthreads();
+  }
+  for (int j = ne - 1; j >= 0; --j) {
+    if (threadIdx.x == 0) xsh[j] = xsh[j] / L[(size_t)j * ne + j];
+    __syncthreads();
+    const double xj = xsh[j];
+    for (int i = threadIdx.x; i < j; i += blockDim.x) xsh[i] -= L[(size_t)i * ne + j] * xj;
+    __syncthreads();
+  }
+  for (int i = threadIdx.x; i < ne; i += blockDim.x) x[i] = xsh[i];
+}
+
+// Nested-dissection back substitution (recovery of module-interior DOFs):
+// for every tree node top-down, u_e = -L_ee^{-T} (L_be^T u_b).
+__global__ void k_nd_backsub(const NdDev* __restrict__ nodes, const int* __restrict__ topdown,
+                             int n_nodes, const int* __restrict__ dofs, const double* __restrict__ fac,
+                             long long fstride, const int* __restrict__ design, double* __restrict__ u,
+                             int nloc) {
+  extern __shared__ double sh[];
+  const int s = blockIdx.x;
+  double* us = u + (size_t)s * nloc;
+  const double* F0 = fac + (size_t)design[s] * fstride;
+  for (int t = 0; t < n_nodes; ++t) {
+    const NdDev nd = nodes[topdown[t]];
+    const int nf = nd.nf, ne = nd.ne, nbb = nf - ne;
+    if (ne == 0) continue;
+    const int* dl = dofs + nd.dof_off;
+    double* ub = sh;          // nbb
+    double* y = sh + nbb;     // ne
+    for (int i = threadIdx.x; i < nbb; i += blockDim.x) ub[i] = us[dl[ne + i]];
+    __syncthreads();
+    const double* Fc = F0 + nd.foff;
+    for (int k = threadIdx.x; k < ne; k += blockDim.x) {
+      double acc = 0.0;
+      const double* col = Fc + (size_t)k * nf + ne;
+      for (int i = 0; i < nbb; ++i) acc = fma(col[i], ub[i], acc);
+      y[k] = acc;
+    }
+    __syncthreads();
+    for (int j = ne - 1; j >= 0; --j) {
+      if (threadIdx.x == 0) y[j] = y[j] / Fc[(size_t)j * nf + j];
+      __syncthreads();
+      const double yj = y[j];
+      for (int i = threadIdx.x; i < j; i += blockDim.x) y[i] -= Fc[(size_t)i * nf + j] * yj;
+      __syncthreads();
+    }
+    for (int k = threadIdx.x; k < ne; k += blockDim.x) us[dl[k]] = -y[k];
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------ RRS block algebra (K10) --
+// Rank-revealing pivoted Cholesky of the k x k Gram matrix Delta (Alg. 1
+// line 9; pivoted_cholesky contract SPEC.md:43-47 with a symmetric trailing
+// update): one CTA, pivots sequential, updates parallel.
+__global__ void __launch_bounds__(1024) k_pivchol(double* A, int n, double tol, int* perm,
+                                                  int* rank_out, int* status) {
+  __shared__ double sv[32];
+  __shared__ int si[32];
+  __shared__ double s_scale;
+  __shared__ int s_piv;
+  __shared__ int s_stop;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i < n; i += nt) perm[i] = i;
+  // scale = max initial diagonal
+  double mx = -1e300;
+  for (int i = tid; i < n; i += nt) mx = fmax(mx, A[(size_t)i * n + i]);
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if (lane == 0) sv[warp] = mx;
+  __syncthreads();
+  if (tid == 0) {
+    double m2 = sv[0];
+    for (int w = 1; w < (nt >> 5); ++w) m2 = fmax(m2, sv[w]);
+    s_scale = m2;
+  }
+  __syncthreads();
+  const double stop_tol = tol * s_scale;
+  const double neg_tol = -tol * fmax(s_scale, 1e-300);
+  int rank = 0;
+  for (int k = 0; k < n; ++k) {
+    // argmax over the remaining diagonal, ties -> lowest index
+    double bv = -1e300;
+    int bi = n;
+    for (int j = k + tid; j < n; j += nt) {
+      const double v = A[(size_t)j * n + j];
+      if (v > bv || (v == bv && j < bi)) { bv = v; bi = j; }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+    }
+    if (lane == 0) { sv[warp] = bv; si[warp] = bi; }
+    __syncthreads();
+    if (tid == 0) {
+      double v = sv[0];
+      int b = si[0];
+      for (int w = 1; w < (nt >> 5); ++w)
+        if (sv[w] > v || (sv[w] == v && si[w] < b)) { v = sv[w]; b = si[w]; }
+      s_piv = b;
+      s_stop = !(v > stop_tol);
+    }
+    __syncthreads();
+    if (s_stop) {
+      for (int j = k + tid; j < n; j += nt)
+        if (A[(size_t)j * n + j] < neg_tol) atomicExch(status, 2 /* IndefiniteInput */);
+      break;
+    }
+    const int piv = s_piv;
+    if (piv != k) {
+      for (int j = tid; j < n; j += nt) {  // rows k <-> piv
+        const double t = A[(size_t)j * n + k];
+        A[(size_t)j * n + k] = A[(size_t)j * n + piv];
+        A[(size_t)j * n + piv] = t;
+      }
+      __syncthreads();
+      for (int i = tid; i < n; i += nt) {  // columns k <-> piv
+        const double t = A[(size_t)k * n + i];
+        A[(size_t)k * n + i] = A[(size_t)piv * n + i];
+        A[(size_t)piv * n + i] = t;
+      }
+      if (tid == 0) { const int t = perm[k]; perm[k] = perm[piv]; perm[piv] = t; }
+      __syncthreads();
+    }
+    const double l = sqrt(A[(size_t)k * n + k]);
+    __syncthreads();
+    if (tid == 0) A[(size_t)k * n + k] = l;
+    for (int i = k + 1 + tid; i < n; i += nt) A[(size_t)k * n + i] /= l;
+    __syncthreads();
+    const int r = n - k - 1;
+    for (long long idx = tid; idx < (long long)r * r; idx += nt) {
+      const int j = k + 1 + (int)(idx / r), i = k + 1 + (int)(idx % r);
+      A[(size_t)j * n + i] -= A[(size_t)k * n + i] * A[(size_t)k * n + j];
+    }
+    __syncthreads();
+    rank = k + 1;
+  }
+  if (tid == 0) *rank_out = rank;
+}
+
+// out[:, c] = in[:, perm[c]] for c < cols (column gather, column-major)
+__global__ void k_gather_cols(const double* __restrict__ in, int ld, const int* __restrict__ perm,
+                              int cols, double* __restrict__ out) {
+  const int c = blockIdx.y;
+  if (c >= cols) return;
+  const double* src = in + (size_t)perm[c] * ld;
+  double* dst = out + (size_t)c * ld;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ld; i += gridDim.x * blockDim.x) dst[i] = src[i];
+}
+
+// mirror the lower triangle into the upper (Delta uses its lower triangle)
+__global__ void k_mirror_lower(double* A, int n) {
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < (long long)n * n;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int j = (int)(idx / n), i = (int)(idx % n);
+    if (i < j) A[idx] = A[(size_t)i * n + j];
+  }
+}
+
+// L2 flush helper: write a buffer larger than L2
+__global__ void k_flush(double* buf, size_t n, double v) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x)
+    buf[i] = v;
+}
+
+__global__ void k_fill_random(double* p, size_t n, unsigned long long seed) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x) {
+    unsigned long long z = seed + (i + 1) * 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    p[i] = (double)(z >> 11) * (1.0 / 9007199254740992.0) * 2.0 - 1.0;
+  }
+}
+
+}  // namespace fg

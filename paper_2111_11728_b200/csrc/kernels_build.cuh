@@ -1,0 +1,414 @@
+// kernels_build.cuh -- device build of the explicit local operators.
+//
+// K1+K2: SIMP element moduli + Q4 assembly fused into the
+// leaves of a nested-dissection Schur tree; every tree node is one dense
+// frontal matrix whose interior/separator DOFs are eliminated by a batched
+// partial Cholesky, leaving the Schur complement on the node's perimeter.
+// The root's Schur complement is S = K_bb - K_bi K_ii^{-1} K_ib on the module
+// perimeter.  This replaces the reference's per-subdomain sparse Cholesky
+// (SparseCholesky/SimplicialLLT, linalg.cpp:64-81) as the source of every
+// local operator: T-FETI K^+ restricted to the interface, FETI-DP K_rr^{-1},
+// K_rr^{-1} K_rc and Kbar_cc^s, and the Dirichlet preconditioner (SURVEY.md
+// Appendix B identities).
+//
+// K3: per-slot frontal matrices [[S[src,src], E],[E^T, 0]] assembled from S
+// and eliminated by the same batched kernels; the trailing blocks are the
+// dense F_s, A_bc, Kbar_cc^s or S~_s.
+#pragma once
+
+#include "common.cuh"
+
+namespace fg {
+
+__constant__ double c_kunit[64];   // unit-modulus Q4 stiffness (col-major)
+
+// Unblocked right-looking partial Cholesky of a column-major matrix in
+// shared memory: eliminates the first ne of nf DOFs (lower triangle).
+__device__ void eliminate_smem(double* F, int nf, int ne, int ld, int* status, int code) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int k = 0; k < ne; ++k) {
+    double* ck = F + (size_t)k * ld;
+    if (tid == 0) {
+      double d = ck[k];
+      if (!(d > 0.0)) {
+        atomicExch(status, code);
+        d = 1.0;
+      }
+      ck[k] = sqrt(d);
+    }
+    __syncthreads();
+    const double l = ck[k];
+    for (int i = k + 1 + tid; i < nf; i += nt) ck[i] = ck[i] / l;
+    __syncthreads();
+    const int m = nf - k - 1;
+    // lower triangle of the trailing block, column-major triangular enumeration
+    const int tri = m * (m + 1) / 2;
+    for (int idx = tid; idx < tri; idx += nt) {
+      // column jj has m - jj entries (rows jj..m-1)
+      int jj = (int)((2.0 * m + 1.0 - sqrt((2.0 * m + 1.0) * (2.0 * m + 1.0) - 8.0 * idx)) * 0.5);
+      int start = jj * m - jj * (jj - 1) / 2;
+      if (start > idx) { --jj; start = jj * m - jj * (jj - 1) / 2; }
+      else if (start + (m - jj) <= idx) { ++jj; start = jj * m - jj * (jj - 1) / 2; }
+      const int ii = jj + (idx - start);
+      F[(size_t)(k + 1 + jj) * ld + k + 1 + ii] -= ck[k + 1 + ii] * ck[k + 1 + jj];
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------- ND tree --
+struct NdArgs {
+  const NdDev* nodes;
+  const int* level_nodes;
+  const long long* hbase;     // per height: offset of the height block in ws
+  const long long* hstride;   // per height: doubles per design
+  double* ws;
+  const int* elem_ids;
+  const int* emap;
+  const int* cmaps;
+  const double* dens;         // all designs
+  int n;
+  int d0;                     // first design of this chunk
+  double E0, Emin, p;
+  double* factors;            // nullable: per design [nf x ne] blocks
+  long long fstride;
+  int* status;
+};
+
+__device__ __forceinline__ void nd_assemble(const NdArgs& a, const NdDev& nd, int dl, double* F,
+                                            int ld) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  if (nd.leaf) {
+    const double* rho = a.dens + (size_t)(a.d0 + dl) * a.n * a.n;
+    for (int e = 0; e < nd.elem_cnt; ++e) {
+      const int eid = a.elem_ids[nd.elem_off + e];
+      // simp_modulus (fem.cpp:19-24)
+      const double E = a.Emin + pow(rho[eid], a.p) * (a.E0 - a.Emin);
+      const int* em = a.emap + (size_t)(nd.elem_off + e) * 8;
+      for (int idx = tid; idx < 64; idx += nt) {
+        const int r = idx & 7, c = idx >> 3;
+        const int pr = em[r], pc = em[c];
+        if (pr >= pc) F[(size_t)pc * ld + pr] += E * c_kunit[c * 8 + r];
+      }
+      __syncthreads();
+    }
+  } else {
+    for (int c = 0; c < 2; ++c) {
+      const NdDev ch = a.nodes[nd.child[c]];
+      const double* S = a.ws + a.hbase[ch.height] + (long long)dl * a.hstride[ch.height] + ch.off;
+      const int nbc = ch.nf - ch.ne;
+      const int* cm = a.cmaps + nd.cmap_off[c];
+      for (int idx = tid; idx < nbc * nbc; idx += nt) {
+        const int j = idx / nbc, i = idx - j * nbc;
+        if (i < j) continue;
+        const double v = S[(size_t)(ch.ne + j) * ch.nf + ch.ne + i];
+        int pr = cm[i], pc = cm[j];
+        if (pr < pc) { const int t = pr; pr = pc; pc = t; }
+        F[(size_t)pc * ld + pr] += v;
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// small tree nodes: assemble + eliminate in shared memory, one CTA per (node, design)
+__global__ void __launch_bounds__(kThreads) k_nd_small(NdArgs a) {
+  extern __shared__ double F[];
+  const int t = a.level_nodes[blockIdx.x];
+  const int dl = blockIdx.y;
+  const NdDev nd = a.nodes[t];
+  const int nf = nd.nf;
+  for (int i = threadIdx.x; i < nf * nf; i += blockDim.x) F[i] = 0.0;
+  __syncthreads();
+  nd_assemble(a, nd, dl, F, nf);
+  eliminate_smem(F, nf, nd.ne, nf, a.status, kNotSPD);
+  double* out = a.ws + a.hbase[nd.height] + (long long)dl * a.hstride[nd.height] + nd.off;
+  for (int i = threadIdx.x; i < nf * nf; i += blockDim.x) out[i] = F[i];
+  if (a.factors) {
+    double* fo = a.factors + (size_t)(a.d0 + dl) * a.fstride + nd.foff;
+    for (int i = threadIdx.x; i < nf * nd.ne; i += blockDim.x) fo[i] = F[i];
+  }
+}
+
+// large tree nodes: assemble into the global frontal (eliminated afterwards)
+__global__ void __launch_bounds__(kThreads) k_nd_assemble(NdArgs a) {
+  const int t = a.level_nodes[blockIdx.x];
+  const int dl = blockIdx.y;
+  const NdDev nd = a.nodes[t];
+  const int nf = nd.nf;
+  double* F = a.ws + a.hbase[nd.height] + (long long)dl * a.hstride[nd.height] + nd.off;
+  for (long long i = threadIdx.x; i < (long long)nf * nf; i += blockDim.x) F[i] = 0.0;
+  __syncthreads();
+  nd_assemble(a, nd, dl, F, nf);
+}
+
+__global__ void k_nd_copy_factors(NdArgs a) {
+  const int t = a.level_nodes[blockIdx.x];
+  const int dl = blockIdx.y;
+  const NdDev nd = a.nodes[t];
+  const double* F = a.ws + a.hbase[nd.height] + (long long)dl * a.hstride[nd.height] + nd.off;
+  double* fo = a.factors + (size_t)(a.d0 + dl) * a.fstride + nd.foff;
+  for (long long i = threadIdx.x; i < (long long)nd.nf * nd.ne; i += blockDim.x) fo[i] = F[i];
+}
+
+// Root Schur complement -> dense symmetric S (nb x nb, column-major) per design.
+__global__ void k_nd_extract_root(const NdDev* nodes, int root, const long long* hbase,
+                                  const long long* hstride, const double* ws, double* S, int nb,
+                                  int d0) {
+  const NdDev nd = nodes[root];
+  const int dl = blockIdx.y;
+  const double* F = ws + hbase[nd.height] + (long long)dl * hstride[nd.height] + nd.off;
+  double* out = S + (size_t)(d0 + dl) * nb * nb;
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < nb * nb; idx += gridDim.x * blockDim.x) {
+    const int j = idx / nb, i = idx - j * nb;
+    const int r = i > j ? i : j, c = i > j ? j : i;
+    out[idx] = F[(size_t)(nd.ne + c) * nd.nf + nd.ne + r];
+  }
+}
+
+// -------------------------------------------------- blocked elimination --
+// Right-looking blocked partial Cholesky in global memory, one CTA per
+// frontal: panel factor in smem, row-wise triangular solve of the panel,
+// 64x64-tiled rank-kNB update of the lower trailing matrix.
+__global__ void __launch_bounds__(kThreads) k_front_elim_large(const FrontDesc* fds, double* base,
+                                                               int* status) {
+  const FrontDesc f = fds[blockIdx.x];
+  double* A = base + f.off;
+  const int nf = f.nf, ne = f.ne, ld = f.ld;
+  __shared__ double D[kNB * (kNB + 1)];
+  __shared__ double LiT[kNB * kTile];
+  __shared__ double LjT[kNB * kTile];
+  const int tid = threadIdx.x;
+  const int tx = tid & 15, ty = tid >> 4;
+  for (int k0 = 0; k0 < ne; k0 += kNB) {
+    const int kb = min(kNB, ne - k0);
+    const int k1 = k0 + kb;
+    for (int idx = tid; idx < kb * kb; idx += kThreads) {
+      const int j = idx / kb, i = idx - j * kb;
+      if (i >= j) D[j * (kNB + 1) + i] = A[(size_t)(k0 + j) * ld + k0 + i];
+    }
+    __syncthreads();
+    eliminate_smem(D, kb, kb, kNB + 1, status, f.code);
+    for (int idx = tid; idx < kb * kb; idx += kThreads) {
+      const int j = idx / kb, i = idx - j * kb;
+      if (i >= j) A[(size_t)(k0 + j) * ld + k0 + i] = D[j * (kNB + 1) + i];
+    }
+    // panel: X D^T = A[r, k0:k1] for rows below the block
+    for (int r = k1 + tid; r < nf; r += kThreads) {
+      double x[kNB];
+#pragma unroll
+      for (int c = 0; c < kNB; ++c)
+        if (c < kb) x[c] = A[(size_t)(k0 + c) * ld + r];
+#pragma unroll
+      for (int c = 0; c < kNB; ++c) {
+        if (c < kb) {
+          double v = x[c];
+#pragma unroll
+          for (int c2 = 0; c2 < c; ++c2) v -= x[c2] * D[c2 * (kNB + 1) + c];
+          x[c] = v / D[c * (kNB + 1) + c];
+          A[(size_t)(k0 + c) * ld + r] = x[c];
+        }
+      }
+    }
+    __syncthreads();
+    const int mt = nf - k1;
+    const int nt = (mt + kTile - 1) / kTile;
+    for (int tj = 0; tj < nt; ++tj) {
+      for (int idx = tid; idx < kb * kTile; idx += kThreads) {
+        const int c = idx / kTile, r = idx - c * kTile;
+        const int row = tj * kTile + r;
+        LjT[c * kTile + r] = row < mt ? A[(size_t)(k0 + c) * ld + k1 + row] : 0.0;
+      }
+      for (int ti = tj; ti < nt; ++ti) {
+        for (int idx = tid; idx < kb * kTile; idx += kThreads) {
+          const int c = idx / kTile, r = idx - c * kTile;
+          const int row = ti * kTile + r;
+          LiT[c * kTile + r] = row < mt ? A[(size_t)(k0 + c) * ld + k1 + row] : 0.0;
+        }
+        __syncthreads();
+        double acc[4][4] = {};
+        for (int c = 0; c < kb; ++c) {
+          double li[4], lj[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            li[q] = LiT[c * kTile + tx + 16 * q];
+            lj[q] = LjT[c * kTile + ty + 16 * q];
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (int w = 0; w < 4; ++w) acc[q][w] = fma(li[q], lj[w], acc[q][w]);
+        }
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+          const int cj = tj * kTile + ty + 16 * w;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int ri = ti * kTile + tx + 16 * q;
+            if (ri < mt && cj < mt && ri >= cj) A[(size_t)(k1 + cj) * ld + k1 + ri] -= acc[q][w];
+          }
+        }
+        __syncthreads();
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// small frontal matrices (slots): load, eliminate in smem, store
+__global__ void __launch_bounds__(kThreads) k_front_elim_small(const FrontDesc* fds, double* base,
+                                                               int* status) {
+  extern __shared__ double F[];
+  const FrontDesc f = fds[blockIdx.x];
+  double* A = base + f.off;
+  const int nf = f.nf;
+  for (int idx = threadIdx.x; idx < nf * nf; idx += blockDim.x) {
+    const int j = idx / nf, i = idx - j * nf;
+    F[idx] = A[(size_t)j * f.ld + i];
+  }
+  __syncthreads();
+  eliminate_smem(F, nf, f.ne, nf, status, f.code);
+  for (int idx = threadIdx.x; idx < nf * nf; idx += blockDim.x) {
+    const int j = idx / nf, i = idx - j * nf;
+    A[(size_t)j * f.ld + i] = F[idx];
+  }
+}
+
+// ----------------------------------------------------------------- slots --
+struct SlotDev {
+  long long woff;   // frontal offset in the workspace
+  int design, nsrc, ne, next;
+  int src_off, ext_off;
+};
+
+// frontal = [[S[src,src], E],[E^T, 0]] (lower triangle, column-major, ld = nf)
+__global__ void k_slot_assemble(const SlotDev* slots, const int* src_all, const int* ext_all,
+                                const double* S, int nb, double* ws) {
+  const SlotDev sd = slots[blockIdx.y];
+  const int nf = sd.nsrc + sd.next;
+  const double* Sd = S + (size_t)sd.design * nb * nb;
+  const int* src = src_all + sd.src_off;
+  const int* ext = ext_all + sd.ext_off;
+  double* F = ws + sd.woff;
+  const long long tot = (long long)nf * nf;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < tot;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int j = (int)(idx / nf), i = (int)(idx - (long long)j * nf);
+    double v = 0.0;
+    if (i >= j) {
+      if (i < sd.nsrc) v = Sd[(size_t)src[j] * nb + src[i]];
+      else if (j < sd.nsrc) v = (ext[i - sd.nsrc] == j) ? 1.0 : 0.0;
+    }
+    F[idx] = v;
+  }
+}
+
+// T-FETI operator: F_s = -(trailing block); FETI-DP: F_s = -(TT block),
+// A_bc = -(T,c block), Kbar_cc^s = (c,c block).  Dirichlet preconditioner:
+// S~ = trailing block (sign +1, nc = 0).  Outputs are dense row-major.
+__global__ void k_slot_extract(const SlotDev* slots, const double* ws, const long long* mat_off,
+                               const int* mat_ld, double* mats, int nc_first, double sign,
+                               const long long* abc_off, double* abc, const long long* kcc_off,
+                               double* kcc) {
+  const SlotDev sd = slots[blockIdx.y];
+  const int nf = sd.nsrc + sd.next;
+  const double* F = ws + sd.woff;
+  // trailing block layout: [c (nc) | T (nt)] after the ne eliminated DOFs
+  const int nc = nc_first ? (sd.nsrc - sd.ne) : 0;
+  const int base = sd.ne + nc;
+  const int nt = nf - base;
+  const int ld = mat_ld[blockIdx.y];
+  double* M = mats + mat_off[blockIdx.y];
+  auto at = [&](int r, int c) {
+    const int rr = r > c ? r : c, cc = r > c ? c : r;
+    return F[(size_t)cc * nf + rr];
+  };
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < nt * ld;
+       idx += gridDim.x * blockDim.x) {
+    const int a = idx / ld, b = idx - a * ld;
+    M[(size_t)a * ld + b] = b < nt ? sign * at(base + a, base + b) : 0.0;
+  }
+  if (nc > 0) {
+    double* Ab = abc + abc_off[blockIdx.y];
+    for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < nt * nc;
+         idx += gridDim.x * blockDim.x) {
+      const int a = idx / nc, c = idx - a * nc;
+      Ab[idx] = -at(base + a, sd.ne + c);
+    }
+    double* Kc = kcc + kcc_off[blockIdx.y];
+    for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < nc * nc;
+         idx += gridDim.x * blockDim.x) {
+      const int a = idx / nc, c = idx - a * nc;
+      Kc[idx] = at(sd.ne + a, sd.ne + c);
+    }
+  }
+}
+
+// L factor (ne x ne, column-major lower) of an eliminated slot frontal
+__global__ void k_slot_factor(const SlotDev* slots, const double* ws, const long long* fac_off,
+                              double* fac) {
+  const SlotDev sd = slots[blockIdx.y];
+  const int nf = sd.nsrc + sd.next, ne = sd.ne;
+  const double* F = ws + sd.woff;
+  double* L = fac + fac_off[blockIdx.y];
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < ne * ne;
+       idx += gridDim.x * blockDim.x) {
+    const int j = idx / ne, i = idx - j * ne;
+    L[idx] = i >= j ? F[(size_t)j * nf + i] : 0.0;
+  }
+}
+
+// Boundary block K_bb of the assembled stiffness per design (lumped /
+// super-lumped preconditioners): entries summed over the <= 2
+// elements adjacent to a perimeter node in ascending element order.
+__global__ void k_kbb(const double* dens, int n, double E0, double Emin, double p,
+                      const int* pnode_elem /* nb/2 x 2 x 2 : (elem, corner) */,
+                      const int* perim_dof, int nb, double* Kbb) {
+  const int d = blockIdx.y;
+  const double* rho = dens + (size_t)d * n * n;
+  double* K = Kbb + (size_t)d * nb * nb;
+  const int nn = n + 1;
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < nb * nb;
+       idx += gridDim.x * blockDim.x) {
+    const int j = idx / nb, i = idx - j * nb;
+    const int di = perim_dof[i], dj = perim_dof[j];
+    const int ni = di >> 1, nj = dj >> 1;
+    double v = 0.0;
+    for (int q = 0; q < 2; ++q) {
+      const int e = pnode_elem[(i >> 1) * 4 + 2 * q];
+      if (e < 0) continue;
+      const int ci = pnode_elem[(i >> 1) * 4 + 2 * q + 1];
+      const int ex = e % n, ey = e / n;
+      const int n0 = ey * nn + ex;
+      const int en[4] = {n0, n0 + 1, n0 + nn + 1, n0 + nn};
+      int cj = -1;
+      for (int a = 0; a < 4; ++a)
+        if (en[a] == nj) cj = a;
+      if (cj < 0) continue;
+      const double E = Emin + pow(rho[e], p) * (E0 - Emin);
+      v += E * c_kunit[(2 * cj + (dj & 1)) * 8 + 2 * ci + (di & 1)];
+    }
+    (void)ni;
+    K[idx] = v;
+  }
+}
+
+// lumped preconditioner block K_TT (or its diagonal) -> dense row-major
+__global__ void k_pc_lumped(const int* design, const int* t_off, const int* t_cnt, const int* t_all,
+                            const double* Kbb, int nb, const long long* mat_off, const int* mat_ld,
+                            double* mats, int diag_only) {
+  const int sl = blockIdx.y;
+  const int nt = t_cnt[sl], ld = mat_ld[sl];
+  const int* T = t_all + t_off[sl];
+  const double* K = Kbb + (size_t)design[sl] * nb * nb;
+  double* M = mats + mat_off[sl];
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < nt * ld;
+       idx += gridDim.x * blockDim.x) {
+    const int a = idx / ld, b = idx - a * ld;
+    double v = 0.0;
+    if (b < nt && (!diag_only || a == b)) v = K[(size_t)T[b] * nb + T[a]];
+    M[(size_t)a * ld + b] = v;
+  }
+}
+
+}  // namespace fg

@@ -1,0 +1,262 @@
+"""Python mirror of the reference's solver entry points over the C-ABI.
+
+``FetiSystem`` wraps one ``fetigpu_ctx`` (include/fetigpu.h) and exposes the
+reference's operator / plugin interface for this path with the same names
+and argument meaning: ``apply_F`` (DualOperator::apply),
+``apply_precond`` (apply_coarse_preconditioner), ``project``
+(CoarseSpace::project / project_block, decomposition.hpp:136-138), ``rhs``
+(d and lambda0), ``solve`` (pcg / simultaneous_pcg,
+SPEC.md:426-443) and ``recover`` (recover_primal).  Errors are
+raised as the reference's exception types (proj/include/feti/errors.hpp).
+
+There is no CPU fallback: constructing a system without the CUDA library or
+without a GPU raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Optional
+
+import numpy as np
+
+from .problems import Problem
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libfetigpu.so")
+_lib = None
+
+D = C.POINTER(C.c_double)
+I = C.POINTER(C.c_int)
+
+
+# ---- errors (proj/include/feti/errors.hpp:7-69) ---------------------------
+class FetiError(RuntimeError):
+    code = -1
+
+
+def _mk(name, code):
+    return type(name, (FetiError,), {"code": code})
+
+
+NotPositiveDefinite = _mk("NotPositiveDefinite", 1)
+IndefiniteInput = _mk("IndefiniteInput", 2)
+IncompatibleRhs = _mk("IncompatibleRhs", 3)
+EdgeNotOnBoundary = _mk("EdgeNotOnBoundary", 4)
+DimensionMismatch = _mk("DimensionMismatch", 5)
+NodeNotFound = _mk("NodeNotFound", 6)
+InsufficientCorners = _mk("InsufficientCorners", 7)
+ZeroStiffnessDiagonal = _mk("ZeroStiffnessDiagonal", 8)
+SingularInterior = _mk("SingularInterior", 9)
+CoarseSingular = _mk("CoarseSingular", 10)
+SingularRemainder = _mk("SingularRemainder", 11)
+SingularCoarse = _mk("SingularCoarse", 12)
+SingularGlobal = _mk("SingularGlobal", 13)
+NegativeInnerProduct = _mk("NegativeInnerProduct", 14)
+NotConverged = _mk("NotConverged", 15)
+StateSolveFailed = _mk("StateSolveFailed", 16)
+ConfigError = _mk("ConfigError", 17)
+IoError = _mk("IoError", 18)
+InvalidArgument = _mk("InvalidArgument", 20)
+DomainError = _mk("DomainError", 21)
+CudaError = _mk("CudaError", 100)
+NoDevice = _mk("NoDevice", 101)
+OutOfMemory = _mk("OutOfMemory", 102)
+StateError = _mk("StateError", 103)
+_ERRORS = {c.code: c for c in (NotPositiveDefinite, IndefiniteInput, IncompatibleRhs,
+                               EdgeNotOnBoundary, DimensionMismatch, NodeNotFound,
+                               InsufficientCorners, ZeroStiffnessDiagonal, SingularInterior,
+                               CoarseSingular, SingularRemainder, SingularCoarse, SingularGlobal,
+                               NegativeInnerProduct, NotConverged, StateSolveFailed, ConfigError,
+                               IoError, InvalidArgument, DomainError, CudaError, NoDevice,
+                               OutOfMemory, StateError)}
+
+EXPORTED = ["fetigpu_create", "fetigpu_build", "fetigpu_destroy", "fetigpu_last_error",
+            "fetigpu_stats_get", "fetigpu_rows", "fetigpu_apply_F", "fetigpu_apply_F_device",
+            "fetigpu_apply_precond", "fetigpu_apply_precond_device", "fetigpu_project",
+            "fetigpu_project_device", "fetigpu_rhs", "fetigpu_solve", "fetigpu_recover",
+            "fetigpu_local_operator", "fetigpu_device_alloc", "fetigpu_device_free",
+            "fetigpu_host_alloc", "fetigpu_host_free", "fetigpu_memcpy", "fetigpu_fill_random",
+            "fetigpu_synchronize", "fetigpu_time_apply"]
+
+
+class FgProblem(C.Structure):
+    _fields_ = [("sx", C.c_int), ("sy", C.c_int), ("n", C.c_int),
+                ("hx", C.c_double), ("hy", C.c_double),
+                ("E0", C.c_double), ("Emin", C.c_double), ("nu", C.c_double),
+                ("p", C.c_double), ("thickness", C.c_double),
+                ("n_designs", C.c_int), ("densities", D), ("module_type", I),
+                ("n_dirichlet", C.c_int), ("dir_gnode", I), ("dir_dir", I), ("dir_value", D),
+                ("n_tractions", C.c_int), ("tr_sub", I), ("tr_side", I), ("tr_first", I),
+                ("tr_count", I), ("tr_txy", D),
+                ("n_point_loads", C.c_int), ("pl_gnode", I), ("pl_dir", I), ("pl_value", D),
+                ("method", C.c_int), ("scaling", C.c_int), ("precond", C.c_int)]
+
+
+class FgOpts(C.Structure):
+    _fields_ = [("tol", C.c_double), ("rel", C.c_int), ("max_it", C.c_int),
+                ("directions", C.c_int), ("pivot_tol", C.c_double), ("reorth_passes", C.c_int)]
+
+
+class FgTrace(C.Structure):
+    _fields_ = [("status", C.c_int), ("iterations", C.c_int), ("f_applies", C.c_int),
+                ("eps0", C.c_double), ("eps_final", C.c_double), ("cap", C.c_int),
+                ("eps", D), ("kept", I), ("f_app", I), ("solve_ms", C.c_double)]
+
+
+class FgStats(C.Structure):
+    _fields_ = [(k, C.c_int) for k in ("m", "n_sub", "local_dofs", "n_c", "n_kept", "n_iface",
+                                       "max_ns", "n_designs", "n_op_slots", "n_pc_slots")] + \
+               [(k, C.c_double) for k in ("op_bytes", "op_flops_per_col", "main_kernel_bytes",
+                                          "build_ms", "nd_ms", "slot_ms", "coarse_ms",
+                                          "device_bytes")]
+
+
+def lib():
+    """Load libfetigpu.so; raises if the CUDA extension was not built."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} missing: run __graft_entry__.build() (no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        L.fetigpu_last_error.restype = C.c_char_p
+        L.fetigpu_destroy.restype = None
+        L.fetigpu_create.argtypes = [C.POINTER(FgProblem), C.POINTER(C.c_void_p)]
+        _lib = L
+    return _lib
+
+
+def _p(a):
+    if a is None:
+        return None
+    if a.dtype == np.int32:
+        return a.ctypes.data_as(I)
+    return a.ctypes.data_as(D)
+
+
+def check(rc: int):
+    if rc != 0:
+        msg = lib().fetigpu_last_error().decode()
+        raise _ERRORS.get(rc, FetiError)(f"[{rc}] {msg}")
+
+
+def make_struct(prob: Problem, keep: list) -> FgProblem:
+    a = prob.arrays()
+    keep.append(a)
+    s = FgProblem()
+    s.sx, s.sy, s.n = prob.sx, prob.sy, prob.n
+    s.hx, s.hy = prob.hx, prob.hy
+    s.E0, s.Emin, s.nu, s.p, s.thickness = prob.E0, prob.Emin, prob.nu, prob.p, prob.thickness
+    s.n_designs = int(prob.densities.shape[0])
+    s.densities, s.module_type = _p(a["densities"]), _p(a["module_type"])
+    s.n_dirichlet = len(prob.dirichlet)
+    s.dir_gnode, s.dir_dir, s.dir_value = _p(a["dir_gnode"]), _p(a["dir_dir"]), _p(a["dir_value"])
+    s.n_tractions = len(prob.tractions)
+    s.tr_sub, s.tr_side, s.tr_first, s.tr_count, s.tr_txy = (
+        _p(a["tr_sub"]), _p(a["tr_side"]), _p(a["tr_first"]), _p(a["tr_count"]), _p(a["tr_txy"]))
+    s.n_point_loads = len(prob.point_loads)
+    s.pl_gnode, s.pl_dir, s.pl_value = _p(a["pl_gnode"]), _p(a["pl_dir"]), _p(a["pl_value"])
+    s.method, s.scaling, s.precond = prob.method, prob.scaling, prob.precond
+    return s
+
+
+class FetiSystem:
+    """A T-FETI or FETI-DP dual system resident on the GPU (TfetiSystem /
+    FetidpSystem of SPEC.md:346-353)."""
+
+    def __init__(self, prob: Problem, build: bool = True):
+        self.prob = prob
+        self._keep = []
+        st = make_struct(prob, self._keep)
+        h = C.c_void_p()
+        check(lib().fetigpu_create(C.byref(st), C.byref(h)))
+        self.h = h
+        s = self.stats()
+        self.m, self.n_sub, self.local_dofs = s["m"], s["n_sub"], s["local_dofs"]
+        self.n_c = s["n_c"]
+        self.built = False
+        if build:
+            self.build()
+
+    def build(self):
+        """Device build (K1-K3, K6); host setup already ran in fetigpu_create."""
+        check(lib().fetigpu_build(self.h))
+        self.built = True
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().fetigpu_destroy(self.h)
+            self.h = None
+
+    __del__ = close
+
+    def stats(self) -> dict:
+        s = FgStats()
+        check(lib().fetigpu_stats_get(self.h, C.byref(s)))
+        return {k: getattr(s, k) for k, _ in FgStats._fields_}
+
+    def rows(self) -> dict:
+        m = self.m
+        out = {k: np.zeros(m, dtype=np.int32) for k in ("kind", "sub_plus", "dof_plus",
+                                                         "sub_minus", "dof_minus", "mult")}
+        gap, wp, wm = np.zeros(m), np.zeros(m), np.zeros(m)
+        check(lib().fetigpu_rows(self.h, _p(out["kind"]), _p(out["sub_plus"]), _p(out["dof_plus"]),
+                                 _p(out["sub_minus"]), _p(out["dof_minus"]), _p(gap),
+                                 _p(out["mult"]), _p(wp), _p(wm)))
+        out.update(gap=gap, w_plus=wp, w_minus=wm)
+        return out
+
+    def apply_F(self, x: np.ndarray) -> np.ndarray:
+        x = np.asarray(x, dtype=np.float64)
+        cols = 1 if x.ndim == 1 else x.shape[1]
+        X = np.ascontiguousarray(x.reshape(self.m, cols).T)
+        Y = np.zeros_like(X)
+        check(lib().fetigpu_apply_F(self.h, _p(X), _p(Y), C.c_int(cols), C.c_int(self.m)))
+        return Y.T.reshape(x.shape).copy()
+
+    def apply_precond(self, r: np.ndarray, columns: bool = False):
+        r = np.ascontiguousarray(r, dtype=np.float64)
+        z = np.zeros(self.m)
+        Z = np.zeros((self.n_sub, self.m)) if columns else None
+        check(lib().fetigpu_apply_precond(self.h, _p(r), _p(z), _p(Z) if columns else None))
+        return (z, Z.T.copy()) if columns else z
+
+    def project(self, v: np.ndarray) -> np.ndarray:
+        v = np.asarray(v, dtype=np.float64)
+        cols = 1 if v.ndim == 1 else v.shape[1]
+        V = np.ascontiguousarray(v.reshape(self.m, cols).T)
+        check(lib().fetigpu_project(self.h, _p(V), C.c_int(cols), C.c_int(self.m)))
+        return V.T.reshape(v.shape).copy()
+
+    def rhs(self):
+        d, l0 = np.zeros(self.m), np.zeros(self.m)
+        check(lib().fetigpu_rhs(self.h, _p(d), _p(l0)))
+        return d, l0
+
+    def solve(self, tol: float = 1e-6, max_it: int = 1000, directions: int = 0, rel: bool = True,
+              pivot_tol: float = 1e-12, reorth_passes: int = 2):
+        o = FgOpts(tol, 1 if rel else 0, max_it, directions, pivot_tol, reorth_passes)
+        cap = max_it + 2
+        eps, kept, fap = np.zeros(cap), np.zeros(cap, dtype=np.int32), np.zeros(cap, dtype=np.int32)
+        tr = FgTrace(0, 0, 0, 0.0, 0.0, cap, _p(eps), _p(kept), _p(fap), 0.0)
+        lam = np.zeros(self.m)
+        check(lib().fetigpu_solve(self.h, C.byref(o), _p(lam), C.byref(tr)))
+        n = tr.iterations + 1
+        return lam, dict(status=tr.status, iterations=tr.iterations, f_applies=tr.f_applies,
+                         eps0=tr.eps0, eps_final=tr.eps_final, eps=eps[:n].copy(),
+                         kept=kept[:n].copy(), f_app=fap[:n].copy(), solve_ms=tr.solve_ms)
+
+    def recover(self, lam: np.ndarray) -> np.ndarray:
+        lam = np.ascontiguousarray(lam, dtype=np.float64)
+        u = np.zeros((self.n_sub, self.local_dofs))
+        check(lib().fetigpu_recover(self.h, _p(lam), _p(u)))
+        return u
+
+    def local_operator(self, s: int):
+        cap = 8 * self.prob.n
+        ns = C.c_int()
+        dofs = np.zeros(cap, dtype=np.int32)
+        F = np.zeros(cap * cap)
+        check(lib().fetigpu_local_operator(self.h, s, C.byref(ns), _p(dofs), _p(F), cap))
+        n = ns.value
+        return dofs[:n].copy(), F[:n * n].reshape(n, n).copy()
