@@ -148,6 +148,9 @@ typedef struct fetigpu_stats {
   double device_bytes;       /* device memory held by the context */
 } fetigpu_stats;
 
+/* Select the CUDA device used by contexts built afterwards from this host
+ * thread (one process per GPU: the rank's local device). */
+int fetigpu_set_device(int device);
 int fetigpu_create(const fetigpu_problem* p, fetigpu_ctx** out);
 int fetigpu_build(fetigpu_ctx* ctx);
 void fetigpu_destroy(fetigpu_ctx* ctx);

@@ -124,6 +124,11 @@ struct Ctx {
   bool have_rhs = false;
   // stats
   double op_bytes = 0, op_flops = 0, main_bytes = 0;
+  // grow-only staging buffers of the host-pointer entry points
+  DBuf<double> stage_x, stage_y;
+  void stage(size_t n) {
+    if (stage_x.n < n) { stage_x.alloc(n); stage_y.alloc(n); }
+  }
 
   ~Ctx() {
     if (cb) cublasDestroy(cb);
@@ -1357,6 +1362,10 @@ extern "C" {
 
 const char* fetigpu_last_error(void) { return g_err.c_str(); }
 
+int fetigpu_set_device(int device) {
+  return guarded([&] { CK(cudaSetDevice(device)); });
+}
+
 int fetigpu_create(const fetigpu_problem* p, fetigpu_ctx** out) {
   *out = nullptr;
   auto ctx = std::make_unique<fetigpu_ctx>();
@@ -1418,12 +1427,10 @@ int fetigpu_apply_F(fetigpu_ctx* ctx, const double* x, double* y, int ncols, int
     NEED_BUILT(ctx);
     Ctx& c = ctx->c;
     const size_t bytes = (size_t)ld * ncols * 8;
-    DBuf<double> dx, dy;
-    dx.alloc((size_t)ld * ncols);
-    dy.alloc((size_t)ld * ncols);
-    CK(cudaMemcpyAsync(dx.p, x, bytes, cudaMemcpyHostToDevice, c.st));
-    c.apply_F(dx.p, dy.p, ncols, ld, ld);
-    CK(cudaMemcpyAsync(y, dy.p, bytes, cudaMemcpyDeviceToHost, c.st));
+    c.stage((size_t)ld * ncols);
+    CK(cudaMemcpyAsync(c.stage_x.p, x, bytes, cudaMemcpyHostToDevice, c.st));
+    c.apply_F(c.stage_x.p, c.stage_y.p, ncols, ld, ld);
+    CK(cudaMemcpyAsync(y, c.stage_y.p, bytes, cudaMemcpyDeviceToHost, c.st));
     CK(cudaStreamSynchronize(c.st));
   });
 }

@@ -71,7 +71,7 @@ _ERRORS = {c.code: c for c in (NotPositiveDefinite, IndefiniteInput, Incompatibl
                                IoError, InvalidArgument, DomainError, CudaError, NoDevice,
                                OutOfMemory, StateError)}
 
-EXPORTED = ["fetigpu_create", "fetigpu_build", "fetigpu_destroy", "fetigpu_last_error",
+EXPORTED = ["fetigpu_set_device", "fetigpu_create", "fetigpu_build", "fetigpu_destroy", "fetigpu_last_error",
             "fetigpu_stats_get", "fetigpu_rows", "fetigpu_apply_F", "fetigpu_apply_F_device",
             "fetigpu_apply_precond", "fetigpu_apply_precond_device", "fetigpu_project",
             "fetigpu_project_device", "fetigpu_rhs", "fetigpu_solve", "fetigpu_recover",
