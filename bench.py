@@ -186,36 +186,62 @@ def cpu_model():
     return "unknown"
 
 
+def c4_work(sx=64, sy=32, n=64):
+    """Algorithmic work of one C4 F-apply from the partition geometry alone
+    (SURVEY.md 8d / App. A): FETI-DP with every partition vertex primal and the
+    left edge clamped.  n_s = 2(n-1) DOFs per shared module edge; n_c,s = the
+    module's unclamped corner DOFs."""
+    e = 2 * (n - 1)
+    sn2 = snc = sns = 0.0
+    m = 0
+    for sj in range(sy):
+        for si in range(sx):
+            nb = (si > 0) + (si < sx - 1) + (sj > 0) + (sj < sy - 1)
+            ns = e * nb
+            nc = 4 if si == 0 else 8
+            sn2 += ns * ns
+            snc += ns * nc
+            sns += ns
+    m = e * ((sx - 1) * sy + sx * (sy - 1))
+    Nc = 2 * (sx + 1) * (sy + 1) - 2 * (sy + 1)
+    byts = 8 * sn2 + 16 * snc + 8.0 * Nc * Nc + 16.0 * m + 8 * sns
+    flops = 2 * sn2 + 4 * snc + 2.0 * Nc * Nc
+    return {"bytes": byts, "flops_per_col": flops, "main_bytes": 8 * sn2, "m": m, "n_c": Nc}
+
+
 def run_reference(args, ws, rank, dist):
-    """--impl reference: oracle port on host cores, rank 0 only."""
+    """--impl reference: the oracle port on all host cores, rank 0 only; the
+    other ranks exit without work.  No product code on this path."""
     if rank != 0:
         return
-    c4 = c4_bytes()
-    samples = []
-    for i in range(args.warmup + args.steps):
-        r = cpu_sample(steps=1, warmup=0 if i else 1)
-        if i >= args.warmup:
-            samples.append(r)
-    t = statistics.median(s["t_apply_c4_s"] for s in samples)
-    v = c4 / t / 1e9
+    from oracle import pyoracle
+    pyoracle.build()
+    sx, sy = 8, 4
+    prob = pb.config4(sx=sx, sy=sy)
+    o = pyoracle.Oracle(prob)
+    x = np.random.default_rng(0).standard_normal(o.m)
+    for _ in range(args.warmup):
+        o.apply_F(x)
+    ts = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        o.apply_F(x)
+        ts.append(time.perf_counter() - t0)
+    scale = 2048.0 / (sx * sy)
+    t = statistics.median(ts) * scale
+    w = c4_work()
+    v = w["bytes"] / t / 1e9
+    sample = (f"C4 density law on a {sx}x{sy} grid of 64x64 modules ({sx*sy} of 2048 subdomains), "
+              f"median of {args.steps} applies after {args.warmup} warm-up, extrapolated x{scale:.0f}")
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "GB/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded U(0,1) densities, C4 law)",
             "config": {"workload": "C4 FETI-DP F-apply (single direction)", "flush_l2": False},
-            "cpu_baseline": {"value": v, "unit": "GB/s", "cores": samples[0]["cores"], "kind": "port",
-                             "sample": samples[0]["sample"], "cpu_model": cpu_model()},
+            "cpu_baseline": {"value": v, "unit": "GB/s", "cores": os.cpu_count(), "kind": "port",
+                             "sample": sample, "cpu_model": cpu_model()},
             "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
-
-
-def c4_bytes():
-    """Algorithmic bytes of one C4 F-apply."""
-    from paper_2111_11728_b200 import engine
-    g = engine.FetiSystem(pb.config4(), build=False)
-    b = g.stats()["op_bytes"]
-    g.close()
-    return b
 
 
 def solve_table(engine, configs):

@@ -1397,7 +1397,18 @@ int fetigpu_stats_get(const fetigpu_ctx* ctx, fetigpu_stats* s) {
     s->n_kept = c.su.n_kept; s->n_iface = c.su.n_iface; s->max_ns = mx; s->n_designs = c.su.n_designs;
     s->n_op_slots = (int)c.su.op_slots.size();
     s->n_pc_slots = (int)(c.su.precond == FETIGPU_DIRICHLET ? c.su.pc_slots.size() : c.su.pc_lumped_T.size());
-    s->op_bytes = c.op_bytes; s->op_flops_per_col = c.op_flops; s->main_kernel_bytes = c.main_bytes;
+    // algorithmic work per apply, pure index counts
+    double sn2 = 0, snc = 0, sns = 0;
+    const bool dp = c.su.method == FETIGPU_FETIDP;
+    for (auto& S : c.su.subs) {
+      const double ns = (double)S.Top.size();
+      sn2 += ns * ns;
+      sns += ns;
+      if (dp) snc += ns * (double)S.c.size();
+    }
+    s->op_bytes = 8 * sn2 + (dp ? 16 * snc + 8.0 * c.su.Nc * c.su.Nc : 0) + 16.0 * c.su.m + 8 * sns;
+    s->op_flops_per_col = 2 * sn2 + (dp ? 4 * snc + 2.0 * c.su.Nc * c.su.Nc : 0);
+    s->main_kernel_bytes = 8 * sn2;
     s->build_ms = c.build_ms; s->nd_ms = c.nd_ms; s->slot_ms = c.slot_ms; s->coarse_ms = c.coarse_ms;
     s->device_bytes = (double)g_device_bytes;
   });

@@ -81,3 +81,20 @@ def test_build_without_device_fails_loudly():
     g = engine.FetiSystem(pb.config1(sx=2, sy=1, n=4), build=False)
     with pytest.raises((engine.NoDevice, engine.CudaError)):
         g.build()
+
+
+def test_bench_work_formula_matches_library():
+    """bench.py's analytic C4 work (used by the reference arm) equals the
+    library's own count, and SURVEY.md App. A's figures."""
+    import bench
+    from paper_2111_11728_b200 import engine
+    w = bench.c4_work()
+    g = engine.FetiSystem(pb.config4(), build=False)
+    s = g.stats()
+    assert s["m"] == w["m"] == 504000 and s["n_c"] == w["n_c"] == 4224
+    assert s["op_bytes"] == w["bytes"] == 4279246848.0
+    assert abs(s["op_flops_per_col"] * 2048 - 2.183e12) < 1e9
+    for fn, m, nc in ((pb.config2, 3224, 80), (lambda: pb.config3(method=1), 14384, 302),
+                      (pb.config5, 91744, 1118), (lambda: pb.config3(method=0), 15736, 0)):
+        st = engine.FetiSystem(fn(), build=False).stats()
+        assert (st["m"], st["n_c"]) == (m, nc)
