@@ -182,6 +182,15 @@ int fetigpu_recover(fetigpu_ctx* ctx, const double* lambda, double* u);
  * writes n_s, the local DOF ids (ns) and the dense n_s x n_s F_s. */
 int fetigpu_local_operator(fetigpu_ctx* ctx, int s, int* ns, int* dofs, double* F, int cap);
 
+/* Block F-apply (K5, FP64 tensor cores): Q = F W for k columns stored
+ * row-major (W(i,c) = W[i*ldw + c]), device pointers, ctx stream. */
+int fetigpu_apply_F_block_device(fetigpu_ctx* ctx, const double* W, int ldw, double* Q, int ldq, int k);
+int fetigpu_time_apply_block(fetigpu_ctx* ctx, const double* W, double* Q, int k, int reps, double* ms);
+/* Measured FP64 issue peaks of this device (DMMA m8n8k4 and DFMA), TFLOP/s. */
+int fetigpu_fp64_peak(double* tflops_dmma, double* tflops_dfma);
+/* DMMA fragment-layout self test: C (8x8 row-major) = A (8x4) B (4x8). */
+int fetigpu_selftest_dmma(const double* A, const double* B, double* C);
+
 /* Device memory / timing helpers for benchmarks (no torch on the path). */
 int fetigpu_device_alloc(fetigpu_ctx* ctx, size_t bytes, void** ptr);
 int fetigpu_device_free(fetigpu_ctx* ctx, void* ptr);

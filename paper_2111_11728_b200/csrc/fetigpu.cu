@@ -19,6 +19,7 @@
 #include "fetigpu.h"
 #include "kernels_apply.cuh"
 #include "kernels_build.cuh"
+#include "kernels_dmma.cuh"
 #include "setup.hpp"
 
 namespace fg {
@@ -164,6 +165,8 @@ struct Ctx {
                             kSmallFront * kSmallFront * 8));
     CK(cudaFuncSetAttribute(k_front_elim_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             kSmallFront * kSmallFront * 8));
+    CK(cudaFuncSetAttribute(k_block_apply<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBlockSmem));
+    CK(cudaFuncSetAttribute(k_block_apply<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBlockSmem));
   }
 
   double elapsed(cudaEvent_t a, cudaEvent_t b) {
@@ -732,16 +735,70 @@ struct Ctx {
     }
   }
 
-  void apply_precond(const double* r, double* z, double* Zcols) {
+  // Zcols: per-subdomain columns, column-major m x N_s (row_major = false)
+  // or row-major m x N_s (row_major = true)
+  void apply_precond(const double* r, double* z, double* Zcols, bool row_major = false) {
     CK(cudaMemsetAsync(z, 0, su.m * 8, st));
     if (Zcols) CK(cudaMemsetAsync(Zcols, 0, (size_t)su.m * su.Ns * 8, st));
+    const int ldz = row_major ? 1 : su.m, zrs = row_major ? su.Ns : 1;
     if (KRp == 1)
       k_gather_gemv_scatter<1, false><<<su.Ns, kThreads, max_pc_ld * 8, st>>>(
-          d_pc.p, d_pcmat.p, d_pcrows.p, d_pccoef.p, r, z, Zcols, su.m, nullptr, nullptr, 0, 0);
+          d_pc.p, d_pcmat.p, d_pcrows.p, d_pccoef.p, r, z, Zcols, ldz, nullptr, nullptr, 0, 0, zrs);
     else
       k_gather_gemv_scatter<3, false><<<su.Ns, kThreads, max_pc_ld * 8, st>>>(
-          d_pc.p, d_pcmat.p, d_pcrows.p, d_pccoef.p, r, z, Zcols, su.m, nullptr, nullptr, 0, 0);
+          d_pc.p, d_pcmat.p, d_pcrows.p, d_pccoef.p, r, z, Zcols, ldz, nullptr, nullptr, 0, 0, zrs);
     LAUNCH_CHECK();
+  }
+
+  // ---- K5: Q = F W for k columns, row-major blocks (W(i,c) = W[i*ldw + c])
+  DBuf<double> blk_t, blk_T, blk_U;
+  void apply_F_block(const double* W, int ldw, double* Q, int ldq, int k) {
+    const int Ns = su.Ns, m = su.m;
+    if (ldq == k) CK(cudaMemsetAsync(Q, 0, (size_t)m * k * 8, st));
+    else CK(cudaMemset2DAsync(Q, (size_t)ldq * 8, 0, (size_t)k * 8, m, st));
+    BlockApplyArgs a{d_op.p, d_opmat.p, d_oprows.p, d_opcoef.p, KR, nullptr, nullptr, nullptr, nullptr, 0,
+                     W, ldw, Q, ldq, k};
+    int max_ns = 0;
+    for (int n : op_ns) max_ns = std::max(max_ns, n);
+    if (su.method == FETIGPU_FETIDP) {
+      const int Nc = su.Nc;
+      int tot_c = 0;
+      for (auto& S : su.subs) tot_c += (int)S.c.size();
+      if (blk_t.n < (size_t)tot_c * k) blk_t.alloc((size_t)tot_c * k);
+      if (blk_T.n < (size_t)Nc * k) { blk_T.alloc((size_t)Nc * k); blk_U.alloc((size_t)Nc * k); }
+      k_block_dp_t<<<dim3((k + 63) / 64, Ns), 256, 0, st>>>(d_op.p, d_dp.p, d_oprows.p, d_opcoef.p, d_abc.p, W,
+                                                             ldw, k, blk_t.p, k);
+      k_coarse_gather_block<<<dim3((k + 255) / 256, Nc), 256, 0, st>>>(d_optr.p, d_oidx.p, blk_t.p, k, Nc, k,
+                                                                       blk_T.p, k);
+      const double one = 1.0, zero = 0.0;
+      // U = Kbar^{-1} T  (row-major N_c x k == column-major k x N_c: U^T = T^T Kinv)
+      CB(cublasDgemm(cb, CUBLAS_OP_N, CUBLAS_OP_N, k, Nc, Nc, &one, blk_T.p, k, d_Kinv.p, Nc, &zero, blk_U.p, k));
+      a.dps = d_dp.p; a.abc = d_abc.p; a.cmap = d_cmap.p; a.U = blk_U.p; a.ldu = k;
+      max_ns += 8;
+    }
+    dim3 grid((k + kBN - 1) / kBN, (max_ns + kBM - 1) / kBM, Ns);
+    if (KR == 1) k_block_apply<1><<<grid, 256, kBlockSmem, st>>>(a);
+    else k_block_apply<3><<<grid, 256, kBlockSmem, st>>>(a);
+    LAUNCH_CHECK();
+  }
+
+  // v <- P v for a row-major block (m x ncols, ld = ncols), T-FETI only
+  void project_rm(double* v, int ncols) {
+    if (su.method != FETIGPU_TFETI) return;
+    const int nc = 3 * su.Ns;
+    DBuf<double> g, h, corr;
+    g.alloc((size_t)nc * ncols);
+    h.alloc((size_t)nc * ncols);
+    corr.alloc((size_t)su.m * ncols);
+    corr.zero(st);
+    k_proj_gather<<<dim3(su.Ns, ncols), kThreads, 0, st>>>(d_pj.p, d_pcrows.p, d_pjcoef.p, d_RT.p, d_rt_off.p, v, 1,
+                                                          g.p, nc, -1.0, ncols);
+    k_small_gemm<<<dim3(grid_for(nc), ncols), kThreads, 0, st>>>(d_H.p, nc, g.p, nc, h.p, nc);
+    k_proj_scatter<<<dim3(su.Ns, ncols), kThreads, 0, st>>>(d_pj.p, d_pcrows.p, d_pjcoef.p, d_RT.p, d_rt_off.p,
+                                                           h.p, nc, corr.p, 1, ncols);
+    k_add<<<grid_for((long long)su.m * ncols), kThreads, 0, st>>>(su.m * ncols, corr.p, v, 0, 0);
+    LAUNCH_CHECK();
+    CK(cudaStreamSynchronize(st));
   }
 
   // corr = P v - v for ncols columns (T-FETI); caller adds
@@ -1202,11 +1259,13 @@ int Ctx::solve(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_trace* 
 // one search direction per subdomain, Delta = Q^T W factorized by the
 // rank-revealing Cholesky, W, Q compressed to F-orthonormal columns, and the
 // new block re-orthogonalized against all stored blocks (CGS, 2 passes).
+// Blocks are row-major (m x k, k fastest) so the K5 block apply gathers and
+// scatters whole contiguous rows; cuBLAS sees them as column-major k x m.
 int Ctx::solve_rrs(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_trace* tr) {
   const int m = su.m, Ns = su.Ns;
   const int passes = std::max(1, o.reorth_passes);
   rhs();
-  DBuf<double> lam, r, z, q, tmp, Z, W, Q, Wsel, Delta, gamma;
+  DBuf<double> lam, r, z, q, tmp, Z, W, Wsel, Delta, gamma;
   DBuf<int> perm, rank_d;
   DBuf<Scal> sc;
   lam.alloc(m); r.alloc(m); z.alloc(m); q.alloc(m); tmp.alloc(m);
@@ -1227,7 +1286,7 @@ int Ctx::solve_rrs(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_tra
   int fapp = 1;
   k_sub<<<grid_for(m), kThreads, 0, st>>>(m, d_d.p, q.p, r.p);
   project(r.p, 1, m);
-  apply_precond(r.p, z.p, Z.p);  // Alg. 1 line 2 (columns) and z = Z 1
+  apply_precond(r.p, z.p, Z.p, true);  // Alg. 1 line 2 (columns) and z = Z 1
   dots({{r.p, z.p}, {r.p, r.p}, {z.p, z.p}}, &sc.p->rz);
   CK(cudaMemcpyAsync(hs, sc.p, sizeof(Scal), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
@@ -1238,7 +1297,7 @@ int Ctx::solve_rrs(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_tra
   };
   const double eps0 = metric(*hs);
   double eps = eps0;
-  int it = 0, status = FETIGPU_MAX_ITER, k = Ns;
+  int it = 0, status = FETIGPU_MAX_ITER;
   auto push = [&](double e, int kept) {
     if (tr && it < tr->cap) {
       if (tr->eps) tr->eps[it] = e;
@@ -1248,17 +1307,18 @@ int Ctx::solve_rrs(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_tra
   };
   push(eps0, Ns);
   CK(cudaMemcpyAsync(W.p, Z.p, (size_t)m * Ns * 8, cudaMemcpyDeviceToDevice, st));
-  project(W.p, Ns, m);  // line 3
+  project_rm(W.p, Ns);  // line 3
   const double target = o.rel ? o.tol * eps0 : o.tol;
   while (true) {
     if (eps <= target) { status = FETIGPU_CONVERGED; break; }
     if (it >= o.max_it) { status = FETIGPU_MAX_ITER; break; }
+    const int k = Ns;
     auto Qb = std::make_unique<DBuf<double>>();
     Qb->alloc((size_t)m * k);
-    apply_F(W.p, Qb->p, k, m, m);  // line 7
+    apply_F_block(W.p, k, Qb->p, k, k);  // line 7 (K5)
     fapp += k;
-    // line 8: Delta = Q^T W (lower triangle used)
-    CB(cublasDgemm(cb, CUBLAS_OP_T, CUBLAS_OP_N, k, k, m, &one, Qb->p, m, W.p, m, &zero, Delta.p, k));
+    // line 8: Delta = Q^T W (column-major k x k; lower triangle used)
+    CB(cublasDgemm(cb, CUBLAS_OP_N, CUBLAS_OP_T, k, k, m, &one, Qb->p, k, W.p, k, &zero, Delta.p, k));
     k_mirror_lower<<<grid_for((long long)k * k), kThreads, 0, st>>>(Delta.p, k);
     // line 9
     k_pivchol<<<1, 1024, 0, st>>>(Delta.p, k, o.pivot_tol, perm.p, rank_d.p, d_status.p);
@@ -1268,27 +1328,30 @@ int Ctx::solve_rrs(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_tra
     CK(cudaStreamSynchronize(st));
     int hstat = 0;
     CK(cudaMemcpy(&hstat, d_status.p, sizeof(int), cudaMemcpyDeviceToHost));
-    if (hstat) { CK(cudaMemset(d_status.p, 0, sizeof(int))); fail(FETIGPU_E_INDEFINITE_INPUT, "pivoted Cholesky: negative pivot"); }
+    if (hstat) {
+      CK(cudaMemset(d_status.p, 0, sizeof(int)));
+      fail(FETIGPU_E_INDEFINITE_INPUT, "pivoted Cholesky: negative pivot");
+    }
     if (rank == 0) { status = FETIGPU_BREAKDOWN; break; }
-    // lines 10-11: W <- W N^T [L~^{-T}; 0], same for Q
+    // lines 10-11: W <- W N^T [L~^{-T}; 0]  ==  (L~^{-1} W_sel^T)^T, same for Q
     auto Wb = std::make_unique<DBuf<double>>();
     Wb->alloc((size_t)m * rank);
-    k_gather_cols<<<dim3(grid_for(m), rank), kThreads, 0, st>>>(W.p, m, perm.p, rank, Wb->p);
-    k_gather_cols<<<dim3(grid_for(m), rank), kThreads, 0, st>>>(Qb->p, m, perm.p, rank, Wsel.p);
-    CB(cublasDtrsm(cb, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, m, rank,
-                   &one, Delta.p, k, Wb->p, m));
-    CB(cublasDtrsm(cb, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, m, rank,
-                   &one, Delta.p, k, Wsel.p, m));
+    k_gather_cols_rm<<<grid_for((long long)m * rank), kThreads, 0, st>>>(W.p, k, perm.p, rank, m, Wb->p, rank);
+    k_gather_cols_rm<<<grid_for((long long)m * rank), kThreads, 0, st>>>(Qb->p, k, perm.p, rank, m, Wsel.p, rank);
+    CB(cublasDtrsm(cb, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, rank, m, &one,
+                   Delta.p, k, Wb->p, rank));
+    CB(cublasDtrsm(cb, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, rank, m, &one,
+                   Delta.p, k, Wsel.p, rank));
     Qb->alloc((size_t)m * rank);
     CK(cudaMemcpyAsync(Qb->p, Wsel.p, (size_t)m * rank * 8, cudaMemcpyDeviceToDevice, st));
     // lines 13-15
-    CB(cublasDgemv(cb, CUBLAS_OP_T, m, rank, &one, Wb->p, m, r.p, 1, &zero, gamma.p, 1));
-    CB(cublasDgemv(cb, CUBLAS_OP_N, m, rank, &one, Wb->p, m, gamma.p, 1, &one, lam.p, 1));
-    CB(cublasDgemv(cb, CUBLAS_OP_N, m, rank, &one, Qb->p, m, gamma.p, 1, &zero, tmp.p, 1));
+    CB(cublasDgemv(cb, CUBLAS_OP_N, rank, m, &one, Wb->p, rank, r.p, 1, &zero, gamma.p, 1));
+    CB(cublasDgemv(cb, CUBLAS_OP_T, rank, m, &one, Wb->p, rank, gamma.p, 1, &one, lam.p, 1));
+    CB(cublasDgemv(cb, CUBLAS_OP_T, rank, m, &one, Qb->p, rank, gamma.p, 1, &zero, tmp.p, 1));
     project(tmp.p, 1, m);
     k_axpy<<<grid_for(m), kThreads, 0, st>>>(m, -1.0, tmp.p, r.p);
     // line 16
-    apply_precond(r.p, z.p, Z.p);
+    apply_precond(r.p, z.p, Z.p, true);
     dots({{r.p, z.p}, {r.p, r.p}, {z.p, z.p}}, &sc.p->rz);
     CK(cudaMemcpyAsync(hs, sc.p, sizeof(Scal), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
@@ -1299,20 +1362,19 @@ int Ctx::solve_rrs(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_tra
     Qs.push_back(std::move(Qb));
     widths.push_back(rank);
     // line 17
-    k = Ns;
     CK(cudaMemcpyAsync(W.p, Z.p, (size_t)m * Ns * 8, cudaMemcpyDeviceToDevice, st));
-    project(W.p, Ns, m);
-    // lines 18-21: block classical Gram-Schmidt, `passes` passes
+    project_rm(W.p, Ns);
+    // lines 18-21: block classical Gram-Schmidt against all stored blocks, `passes` passes
     Psis.resize(Ws.size());
     for (size_t j = 0; j < Ws.size(); ++j)
       if (!Psis[j]) { Psis[j] = std::make_unique<DBuf<double>>(); Psis[j]->alloc((size_t)widths[j] * Ns); }
     for (int p = 0; p < passes; ++p) {
-      for (size_t j = 0; j < Ws.size(); ++j)
-        CB(cublasDgemm(cb, CUBLAS_OP_T, CUBLAS_OP_N, widths[j], Ns, m, &one, Qs[j]->p, m, W.p, m, &zero,
+      for (size_t j = 0; j < Ws.size(); ++j)  // Psi_j = Q_j^T W   (k_j x Ns)
+        CB(cublasDgemm(cb, CUBLAS_OP_N, CUBLAS_OP_T, widths[j], Ns, m, &one, Qs[j]->p, widths[j], W.p, Ns, &zero,
                        Psis[j]->p, widths[j]));
-      for (size_t j = 0; j < Ws.size(); ++j)
-        CB(cublasDgemm(cb, CUBLAS_OP_N, CUBLAS_OP_N, m, Ns, widths[j], &mone, Ws[j]->p, m, Psis[j]->p,
-                       widths[j], &one, W.p, m));
+      for (size_t j = 0; j < Ws.size(); ++j)  // W -= W_j Psi_j  ==  W^T -= Psi_j^T W_j^T
+        CB(cublasDgemm(cb, CUBLAS_OP_T, CUBLAS_OP_N, Ns, m, widths[j], &mone, Psis[j]->p, widths[j], Ws[j]->p,
+                       widths[j], &one, W.p, Ns));
     }
   }
   CK(cudaEventRecord(ev1, st));
@@ -1537,6 +1599,80 @@ int fetigpu_local_operator(fetigpu_ctx* ctx, int s, int* ns, int* dofs, double* 
     CK(cudaStreamSynchronize(c.st));
     for (int a = 0; a < n; ++a)
       for (int b = 0; b < n; ++b) F[(size_t)a * n + b] = tmp[(size_t)a * ld + b];
+  });
+}
+
+int fetigpu_apply_F_block_device(fetigpu_ctx* ctx, const double* W, int ldw, double* Q, int ldq, int k) {
+  return guarded([&] {
+    NEED_BUILT(ctx);
+    ctx->c.apply_F_block(W, ldw, Q, ldq, k);
+  });
+}
+
+int fetigpu_time_apply_block(fetigpu_ctx* ctx, const double* W, double* Q, int k, int reps, double* ms) {
+  return guarded([&] {
+    NEED_BUILT(ctx);
+    Ctx& c = ctx->c;
+    cudaEvent_t a, b;
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+    CK(cudaEventRecord(a, c.st));
+    for (int r = 0; r < reps; ++r) c.apply_F_block(W, k, Q, k, k);
+    CK(cudaEventRecord(b, c.st));
+    CK(cudaEventSynchronize(b));
+    float t = 0;
+    CK(cudaEventElapsedTime(&t, a, b));
+    ms[0] = t / reps;
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+  });
+}
+
+int fetigpu_fp64_peak(double* tflops_dmma, double* tflops_dfma) {
+  return guarded([&] {
+    int dev = 0, sms = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    double* out = nullptr;
+    CK(cudaMalloc(&out, 8));
+    cudaEvent_t a, b;
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+    const int iters = 20000, blocks = sms * 4;
+    for (int pass = 0; pass < 2; ++pass) {  // first pass warms up
+      CK(cudaEventRecord(a));
+      k_peak_dmma<<<blocks, 256>>>(out, iters);
+      CK(cudaEventRecord(b));
+      CK(cudaEventSynchronize(b));
+      float t = 0;
+      CK(cudaEventElapsedTime(&t, a, b));
+      *tflops_dmma = (double)blocks * 8 * iters * 8 * 512 / (t * 1e-3) / 1e12;
+      CK(cudaEventRecord(a));
+      k_peak_dfma<<<blocks, 256>>>(out, iters);
+      CK(cudaEventRecord(b));
+      CK(cudaEventSynchronize(b));
+      CK(cudaEventElapsedTime(&t, a, b));
+      *tflops_dfma = (double)blocks * 256 * iters * 8 * 2 / (t * 1e-3) / 1e12;
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFree(out);
+  });
+}
+
+int fetigpu_selftest_dmma(const double* A, const double* B, double* C) {
+  return guarded([&] {
+    double *dA, *dB, *dC;
+    CK(cudaMalloc(&dA, 32 * 8));
+    CK(cudaMalloc(&dB, 32 * 8));
+    CK(cudaMalloc(&dC, 64 * 8));
+    CK(cudaMemcpy(dA, A, 32 * 8, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dB, B, 32 * 8, cudaMemcpyHostToDevice));
+    k_dmma_selftest<<<1, 32>>>(dA, dB, dC);
+    CK(cudaMemcpy(C, dC, 64 * 8, cudaMemcpyDeviceToHost));
+    cudaFree(dA);
+    cudaFree(dB);
+    cudaFree(dC);
   });
 }
 

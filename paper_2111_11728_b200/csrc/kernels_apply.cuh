@@ -25,7 +25,7 @@ __global__ void __launch_bounds__(kThreads) k_gather_gemv_scatter(
     const OpSub* __restrict__ subs, const double* __restrict__ mats, const int* __restrict__ rows,
     const double* __restrict__ coefs, const double* __restrict__ x, double* __restrict__ y,
     double* __restrict__ zcols, int ldz, double* __restrict__ vbuf, const int* __restrict__ voff,
-    int ldx, int ldy) {
+    int ldx, int ldy, int zrs = 1) {
   extern __shared__ double xs[];
   const int s = blockIdx.x;
   const int col = blockIdx.y;
@@ -79,7 +79,7 @@ __global__ void __launch_bounds__(kThreads) k_gather_gemv_scatter(
           if (r >= 0) {
             const double c = cf[i * KR + k] * v;
             atomicAdd(yc + r, c);
-            if (zcols) zcols[(size_t)s * ldz + r] = c;
+            if (zcols) zcols[(size_t)s * ldz + (size_t)r * zrs] = c;
           }
         }
       }
@@ -172,7 +172,7 @@ __global__ void k_dp_phase2(const OpSub* __restrict__ subs, const DpSub* __restr
 __global__ void k_proj_gather(const OpSub* __restrict__ psubs, const int* __restrict__ rows,
                               const double* __restrict__ coefs, const double* __restrict__ RT,
                               const int* __restrict__ rt_off, const double* __restrict__ v, int ldv,
-                              double* __restrict__ g, int ldg, double sign) {
+                              double* __restrict__ g, int ldg, double sign, int rs = 1) {
   const int s = blockIdx.x, col = blockIdx.y;
   const OpSub d = psubs[s];
   const double* vc = v + (size_t)col * ldv;
@@ -182,7 +182,7 @@ __global__ void k_proj_gather(const OpSub* __restrict__ psubs, const int* __rest
     double xj = 0.0;
     for (int k = 0; k < 3; ++k) {
       const int r = rows[d.map_off + j * 3 + k];
-      if (r >= 0) xj += coefs[d.map_off + j * 3 + k] * vc[r];
+      if (r >= 0) xj += coefs[d.map_off + j * 3 + k] * vc[(size_t)r * rs];
     }
     a0 += R[j * 3] * xj;
     a1 += R[j * 3 + 1] * xj;
@@ -215,7 +215,7 @@ __global__ void k_small_gemm(const double* __restrict__ H, int n, const double* 
 __global__ void k_proj_scatter(const OpSub* __restrict__ psubs, const int* __restrict__ rows,
                                const double* __restrict__ coefs, const double* __restrict__ RT,
                                const int* __restrict__ rt_off, const double* __restrict__ h, int ldh,
-                               double* __restrict__ corr, int ldc) {
+                               double* __restrict__ corr, int ldc, int rs = 1) {
   const int s = blockIdx.x, col = blockIdx.y;
   const OpSub d = psubs[s];
   const double* R = RT + rt_off[s];
@@ -226,7 +226,7 @@ __global__ void k_proj_scatter(const OpSub* __restrict__ psubs, const int* __res
     const double v = R[j * 3] * h0 + R[j * 3 + 1] * h1 + R[j * 3 + 2] * h2;
     for (int k = 0; k < 3; ++k) {
       const int r = rows[d.map_off + j * 3 + k];
-      if (r >= 0) atomicAdd(cc + r, coefs[d.map_off + j * 3 + k] * v);
+      if (r >= 0) atomicAdd(cc + (size_t)r * rs, coefs[d.map_off + j * 3 + k] * v);
     }
   }
 }
@@ -501,6 +501,16 @@ __global__ void k_gather_cols(const double* __restrict__ in, int ld, const int* 
   const double* src = in + (size_t)perm[c] * ld;
   double* dst = out + (size_t)c * ld;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ld; i += gridDim.x * blockDim.x) dst[i] = src[i];
+}
+
+// row-major: out(i, c) = in(i, perm[c]) for c < cols
+__global__ void k_gather_cols_rm(const double* __restrict__ in, int ldi, const int* __restrict__ perm,
+                                 int cols, int m, double* __restrict__ out, int ldo) {
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < (long long)m * cols;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(idx / cols), c = (int)(idx - (long long)i * cols);
+    out[(size_t)i * ldo + c] = in[(size_t)i * ldi + perm[c]];
+  }
 }
 
 // mirror the lower triangle into the upper (Delta uses its lower triangle)

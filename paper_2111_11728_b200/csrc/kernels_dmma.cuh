@@ -1,0 +1,260 @@
+// kernels_dmma.cuh -- FP64 tensor-core (DMMA) kernels.
+//
+// On sm_100a the FP64 tensor path is mma.sync.m8n8k4.f64 (SASS DMMA); tcgen05
+// has no f64 kind.  K5: the block F-apply Q = F W for k
+// search directions (Alg. 1 line 7) as one batched GEMM per subdomain with the
+// B_s^T gather of W rows fused into the B-tile loader and the signed B_s
+// scatter fused into the epilogue; FETI-DP's coarse correction rides along
+// as n_c extra inner-dimension columns ([F_s | A_bc] [X_s ; U_s]).
+#pragma once
+
+#include "common.cuh"
+
+namespace fg {
+
+__device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// --------------------------------------------------------- self test --
+// C (8x8 row-major) = A (8x4 row-major) B (4x8 row-major) with the fragment
+// layout a = A[lane/4][lane%4], b = B[lane%4][lane/4],
+// (c0, c1) = C[lane/4][2(lane%4) + {0,1}].
+__global__ void k_dmma_selftest(const double* A, const double* B, double* C) {
+  const int lane = threadIdx.x & 31;
+  double d0 = 0.0, d1 = 0.0;
+  dmma_8x8x4(d0, d1, A[(lane >> 2) * 4 + (lane & 3)], B[(lane & 3) * 8 + (lane >> 2)]);
+  C[(lane >> 2) * 8 + 2 * (lane & 3)] = d0;
+  C[(lane >> 2) * 8 + 2 * (lane & 3) + 1] = d1;
+}
+
+// ------------------------------------------------------- FP64 peaks --
+// Sustained issue rate of independent DMMAs / DFMAs from registers.
+__global__ void __launch_bounds__(256) k_peak_dmma(double* out, int iters) {
+  double acc[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) acc[i] = 0.0;
+  double a = 1.0 + 1e-9 * threadIdx.x, b = 1.0 - 1e-9 * threadIdx.x;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) dmma_8x8x4(acc[2 * i], acc[2 * i + 1], a, b);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) s += acc[i];
+  if (s == 12345.678) out[0] = s;
+}
+__global__ void __launch_bounds__(256) k_peak_dfma(double* out, int iters) {
+  double acc[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) acc[i] = threadIdx.x * 1e-9 + i;
+  const double a = 0.999999, b = 1e-7;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[i] = fma(acc[i], a, b);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += acc[i];
+  if (s == 12345.678) out[0] = s;
+}
+
+// --------------------------------------------------- K5 block apply --
+// Row-major blocks: W(i, c) = W[i * ldw + c].  Per subdomain s, tile
+// (BM rows of F_s) x (BN columns of W), inner dimension n_s (+ n_c).
+constexpr int kBM = 128, kBN = 64, kBK = 16;
+constexpr int kApad = kBK + 4;   // 2 wavefronts per 8x4 A fragment load
+constexpr int kBpad = kBN + 8;   // 2 wavefronts per 4x8 B fragment load
+constexpr int kBlockSmem = (2 * kBM * kApad + 2 * kBK * kBpad) * 8;
+
+struct BlockApplyArgs {
+  const OpSub* subs;
+  const double* mats;
+  const int* rows;
+  const double* coefs;
+  int KR;
+  const DpSub* dps;      // nullable (T-FETI)
+  const double* abc;
+  const int* cmap;
+  const double* U;       // N_c x k row-major (coarse solution), nullable
+  int ldu;
+  const double* W;
+  int ldw;
+  double* Q;
+  int ldq;
+  int k;
+};
+
+template <int KR>
+__global__ void __launch_bounds__(256) k_block_apply(BlockApplyArgs a) {
+  extern __shared__ __align__(16) double dsm[];
+  double (*As)[kBM * kApad] = reinterpret_cast<double (*)[kBM * kApad]>(dsm);
+  double (*Bs)[kBK * kBpad] = reinterpret_cast<double (*)[kBK * kBpad]>(dsm + 2 * kBM * kApad);
+  const int s = blockIdx.z;
+  const OpSub d = a.subs[s];
+  const int ns = d.ns;
+  const int nc = a.dps ? a.dps[s].nc : 0;
+  const int kin = ns + nc;
+  const int row0 = blockIdx.y * kBM;
+  if (row0 >= ns) return;
+  const int col0 = blockIdx.x * kBN;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wr = warp >> 1, wc = warp & 1;         // 4 x 2 warps, warp tile 32 x 32
+  const double* F = a.mats + d.moff;
+  const int* rw = a.rows + d.map_off;
+  const double* cf = a.coefs + d.map_off;
+  const double* Abc = a.dps ? a.abc + a.dps[s].abc_off : nullptr;
+  const int* cm = a.dps ? a.cmap + a.dps[s].cmap_off : nullptr;
+
+  // tile loaders: A tile 128 x 16 (each thread 8 values), B tile 16 x 64 (4 values)
+  double ra[8], rb[4];
+  auto load_tiles = [&](int kk) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int idx = tid + q * 256;           // 0..2047
+      const int r = idx >> 4, c = idx & 15;
+      const int gi = row0 + r, gj = kk + c;
+      double v = 0.0;
+      if (gi < ns) {
+        if (gj < ns) v = F[(size_t)gi * d.ld + gj];
+        else if (gj < kin) v = Abc[(size_t)gi * nc + (gj - ns)];
+      }
+      ra[q] = v;
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int idx = tid + q * 256;           // 0..1023
+      const int r = idx >> 6, c = idx & 63;
+      const int gj = kk + r, gc = col0 + c;
+      double v = 0.0;
+      if (gc < a.k) {
+        if (gj < ns) {
+#pragma unroll
+          for (int t = 0; t < KR; ++t) {
+            const int row = rw[gj * KR + t];
+            if (row >= 0) v += cf[gj * KR + t] * a.W[(size_t)row * a.ldw + gc];
+          }
+        } else if (gj < kin) {
+          v = a.U[(size_t)cm[gj - ns] * a.ldu + gc];
+        }
+      }
+      rb[q] = v;
+    }
+  };
+  auto store_tiles = [&](int buf) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int idx = tid + q * 256;
+      As[buf][(idx >> 4) * kApad + (idx & 15)] = ra[q];
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int idx = tid + q * 256;
+      Bs[buf][(idx >> 6) * kBpad + (idx & 63)] = rb[q];
+    }
+  };
+
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  const int nk = (kin + kBK - 1) / kBK;
+  load_tiles(0);
+  store_tiles(0);
+  __syncthreads();
+  for (int t = 0; t < nk; ++t) {
+    const int buf = t & 1;
+    if (t + 1 < nk) load_tiles((t + 1) * kBK);
+    const double* A_ = As[buf];
+    const double* B_ = Bs[buf];
+#pragma unroll
+    for (int k4 = 0; k4 < kBK; k4 += 4) {
+      double af[4], bf[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        af[i] = A_[(wr * 32 + i * 8 + (lane >> 2)) * kApad + k4 + (lane & 3)];
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        bf[j] = B_[(k4 + (lane & 3)) * kBpad + wc * 32 + j * 8 + (lane >> 2)];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+    if (t + 1 < nk) store_tiles(buf ^ 1);
+    __syncthreads();
+  }
+  // epilogue: signed scatter of rows into Q (exactly two contributions per
+  // dual row overall -> order-independent atomics)
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int li = row0 + wr * 32 + i * 8 + (lane >> 2);
+    if (li >= ns) continue;
+#pragma unroll
+    for (int t = 0; t < KR; ++t) {
+      const int row = rw[li * KR + t];
+      if (row < 0) continue;
+      const double c = cf[li * KR + t];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int gc = col0 + wc * 32 + j * 8 + 2 * (lane & 3);
+        double* q = a.Q + (size_t)row * a.ldq + gc;
+        if (gc < a.k) atomicAdd(q, c * acc[i][j][0]);
+        if (gc + 1 < a.k) atomicAdd(q + 1, c * acc[i][j][1]);
+      }
+    }
+  }
+}
+
+// FETI-DP coarse pre-pass for a block: T_s = A_bc^T (B_s^T W)   (n_c x k)
+__global__ void __launch_bounds__(256) k_block_dp_t(const OpSub* __restrict__ subs,
+                                                    const DpSub* __restrict__ dps,
+                                                    const int* __restrict__ rows,
+                                                    const double* __restrict__ coefs,
+                                                    const double* __restrict__ abc,
+                                                    const double* __restrict__ W, int ldw, int k,
+                                                    double* __restrict__ tbuf, int ldt) {
+  const int s = blockIdx.y;
+  const OpSub d = subs[s];
+  const DpSub p = dps[s];
+  const int col = blockIdx.x * 64 + (threadIdx.x & 63);
+  const int grp = threadIdx.x >> 6;  // 4 groups split the inner range
+  __shared__ double red[4][8][64];
+  double acc[8] = {};
+  const double* Ab = abc + p.abc_off;
+  if (col < k) {
+    for (int j = grp; j < d.ns; j += 4) {
+      const int r = rows[d.map_off + j];
+      const double x = r >= 0 ? coefs[d.map_off + j] * W[(size_t)r * ldw + col] : 0.0;
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        if (c < p.nc) acc[c] = fma(Ab[(size_t)j * p.nc + c], x, acc[c]);
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < 8; ++c) red[grp][c][threadIdx.x & 63] = acc[c];
+  __syncthreads();
+  if (grp == 0 && col < k) {
+    for (int c = 0; c < p.nc; ++c)
+      tbuf[(size_t)(p.t_off + c) * ldt + col] =
+          red[0][c][threadIdx.x] + red[1][c][threadIdx.x] + red[2][c][threadIdx.x] + red[3][c][threadIdx.x];
+  }
+}
+
+// coarse block assembly in ascending subdomain order: T(i, :) = sum_owners tbuf
+__global__ void k_coarse_gather_block(const int* __restrict__ optr, const int* __restrict__ oidx,
+                                      const double* __restrict__ tbuf, int ldt, int nc, int k,
+                                      double* __restrict__ out, int ldo) {
+  const int i = blockIdx.y;
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < k; c += gridDim.x * blockDim.x) {
+    double v = 0.0;
+    for (int q = optr[i]; q < optr[i + 1]; ++q) v += tbuf[(size_t)oidx[q] * ldt + c];
+    out[(size_t)i * ldo + c] = v;
+  }
+}
+
+}  // namespace fg

@@ -77,7 +77,8 @@ EXPORTED = ["fetigpu_set_device", "fetigpu_create", "fetigpu_build", "fetigpu_de
             "fetigpu_project_device", "fetigpu_rhs", "fetigpu_solve", "fetigpu_recover",
             "fetigpu_local_operator", "fetigpu_device_alloc", "fetigpu_device_free",
             "fetigpu_host_alloc", "fetigpu_host_free", "fetigpu_memcpy", "fetigpu_fill_random",
-            "fetigpu_synchronize", "fetigpu_time_apply"]
+            "fetigpu_synchronize", "fetigpu_time_apply", "fetigpu_apply_F_block_device",
+            "fetigpu_time_apply_block", "fetigpu_fp64_peak", "fetigpu_selftest_dmma"]
 
 
 class FgProblem(C.Structure):
@@ -138,6 +139,21 @@ def check(rc: int):
     if rc != 0:
         msg = lib().fetigpu_last_error().decode()
         raise _ERRORS.get(rc, FetiError)(f"[{rc}] {msg}")
+
+
+def fp64_peak():
+    """(DMMA, DFMA) FP64 TFLOP/s measured on the current device."""
+    a, b = C.c_double(), C.c_double()
+    check(lib().fetigpu_fp64_peak(C.byref(a), C.byref(b)))
+    return a.value, b.value
+
+
+def dmma_selftest(A: np.ndarray, B: np.ndarray) -> np.ndarray:
+    A = np.ascontiguousarray(A, dtype=np.float64)
+    B = np.ascontiguousarray(B, dtype=np.float64)
+    Cm = np.zeros((8, 8))
+    check(lib().fetigpu_selftest_dmma(_p(A), _p(B), _p(Cm)))
+    return Cm
 
 
 def make_struct(prob: Problem, keep: list) -> FgProblem:
@@ -251,6 +267,27 @@ class FetiSystem:
         u = np.zeros((self.n_sub, self.local_dofs))
         check(lib().fetigpu_recover(self.h, _p(lam), _p(u)))
         return u
+
+    def apply_F_block(self, W: np.ndarray) -> np.ndarray:
+        """K5 block apply Q = F W on the device (W: m x k, row-major blocks)."""
+        W = np.ascontiguousarray(W, dtype=np.float64)
+        m, k = W.shape
+        L = lib()
+        nbytes = C.c_size_t(W.nbytes)
+        dW, dQ = C.c_void_p(), C.c_void_p()
+        check(L.fetigpu_device_alloc(self.h, nbytes, C.byref(dW)))
+        check(L.fetigpu_device_alloc(self.h, nbytes, C.byref(dQ)))
+        try:
+            Q = np.empty_like(W)
+            check(L.fetigpu_memcpy(self.h, dW, W.ctypes.data_as(C.c_void_p), nbytes, 1))
+            check(L.fetigpu_apply_F_block_device(self.h, C.cast(dW, D), C.c_int(k), C.cast(dQ, D),
+                                                 C.c_int(k), C.c_int(k)))
+            check(L.fetigpu_memcpy(self.h, Q.ctypes.data_as(C.c_void_p), dQ, nbytes, 2))
+            check(L.fetigpu_synchronize(self.h))
+        finally:
+            L.fetigpu_device_free(self.h, dW)
+            L.fetigpu_device_free(self.h, dQ)
+        return Q
 
     def local_operator(self, s: int):
         cap = 8 * self.prob.n

@@ -187,3 +187,32 @@ def test_dense_operator_C1(oracle_mod):
     assert rel(Fg, Fo) < 1e-10
     assert rel(Fg, Fg.T) < 1e-13          # symmetry
     assert np.linalg.eigvalsh(0.5 * (Fg + Fg.T)).min() > -1e-10 * np.abs(Fg).max()
+
+
+def test_dmma_fragment_layout():
+    from paper_2111_11728_b200 import engine
+    rng = np.random.default_rng(0)
+    A, B = rng.standard_normal((8, 4)), rng.standard_normal((4, 8))
+    Cm = engine.dmma_selftest(A, B)
+    assert np.abs(Cm - A @ B).max() < 1e-14
+
+
+def test_fp64_peak_reported():
+    from paper_2111_11728_b200 import engine
+    dmma, dfma = engine.fp64_peak()
+    print("FP64 peak TFLOP/s: DMMA %.1f DFMA %.1f" % (dmma, dfma))
+    assert dmma > 1.0 and dfma > 1.0
+
+
+@pytest.mark.parametrize("name", ["C1", "C1b", "C2s", "C3tf_s", "C3dp_s", "C5s", "C4s", "C1_dir_k"])
+@pytest.mark.parametrize("k", [1, 7, 64, 130])
+def test_block_apply(name, k, oracle_mod):
+    """K5 (DMMA block apply, fused gather/scatter) against the per-column GEMV
+    apply and the oracle."""
+    g, o, r = systems(name, oracle_mod)
+    W = np.random.default_rng(k).standard_normal((g.m, k))
+    Qb = g.apply_F_block(W)
+    Qc = g.apply_F(W)
+    for c in sorted({0, k // 2, k - 1}):
+        accurate(Qb[:, c], o.apply_F(W[:, c]), r.apply_F(W[:, c]), f"{name} block col{c}")
+    assert rel(Qb, Qc) <= max(1e-12, 10 * rel(o.apply_F(W[:, 0]), r.apply_F(W[:, 0])))
