@@ -268,6 +268,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-solves", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-block", action="store_true")
+    ap.add_argument("--block-k", type=int, default=2048)
+    ap.add_argument("--block-reps", type=int, default=3)
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -339,6 +342,30 @@ def main():
     t_e2e = max_over_ranks(dist, (time.perf_counter() - t0) / args.steps)
     e2e = st["op_bytes"] * total_steps / (t_e2e * args.steps) / 1e9
 
+    # ---- K5 block apply (Alg. 1 line 7) at the C4 block width k = N_s = 2048
+    block = None
+    if not args.no_block:
+        k = args.block_k
+        dW, dQ = C.c_void_p(), C.c_void_p()
+        engine.check(L.fetigpu_device_alloc(g.h, C.c_size_t(8 * m * k), C.byref(dW)))
+        engine.check(L.fetigpu_device_alloc(g.h, C.c_size_t(8 * m * k), C.byref(dQ)))
+        Wp, Qp = C.cast(dW, C.POINTER(C.c_double)), C.cast(dQ, C.POINTER(C.c_double))
+        engine.check(L.fetigpu_fill_random(g.h, Wp, C.c_size_t(m * k), C.c_ulonglong(99)))
+        bms = (C.c_double * 1)()
+        engine.check(L.fetigpu_time_apply_block(g.h, Wp, Qp, k, 1, bms))      # warm-up
+        barrier(dist)
+        engine.check(L.fetigpu_time_apply_block(g.h, Wp, Qp, k, args.block_reps, bms))
+        t_blk = max_over_ranks(dist, bms[0])
+        dmma, dfma = engine.fp64_peak()
+        flops = st["op_flops_per_col"] * k
+        tf = flops / (t_blk * 1e-3) / 1e12
+        block = {"k": k, "ms": t_blk, "flops": flops, "tflops": tf * ws, "peak_dmma_tflops": dmma,
+                 "peak_dfma_tflops": dfma, "frac": tf / dmma, "peak_kind": "measured (fetigpu_fp64_peak)",
+                 "kernel": "k_block_apply<1> (DMMA m8n8k4) + coarse pre-pass + cuBLAS DGEMM"}
+        L.fetigpu_device_free(g.h, dW)
+        L.fetigpu_device_free(g.h, dQ)
+        log("block", block)
+
     solves = None
     if rank == 0 and not args.no_solves:
         g.close()
@@ -383,6 +410,7 @@ def main():
             "build": {"ms": st["build_ms"], "nd_ms": st["nd_ms"], "slot_ms": st["slot_ms"],
                       "wall_s": build_wall},
             "cpu_baseline": cpu,
+            "block_apply": block,
             "solves": solves,
         }
         print(json.dumps(line), flush=True)

@@ -94,6 +94,11 @@ struct Ctx {
   int KR = 1;
   DBuf<OpSub> d_op;
   DBuf<double> d_opmat, d_opcoef, d_opfac;
+  // coefficients used with the explicit operators: all ones once the +-1
+  // constraint signs are folded into F_s / A_bc (FETI-DP), else d_opcoef
+  DBuf<double> d_opcoef_apply;
+  bool folded = false;
+  std::vector<std::vector<double>> slot_sign;
   DBuf<int> d_oprows, d_slot_of, d_fac_ne, d_top_pos, d_top_off;
   DBuf<long long> d_fac_off;
   std::vector<int> op_ns, op_ld;
@@ -167,6 +172,7 @@ struct Ctx {
                             kSmallFront * kSmallFront * 8));
     CK(cudaFuncSetAttribute(k_block_apply<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBlockSmem));
     CK(cudaFuncSetAttribute(k_block_apply<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBlockSmem));
+    CK(cudaFuncSetAttribute(k_block_apply_dp, cudaFuncAttributeMaxDynamicSharedMemorySize, kAsyncSmem));
   }
 
   double elapsed(cudaEvent_t a, cudaEvent_t b) {
@@ -619,6 +625,46 @@ struct Ctx {
       d_fbar.alloc(std::max(1, su.Nc));
       build_coarse(so, osub, oloc);
     }
+    // ---- fold the +-1 signs of the FETI-DP constraint rows into F_s and A_bc
+    d_opcoef_apply.upload(coef, st);
+    if (dp) {
+      const int nsl = (int)su.op_slots.size();
+      slot_sign.assign(nsl, {});
+      bool ok = true;
+      for (int s = 0; s < Ns && ok; ++s) {
+        const int sl = su.subs[s].op_slot;
+        std::vector<double> sg(op_ns[sl]);
+        for (int a = 0; a < op_ns[sl]; ++a) sg[a] = coef[ops[s].map_off + a];
+        if (slot_sign[sl].empty()) slot_sign[sl] = sg;
+        else if (slot_sign[sl] != sg) ok = false;
+      }
+      if (ok) {
+        std::vector<long long> ao(nsl);
+        std::vector<int> ncv(nsl), soff(nsl), nsv(nsl);
+        std::vector<double> sgn;
+        for (int i = 0; i < nsl; ++i) {
+          ao[i] = so.abc_off[i];
+          ncv[i] = (int)su.op_slots[i].src.size() - su.op_slots[i].ne;
+          soff[i] = (int)sgn.size();
+          nsv[i] = op_ns[i];
+          sgn.insert(sgn.end(), slot_sign[i].begin(), slot_sign[i].end());
+        }
+        DBuf<long long> dmo, dao;
+        DBuf<int> dns, dld, dnc, dso;
+        DBuf<double> dsg;
+        dmo.upload(op_moff, st); dao.upload(ao, st); dns.upload(nsv, st); dld.upload(op_ld, st);
+        dnc.upload(ncv, st); dso.upload(soff, st); dsg.upload(sgn, st);
+        k_fold_signs<<<dim3(64, nsl), kThreads, 0, st>>>(dmo.p, dns.p, dld.p, dao.p, dnc.p, dso.p, dsg.p,
+                                                        d_opmat.p, d_abc.p);
+        LAUNCH_CHECK();
+        std::vector<double> ones(coef.size(), 1.0);
+        for (size_t i = 0; i < rows.size(); ++i)
+          if (rows[i] < 0) ones[i] = 0.0;
+        d_opcoef_apply.upload(ones, st);
+        CK(cudaStreamSynchronize(st));
+        folded = true;
+      }
+    }
     // ---- scratch
     const size_t m = std::max(1, su.m);
     d_v1.alloc(m); d_v2.alloc(m); d_v3.alloc(m);
@@ -715,20 +761,20 @@ struct Ctx {
       for (int c = 0; c < ncols; ++c) CK(cudaMemsetAsync(y + (size_t)c * ldy, 0, su.m * 8, st));
       dim3 grid(Ns, ncols);
       k_gather_gemv_scatter<3, false><<<grid, kThreads, max_ld * 8, st>>>(
-          d_op.p, d_opmat.p, d_oprows.p, d_opcoef.p, x, y, nullptr, 0, nullptr, nullptr, ldx, ldy);
+          d_op.p, d_opmat.p, d_oprows.p, d_opcoef_apply.p, x, y, nullptr, 0, nullptr, nullptr, ldx, ldy);
       LAUNCH_CHECK();
     } else {
       for (int c = 0; c < ncols; ++c) {
         const double* xc = x + (size_t)c * ldx;
         double* yc = y + (size_t)c * ldy;
         k_gather_gemv_scatter<1, true><<<Ns, kThreads, max_ld * 8, st>>>(
-            d_op.p, d_opmat.p, d_oprows.p, d_opcoef.p, xc, nullptr, nullptr, 0, d_vbuf.p, d_voff.p, ldx, 0);
-        k_dp_t<<<Ns, kThreads, 0, st>>>(d_op.p, d_dp.p, d_oprows.p, d_opcoef.p, d_abc.p, xc, d_tbuf.p);
+            d_op.p, d_opmat.p, d_oprows.p, d_opcoef_apply.p, xc, nullptr, nullptr, 0, d_vbuf.p, d_voff.p, ldx, 0);
+        k_dp_t<<<Ns, kThreads, 0, st>>>(d_op.p, d_dp.p, d_oprows.p, d_opcoef_apply.p, d_abc.p, xc, d_tbuf.p);
         k_coarse_gather<<<grid_for(su.Nc), kThreads, 0, st>>>(d_optr.p, d_oidx.p, d_tbuf.p, su.Nc, d_g.p,
                                                              1.0, nullptr);
         k_dense_gemv<<<grid_for((long long)su.Nc * 32), kThreads, 0, st>>>(d_Kinv.p, su.Nc, d_g.p, d_h.p);
         CK(cudaMemsetAsync(yc, 0, su.m * 8, st));
-        k_dp_phase2<<<Ns, kThreads, 0, st>>>(d_op.p, d_dp.p, d_oprows.p, d_opcoef.p, d_abc.p, d_cmap.p,
+        k_dp_phase2<<<Ns, kThreads, 0, st>>>(d_op.p, d_dp.p, d_oprows.p, d_opcoef_apply.p, d_abc.p, d_cmap.p,
                                              d_h.p, d_vbuf.p, yc, 1.0);
         LAUNCH_CHECK();
       }
@@ -756,7 +802,7 @@ struct Ctx {
     const int Ns = su.Ns, m = su.m;
     if (ldq == k) CK(cudaMemsetAsync(Q, 0, (size_t)m * k * 8, st));
     else CK(cudaMemset2DAsync(Q, (size_t)ldq * 8, 0, (size_t)k * 8, m, st));
-    BlockApplyArgs a{d_op.p, d_opmat.p, d_oprows.p, d_opcoef.p, KR, nullptr, nullptr, nullptr, nullptr, 0,
+    BlockApplyArgs a{d_op.p, d_opmat.p, d_oprows.p, d_opcoef_apply.p, KR, nullptr, nullptr, nullptr, nullptr, 0,
                      W, ldw, Q, ldq, k};
     int max_ns = 0;
     for (int n : op_ns) max_ns = std::max(max_ns, n);
@@ -766,7 +812,7 @@ struct Ctx {
       for (auto& S : su.subs) tot_c += (int)S.c.size();
       if (blk_t.n < (size_t)tot_c * k) blk_t.alloc((size_t)tot_c * k);
       if (blk_T.n < (size_t)Nc * k) { blk_T.alloc((size_t)Nc * k); blk_U.alloc((size_t)Nc * k); }
-      k_block_dp_t<<<dim3((k + 63) / 64, Ns), 256, 0, st>>>(d_op.p, d_dp.p, d_oprows.p, d_opcoef.p, d_abc.p, W,
+      k_block_dp_t<<<dim3((k + 63) / 64, Ns), 256, 0, st>>>(d_op.p, d_dp.p, d_oprows.p, d_opcoef_apply.p, d_abc.p, W,
                                                              ldw, k, blk_t.p, k);
       k_coarse_gather_block<<<dim3((k + 255) / 256, Nc), 256, 0, st>>>(d_optr.p, d_oidx.p, blk_t.p, k, Nc, k,
                                                                        blk_T.p, k);
@@ -777,7 +823,10 @@ struct Ctx {
       max_ns += 8;
     }
     dim3 grid((k + kBN - 1) / kBN, (max_ns + kBM - 1) / kBM, Ns);
-    if (KR == 1) k_block_apply<1><<<grid, 256, kBlockSmem, st>>>(a);
+    const bool fast = folded && (k % 2 == 0) && (ldw % 2 == 0) && (ldq % 2 == 0) &&
+                      ((uintptr_t)W % 16 == 0) && ((uintptr_t)Q % 16 == 0);
+    if (fast) k_block_apply_dp<<<grid, 256, kAsyncSmem, st>>>(a);
+    else if (KR == 1) k_block_apply<1><<<grid, 256, kBlockSmem, st>>>(a);
     else k_block_apply<3><<<grid, 256, kBlockSmem, st>>>(a);
     LAUNCH_CHECK();
   }
@@ -871,7 +920,7 @@ struct Ctx {
                                                            1.0, nullptr);
       k_dense_gemv<<<grid_for((long long)su.Nc * 32), kThreads, 0, st>>>(d_Kinv.p, su.Nc, d_fbar.p, d_h.p);
       CK(cudaMemsetAsync(d_v2.p, 0, m * 8, st));
-      k_dp_phase2<<<su.Ns, kThreads, 0, st>>>(d_op.p, d_dp.p, d_oprows.p, d_opcoef.p, d_abc.p, d_cmap.p, d_h.p,
+      k_dp_phase2<<<su.Ns, kThreads, 0, st>>>(d_op.p, d_dp.p, d_oprows.p, d_opcoef_apply.p, d_abc.p, d_cmap.p, d_h.p,
                                               nullptr, d_v2.p, 0.0);
       k_sub<<<grid_for(m), kThreads, 0, st>>>(m, d_v1.p, d_v2.p, d_d.p);
       CK(cudaMemsetAsync(d_lam0.p, 0, m * 8, st));
@@ -897,7 +946,7 @@ struct Ctx {
       launch_bnd_rhs(lambda_dev, nullptr);
     } else {
       // u_c = Kbar^{-1} (fbar_c + F_rc^T lambda)
-      k_dp_t<<<Ns, kThreads, 0, st>>>(d_op.p, d_dp.p, d_oprows.p, d_opcoef.p, d_abc.p, lambda_dev, d_tbuf.p);
+      k_dp_t<<<Ns, kThreads, 0, st>>>(d_op.p, d_dp.p, d_oprows.p, d_opcoef_apply.p, d_abc.p, lambda_dev, d_tbuf.p);
       k_coarse_gather<<<grid_for(su.Nc), kThreads, 0, st>>>(d_optr.p, d_oidx.p, d_tbuf.p, su.Nc, d_g.p, 1.0,
                                                            d_fbar.p);
       uc.alloc(std::max(1, su.Nc));
@@ -1598,7 +1647,10 @@ int fetigpu_local_operator(fetigpu_ctx* ctx, int s, int* ns, int* dofs, double* 
     CK(cudaMemcpyAsync(tmp.data(), c.d_opmat.p + c.op_moff[sl], tmp.size() * 8, cudaMemcpyDeviceToHost, c.st));
     CK(cudaStreamSynchronize(c.st));
     for (int a = 0; a < n; ++a)
-      for (int b = 0; b < n; ++b) F[(size_t)a * n + b] = tmp[(size_t)a * ld + b];
+      for (int b = 0; b < n; ++b) {
+        const double sg = c.folded ? c.slot_sign[sl][a] * c.slot_sign[sl][b] : 1.0;
+        F[(size_t)a * n + b] = sg * tmp[(size_t)a * ld + b];
+      }
   });
 }
 
@@ -1733,11 +1785,11 @@ int fetigpu_time_apply(fetigpu_ctx* ctx, const double* x, double* y, int ncols, 
       for (int col = 0; col < ncols; ++col) {
         if (c.su.method == FETIGPU_TFETI)
           k_gather_gemv_scatter<3, false><<<dim3(c.su.Ns, 1), kThreads, c.max_ld * 8, c.st>>>(
-              c.d_op.p, c.d_opmat.p, c.d_oprows.p, c.d_opcoef.p, x + (size_t)col * c.su.m,
+              c.d_op.p, c.d_opmat.p, c.d_oprows.p, c.d_opcoef_apply.p, x + (size_t)col * c.su.m,
               y + (size_t)col * c.su.m, nullptr, 0, nullptr, nullptr, c.su.m, c.su.m);
         else
           k_gather_gemv_scatter<1, true><<<c.su.Ns, kThreads, c.max_ld * 8, c.st>>>(
-              c.d_op.p, c.d_opmat.p, c.d_oprows.p, c.d_opcoef.p, x + (size_t)col * c.su.m, nullptr, nullptr, 0,
+              c.d_op.p, c.d_opmat.p, c.d_oprows.p, c.d_opcoef_apply.p, x + (size_t)col * c.su.m, nullptr, nullptr, 0,
               c.d_vbuf.p, c.d_voff.p, c.su.m, 0);
       }
       CK(cudaEventRecord(ev[2 * r + 1], c.st));

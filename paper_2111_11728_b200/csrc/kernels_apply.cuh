@@ -522,6 +522,28 @@ __global__ void k_mirror_lower(double* A, int n) {
   }
 }
 
+// Fold the +-1 constraint signs of a FETI-DP slot into its explicit operators:
+// F'' = S F S (row-major ns x ld), A'' = S A_bc (ns x nc).  Exact.
+__global__ void k_fold_signs(const long long* __restrict__ moff, const int* __restrict__ ns_,
+                             const int* __restrict__ ld_, const long long* __restrict__ aoff,
+                             const int* __restrict__ nc_, const int* __restrict__ soff,
+                             const double* __restrict__ sgn, double* __restrict__ mats,
+                             double* __restrict__ abc) {
+  const int sl = blockIdx.y;
+  const int ns = ns_[sl], ld = ld_[sl], nc = nc_[sl];
+  const double* sg = sgn + soff[sl];
+  double* M = mats + moff[sl];
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < ns * ns; idx += gridDim.x * blockDim.x) {
+    const int i = idx / ns, j = idx - i * ns;
+    M[(size_t)i * ld + j] *= sg[i] * sg[j];
+  }
+  if (abc) {
+    double* A = abc + aoff[sl];
+    for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < ns * nc; idx += gridDim.x * blockDim.x)
+      A[idx] *= sg[idx / nc];
+  }
+}
+
 // L2 flush helper: write a buffer larger than L2
 __global__ void k_flush(double* buf, size_t n, double v) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;

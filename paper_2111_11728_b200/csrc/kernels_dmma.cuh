@@ -210,6 +210,117 @@ __global__ void __launch_bounds__(256) k_block_apply(BlockApplyArgs a) {
   }
 }
 
+// --------------------- K5, FETI-DP fast path: cp.async multistage pipeline --
+// Requires sign-folded operators (F'' = S F S, A'' = S A_bc with S = diag of
+// the +-1 B_s entries; exact) so the gather/scatter are unsigned, KR = 1, and
+// k, ldw, ldu even.  A tile rows (F'' rows / A'' rows) and B tile rows
+// (W rows / U rows) are contiguous 16-byte chunks copied straight into shared
+// memory; out-of-range chunks are zero-filled.
+constexpr int kStages = 3;
+constexpr int kAsyncSmem = (kStages * (kBM * kApad + kBK * kBpad)) * 8 + (512 + 16) * 4;
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  const int n = valid ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(n));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+__global__ void __launch_bounds__(256, 2) k_block_apply_dp(BlockApplyArgs a) {
+  extern __shared__ __align__(16) double dsm[];
+  double* As = dsm;                                   // kStages x (kBM x kApad)
+  double* Bs = dsm + kStages * kBM * kApad;           // kStages x (kBK x kBpad)
+  int* srow = reinterpret_cast<int*>(Bs + kStages * kBK * kBpad);
+  const int s = blockIdx.z;
+  const OpSub d = a.subs[s];
+  const int ns = d.ns;
+  const DpSub p = a.dps[s];
+  const int nc = p.nc;
+  const int kin = ns + nc;
+  const int row0 = blockIdx.y * kBM;
+  if (row0 >= ns) return;
+  const int col0 = blockIdx.x * kBN;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wr = warp >> 1, wc = warp & 1;
+  const double* F = a.mats + d.moff;
+  const double* Abc = a.abc + p.abc_off;
+  const int* rw = a.rows + d.map_off;
+  for (int j = tid; j < kin; j += 256) srow[j] = j < ns ? rw[j] : a.cmap[p.cmap_off + j - ns];
+  __syncthreads();
+  const int nk = (kin + kBK - 1) / kBK;
+  auto issue = [&](int t) {
+    const int kk = t * kBK, st = t % kStages;
+    double* A_ = As + st * kBM * kApad;
+    double* B_ = Bs + st * kBK * kBpad;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {        // A: 128 rows x 8 chunks
+      const int idx = tid + q * 256;
+      const int r = idx >> 3, c2 = (idx & 7) * 2;
+      const int gi = row0 + r, gj = kk + c2;
+      const double* src = F;
+      bool ok = gi < ns && gj < kin;
+      if (ok) src = gj < ns ? F + (size_t)gi * d.ld + gj : Abc + (size_t)gi * nc + (gj - ns);
+      cp_async16(A_ + r * kApad + c2, src, ok);
+    }
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {        // B: 16 rows x 32 chunks
+      const int idx = tid + q * 256;
+      const int r = idx >> 5, c2 = (idx & 31) * 2;
+      const int gj = kk + r, gc = col0 + c2;
+      const double* src = a.W;
+      bool ok = gj < kin && gc < a.k;
+      if (ok) src = gj < ns ? a.W + (size_t)srow[gj] * a.ldw + gc : a.U + (size_t)srow[gj] * a.ldu + gc;
+      cp_async16(B_ + r * kBpad + c2, src, ok);
+    }
+  };
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+#pragma unroll
+  for (int t = 0; t < kStages - 1; ++t) {
+    if (t < nk) issue(t);
+    cp_async_commit();
+  }
+  for (int t = 0; t < nk; ++t) {
+    cp_async_wait<kStages - 2>();
+    __syncthreads();
+    if (t + kStages - 1 < nk) issue(t + kStages - 1);
+    cp_async_commit();
+    const double* A_ = As + (t % kStages) * kBM * kApad;
+    const double* B_ = Bs + (t % kStages) * kBK * kBpad;
+#pragma unroll
+    for (int k4 = 0; k4 < kBK; k4 += 4) {
+      double af[4], bf[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) af[i] = A_[(wr * 32 + i * 8 + (lane >> 2)) * kApad + k4 + (lane & 3)];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bf[j] = B_[(k4 + (lane & 3)) * kBpad + wc * 32 + j * 8 + (lane >> 2)];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+  }
+  cp_async_wait<0>();
+  // unsigned scatter: two contributions per dual row -> order-independent
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int li = row0 + wr * 32 + i * 8 + (lane >> 2);
+    if (li >= ns) continue;
+    double* qrow = a.Q + (size_t)srow[li] * a.ldq;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int gc = col0 + wc * 32 + j * 8 + 2 * (lane & 3);
+      if (gc < a.k) atomicAdd(qrow + gc, acc[i][j][0]);
+      if (gc + 1 < a.k) atomicAdd(qrow + gc + 1, acc[i][j][1]);
+    }
+  }
+}
+
 // FETI-DP coarse pre-pass for a block: T_s = A_bc^T (B_s^T W)   (n_c x k)
 __global__ void __launch_bounds__(256) k_block_dp_t(const OpSub* __restrict__ subs,
                                                     const DpSub* __restrict__ dps,
@@ -218,6 +329,7 @@ __global__ void __launch_bounds__(256) k_block_dp_t(const OpSub* __restrict__ su
                                                     const double* __restrict__ abc,
                                                     const double* __restrict__ W, int ldw, int k,
                                                     double* __restrict__ tbuf, int ldt) {
+  // (coefs are the apply coefficients: unit when the operators are sign-folded)
   const int s = blockIdx.y;
   const OpSub d = subs[s];
   const DpSub p = dps[s];
