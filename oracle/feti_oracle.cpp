@@ -1491,6 +1491,54 @@ double fo_admissibility_error(void* h) {
   }
   return err;
 }
+// K^s x for one subdomain (assembled local stiffness, fem.cpp:86-119)
+int fo_local_apply(void* h, int s, const double* x, double* y) {
+  auto* o = static_cast<Oracle*>(h);
+  if (s < 0 || s >= o->Ns) return InvalidArgument;
+  o->subs[s].K.matvec(x, y);
+  return 0;
+}
+// T-FETI: max_i |(G lambda - e)_i| over all rows (constraint_residual_inf,
+// decomposition.hpp:141-142)
+double fo_coarse_residual(void* h, const double* lambda) {
+  auto* o = static_cast<Oracle*>(h);
+  if (o->P.method != 0) return 0.0;
+  double mx = 0.0;
+  for (int a = 0; a < 3 * o->Ns; ++a) {
+    double v = dot_(o->Gt.col(a), lambda, o->m) - o->e[a];
+    mx = std::max(mx, std::abs(v));
+  }
+  return mx;
+}
+// pseudo_solve with the compatibility check (linalg.cpp:191-204)
+int fo_pseudo_solve(void* h, int s, const double* rhs, double* x) {
+  auto* o = static_cast<Oracle*>(h);
+  return guarded([&] {
+    if (o->P.method != 0) fail(ConfigError, "pseudo_solve needs T-FETI factors");
+    Sub& S = o->subs[s];
+    double rn = 0.0;
+    for (int i = 0; i < o->nloc; ++i) rn += rhs[i] * rhs[i];
+    rn = std::sqrt(rn);
+    for (int c = 0; c < 3; ++c) {
+      double pr = 0.0, nr = 0.0;
+      for (int i = 0; i < o->nloc; ++i) { pr += o->R(i, c) * rhs[i]; nr += o->R(i, c) * o->R(i, c); }
+      if (std::abs(pr) > 1e-8 * rn * std::sqrt(nr))
+        fail(IncompatibleRhs, "rhs has a nullspace component: |R^T rhs| = " + std::to_string(std::abs(pr)));
+    }
+    std::vector<double> b(S.keep.size());
+    for (size_t i = 0; i < S.keep.size(); ++i) b[i] = rhs[S.keep[i]];
+    S.kred.solve(b.data());
+    for (int i = 0; i < o->nloc; ++i) x[i] = 0.0;
+    for (size_t i = 0; i < S.keep.size(); ++i) x[S.keep[i]] = b[i];
+  });
+}
+int fo_fixed_dofs(void* h, int* out) {
+  auto* o = static_cast<Oracle*>(h);
+  if (o->P.method != 0) return ConfigError;
+  for (int i = 0; i < 3; ++i) out[i] = o->subs[0].fixed[i];
+  return 0;
+}
+
 int fo_direct_solve(void* h, double* u) {
   return guarded([&] { static_cast<Oracle*>(h)->direct(u); });
 }

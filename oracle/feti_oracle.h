@@ -100,6 +100,10 @@ double fo_admissibility_error(void* h);
 /* global direct oracle: merged global DOFs, band Cholesky;
  * u is written per subdomain copy (N_s * local DOFs). */
 int fo_direct_solve(void* h, double* u);
+int fo_local_apply(void* h, int s, const double* x, double* y);
+double fo_coarse_residual(void* h, const double* lambda);
+int fo_pseudo_solve(void* h, int s, const double* rhs, double* x);
+int fo_fixed_dofs(void* h, int* out);
 
 /* kernel-level entry points for the SPEC examples */
 int fo_simp_modulus(double rho, double E0, double Emin, double p, double* out);

@@ -63,12 +63,9 @@ def lib():
         L = C.CDLL(_LIB_PATH)
         L.fo_last_error.restype = C.c_char_p
         L.fo_admissibility_error.restype = C.c_double
+        L.fo_coarse_residual.restype = C.c_double
         L.fo_create.argtypes = [C.POINTER(FoProblem), C.POINTER(C.c_void_p)]
         L.fo_destroy.argtypes = [C.c_void_p]
-        for name in ("fo_info", "fo_rows", "fo_apply_F", "fo_apply_precond", "fo_project",
-                     "fo_rhs", "fo_solve", "fo_recover", "fo_local_diag", "fo_load_vectors",
-                     "fo_admissibility_error", "fo_direct_solve"):
-            getattr(L, name).argtypes = None
         _lib = L
     return _lib
 
@@ -192,6 +189,27 @@ class Oracle:
 
     def admissibility_error(self) -> float:
         return float(lib().fo_admissibility_error(self.h))
+
+    def local_apply(self, s: int, x: np.ndarray) -> np.ndarray:
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        y = np.zeros(self.local_dofs)
+        _check(lib().fo_local_apply(self.h, s, _p(x), _p(y)))
+        return y
+
+    def coarse_residual(self, lam: np.ndarray) -> float:
+        lam = np.ascontiguousarray(lam, dtype=np.float64)
+        return float(lib().fo_coarse_residual(self.h, _p(lam)))
+
+    def pseudo_solve(self, s: int, rhs: np.ndarray) -> np.ndarray:
+        rhs = np.ascontiguousarray(rhs, dtype=np.float64)
+        x = np.zeros(self.local_dofs)
+        _check(lib().fo_pseudo_solve(self.h, s, _p(rhs), _p(x)))
+        return x
+
+    def fixed_dofs(self):
+        out = np.zeros(3, dtype=np.int32)
+        _check(lib().fo_fixed_dofs(self.h, _p(out)))
+        return out.tolist()
 
     def direct(self) -> np.ndarray:
         u = np.zeros((self.n_sub, self.local_dofs))
