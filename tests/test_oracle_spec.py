@@ -181,8 +181,8 @@ def test_mbb_geometry(oracle_mod):
         assert o.m == g[key] and o.m + o.n_c > 10000   # FETI-DP: 9,976 dual + 234 primal
         if method == 0:
             assert o.n_iface == g["tfeti_iface"]
-        if method == 1:
-            assert o.n_c == g["fetidp_nc"]
+        if method == 1:   # 234 corner DOFs minus the 4 pinned (eliminated)
+            assert o.n_c == g["fetidp_nc"] - 4
 
 
 def test_constraint_counts(oracle_mod):
