@@ -104,6 +104,8 @@ struct Ctx {
   std::vector<int> op_ns, op_ld;
   std::vector<long long> op_moff, op_foff;
   int max_ld = 0, max_ne = 0;
+  int rsplit = 1;     // CTAs per subdomain in the GEMV kernels (few subdomains)
+  int pc_rsplit = 1;
   // slot src/ext lists
   DBuf<int> d_op_src, d_op_ext, d_op_src_off, d_op_ext_off;
   // preconditioner
@@ -127,6 +129,7 @@ struct Ctx {
   // scratch vectors
   DBuf<double> d_v1, d_v2, d_v3, d_g, d_h, d_partial;
   DBuf<double> d_d, d_lam0;
+  DBuf<unsigned int> d_counter;
   bool have_rhs = false;
   // stats
   double op_bytes = 0, op_flops = 0, main_bytes = 0;
@@ -670,8 +673,13 @@ struct Ctx {
     d_v1.alloc(m); d_v2.alloc(m); d_v3.alloc(m);
     d_g.alloc(3 * (size_t)Ns + 8); d_h.alloc(3 * (size_t)Ns + 8);
     d_partial.alloc(4 * kDotBlocks);
+    d_counter.alloc(1);
+    d_counter.zero(st);
     d_d.alloc(m); d_lam0.alloc(m);
 
+    // ---- GEMV row split: aim for >= 4 CTAs per SM when subdomains are few
+    rsplit = std::max(1, std::min(8, (4 * 148 + Ns - 1) / Ns));
+    pc_rsplit = rsplit;
     // ---- work per apply
     double sn2 = 0, snc = 0, sns = 0;
     for (int s = 0; s < Ns; ++s) {
@@ -759,7 +767,7 @@ struct Ctx {
     const int Ns = su.Ns;
     if (su.method == FETIGPU_TFETI) {
       for (int c = 0; c < ncols; ++c) CK(cudaMemsetAsync(y + (size_t)c * ldy, 0, su.m * 8, st));
-      dim3 grid(Ns, ncols);
+      dim3 grid(Ns, ncols, rsplit);
       k_gather_gemv_scatter<3, false><<<grid, kThreads, max_ld * 8, st>>>(
           d_op.p, d_opmat.p, d_oprows.p, d_opcoef_apply.p, x, y, nullptr, 0, nullptr, nullptr, ldx, ldy);
       LAUNCH_CHECK();
@@ -767,7 +775,7 @@ struct Ctx {
       for (int c = 0; c < ncols; ++c) {
         const double* xc = x + (size_t)c * ldx;
         double* yc = y + (size_t)c * ldy;
-        k_gather_gemv_scatter<1, true><<<Ns, kThreads, max_ld * 8, st>>>(
+        k_gather_gemv_scatter<1, true><<<dim3(Ns, 1, rsplit), kThreads, max_ld * 8, st>>>(
             d_op.p, d_opmat.p, d_oprows.p, d_opcoef_apply.p, xc, nullptr, nullptr, 0, d_vbuf.p, d_voff.p, ldx, 0);
         k_dp_t<<<Ns, kThreads, 0, st>>>(d_op.p, d_dp.p, d_oprows.p, d_opcoef_apply.p, d_abc.p, xc, d_tbuf.p);
         k_coarse_gather<<<grid_for(su.Nc), kThreads, 0, st>>>(d_optr.p, d_oidx.p, d_tbuf.p, su.Nc, d_g.p,
@@ -788,10 +796,10 @@ struct Ctx {
     if (Zcols) CK(cudaMemsetAsync(Zcols, 0, (size_t)su.m * su.Ns * 8, st));
     const int ldz = row_major ? 1 : su.m, zrs = row_major ? su.Ns : 1;
     if (KRp == 1)
-      k_gather_gemv_scatter<1, false><<<su.Ns, kThreads, max_pc_ld * 8, st>>>(
+      k_gather_gemv_scatter<1, false><<<dim3(su.Ns, 1, pc_rsplit), kThreads, max_pc_ld * 8, st>>>(
           d_pc.p, d_pcmat.p, d_pcrows.p, d_pccoef.p, r, z, Zcols, ldz, nullptr, nullptr, 0, 0, zrs);
     else
-      k_gather_gemv_scatter<3, false><<<su.Ns, kThreads, max_pc_ld * 8, st>>>(
+      k_gather_gemv_scatter<3, false><<<dim3(su.Ns, 1, pc_rsplit), kThreads, max_pc_ld * 8, st>>>(
           d_pc.p, d_pcmat.p, d_pcrows.p, d_pccoef.p, r, z, Zcols, ldz, nullptr, nullptr, 0, 0, zrs);
     LAUNCH_CHECK();
   }
@@ -975,8 +983,8 @@ struct Ctx {
     for (auto& p : pairs) { a.a[k] = p.first; a.b[k] = p.second; ++k; }
     a.npairs = k;
     a.n = su.m;
-    k_dot_partial<<<kDotBlocks, kThreads, 0, st>>>(a, d_partial.p);
-    k_dot_final<<<1, 32 * k, 0, st>>>(d_partial.p, k, out);
+    const int nblk = std::max(1, std::min(kDotBlocks, (su.m + 4 * kThreads - 1) / (4 * kThreads)));
+    k_dot_fused<<<nblk, kThreads, 0, st>>>(a, d_partial.p, d_counter.p, out);
     LAUNCH_CHECK();
   }
 
@@ -1203,6 +1211,9 @@ void Ctx::launch_add_rigid(double* u, const double* alpha) {
 // pcg single / FO: z = P Fbar^{-1} P r, eps_r = sqrt(r^T z)
 // (PAPER.md:384); FO keeps F-normalized directions and re-orthogonalizes by
 // classical Gram-Schmidt with `reorth_passes` passes.
+// The whole iteration is device resident (scalars in device memory, breakdown
+// flagged on the device) and captured once into a CUDA graph; the host
+// replays it and reads back one 64-byte scalar record per iteration.
 int Ctx::solve(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_trace* tr) {
   if (o.directions == FETIGPU_RRS) return solve_rrs(o, lambda_host, tr);
   const int m = su.m;
@@ -1211,13 +1222,17 @@ int Ctx::solve(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_trace* 
   rhs();
   DBuf<double> lam, r, z, w, q, corr, Wst, Qst, psi;
   DBuf<Scal> sc;
+  DBuf<int> cnt;
   lam.alloc(m); r.alloc(m); z.alloc(m); w.alloc(m); q.alloc(m); corr.alloc(m);
   sc.alloc(1);
   sc.zero(st);
+  cnt.alloc(1);
+  cnt.zero(st);
+  const int cap = std::max(1, o.max_it);
   if (fo) {
-    Wst.alloc((size_t)m * std::max(1, o.max_it));
-    Qst.alloc((size_t)m * std::max(1, o.max_it));
-    psi.alloc(std::max(1, o.max_it));
+    Wst.alloc((size_t)m * cap);
+    Qst.alloc((size_t)m * cap);
+    psi.alloc(cap);
   }
   Scal* hs = nullptr;
   CK(cudaMallocHost(&hs, sizeof(Scal)));
@@ -1231,6 +1246,7 @@ int Ctx::solve(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_trace* 
   project(r.p, 1, m);
   precond_projected(r.p, z.p, nullptr);
   dots({{r.p, z.p}, {r.p, r.p}, {z.p, z.p}}, &sc.p->rz);
+  k_shift_rz<<<1, 1, 0, st>>>(sc.p);
   CK(cudaMemcpyAsync(hs, sc.p, sizeof(Scal), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   auto metric = [&](const Scal& s) {
@@ -1239,7 +1255,7 @@ int Ctx::solve(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_trace* 
     return std::sqrt(std::max(s.rz, 0.0));
   };
   const double eps0 = metric(*hs);
-  double eps = eps0, rz_old = hs->rz;
+  double eps = eps0;
   int it = 0, status = FETIGPU_MAX_ITER;
   auto push = [&](double e, int kept) {
     if (tr && it < tr->cap) {
@@ -1251,44 +1267,53 @@ int Ctx::solve(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_trace* 
   push(eps0, 1);
   CK(cudaMemcpyAsync(w.p, z.p, m * 8, cudaMemcpyDeviceToDevice, st));
   const double target = o.rel ? o.tol * eps0 : o.tol;
-  const double one = 1.0, mone = -1.0, zero = 0.0;
-  while (true) {
-    if (eps <= target) { status = FETIGPU_CONVERGED; break; }
-    if (it >= o.max_it) { status = FETIGPU_MAX_ITER; break; }
+  // one PCG / FO iteration (everything on the stream, no host work)
+  auto body = [&]() {
     apply_F(w.p, q.p, 1, m, m);
-    ++fapp;
     dots({{w.p, q.p}, {w.p, r.p}}, &sc.p->delta);
     if (tf) proj_corr(q.p, m, corr.p, m, 1);
-    // breakdown check needs delta before the update
-    CK(cudaMemcpyAsync(hs, sc.p, sizeof(Scal), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    if (!(hs->delta > 0.0)) { status = FETIGPU_BREAKDOWN; break; }
     k_pcg_update<<<grid_for(m), kThreads, 0, st>>>(m, sc.p, fo ? 1 : 0, w.p, q.p, tf ? corr.p : nullptr, lam.p,
                                                    r.p);
     precond_projected(r.p, z.p, nullptr);
     dots({{r.p, z.p}, {r.p, r.p}, {z.p, z.p}}, &sc.p->rz);
     if (fo) {
-      k_fo_store<<<grid_for(m), kThreads, 0, st>>>(m, sc.p, w.p, q.p, Wst.p + (size_t)it * m,
-                                                   Qst.p + (size_t)it * m);
+      k_fo_store2<<<grid_for(m), kThreads, 0, st>>>(m, sc.p, cnt.p, w.p, q.p, Wst.p, Qst.p);
+      k_inc<<<1, 1, 0, st>>>(cnt.p);
+      CK(cudaMemcpyAsync(w.p, z.p, m * 8, cudaMemcpyDeviceToDevice, st));
+      for (int pss = 0; pss < passes; ++pss) {
+        k_fo_psi<<<cap, kThreads, 0, st>>>(Qst.p, m, cnt.p, w.p, psi.p);
+        k_fo_sub<<<(m + 31) / 32, 256, 0, st>>>(Wst.p, m, cnt.p, psi.p, w.p);
+      }
+    } else {
+      k_cg_dir2<<<grid_for(m), kThreads, 0, st>>>(m, sc.p, z.p, w.p);
+      k_shift_rz<<<1, 1, 0, st>>>(sc.p);
     }
     CK(cudaMemcpyAsync(hs, sc.p, sizeof(Scal), cudaMemcpyDeviceToHost, st));
+    LAUNCH_CHECK();
+  };
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  bool use_graph = true;
+  if (use_graph) {
+    CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    body();
+    CK(cudaStreamEndCapture(st, &graph));
+    CK(cudaGraphInstantiate(&exec, graph, 0));
+  }
+  while (true) {
+    if (eps <= target) { status = FETIGPU_CONVERGED; break; }
+    if (it >= o.max_it) { status = FETIGPU_MAX_ITER; break; }
+    if (use_graph) CK(cudaGraphLaunch(exec, st));
+    else body();
     CK(cudaStreamSynchronize(st));
+    if (hs->breakdown != 0.0) { status = FETIGPU_BREAKDOWN; break; }
+    ++fapp;
     eps = metric(*hs);
     ++it;
     push(eps, 1);
-    if (fo) {
-      CK(cudaMemcpyAsync(w.p, z.p, m * 8, cudaMemcpyDeviceToDevice, st));
-      for (int pss = 0; pss < passes; ++pss) {
-        CB(cublasDgemv(cb, CUBLAS_OP_T, m, it, &one, Qst.p, m, w.p, 1, &zero, psi.p, 1));
-        CB(cublasDgemv(cb, CUBLAS_OP_N, m, it, &mone, Wst.p, m, psi.p, 1, &one, w.p, 1));
-      }
-    } else {
-      const double beta = hs->rz / rz_old;
-      k_xpby<<<grid_for(m), kThreads, 0, st>>>(m, z.p, beta, w.p);
-    }
-    rz_old = hs->rz;
-    LAUNCH_CHECK();
   }
+  if (exec) cudaGraphExecDestroy(exec);
+  if (graph) cudaGraphDestroy(graph);
   CK(cudaEventRecord(ev1, st));
   const double ms = elapsed(ev0, ev1);
   CK(cudaMemcpyAsync(lambda_host, lam.p, m * 8, cudaMemcpyDeviceToHost, st));
@@ -1784,11 +1809,11 @@ int fetigpu_time_apply(fetigpu_ctx* ctx, const double* x, double* y, int ncols, 
       CK(cudaEventRecord(ev[2 * r], c.st));
       for (int col = 0; col < ncols; ++col) {
         if (c.su.method == FETIGPU_TFETI)
-          k_gather_gemv_scatter<3, false><<<dim3(c.su.Ns, 1), kThreads, c.max_ld * 8, c.st>>>(
+          k_gather_gemv_scatter<3, false><<<dim3(c.su.Ns, 1, c.rsplit), kThreads, c.max_ld * 8, c.st>>>(
               c.d_op.p, c.d_opmat.p, c.d_oprows.p, c.d_opcoef_apply.p, x + (size_t)col * c.su.m,
               y + (size_t)col * c.su.m, nullptr, 0, nullptr, nullptr, c.su.m, c.su.m);
         else
-          k_gather_gemv_scatter<1, true><<<c.su.Ns, kThreads, c.max_ld * 8, c.st>>>(
+          k_gather_gemv_scatter<1, true><<<dim3(c.su.Ns, 1, c.rsplit), kThreads, c.max_ld * 8, c.st>>>(
               c.d_op.p, c.d_opmat.p, c.d_oprows.p, c.d_opcoef_apply.p, x + (size_t)col * c.su.m, nullptr, nullptr, 0,
               c.d_vbuf.p, c.d_voff.p, c.su.m, 0);
       }

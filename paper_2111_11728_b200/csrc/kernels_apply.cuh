@@ -47,8 +47,9 @@ __global__ void __launch_bounds__(kThreads) k_gather_gemv_scatter(
   __syncthreads();
   const double* A = mats + d.moff;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nw = blockDim.x >> 5;
-  for (int i = warp; i < d.ns; i += nw) {
+  // rows are split over gridDim.z CTAs when there are few subdomains
+  const int nw = (blockDim.x >> 5) * gridDim.z;
+  for (int i = warp + (blockDim.x >> 5) * blockIdx.z; i < d.ns; i += nw) {
     const double2* Ai = reinterpret_cast<const double2*>(A + (size_t)i * d.ld);
     double acc0 = 0.0, acc1 = 0.0;
     const int n2 = d.ld >> 1;
@@ -231,6 +232,17 @@ __global__ void k_proj_scatter(const OpSub* __restrict__ psubs, const int* __res
   }
 }
 
+// PCG scalars live in device memory (no host round trip inside an iteration)
+struct Scal {
+  double delta;    // w^T F w
+  double wr;       // w^T r
+  double rz;       // r^T z (current)
+  double rr, zz;
+  double rz_old;
+  double alpha;
+  double breakdown;  // set to 1 by k_pcg_update when w^T F w <= 0
+};
+
 // ------------------------------------------------------------- reductions --
 // Deterministic multi-dot: fixed grid, fixed per-block order, final pass in
 // fixed order.  pairs: up to 4 (a_k, b_k) products of length n.
@@ -272,17 +284,111 @@ __global__ void k_dot_final(const double* partial, int npairs, double* out) {
   if (lane == 0) out[k] = acc;
 }
 
+// Single-launch deterministic multi-dot: fixed grid, per-block partials in a
+// fixed slot, the last block to finish sums them in fixed order.
+__global__ void __launch_bounds__(kThreads) k_dot_fused(DotArgs args, double* partial,
+                                                        unsigned int* counter, double* out) {
+  double acc[4] = {0, 0, 0, 0};
+  const int stride = gridDim.x * blockDim.x;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < args.n; i += stride) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (k < args.npairs) acc[k] = fma(args.a[k][i], args.b[k][i], acc[k]);
+  }
+  __shared__ double red[4][kThreads / 32];
+  __shared__ bool last;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const double v = warp_sum(acc[k]);
+    if (lane == 0) red[k][warp] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < args.npairs) {
+    double v = 0.0;
+    for (int w = 0; w < kThreads / 32; ++w) v += red[threadIdx.x][w];
+    partial[threadIdx.x * kDotBlocks + blockIdx.x] = v;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  const int k = warp;
+  if (k < args.npairs) {
+    double a = 0.0;
+    for (int b = lane; b < (int)gridDim.x; b += 32) a += ((volatile double*)partial)[k * kDotBlocks + b];
+    a = warp_sum(a);
+    if (lane == 0) out[k] = a;
+  }
+  if (threadIdx.x == 0) *counter = 0u;
+}
+
+// FO re-orthogonalization against the first *cnt stored directions
+// (column-major m x cap): psi_j = q_j^T w, then w -= sum_j psi_j w_j.
+// The column count lives in device memory so the iteration graph is static.
+__global__ void __launch_bounds__(kThreads) k_fo_psi(const double* __restrict__ Q, int m,
+                                                     const int* __restrict__ cnt,
+                                                     const double* __restrict__ w,
+                                                     double* __restrict__ psi) {
+  const int j = blockIdx.x;
+  if (j >= *cnt) return;
+  const double* q = Q + (size_t)j * m;
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < m; i += blockDim.x) acc = fma(q[i], w[i], acc);
+  __shared__ double red[kThreads / 32];
+  acc = warp_sum(acc);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int k = 0; k < kThreads / 32; ++k) s += red[k];
+    psi[j] = s;
+  }
+}
+// 32 rows per CTA (lane <-> row, coalesced per column), the 8 warps split the
+// columns j = warp, warp+8, ...; partial sums reduced over warps in fixed order.
+__global__ void __launch_bounds__(256) k_fo_sub(const double* __restrict__ W, int m,
+                                                const int* __restrict__ cnt,
+                                                const double* __restrict__ psi,
+                                                double* __restrict__ w) {
+  const int c = *cnt;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int i = blockIdx.x * 32 + lane;
+  __shared__ double part[8][33];
+  double v = 0.0;
+  if (i < m)
+    for (int j = warp; j < c; j += 8) v = fma(W[(size_t)j * m + i], psi[j], v);
+  part[warp][lane] = v;
+  __syncthreads();
+  if (warp == 0 && i < m) {
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += part[k][lane];
+    w[i] -= s;
+  }
+}
+__global__ void k_fo_store2(int n, const Scal* sc, const int* __restrict__ cnt,
+                            const double* __restrict__ w, const double* __restrict__ q,
+                            double* __restrict__ Wst, double* __restrict__ Qst) {
+  const double inv = 1.0 / sqrt(sc->delta);
+  const int j = *cnt;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    Wst[(size_t)j * n + i] = w[i] * inv;
+    Qst[(size_t)j * n + i] = q[i] * inv;
+  }
+}
+__global__ void k_inc(int* cnt) { *cnt += 1; }
+// w = z + beta w with beta = rz / rz_old from device scalars; then rz_old = rz
+__global__ void k_cg_dir2(int n, Scal* sc, const double* __restrict__ z, double* __restrict__ w) {
+  const double beta = sc->rz / sc->rz_old;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    w[i] = fma(beta, w[i], z[i]);
+}
+__global__ void k_shift_rz(Scal* sc) { sc->rz_old = sc->rz; }
+
 // ------------------------------------------------------- vector updates --
-// PCG scalars live in device memory (no host round trip inside an iteration)
-struct Scal {
-  double delta;    // w^T F w
-  double wr;       // w^T r
-  double rz;       // r^T z (current)
-  double rr, zz;
-  double rz_old;
-  double alpha;
-  double pad;
-};
 
 __global__ void k_axpy(int n, double a, const double* __restrict__ x, double* __restrict__ y) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
@@ -298,6 +404,10 @@ __global__ void k_add(int n, const double* __restrict__ c, double* __restrict__ 
 __global__ void k_pcg_update(int n, Scal* sc, int fo, const double* __restrict__ w,
                              const double* __restrict__ q, const double* __restrict__ corr,
                              double* __restrict__ lambda, double* __restrict__ r) {
+  if (!(sc->delta > 0.0)) {  // breakdown: leave lambda, r untouched
+    if (blockIdx.x == 0 && threadIdx.x == 0) sc->breakdown = 1.0;
+    return;
+  }
   const double alpha = (fo ? sc->wr : sc->rz) / sc->delta;
   if (blockIdx.x == 0 && threadIdx.x == 0) sc->alpha = alpha;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
