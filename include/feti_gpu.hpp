@@ -125,7 +125,7 @@ class DualSystem {
     const int cap = o.max_iterations + 2;
     std::vector<double> eps(cap);
     std::vector<int> kept(cap), fap(cap);
-    fetigpu_trace t{0, 0, 0, 0.0, 0.0, cap, eps.data(), kept.data(), fap.data(), 0.0};
+    fetigpu_trace t{0, 0, 0, 0.0, 0.0, cap, eps.data(), kept.data(), fap.data(), 0.0, {}};
     check(fetigpu_solve(ctx_, &so, lam.data(), &t));
     if (tr) {
       tr->status = t.status;

@@ -134,6 +134,10 @@ typedef struct fetigpu_trace {
   int* kept;
   int* f_app;
   double solve_ms;           /* device time of the iteration loop */
+  /* RRS device time per phase (ms, summed over iterations): F W, Gram,
+   * pivoted Cholesky, compression, gamma/lambda/r update, preconditioner +
+   * metric, projection of Z, re-orthogonalization */
+  double phase_ms[8];
 } fetigpu_trace;
 
 /* Build statistics and the per-apply algorithmic work. */

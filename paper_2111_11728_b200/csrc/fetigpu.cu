@@ -1340,16 +1340,27 @@ int Ctx::solve_rrs(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_tra
   const int passes = std::max(1, o.reorth_passes);
   rhs();
   DBuf<double> lam, r, z, q, tmp, Z, W, Wsel, Delta, gamma;
-  DBuf<int> perm, rank_d;
+  DBuf<int> perm, rank_d, ctl;
   DBuf<Scal> sc;
+  DBuf<double> Linv;
   lam.alloc(m); r.alloc(m); z.alloc(m); q.alloc(m); tmp.alloc(m);
-  Z.alloc((size_t)m * Ns); W.alloc((size_t)m * Ns); Wsel.alloc((size_t)m * Ns);
+  Z.alloc((size_t)m * Ns); W.alloc((size_t)m * Ns); Wsel.alloc((size_t)m * round_up(Ns, 8));
+  ctl.alloc(4);
+  Linv.alloc((size_t)Ns * Ns);
+  int coop_blocks = 0;
+  {
+    int dev = 0, sms = 0, per_sm = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pivchol_coop, 512, 0));
+    coop_blocks = sms * std::max(1, std::min(per_sm, 2));
+  }
   Delta.alloc((size_t)Ns * Ns); gamma.alloc(Ns);
   perm.alloc(Ns); rank_d.alloc(1);
   sc.alloc(1);
   sc.zero(st);
   std::vector<std::unique_ptr<DBuf<double>>> Ws, Qs, Psis;
-  std::vector<int> widths;
+  std::vector<int> widths, lds;
   Scal* hs = nullptr;
   CK(cudaMallocHost(&hs, sizeof(Scal)));
   std::unique_ptr<Scal, decltype(&cudaFreeHost)> hs_guard(hs, cudaFreeHost);
@@ -1383,20 +1394,40 @@ int Ctx::solve_rrs(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_tra
   CK(cudaMemcpyAsync(W.p, Z.p, (size_t)m * Ns * 8, cudaMemcpyDeviceToDevice, st));
   project_rm(W.p, Ns);  // line 3
   const double target = o.rel ? o.tol * eps0 : o.tol;
+  cudaEvent_t pev[9];
+  for (auto& e : pev) CK(cudaEventCreate(&e));
+  double phase[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  auto mark = [&](int i) { CK(cudaEventRecord(pev[i], st)); };
   while (true) {
     if (eps <= target) { status = FETIGPU_CONVERGED; break; }
     if (it >= o.max_it) { status = FETIGPU_MAX_ITER; break; }
     const int k = Ns;
     auto Qb = std::make_unique<DBuf<double>>();
     Qb->alloc((size_t)m * k);
+    mark(0);
     apply_F_block(W.p, k, Qb->p, k, k);  // line 7 (K5)
+    mark(1);
     fapp += k;
     // line 8: Delta = Q^T W (column-major k x k; lower triangle used)
     CB(cublasDgemm(cb, CUBLAS_OP_N, CUBLAS_OP_T, k, k, m, &one, Qb->p, k, W.p, k, &zero, Delta.p, k));
     k_mirror_lower<<<grid_for((long long)k * k), kThreads, 0, st>>>(Delta.p, k);
+    mark(2);
     // line 9
-    k_pivchol<<<1, 1024, 0, st>>>(Delta.p, k, o.pivot_tol, perm.p, rank_d.p, d_status.p);
+    if (k <= 64) {
+      k_pivchol<<<1, 1024, 0, st>>>(Delta.p, k, o.pivot_tol, perm.p, rank_d.p, d_status.p);
+    } else {
+      double* dp = Delta.p;
+      double tolv = o.pivot_tol;
+      int kk = k;
+      int* pp = perm.p;
+      int* rp = rank_d.p;
+      int* sp = d_status.p;
+      int* cp = ctl.p;
+      void* args[] = {&dp, &kk, &tolv, &pp, &rp, &sp, &cp};
+      CK(cudaLaunchCooperativeKernel((void*)k_pivchol_coop, coop_blocks, 512, args, 0, st));
+    }
     LAUNCH_CHECK();
+    mark(3);
     int rank = 0;
     CK(cudaMemcpyAsync(&rank, rank_d.p, sizeof(int), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
@@ -1407,26 +1438,36 @@ int Ctx::solve_rrs(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_tra
       fail(FETIGPU_E_INDEFINITE_INPUT, "pivoted Cholesky: negative pivot");
     }
     if (rank == 0) { status = FETIGPU_BREAKDOWN; break; }
-    // lines 10-11: W <- W N^T [L~^{-T}; 0]  ==  (L~^{-1} W_sel^T)^T, same for Q
+    // lines 10-11: W <- W N^T [L~^{-T}; 0]  ==  (L~^{-1} W_sel^T)^T, same for Q.
+    // Stored blocks are k_j x m column-major (cuBLAS view) with the leading
+    // dimension padded to a multiple of 8 (aligned cuBLAS paths).
+    const int rp = round_up(rank, 8);
     auto Wb = std::make_unique<DBuf<double>>();
-    Wb->alloc((size_t)m * rank);
-    k_gather_cols_rm<<<grid_for((long long)m * rank), kThreads, 0, st>>>(W.p, k, perm.p, rank, m, Wb->p, rank);
-    k_gather_cols_rm<<<grid_for((long long)m * rank), kThreads, 0, st>>>(Qb->p, k, perm.p, rank, m, Wsel.p, rank);
-    CB(cublasDtrsm(cb, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, rank, m, &one,
-                   Delta.p, k, Wb->p, rank));
-    CB(cublasDtrsm(cb, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, rank, m, &one,
-                   Delta.p, k, Wsel.p, rank));
-    Qb->alloc((size_t)m * rank);
-    CK(cudaMemcpyAsync(Qb->p, Wsel.p, (size_t)m * rank * 8, cudaMemcpyDeviceToDevice, st));
+    Wb->alloc((size_t)m * rp);
+    launch_identity(Linv.p, rank);
+    CB(cublasDtrsm(cb, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, rank, rank,
+                   &one, Delta.p, k, Linv.p, rank));
+    k_gather_cols_rm<<<grid_for((long long)m * rank), kThreads, 0, st>>>(W.p, k, perm.p, rank, m, Wsel.p, rp);
+    CB(cublasDtrmm(cb, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, rank, m, &one,
+                   Linv.p, rank, Wsel.p, rp, Wb->p, rp));
+    k_gather_cols_rm<<<grid_for((long long)m * rank), kThreads, 0, st>>>(Qb->p, k, perm.p, rank, m, Wsel.p, rp);
+    auto Qc = std::make_unique<DBuf<double>>();
+    Qc->alloc((size_t)m * rp);
+    CB(cublasDtrmm(cb, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, rank, m, &one,
+                   Linv.p, rank, Wsel.p, rp, Qc->p, rp));
+    Qb = std::move(Qc);
+    mark(4);
     // lines 13-15
-    CB(cublasDgemv(cb, CUBLAS_OP_N, rank, m, &one, Wb->p, rank, r.p, 1, &zero, gamma.p, 1));
-    CB(cublasDgemv(cb, CUBLAS_OP_T, rank, m, &one, Wb->p, rank, gamma.p, 1, &one, lam.p, 1));
-    CB(cublasDgemv(cb, CUBLAS_OP_T, rank, m, &one, Qb->p, rank, gamma.p, 1, &zero, tmp.p, 1));
+    CB(cublasDgemv(cb, CUBLAS_OP_N, rank, m, &one, Wb->p, rp, r.p, 1, &zero, gamma.p, 1));
+    CB(cublasDgemv(cb, CUBLAS_OP_T, rank, m, &one, Wb->p, rp, gamma.p, 1, &one, lam.p, 1));
+    CB(cublasDgemv(cb, CUBLAS_OP_T, rank, m, &one, Qb->p, rp, gamma.p, 1, &zero, tmp.p, 1));
     project(tmp.p, 1, m);
     k_axpy<<<grid_for(m), kThreads, 0, st>>>(m, -1.0, tmp.p, r.p);
+    mark(5);
     // line 16
     apply_precond(r.p, z.p, Z.p, true);
     dots({{r.p, z.p}, {r.p, r.p}, {z.p, z.p}}, &sc.p->rz);
+    mark(6);
     CK(cudaMemcpyAsync(hs, sc.p, sizeof(Scal), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     eps = metric(*hs);
@@ -1435,22 +1476,35 @@ int Ctx::solve_rrs(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_tra
     Ws.push_back(std::move(Wb));
     Qs.push_back(std::move(Qb));
     widths.push_back(rank);
+    lds.push_back(rp);
     // line 17
     CK(cudaMemcpyAsync(W.p, Z.p, (size_t)m * Ns * 8, cudaMemcpyDeviceToDevice, st));
     project_rm(W.p, Ns);
+    mark(7);
     // lines 18-21: block classical Gram-Schmidt against all stored blocks, `passes` passes
     Psis.resize(Ws.size());
     for (size_t j = 0; j < Ws.size(); ++j)
-      if (!Psis[j]) { Psis[j] = std::make_unique<DBuf<double>>(); Psis[j]->alloc((size_t)widths[j] * Ns); }
+      if (!Psis[j]) { Psis[j] = std::make_unique<DBuf<double>>(); Psis[j]->alloc((size_t)lds[j] * Ns); }
     for (int p = 0; p < passes; ++p) {
       for (size_t j = 0; j < Ws.size(); ++j)  // Psi_j = Q_j^T W   (k_j x Ns)
-        CB(cublasDgemm(cb, CUBLAS_OP_N, CUBLAS_OP_T, widths[j], Ns, m, &one, Qs[j]->p, widths[j], W.p, Ns, &zero,
-                       Psis[j]->p, widths[j]));
+        CB(cublasDgemm(cb, CUBLAS_OP_N, CUBLAS_OP_T, widths[j], Ns, m, &one, Qs[j]->p, lds[j], W.p, Ns, &zero,
+                       Psis[j]->p, lds[j]));
       for (size_t j = 0; j < Ws.size(); ++j)  // W -= W_j Psi_j  ==  W^T -= Psi_j^T W_j^T
-        CB(cublasDgemm(cb, CUBLAS_OP_T, CUBLAS_OP_N, Ns, m, widths[j], &mone, Psis[j]->p, widths[j], Ws[j]->p,
-                       widths[j], &one, W.p, Ns));
+        CB(cublasDgemm(cb, CUBLAS_OP_T, CUBLAS_OP_N, Ns, m, widths[j], &mone, Psis[j]->p, lds[j], Ws[j]->p,
+                       lds[j], &one, W.p, Ns));
+    }
+    mark(8);
+    CK(cudaEventSynchronize(pev[8]));
+    float t = 0;
+    const int pidx[8][2] = {{0, 1}, {1, 2}, {2, 3}, {3, 4}, {4, 5}, {5, 6}, {6, 7}, {7, 8}};
+    for (int q = 0; q < 8; ++q) {
+      CK(cudaEventElapsedTime(&t, pev[pidx[q][0]], pev[pidx[q][1]]));
+      phase[q] += t;
     }
   }
+  for (auto& e : pev) cudaEventDestroy(e);
+  if (tr)
+    for (int q = 0; q < 8; ++q) tr->phase_ms[q] = phase[q];
   CK(cudaEventRecord(ev1, st));
   const double ms = elapsed(ev0, ev1);
   CK(cudaMemcpyAsync(lambda_host, lam.p, m * 8, cudaMemcpyDeviceToHost, st));

@@ -14,6 +14,8 @@
 // accumulate_Bs chain (decomposition.hpp:98-101, linalg.cpp:206-213).
 #pragma once
 
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 
 namespace fg {
@@ -601,6 +603,100 @@ __global__ void __launch_bounds__(1024) k_pivchol(double* A, int n, double tol, 
     rank = k + 1;
   }
   if (tid == 0) *rank_out = rank;
+}
+
+// Same algorithm and per-element arithmetic as k_pivchol, spread over a
+// cooperative grid: block 0 selects the pivot, swaps and scales column k; all
+// blocks share the rank-1 trailing update; two grid syncs per pivot.
+__global__ void __launch_bounds__(512) k_pivchol_coop(double* A, int n, double tol, int* perm,
+                                                      int* rank_out, int* status, int* ctl) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double sv[16];
+  __shared__ int si[16];
+  __shared__ double s_scale;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int lane = tid & 31, warp = tid >> 5, nwarp = nt >> 5;
+  const bool b0 = blockIdx.x == 0;
+  if (b0) {
+    for (int i = tid; i < n; i += nt) perm[i] = i;
+    double mx = -1e300;
+    for (int i = tid; i < n; i += nt) mx = fmax(mx, A[(size_t)i * n + i]);
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 0) sv[warp] = mx;
+    __syncthreads();
+    if (tid == 0) {
+      double m2 = sv[0];
+      for (int w = 1; w < nwarp; ++w) m2 = fmax(m2, sv[w]);
+      s_scale = m2;
+    }
+    __syncthreads();
+  }
+  int k = 0;
+  for (; k < n; ++k) {
+    if (b0) {
+      const double stop_tol = tol * s_scale;
+      const double neg_tol = -tol * fmax(s_scale, 1e-300);
+      double bv = -1e300;
+      int bi = n;
+      for (int j = k + tid; j < n; j += nt) {
+        const double v = A[(size_t)j * n + j];
+        if (v > bv || (v == bv && j < bi)) { bv = v; bi = j; }
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+      }
+      if (lane == 0) { sv[warp] = bv; si[warp] = bi; }
+      __syncthreads();
+      if (tid == 0) {
+        double v = sv[0];
+        int b = si[0];
+        for (int w = 1; w < nwarp; ++w)
+          if (sv[w] > v || (sv[w] == v && si[w] < b)) { v = sv[w]; b = si[w]; }
+        ctl[0] = b;
+        ctl[1] = !(v > stop_tol);
+      }
+      __syncthreads();
+      if (ctl[1]) {
+        for (int j = k + tid; j < n; j += nt)
+          if (A[(size_t)j * n + j] < neg_tol) atomicExch(status, 2);
+      } else {
+        const int piv = ctl[0];
+        if (piv != k) {
+          for (int j = tid; j < n; j += nt) {
+            const double t = A[(size_t)j * n + k];
+            A[(size_t)j * n + k] = A[(size_t)j * n + piv];
+            A[(size_t)j * n + piv] = t;
+          }
+          __syncthreads();
+          for (int i = tid; i < n; i += nt) {
+            const double t = A[(size_t)k * n + i];
+            A[(size_t)k * n + i] = A[(size_t)piv * n + i];
+            A[(size_t)piv * n + i] = t;
+          }
+          if (tid == 0) { const int t = perm[k]; perm[k] = perm[piv]; perm[piv] = t; }
+          __syncthreads();
+        }
+        const double l = sqrt(A[(size_t)k * n + k]);
+        __syncthreads();
+        if (tid == 0) A[(size_t)k * n + k] = l;
+        for (int i = k + 1 + tid; i < n; i += nt) A[(size_t)k * n + i] /= l;
+      }
+      __threadfence();
+    }
+    grid.sync();
+    if (((volatile int*)ctl)[1]) break;
+    const int r = n - k - 1;
+    const long long tot = (long long)r * r;
+    for (long long idx = blockIdx.x * (long long)nt + tid; idx < tot; idx += (long long)gridDim.x * nt) {
+      const int j = k + 1 + (int)(idx / r), i = k + 1 + (int)(idx % r);
+      A[(size_t)j * n + i] -= A[(size_t)k * n + i] * A[(size_t)k * n + j];
+    }
+    grid.sync();
+  }
+  if (b0 && tid == 0) *rank_out = k;
 }
 
 // out[:, c] = in[:, perm[c]] for c < cols (column gather, column-major)

@@ -102,7 +102,8 @@ class FgOpts(C.Structure):
 class FgTrace(C.Structure):
     _fields_ = [("status", C.c_int), ("iterations", C.c_int), ("f_applies", C.c_int),
                 ("eps0", C.c_double), ("eps_final", C.c_double), ("cap", C.c_int),
-                ("eps", D), ("kept", I), ("f_app", I), ("solve_ms", C.c_double)]
+                ("eps", D), ("kept", I), ("f_app", I), ("solve_ms", C.c_double),
+                ("phase_ms", C.c_double * 8)]
 
 
 class FgStats(C.Structure):
@@ -255,12 +256,14 @@ class FetiSystem:
         cap = max_it + 2
         eps, kept, fap = np.zeros(cap), np.zeros(cap, dtype=np.int32), np.zeros(cap, dtype=np.int32)
         tr = FgTrace(0, 0, 0, 0.0, 0.0, cap, _p(eps), _p(kept), _p(fap), 0.0)
+        tr.phase_ms = (C.c_double * 8)(*([0.0] * 8))
         lam = np.zeros(self.m)
         check(lib().fetigpu_solve(self.h, C.byref(o), _p(lam), C.byref(tr)))
         n = tr.iterations + 1
         return lam, dict(status=tr.status, iterations=tr.iterations, f_applies=tr.f_applies,
                          eps0=tr.eps0, eps_final=tr.eps_final, eps=eps[:n].copy(),
-                         kept=kept[:n].copy(), f_app=fap[:n].copy(), solve_ms=tr.solve_ms)
+                         kept=kept[:n].copy(), f_app=fap[:n].copy(), solve_ms=tr.solve_ms,
+                         phase_ms=list(tr.phase_ms))
 
     def recover(self, lam: np.ndarray) -> np.ndarray:
         lam = np.ascontiguousarray(lam, dtype=np.float64)

@@ -30,7 +30,9 @@ st = g.stats()
 lam, tr = g.solve(tol=args.tol, max_it=args.max_it, directions=dirs)
 out = {"config": args.config, "method": prob.method, "dirs": dirs, "m": g.m, "build_ms": st["build_ms"],
        "build_wall_s": tb, "gpu": {k: tr[k] for k in ("status", "iterations", "f_applies", "solve_ms")},
-       "gpu_rel_res": tr["eps_final"] / max(tr["eps0"], 1e-300), "kept_head": tr["kept"][:8].tolist()}
+       "gpu_rel_res": tr["eps_final"] / max(tr["eps0"], 1e-300), "kept_head": tr["kept"][:8].tolist(),
+       "phase_ms": dict(zip(["FW", "gram", "pivchol", "compress", "update", "precond", "projZ", "reorth"],
+                            [round(x, 2) for x in tr["phase_ms"]]))}
 if args.recover:
     t0 = time.perf_counter()
     u = g.recover(lam)
