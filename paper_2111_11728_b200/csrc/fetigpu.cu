@@ -98,6 +98,12 @@ struct Ctx {
   // constraint signs are folded into F_s / A_bc (FETI-DP), else d_opcoef
   DBuf<double> d_opcoef_apply;
   bool folded = false;
+  // symmetric-packed operator tiles for the GEMV (used when rsplit == 1)
+  bool use_sym = false;
+  DBuf<double> d_symtiles;
+  DBuf<SymSub> d_sym;
+  double sym_bytes = 0;
+  int sym_smem = 0;
   std::vector<std::vector<double>> slot_sign;
   DBuf<int> d_oprows, d_slot_of, d_fac_ne, d_top_pos, d_top_off;
   DBuf<long long> d_fac_off;
@@ -680,6 +686,44 @@ struct Ctx {
     // ---- GEMV row split: aim for >= 4 CTAs per SM when subdomains are few
     rsplit = std::max(1, std::min(8, (4 * 148 + Ns - 1) / Ns));
     pc_rsplit = rsplit;
+    // ---- symmetric-packed copy of F_s for the single-vector apply (K4)
+    const char* nosym = getenv("FETIGPU_NO_SYM");
+    const char* forcesym = getenv("FETIGPU_FORCE_SYM");
+    const bool want_sym = rsplit == 1 || (forcesym && forcesym[0] == '1');
+    if (want_sym && !(nosym && nosym[0] == '1')) {
+      const int nsl = (int)su.op_slots.size();
+      std::vector<long long> toff(nsl);
+      long long tt = 0;
+      int nbmax = 0;
+      for (int i = 0; i < nsl; ++i) {
+        const int nb = (op_ns[i] + 31) / 32;
+        toff[i] = tt;
+        tt += (long long)nb * (nb + 1) / 2 * 1024;
+        nbmax = std::max(nbmax, nb);
+      }
+      d_symtiles.alloc(tt);
+      DBuf<long long> dmo, dto;
+      DBuf<int> dns, dld;
+      dmo.upload(op_moff, st); dto.upload(toff, st); dns.upload(op_ns, st); dld.upload(op_ld, st);
+      k_pack_sym<<<dim3(64, nsl), kThreads, 0, st>>>(dmo.p, dns.p, dld.p, dto.p, d_opmat.p, d_symtiles.p);
+      LAUNCH_CHECK();
+      std::vector<SymSub> ss(Ns);
+      sym_bytes = 0;
+      for (int s = 0; s < Ns; ++s) {
+        const int sl = su.subs[s].op_slot;
+        const int nb = (op_ns[sl] + 31) / 32;
+        ss[s] = {toff[sl], op_ns[sl], nb, ops[s].map_off, 0};
+        sym_bytes += (double)nb * (nb + 1) / 2 * 1024 * 8;
+      }
+      d_sym.upload(ss, st);
+      sym_smem = nbmax * 32 * (1 + kSymWarps) * 8;
+      if (sym_smem > 48 * 1024) {
+        CK(cudaFuncSetAttribute(k_sym_gemv_scatter<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sym_smem));
+        CK(cudaFuncSetAttribute(k_sym_gemv_scatter<3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sym_smem));
+      }
+      CK(cudaStreamSynchronize(st));
+      use_sym = true;
+    }
     // ---- work per apply
     double sn2 = 0, snc = 0, sns = 0;
     for (int s = 0; s < Ns; ++s) {
@@ -767,16 +811,27 @@ struct Ctx {
     const int Ns = su.Ns;
     if (su.method == FETIGPU_TFETI) {
       for (int c = 0; c < ncols; ++c) CK(cudaMemsetAsync(y + (size_t)c * ldy, 0, su.m * 8, st));
-      dim3 grid(Ns, ncols, rsplit);
-      k_gather_gemv_scatter<3, false><<<grid, kThreads, max_ld * 8, st>>>(
-          d_op.p, d_opmat.p, d_oprows.p, d_opcoef_apply.p, x, y, nullptr, 0, nullptr, nullptr, ldx, ldy);
+      if (use_sym) {
+        for (int c = 0; c < ncols; ++c)
+          k_sym_gemv_scatter<3, false><<<Ns, 256, sym_smem, st>>>(d_sym.p, d_symtiles.p, d_oprows.p,
+                                                                  d_opcoef_apply.p, x + (size_t)c * ldx,
+                                                                  y + (size_t)c * ldy, nullptr, nullptr);
+      } else {
+        dim3 grid(Ns, ncols, rsplit);
+        k_gather_gemv_scatter<3, false><<<grid, kThreads, max_ld * 8, st>>>(
+            d_op.p, d_opmat.p, d_oprows.p, d_opcoef_apply.p, x, y, nullptr, 0, nullptr, nullptr, ldx, ldy);
+      }
       LAUNCH_CHECK();
     } else {
       for (int c = 0; c < ncols; ++c) {
         const double* xc = x + (size_t)c * ldx;
         double* yc = y + (size_t)c * ldy;
-        k_gather_gemv_scatter<1, true><<<dim3(Ns, 1, rsplit), kThreads, max_ld * 8, st>>>(
-            d_op.p, d_opmat.p, d_oprows.p, d_opcoef_apply.p, xc, nullptr, nullptr, 0, d_vbuf.p, d_voff.p, ldx, 0);
+        if (use_sym)
+          k_sym_gemv_scatter<1, true><<<Ns, 256, sym_smem, st>>>(d_sym.p, d_symtiles.p, d_oprows.p,
+                                                                 d_opcoef_apply.p, xc, nullptr, d_vbuf.p, d_voff.p);
+        else
+          k_gather_gemv_scatter<1, true><<<dim3(Ns, 1, rsplit), kThreads, max_ld * 8, st>>>(
+              d_op.p, d_opmat.p, d_oprows.p, d_opcoef_apply.p, xc, nullptr, nullptr, 0, d_vbuf.p, d_voff.p, ldx, 0);
         k_dp_t<<<Ns, kThreads, 0, st>>>(d_op.p, d_dp.p, d_oprows.p, d_opcoef_apply.p, d_abc.p, xc, d_tbuf.p);
         k_coarse_gather<<<grid_for(su.Nc), kThreads, 0, st>>>(d_optr.p, d_oidx.p, d_tbuf.p, su.Nc, d_g.p,
                                                              1.0, nullptr);
@@ -1598,7 +1653,7 @@ int fetigpu_stats_get(const fetigpu_ctx* ctx, fetigpu_stats* s) {
     }
     s->op_bytes = 8 * sn2 + (dp ? 16 * snc + 8.0 * c.su.Nc * c.su.Nc : 0) + 16.0 * c.su.m + 8 * sns;
     s->op_flops_per_col = 2 * sn2 + (dp ? 4 * snc + 2.0 * c.su.Nc * c.su.Nc : 0);
-    s->main_kernel_bytes = 8 * sn2;
+    s->main_kernel_bytes = c.use_sym ? c.sym_bytes : 8 * sn2;
     s->build_ms = c.build_ms; s->nd_ms = c.nd_ms; s->slot_ms = c.slot_ms; s->coarse_ms = c.coarse_ms;
     s->device_bytes = (double)g_device_bytes;
   });
@@ -1862,14 +1917,24 @@ int fetigpu_time_apply(fetigpu_ctx* ctx, const double* x, double* y, int ncols, 
       if (flush_l2) k_flush<<<grid_for((long long)fl_n), kThreads, 0, c.st>>>(fl.p, fl_n, (double)r);
       CK(cudaEventRecord(ev[2 * r], c.st));
       for (int col = 0; col < ncols; ++col) {
-        if (c.su.method == FETIGPU_TFETI)
+        const double* xc = x + (size_t)col * c.su.m;
+        double* yc = y + (size_t)col * c.su.m;
+        if (c.use_sym) {
+          if (c.su.method == FETIGPU_TFETI)
+            k_sym_gemv_scatter<3, false><<<c.su.Ns, 256, c.sym_smem, c.st>>>(
+                c.d_sym.p, c.d_symtiles.p, c.d_oprows.p, c.d_opcoef_apply.p, xc, yc, nullptr, nullptr);
+          else
+            k_sym_gemv_scatter<1, true><<<c.su.Ns, 256, c.sym_smem, c.st>>>(
+                c.d_sym.p, c.d_symtiles.p, c.d_oprows.p, c.d_opcoef_apply.p, xc, nullptr, c.d_vbuf.p, c.d_voff.p);
+        } else if (c.su.method == FETIGPU_TFETI) {
           k_gather_gemv_scatter<3, false><<<dim3(c.su.Ns, 1, c.rsplit), kThreads, c.max_ld * 8, c.st>>>(
-              c.d_op.p, c.d_opmat.p, c.d_oprows.p, c.d_opcoef_apply.p, x + (size_t)col * c.su.m,
-              y + (size_t)col * c.su.m, nullptr, 0, nullptr, nullptr, c.su.m, c.su.m);
-        else
+              c.d_op.p, c.d_opmat.p, c.d_oprows.p, c.d_opcoef_apply.p, xc, yc, nullptr, 0, nullptr, nullptr,
+              c.su.m, c.su.m);
+        } else {
           k_gather_gemv_scatter<1, true><<<dim3(c.su.Ns, 1, c.rsplit), kThreads, c.max_ld * 8, c.st>>>(
-              c.d_op.p, c.d_opmat.p, c.d_oprows.p, c.d_opcoef_apply.p, x + (size_t)col * c.su.m, nullptr, nullptr, 0,
-              c.d_vbuf.p, c.d_voff.p, c.su.m, 0);
+              c.d_op.p, c.d_opmat.p, c.d_oprows.p, c.d_opcoef_apply.p, xc, nullptr, nullptr, 0, c.d_vbuf.p,
+              c.d_voff.p, c.su.m, 0);
+        }
       }
       CK(cudaEventRecord(ev[2 * r + 1], c.st));
     }

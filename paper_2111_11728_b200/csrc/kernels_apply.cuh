@@ -90,6 +90,120 @@ __global__ void __launch_bounds__(kThreads) k_gather_gemv_scatter(
   }
 }
 
+// ------------------------------------ K4 on symmetric-packed F_s (C4 path) --
+// F_s is symmetric: only the lower block-triangle of 32x32 tiles is stored
+// (tile (bi,bj), bi >= bj, row-major, zero padded; tiles ordered bi-major), so
+// each apply streams ~55% of the full-matrix bytes.  A warp owns tiles
+// w, w+8, ...: per tile it loads 32 coalesced 256-byte rows, accumulates the
+// transposed (column) part lane-privately and the row part through a
+// 31-shuffle transpose-reduce; per-warp partial vectors in shared memory are
+// summed in fixed warp order, so the result is deterministic.
+struct SymSub {
+  long long toff;   // offset of the packed tiles
+  int ns, nb;       // DOFs, 32-blocks
+  int map_off;
+  int pad;
+};
+constexpr int kSymWarps = 8;
+
+template <int KR, bool STORE_V>
+__global__ void __launch_bounds__(256) k_sym_gemv_scatter(
+    const SymSub* __restrict__ subs, const double* __restrict__ tiles, const int* __restrict__ rows,
+    const double* __restrict__ coefs, const double* __restrict__ x, double* __restrict__ y,
+    double* __restrict__ vbuf, const int* __restrict__ voff) {
+  extern __shared__ double shm[];
+  const SymSub d = subs[blockIdx.x];
+  const int npad = d.nb * 32;
+  double* xs = shm;                   // npad
+  double* part = shm + npad;          // kSymWarps x npad
+  const int* rw = rows + d.map_off;
+  const double* cf = coefs + d.map_off;
+  for (int j = threadIdx.x; j < npad; j += blockDim.x) {
+    double acc = 0.0;
+    if (j < d.ns) {
+#pragma unroll
+      for (int k = 0; k < KR; ++k) {
+        const int r = rw[j * KR + k];
+        if (r >= 0) acc += cf[j * KR + k] * x[r];
+      }
+    }
+    xs[j] = acc;
+  }
+  for (int j = threadIdx.x; j < kSymWarps * npad; j += blockDim.x) part[j] = 0.0;
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* pw = part + warp * npad;
+  const int ntiles = d.nb * (d.nb + 1) / 2;
+  const double* T0 = tiles + d.toff;
+  for (int t = warp; t < ntiles; t += kSymWarps) {
+    int bi = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+    while (bi * (bi + 1) / 2 > t) --bi;
+    while ((bi + 1) * (bi + 2) / 2 <= t) ++bi;
+    const int bj = t - bi * (bi + 1) / 2;
+    const double* T = T0 + (size_t)t * 1024;
+    double f[32];
+#pragma unroll
+    for (int r = 0; r < 32; ++r) f[r] = __ldcs(T + r * 32 + lane);
+    const double xj = xs[bj * 32 + lane];
+    double c = 0.0;
+#pragma unroll
+    for (int r = 0; r < 32; ++r) {
+      c = fma(f[r], xs[bi * 32 + r], c);   // column part: sum_r F[r][lane] x_i[r]
+      f[r] *= xj;                          // row part products
+    }
+    // transpose-reduce: lane l ends with sum over lanes of f[l]
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+      const bool hi = (lane & o) != 0;
+#pragma unroll
+      for (int q = 0; q < o; ++q) {
+        const double keep = hi ? f[q + o] : f[q];
+        const double send = hi ? f[q] : f[q + o];
+        f[q] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+      }
+    }
+    pw[bi * 32 + lane] += f[0];
+    if (bi != bj) pw[bj * 32 + lane] += c;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < d.ns; i += blockDim.x) {
+    double v = 0.0;
+#pragma unroll
+    for (int w = 0; w < kSymWarps; ++w) v += part[w * npad + i];
+    if (STORE_V) {
+      vbuf[voff[blockIdx.x] + i] = v;
+    } else {
+#pragma unroll
+      for (int k = 0; k < KR; ++k) {
+        const int r = rw[i * KR + k];
+        if (r >= 0) atomicAdd(y + r, cf[i * KR + k] * v);
+      }
+    }
+  }
+}
+
+// pack the lower block-triangle of a row-major symmetric ns x ld matrix
+__global__ void k_pack_sym(const long long* __restrict__ moff, const int* __restrict__ ns_,
+                           const int* __restrict__ ld_, const long long* __restrict__ toff,
+                           const double* __restrict__ mats, double* __restrict__ tiles) {
+  const int sl = blockIdx.y;
+  const int ns = ns_[sl], ld = ld_[sl];
+  const int nb = (ns + 31) / 32;
+  const long long tot = (long long)nb * (nb + 1) / 2 * 1024;
+  const double* M = mats + moff[sl];
+  double* T = tiles + toff[sl];
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < tot;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int t = (int)(idx >> 10), e = (int)(idx & 1023);
+    int bi = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+    while (bi * (bi + 1) / 2 > t) --bi;
+    while ((bi + 1) * (bi + 2) / 2 <= t) ++bi;
+    const int bj = t - bi * (bi + 1) / 2;
+    const int r = bi * 32 + (e >> 5), c = bj * 32 + (e & 31);
+    T[idx] = (r < ns && c < ns) ? M[(size_t)r * ld + c] : 0.0;
+  }
+}
+
 // FETI-DP coarse coupling, phase 1: t_s = A_bc^T x_s (after k_gather_gemv_scatter
 // stored v_s = F_s x_s): x_s is re-gathered (1 row per DOF).
 __global__ void k_dp_t(const OpSub* __restrict__ subs, const DpSub* __restrict__ dps,

@@ -216,3 +216,61 @@ def test_block_apply(name, k, oracle_mod):
     for c in sorted({0, k // 2, k - 1}):
         accurate(Qb[:, c], o.apply_F(W[:, c]), r.apply_F(W[:, c]), f"{name} block col{c}")
     assert rel(Qb, Qc) <= max(1e-12, 10 * rel(o.apply_F(W[:, 0]), r.apply_F(W[:, 0])))
+
+
+@pytest.mark.parametrize("name", ["C1", "C1b", "C2s", "C3tf_s", "C3dp_s", "C4s"])
+def test_symmetric_packed_apply(name, oracle_mod, monkeypatch):
+    """The symmetric-packed F_s GEMV (lower block-triangle tiles, used by
+    default when subdomains are plentiful) against the full-matrix kernel and
+    the oracle; forced on here for small cases."""
+    from paper_2111_11728_b200 import engine
+    g, o, r = systems(name, oracle_mod)
+    monkeypatch.setenv("FETIGPU_FORCE_SYM", "1")
+    gs = engine.FetiSystem(CASES[name]())
+    monkeypatch.delenv("FETIGPU_FORCE_SYM")
+    st = gs.stats()
+    assert st["main_kernel_bytes"] > 0
+    X = np.random.default_rng(21).standard_normal((g.m, 2))
+    Ys, Yf = gs.apply_F(X), g.apply_F(X)
+    for c in range(2):
+        accurate(Ys[:, c], o.apply_F(X[:, c]), r.apply_F(X[:, c]), f"{name} sym col{c}")
+    assert rel(Ys, Yf) <= max(1e-12, 10 * rel(o.apply_F(X[:, 0]), r.apply_F(X[:, 0])))
+    # deterministic: repeated applies are bit-identical
+    assert np.array_equal(gs.apply_F(X[:, 0]), Ys[:, 0])
+    lg, tg = gs.solve(tol=1e-6, max_it=400, directions=1)
+    lo, to = o.solve(tol=1e-6, max_it=400, directions=1)
+    assert abs(tg["iterations"] - to["iterations"]) <= 1
+    gs.close()
+
+
+@pytest.mark.parametrize("name", ["C1", "C2s", "C3tf_s", "C3dp_s", "C5s", "C4s"])
+def test_recovered_interface_jump(name, oracle_mod):
+    """after convergence at eps 1e-8 the recovered
+    displacements satisfy B u = c to 1e-6 relative (T-FETI rows incl.
+    Dirichlet gaps; FETI-DP: every pair row, plus corners and supports by
+    construction), and the copies of every shared global DOF agree."""
+    g, o, r = systems(name, oracle_mod)
+    lam, tr = g.solve(tol=1e-8, max_it=2000, directions=1)
+    assert tr["status"] == 0
+    u = g.recover(lam)
+    rows = g.rows()
+    jump = np.where(rows["kind"] == 0,
+                    u[rows["sub_plus"], rows["dof_plus"]] - u[rows["sub_minus"], rows["dof_minus"]],
+                    u[rows["sub_plus"], rows["dof_plus"]] - rows["gap"])
+    assert np.linalg.norm(jump) <= 1e-6 * np.linalg.norm(u)
+    # all owner copies of each global node agree (covers FETI-DP corners)
+    p = g.prob
+    n, gx = p.n, p.gx_nodes
+    vals = {}
+    for s in range(p.n_sub):
+        si, sj = s % p.sx, s // p.sx
+        for iy in (0, n):
+            for ix in range(n + 1):
+                key = ((sj * n + iy) * gx + si * n + ix)
+                vals.setdefault(key, []).append(u[s, 2 * (iy * (n + 1) + ix):2 * (iy * (n + 1) + ix) + 2])
+        for ix in (0, n):
+            for iy in range(n + 1):
+                key = ((sj * n + iy) * gx + si * n + ix)
+                vals.setdefault(key, []).append(u[s, 2 * (iy * (n + 1) + ix):2 * (iy * (n + 1) + ix) + 2])
+    spread = max(np.abs(np.array(v) - v[0]).max() for v in vals.values())
+    assert spread <= 1e-6 * np.abs(u).max()

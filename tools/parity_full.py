@@ -13,12 +13,13 @@ from paper_2111_11728_b200 import engine, problems as pb  # noqa: E402
 
 name = sys.argv[1]
 max_it = int(sys.argv[2]) if len(sys.argv) > 2 else 200
+tol = float(sys.argv[3]) if len(sys.argv) > 3 else 1e-6
 prob = pb.CONFIGS[name]()
-out = {"config": name, "method": prob.method, "directions": prob.directions, "tol": 1e-6,
+out = {"config": name, "method": prob.method, "directions": prob.directions, "tol": tol,
        "host_cores": os.cpu_count()}
 g = engine.FetiSystem(prob)
 st = g.stats()
-lg, tg = g.solve(tol=1e-6, max_it=max_it, directions=prob.directions)
+lg, tg = g.solve(tol=tol, max_it=max_it, directions=prob.directions)
 ug = g.recover(lg)
 out["gpu"] = {"build_ms": st["build_ms"], "solve_ms": tg["solve_ms"], "iterations": tg["iterations"],
               "status": tg["status"], "kept": tg["kept"].tolist(), "rel_res": tg["eps_final"] / tg["eps0"],
@@ -27,11 +28,29 @@ t0 = time.perf_counter()
 o = pyoracle.Oracle(prob)
 tb = time.perf_counter() - t0
 t0 = time.perf_counter()
-lo, to = o.solve(tol=1e-6, max_it=max_it, directions=prob.directions)
+lo, to = o.solve(tol=tol, max_it=max_it, directions=prob.directions)
 ts = time.perf_counter() - t0
 uo = o.recover(lo)
 out["oracle"] = {"build_s": tb, "solve_s": ts, "iterations": to["iterations"], "status": to["status"],
                  "kept": to["kept"].tolist(), "rel_res": to["eps_final"] / to["eps0"]}
 out["u_rel_l2_gpu_vs_oracle"] = float(np.linalg.norm(ug - uo) / np.linalg.norm(uo))
+# energy norm ||u_g - u_o||_K / ||u_o||_K with the oracle's assembled K^s
+num = den = 0.0
+for s_ in range(o.n_sub):
+    du = ug[s_] - uo[s_]
+    num += du @ o.local_apply(s_, du)
+    den += uo[s_] @ o.local_apply(s_, uo[s_])
+out["u_rel_energy_gpu_vs_oracle"] = float(np.sqrt(max(num, 0.0) / den))
+# L2 restricted to nodes that touch a solid element (rho > 0.5)
+n = prob.n
+mask = np.zeros((o.n_sub, o.local_dofs), bool)
+for s_ in range(o.n_sub):
+    rho = prob.densities[prob.module_type[s_]]
+    for ey in range(n):
+        for ex in range(n):
+            if rho[ey, ex] > 0.5:
+                for a in (ey * (n + 1) + ex, ey * (n + 1) + ex + 1, (ey + 1) * (n + 1) + ex, (ey + 1) * (n + 1) + ex + 1):
+                    mask[s_, 2 * a:2 * a + 2] = True
+out["u_rel_l2_solid_nodes"] = float(np.linalg.norm((ug - uo)[mask]) / np.linalg.norm(uo[mask]))
 out["iteration_diff"] = tg["iterations"] - to["iterations"]
 print(json.dumps(out))
