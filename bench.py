@@ -189,6 +189,24 @@ def cpu_sample(steps=3, warmup=1, sample=(8, 4)):
                       f"extrapolated x{scale:.0f} in subdomains"}
 
 
+def cpu_solves():
+    """The oracle's full PCG solves (implicit per-subdomain solves, all host
+    cores) for the two configs whose CPU solve fits a bounded budget."""
+    from oracle import pyoracle
+    out = {}
+    for name, fn, dirs in (("C2", pb.config2, 1), ("C3-fetidp", lambda: pb.config3(method=1), 1)):
+        t0 = time.perf_counter()
+        o = pyoracle.Oracle(fn())
+        tb = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        _, tr = o.solve(tol=1e-6, max_it=2000, directions=dirs)
+        out[name] = {"build_s": tb, "solve_s": time.perf_counter() - t0, "iterations": tr["iterations"],
+                     "status": ["converged", "max_iter", "breakdown"][tr["status"]],
+                     "directions": ["single", "fo", "rrs"][dirs]}
+        log("cpu", name, out[name])
+    return out
+
+
 def cpu_model():
     try:
         for ln in open("/proc/cpuinfo"):
@@ -384,8 +402,10 @@ def main():
         solves = solve_table(engine, [
             ("C1", pb.config1, dict(tol=1e-6, max_it=2000, directions=0)),
             ("C2", pb.config2, dict(tol=1e-6, max_it=2000, directions=0)),
+            ("C2-fo", pb.config2, dict(tol=1e-6, max_it=2000, directions=1)),
             ("C3-tfeti", lambda: pb.config3(method=0), dict(tol=1e-6, max_it=2000, directions=1)),
             ("C3-fetidp", lambda: pb.config3(method=1), dict(tol=1e-6, max_it=2000, directions=1)),
+            ("C5", pb.config5, dict(tol=1e-6, max_it=200, directions=2)),
         ])
 
     cpu = None
@@ -395,6 +415,8 @@ def main():
             cpu = {"value": st["op_bytes"] / r["t_apply_c4_s"] / 1e9, "unit": "GB/s",
                    "cores": r["cores"], "kind": "port", "sample": r["sample"],
                    "cpu_model": cpu_model(), "t_apply_c4_s": r["t_apply_c4_s"]}
+            if not args.no_solves:
+                cpu["solves"] = cpu_solves()
         except Exception as e:  # the checker is optional for the GPU number
             log("cpu baseline failed:", e)
 

@@ -283,14 +283,24 @@ static PivChol pivoted_cholesky(Mat a, double tol) {
 // PivotedCholesky::compress (linalg.cpp:131-138): W[:, perm[:rank]] Ltilde^{-T}
 static Mat compress(const PivChol& pc, const Mat& w) {
   Mat out(w.r, pc.rank);
-  std::vector<double> row(pc.rank);
-  for (int i = 0; i < w.r; ++i) {
-    for (int k = 0; k < pc.rank; ++k) {
-      double s = w(i, pc.perm[k]);
-      for (int j = 0; j < k; ++j) s -= pc.lower(k, j) * row[j];
-      row[k] = s / pc.lower(k, k);
+  // row-wise forward substitution; rows are independent (parallel, same
+  // per-row arithmetic as the sequential loop)
+  Mat Lt(pc.rank, pc.rank);  // Lt(j, k) = lower(k, j): contiguous rows of L~
+  for (int k = 0; k < pc.rank; ++k)
+    for (int j = 0; j <= k; ++j) Lt(j, k) = pc.lower(k, j);
+#pragma omp parallel
+  {
+    std::vector<double> row(pc.rank);
+#pragma omp for schedule(static)
+    for (int i = 0; i < w.r; ++i) {
+      for (int k = 0; k < pc.rank; ++k) {
+        double s = w(i, pc.perm[k]);
+        const double* lk = Lt.col(k);
+        for (int j = 0; j < k; ++j) s -= lk[j] * row[j];
+        row[k] = s / lk[k];
+      }
+      for (int k = 0; k < pc.rank; ++k) out(i, k) = row[k];
     }
-    for (int k = 0; k < pc.rank; ++k) out(i, k) = row[k];
   }
   return out;
 }
@@ -1233,10 +1243,12 @@ int Oracle::solve(const fo_opts& o, double* lambda, fo_trace* tr) {
       Q = compress(pc, Q);
       const int kr = pc.rank;
       std::vector<double> gamma(kr);
+#pragma omp parallel for schedule(static)
       for (int c = 0; c < kr; ++c) gamma[c] = dot(W.col(c), r.data(), m);
       std::fill(tmp.begin(), tmp.end(), 0.0);
-      for (int c = 0; c < kr; ++c)
-        for (int i = 0; i < m; ++i) {
+#pragma omp parallel for schedule(static)
+      for (int i = 0; i < m; ++i)
+        for (int c = 0; c < kr; ++c) {
           lambda[i] += W(i, c) * gamma[c];
           tmp[i] += Q(i, c) * gamma[c];
         }

@@ -104,6 +104,10 @@ struct Ctx {
   DBuf<SymSub> d_sym;
   double sym_bytes = 0;
   int sym_smem = 0;
+  bool pc_sym = false;
+  DBuf<double> d_pcsymtiles;
+  DBuf<SymSub> d_pcsym;
+  int pc_sym_smem = 0;
   std::vector<std::vector<double>> slot_sign;
   DBuf<int> d_oprows, d_slot_of, d_fac_ne, d_top_pos, d_top_off;
   DBuf<long long> d_fac_off;
@@ -723,6 +727,41 @@ struct Ctx {
       }
       CK(cudaStreamSynchronize(st));
       use_sym = true;
+      // same packing for the (symmetric) preconditioner blocks S~_s / K_TT
+      const int npc2 = (int)pc_moff.size();
+      std::vector<long long> ptoff(npc2);
+      std::vector<int> pns(npc2);
+      long long pt = 0;
+      int pnbmax = 0;
+      for (int i = 0; i < npc2; ++i) {
+        pns[i] = su.precond == FETIGPU_DIRICHLET ? (int)(su.pc_slots[i].src.size() - su.pc_slots[i].ne)
+                                                 : (int)su.pc_lumped_T[i].size();
+        const int nb = (pns[i] + 31) / 32;
+        ptoff[i] = pt;
+        pt += (long long)nb * (nb + 1) / 2 * 1024;
+        pnbmax = std::max(pnbmax, nb);
+      }
+      d_pcsymtiles.alloc(pt);
+      DBuf<long long> pmo, pto;
+      DBuf<int> pnsd, pldd;
+      pmo.upload(pc_moff, st); pto.upload(ptoff, st); pnsd.upload(pns, st); pldd.upload(pc_ld, st);
+      k_pack_sym<<<dim3(64, npc2), kThreads, 0, st>>>(pmo.p, pnsd.p, pldd.p, pto.p, d_pcmat.p, d_pcsymtiles.p);
+      LAUNCH_CHECK();
+      std::vector<SymSub> pss(Ns);
+      for (int s = 0; s < Ns; ++s) {
+        const int sl = su.subs[s].pc_slot;
+        pss[s] = {ptoff[sl], pns[sl], (pns[sl] + 31) / 32, pcs[s].map_off, 0};
+      }
+      d_pcsym.upload(pss, st);
+      pc_sym_smem = pnbmax * 32 * (1 + kSymWarps) * 8;
+      if (pc_sym_smem > 48 * 1024) {
+        CK(cudaFuncSetAttribute(k_sym_gemv_scatter<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                pc_sym_smem));
+        CK(cudaFuncSetAttribute(k_sym_gemv_scatter<3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                std::max(pc_sym_smem, sym_smem)));
+      }
+      CK(cudaStreamSynchronize(st));
+      pc_sym = true;
     }
     // ---- work per apply
     double sn2 = 0, snc = 0, sns = 0;
@@ -826,17 +865,20 @@ struct Ctx {
       for (int c = 0; c < ncols; ++c) {
         const double* xc = x + (size_t)c * ldx;
         double* yc = y + (size_t)c * ldy;
+        // phase 1: v_s = F''_s x_s and t_s = A''^T x_s (one kernel)
         if (use_sym)
           k_sym_gemv_scatter<1, true><<<Ns, 256, sym_smem, st>>>(d_sym.p, d_symtiles.p, d_oprows.p,
-                                                                 d_opcoef_apply.p, xc, nullptr, d_vbuf.p, d_voff.p);
+                                                                 d_opcoef_apply.p, xc, nullptr, d_vbuf.p, d_voff.p,
+                                                                 d_dp.p, d_abc.p, d_tbuf.p);
         else
           k_gather_gemv_scatter<1, true><<<dim3(Ns, 1, rsplit), kThreads, max_ld * 8, st>>>(
-              d_op.p, d_opmat.p, d_oprows.p, d_opcoef_apply.p, xc, nullptr, nullptr, 0, d_vbuf.p, d_voff.p, ldx, 0);
-        k_dp_t<<<Ns, kThreads, 0, st>>>(d_op.p, d_dp.p, d_oprows.p, d_opcoef_apply.p, d_abc.p, xc, d_tbuf.p);
-        k_coarse_gather<<<grid_for(su.Nc), kThreads, 0, st>>>(d_optr.p, d_oidx.p, d_tbuf.p, su.Nc, d_g.p,
-                                                             1.0, nullptr);
+              d_op.p, d_opmat.p, d_oprows.p, d_opcoef_apply.p, xc, nullptr, nullptr, 0, d_vbuf.p, d_voff.p, ldx, 0,
+              1, d_dp.p, d_abc.p, d_tbuf.p);
+        // coarse: t = sum B_c^T t_s (fixed order), y := 0, u = Kbar^{-1} t
+        k_coarse_gather<<<grid_for(std::max(su.Nc, su.m)), kThreads, 0, st>>>(d_optr.p, d_oidx.p, d_tbuf.p, su.Nc,
+                                                                             d_g.p, 1.0, nullptr, yc, su.m);
         k_dense_gemv<<<grid_for((long long)su.Nc * 32), kThreads, 0, st>>>(d_Kinv.p, su.Nc, d_g.p, d_h.p);
-        CK(cudaMemsetAsync(yc, 0, su.m * 8, st));
+        // phase 2: y = sum_s B_s (v_s + A''_s u_s)
         k_dp_phase2<<<Ns, kThreads, 0, st>>>(d_op.p, d_dp.p, d_oprows.p, d_opcoef_apply.p, d_abc.p, d_cmap.p,
                                              d_h.p, d_vbuf.p, yc, 1.0);
         LAUNCH_CHECK();
@@ -850,6 +892,16 @@ struct Ctx {
     CK(cudaMemsetAsync(z, 0, su.m * 8, st));
     if (Zcols) CK(cudaMemsetAsync(Zcols, 0, (size_t)su.m * su.Ns * 8, st));
     const int ldz = row_major ? 1 : su.m, zrs = row_major ? su.Ns : 1;
+    if (pc_sym && !Zcols) {
+      if (KRp == 1)
+        k_sym_gemv_scatter<1, false><<<su.Ns, 256, pc_sym_smem, st>>>(d_pcsym.p, d_pcsymtiles.p, d_pcrows.p,
+                                                                      d_pccoef.p, r, z, nullptr, nullptr);
+      else
+        k_sym_gemv_scatter<3, false><<<su.Ns, 256, pc_sym_smem, st>>>(d_pcsym.p, d_pcsymtiles.p, d_pcrows.p,
+                                                                      d_pccoef.p, r, z, nullptr, nullptr);
+      LAUNCH_CHECK();
+      return;
+    }
     if (KRp == 1)
       k_gather_gemv_scatter<1, false><<<dim3(su.Ns, 1, pc_rsplit), kThreads, max_pc_ld * 8, st>>>(
           d_pc.p, d_pcmat.p, d_pcrows.p, d_pccoef.p, r, z, Zcols, ldz, nullptr, nullptr, 0, 0, zrs);
@@ -1925,7 +1977,8 @@ int fetigpu_time_apply(fetigpu_ctx* ctx, const double* x, double* y, int ncols, 
                 c.d_sym.p, c.d_symtiles.p, c.d_oprows.p, c.d_opcoef_apply.p, xc, yc, nullptr, nullptr);
           else
             k_sym_gemv_scatter<1, true><<<c.su.Ns, 256, c.sym_smem, c.st>>>(
-                c.d_sym.p, c.d_symtiles.p, c.d_oprows.p, c.d_opcoef_apply.p, xc, nullptr, c.d_vbuf.p, c.d_voff.p);
+                c.d_sym.p, c.d_symtiles.p, c.d_oprows.p, c.d_opcoef_apply.p, xc, nullptr, c.d_vbuf.p, c.d_voff.p,
+                c.d_dp.p, c.d_abc.p, c.d_tbuf.p);
         } else if (c.su.method == FETIGPU_TFETI) {
           k_gather_gemv_scatter<3, false><<<dim3(c.su.Ns, 1, c.rsplit), kThreads, c.max_ld * 8, c.st>>>(
               c.d_op.p, c.d_opmat.p, c.d_oprows.p, c.d_opcoef_apply.p, xc, yc, nullptr, 0, nullptr, nullptr,
@@ -1933,7 +1986,7 @@ int fetigpu_time_apply(fetigpu_ctx* ctx, const double* x, double* y, int ncols, 
         } else {
           k_gather_gemv_scatter<1, true><<<dim3(c.su.Ns, 1, c.rsplit), kThreads, c.max_ld * 8, c.st>>>(
               c.d_op.p, c.d_opmat.p, c.d_oprows.p, c.d_opcoef_apply.p, xc, nullptr, nullptr, 0, c.d_vbuf.p,
-              c.d_voff.p, c.su.m, 0);
+              c.d_voff.p, c.su.m, 0, 1, c.d_dp.p, c.d_abc.p, c.d_tbuf.p);
         }
       }
       CK(cudaEventRecord(ev[2 * r + 1], c.st));
@@ -1948,7 +2001,7 @@ int fetigpu_time_apply(fetigpu_ctx* ctx, const double* x, double* y, int ncols, 
     ms[0] = tot / reps;
     ms[1] = tot_main / reps;
     ms[2] = ms[1] / ms[0];
-    if (launches) *launches = (c.su.method == FETIGPU_TFETI ? 1 : 5) * ncols;
+    if (launches) *launches = (c.su.method == FETIGPU_TFETI ? 1 : 4) * ncols;
   });
 }
 

@@ -22,12 +22,40 @@ namespace fg {
 
 // ------------------------------------------------------------ the F-apply --
 // KR = max dual rows touching one local DOF (1 FETI-DP, <= 3 T-FETI cross points)
+// FETI-DP coarse pre-pass fused into the GEMV CTA (x_s already in smem):
+// t_s = A''^T x_s for the subdomain's <= 8 primal DOFs (rsplit slice 0 only).
+__device__ __forceinline__ void fused_dp_t(const DpSub& p, const double* __restrict__ abc,
+                                           const double* xs, int ns, double* __restrict__ tbuf) {
+  __shared__ double red[8][kThreads / 32];
+  double acc[8] = {};
+  const double* Ab = abc + p.abc_off;
+  for (int j = threadIdx.x; j < ns; j += blockDim.x) {
+    const double xj = xs[j];
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+      if (c < p.nc) acc[c] = fma(Ab[(size_t)j * p.nc + c], xj, acc[c]);
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const double v = warp_sum(acc[c]);
+    if (lane == 0) red[c][warp] = v;
+  }
+  __syncthreads();
+  if ((int)threadIdx.x < p.nc) {
+    double v = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) v += red[threadIdx.x][w];
+    tbuf[p.t_off + threadIdx.x] = v;
+  }
+}
+
 template <int KR, bool STORE_V>
 __global__ void __launch_bounds__(kThreads) k_gather_gemv_scatter(
     const OpSub* __restrict__ subs, const double* __restrict__ mats, const int* __restrict__ rows,
     const double* __restrict__ coefs, const double* __restrict__ x, double* __restrict__ y,
     double* __restrict__ zcols, int ldz, double* __restrict__ vbuf, const int* __restrict__ voff,
-    int ldx, int ldy, int zrs = 1) {
+    int ldx, int ldy, int zrs = 1, const DpSub* __restrict__ dps = nullptr,
+    const double* __restrict__ abc = nullptr, double* __restrict__ tbuf = nullptr) {
   extern __shared__ double xs[];
   const int s = blockIdx.x;
   const int col = blockIdx.y;
@@ -47,6 +75,7 @@ __global__ void __launch_bounds__(kThreads) k_gather_gemv_scatter(
     xs[j] = acc;
   }
   __syncthreads();
+  if (STORE_V && dps && blockIdx.z == 0) fused_dp_t(dps[s], abc, xs, d.ns, tbuf);
   const double* A = mats + d.moff;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // rows are split over gridDim.z CTAs when there are few subdomains
@@ -110,7 +139,8 @@ template <int KR, bool STORE_V>
 __global__ void __launch_bounds__(256) k_sym_gemv_scatter(
     const SymSub* __restrict__ subs, const double* __restrict__ tiles, const int* __restrict__ rows,
     const double* __restrict__ coefs, const double* __restrict__ x, double* __restrict__ y,
-    double* __restrict__ vbuf, const int* __restrict__ voff) {
+    double* __restrict__ vbuf, const int* __restrict__ voff, const DpSub* __restrict__ dps = nullptr,
+    const double* __restrict__ abc = nullptr, double* __restrict__ tbuf = nullptr) {
   extern __shared__ double shm[];
   const SymSub d = subs[blockIdx.x];
   const int npad = d.nb * 32;
@@ -131,6 +161,7 @@ __global__ void __launch_bounds__(256) k_sym_gemv_scatter(
   }
   for (int j = threadIdx.x; j < kSymWarps * npad; j += blockDim.x) part[j] = 0.0;
   __syncthreads();
+  if (STORE_V && dps) fused_dp_t(dps[blockIdx.x], abc, xs, d.ns, tbuf);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double* pw = part + warp * npad;
   const int ntiles = d.nb * (d.nb + 1) / 2;
@@ -241,7 +272,10 @@ __global__ void k_dp_t(const OpSub* __restrict__ subs, const DpSub* __restrict__
 // subdomain order) of the per-subdomain entries -> deterministic assembly
 __global__ void k_coarse_gather(const int* __restrict__ optr, const int* __restrict__ oidx,
                                 const double* __restrict__ tbuf, int nc, double* __restrict__ out,
-                                double sign, const double* __restrict__ add) {
+                                double sign, const double* __restrict__ add,
+                                double* __restrict__ zero_y = nullptr, int ny = 0) {
+  if (zero_y)  // the apply's output is zeroed here, between phase 1 and phase 2
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ny; i += gridDim.x * blockDim.x) zero_y[i] = 0.0;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nc; i += gridDim.x * blockDim.x) {
     double v = add ? add[i] : 0.0;
     for (int k = optr[i]; k < optr[i + 1]; ++k) v += sign * tbuf[oidx[k]];
