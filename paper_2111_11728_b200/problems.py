@@ -247,3 +247,50 @@ def config5(seed: int = 1, sx: int = 32, sy: int = 16, n: int = 48, n_designs: i
 
 
 CONFIGS = {"C1": config1, "C2": config2, "C3": config3, "C4": config4, "C5": config5}
+
+
+# ---- academic presets (Fig. 2), SURVEY.md 8f rank 3 ----
+def _layers(n: int, count: int) -> np.ndarray:
+    """n x n module with `count` horizontal layers alternating stiff (1) /
+    compliant (0), stiff at the bottom; n must be divisible by count."""
+    if n % count:
+        raise ValueError("element rows per subdomain must be divisible by the layer count")
+    rows = (np.arange(n) // (n // count)) % 2 == 0
+    return np.repeat(rows[:, None], n, axis=1).astype(np.float64)
+
+
+def laminated_beam(n: int = 14, count: int = 9, layers: int = 7, contrast: float = 1e4,
+                   method: int = TFETI, scaling: int = KSCALING, precond: int = DIRICHLET) -> Problem:
+    """1 x 9 row of square modules with 7 alternating layers, clamped left,
+    tensile normal + tangential traction on the right edge."""
+    dens = _layers(n, layers)[None]
+    return Problem(count, 1, n, dens, np.zeros(count, np.int32), method=method, scaling=scaling,
+                   precond=precond, Emin=1.0 / contrast, p=1.0, dirichlet=left_clamp(count, 1, n),
+                   tractions=[(count - 1, RIGHT, 0, n, 1.0, 1.0)], name="laminated_beam")
+
+
+def grid3x3_layered(n: int = 14, layers: int = 7, contrast: float = 1e4, method: int = TFETI,
+                    scaling: int = KSCALING, precond: int = DIRICHLET) -> Problem:
+    """3 x 3 grid of layered modules (cross points)."""
+    dens = _layers(n, layers)[None]
+    return Problem(3, 3, n, dens, np.zeros(9, np.int32), method=method, scaling=scaling, precond=precond,
+                   Emin=1.0 / contrast, p=1.0, dirichlet=left_clamp(3, 3, n),
+                   tractions=[(sj * 3 + 2, RIGHT, 0, n, 1.0, 1.0) for sj in range(3)], name="grid3x3_layered")
+
+
+def grid4x4_inclusion(n: int = 8, contrast: float = 1e4, inclusion: int = None, method: int = TFETI,
+                      scaling: int = KSCALING, precond: int = DIRICHLET) -> Problem:
+    """4 x 4 grid of compliant modules each with a centred stiff square
+    inclusion that does not touch the module boundary."""
+    inc = n // 2 if inclusion is None else inclusion
+    d = np.zeros((n, n))
+    a = (n - inc) // 2
+    if inc > 0:
+        d[a:a + inc, a:a + inc] = 1.0
+    return Problem(4, 4, n, d[None], np.zeros(16, np.int32), method=method, scaling=scaling, precond=precond,
+                   Emin=1.0 / contrast, p=1.0, dirichlet=left_clamp(4, 4, n),
+                   tractions=[(sj * 4 + 3, RIGHT, 0, n, 1.0, 1.0) for sj in range(4)], name="grid4x4_inclusion")
+
+
+PRESETS = {"laminated_beam": laminated_beam, "grid3x3_layered": grid3x3_layered,
+           "grid4x4_inclusion": grid4x4_inclusion}

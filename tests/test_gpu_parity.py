@@ -18,6 +18,8 @@ roundoff-chaotic (the double oracle and the refined oracle differ by up to
 roundoff spread (+1)."""
 ACC_FACTOR = 10.0
 
+import os
+
 import numpy as np
 import pytest
 
@@ -274,3 +276,48 @@ def test_recovered_interface_jump(name, oracle_mod):
                 vals.setdefault(key, []).append(u[s, 2 * (iy * (n + 1) + ix):2 * (iy * (n + 1) + ix) + 2])
     spread = max(np.abs(np.array(v) - v[0]).max() for v in vals.values())
     assert spread <= 1e-6 * np.abs(u).max()
+
+
+@pytest.mark.parametrize("preset", ["laminated_beam", "grid3x3_layered", "grid4x4_inclusion"])
+def test_twelve_variant_grid(preset, oracle_mod, tmp_path):
+    """The paper's 12-variant protocol on the desk-scale
+    academic presets: GPU vs oracle iteration counts, FO/RRS exact to +-1,
+    single direction within 10% (roundoff-chaotic, see module docstring)."""
+    import subprocess, sys, csv as _csv
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = tmp_path / preset
+    r = subprocess.run([sys.executable, os.path.join(root, "tools", "run_grid.py"), "--problem", preset,
+                        "--out", str(out), "--oracle"], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr
+    rows = list(_csv.DictReader(open(out / "summary.csv")))
+    assert len(rows) == 12
+    for row in rows:
+        gi, oi = int(row["iterations"]), int(row["oracle_iterations"])
+        assert row["status"] == row["oracle_status"], row
+        tol = 1 if not row["variant"].endswith("single") else max(1, int(0.1 * oi))
+        assert abs(gi - oi) <= tol, row
+    header = open(out / "tfeti_k_rrs.csv").readline().strip()
+    assert header == "iter,eps_r,kept_dirs,F_applies,cum_local_solves"   # SPEC.md:571
+
+
+def test_modular_simp_loop(oracle_mod):
+    """a few modular SIMP/OC iterations driven by the GPU
+    solver: compliance equals f^T u of the state solve,
+    decreases over the run, and the volume constraint holds."""
+    from paper_2111_11728_b200 import simp
+    n, sx, sy = 8, 6, 2
+    types = np.array([0, 1, 2, 2, 1, 0] * 2, np.int32)          # mirror-symmetric module layout
+    gxn = sx * n + 1
+    prob = pb.Problem(sx, sy, n, np.full((3, n, n), 0.5), types, method=pb.FETIDP, scaling=pb.KSCALING,
+                      precond=pb.DIRICHLET, Emin=1e-9, dirichlet=pb.bottom_corner_pins(sx, sy, n),
+                      point_loads=[((sy * n) * gxn + (sx * n) // 2, 1, -1.0)])
+    st = simp.optimize(prob, iterations=8, volfrac=0.5, directions=2)
+    c = st.compliance
+    assert all(s["status"] == 0 for s in st.solves)
+    assert c[-1] < c[0]
+    assert abs(st.volume[-1] - 0.5) < 1e-4
+    # compliance of the first (uniform) design against the oracle's f^T u
+    o = oracle_mod.Oracle(prob.replace(densities=np.full((3, n, n), 0.5)))
+    lo, to = o.solve(tol=1e-10, max_it=1000, directions=1)
+    fu = float((o.loads() * o.recover(lo)).sum())
+    assert abs(c[0] - fu) <= 1e-5 * abs(fu)
