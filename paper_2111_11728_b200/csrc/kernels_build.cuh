@@ -169,26 +169,19 @@ __global__ void k_nd_extract_root(const NdDev* nodes, int root, const long long*
 // -------------------------------------------------- blocked elimination --
 // Right-looking blocked partial Cholesky in global memory, one CTA per
 // frontal: panel factor in smem, row-wise triangular solve of the panel,
-// 64x64-tiled rank-kNB update of the lower trailing matrix on FP64 tensor
-// cores (mma.sync.m8n8k4.f64, 8 warps as 2 x 4 warp tiles of 32 x 16).
-__device__ __forceinline__ void dmma_884(double& d0, double& d1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-               : "+d"(d0), "+d"(d1)
-               : "d"(a), "d"(b));
-}
-constexpr int kTpad = kTile + 4;   // 2 wavefronts per fragment load
-
+// 64x64-tiled rank-kNB update of the lower trailing matrix (4x4 register
+// tiles on the DFMA pipe; a DMMA variant measured ~15% slower here because
+// the update is bound by the global read-modify-write of the tiles).
 __global__ void __launch_bounds__(kThreads) k_front_elim_large(const FrontDesc* fds, double* base,
                                                                int* status) {
   const FrontDesc f = fds[blockIdx.x];
   double* A = base + f.off;
   const int nf = f.nf, ne = f.ne, ld = f.ld;
   __shared__ double D[kNB * (kNB + 1)];
-  __shared__ double LiT[kNB * kTpad];
-  __shared__ double LjT[kNB * kTpad];
+  __shared__ double LiT[kNB * kTile];
+  __shared__ double LjT[kNB * kTile];
   const int tid = threadIdx.x;
-  const int lane = tid & 31, warp = tid >> 5;
-  const int wr = warp >> 2, wc = warp & 3;   // warp tile rows 32*wr.., cols 16*wc..
+  const int tx = tid & 15, ty = tid >> 4;
   for (int k0 = 0; k0 < ne; k0 += kNB) {
     const int kb = min(kNB, ne - k0);
     const int k1 = k0 + kb;
@@ -222,46 +215,39 @@ __global__ void __launch_bounds__(kThreads) k_front_elim_large(const FrontDesc* 
     __syncthreads();
     const int mt = nf - k1;
     const int nt = (mt + kTile - 1) / kTile;
-    const int kq = (kb + 3) & ~3;
     for (int tj = 0; tj < nt; ++tj) {
-      for (int idx = tid; idx < kNB * kTile; idx += kThreads) {
+      for (int idx = tid; idx < kb * kTile; idx += kThreads) {
         const int c = idx / kTile, r = idx - c * kTile;
         const int row = tj * kTile + r;
-        LjT[c * kTpad + r] = (c < kb && row < mt) ? A[(size_t)(k0 + c) * ld + k1 + row] : 0.0;
+        LjT[c * kTile + r] = row < mt ? A[(size_t)(k0 + c) * ld + k1 + row] : 0.0;
       }
       for (int ti = tj; ti < nt; ++ti) {
-        for (int idx = tid; idx < kNB * kTile; idx += kThreads) {
+        for (int idx = tid; idx < kb * kTile; idx += kThreads) {
           const int c = idx / kTile, r = idx - c * kTile;
           const int row = ti * kTile + r;
-          LiT[c * kTpad + r] = (c < kb && row < mt) ? A[(size_t)(k0 + c) * ld + k1 + row] : 0.0;
+          LiT[c * kTile + r] = row < mt ? A[(size_t)(k0 + c) * ld + k1 + row] : 0.0;
         }
         __syncthreads();
-        double acc[4][2][2];
+        double acc[4][4] = {};
+        for (int c = 0; c < kb; ++c) {
+          double li[4], lj[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+          for (int q = 0; q < 4; ++q) {
+            li[q] = LiT[c * kTile + tx + 16 * q];
+            lj[q] = LjT[c * kTile + ty + 16 * q];
+          }
 #pragma unroll
-          for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-        for (int k4 = 0; k4 < kq; k4 += 4) {
-          double af[4], bf[2];
+          for (int q = 0; q < 4; ++q)
 #pragma unroll
-          for (int i = 0; i < 4; ++i) af[i] = LiT[(k4 + (lane & 3)) * kTpad + wr * 32 + i * 8 + (lane >> 2)];
-#pragma unroll
-          for (int j = 0; j < 2; ++j) bf[j] = LjT[(k4 + (lane & 3)) * kTpad + wc * 16 + j * 8 + (lane >> 2)];
-#pragma unroll
-          for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int j = 0; j < 2; ++j) dmma_884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+            for (int w = 0; w < 4; ++w) acc[q][w] = fma(li[q], lj[w], acc[q][w]);
         }
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int ri = ti * kTile + wr * 32 + i * 8 + (lane >> 2);
+        for (int w = 0; w < 4; ++w) {
+          const int cj = tj * kTile + ty + 16 * w;
 #pragma unroll
-          for (int j = 0; j < 2; ++j) {
-            const int cj = tj * kTile + wc * 16 + j * 8 + 2 * (lane & 3);
-            if (ri < mt) {
-              if (cj < mt && ri >= cj) A[(size_t)(k1 + cj) * ld + k1 + ri] -= acc[i][j][0];
-              if (cj + 1 < mt && ri >= cj + 1) A[(size_t)(k1 + cj + 1) * ld + k1 + ri] -= acc[i][j][1];
-            }
+          for (int q = 0; q < 4; ++q) {
+            const int ri = ti * kTile + tx + 16 * q;
+            if (ri < mt && cj < mt && ri >= cj) A[(size_t)(k1 + cj) * ld + k1 + ri] -= acc[q][w];
           }
         }
         __syncthreads();
