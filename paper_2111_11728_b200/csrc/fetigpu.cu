@@ -957,12 +957,24 @@ struct Ctx {
     corr.zero(st);
     k_proj_gather<<<dim3(su.Ns, ncols), kThreads, 0, st>>>(d_pj.p, d_pcrows.p, d_pjcoef.p, d_RT.p, d_rt_off.p, v, 1,
                                                           g.p, nc, -1.0, ncols);
-    k_small_gemm<<<dim3(grid_for(nc), ncols), kThreads, 0, st>>>(d_H.p, nc, g.p, nc, h.p, nc);
+    small_gemm(g.p, h.p, ncols);
     k_proj_scatter<<<dim3(su.Ns, ncols), kThreads, 0, st>>>(d_pj.p, d_pcrows.p, d_pjcoef.p, d_RT.p, d_rt_off.p,
                                                            h.p, nc, corr.p, 1, ncols);
     k_add<<<grid_for((long long)su.m * ncols), kThreads, 0, st>>>(su.m * ncols, corr.p, v, 0, 0);
     LAUNCH_CHECK();
     CK(cudaStreamSynchronize(st));
+  }
+
+  // h = H g for ncols columns of length 3N_s (H symmetric, column-major)
+  void small_gemm(const double* g, double* h, int ncols) {
+    const int nc = 3 * su.Ns;
+    if (ncols == 1) {
+      k_dense_gemv<<<grid_for((long long)nc * 32), kThreads, 0, st>>>(d_H.p, nc, g, h);
+    } else {
+      const double one = 1.0, zero = 0.0;
+      CB(cublasDgemm(cb, CUBLAS_OP_N, CUBLAS_OP_N, nc, ncols, nc, &one, d_H.p, nc, g, nc, &zero, h, nc));
+    }
+    LAUNCH_CHECK();
   }
 
   // corr = P v - v for ncols columns (T-FETI); caller adds
@@ -979,7 +991,7 @@ struct Ctx {
     }
     k_proj_gather<<<dim3(su.Ns, ncols), kThreads, 0, st>>>(d_pj.p, d_pcrows.p, d_pjcoef.p, d_RT.p,
                                                           d_rt_off.p, v, ldv, gp, nc, gsign);
-    k_small_gemm<<<dim3(grid_for(nc), ncols), kThreads, 0, st>>>(d_H.p, nc, gp, nc, hp, nc);
+    small_gemm(gp, hp, ncols);
     for (int c = 0; c < ncols; ++c) CK(cudaMemsetAsync(corr + (size_t)c * ldc, 0, su.m * 8, st));
     k_proj_scatter<<<dim3(su.Ns, ncols), kThreads, 0, st>>>(d_pj.p, d_pcrows.p, d_pjcoef.p, d_RT.p,
                                                            d_rt_off.p, hp, nc, corr, ldc);
@@ -1020,7 +1032,7 @@ struct Ctx {
       gap.upload(su.gap, st);
       k_sub<<<grid_for(m), kThreads, 0, st>>>(m, d_v1.p, gap.p, d_d.p);
       // lambda0 = G^T (G G^T)^{-1} e = -B R H e
-      k_small_gemm<<<grid_for(3 * su.Ns), kThreads, 0, st>>>(d_H.p, 3 * su.Ns, d_e.p, 3 * su.Ns, d_h.p, 3 * su.Ns);
+      small_gemm(d_e.p, d_h.p, 1);
       CK(cudaMemsetAsync(d_v2.p, 0, m * 8, st));
       k_proj_scatter<<<su.Ns, kThreads, 0, st>>>(d_pj.p, d_pcrows.p, d_pjcoef.p, d_RT.p, d_rt_off.p, d_h.p,
                                                  3 * su.Ns, d_v2.p, m);
@@ -1057,7 +1069,7 @@ struct Ctx {
       k_proj_gather<<<su.Ns, kThreads, 0, st>>>(d_pj.p, d_pcrows.p, d_pjcoef.p, d_RT.p, d_rt_off.p, d_v2.p, m,
                                                 d_g.p, 3 * Ns, -1.0);
       alpha.alloc(3 * (size_t)Ns);
-      k_small_gemm<<<grid_for(3 * Ns), kThreads, 0, st>>>(d_H.p, 3 * Ns, d_g.p, 3 * Ns, alpha.p, 3 * Ns);
+      small_gemm(d_g.p, alpha.p, 1);
       launch_bnd_rhs(lambda_dev, nullptr);
     } else {
       // u_c = Kbar^{-1} (fbar_c + F_rc^T lambda)
