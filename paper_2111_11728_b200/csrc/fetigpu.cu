@@ -139,7 +139,7 @@ struct Ctx {
   // scratch vectors
   DBuf<double> d_v1, d_v2, d_v3, d_g, d_h, d_partial;
   DBuf<double> d_d, d_lam0;
-  DBuf<unsigned int> d_counter;
+  DBuf<unsigned int> d_counter, d_counter2;
   bool have_rhs = false;
   // stats
   double op_bytes = 0, op_flops = 0, main_bytes = 0;
@@ -685,6 +685,8 @@ struct Ctx {
     d_partial.alloc(4 * kDotBlocks);
     d_counter.alloc(1);
     d_counter.zero(st);
+    d_counter2.alloc(1);
+    d_counter2.zero(st);
     d_d.alloc(m); d_lam0.alloc(m);
 
     // ---- GEMV row split: aim for >= 4 CTAs per SM when subdomains are few
@@ -1102,7 +1104,7 @@ struct Ctx {
     for (auto& p : pairs) { a.a[k] = p.first; a.b[k] = p.second; ++k; }
     a.npairs = k;
     a.n = su.m;
-    const int nblk = std::max(1, std::min(kDotBlocks, (su.m + 4 * kThreads - 1) / (4 * kThreads)));
+    const int nblk = std::max(1, std::min(kDotBlocks, (su.m + 4095) / 4096));
     k_dot_fused<<<nblk, kThreads, 0, st>>>(a, d_partial.p, d_counter.p, out);
     LAUNCH_CHECK();
   }
@@ -1348,11 +1350,14 @@ int Ctx::solve(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_trace* 
   cnt.alloc(1);
   cnt.zero(st);
   const int cap = std::max(1, o.max_it);
+  DBuf<double> psi_part;
   if (fo) {
     Wst.alloc((size_t)m * cap);
     Qst.alloc((size_t)m * cap);
     psi.alloc(cap);
   }
+  const int psi_S = std::max(1, std::min(16, m / 2048));
+  if (fo) psi_part.alloc((size_t)cap * psi_S);
   Scal* hs = nullptr;
   CK(cudaMallocHost(&hs, sizeof(Scal)));
   std::unique_ptr<Scal, decltype(&cudaFreeHost)> hs_guard(hs, cudaFreeHost);
@@ -1400,7 +1405,8 @@ int Ctx::solve(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_trace* 
       k_inc<<<1, 1, 0, st>>>(cnt.p);
       CK(cudaMemcpyAsync(w.p, z.p, m * 8, cudaMemcpyDeviceToDevice, st));
       for (int pss = 0; pss < passes; ++pss) {
-        k_fo_psi<<<cap, kThreads, 0, st>>>(Qst.p, m, cnt.p, w.p, psi.p);
+        k_fo_psi_seg<<<dim3(cap, psi_S), 256, 0, st>>>(Qst.p, m, cnt.p, w.p, psi_part.p);
+        k_fo_psi_sum<<<(cap + 255) / 256, 256, 0, st>>>(cnt.p, psi_S, psi_part.p, psi.p);
         k_fo_sub<<<(m + 31) / 32, 256, 0, st>>>(Wst.p, m, cnt.p, psi.p, w.p);
       }
     } else {

@@ -519,6 +519,46 @@ __global__ void __launch_bounds__(256) k_fo_sub(const double* __restrict__ W, in
     w[i] -= s;
   }
 }
+// psi_j = q_j^T w for j < *cnt on a (column x row-segment) grid: CTA (j, s)
+// reduces rows [s*chunk, (s+1)*chunk) of column j into partial[j*S + s];
+// k_fo_psi_sum adds the S partials of each column in fixed order.
+__global__ void __launch_bounds__(256) k_fo_psi_seg(const double* __restrict__ Q, int m,
+                                                    const int* __restrict__ cnt,
+                                                    const double* __restrict__ w,
+                                                    double* __restrict__ partial) {
+  const int j = blockIdx.x;
+  if (j >= *cnt) return;
+  const int S = gridDim.y, s = blockIdx.y;
+  const int chunk = (m + S - 1) / S;
+  const int i0 = s * chunk, i1 = min(m, i0 + chunk);
+  const double* q = Q + (size_t)j * m;
+  double a0 = 0.0, a1 = 0.0;
+  int i = i0 + threadIdx.x;
+  for (; i + 256 < i1; i += 512) {
+    a0 = fma(q[i], w[i], a0);
+    a1 = fma(q[i + 256], w[i + 256], a1);
+  }
+  if (i < i1) a0 = fma(q[i], w[i], a0);
+  double acc = warp_sum(a0 + a1);
+  __shared__ double red[8];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int k = 0; k < 8; ++k) t += red[k];
+    partial[(size_t)j * S + s] = t;
+  }
+}
+__global__ void k_fo_psi_sum(const int* __restrict__ cnt, int S, const double* __restrict__ partial,
+                             double* __restrict__ psi) {
+  const int c = *cnt;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < c; j += gridDim.x * blockDim.x) {
+    double t = 0.0;
+    for (int s = 0; s < S; ++s) t += partial[(size_t)j * S + s];
+    psi[j] = t;
+  }
+}
+
 __global__ void k_fo_store2(int n, const Scal* sc, const int* __restrict__ cnt,
                             const double* __restrict__ w, const double* __restrict__ q,
                             double* __restrict__ Wst, double* __restrict__ Qst) {
