@@ -323,3 +323,18 @@ def test_modular_simp_loop(oracle_mod):
     lo, to = o.solve(tol=1e-10, max_it=1000, directions=1)
     fu = float((o.loads() * o.recover(lo)).sum())
     assert abs(c[0] - fu) <= 1e-5 * abs(fu)
+
+
+def test_floating_tfeti_rank_deficient_coarse(oracle_mod):
+    """No supports, self-equilibrated load: G G^T has rank 3N_s - 3 and the
+    rank-revealing filter keeps 9 of 12 rows; the GPU solve
+    matches the oracle and the displacements agree up to rigid motion."""
+    from paper_2111_11728_b200 import engine
+    p = pb.config1(sx=2, sy=2, n=4).replace(dirichlet=[], tractions=[(1, pb.RIGHT, 0, 4, 1.0, 0.0),
+                                                                        (0, pb.LEFT, 0, 4, -1.0, 0.0)])
+    g, o = engine.FetiSystem(p), oracle_mod.Oracle(p)
+    assert g.stats()["n_kept"] == o.n_kept == 9
+    lg, tg = g.solve(tol=1e-10, directions=1)
+    lo, to = o.solve(tol=1e-10, directions=1)
+    assert tg["status"] == to["status"] == 0 and abs(tg["iterations"] - to["iterations"]) <= 1
+    assert rel(g.project(lg - lo), lo) < 1e-8       # same multipliers on range(P)
