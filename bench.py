@@ -409,6 +409,8 @@ def main():
             ("C3-tfeti", lambda: pb.config3(method=0), dict(tol=1e-6, max_it=2000, directions=1)),
             ("C3-fetidp", lambda: pb.config3(method=1), dict(tol=1e-6, max_it=2000, directions=1)),
             ("C5", pb.config5, dict(tol=1e-6, max_it=200, directions=2)),
+            ("C4-cg", pb.config4, dict(tol=1e-6, max_it=3000, directions=0)),
+            ("C4-fo", pb.config4, dict(tol=1e-6, max_it=3000, directions=1)),
         ])
 
     cpu = None

@@ -1104,7 +1104,7 @@ struct Ctx {
     for (auto& p : pairs) { a.a[k] = p.first; a.b[k] = p.second; ++k; }
     a.npairs = k;
     a.n = su.m;
-    const int nblk = std::max(1, std::min(kDotBlocks, (su.m + 4095) / 4096));
+    const int nblk = std::max(1, std::min(kDotBlocks, (su.m + 1023) / 1024));
     k_dot_fused<<<nblk, kThreads, 0, st>>>(a, d_partial.p, d_counter.p, out);
     LAUNCH_CHECK();
   }
@@ -1356,7 +1356,7 @@ int Ctx::solve(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_trace* 
     Qst.alloc((size_t)m * cap);
     psi.alloc(cap);
   }
-  const int psi_S = std::max(1, std::min(16, m / 2048));
+  const int psi_S = std::max(1, std::min(64, m / 2048));
   if (fo) psi_part.alloc((size_t)cap * psi_S);
   Scal* hs = nullptr;
   CK(cudaMallocHost(&hs, sizeof(Scal)));

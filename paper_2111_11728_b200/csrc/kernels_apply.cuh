@@ -283,21 +283,42 @@ __global__ void k_coarse_gather(const int* __restrict__ optr, const int* __restr
   }
 }
 
-// dense row-major GEMV y = M x (one warp per row), n x n
-__global__ void k_dense_gemv(const double* __restrict__ M, int n, const double* __restrict__ x,
-                             double* __restrict__ y) {
+// dense row-major GEMV y = M x (one warp per row), n x n; 128-bit loads and
+// four independent accumulators keep ~4 KB in flight per warp
+__global__ void __launch_bounds__(256) k_dense_gemv(const double* __restrict__ M, int n,
+                                                    const double* __restrict__ x,
+                                                    double* __restrict__ y) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
   for (int i = warp; i < n; i += nwarps) {
     const double* Mi = M + (size_t)i * n;
-    double acc = 0.0;
-    for (int j = lane; j < n; j += 32) acc = fma(Mi[j], x[j], acc);
-    acc = warp_sum(acc);
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    if ((n & 1) == 0) {
+      const double2* M2 = reinterpret_cast<const double2*>(Mi);
+      const int n2 = n >> 1;
+      int j = lane;
+      for (; j + 32 < n2; j += 64) {
+        const double2 u = __ldcs(M2 + j), v = __ldcs(M2 + j + 32);
+        a0 = fma(u.x, x[2 * j], a0);
+        a1 = fma(u.y, x[2 * j + 1], a1);
+        a2 = fma(v.x, x[2 * j + 64], a2);
+        a3 = fma(v.y, x[2 * j + 65], a3);
+      }
+      for (; j < n2; j += 32) {
+        const double2 u = __ldcs(M2 + j);
+        a0 = fma(u.x, x[2 * j], a0);
+        a1 = fma(u.y, x[2 * j + 1], a1);
+      }
+    } else {
+      for (int j = lane; j < n; j += 32) a0 = fma(Mi[j], x[j], a0);
+    }
+    const double acc = warp_sum((a0 + a1) + (a2 + a3));
     if (lane == 0) y[i] = acc;
   }
 }
 
-// FETI-DP phase 2: v_s += A_bc u[cmap]; scatter sign * v_s
+// FETI-DP phase 2: v_s += A_bc u[cmap]; scatter sign * v_s.  A_bc rows are
+// n_c (4 or 8) contiguous doubles, read as 128-bit pairs.
 __global__ void k_dp_phase2(const OpSub* __restrict__ subs, const DpSub* __restrict__ dps,
                             const int* __restrict__ rows, const double* __restrict__ coefs,
                             const double* __restrict__ abc, const int* __restrict__ cmap,
@@ -307,12 +328,22 @@ __global__ void k_dp_phase2(const OpSub* __restrict__ subs, const DpSub* __restr
   const OpSub d = subs[s];
   const DpSub p = dps[s];
   __shared__ double uc[8];
-  if (threadIdx.x < p.nc) uc[threadIdx.x] = u[cmap[p.cmap_off + threadIdx.x]];
+  if (threadIdx.x < 8) uc[threadIdx.x] = threadIdx.x < p.nc ? u[cmap[p.cmap_off + threadIdx.x]] : 0.0;
   __syncthreads();
   const double* Ab = abc + p.abc_off;
+  const bool vec = (p.nc & 1) == 0 && (p.abc_off & 1) == 0;
   for (int j = threadIdx.x; j < d.ns; j += blockDim.x) {
     double v = vbuf ? vscale * vbuf[p.v_off + j] : 0.0;
-    for (int c = 0; c < p.nc; ++c) v = fma(Ab[(size_t)j * p.nc + c], uc[c], v);
+    if (vec) {
+      const double2* A2 = reinterpret_cast<const double2*>(Ab + (size_t)j * p.nc);
+      for (int c = 0; c < (p.nc >> 1); ++c) {
+        const double2 a = __ldcs(A2 + c);
+        v = fma(a.x, uc[2 * c], v);
+        v = fma(a.y, uc[2 * c + 1], v);
+      }
+    } else {
+      for (int c = 0; c < p.nc; ++c) v = fma(Ab[(size_t)j * p.nc + c], uc[c], v);
+    }
     const int r = rows[d.map_off + j];
     if (r >= 0) atomicAdd(y + r, coefs[d.map_off + j] * v);
   }
@@ -402,7 +433,7 @@ struct DotArgs {
   int npairs;
   int n;
 };
-constexpr int kDotBlocks = 296;
+constexpr int kDotBlocks = 1184;
 __global__ void __launch_bounds__(kThreads) k_dot_partial(DotArgs args, double* partial) {
   double acc[4] = {0, 0, 0, 0};
   const int stride = gridDim.x * blockDim.x;
