@@ -8,7 +8,9 @@
 #include <cublas_v2.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <memory>
 #include <numeric>
@@ -71,13 +73,58 @@ struct DBuf {
 };
 
 static inline int round_up(int v, int a) { return (v + a - 1) / a * a; }
+
+// FETIGPU_TIMING=1: host wall-clock marks of the build phases on stderr
+struct PhaseTimer {
+  bool on;
+  std::chrono::steady_clock::time_point t0, last;
+  PhaseTimer() {
+    const char* e = getenv("FETIGPU_TIMING");
+    on = e && e[0] == '1';
+    t0 = last = std::chrono::steady_clock::now();
+  }
+  void mark(const char* what, cudaStream_t st) {
+    if (!on) return;
+    cudaStreamSynchronize(st);
+    const auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "[fetigpu] %-28s %8.2f ms (total %8.2f)\n", what,
+            std::chrono::duration<double, std::milli>(now - last).count(),
+            std::chrono::duration<double, std::milli>(now - t0).count());
+    last = now;
+  }
+};
 static inline int grid_for(long long n, int threads = kThreads, int cap = 148 * 16) {
   long long g = (n + threads - 1) / threads;
   return (int)std::max<long long>(1, std::min<long long>(g, cap));
 }
 
+// Grow-only device scratch buffers keyed by slot: build temporaries reuse
+// them instead of cudaMalloc/cudaFree per level / chunk (cudaFree is a
+// device-wide synchronization).
+struct Scratch {
+  std::vector<std::unique_ptr<DBuf<char>>> bufs;
+  void* get(int id, size_t bytes) {
+    if ((int)bufs.size() <= id) bufs.resize(id + 1);
+    if (!bufs[id]) bufs[id] = std::make_unique<DBuf<char>>();
+    if (bufs[id]->n < bytes) bufs[id]->alloc(bytes + bytes / 4);
+    return bufs[id]->p;
+  }
+  template <class T>
+  T* upload(int id, const std::vector<T>& v, cudaStream_t st) {
+    T* p = static_cast<T*>(get(id, std::max<size_t>(1, v.size()) * sizeof(T)));
+    if (!v.empty()) CK(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, st));
+    return p;
+  }
+  void release(int id) {
+    if (id < (int)bufs.size() && bufs[id]) bufs[id]->release();
+  }
+};
+enum ScratchId { kScWs = 0, kScDescA, kScDescB, kScSlots, kScSrc, kScExt, kScMo, kScMl, kScAo, kScKo, kScFo,
+                 kScMisc };
+
 struct Ctx {
   Setup su;
+  Scratch scratch;
   cudaStream_t st = nullptr;
   cublasHandle_t cb = nullptr;
   bool built = false;
@@ -203,18 +250,37 @@ struct Ctx {
       if (f.nf <= kSmallFront && f.ld == f.nf) { small.push_back(f); nfmax = std::max(nfmax, f.nf); }
       else large.push_back(f);
     }
-    DBuf<FrontDesc> ds, dl;
     if (!small.empty()) {
-      ds.upload(small, st);
-      k_front_elim_small<<<(int)small.size(), kThreads, nfmax * nfmax * 8, st>>>(ds.p, base, d_status.p);
+      FrontDesc* ds = scratch.upload(kScDescA, small, st);
+      const int thr = nfmax <= 64 ? 64 : (nfmax <= 96 ? 128 : kThreads);
+      k_front_elim_small<<<(int)small.size(), thr, nfmax * nfmax * 8, st>>>(ds, base, d_status.p);
       LAUNCH_CHECK();
     }
     if (!large.empty()) {
-      dl.upload(large, st);
-      k_front_elim_large<<<(int)large.size(), kThreads, 0, st>>>(dl.p, base, d_status.p);
+      FrontDesc* dl = scratch.upload(kScDescB, large, st);
+      bpc(dl, large, base);
+    }
+  }
+
+  // batched blocked partial Cholesky over all frontals in `fs` (device copy `d`)
+  void bpc(const FrontDesc* d, const std::vector<FrontDesc>& fs, double* base) {
+    const char* legacy = getenv("FETIGPU_LEGACY_ELIM");
+    if (legacy && legacy[0] == '1') {
+      k_front_elim_large<<<(int)fs.size(), kThreads, 0, st>>>(d, base, d_status.p);
+      LAUNCH_CHECK();
+      return;
+    }
+    int ne_max = 0, nf_max = 0;
+    for (auto& f : fs) { ne_max = std::max(ne_max, f.ne); nf_max = std::max(nf_max, f.nf); }
+    const int B = (int)fs.size();
+    for (int k0 = 0; k0 < ne_max; k0 += kNB) {
+      k_bpc_diag<<<B, kThreads, 0, st>>>(d, base, k0, d_status.p);
+      const int rows = std::max(1, nf_max - k0 - 1);
+      k_bpc_trsm<<<dim3((rows + kThreads - 1) / kThreads, B), kThreads, 0, st>>>(d, base, k0);
+      const int nt = (rows + kTile - 1) / kTile;
+      k_bpc_update<<<dim3(nt * (nt + 1) / 2, B), kThreads, 0, st>>>(d, base, k0);
       LAUNCH_CHECK();
     }
-    CK(cudaStreamSynchronize(st));
   }
 
   void build_nd() {
@@ -253,10 +319,10 @@ struct Ctx {
     for (long long s : P.height_stride) per_design += s;
     size_t free_b = 0, tot_b = 0;
     CK(cudaMemGetInfo(&free_b, &tot_b));
-    const long long budget = std::max<long long>(256ll << 20, (long long)(free_b * 0.3));
+    // workspace capped at 8 GB: more, smaller chunks beat one huge cold cudaMalloc
+    const long long budget = std::max<long long>(256ll << 20, std::min<long long>(8ll << 30, (long long)(free_b * 0.3)));
     const int chunk = (int)std::max<long long>(1, std::min<long long>(D, budget / (per_design * 8)));
-    DBuf<double> ws;
-    ws.alloc((size_t)chunk * per_design);
+    double* ws_p = static_cast<double*>(scratch.get(kScWs, (size_t)chunk * per_design * 8));
     // per-height node lists split by size
     std::vector<std::vector<int>> hsmall(P.max_height + 1), hlarge(P.max_height + 1);
     std::vector<int> hnfmax(P.max_height + 1, 0);
@@ -278,14 +344,15 @@ struct Ctx {
       long long acc = 0;
       for (int h = 0; h <= P.max_height; ++h) { hbase[h] = acc; acc += (long long)dc * P.height_stride[h]; }
       d_hbase.upload(hbase, st);
-      NdArgs a{d_nodes.p, nullptr, d_hbase.p, d_hstride.p, ws.p, d_elem_ids.p, d_emap.p, d_cmaps.p,
+      NdArgs a{d_nodes.p, nullptr, d_hbase.p, d_hstride.p, ws_p, d_elem_ids.p, d_emap.p, d_cmaps.p,
                d_dens.p, n, d0, su.E0, su.Emin, su.p, keep_factors ? d_ndfac.p : nullptr,
                P.factor_stride, d_status.p};
       for (int h = 0; h <= P.max_height; ++h) {
         if (!hsmall[h].empty()) {
           a.level_nodes = dsm[h].p;
           dim3 grid((unsigned)hsmall[h].size(), dc);
-          k_nd_small<<<grid, kThreads, hnfmax[h] * hnfmax[h] * 8, st>>>(a);
+          const int thr = hnfmax[h] <= 64 ? 64 : (hnfmax[h] <= 96 ? 128 : kThreads);
+          k_nd_small<<<grid, thr, hnfmax[h] * hnfmax[h] * 8, st>>>(a);
           LAUNCH_CHECK();
         }
         if (!hlarge[h].empty()) {
@@ -300,19 +367,16 @@ struct Ctx {
               fds.push_back({hbase[h] + (long long)dl * P.height_stride[h] + nd.off, nd.nf, nd.ne, nd.nf,
                              FETIGPU_E_SINGULAR_INTERIOR});
             }
-          DBuf<FrontDesc> dfd;
-          dfd.upload(fds, st);
-          k_front_elim_large<<<(int)fds.size(), kThreads, 0, st>>>(dfd.p, ws.p, d_status.p);
-          LAUNCH_CHECK();
+          FrontDesc* dfd = scratch.upload(kScDescB, fds, st);
+          bpc(dfd, fds, ws_p);
           if (keep_factors) {
             k_nd_copy_factors<<<grid, kThreads, 0, st>>>(a);
             LAUNCH_CHECK();
           }
-          CK(cudaStreamSynchronize(st));
         }
       }
       k_nd_extract_root<<<dim3(grid_for((long long)nb * nb), dc), kThreads, 0, st>>>(
-          d_nodes.p, P.root, d_hbase.p, d_hstride.p, ws.p, d_S.p, nb, d0);
+          d_nodes.p, P.root, d_hbase.p, d_hstride.p, ws_p, d_S.p, nb, d0);
       LAUNCH_CHECK();
       CK(cudaStreamSynchronize(st));
     }
@@ -345,9 +409,9 @@ struct Ctx {
     dext.upload(ext_all, st);
     size_t free_b = 0, tot_b = 0;
     CK(cudaMemGetInfo(&free_b, &tot_b));
-    const long long budget = std::max<long long>(256ll << 20, (long long)(free_b * 0.3)) / 8;
+    const long long budget =
+        std::max<long long>(256ll << 20, std::min<long long>(8ll << 30, (long long)(free_b * 0.3))) / 8;
     size_t i0 = 0;
-    DBuf<double> ws;
     while (i0 < slots.size()) {
       long long used = 0;
       size_t i1 = i0;
@@ -361,41 +425,40 @@ struct Ctx {
         chunk.push_back(d);
         ++i1;
       }
-      ws.alloc(used);
-      DBuf<SlotDev> dchunk;
-      dchunk.upload(chunk, st);
+      double* ws = static_cast<double*>(scratch.get(kScWs, (size_t)used * 8));
+      SlotDev* dchunk = scratch.upload(kScSlots, chunk, st);
       const int nch = (int)chunk.size();
-      k_slot_assemble<<<dim3(64, nch), kThreads, 0, st>>>(dchunk.p, dsrc.p, dext.p, d_S.p, su.nb, ws.p);
+      k_slot_assemble<<<dim3(64, nch), kThreads, 0, st>>>(dchunk, dsrc.p, dext.p, d_S.p, su.nb, ws);
       LAUNCH_CHECK();
       std::vector<FrontDesc> fds;
       for (auto& c : chunk) fds.push_back({c.woff, c.nsrc + c.next, c.ne, c.nsrc + c.next, errcode});
-      eliminate(fds, ws.p);
+      eliminate(fds, ws);
       auto sub = [&](const std::vector<long long>& v) {
         return std::vector<long long>(v.begin() + i0, v.begin() + i1);
       };
-      DBuf<long long> dmo, dao, dko, dfo;
-      DBuf<int> dml;
-      dmo.upload(sub(out.mat_off), st);
-      dml.upload(std::vector<int>(out.mat_ld.begin() + i0, out.mat_ld.begin() + i1), st);
-      if (abc) { dao.upload(sub(out.abc_off), st); dko.upload(sub(out.kcc_off), st); }
-      k_slot_extract<<<dim3(32, nch), kThreads, 0, st>>>(dchunk.p, ws.p, dmo.p, dml.p, mats,
-                                                         nc_first ? 1 : 0, sign, abc ? dao.p : nullptr,
-                                                         abc, abc ? dko.p : nullptr, kcc);
+      long long* dmo = scratch.upload(kScMo, sub(out.mat_off), st);
+      int* dml = scratch.upload(kScMl, std::vector<int>(out.mat_ld.begin() + i0, out.mat_ld.begin() + i1), st);
+      long long* dao = abc ? scratch.upload(kScAo, sub(out.abc_off), st) : nullptr;
+      long long* dko = abc ? scratch.upload(kScKo, sub(out.kcc_off), st) : nullptr;
+      k_slot_extract<<<dim3(32, nch), kThreads, 0, st>>>(dchunk, ws, dmo, dml, mats, nc_first ? 1 : 0, sign, dao,
+                                                         abc, dko, kcc);
       LAUNCH_CHECK();
       if (fac) {
-        dfo.upload(sub(out.fac_off), st);
-        k_slot_factor<<<dim3(32, nch), kThreads, 0, st>>>(dchunk.p, ws.p, dfo.p, fac);
+        long long* dfo = scratch.upload(kScFo, sub(out.fac_off), st);
+        k_slot_factor<<<dim3(32, nch), kThreads, 0, st>>>(dchunk, ws, dfo, fac);
         LAUNCH_CHECK();
       }
-      CK(cudaStreamSynchronize(st));
+      if (i1 < slots.size()) CK(cudaStreamSynchronize(st));  // host vectors reused next chunk
       i0 = i1;
     }
     check_status();
   }
 
+  PhaseTimer ptimer;
   void build_ops() {
     const int Ns = su.Ns, nb = su.nb;
     const bool dp = su.method == FETIGPU_FETIDP;
+    ptimer.mark("build_ops start", st);
     // ---- operator slots
     const int nslot = (int)su.op_slots.size();
     SlotOut so;
@@ -416,8 +479,10 @@ struct Ctx {
     d_opmat.alloc(mo);
     d_opfac.alloc(fo);
     if (dp) { d_abc.alloc(ao); d_kccs.alloc(ko); }
+    ptimer.mark("op slot planning", st);
     run_slots(su.op_slots, so, d_opmat.p, -1.0, dp, dp ? d_abc.p : nullptr, dp ? d_kccs.p : nullptr,
               d_opfac.p, dp ? FETIGPU_E_SINGULAR_REMAINDER : FETIGPU_E_NOT_POSITIVE_DEFINITE);
+    ptimer.mark("op slots (device)", st);
     // slot src/ext lists for rhs / recovery
     {
       std::vector<int> src, ext, so_, eo_, fne;
@@ -434,50 +499,60 @@ struct Ctx {
       d_fac_off.upload(so.fac_off, st);
     }
     // ---- per-subdomain operator maps
+    // flat (subdomain, perimeter position) -> up to 3 (row, sign, weight) entries
     struct Ent { int row; double coef; double w; };
-    std::vector<std::vector<std::vector<Ent>>> ent(Ns);  // [s][perimeter pos] -> entries
-    for (int s = 0; s < Ns; ++s) ent[s].assign(nb, {});
+    KR = dp ? 1 : 3;
+    KRp = KR;
+    std::vector<Ent> ent((size_t)Ns * nb * 3);
+    std::vector<unsigned char> ecnt((size_t)Ns * nb, 0);
+    auto add_ent = [&](int s, int pos, Ent e) {
+      const size_t k = (size_t)s * nb + pos;
+      if (ecnt[k] >= KR) fail(FETIGPU_E_STATE, "too many dual rows per DOF");
+      ent[k * 3 + ecnt[k]++] = e;
+    };
     for (int i = 0; i < su.m; ++i) {
       const Row& r = su.rows[i];
-      ent[r.sp][su.dpos[r.dp]].push_back({i, 1.0, su.wplus[i]});
-      if (r.kind == 0) ent[r.sm][su.dpos[r.dm]].push_back({i, -1.0, su.wminus[i]});
+      add_ent(r.sp, su.dpos[r.dp], {i, 1.0, su.wplus[i]});
+      if (r.kind == 0) add_ent(r.sm, su.dpos[r.dm], {i, -1.0, su.wminus[i]});
     }
-    KR = dp ? 1 : 3;
-    for (int s = 0; s < Ns; ++s)
-      for (int i = 0; i < nb; ++i)
-        if ((int)ent[s][i].size() > KR) fail(FETIGPU_E_STATE, "too many dual rows per DOF");
-    KRp = KR;
     std::vector<OpSub> ops(Ns), pcs(Ns), pjs(Ns);
-    std::vector<int> rows, prow, slot_of(Ns), top_pos, top_off(Ns), design(Ns);
-    std::vector<double> coef, pcoef, pjcoef, RT;
-    std::vector<int> rt_off(Ns);
+    std::vector<int> slot_of(Ns), top_off(Ns), design(Ns), rt_off(Ns);
+    size_t ntop = 0, nT = 0;
+    for (int s = 0; s < Ns; ++s) { ntop += su.subs[s].Top.size(); nT += su.subs[s].T.size(); }
+    std::vector<int> rows(ntop * KR), prow(nT * KRp), top_pos(ntop);
+    std::vector<double> coef(ntop * KR), pcoef(nT * KRp), pjcoef(nT * KRp), RT(nT * 3);
+    size_t io = 0, ip = 0;
     for (int s = 0; s < Ns; ++s) {
       const SubPlan& S = su.subs[s];
       const int sl = S.op_slot;
       slot_of[s] = sl;
       design[s] = S.design;
-      ops[s] = {op_moff[sl], op_ns[sl], op_ld[sl], (int)rows.size(), 0};
-      top_off[s] = (int)top_pos.size();
+      ops[s] = {op_moff[sl], op_ns[sl], op_ld[sl], (int)(io * KR), 0};
+      top_off[s] = (int)io;
       for (int t : S.Top) {
-        top_pos.push_back(t);
-        for (int k = 0; k < KR; ++k) {
-          if (k < (int)ent[s][t].size()) { rows.push_back(ent[s][t][k].row); coef.push_back(ent[s][t][k].coef); }
-          else { rows.push_back(-1); coef.push_back(0.0); }
+        const size_t k = (size_t)s * nb + t;
+        top_pos[io] = t;
+        for (int q = 0; q < KR; ++q) {
+          const bool has = q < ecnt[k];
+          rows[io * KR + q] = has ? ent[k * 3 + q].row : -1;
+          coef[io * KR + q] = has ? ent[k * 3 + q].coef : 0.0;
         }
+        ++io;
       }
       // preconditioner / projector maps over T
-      pcs[s] = {0, (int)S.T.size(), 0, (int)prow.size(), 0};
+      pcs[s] = {0, (int)S.T.size(), 0, (int)(ip * KRp), 0};
       pjs[s] = pcs[s];
-      rt_off[s] = (int)RT.size();
+      rt_off[s] = (int)(ip * 3);
       for (int t : S.T) {
-        for (int k = 0; k < KRp; ++k) {
-          if (k < (int)ent[s][t].size()) {
-            prow.push_back(ent[s][t][k].row);
-            pcoef.push_back(ent[s][t][k].coef * ent[s][t][k].w);
-            pjcoef.push_back(ent[s][t][k].coef);
-          } else { prow.push_back(-1); pcoef.push_back(0.0); pjcoef.push_back(0.0); }
+        const size_t k = (size_t)s * nb + t;
+        for (int q = 0; q < KRp; ++q) {
+          const bool has = q < ecnt[k];
+          prow[ip * KRp + q] = has ? ent[k * 3 + q].row : -1;
+          pcoef[ip * KRp + q] = has ? ent[k * 3 + q].coef * ent[k * 3 + q].w : 0.0;
+          pjcoef[ip * KRp + q] = has ? ent[k * 3 + q].coef : 0.0;
         }
-        for (int k = 0; k < 3; ++k) RT.push_back(su.Rb[(size_t)k * nb + t]);
+        for (int q = 0; q < 3; ++q) RT[ip * 3 + q] = su.Rb[(size_t)q * nb + t];
+        ++ip;
       }
     }
     d_oprows.upload(rows, st); d_opcoef.upload(coef, st);
@@ -485,6 +560,7 @@ struct Ctx {
     d_top_pos.upload(top_pos, st); d_top_off.upload(top_off, st);
     d_pcrows.upload(prow, st); d_pccoef.upload(pcoef, st);
 
+    ptimer.mark("per-subdomain maps (host)", st);
     // ---- preconditioner matrices
     std::vector<long long> pc_moff;
     std::vector<int> pc_ld;
@@ -549,6 +625,7 @@ struct Ctx {
       LAUNCH_CHECK();
       CK(cudaStreamSynchronize(st));
     }
+    ptimer.mark("preconditioner slots", st);
     for (int s = 0; s < Ns; ++s) {
       const int sl = su.subs[s].pc_slot;
       pcs[s].moff = pc_moff[sl];
@@ -638,6 +715,7 @@ struct Ctx {
       d_fbar.alloc(std::max(1, su.Nc));
       build_coarse(so, osub, oloc);
     }
+    ptimer.mark("projector/boundary data", st);
     // ---- fold the +-1 signs of the FETI-DP constraint rows into F_s and A_bc
     d_opcoef_apply.upload(coef, st);
     if (dp) {
@@ -678,6 +756,7 @@ struct Ctx {
         folded = true;
       }
     }
+    ptimer.mark("coarse problem + folding", st);
     // ---- scratch
     const size_t m = std::max(1, su.m);
     d_v1.alloc(m); d_v2.alloc(m); d_v3.alloc(m);
@@ -765,6 +844,7 @@ struct Ctx {
       CK(cudaStreamSynchronize(st));
       pc_sym = true;
     }
+    ptimer.mark("symmetric packing", st);
     // ---- work per apply
     double sn2 = 0, snc = 0, sns = 0;
     for (int s = 0; s < Ns; ++s) {
@@ -835,13 +915,17 @@ struct Ctx {
   void launch_symmetrize(double* A, int n);
 
   void build() {
+    ptimer = PhaseTimer();
     CK(cudaEventRecord(ev0, st));
     CK(cudaMemcpyToSymbolAsync(c_kunit, su.kunit, sizeof(su.kunit), 0, cudaMemcpyHostToDevice, st));
     build_nd();
+    ptimer.mark("nested dissection", st);
     CK(cudaEventRecord(ev1, st));
     nd_ms = elapsed(ev0, ev1);
     build_ops();
     CK(cudaEventRecord(ev2, st));
+    CK(cudaStreamSynchronize(st));
+    scratch.release(kScWs);
     slot_ms = elapsed(ev1, ev2);
     build_ms = elapsed(ev0, ev2);
     built = true;

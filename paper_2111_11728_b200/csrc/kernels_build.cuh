@@ -257,6 +257,123 @@ __global__ void __launch_bounds__(kThreads) k_front_elim_large(const FrontDesc* 
   }
 }
 
+// ------------------------------- batched blocked partial Cholesky (BPC) --
+// The same right-looking algorithm as k_front_elim_large, but every panel
+// step is three launches over ALL frontals of a batch, so each phase gets a
+// full GPU of CTAs: (1) factor the kb x kb diagonal block (1 CTA / frontal),
+// (2) triangular-solve the panel rows below it (CTAs over row blocks),
+// (3) rank-kb update of the lower trailing matrix, one 64x64 tile per CTA on
+// FP64 tensor cores (mma.sync.m8n8k4.f64, 8 warps as 2 x 4 warp tiles).
+__device__ __forceinline__ void dmma_884b(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+constexpr int kBpcPad = kTile + 4;
+
+__global__ void __launch_bounds__(kThreads) k_bpc_diag(const FrontDesc* fds, double* base, int k0,
+                                                       int* status) {
+  const FrontDesc f = fds[blockIdx.x];
+  if (k0 >= f.ne) return;
+  __shared__ double D[kNB * (kNB + 1)];
+  double* A = base + f.off;
+  const int kb = min(kNB, f.ne - k0), ld = f.ld;
+  for (int idx = threadIdx.x; idx < kb * kb; idx += kThreads) {
+    const int j = idx / kb, i = idx - j * kb;
+    if (i >= j) D[j * (kNB + 1) + i] = A[(size_t)(k0 + j) * ld + k0 + i];
+  }
+  __syncthreads();
+  eliminate_smem(D, kb, kb, kNB + 1, status, f.code);
+  for (int idx = threadIdx.x; idx < kb * kb; idx += kThreads) {
+    const int j = idx / kb, i = idx - j * kb;
+    if (i >= j) A[(size_t)(k0 + j) * ld + k0 + i] = D[j * (kNB + 1) + i];
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) k_bpc_trsm(const FrontDesc* fds, double* base, int k0) {
+  const FrontDesc f = fds[blockIdx.y];
+  if (k0 >= f.ne) return;
+  const int kb = min(kNB, f.ne - k0), k1 = k0 + kb, ld = f.ld;
+  const int r = k1 + blockIdx.x * kThreads + threadIdx.x;
+  if (k1 + blockIdx.x * kThreads >= f.nf) return;
+  __shared__ double D[kNB * (kNB + 1)];
+  double* A = base + f.off;
+  for (int idx = threadIdx.x; idx < kb * kb; idx += kThreads) {
+    const int j = idx / kb, i = idx - j * kb;
+    if (i >= j) D[j * (kNB + 1) + i] = A[(size_t)(k0 + j) * ld + k0 + i];
+  }
+  __syncthreads();
+  if (r >= f.nf) return;
+  double x[kNB];
+#pragma unroll
+  for (int c = 0; c < kNB; ++c)
+    if (c < kb) x[c] = A[(size_t)(k0 + c) * ld + r];
+#pragma unroll
+  for (int c = 0; c < kNB; ++c) {
+    if (c < kb) {
+      double v = x[c];
+#pragma unroll
+      for (int c2 = 0; c2 < c; ++c2) v -= x[c2] * D[c2 * (kNB + 1) + c];
+      x[c] = v / D[c * (kNB + 1) + c];
+      A[(size_t)(k0 + c) * ld + r] = x[c];
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) k_bpc_update(const FrontDesc* fds, double* base, int k0) {
+  const FrontDesc f = fds[blockIdx.y];
+  if (k0 >= f.ne) return;
+  const int kb = min(kNB, f.ne - k0), k1 = k0 + kb, ld = f.ld;
+  const int mt = f.nf - k1;
+  const int nt = (mt + kTile - 1) / kTile;
+  const int t = blockIdx.x;
+  if (t >= nt * (nt + 1) / 2) return;
+  int ti = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+  while (ti * (ti + 1) / 2 > t) --ti;
+  while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
+  const int tj = t - ti * (ti + 1) / 2;
+  __shared__ double LiT[kNB * kBpcPad];
+  __shared__ double LjT[kNB * kBpcPad];
+  double* A = base + f.off;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wr = warp >> 2, wc = warp & 3;
+  for (int idx = tid; idx < kNB * kTile; idx += kThreads) {
+    const int c = idx / kTile, r = idx - c * kTile;
+    const int ri = ti * kTile + r, rj = tj * kTile + r;
+    LiT[c * kBpcPad + r] = (c < kb && ri < mt) ? A[(size_t)(k0 + c) * ld + k1 + ri] : 0.0;
+    LjT[c * kBpcPad + r] = (c < kb && rj < mt) ? A[(size_t)(k0 + c) * ld + k1 + rj] : 0.0;
+  }
+  __syncthreads();
+  double acc[4][2][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  const int kq = (kb + 3) & ~3;
+  for (int k4 = 0; k4 < kq; k4 += 4) {
+    double af[4], bf[2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) af[i] = LiT[(k4 + (lane & 3)) * kBpcPad + wr * 32 + i * 8 + (lane >> 2)];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) bf[j] = LjT[(k4 + (lane & 3)) * kBpcPad + wc * 16 + j * 8 + (lane >> 2)];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) dmma_884b(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int ri = ti * kTile + wr * 32 + i * 8 + (lane >> 2);
+    if (ri >= mt) continue;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int cj = tj * kTile + wc * 16 + j * 8 + 2 * (lane & 3);
+      if (cj < mt && ri >= cj) A[(size_t)(k1 + cj) * ld + k1 + ri] -= acc[i][j][0];
+      if (cj + 1 < mt && ri >= cj + 1) A[(size_t)(k1 + cj + 1) * ld + k1 + ri] -= acc[i][j][1];
+    }
+  }
+}
+
 // small frontal matrices (slots): load, eliminate in smem, store
 __global__ void __launch_bounds__(kThreads) k_front_elim_small(const FrontDesc* fds, double* base,
                                                                int* status) {
