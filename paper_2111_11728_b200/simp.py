@@ -74,7 +74,7 @@ def optimize(prob: Problem, iterations: int = 10, volfrac: float = 0.5, rmin: fl
              move: float = 0.2, damping: float = 0.5, rho_min: float = 1e-3, tol: float = 1e-6,
              directions: int = 2, snapshots=()) -> SimpState:
     """Runs `iterations` OC steps from the uniform design rho = volfrac."""
-    from .engine import FetiSystem
+    from .engine import FetiSystem, IndefiniteInput
     n, T = prob.n, prob.densities.shape[0]
     types = np.asarray(prob.module_type)
     counts = np.bincount(types, minlength=T).astype(float)
@@ -87,10 +87,18 @@ def optimize(prob: Problem, iterations: int = 10, volfrac: float = 0.5, rmin: fl
     snaps = {}
     for it in range(iterations):
         g = FetiSystem(prob.replace(densities=rho.copy()))
-        lam, tr = g.solve(tol=tol, max_it=2000, directions=directions)
+        used = directions
+        try:
+            lam, tr = g.solve(tol=tol, max_it=2000, directions=directions)
+        except IndefiniteInput:
+            # RRS Gram lost positivity beyond pivot_tol: the
+            # application falls back to FO for this state solve
+            used = 1
+            lam, tr = g.solve(tol=tol, max_it=2000, directions=1)
         u = g.recover(lam)
         g.close()
-        state.solves.append({"iterations": tr["iterations"], "status": tr["status"], "solve_ms": tr["solve_ms"]})
+        state.solves.append({"iterations": tr["iterations"], "status": tr["status"], "solve_ms": tr["solve_ms"],
+                             "directions": used})
         # compliance and sensitivities per element, summed per module type
         dc = np.zeros((T, n * n))
         comp = 0.0

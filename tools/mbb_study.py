@@ -40,6 +40,7 @@ out = {"modules": [sx, sy], "elems_per_module": n, "types": 16,
        "total_subdomain_dofs": sx * sy * 2 * (n + 1) ** 2, "simp_wall_s": time.perf_counter() - t0,
        "compliance": st.compliance, "state_solves": st.solves, "snapshots": {}}
 print("SIMP done", out["simp_wall_s"], st.compliance[:3], st.compliance[-3:], flush=True)
+print("state solves", st.solves, flush=True)
 for it in snaps:
     dens = st.snapshots[it]
     row = {}
