@@ -1033,22 +1033,28 @@ struct Ctx {
   }
 
   // v <- P v for a row-major block (m x ncols, ld = ncols), T-FETI only
+  // grow-only scratch for the multi-column projector paths: no cudaMalloc /
+  // cudaFree (both device-synchronising) inside solver iterations once warm
+  DBuf<double> ws_g, ws_h, ws_corr;
+  static double* grow(DBuf<double>& b, size_t n) {
+    if (b.n < n) b.alloc(n);
+    return b.p;
+  }
+
   void project_rm(double* v, int ncols) {
     if (su.method != FETIGPU_TFETI) return;
     const int nc = 3 * su.Ns;
-    DBuf<double> g, h, corr;
-    g.alloc((size_t)nc * ncols);
-    h.alloc((size_t)nc * ncols);
-    corr.alloc((size_t)su.m * ncols);
-    corr.zero(st);
+    double* g = grow(ws_g, (size_t)nc * ncols);
+    double* h = grow(ws_h, (size_t)nc * ncols);
+    double* corr = grow(ws_corr, (size_t)su.m * ncols);
+    CK(cudaMemsetAsync(corr, 0, (size_t)su.m * ncols * 8, st));
     k_proj_gather<<<dim3(su.Ns, ncols), kThreads, 0, st>>>(d_pj.p, d_pcrows.p, d_pjcoef.p, d_RT.p, d_rt_off.p, v, 1,
-                                                          g.p, nc, -1.0, ncols);
-    small_gemm(g.p, h.p, ncols);
+                                                          g, nc, -1.0, ncols);
+    small_gemm(g, h, ncols);
     k_proj_scatter<<<dim3(su.Ns, ncols), kThreads, 0, st>>>(d_pj.p, d_pcrows.p, d_pjcoef.p, d_RT.p, d_rt_off.p,
-                                                           h.p, nc, corr.p, 1, ncols);
-    k_add<<<grid_for((long long)su.m * ncols), kThreads, 0, st>>>(su.m * ncols, corr.p, v, 0, 0);
+                                                           h, nc, corr, 1, ncols);
+    k_add<<<grid_for((long long)su.m * ncols), kThreads, 0, st>>>(su.m * ncols, corr, v, 0, 0);
     LAUNCH_CHECK();
-    CK(cudaStreamSynchronize(st));
   }
 
   // h = H g for ncols columns of length 3N_s (H symmetric, column-major)
@@ -1066,34 +1072,31 @@ struct Ctx {
   // corr = P v - v for ncols columns (T-FETI); caller adds
   void proj_corr(const double* v, int ldv, double* corr, int ldc, int ncols, double gsign = -1.0) {
     const int nc = 3 * su.Ns;
-    DBuf<double> g, h;
     double* gp = d_g.p;
     double* hp = d_h.p;
     if (ncols > 1) {
-      g.alloc((size_t)nc * ncols);
-      h.alloc((size_t)nc * ncols);
-      gp = g.p;
-      hp = h.p;
+      gp = grow(ws_g, (size_t)nc * ncols);
+      hp = grow(ws_h, (size_t)nc * ncols);
     }
     k_proj_gather<<<dim3(su.Ns, ncols), kThreads, 0, st>>>(d_pj.p, d_pcrows.p, d_pjcoef.p, d_RT.p,
                                                           d_rt_off.p, v, ldv, gp, nc, gsign);
     small_gemm(gp, hp, ncols);
-    for (int c = 0; c < ncols; ++c) CK(cudaMemsetAsync(corr + (size_t)c * ldc, 0, su.m * 8, st));
+    if (ldc == su.m)
+      CK(cudaMemsetAsync(corr, 0, (size_t)su.m * ncols * 8, st));
+    else
+      for (int c = 0; c < ncols; ++c) CK(cudaMemsetAsync(corr + (size_t)c * ldc, 0, su.m * 8, st));
     k_proj_scatter<<<dim3(su.Ns, ncols), kThreads, 0, st>>>(d_pj.p, d_pcrows.p, d_pjcoef.p, d_RT.p,
                                                            d_rt_off.p, hp, nc, corr, ldc);
     LAUNCH_CHECK();
-    if (ncols > 1) CK(cudaStreamSynchronize(st));
   }
 
   void project(double* v, int ncols, int ld) {
     if (su.method != FETIGPU_TFETI) return;
-    DBuf<double> corr;
     double* cp = d_v3.p;
-    if (ncols > 1) { corr.alloc((size_t)su.m * ncols); cp = corr.p; }
+    if (ncols > 1) cp = grow(ws_corr, (size_t)su.m * ncols);
     proj_corr(v, ld, cp, su.m, ncols);
     k_add<<<dim3(grid_for(su.m), ncols), kThreads, 0, st>>>(su.m, cp, v, su.m, ld);
     LAUNCH_CHECK();
-    if (ncols > 1) CK(cudaStreamSynchronize(st));
   }
 
   // per-subdomain boundary rhs b = (f - B^T lambda)[src] - S[src,D] gD - S[src,c] u_c
@@ -1547,13 +1550,18 @@ int Ctx::solve(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_trace* 
 int Ctx::solve_rrs(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_trace* tr) {
   const int m = su.m, Ns = su.Ns;
   const int passes = std::max(1, o.reorth_passes);
+  PhaseTimer pt;
   rhs();
-  DBuf<double> lam, r, z, q, tmp, Z, W, Wsel, Delta, gamma;
+  pt.mark("rrs rhs", st);
+  // Two m x N_s row-major work blocks only: W (directions; the preconditioner
+  // writes its columns straight into it, Alg. 1 lines 2/16-17) and Qb = F W.
+  // The compression gathers go into the free arena tail and into W.
+  DBuf<double> lam, r, z, q, tmp, W, Qb, Delta, gamma;
   DBuf<int> perm, rank_d, ctl;
   DBuf<Scal> sc;
   DBuf<double> Linv;
   lam.alloc(m); r.alloc(m); z.alloc(m); q.alloc(m); tmp.alloc(m);
-  Z.alloc((size_t)m * Ns); W.alloc((size_t)m * Ns); Wsel.alloc((size_t)m * round_up(Ns, 8));
+  W.alloc((size_t)m * Ns); Qb.alloc((size_t)m * Ns);
   ctl.alloc(4);
   Linv.alloc((size_t)Ns * Ns);
   int coop_blocks = 0;
@@ -1563,24 +1571,60 @@ int Ctx::solve_rrs(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_tra
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pivchol_coop, 512, 0));
     coop_blocks = sms * std::max(1, std::min(per_sm, 2));
+    CK(cudaFuncSetAttribute(k_pivchol, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            kPivcholSmemMax * kPivcholSmemMax * 8));
   }
   Delta.alloc((size_t)Ns * Ns); gamma.alloc(Ns);
   perm.alloc(Ns); rank_d.alloc(1);
   sc.alloc(1);
   sc.zero(st);
-  std::vector<std::unique_ptr<DBuf<double>>> Ws, Qs, Psis;
-  std::vector<int> widths, lds;
+  // Stored F-orthonormal directions W_j and Q_j = F W_j (m x rank_j column-
+  // major blocks, ld m) packed side by side into a few large chunks, so the
+  // re-orthogonalization against every stored block is one GEMM pair per
+  // chunk per pass.  Chunk capacity doubles the store (O(log K) chunks, no
+  // copies) and is clamped to the free device memory.
+  struct Chunk {
+    std::unique_ptr<DBuf<double>> w, q;
+    int cap, used, off;
+  };
+  std::vector<Chunk> chunks;
+  DBuf<double> Psi;
+  int K = 0;
+  auto append_slot = [&](int rank, double** wn, double** qn) {
+    if (chunks.empty() || chunks.back().used + rank > chunks.back().cap) {
+      size_t freeb = 0, total = 0;
+      CK(cudaMemGetInfo(&freeb, &total));
+      const size_t margin = std::max<size_t>(size_t(1) << 30, total / 64);
+      const long long fit = freeb > margin ? (long long)((freeb - margin) / (16.0 * m)) : 0;
+      const int c = (int)std::min<long long>(std::max(rank, std::max(Ns, K)), fit);
+      if (c < rank)
+        fail(FETIGPU_E_OUT_OF_MEMORY, "RRS: out of device memory for the stored directions (K = " +
+                                          std::to_string(K + rank) + " columns of length m = " + std::to_string(m) +
+                                          ")");
+      Chunk ch{std::unique_ptr<DBuf<double>>(new DBuf<double>), std::unique_ptr<DBuf<double>>(new DBuf<double>), c, 0,
+               K};
+      ch.w->alloc((size_t)m * c);
+      ch.q->alloc((size_t)m * c);
+      chunks.push_back(std::move(ch));
+    }
+    Chunk& ch = chunks.back();
+    *wn = ch.w->p + (size_t)ch.used * m;
+    *qn = ch.q->p + (size_t)ch.used * m;
+    ch.used += rank;
+    if (Psi.n < (size_t)(K + rank) * Ns) Psi.alloc((size_t)std::max(K + rank, 2 * K) * Ns);
+  };
   Scal* hs = nullptr;
   CK(cudaMallocHost(&hs, sizeof(Scal)));
   std::unique_ptr<Scal, decltype(&cudaFreeHost)> hs_guard(hs, cudaFreeHost);
   const double one = 1.0, mone = -1.0, zero = 0.0;
+  pt.mark("rrs setup", st);
   CK(cudaEventRecord(ev0, st));
   CK(cudaMemcpyAsync(lam.p, d_lam0.p, m * 8, cudaMemcpyDeviceToDevice, st));
   apply_F(lam.p, q.p, 1, m, m);
   int fapp = 1;
   k_sub<<<grid_for(m), kThreads, 0, st>>>(m, d_d.p, q.p, r.p);
   project(r.p, 1, m);
-  apply_precond(r.p, z.p, Z.p, true);  // Alg. 1 line 2 (columns) and z = Z 1
+  apply_precond(r.p, z.p, W.p, true);  // Alg. 1 line 2 (columns) and z = Z 1
   dots({{r.p, z.p}, {r.p, r.p}, {z.p, z.p}}, &sc.p->rz);
   CK(cudaMemcpyAsync(hs, sc.p, sizeof(Scal), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
@@ -1600,30 +1644,29 @@ int Ctx::solve_rrs(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_tra
     }
   };
   push(eps0, Ns);
-  CK(cudaMemcpyAsync(W.p, Z.p, (size_t)m * Ns * 8, cudaMemcpyDeviceToDevice, st));
   project_rm(W.p, Ns);  // line 3
   const double target = o.rel ? o.tol * eps0 : o.tol;
   cudaEvent_t pev[9];
   for (auto& e : pev) CK(cudaEventCreate(&e));
   double phase[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   auto mark = [&](int i) { CK(cudaEventRecord(pev[i], st)); };
+  const char* tenv = getenv("FETIGPU_TRACE");  // per-iteration RRS line on stderr
+  const bool trace_on = tenv && tenv[0] == '1';
   while (true) {
     if (eps <= target) { status = FETIGPU_CONVERGED; break; }
     if (it >= o.max_it) { status = FETIGPU_MAX_ITER; break; }
     const int k = Ns;
-    auto Qb = std::make_unique<DBuf<double>>();
-    Qb->alloc((size_t)m * k);
     mark(0);
-    apply_F_block(W.p, k, Qb->p, k, k);  // line 7 (K5)
+    apply_F_block(W.p, k, Qb.p, k, k);  // line 7 (K5)
     mark(1);
     fapp += k;
     // line 8: Delta = Q^T W (column-major k x k; lower triangle used)
-    CB(cublasDgemm(cb, CUBLAS_OP_N, CUBLAS_OP_T, k, k, m, &one, Qb->p, k, W.p, k, &zero, Delta.p, k));
+    CB(cublasDgemm(cb, CUBLAS_OP_N, CUBLAS_OP_T, k, k, m, &one, Qb.p, k, W.p, k, &zero, Delta.p, k));
     k_mirror_lower<<<grid_for((long long)k * k), kThreads, 0, st>>>(Delta.p, k);
     mark(2);
     // line 9
-    if (k <= 64) {
-      k_pivchol<<<1, 1024, 0, st>>>(Delta.p, k, o.pivot_tol, perm.p, rank_d.p, d_status.p);
+    if (k <= kPivcholSmemMax) {
+      k_pivchol<<<1, 1024, (size_t)k * k * 8, st>>>(Delta.p, k, o.pivot_tol, perm.p, rank_d.p, d_status.p);
     } else {
       double* dp = Delta.p;
       double tolv = o.pivot_tol;
@@ -1647,34 +1690,33 @@ int Ctx::solve_rrs(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_tra
       fail(FETIGPU_E_INDEFINITE_INPUT, "pivoted Cholesky: negative pivot");
     }
     if (rank == 0) { status = FETIGPU_BREAKDOWN; break; }
-    // lines 10-11: W <- W N^T [L~^{-T}; 0]  ==  (L~^{-1} W_sel^T)^T, same for Q.
-    // Stored blocks are k_j x m column-major (cuBLAS view) with the leading
-    // dimension padded to a multiple of 8 (aligned cuBLAS paths).
-    const int rp = round_up(rank, 8);
-    auto Wb = std::make_unique<DBuf<double>>();
-    Wb->alloc((size_t)m * rp);
+    // lines 10-11: W_new = W N^T [L~^{-T}; 0] = W_sel L~^{-T} (m x rank, appended
+    // to the arena at column K); same for Q.
+    double *Wn = nullptr, *Qn = nullptr;
+    append_slot(rank, &Wn, &Qn);
     launch_identity(Linv.p, rank);
     CB(cublasDtrsm(cb, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, rank, rank,
                    &one, Delta.p, k, Linv.p, rank));
-    k_gather_cols_rm<<<grid_for((long long)m * rank), kThreads, 0, st>>>(W.p, k, perm.p, rank, m, Wsel.p, rp);
-    CB(cublasDtrmm(cb, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, rank, m, &one,
-                   Linv.p, rank, Wsel.p, rp, Wb->p, rp));
-    k_gather_cols_rm<<<grid_for((long long)m * rank), kThreads, 0, st>>>(Qb->p, k, perm.p, rank, m, Wsel.p, rp);
-    auto Qc = std::make_unique<DBuf<double>>();
-    Qc->alloc((size_t)m * rp);
-    CB(cublasDtrmm(cb, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, rank, m, &one,
-                   Linv.p, rank, Wsel.p, rp, Qc->p, rp));
-    Qb = std::move(Qc);
+    // W_sel lands in Q's (still free) arena slot, W_new = W_sel L~^{-T} in W's;
+    // then Q_sel lands in W (no longer needed) and Q_new = Q_sel L~^{-T}.
+    const dim3 tgrid((m + 31) / 32, (rank + 31) / 32);
+    k_gather_cols_t<<<tgrid, dim3(32, 8), 0, st>>>(W.p, k, perm.p, rank, m, Qn, m);
+    CB(cublasDtrmm(cb, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, m, rank, &one,
+                   Linv.p, rank, Qn, m, Wn, m));
+    k_gather_cols_t<<<tgrid, dim3(32, 8), 0, st>>>(Qb.p, k, perm.p, rank, m, W.p, m);
+    CB(cublasDtrmm(cb, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, m, rank, &one,
+                   Linv.p, rank, W.p, m, Qn, m));
+    K += rank;
     mark(4);
     // lines 13-15
-    CB(cublasDgemv(cb, CUBLAS_OP_N, rank, m, &one, Wb->p, rp, r.p, 1, &zero, gamma.p, 1));
-    CB(cublasDgemv(cb, CUBLAS_OP_T, rank, m, &one, Wb->p, rp, gamma.p, 1, &one, lam.p, 1));
-    CB(cublasDgemv(cb, CUBLAS_OP_T, rank, m, &one, Qb->p, rp, gamma.p, 1, &zero, tmp.p, 1));
+    CB(cublasDgemv(cb, CUBLAS_OP_T, m, rank, &one, Wn, m, r.p, 1, &zero, gamma.p, 1));
+    CB(cublasDgemv(cb, CUBLAS_OP_N, m, rank, &one, Wn, m, gamma.p, 1, &one, lam.p, 1));
+    CB(cublasDgemv(cb, CUBLAS_OP_N, m, rank, &one, Qn, m, gamma.p, 1, &zero, tmp.p, 1));
     project(tmp.p, 1, m);
     k_axpy<<<grid_for(m), kThreads, 0, st>>>(m, -1.0, tmp.p, r.p);
     mark(5);
     // line 16
-    apply_precond(r.p, z.p, Z.p, true);
+    apply_precond(r.p, z.p, W.p, true);
     dots({{r.p, z.p}, {r.p, r.p}, {z.p, z.p}}, &sc.p->rz);
     mark(6);
     CK(cudaMemcpyAsync(hs, sc.p, sizeof(Scal), cudaMemcpyDeviceToHost, st));
@@ -1682,25 +1724,24 @@ int Ctx::solve_rrs(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_tra
     eps = metric(*hs);
     ++it;
     push(eps, rank);
-    Ws.push_back(std::move(Wb));
-    Qs.push_back(std::move(Qb));
-    widths.push_back(rank);
-    lds.push_back(rp);
+    if (trace_on) {
+      float te = 0;
+      CK(cudaEventElapsedTime(&te, ev0, pev[6]));
+      fprintf(stderr, "[fetigpu] rrs it %4d  eps/eps0 %.3e  rank %5d  K %7d  t %9.1f ms\n", it, eps / eps0, rank, K,
+              te);
+    }
     // line 17
-    CK(cudaMemcpyAsync(W.p, Z.p, (size_t)m * Ns * 8, cudaMemcpyDeviceToDevice, st));
     project_rm(W.p, Ns);
     mark(7);
-    // lines 18-21: block classical Gram-Schmidt against all stored blocks, `passes` passes
-    Psis.resize(Ws.size());
-    for (size_t j = 0; j < Ws.size(); ++j)
-      if (!Psis[j]) { Psis[j] = std::make_unique<DBuf<double>>(); Psis[j]->alloc((size_t)lds[j] * Ns); }
+    // lines 18-21: block classical Gram-Schmidt against all stored blocks,
+    // `passes` passes.  W is row-major m x Ns (= column-major Ns x m).
     for (int p = 0; p < passes; ++p) {
-      for (size_t j = 0; j < Ws.size(); ++j)  // Psi_j = Q_j^T W   (k_j x Ns)
-        CB(cublasDgemm(cb, CUBLAS_OP_N, CUBLAS_OP_T, widths[j], Ns, m, &one, Qs[j]->p, lds[j], W.p, Ns, &zero,
-                       Psis[j]->p, lds[j]));
-      for (size_t j = 0; j < Ws.size(); ++j)  // W -= W_j Psi_j  ==  W^T -= Psi_j^T W_j^T
-        CB(cublasDgemm(cb, CUBLAS_OP_T, CUBLAS_OP_N, Ns, m, widths[j], &mone, Psis[j]->p, lds[j], Ws[j]->p,
-                       lds[j], &one, W.p, Ns));
+      for (const Chunk& ch : chunks)  // Psi = Q_all^T W   (K x Ns, ld K)
+        CB(cublasDgemm(cb, CUBLAS_OP_T, CUBLAS_OP_T, ch.used, Ns, m, &one, ch.q->p, m, W.p, Ns, &zero,
+                       Psi.p + ch.off, K));
+      for (const Chunk& ch : chunks)  // W -= W_all Psi   ==   W^T -= Psi^T W_all^T
+        CB(cublasDgemm(cb, CUBLAS_OP_T, CUBLAS_OP_T, Ns, m, ch.used, &mone, Psi.p + ch.off, K, ch.w->p, m, &one,
+                       W.p, Ns));
     }
     mark(8);
     CK(cudaEventSynchronize(pev[8]));
@@ -1718,6 +1759,7 @@ int Ctx::solve_rrs(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_tra
   const double ms = elapsed(ev0, ev1);
   CK(cudaMemcpyAsync(lambda_host, lam.p, m * 8, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
+  pt.mark("rrs loop + readback", st);
   if (tr) {
     tr->status = status;
     tr->iterations = it;
@@ -1726,6 +1768,8 @@ int Ctx::solve_rrs(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_tra
     tr->eps_final = eps;
     tr->solve_ms = ms;
   }
+  chunks.clear();
+  pt.mark("rrs store release", st);
   return 0;
 }
 

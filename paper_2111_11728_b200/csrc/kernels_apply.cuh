@@ -738,16 +738,25 @@ __global__ void k_nd_backsub(const NdDev* __restrict__ nodes, const int* __restr
 // Rank-revealing pivoted Cholesky of the k x k Gram matrix Delta (Alg. 1
 // line 9; pivoted_cholesky contract SPEC.md:43-47 with a symmetric trailing
 // update): one CTA, pivots sequential, updates parallel.
-__global__ void __launch_bounds__(1024) k_pivchol(double* A, int n, double tol, int* perm,
+// Staged in shared memory when n*n doubles fit (n <= kPivcholSmemMax); the
+// global-memory form is kept for the cooperative kernel's size range.
+constexpr int kPivcholSmemMax = 160;
+__global__ void __launch_bounds__(1024) k_pivchol(double* Ag, int n, double tol, int* perm,
                                                   int* rank_out, int* status) {
+  extern __shared__ double s_a[];
   __shared__ double sv[32];
   __shared__ int si[32];
   __shared__ double s_scale;
   __shared__ int s_piv;
   __shared__ int s_stop;
   const int tid = threadIdx.x, nt = blockDim.x;
-  const int lane = tid & 31, warp = tid >> 5;
+  const int lane = tid & 31, warp = tid >> 5, nwarp = nt >> 5;
+  const bool staged = n <= kPivcholSmemMax;
+  double* A = staged ? s_a : Ag;
+  if (staged)
+    for (int i = tid; i < n * n; i += nt) A[i] = Ag[i];
   for (int i = tid; i < n; i += nt) perm[i] = i;
+  __syncthreads();
   // scale = max initial diagonal
   double mx = -1e300;
   for (int i = tid; i < n; i += nt) mx = fmax(mx, A[(size_t)i * n + i]);
@@ -756,7 +765,7 @@ __global__ void __launch_bounds__(1024) k_pivchol(double* A, int n, double tol, 
   __syncthreads();
   if (tid == 0) {
     double m2 = sv[0];
-    for (int w = 1; w < (nt >> 5); ++w) m2 = fmax(m2, sv[w]);
+    for (int w = 1; w < nwarp; ++w) m2 = fmax(m2, sv[w]);
     s_scale = m2;
   }
   __syncthreads();
@@ -781,7 +790,7 @@ __global__ void __launch_bounds__(1024) k_pivchol(double* A, int n, double tol, 
     if (tid == 0) {
       double v = sv[0];
       int b = si[0];
-      for (int w = 1; w < (nt >> 5); ++w)
+      for (int w = 1; w < nwarp; ++w)
         if (sv[w] > v || (sv[w] == v && si[w] < b)) { v = sv[w]; b = si[w]; }
       s_piv = b;
       s_stop = !(v > stop_tol);
@@ -813,13 +822,17 @@ __global__ void __launch_bounds__(1024) k_pivchol(double* A, int n, double tol, 
     if (tid == 0) A[(size_t)k * n + k] = l;
     for (int i = k + 1 + tid; i < n; i += nt) A[(size_t)k * n + i] /= l;
     __syncthreads();
-    const int r = n - k - 1;
-    for (long long idx = tid; idx < (long long)r * r; idx += nt) {
-      const int j = k + 1 + (int)(idx / r), i = k + 1 + (int)(idx % r);
-      A[(size_t)j * n + i] -= A[(size_t)k * n + i] * A[(size_t)k * n + j];
+    // trailing rank-1 update: a warp per row j, lanes over i
+    for (int j = k + 1 + warp; j < n; j += nwarp) {
+      const double akj = A[(size_t)k * n + j];
+      for (int i = k + 1 + lane; i < n; i += 32) A[(size_t)j * n + i] -= A[(size_t)k * n + i] * akj;
     }
     __syncthreads();
     rank = k + 1;
+  }
+  if (staged) {
+    __syncthreads();
+    for (int i = tid; i < n * n; i += nt) Ag[i] = A[i];
   }
   if (tid == 0) *rank_out = rank;
 }
@@ -936,6 +949,23 @@ __global__ void k_gather_cols_rm(const double* __restrict__ in, int ldi, const i
     const int i = (int)(idx / cols), c = (int)(idx - (long long)i * cols);
     out[(size_t)i * ldo + c] = in[(size_t)i * ldi + perm[c]];
   }
+}
+
+// Transposing column gather: out(i, c) = in(i, perm[c]), in row-major m x ldi,
+// out column-major (ld ldo).  32 x 32 tiles through shared memory so both the
+// gathered reads (rows of `in`) and the column writes are coalesced.
+__global__ void __launch_bounds__(256) k_gather_cols_t(const double* __restrict__ in, int ldi,
+                                                       const int* __restrict__ perm, int cols, int m,
+                                                       double* __restrict__ out, int ldo) {
+  __shared__ double tile[32][33];
+  const int i0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int pc = c0 + tx < cols ? perm[c0 + tx] : 0;
+  for (int r = ty; r < 32; r += 8)
+    if (i0 + r < m && c0 + tx < cols) tile[r][tx] = in[(size_t)(i0 + r) * ldi + pc];
+  __syncthreads();
+  for (int c = ty; c < 32; c += 8)
+    if (c0 + c < cols && i0 + tx < m) out[(size_t)(c0 + c) * ldo + i0 + tx] = tile[tx][c];
 }
 
 // mirror the lower triangle into the upper (Delta uses its lower triangle)

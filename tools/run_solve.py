@@ -19,6 +19,8 @@ ap.add_argument("--tol", type=float, default=1e-6)
 ap.add_argument("--max-it", type=int, default=1000)
 ap.add_argument("--oracle", action="store_true")
 ap.add_argument("--recover", action="store_true")
+ap.add_argument("--verify", action="store_true",
+                help="recompute eps = sqrt(r^T M r), r = P(d - F lambda), from scratch and compare with the trace")
 args = ap.parse_args()
 fn = pb.CONFIGS[args.config]
 prob = fn(method=args.method) if (args.method is not None and args.config == "C3") else fn()
@@ -31,8 +33,16 @@ lam, tr = g.solve(tol=args.tol, max_it=args.max_it, directions=dirs)
 out = {"config": args.config, "method": prob.method, "dirs": dirs, "m": g.m, "build_ms": st["build_ms"],
        "build_wall_s": tb, "gpu": {k: tr[k] for k in ("status", "iterations", "f_applies", "solve_ms")},
        "gpu_rel_res": tr["eps_final"] / max(tr["eps0"], 1e-300), "kept_head": tr["kept"][:8].tolist(),
+       "eps_rel_head": [float(e / tr["eps0"]) for e in tr["eps"][:16]],
        "phase_ms": dict(zip(["FW", "gram", "pivchol", "compress", "update", "precond", "projZ", "reorth"],
                             [round(x, 2) for x in tr["phase_ms"]]))}
+if args.verify:
+    d, _ = g.rhs()
+    rr = g.project(d - g.apply_F(lam))
+    zz = g.apply_precond(rr)
+    eps_true = float(np.sqrt(max(rr @ zz, 0.0)))
+    out["verify"] = {"eps_trace": tr["eps_final"], "eps_recomputed": eps_true, "eps0": tr["eps0"],
+                     "rel_recomputed": eps_true / tr["eps0"], "lambda_norm": float(np.linalg.norm(lam))}
 if args.recover:
     t0 = time.perf_counter()
     u = g.recover(lam)
