@@ -10,6 +10,7 @@
 // in namespace fetigpu.
 #pragma once
 
+#include <algorithm>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -169,5 +170,33 @@ class FetidpSystem : public DualSystem {
  public:
   explicit FetidpSystem(const fetigpu_problem& p) : DualSystem(with_method(p, FETIGPU_FETIDP)) { build(); }
 };
+
+// PivotedCholesky / pivoted_cholesky (linalg.hpp:72-89): same fields, dense
+// column-major storage; the factorization and the compression run on the GPU.
+struct PivotedCholesky {
+  std::vector<int> permutation;  // permutation[k] = original index of pivot k
+  std::vector<double> lower;     // dim x rank, column-major, pivot order
+  int rank = 0;
+  int dim = 0;
+  // W N^T [L~^{-T}; 0] for w: rows x dim column-major -> rows x rank
+  std::vector<double> compress(const std::vector<double>& w, int rows) const {
+    std::vector<double> full((size_t)dim * dim, 0.0);
+    std::copy(lower.begin(), lower.end(), full.begin());
+    std::vector<double> out((size_t)rows * rank);
+    check(fetigpu_pivoted_compress(permutation.data(), full.data(), dim, rank, w.data(), rows, out.data()));
+    return out;
+  }
+};
+
+// a: n x n column-major symmetric PSD
+inline PivotedCholesky pivoted_cholesky(const std::vector<double>& a, int n, double pivot_tol = 1e-12) {
+  PivotedCholesky pc;
+  pc.dim = n;
+  pc.permutation.resize(n);
+  std::vector<double> full((size_t)n * n);
+  check(fetigpu_pivoted_cholesky(a.data(), n, pivot_tol, pc.permutation.data(), full.data(), &pc.rank));
+  pc.lower.assign(full.begin(), full.begin() + (size_t)n * pc.rank);
+  return pc;
+}
 
 }  // namespace fetigpu

@@ -190,6 +190,24 @@ int fetigpu_local_operator(fetigpu_ctx* ctx, int s, int* ns, int* dofs, double* 
  * row-major (W(i,c) = W[i*ldw + c]), device pointers, ctx stream. */
 int fetigpu_apply_F_block_device(fetigpu_ctx* ctx, const double* W, int ldw, double* Q, int ldq, int k);
 int fetigpu_time_apply_block(fetigpu_ctx* ctx, const double* W, double* Q, int k, int reps, double* ms);
+/* Rank-revealing pivoted Cholesky, Alg. 1 line 9 -- replaces
+ * feti::pivoted_cholesky (proj/include/feti/linalg.hpp:80, linalg.cpp:83-138)
+ * with the SPEC.md:43-47 contract (symmetric trailing update):
+ * N A N^T = L L^T, L = [[L~, 0], [X, 0]], pivots by largest remaining
+ * diagonal (ties -> lowest index), stop when it is <= tol * max initial
+ * diagonal.  a: n x n column-major symmetric (lower triangle read).  Outputs
+ * perm[n] (pivot order), lower (n x n column-major; columns < *rank hold L,
+ * the rest zero) and *rank.  Runs the device kernel the RRS solver uses.
+ * FETIGPU_E_INDEFINITE_INPUT when a remaining diagonal is below -tol * scale. */
+int fetigpu_pivoted_cholesky(const double* a, int n, double tol, int* perm, double* lower, int* rank);
+/* Basis compression W N^T [L~^{-T}; 0], Alg. 1 lines 10-11 -- replaces
+ * feti::PivotedCholesky::compress (linalg.hpp:79, linalg.cpp:131-138).
+ * perm/lower/rank as returned by fetigpu_pivoted_cholesky (lower n x n
+ * column-major); w: rows x n column-major; out: rows x rank column-major.
+ * Same device operations as the RRS solver (L~^{-1} by a triangular solve
+ * on the identity, column gather, triangular multiply). */
+int fetigpu_pivoted_compress(const int* perm, const double* lower, int n, int rank, const double* w, int rows,
+                             double* out);
 /* Measured FP64 issue peaks of this device (DMMA m8n8k4 and DFMA), TFLOP/s. */
 int fetigpu_fp64_peak(double* tflops_dmma, double* tflops_dfma);
 /* DMMA fragment-layout self test: C (8x8 row-major) = A (8x4) B (4x8). */

@@ -1541,6 +1541,85 @@ int Ctx::solve(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_trace* 
   return 0;
 }
 
+// Launch the cluster pivoted Cholesky with the smallest cluster whose
+// distributed shared memory holds the n x n Gram matrix; false if none fits
+// (n > kPivcholClusterMaxN or the cluster cannot be scheduled).
+template <int CL>
+static bool pivchol_cluster_try(double* A, int n, double tol, int* perm, int* rank, int* status, double* gx,
+                                cudaStream_t st) {
+  const int R = (n + CL - 1) / CL;
+  const size_t smem = ((size_t)R * n + 3 * (size_t)n) * 8;
+  if (smem > 225 * 1024) return false;
+  static int ok = -1;  // per instantiation: attributes set and cluster schedulable
+  if (ok < 0) {
+    ok = 0;
+    if (cudaFuncSetAttribute(k_pivchol_cl<CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, 225 * 1024) !=
+        cudaSuccess) { cudaGetLastError(); return false; }
+    if (CL > 8 && cudaFuncSetAttribute(k_pivchol_cl<CL>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
+                      cudaSuccess) { cudaGetLastError(); return false; }
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    cfg.gridDim = dim3(CL);
+    cfg.blockDim = dim3(512);
+    cfg.dynamicSmemBytes = 225 * 1024;
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CL;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = CL > 1 ? 1 : 0;
+    int nclusters = 1;
+    if (CL > 1 && cudaOccupancyMaxActiveClusters(&nclusters, k_pivchol_cl<CL>, &cfg) != cudaSuccess) {
+      cudaGetLastError();
+      nclusters = 0;
+    }
+    ok = nclusters > 0 ? 1 : 0;
+  }
+  if (!ok) return false;
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute at[1];
+  cfg.gridDim = dim3(CL);
+  cfg.blockDim = dim3(512);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CL;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = CL > 1 ? 1 : 0;
+  CK(cudaLaunchKernelEx(&cfg, k_pivchol_cl<CL>, A, n, tol, perm, rank, status, gx));
+  return true;
+}
+
+static bool launch_pivchol_cluster(double* A, int n, double tol, int* perm, int* rank, int* status, double* gx,
+                                   cudaStream_t st) {
+  if (n > kPivcholClusterMaxN) return false;
+  return pivchol_cluster_try<1>(A, n, tol, perm, rank, status, gx, st) ||
+         pivchol_cluster_try<2>(A, n, tol, perm, rank, status, gx, st) ||
+         pivchol_cluster_try<4>(A, n, tol, perm, rank, status, gx, st) ||
+         pivchol_cluster_try<8>(A, n, tol, perm, rank, status, gx, st) ||
+         pivchol_cluster_try<16>(A, n, tol, perm, rank, status, gx, st);
+}
+
+// Alg. 1 line 9 on a symmetric n x n matrix already in device memory (full
+// storage): the cluster kernel when the matrix fits distributed shared memory,
+// else the cooperative-grid kernel.  Scratch: ctl 4 ints, gx n + 64 doubles.
+static void launch_pivchol(double* A, int n, double tol, int* perm, int* rank, int* status, int* ctl, double* gx,
+                           cudaStream_t st) {
+  if (launch_pivchol_cluster(A, n, tol, perm, rank, status, gx, st)) return;
+  static int coop_blocks = 0;
+  if (!coop_blocks) {
+    int dev = 0, sms = 0, per_sm = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pivchol_coop, 512, 0));
+    coop_blocks = sms * std::max(1, std::min(per_sm, 2));
+  }
+  void* args[] = {&A, &n, &tol, &perm, &rank, &status, &ctl};
+  CK(cudaLaunchCooperativeKernel((void*)k_pivchol_coop, coop_blocks, 512, args, 0, st));
+}
+
 // Rank-Revealing Simultaneous FETI, Alg. 1 of PAPER.md:302-351:
 // one search direction per subdomain, Delta = Q^T W factorized by the
 // rank-revealing Cholesky, W, Q compressed to F-orthonormal columns, and the
@@ -1563,17 +1642,9 @@ int Ctx::solve_rrs(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_tra
   lam.alloc(m); r.alloc(m); z.alloc(m); q.alloc(m); tmp.alloc(m);
   W.alloc((size_t)m * Ns); Qb.alloc((size_t)m * Ns);
   ctl.alloc(4);
+  DBuf<double> pivx;
+  pivx.alloc((size_t)Ns + 64);
   Linv.alloc((size_t)Ns * Ns);
-  int coop_blocks = 0;
-  {
-    int dev = 0, sms = 0, per_sm = 0;
-    CK(cudaGetDevice(&dev));
-    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pivchol_coop, 512, 0));
-    coop_blocks = sms * std::max(1, std::min(per_sm, 2));
-    CK(cudaFuncSetAttribute(k_pivchol, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            kPivcholSmemMax * kPivcholSmemMax * 8));
-  }
   Delta.alloc((size_t)Ns * Ns); gamma.alloc(Ns);
   perm.alloc(Ns); rank_d.alloc(1);
   sc.alloc(1);
@@ -1665,19 +1736,7 @@ int Ctx::solve_rrs(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_tra
     k_mirror_lower<<<grid_for((long long)k * k), kThreads, 0, st>>>(Delta.p, k);
     mark(2);
     // line 9
-    if (k <= kPivcholSmemMax) {
-      k_pivchol<<<1, 1024, (size_t)k * k * 8, st>>>(Delta.p, k, o.pivot_tol, perm.p, rank_d.p, d_status.p);
-    } else {
-      double* dp = Delta.p;
-      double tolv = o.pivot_tol;
-      int kk = k;
-      int* pp = perm.p;
-      int* rp = rank_d.p;
-      int* sp = d_status.p;
-      int* cp = ctl.p;
-      void* args[] = {&dp, &kk, &tolv, &pp, &rp, &sp, &cp};
-      CK(cudaLaunchCooperativeKernel((void*)k_pivchol_coop, coop_blocks, 512, args, 0, st));
-    }
+    launch_pivchol(Delta.p, k, o.pivot_tol, perm.p, rank_d.p, d_status.p, ctl.p, pivx.p, st);
     LAUNCH_CHECK();
     mark(3);
     int rank = 0;
@@ -2041,6 +2100,75 @@ int fetigpu_fp64_peak(double* tflops_dmma, double* tflops_dfma) {
     cudaEventDestroy(a);
     cudaEventDestroy(b);
     cudaFree(out);
+  });
+}
+
+int fetigpu_pivoted_cholesky(const double* a, int n, double tol, int* perm, double* lower, int* rank) {
+  return guarded([&] {
+    if (n < 0 || (n > 0 && (!a || !perm || !lower || !rank))) fail(FETIGPU_E_INVALID_ARGUMENT, "bad arguments");
+    *rank = 0;
+    if (n == 0) return;
+    cudaStream_t st;
+    CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    std::unique_ptr<CUstream_st, decltype(&cudaStreamDestroy)> st_guard(st, cudaStreamDestroy);
+    DBuf<double> A;
+    DBuf<int> p, r, status, ctl;
+    DBuf<double> gx;
+    A.alloc((size_t)n * n);
+    p.alloc(n); r.alloc(1); status.alloc(1); ctl.alloc(4); gx.alloc((size_t)n + 64);
+    status.zero(st);
+    CK(cudaMemcpyAsync(A.p, a, (size_t)n * n * 8, cudaMemcpyHostToDevice, st));
+    k_mirror_lower<<<grid_for((long long)n * n), kThreads, 0, st>>>(A.p, n);
+    launch_pivchol(A.p, n, tol, p.p, r.p, status.p, ctl.p, gx.p, st);
+    LAUNCH_CHECK();
+    int hstat = 0;
+    std::vector<double> full((size_t)n * n);
+    CK(cudaMemcpyAsync(full.data(), A.p, (size_t)n * n * 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(perm, p.p, (size_t)n * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(rank, r.p, 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&hstat, status.p, 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (hstat) fail(FETIGPU_E_INDEFINITE_INPUT, "pivoted Cholesky: negative pivot");
+    // L: column k (k < rank) holds rows i >= k; everything else zero
+    for (int k = 0; k < n; ++k)
+      for (int i = 0; i < n; ++i)
+        lower[(size_t)k * n + i] = (k < *rank && i >= k) ? full[(size_t)k * n + i] : 0.0;
+  });
+}
+
+int fetigpu_pivoted_compress(const int* perm, const double* lower, int n, int rank, const double* w, int rows,
+                             double* out) {
+  return guarded([&] {
+    if (n < 0 || rank < 0 || rank > n || rows < 0 || (rank > 0 && rows > 0 && (!perm || !lower || !w || !out)))
+      fail(FETIGPU_E_INVALID_ARGUMENT, "bad arguments");
+    if (rank == 0 || rows == 0) return;
+    cudaStream_t st;
+    CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    std::unique_ptr<CUstream_st, decltype(&cudaStreamDestroy)> st_guard(st, cudaStreamDestroy);
+    cublasHandle_t h;
+    CB(cublasCreate(&h));
+    std::unique_ptr<cublasContext, decltype(&cublasDestroy)> h_guard(h, cublasDestroy);
+    CB(cublasSetStream(h, st));
+    DBuf<double> L, Linv, W, Wsel, O;
+    DBuf<int> p;
+    L.alloc((size_t)n * n); Linv.alloc((size_t)rank * rank);
+    W.alloc((size_t)rows * n); Wsel.alloc((size_t)rows * rank); O.alloc((size_t)rows * rank);
+    p.alloc(n);
+    CK(cudaMemcpyAsync(L.p, lower, (size_t)n * n * 8, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(W.p, w, (size_t)rows * n * 8, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(p.p, perm, (size_t)n * 4, cudaMemcpyHostToDevice, st));
+    // L~^{-1} by a triangular solve on the identity, W_sel = W N^T[:, :rank],
+    // out = W_sel L~^{-T}: the solver's compression (Alg. 1 lines 10-11)
+    k_identity<<<grid_for((long long)rank * rank), kThreads, 0, st>>>(Linv.p, rank);
+    const double one = 1.0;
+    CB(cublasDtrsm(h, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, rank, rank, &one,
+                   L.p, n, Linv.p, rank));
+    k_gather_cols<<<dim3(grid_for(rows), rank), kThreads, 0, st>>>(W.p, rows, p.p, rank, Wsel.p);
+    CB(cublasDtrmm(h, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, rows, rank, &one,
+                   Linv.p, rank, Wsel.p, rows, O.p, rows));
+    LAUNCH_CHECK();
+    CK(cudaMemcpyAsync(out, O.p, (size_t)rows * rank * 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
   });
 }
 

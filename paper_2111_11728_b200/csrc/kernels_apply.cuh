@@ -738,103 +738,210 @@ __global__ void k_nd_backsub(const NdDev* __restrict__ nodes, const int* __restr
 // Rank-revealing pivoted Cholesky of the k x k Gram matrix Delta (Alg. 1
 // line 9; pivoted_cholesky contract SPEC.md:43-47 with a symmetric trailing
 // update): one CTA, pivots sequential, updates parallel.
-// Staged in shared memory when n*n doubles fit (n <= kPivcholSmemMax); the
-// global-memory form is kept for the cooperative kernel's size range.
-constexpr int kPivcholSmemMax = 160;
-__global__ void __launch_bounds__(1024) k_pivchol(double* Ag, int n, double tol, int* perm,
-                                                  int* rank_out, int* status) {
-  extern __shared__ double s_a[];
-  __shared__ double sv[32];
-  __shared__ int si[32];
-  __shared__ double s_scale;
-  __shared__ int s_piv;
-  __shared__ int s_stop;
+// Rank-revealing pivoted Cholesky on one thread-block cluster of CL CTAs:
+// the n x n Gram matrix lives in the cluster's distributed shared memory, row j
+// on CTA j % CL (local row j / CL), so k <= 640 stays on chip with CL = 16.
+// Four barriers per pivot:
+//   each CTA publishes its best remaining diagonal (tracked during the
+//   previous trailing update) -> cluster barrier (1) -> every warp reduces the
+//   CL candidates (ties -> lowest index, so all pick the same pivot) -> the
+//   owners of rows k and piv fetch the partner row over DSMEM with the column
+//   transposition applied -> (2) -> rows rewritten, columns k <-> piv swapped
+//   in every other row, row k scaled by 1/sqrt(pivot) from the fetched copy
+//   and published -> (3) -> every CTA copies row k -> CTA barrier (4) ->
+//   rank-1 update of its own rows.
+// The one-to-all traffic (candidates, pivot row) goes through a small global
+// scratch `gx` (L2; the cluster barrier orders it and invalidates L1): a DSMEM
+// broadcast would serialise on the owner's shared-memory port.
+// Per-element arithmetic and tie-breaking are those of the right-looking
+// algorithm in k_pivchol_coop (and the oracle): results are bit-identical.
+constexpr int kPivcholClusterMaxN = 640;
+template <int CL>
+__global__ void __launch_bounds__(512) k_pivchol_cl(double* Ag, int n, double tol, int* perm, int* rank_out,
+                                                    int* status, double* gx /* n + 4*CL */) {
+  namespace cg = cooperative_groups;
+  extern __shared__ double s_dyn[];
+  __shared__ double s_wv[16];
+  __shared__ int s_wi[16];
+  const int R = (n + CL - 1) / CL;
+  double* A = s_dyn;                   // R x n, own rows
+  double* prow = A + (size_t)R * n;    // copy of the scaled pivot row
+  double* tmpk = prow + n;             // incoming row for local row k
+  double* tmpp = tmpk + n;             // incoming row for local row piv
+  double* gcand = gx + n;              // per CTA: (value, index, max diag)
   const int tid = threadIdx.x, nt = blockDim.x;
   const int lane = tid & 31, warp = tid >> 5, nwarp = nt >> 5;
-  const bool staged = n <= kPivcholSmemMax;
-  double* A = staged ? s_a : Ag;
-  if (staged)
-    for (int i = tid; i < n * n; i += nt) A[i] = Ag[i];
-  for (int i = tid; i < n; i += nt) perm[i] = i;
-  __syncthreads();
-  // scale = max initial diagonal
-  double mx = -1e300;
-  for (int i = tid; i < n; i += nt) mx = fmax(mx, A[(size_t)i * n + i]);
-  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  if (lane == 0) sv[warp] = mx;
-  __syncthreads();
-  if (tid == 0) {
-    double m2 = sv[0];
-    for (int w = 1; w < nwarp; ++w) m2 = fmax(m2, sv[w]);
-    s_scale = m2;
-  }
-  __syncthreads();
-  const double stop_tol = tol * s_scale;
-  const double neg_tol = -tol * fmax(s_scale, 1e-300);
-  int rank = 0;
-  for (int k = 0; k < n; ++k) {
-    // argmax over the remaining diagonal, ties -> lowest index
-    double bv = -1e300;
-    int bi = n;
-    for (int j = k + tid; j < n; j += nt) {
-      const double v = A[(size_t)j * n + j];
-      if (v > bv || (v == bv && j < bi)) { bv = v; bi = j; }
-    }
+  int me = 0;
+  if constexpr (CL > 1) me = (int)cg::this_cluster().block_rank();
+  auto csync = [&]() {
+    if constexpr (CL > 1) cg::this_cluster().sync();
+    else __syncthreads();
+  };
+  auto remote = [&](double* p, int r) -> double* {
+    if constexpr (CL > 1) return cg::this_cluster().map_shared_rank(p, r);
+    else return p;
+  };
+  auto better = [](double v, int i, double bv, int bi) { return v > bv || (v == bv && i < bi); };
+  auto ldx = [](const double* p) -> double {  // L2 read for peers; same-SM data may sit in L1
+    if constexpr (CL > 1) return __ldcg(p);
+    else return *(volatile const double*)p;
+  };
+  auto warp_best = [&](double& v, int& i) {
     for (int o = 16; o > 0; o >>= 1) {
-      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-      if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+      const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, i, o);
+      if (better(ov, oi, v, i)) { v = ov; i = oi; }
     }
-    if (lane == 0) { sv[warp] = bv; si[warp] = bi; }
+  };
+  // publish this CTA's candidate (after the per-warp partials are in s_wv/s_wi)
+  auto publish = [&](double mx) {
+    if constexpr (CL == 1) return;  // single CTA: the warp partials in s_wv / s_wi are read directly
     __syncthreads();
-    if (tid == 0) {
-      double v = sv[0];
-      int b = si[0];
-      for (int w = 1; w < nwarp; ++w)
-        if (sv[w] > v || (sv[w] == v && si[w] < b)) { v = sv[w]; b = si[w]; }
-      s_piv = b;
-      s_stop = !(v > stop_tol);
+    if (warp == 0) {
+      double v = lane < nwarp ? s_wv[lane] : -1e300;
+      int i = lane < nwarp ? s_wi[lane] : n;
+      warp_best(v, i);
+      if (lane == 0) {
+        gcand[3 * me] = v;
+        gcand[3 * me + 1] = (double)i;
+        gcand[3 * me + 2] = mx;
+      }
     }
-    __syncthreads();
-    if (s_stop) {
-      for (int j = k + tid; j < n; j += nt)
-        if (A[(size_t)j * n + j] < neg_tol) atomicExch(status, 2 /* IndefiniteInput */);
+  };
+  for (int lr = 0; lr < R; ++lr) {
+    const int j = lr * CL + me;
+    if (j < n)
+      for (int i = tid; i < n; i += nt) A[(size_t)lr * n + i] = Ag[(size_t)j * n + i];
+  }
+  if (me == 0)
+    for (int i = tid; i < n; i += nt) perm[i] = i;
+  __syncthreads();
+  // scale = max initial diagonal over the cluster; first candidates (k = 0)
+  double bv = -1e300, mx = -1e300;
+  int bi = n;
+  for (int lr = tid; lr < R; lr += nt) {
+    const int j = lr * CL + me;
+    if (j < n) {
+      const double v = A[(size_t)lr * n + j];
+      mx = fmax(mx, v);
+      if (better(v, j, bv, bi)) { bv = v; bi = j; }
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  warp_best(bv, bi);
+  __shared__ double s_mx[16];
+  if (lane == 0) { s_wv[warp] = bv; s_wi[warp] = bi; s_mx[warp] = mx; }
+  __syncthreads();
+  double cmx = -1e300;
+  for (int w = 0; w < nwarp; ++w) cmx = fmax(cmx, s_mx[w]);
+  publish(cmx);
+  csync();
+  double scale = -1e300;
+  if constexpr (CL == 1) scale = cmx;
+  else
+    for (int r = lane; r < CL; r += 32) scale = fmax(scale, ldx(&gcand[3 * r + 2]));
+  for (int o = 16; o > 0; o >>= 1) scale = fmax(scale, __shfl_xor_sync(0xffffffffu, scale, o));
+  const double stop_tol = tol * scale;
+  const double neg_tol = -tol * fmax(scale, 1e-300);
+  int rank = 0;
+  bool first = true;
+  for (int k = 0; k < n; ++k) {
+    if (!first) csync();  // (1) candidates of the previous update visible
+    first = false;
+    double v = -1e300;
+    int b = n;
+    if constexpr (CL == 1) {
+      if (lane < nwarp) { v = s_wv[lane]; b = s_wi[lane]; }
+    } else if (lane < CL) {
+      v = ldx(&gcand[3 * lane]);
+      b = (int)ldx(&gcand[3 * lane + 1]);
+    }
+    warp_best(v, b);
+    if (!(v > stop_tol)) {
+      for (int lr = tid; lr < R; lr += nt) {
+        const int j = lr * CL + me;
+        if (j >= k && j < n && A[(size_t)lr * n + j] < neg_tol) atomicExch(status, 2 /* IndefiniteInput */);
+      }
       break;
     }
-    const int piv = s_piv;
+    const int piv = b;
+    const int ok = k % CL, op = piv % CL;
+    double* rowk = A + (size_t)(k / CL) * n;   // valid on CTA ok
     if (piv != k) {
-      for (int j = tid; j < n; j += nt) {  // rows k <-> piv
-        const double t = A[(size_t)j * n + k];
-        A[(size_t)j * n + k] = A[(size_t)j * n + piv];
-        A[(size_t)j * n + piv] = t;
+      // fetch the partner rows (old contents) with columns k <-> piv swapped
+      if (me == ok) {
+        const double* src = remote(A, op) + (size_t)(piv / CL) * n;
+        for (int i = tid; i < n; i += nt) tmpk[i] = src[i == k ? piv : (i == piv ? k : i)];
       }
-      __syncthreads();
-      for (int i = tid; i < n; i += nt) {  // columns k <-> piv
-        const double t = A[(size_t)k * n + i];
-        A[(size_t)k * n + i] = A[(size_t)piv * n + i];
-        A[(size_t)piv * n + i] = t;
+      if (me == op) {
+        const double* src = remote(A, ok) + (size_t)(k / CL) * n;
+        for (int i = tid; i < n; i += nt) tmpp[i] = src[i == k ? piv : (i == piv ? k : i)];
       }
-      if (tid == 0) { const int t = perm[k]; perm[k] = perm[piv]; perm[piv] = t; }
-      __syncthreads();
     }
-    const double l = sqrt(A[(size_t)k * n + k]);
-    __syncthreads();
-    if (tid == 0) A[(size_t)k * n + k] = l;
-    for (int i = k + 1 + tid; i < n; i += nt) A[(size_t)k * n + i] /= l;
-    __syncthreads();
-    // trailing rank-1 update: a warp per row j, lanes over i
-    for (int j = k + 1 + warp; j < n; j += nwarp) {
-      const double akj = A[(size_t)k * n + j];
-      for (int i = k + 1 + lane; i < n; i += 32) A[(size_t)j * n + i] -= A[(size_t)k * n + i] * akj;
+    csync();  // (2) partner rows read, all candidate reads done
+    const double* srck = piv != k ? tmpk : rowk;
+    double l = 0.0;
+    if (me == ok) l = sqrt(srck[k]);
+    if (piv != k) {
+      for (int lr = tid; lr < R; lr += nt) {  // other rows: columns k <-> piv
+        const int j = lr * CL + me;
+        if (j >= n || j == k || j == piv) continue;
+        double* row = A + (size_t)lr * n;
+        const double t = row[k];
+        row[k] = row[piv];
+        row[piv] = t;
+      }
+      if (me == op) {
+        double* row = A + (size_t)(piv / CL) * n;
+        for (int i = tid; i < n; i += nt) row[i] = tmpp[i];
+      }
+      if (me == 0 && tid == 0) { const int t = perm[k]; perm[k] = perm[piv]; perm[piv] = t; }
     }
-    __syncthreads();
+    if (me == ok)  // row k := fetched row, entries right of the pivot scaled and published
+      for (int i = tid; i < n; i += nt)
+        if (i != k) {
+          const double x = i > k ? srck[i] / l : srck[i];
+          rowk[i] = x;
+          if (CL > 1 && i > k) gx[i] = x;
+        }
+    csync();  // (3) scaled pivot row visible
+    if (me == ok && tid == 0) rowk[k] = l;  // nobody reads the pivot entry after (3)
+    if constexpr (CL > 1) {
+      if (me != ok)
+        for (int i = k + 1 + tid; i < n; i += nt) prow[i] = __ldcg(&gx[i]);
+      else
+        for (int i = k + 1 + tid; i < n; i += nt) prow[i] = rowk[i];
+    } else {
+      for (int i = k + 1 + tid; i < n; i += nt) prow[i] = rowk[i];
+    }
+    __syncthreads();  // (4)
+    // trailing rank-1 update of own rows j > k (a warp per row, lanes over i),
+    // tracking the best updated diagonal as the next candidate
+    bv = -1e300;
+    bi = n;
+    for (int lr = warp; lr < R; lr += nwarp) {
+      const int j = lr * CL + me;
+      if (j <= k || j >= n) continue;
+      double* row = A + (size_t)lr * n;
+      const double akj = prow[j];
+      for (int i = k + 1 + lane; i < n; i += 32) {
+        const double nv = row[i] - prow[i] * akj;
+        row[i] = nv;
+        if (i == j && better(nv, j, bv, bi)) { bv = nv; bi = j; }
+      }
+    }
+    warp_best(bv, bi);
+    if (lane == 0) { s_wv[warp] = bv; s_wi[warp] = bi; }
+    publish(0.0);
     rank = k + 1;
   }
-  if (staged) {
-    __syncthreads();
-    for (int i = tid; i < n * n; i += nt) Ag[i] = A[i];
+  csync();  // no CTA leaves while a peer may still read its shared memory
+  for (int lr = 0; lr < R; ++lr) {
+    const int j = lr * CL + me;
+    if (j < n)
+      for (int i = tid; i < n; i += nt) Ag[(size_t)j * n + i] = A[(size_t)lr * n + i];
   }
-  if (tid == 0) *rank_out = rank;
+  if (me == 0 && tid == 0) *rank_out = rank;
 }
 
 // Same algorithm and per-element arithmetic as k_pivchol, spread over a

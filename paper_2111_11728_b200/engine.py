@@ -78,7 +78,8 @@ EXPORTED = ["fetigpu_set_device", "fetigpu_create", "fetigpu_build", "fetigpu_de
             "fetigpu_local_operator", "fetigpu_device_alloc", "fetigpu_device_free",
             "fetigpu_host_alloc", "fetigpu_host_free", "fetigpu_memcpy", "fetigpu_fill_random",
             "fetigpu_synchronize", "fetigpu_time_apply", "fetigpu_apply_F_block_device",
-            "fetigpu_time_apply_block", "fetigpu_fp64_peak", "fetigpu_selftest_dmma"]
+            "fetigpu_time_apply_block", "fetigpu_fp64_peak", "fetigpu_selftest_dmma",
+            "fetigpu_pivoted_cholesky", "fetigpu_pivoted_compress"]
 
 
 class FgProblem(C.Structure):
@@ -147,6 +148,37 @@ def fp64_peak():
     a, b = C.c_double(), C.c_double()
     check(lib().fetigpu_fp64_peak(C.byref(a), C.byref(b)))
     return a.value, b.value
+
+
+def pivoted_cholesky(a: np.ndarray, tol: float = 1e-12):
+    """Device rank-revealing pivoted Cholesky (feti::pivoted_cholesky,
+    linalg.hpp:80; SPEC.md:43-47).  Returns (perm, L[:, :rank], rank) with
+    A[perm][:, perm] = L L^T on the kept block, like oracle.pyoracle's helper."""
+    a = np.asarray(a, dtype=np.float64)
+    n = a.shape[0]
+    A = np.asfortranarray(a)
+    perm = np.zeros(max(n, 1), dtype=np.int32)
+    low = np.zeros(max(n * n, 1))
+    rank = C.c_int()
+    check(lib().fetigpu_pivoted_cholesky(A.ctypes.data_as(D), n, C.c_double(tol), _p(perm), _p(low),
+                                         C.byref(rank)))
+    L = low[:n * n].reshape(n, n).T[:, :rank.value].copy()
+    return perm[:n], L, rank.value
+
+
+def compress(perm, lower, rank: int, w: np.ndarray) -> np.ndarray:
+    """Device W N^T [L~^{-T}; 0] (PivotedCholesky::compress, linalg.hpp:79);
+    `lower` is the n x rank block from pivoted_cholesky."""
+    n = len(perm)
+    low = np.zeros((n, n))
+    low[:, :rank] = lower
+    lowf = np.ascontiguousarray(low.T).reshape(-1)      # column-major n x n
+    pv = np.ascontiguousarray(perm, dtype=np.int32)
+    W = np.asfortranarray(w, dtype=np.float64)
+    out = np.zeros((w.shape[0], max(rank, 1)), order="F")
+    check(lib().fetigpu_pivoted_compress(_p(pv), _p(lowf), n, rank, W.ctypes.data_as(D), w.shape[0],
+                                         out.ctypes.data_as(D)))
+    return np.ascontiguousarray(out[:, :rank])
 
 
 def dmma_selftest(A: np.ndarray, B: np.ndarray) -> np.ndarray:

@@ -37,7 +37,14 @@ int main() {
     auto lam = sys.solve(o, &tr);
     auto u = sys.recover_primal(lam);
     std::printf("solve status %d iterations %d tip uy %.6e\n", tr.status, tr.iterations, u[1][2 * n + 1]);
-    return tr.status == 0 ? 0 : 3;
+    // pivoted_cholesky / PivotedCholesky::compress (linalg.hpp:72-89)
+    std::vector<double> a{1.0, 2.0, 2.0, 4.0 + 1e-3};  // 2x2 column-major, pivot 1 first
+    auto pc = fetigpu::pivoted_cholesky(a, 2);
+    std::vector<double> w{1.0, 0.0, 0.0, 1.0};
+    auto c = pc.compress(w, 2);
+    std::printf("pivchol rank %d perm %d %d L00 %.6f compress %zu\n", pc.rank, pc.permutation[0],
+                pc.permutation[1], pc.lower[0], c.size());
+    return tr.status == 0 && pc.rank == 2 && pc.permutation[0] == 1 ? 0 : 3;
   } catch (const std::exception& e) {
     std::printf("exception: %s\n", e.what());
     return 2;

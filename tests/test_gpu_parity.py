@@ -339,3 +339,50 @@ def test_floating_tfeti_rank_deficient_coarse(oracle_mod):
     assert tg["status"] == to["status"] == 0 and abs(tg["iterations"] - to["iterations"]) <= 1
     # same multipliers on range(P)
     assert np.linalg.norm(g.project(lg - lo)) < 1e-8 * np.linalg.norm(lo)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,deficit", [(1, 0), (5, 0), (32, 3), (96, 7), (160, 0), (161, 3), (300, 20),
+                                       (512, 0), (640, 11), (700, 5), (1024, 0)])
+def test_pivoted_cholesky_device(n, deficit, oracle_mod):
+    """fetigpu_pivoted_cholesky (linalg.hpp:80) vs the oracle on
+    graded PSD Gram matrices of rank n - deficit.  Covers the cluster kernel
+    at every cluster size (1..16 CTAs, n <= 640) and the cooperative-grid
+    kernel above.  Rank and pivot order must be identical; L agrees to
+    rounding (the device contracts a*b+c into FMA, the oracle does not)."""
+    from paper_2111_11728_b200 import engine
+    rng = np.random.default_rng(1000 + n)
+    r = n - deficit
+    X = rng.standard_normal((n, r)) * np.logspace(0, -3, r)
+    A = X @ X.T
+    pg, Lg, rg = engine.pivoted_cholesky(A)
+    po, Lo, ro = oracle_mod.pivoted_cholesky(A)
+    assert rg == ro == r
+    assert np.array_equal(pg, po)
+    assert np.linalg.norm(Lg - Lo) <= 1e-9 * np.linalg.norm(Lo)
+    Ap = A[np.ix_(pg, pg)]
+    assert np.linalg.norm(Ap[:, :r] - (Lg @ Lg[:r].T)) <= 1e-13 * n * np.linalg.norm(A)
+    # compression W N^T [L~^{-T}; 0] (PivotedCholesky::compress) vs the oracle's
+    W = rng.standard_normal((257, n))
+    cg = engine.compress(pg, Lg, rg, W)
+    co = oracle_mod.compress(po, Lo, ro, W)
+    assert cg.shape == co.shape == (257, r)
+    # W L~^{-T} amplifies the rounding difference of L by cond(L~) ~ 1e3 here
+    assert np.linalg.norm(cg - co) <= 1e-6 * np.linalg.norm(co)
+
+
+@pytest.mark.gpu
+def test_pivoted_cholesky_device_edge_cases(oracle_mod):
+    from paper_2111_11728_b200 import engine
+    # negative remaining diagonal -> IndefiniteInput, like the oracle (code 2)
+    with pytest.raises(engine.IndefiniteInput):
+        engine.pivoted_cholesky(np.diag([1.0, -1.0]))
+    with pytest.raises(oracle_mod.OracleError):
+        oracle_mod.pivoted_cholesky(np.diag([1.0, -1.0]))
+    # all-zero matrix: rank 0, identity permutation
+    p, L, r = engine.pivoted_cholesky(np.zeros((4, 4)))
+    assert r == 0 and list(p) == [0, 1, 2, 3] and L.shape == (4, 0)
+    # ties -> lowest index (SPEC.md:43-47)
+    p, L, r = engine.pivoted_cholesky(np.eye(3) * 2.0)
+    assert r == 3 and list(p) == [0, 1, 2]
+    assert np.allclose(L, np.sqrt(2.0) * np.eye(3))
