@@ -275,6 +275,24 @@ def run_reference(args, ws, rank, dist):
     print(json.dumps(line), flush=True)
 
 
+def apply_time_us(engine, g, reps=200):
+    """Device time of one F-apply (CUDA events around each apply, after 20
+    warm-up applies, no L2 flush): for C1-C3/C5 the operator fits L2."""
+    L = engine.lib()
+    m = g.m
+    dx, dy = C.c_void_p(), C.c_void_p()
+    engine.check(L.fetigpu_device_alloc(g.h, C.c_size_t(8 * m), C.byref(dx)))
+    engine.check(L.fetigpu_device_alloc(g.h, C.c_size_t(8 * m), C.byref(dy)))
+    xp, yp = C.cast(dx, C.POINTER(C.c_double)), C.cast(dy, C.POINTER(C.c_double))
+    engine.check(L.fetigpu_fill_random(g.h, xp, C.c_size_t(m), C.c_ulonglong(7)))
+    ms, n = (C.c_double * 3)(), C.c_int()
+    engine.check(L.fetigpu_time_apply(g.h, xp, yp, 1, 20, 0, ms, C.byref(n)))
+    engine.check(L.fetigpu_time_apply(g.h, xp, yp, 1, reps, 0, ms, C.byref(n)))
+    L.fetigpu_device_free(g.h, dx)
+    L.fetigpu_device_free(g.h, dy)
+    return ms[0] * 1e3
+
+
 def solve_table(engine, configs):
     out = {}
     for name, fn, kw in configs:
@@ -286,6 +304,13 @@ def solve_table(engine, configs):
                      "iterations": tr["iterations"], "status": ["converged", "max_iter", "breakdown"][tr["status"]],
                      "rel_residual": tr["eps_final"] / tr["eps0"] if tr["eps0"] > 0 else 0.0,
                      "m": st["m"], "directions": ["single", "fo", "rrs"][kw.get("directions", 0)]}
+        if not name.startswith("C4"):
+            # C1-C3 and C5 operators are L2-resident -- time per apply and
+            # effective GB/s of the formula bytes, labelled as such (no HBM-fraction claim)
+            us = apply_time_us(engine, g)
+            out[name]["apply_us"] = round(us, 2)
+            out[name]["apply_formula_bytes"] = st["op_bytes"]
+            out[name]["apply_effective_GBps_L2_resident"] = round(st["op_bytes"] / (us * 1e-6) / 1e9, 1)
         g.close()
         log(name, out[name])
     return out

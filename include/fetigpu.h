@@ -150,6 +150,8 @@ typedef struct fetigpu_stats {
   double build_ms;           /* device time of fetigpu_build */
   double nd_ms, slot_ms, coarse_ms;
   double device_bytes;       /* device memory held by the context */
+  int host_pipeline;         /* 1: fetigpu_apply_F overlaps the H2D of x with the GEMV */
+  int reserved_;
 } fetigpu_stats;
 
 /* Select the CUDA device used by contexts built afterwards from this host

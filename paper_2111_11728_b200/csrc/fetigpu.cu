@@ -196,7 +196,24 @@ struct Ctx {
     if (stage_x.n < n) { stage_x.alloc(n); stage_y.alloc(n); }
   }
 
+  // Host-buffer F-apply pipeline (fetigpu_apply_F with host pointers, FETI-DP
+  // on the symmetric path): lambda goes over PCIe in kPipe row-prefix chunks on
+  // a copy stream; the subdomains of chunk c (rows < pipe_need[c]) start their
+  // phase-1 GEMV on their own stream as soon as that prefix has landed, so the
+  // H2D copy overlaps the operator stream and the chunks fill the GPU together.
+  static constexpr int kPipe = 4;
+  cudaStream_t pipe_st[kPipe] = {}, pipe_cp = nullptr;
+  cudaEvent_t pipe_in[kPipe] = {}, pipe_done[kPipe] = {}, pipe_start = nullptr;
+  int pipe_s0[kPipe + 1] = {}, pipe_need[kPipe] = {};
+  bool pipe_ready = false;
+  std::vector<int> sub_maxrow;  // per subdomain: largest dual row it touches (-1: none)
+
   ~Ctx() {
+    for (auto& e : pipe_in) if (e) cudaEventDestroy(e);
+    for (auto& e : pipe_done) if (e) cudaEventDestroy(e);
+    if (pipe_start) cudaEventDestroy(pipe_start);
+    for (auto& q : pipe_st) if (q) cudaStreamDestroy(q);
+    if (pipe_cp) cudaStreamDestroy(pipe_cp);
     if (cb) cublasDestroy(cb);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
@@ -555,6 +572,11 @@ struct Ctx {
         ++ip;
       }
     }
+    sub_maxrow.assign(Ns, -1);
+    for (int s = 0; s < Ns; ++s) {
+      const size_t b = (size_t)top_off[s] * KR, e = b + su.subs[s].Top.size() * (size_t)KR;
+      for (size_t q = b; q < e; ++q) sub_maxrow[s] = std::max(sub_maxrow[s], rows[q]);
+    }
     d_oprows.upload(rows, st); d_opcoef.upload(coef, st);
     d_slot_of.upload(slot_of, st); d_design.upload(design, st);
     d_top_pos.upload(top_pos, st); d_top_off.upload(top_off, st);
@@ -845,6 +867,7 @@ struct Ctx {
       pc_sym = true;
     }
     ptimer.mark("symmetric packing", st);
+    setup_pipe();
     // ---- work per apply
     double sn2 = 0, snc = 0, sns = 0;
     for (int s = 0; s < Ns; ++s) {
@@ -970,6 +993,76 @@ struct Ctx {
         LAUNCH_CHECK();
       }
     }
+  }
+
+  void setup_pipe() {
+    pipe_ready = false;
+    const char* off = getenv("FETIGPU_NO_PIPE");
+    if ((off && off[0] == '1') || !use_sym || su.method != FETIGPU_FETIDP || su.Ns < 4 * kPipe) return;
+    int run = -1;
+    for (int c = 0; c < kPipe; ++c) {
+      pipe_s0[c] = (int)((long long)su.Ns * c / kPipe);
+      pipe_s0[c + 1] = (int)((long long)su.Ns * (c + 1) / kPipe);
+      for (int s = pipe_s0[c]; s < pipe_s0[c + 1]; ++s) run = std::max(run, sub_maxrow[s]);
+      pipe_need[c] = run + 1;  // rows [0, need) cover every row chunks 0..c gather
+    }
+    // worthwhile only if the first chunks need a real prefix of lambda
+    if (pipe_need[kPipe / 2 - 1] > (long long)su.m * 3 / 4) return;
+    if (!pipe_cp) {
+      CK(cudaStreamCreateWithFlags(&pipe_cp, cudaStreamNonBlocking));
+      for (int c = 0; c < kPipe; ++c) {
+        CK(cudaStreamCreateWithFlags(&pipe_st[c], cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&pipe_in[c], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&pipe_done[c], cudaEventDisableTiming));
+      }
+      CK(cudaEventCreateWithFlags(&pipe_start, cudaEventDisableTiming));
+    }
+    pipe_ready = true;
+  }
+
+  // y = F x with x, y in (pinned) host memory; the result is identical to
+  // the device path (same kernels per subdomain, same phase-2 order)
+  void apply_F_host(const double* xh, double* yh) {
+    const int m = su.m;
+    stage(m);
+    double* x = stage_x.p;
+    double* y = stage_y.p;
+    if (!pipe_ready) {
+      CK(cudaMemcpyAsync(x, xh, (size_t)m * 8, cudaMemcpyHostToDevice, st));
+      apply_F(x, y, 1, m, m);
+    } else {
+      CK(cudaEventRecord(pipe_start, st));  // after everything already queued on st
+      CK(cudaStreamWaitEvent(pipe_cp, pipe_start, 0));
+      int done = 0;
+      for (int c = 0; c < kPipe; ++c) {
+        const int need = c == kPipe - 1 ? m : pipe_need[c];
+        if (need > done) {
+          CK(cudaMemcpyAsync(x + done, xh + done, (size_t)(need - done) * 8, cudaMemcpyHostToDevice, pipe_cp));
+          done = need;
+        }
+        CK(cudaEventRecord(pipe_in[c], pipe_cp));
+      }
+      for (int c = 0; c < kPipe; ++c) {
+        cudaStream_t q = pipe_st[c];
+        CK(cudaStreamWaitEvent(q, pipe_in[c], 0));
+        const int nblk = pipe_s0[c + 1] - pipe_s0[c];
+        k_sym_gemv_scatter<1, true><<<nblk, 256, sym_smem, q>>>(d_sym.p, d_symtiles.p, d_oprows.p,
+                                                                 d_opcoef_apply.p, x, nullptr, d_vbuf.p, d_voff.p,
+                                                                 d_dp.p, d_abc.p, d_tbuf.p, pipe_s0[c]);
+        LAUNCH_CHECK();
+        CK(cudaEventRecord(pipe_done[c], q));
+        CK(cudaStreamWaitEvent(st, pipe_done[c], 0));
+      }
+      // coarse: t = sum B_c^T t_s (fixed order), y := 0, u = Kbar^{-1} t; phase 2
+      k_coarse_gather<<<grid_for(std::max(su.Nc, m)), kThreads, 0, st>>>(d_optr.p, d_oidx.p, d_tbuf.p, su.Nc, d_g.p,
+                                                                         1.0, nullptr, y, m);
+      k_dense_gemv<<<grid_for((long long)su.Nc * 32), kThreads, 0, st>>>(d_Kinv.p, su.Nc, d_g.p, d_h.p);
+      k_dp_phase2<<<su.Ns, kThreads, 0, st>>>(d_op.p, d_dp.p, d_oprows.p, d_opcoef_apply.p, d_abc.p, d_cmap.p,
+                                              d_h.p, d_vbuf.p, y, 1.0);
+      LAUNCH_CHECK();
+    }
+    CK(cudaMemcpyAsync(yh, y, (size_t)m * 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
   }
 
   // Zcols: per-subdomain columns, column-major m x N_s (row_major = false)
@@ -1898,6 +1991,8 @@ int fetigpu_stats_get(const fetigpu_ctx* ctx, fetigpu_stats* s) {
     s->m = c.su.m; s->n_sub = c.su.Ns; s->local_dofs = c.su.nloc; s->n_c = c.su.Nc;
     s->n_kept = c.su.n_kept; s->n_iface = c.su.n_iface; s->max_ns = mx; s->n_designs = c.su.n_designs;
     s->n_op_slots = (int)c.su.op_slots.size();
+    s->host_pipeline = c.pipe_ready ? 1 : 0;
+    s->reserved_ = 0;
     s->n_pc_slots = (int)(c.su.precond == FETIGPU_DIRICHLET ? c.su.pc_slots.size() : c.su.pc_lumped_T.size());
     // algorithmic work per apply, pure index counts
     double sn2 = 0, snc = 0, sns = 0;
@@ -1939,6 +2034,10 @@ int fetigpu_apply_F(fetigpu_ctx* ctx, const double* x, double* y, int ncols, int
   return guarded([&] {
     NEED_BUILT(ctx);
     Ctx& c = ctx->c;
+    if (ncols == 1) {
+      c.apply_F_host(x, y);
+      return;
+    }
     const size_t bytes = (size_t)ld * ncols * 8;
     c.stage((size_t)ld * ncols);
     CK(cudaMemcpyAsync(c.stage_x.p, x, bytes, cudaMemcpyHostToDevice, c.st));

@@ -140,9 +140,10 @@ __global__ void __launch_bounds__(256) k_sym_gemv_scatter(
     const SymSub* __restrict__ subs, const double* __restrict__ tiles, const int* __restrict__ rows,
     const double* __restrict__ coefs, const double* __restrict__ x, double* __restrict__ y,
     double* __restrict__ vbuf, const int* __restrict__ voff, const DpSub* __restrict__ dps = nullptr,
-    const double* __restrict__ abc = nullptr, double* __restrict__ tbuf = nullptr) {
+    const double* __restrict__ abc = nullptr, double* __restrict__ tbuf = nullptr, int s0 = 0) {
   extern __shared__ double shm[];
-  const SymSub d = subs[blockIdx.x];
+  const int s = s0 + blockIdx.x;   // subdomain (s0: first subdomain of a pipelined chunk)
+  const SymSub d = subs[s];
   const int npad = d.nb * 32;
   double* xs = shm;                   // npad
   double* part = shm + npad;          // kSymWarps x npad
@@ -161,7 +162,7 @@ __global__ void __launch_bounds__(256) k_sym_gemv_scatter(
   }
   for (int j = threadIdx.x; j < kSymWarps * npad; j += blockDim.x) part[j] = 0.0;
   __syncthreads();
-  if (STORE_V && dps) fused_dp_t(dps[blockIdx.x], abc, xs, d.ns, tbuf);
+  if (STORE_V && dps) fused_dp_t(dps[s], abc, xs, d.ns, tbuf);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double* pw = part + warp * npad;
   const int ntiles = d.nb * (d.nb + 1) / 2;
@@ -202,7 +203,7 @@ __global__ void __launch_bounds__(256) k_sym_gemv_scatter(
 #pragma unroll
     for (int w = 0; w < kSymWarps; ++w) v += part[w * npad + i];
     if (STORE_V) {
-      vbuf[voff[blockIdx.x] + i] = v;
+      vbuf[voff[s] + i] = v;
     } else {
 #pragma unroll
       for (int k = 0; k < KR; ++k) {

@@ -112,7 +112,8 @@ class FgStats(C.Structure):
                                        "max_ns", "n_designs", "n_op_slots", "n_pc_slots")] + \
                [(k, C.c_double) for k in ("op_bytes", "op_flops_per_col", "main_kernel_bytes",
                                           "build_ms", "nd_ms", "slot_ms", "coarse_ms",
-                                          "device_bytes")]
+                                          "device_bytes")] + \
+               [("host_pipeline", C.c_int), ("reserved_", C.c_int)]
 
 
 def lib():

@@ -386,3 +386,39 @@ def test_pivoted_cholesky_device_edge_cases(oracle_mod):
     p, L, r = engine.pivoted_cholesky(np.eye(3) * 2.0)
     assert r == 3 and list(p) == [0, 1, 2]
     assert np.allclose(L, np.sqrt(2.0) * np.eye(3))
+
+
+def test_host_pipelined_apply(oracle_mod, monkeypatch):
+    """fetigpu_apply_F on host buffers overlaps the H2D copy of lambda with
+    the phase-1 GEMV (row-prefix chunks on separate streams, FETI-DP on the
+    symmetric path).  Same kernels per subdomain and the same phase-2 order as
+    the device path, so the result must be bit-identical to it, and match the
+    oracle."""
+    from paper_2111_11728_b200 import engine
+    import ctypes as C
+    prob = pb.config4(sx=8, sy=4, n=8)
+    monkeypatch.setenv("FETIGPU_FORCE_SYM", "1")
+    g = engine.FetiSystem(prob)
+    monkeypatch.delenv("FETIGPU_FORCE_SYM")
+    assert g.stats()["host_pipeline"] == 1
+    m = g.m
+    x = np.random.default_rng(5).standard_normal(m)
+    y_host = g.apply_F(x)                                  # pipelined host path
+    L = engine.lib()
+    dx, dy = C.c_void_p(), C.c_void_p()
+    engine.check(L.fetigpu_device_alloc(g.h, C.c_size_t(8 * m), C.byref(dx)))
+    engine.check(L.fetigpu_device_alloc(g.h, C.c_size_t(8 * m), C.byref(dy)))
+    engine.check(L.fetigpu_memcpy(g.h, dx, x.ctypes.data_as(C.c_void_p), C.c_size_t(8 * m), 1))
+    engine.check(L.fetigpu_apply_F_device(g.h, C.cast(dx, C.POINTER(C.c_double)),
+                                          C.cast(dy, C.POINTER(C.c_double)), 1, m))
+    y_dev = np.zeros(m)
+    engine.check(L.fetigpu_memcpy(g.h, y_dev.ctypes.data_as(C.c_void_p), dy, C.c_size_t(8 * m), 2))
+    engine.check(L.fetigpu_synchronize(g.h))
+    L.fetigpu_device_free(g.h, dx)
+    L.fetigpu_device_free(g.h, dy)
+    assert np.array_equal(y_host, y_dev)
+    for _ in range(3):                                     # repeated, back to back
+        assert np.array_equal(g.apply_F(x), y_host)
+    o = oracle_mod.Oracle(prob)
+    assert rel(y_host, o.apply_F(x)) <= 1e-8
+    g.close()
