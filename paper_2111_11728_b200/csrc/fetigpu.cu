@@ -520,12 +520,13 @@ struct Ctx {
     struct Ent { int row; double coef; double w; };
     KR = dp ? 1 : 3;
     KRp = KR;
-    std::vector<Ent> ent((size_t)Ns * nb * 3);
+    // entries are read only below ecnt[k]: no zero fill (Ns x nb x KR of them)
+    std::unique_ptr<Ent[]> ent(new Ent[(size_t)Ns * nb * KR]);
     std::vector<unsigned char> ecnt((size_t)Ns * nb, 0);
     auto add_ent = [&](int s, int pos, Ent e) {
       const size_t k = (size_t)s * nb + pos;
       if (ecnt[k] >= KR) fail(FETIGPU_E_STATE, "too many dual rows per DOF");
-      ent[k * 3 + ecnt[k]++] = e;
+      ent[k * KR + ecnt[k]++] = e;
     };
     for (int i = 0; i < su.m; ++i) {
       const Row& r = su.rows[i];
@@ -551,8 +552,8 @@ struct Ctx {
         top_pos[io] = t;
         for (int q = 0; q < KR; ++q) {
           const bool has = q < ecnt[k];
-          rows[io * KR + q] = has ? ent[k * 3 + q].row : -1;
-          coef[io * KR + q] = has ? ent[k * 3 + q].coef : 0.0;
+          rows[io * KR + q] = has ? ent[k * KR + q].row : -1;
+          coef[io * KR + q] = has ? ent[k * KR + q].coef : 0.0;
         }
         ++io;
       }
@@ -564,9 +565,9 @@ struct Ctx {
         const size_t k = (size_t)s * nb + t;
         for (int q = 0; q < KRp; ++q) {
           const bool has = q < ecnt[k];
-          prow[ip * KRp + q] = has ? ent[k * 3 + q].row : -1;
-          pcoef[ip * KRp + q] = has ? ent[k * 3 + q].coef * ent[k * 3 + q].w : 0.0;
-          pjcoef[ip * KRp + q] = has ? ent[k * 3 + q].coef : 0.0;
+          prow[ip * KRp + q] = has ? ent[k * KR + q].row : -1;
+          pcoef[ip * KRp + q] = has ? ent[k * KR + q].coef * ent[k * KR + q].w : 0.0;
+          pjcoef[ip * KRp + q] = has ? ent[k * KR + q].coef : 0.0;
         }
         for (int q = 0; q < 3; ++q) RT[ip * 3 + q] = su.Rb[(size_t)q * nb + t];
         ++ip;

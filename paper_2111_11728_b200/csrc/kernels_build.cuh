@@ -41,16 +41,25 @@ __device__ void eliminate_smem(double* F, int nf, int ne, int ld, int* status, i
     for (int i = k + 1 + tid; i < nf; i += nt) ck[i] = ck[i] / l;
     __syncthreads();
     const int m = nf - k - 1;
-    // lower triangle of the trailing block, column-major triangular enumeration
-    const int tri = m * (m + 1) / 2;
-    for (int idx = tid; idx < tri; idx += nt) {
-      // column jj has m - jj entries (rows jj..m-1)
-      int jj = (int)((2.0 * m + 1.0 - sqrt((2.0 * m + 1.0) * (2.0 * m + 1.0) - 8.0 * idx)) * 0.5);
-      int start = jj * m - jj * (jj - 1) / 2;
-      if (start > idx) { --jj; start = jj * m - jj * (jj - 1) / 2; }
-      else if (start + (m - jj) <= idx) { ++jj; start = jj * m - jj * (jj - 1) / 2; }
-      const int ii = jj + (idx - start);
+    // lower triangle of the trailing block (column jj holds rows jj..m-1),
+    // folded into a rectangle: column p is paired with column m-1-p (m+1
+    // entries per pair), an odd m leaves the middle column alone.  Each thread
+    // walks its (p, q) positions incrementally: one division per pivot.
+    const int W = m + 1, P = m / 2;
+    const int tot = P * W + ((m & 1) ? P + 1 : 0);
+    int p = tid / W, q = tid - p * W;
+    const int sp = nt / W, sq = nt - sp * W;
+    for (int idx = tid; idx < tot; idx += nt) {
+      int jj, ii;
+      if (p < P) {
+        if (q < m - p) { jj = p; ii = p + q; }
+        else { jj = m - 1 - p; ii = jj + (q - (m - p)); }
+      } else {
+        jj = P; ii = P + q;
+      }
       F[(size_t)(k + 1 + jj) * ld + k + 1 + ii] -= ck[k + 1 + ii] * ck[k + 1 + jj];
+      p += sp; q += sq;
+      if (q >= W) { q -= W; ++p; }
     }
     __syncthreads();
   }

@@ -2,9 +2,13 @@
 #include "setup.hpp"
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <map>
 #include <numeric>
+#include <unordered_map>
 
 namespace fg {
 
@@ -205,7 +209,28 @@ int Setup::owners(int gx, int gy, int* sub, int* lnode) const {
   return cnt;
 }
 
+namespace {
+// FETIGPU_TIMING=1: host wall-clock of the setup phases on stderr
+struct HostMarks {
+  bool on;
+  std::chrono::steady_clock::time_point last;
+  HostMarks() {
+    const char* e = getenv("FETIGPU_TIMING");
+    on = e && e[0] == '1';
+    last = std::chrono::steady_clock::now();
+  }
+  void mark(const char* what) {
+    if (!on) return;
+    const auto t = std::chrono::steady_clock::now();
+    fprintf(stderr, "[fetigpu] setup %-28s %8.2f ms\n", what,
+            std::chrono::duration<double, std::milli>(t - last).count());
+    last = t;
+  }
+};
+}  // namespace
+
 void Setup::load(const fetigpu_problem& P) {
+  HostMarks hm;
   // ---- validation (Material::validate fem.cpp:9-17, DensityField fem.cpp:38-42)
   if (!(P.Emin > 0.0) || !(P.Emin < P.E0)) fail(FETIGPU_E_INVALID_ARGUMENT, "material: need 0 < Emin < E0");
   if (!(P.nu >= 0.0) || !(P.nu < 0.5)) fail(FETIGPU_E_INVALID_ARGUMENT, "material: need 0 <= nu < 0.5");
@@ -229,6 +254,7 @@ void Setup::load(const fetigpu_problem& P) {
     if (d < 0 || d >= n_designs) fail(FETIGPU_E_DIMENSION_MISMATCH, "module_type out of range");
   q4_unit(nu, thickness, hx, hy, kunit);
 
+  hm.mark("validation + copies");
   // ---- ND plan; its root perimeter defines the module boundary order
   nd = make_nd_plan(n, 4);
   const NdNode& root = nd.nodes[nd.root];
@@ -237,14 +263,15 @@ void Setup::load(const fetigpu_problem& P) {
   dpos.assign(nloc, -1);
   for (int i = 0; i < nb; ++i) dpos[perim_dof[i]] = i;
 
+  hm.mark("ND plan");
   // ---- boundary stiffness diagonals per design (sum in element order)
   bdiag.assign(n_designs, std::vector<double>(nb, 0.0));
+  std::vector<double> diag(nloc, 0.0);
   for (int d = 0; d < n_designs; ++d) {
     const double* rho = &densities[(size_t)d * n * n];
-    std::vector<double> diag(nloc, 0.0);
+    for (int i = 0; i < nb; ++i) diag[perim_dof[i]] = 0.0;  // only perimeter DOFs are accumulated
     for (int ey = 0; ey < n; ++ey)
-      for (int ex = 0; ex < n; ++ex) {
-        if (ey != 0 && ey != n - 1 && ex != 0 && ex != n - 1) continue;
+      for (int ex = 0; ex < n; ex += (ey == 0 || ey == n - 1 || ex == n - 1) ? 1 : n - 1) {
         const double e = Emin + std::pow(rho[ey * n + ex], p) * (E0 - Emin);
         const int n0 = ey * nn + ex;
         const int nodes[4] = {n0, n0 + 1, n0 + nn + 1, n0 + nn};
@@ -254,19 +281,28 @@ void Setup::load(const fetigpu_problem& P) {
     for (int i = 0; i < nb; ++i) bdiag[d][i] = diag[perim_dof[i]];
   }
 
+  hm.mark("boundary diagonals");
   // ---- supports
   std::vector<char> presc(2 * (size_t)GX * GY, 0);
-  std::vector<double> pval(2 * (size_t)GX * GY, 0.0);
+  std::unordered_map<long long, double> pvals;  // prescribed values, keyed by 2 g + dir
+  auto pval = [&](long long k) {
+    const auto it = pvals.find(k);
+    return it == pvals.end() ? 0.0 : it->second;
+  };
   for (int k = 0; k < P.n_dirichlet; ++k) {
     const int g = P.dir_gnode[k], dir = P.dir_dir[k];
     if (g < 0 || g >= GX * GY || dir < 0 || dir > 1) fail(FETIGPU_E_NODE_NOT_FOUND, "Dirichlet node not found");
     presc[2 * g + dir] = 1;
-    pval[2 * g + dir] = P.dir_value[k];
+    pvals[2 * (long long)g + dir] = P.dir_value[k];
   }
   auto corner = [&](int gx, int gy) { return gx % n == 0 && gy % n == 0; };
 
   // ---- loads (apply_traction, fem.cpp:121-167; point loads to the lowest owner)
-  std::vector<std::vector<double>> floc(Ns, std::vector<double>(nloc, 0.0));
+  std::vector<std::vector<double>> floc(Ns);  // allocated only for loaded subdomains
+  auto fl = [&](int s) -> std::vector<double>& {
+    if (floc[s].empty()) floc[s].assign(nloc, 0.0);
+    return floc[s];
+  };
   for (int t = 0; t < P.n_tractions; ++t) {
     const int s = P.tr_sub[t], side = P.tr_side[t], first = P.tr_first[t], count = P.tr_count[t];
     if (s < 0 || s >= Ns) fail(FETIGPU_E_DIMENSION_MISMATCH, "traction subdomain out of range");
@@ -282,12 +318,13 @@ void Setup::load(const fetigpu_problem& P) {
     if (first < 0 || count < 0 || first + count > n)
       fail(FETIGPU_E_EDGE_NOT_ON_BOUNDARY, "traction chain leaves the boundary");
     const double half = h / 2.0, tx = P.tr_txy[2 * t], ty = P.tr_txy[2 * t + 1];
+    std::vector<double>& f = fl(s);
     for (int e = first; e < first + count; ++e) {
       const int n0 = node0 + e * stride, n1 = n0 + stride;
-      floc[s][2 * n0] += half * tx;
-      floc[s][2 * n0 + 1] += half * ty;
-      floc[s][2 * n1] += half * tx;
-      floc[s][2 * n1 + 1] += half * ty;
+      f[2 * n0] += half * tx;
+      f[2 * n0 + 1] += half * ty;
+      f[2 * n1] += half * tx;
+      f[2 * n1 + 1] += half * ty;
     }
   }
   int osub[4], onode[4];
@@ -295,14 +332,17 @@ void Setup::load(const fetigpu_problem& P) {
     const int g = P.pl_gnode[k], dir = P.pl_dir[k];
     if (g < 0 || g >= GX * GY || dir < 0 || dir > 1) fail(FETIGPU_E_NODE_NOT_FOUND, "point load node not found");
     owners(g % GX, g / GX, osub, onode);
-    floc[osub[0]][2 * onode[0] + dir] += P.pl_value[k];
+    fl(osub[0])[2 * onode[0] + dir] += P.pl_value[k];
   }
 
+  hm.mark("supports + loads");
   // ---- constraint rows (decomposition.hpp:110-117; same rules as SPEC.md:198-206)
   rows.clear();
   const bool dp = method == FETIGPU_FETIDP;
   for (int gy = 0; gy < GY; ++gy)
-    for (int gx = 0; gx < GX; ++gx) {
+    for (int gx = 0; gx < GX; gx += (gy % n == 0 ? 1 : (gx % n == 0 ? n : n - gx % n))) {
+      // nodes off the module grid lines have one owner: visit grid-line nodes only
+      if (gy % n != 0 && gx % n != 0) continue;
       const int cnt = owners(gx, gy, osub, onode);
       if (cnt < 2 || (dp && corner(gx, gy))) continue;
       const int g = gy * GX + gx;
@@ -320,12 +360,13 @@ void Setup::load(const fetigpu_problem& P) {
         if (!presc[2 * g + dir]) continue;
         const int cnt = owners(g % GX, g / GX, osub, onode);
         for (int a = 0; a < cnt; ++a)
-          rows.push_back({1, osub[a], 2 * onode[a] + dir, -1, -1, pval[2 * g + dir], cnt, g, dir});
+          rows.push_back({1, osub[a], 2 * onode[a] + dir, -1, -1, pval(2 * (long long)g + dir), cnt, g, dir});
       }
   m = (int)rows.size();
   gap.resize(m);
   for (int i = 0; i < m; ++i) gap[i] = rows[i].gap;
 
+  hm.mark("constraint rows");
   // ---- scaling weights (decomposition.hpp:159-175)
   wplus.assign(m, 1.0);
   wminus.assign(m, 0.0);
@@ -350,15 +391,17 @@ void Setup::load(const fetigpu_problem& P) {
     }
   }
 
+  hm.mark("scaling weights");
   // ---- per-subdomain plans
   subs.assign(Ns, SubPlan());
   for (int s = 0; s < Ns; ++s) {
     SubPlan& S = subs[s];
     S.si = s % sx; S.sj = s / sx; S.design = module_type[s];
+    S.f.assign(nb, 0.0);
+    if (floc[s].empty()) continue;
     for (int i = 0; i < nloc; ++i)
       if (floc[s][i] != 0.0 && dpos[i] < 0)
         fail(FETIGPU_E_CONFIG, "loads on module-interior DOFs are not supported");
-    S.f.resize(nb);
     for (int i = 0; i < nb; ++i) S.f[i] = floc[s][perim_dof[i]];
   }
   std::vector<std::vector<char>> touched(Ns, std::vector<char>(nb, 0));
@@ -373,6 +416,7 @@ void Setup::load(const fetigpu_problem& P) {
     for (int i = 0; i < nb; ++i)
       if (touched[s][i]) subs[s].T.push_back(i);
 
+  hm.mark("per-subdomain plans");
   // rigid body modes (decomposition.hpp:119-121), about the module centroid
   Rfull.assign((size_t)nloc * 3, 0.0);
   {
@@ -511,13 +555,17 @@ void Setup::load(const fetigpu_problem& P) {
     }
   } else {
     // FETI-DP split: D (prescribed, eliminated), c (corners), r (rest)
-    std::vector<int> cidx(2 * (size_t)GX * GY, -1);
+    // primal numbering over the partition vertices only: (vertex row, col, dir)
+    std::vector<int> cidx(2 * (size_t)(sx + 1) * (sy + 1), -1);
+    auto cid = [&](int gx, int gy, int dir) -> int& {
+      return cidx[2 * ((size_t)(gy / n) * (sx + 1) + gx / n) + dir];
+    };
     Nc = 0;
     for (int gy = 0; gy < GY; gy += n)
       for (int gx = 0; gx < GX; gx += n) {
         const int g = gy * GX + gx;
         for (int dir = 0; dir < 2; ++dir)
-          if (!presc[2 * g + dir]) cidx[2 * g + dir] = Nc++;
+          if (!presc[2 * g + dir]) cid(gx, gy, dir) = Nc++;
       }
     c_owners.assign(Nc, {});
     for (int s = 0; s < Ns; ++s) {
@@ -526,8 +574,8 @@ void Setup::load(const fetigpu_problem& P) {
       for (int i = 0; i < nb; ++i) {
         const int d = perim_dof[i], v = d / 2, dir = d % 2;
         const int gx = S.si * n + v % nn, gy = S.sj * n + v / nn, g = gy * GX + gx;
-        if (presc[2 * g + dir]) { S.D.push_back(i); S.gD.push_back(pval[2 * g + dir]); }
-        else if (corner(gx, gy)) { S.c.push_back(i); S.cg.push_back(cidx[2 * g + dir]); }
+        if (presc[2 * g + dir]) { S.D.push_back(i); S.gD.push_back(pval(2 * (long long)g + dir)); }
+        else if (corner(gx, gy)) { S.c.push_back(i); S.cg.push_back(cid(gx, gy, dir)); }
         else S.r.push_back(i);
       }
       if (S.c.empty() && S.D.empty()) fail(FETIGPU_E_INSUFFICIENT_CORNERS, "subdomain has no primal DOF");
@@ -558,6 +606,7 @@ void Setup::load(const fetigpu_problem& P) {
     }
   }
 
+  hm.mark("op slots / coarse");
   // ---- preconditioner slots
   for (int s = 0; s < Ns; ++s) {
     SubPlan& S = subs[s];
@@ -594,6 +643,7 @@ void Setup::load(const fetigpu_problem& P) {
       S.pc_slot = it->second;
     }
   }
+  hm.mark("preconditioner slots");
 }
 
 }  // namespace fg
