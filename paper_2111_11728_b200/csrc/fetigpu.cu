@@ -36,9 +36,18 @@ namespace fg {
 #define CB(x)                                                                                  \
   do {                                                                                         \
     cublasStatus_t s_ = (x);                                                                   \
-    if (s_ != CUBLAS_STATUS_SUCCESS) fail(FETIGPU_E_CUDA, std::string(#x) + " failed");        \
+    if (s_ != CUBLAS_STATUS_SUCCESS)                                                           \
+      fail(FETIGPU_E_CUDA, std::string(#x) + " failed (cuBLAS status " + std::to_string((int)s_) + \
+                               ", line " + std::to_string(__LINE__) + ")");                    \
   } while (0)
-#define LAUNCH_CHECK() CK(cudaGetLastError())
+#define LAUNCH_CHECK()                                                                         \
+  do {                                                                                         \
+    cudaError_t e_ = cudaGetLastError();                                                       \
+    if (e_ != cudaSuccess)                                                                     \
+      fail(e_ == cudaErrorMemoryAllocation ? FETIGPU_E_OUT_OF_MEMORY : FETIGPU_E_CUDA,         \
+           std::string("kernel launch before fetigpu.cu:") + std::to_string(__LINE__) + ": " +  \
+               cudaGetErrorString(e_));                                                        \
+  } while (0)
 
 static size_t g_device_bytes = 0;
 
@@ -1517,6 +1526,22 @@ void Ctx::launch_add_rigid(double* u, const double* alpha) {
 // flagged on the device) and captured once into a CUDA graph; the host
 // replays it and reads back one 64-byte scalar record per iteration.
 int Ctx::solve(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_trace* tr) {
+  if (su.m == 0) {  // no dual unknowns (e.g. a single FETI-DP subdomain): converged at iteration 0
+    rhs();
+    if (tr) {
+      tr->status = FETIGPU_CONVERGED;
+      tr->iterations = 0;
+      tr->f_applies = 0;
+      tr->eps0 = tr->eps_final = 0.0;
+      tr->solve_ms = 0.0;
+      if (tr->cap > 0) {
+        if (tr->eps) tr->eps[0] = 0.0;
+        if (tr->kept) tr->kept[0] = o.directions == FETIGPU_RRS ? su.Ns : 1;
+        if (tr->f_app) tr->f_app[0] = 0;
+      }
+    }
+    return 0;
+  }
   if (o.directions == FETIGPU_RRS) return solve_rrs(o, lambda_host, tr);
   const int m = su.m;
   const bool fo = o.directions == FETIGPU_FO;
@@ -2027,6 +2052,7 @@ int fetigpu_rows(const fetigpu_ctx* ctx, int* kind, int* sp, int* dp, int* sm, i
 int fetigpu_apply_F_device(fetigpu_ctx* ctx, const double* x, double* y, int ncols, int ld) {
   return guarded([&] {
     NEED_BUILT(ctx);
+    if (ctx->c.su.m == 0) return;  // no dual unknowns
     ctx->c.apply_F(x, y, ncols, ld, ld);
   });
 }
@@ -2034,6 +2060,7 @@ int fetigpu_apply_F_device(fetigpu_ctx* ctx, const double* x, double* y, int nco
 int fetigpu_apply_F(fetigpu_ctx* ctx, const double* x, double* y, int ncols, int ld) {
   return guarded([&] {
     NEED_BUILT(ctx);
+    if (ctx->c.su.m == 0) return;  // no dual unknowns
     Ctx& c = ctx->c;
     if (ncols == 1) {
       c.apply_F_host(x, y);
@@ -2051,6 +2078,7 @@ int fetigpu_apply_F(fetigpu_ctx* ctx, const double* x, double* y, int ncols, int
 int fetigpu_apply_precond_device(fetigpu_ctx* ctx, const double* r, double* z, double* Z) {
   return guarded([&] {
     NEED_BUILT(ctx);
+    if (ctx->c.su.m == 0) return;  // no dual unknowns
     ctx->c.apply_precond(r, z, Z);
   });
 }
@@ -2058,6 +2086,7 @@ int fetigpu_apply_precond_device(fetigpu_ctx* ctx, const double* r, double* z, d
 int fetigpu_apply_precond(fetigpu_ctx* ctx, const double* r, double* z, double* Zcols) {
   return guarded([&] {
     NEED_BUILT(ctx);
+    if (ctx->c.su.m == 0) return;  // no dual unknowns
     Ctx& c = ctx->c;
     const int m = c.su.m;
     DBuf<double> dr, dz, dZ;
@@ -2075,6 +2104,7 @@ int fetigpu_apply_precond(fetigpu_ctx* ctx, const double* r, double* z, double* 
 int fetigpu_project_device(fetigpu_ctx* ctx, double* v, int ncols, int ld) {
   return guarded([&] {
     NEED_BUILT(ctx);
+    if (ctx->c.su.m == 0) return;  // no dual unknowns
     ctx->c.project(v, ncols, ld);
   });
 }
@@ -2082,6 +2112,7 @@ int fetigpu_project_device(fetigpu_ctx* ctx, double* v, int ncols, int ld) {
 int fetigpu_project(fetigpu_ctx* ctx, double* v, int ncols, int ld) {
   return guarded([&] {
     NEED_BUILT(ctx);
+    if (ctx->c.su.m == 0) return;  // no dual unknowns
     Ctx& c = ctx->c;
     DBuf<double> dv;
     dv.alloc((size_t)ld * ncols);
