@@ -1962,19 +1962,24 @@ static thread_local std::string g_err;
 
 template <class F>
 static int guarded(F&& f) {
+  int rc = 0;
   try {
     f();
     return 0;
   } catch (const Error& e) {
     g_err = e.what();
-    return e.code;
+    rc = e.code;
   } catch (const std::bad_alloc& e) {
     g_err = e.what();
-    return FETIGPU_E_OUT_OF_MEMORY;
+    rc = FETIGPU_E_OUT_OF_MEMORY;
   } catch (const std::exception& e) {
     g_err = e.what();
-    return FETIGPU_E_INVALID_ARGUMENT;
+    rc = FETIGPU_E_INVALID_ARGUMENT;
   }
+  // a failed call must not leave a pending (non-sticky) launch error behind
+  // for the next, unrelated call (e.g. another context's cuBLAS launch)
+  if (rc >= FETIGPU_E_CUDA) cudaGetLastError();
+  return rc;
 }
 #define NEED_BUILT(ctx) \
   if (!(ctx) || !(ctx)->c.built) fail(FETIGPU_E_STATE, "context not built")
