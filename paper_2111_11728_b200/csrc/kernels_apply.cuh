@@ -24,8 +24,22 @@ namespace fg {
 // KR = max dual rows touching one local DOF (1 FETI-DP, <= 3 T-FETI cross points)
 // FETI-DP coarse pre-pass fused into the GEMV CTA (x_s already in smem):
 // t_s = A''^T x_s for the subdomain's <= 8 primal DOFs (rsplit slice 0 only).
+// Deterministic coarse gather fused into phase 1: every owner subdomain of a
+// primal DOF publishes its t entry and counts its arrival; the last owner to
+// arrive sums the owners' entries in fixed (ascending subdomain) order -- the
+// order of k_coarse_gather -- writes g and resets the counter for the next
+// apply.  (Threadfence-reduction pattern: nobody waits.)
+struct CoarseGather {
+  double* g;            // N_c
+  unsigned int* cnt;    // N_c arrival counters, zero between applies
+  const int* optr;      // owners of primal DOF i: oidx[optr[i] .. optr[i+1])
+  const int* oidx;      // -> tbuf index
+  const int* cmap;      // per subdomain: global primal ids
+};
+
 __device__ __forceinline__ void fused_dp_t(const DpSub& p, const double* __restrict__ abc,
-                                           const double* xs, int ns, double* __restrict__ tbuf) {
+                                           const double* xs, int ns, double* __restrict__ tbuf,
+                                           const CoarseGather* cgp = nullptr) {
   __shared__ double red[8][kThreads / 32];
   double acc[8] = {};
   const double* Ab = abc + p.abc_off;
@@ -46,6 +60,19 @@ __device__ __forceinline__ void fused_dp_t(const DpSub& p, const double* __restr
     double v = 0.0;
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) v += red[threadIdx.x][w];
     tbuf[p.t_off + threadIdx.x] = v;
+    if (cgp) {
+      const CoarseGather cg = *cgp;
+      const int gid = cg.cmap[p.cmap_off + threadIdx.x];
+      const int k0 = cg.optr[gid], k1 = cg.optr[gid + 1];
+      __threadfence();  // this t entry is visible device-wide before the arrival is counted
+      if (atomicAdd(cg.cnt + gid, 1u) + 1u == (unsigned)(k1 - k0)) {
+        __threadfence();
+        double g = 0.0;
+        for (int k = k0; k < k1; ++k) g += __ldcg(tbuf + cg.oidx[k]);
+        cg.g[gid] = g;
+        cg.cnt[gid] = 0u;
+      }
+    }
   }
 }
 
@@ -140,10 +167,15 @@ __global__ void __launch_bounds__(256) k_sym_gemv_scatter(
     const SymSub* __restrict__ subs, const double* __restrict__ tiles, const int* __restrict__ rows,
     const double* __restrict__ coefs, const double* __restrict__ x, double* __restrict__ y,
     double* __restrict__ vbuf, const int* __restrict__ voff, const DpSub* __restrict__ dps = nullptr,
-    const double* __restrict__ abc = nullptr, double* __restrict__ tbuf = nullptr, int s0 = 0) {
+    const double* __restrict__ abc = nullptr, double* __restrict__ tbuf = nullptr, int s0 = 0,
+    double* __restrict__ zero_y = nullptr, int ny = 0, int nsub = 1, const CoarseGather* cgp = nullptr) {
   extern __shared__ double shm[];
   const int s = s0 + blockIdx.x;   // subdomain (s0: first subdomain of a pipelined chunk)
   const SymSub d = subs[s];
+  if (STORE_V && zero_y) {  // FETI-DP: phase 1 never writes y, so its slice is zeroed here for phase 2
+    const long long a = (long long)ny * s / nsub, e = (long long)ny * (s + 1) / nsub;
+    for (long long i = a + threadIdx.x; i < e; i += blockDim.x) zero_y[i] = 0.0;
+  }
   const int npad = d.nb * 32;
   double* xs = shm;                   // npad
   double* part = shm + npad;          // kSymWarps x npad
@@ -162,7 +194,7 @@ __global__ void __launch_bounds__(256) k_sym_gemv_scatter(
   }
   for (int j = threadIdx.x; j < kSymWarps * npad; j += blockDim.x) part[j] = 0.0;
   __syncthreads();
-  if (STORE_V && dps) fused_dp_t(dps[s], abc, xs, d.ns, tbuf);
+  if (STORE_V && dps) fused_dp_t(dps[s], abc, xs, d.ns, tbuf, cgp);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double* pw = part + warp * npad;
   const int ntiles = d.nb * (d.nb + 1) / 2;
@@ -281,6 +313,88 @@ __global__ void k_coarse_gather(const int* __restrict__ optr, const int* __restr
     double v = add ? add[i] : 0.0;
     for (int k = optr[i]; k < optr[i + 1]; ++k) v += sign * tbuf[oidx[k]];
     out[i] = v;
+  }
+}
+
+// ------------------------------ FETI-DP coarse solve on the packed inverse --
+// u = Kbar^{-1} g with Kbar^{-1} stored like F_s: lower block-triangle of
+// 32x32 row-major tiles (about half the bytes of the dense inverse).
+// Stage A (k_csym_tiles): warps stream the tiles, reading the matching slices of
+// g = sum_s B_c^T t_s (formed by phase 1's fused last-arriver gather) from L2
+// alongside, and write per tile the row part (for block row bi) and the
+// transposed part (for block row bj).  Stage B (k_csym_reduce) sums those
+// partials per block row in a fixed tile order, so the result is
+// deterministic; no separate gather launch, no atomics.
+__global__ void __launch_bounds__(128) k_csym_tiles(const double* __restrict__ tiles, int nb, int nc,
+                                                    const double* __restrict__ g, double* __restrict__ rowp,
+                                                    double* __restrict__ colp) {
+  const int lane = threadIdx.x & 31;
+  const int ntiles = nb * (nb + 1) / 2;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < ntiles; t += nw) {
+    int bi = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+    while (bi * (bi + 1) / 2 > t) --bi;
+    while ((bi + 1) * (bi + 2) / 2 <= t) ++bi;
+    const int bj = t - bi * (bi + 1) / 2;
+    const double* T = tiles + (size_t)t * 1024;
+    double f[32];
+#pragma unroll
+    for (int r = 0; r < 32; ++r) f[r] = __ldcs(T + r * 32 + lane);
+    // g slices straight from L2, issued with the tile loads (zero beyond nc)
+    const double xj = bj * 32 + lane < nc ? __ldcg(g + bj * 32 + lane) : 0.0;
+    const double xi = bi * 32 + lane < nc ? __ldcg(g + bi * 32 + lane) : 0.0;
+    double c = 0.0;
+#pragma unroll
+    for (int r = 0; r < 32; ++r) {
+      c = fma(f[r], __shfl_sync(0xffffffffu, xi, r), c);   // transposed part: sum_r T[r][lane] g_i[r]
+      f[r] *= xj;
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {      // transpose-reduce: lane l <- sum_c T[l][c] g_j[c]
+      const bool hi = (lane & o) != 0;
+#pragma unroll
+      for (int q = 0; q < o; ++q) {
+        const double keep = hi ? f[q + o] : f[q];
+        const double send = hi ? f[q] : f[q + o];
+        f[q] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+      }
+    }
+    rowp[(size_t)t * 32 + lane] = f[0];
+    colp[(size_t)t * 32 + lane] = bi != bj ? c : 0.0;
+  }
+}
+
+// Stage B: u[b*32 + l] = sum_{j <= b} rowp[tile(b, j)][l] + sum_{j > b} colp[tile(j, b)][l];
+// one CTA of 16 warps per block row b; warp w sums tiles j = w, w + 16, ... in
+// batches of 4 independent loads, warps are combined in fixed order
+__global__ void __launch_bounds__(512) k_csym_reduce(const double* __restrict__ rowp,
+                                                     const double* __restrict__ colp, int nb, int nc,
+                                                     double* __restrict__ u) {
+  __shared__ double red[16][32];
+  const int b = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const size_t rb = (size_t)b * (b + 1) / 2;
+  auto part = [&](int j) -> const double* {
+    return j <= b ? rowp + (rb + j) * 32 + lane : colp + ((size_t)j * (j + 1) / 2 + b) * 32 + lane;
+  };
+  double acc = 0.0;
+  int j = warp;
+  for (; j + 48 < nb; j += 64) {
+    const double v0 = __ldcg(part(j)), v1 = __ldcg(part(j + 16)), v2 = __ldcg(part(j + 32)),
+                 v3 = __ldcg(part(j + 48));
+    acc += v0;
+    acc += v1;
+    acc += v2;
+    acc += v3;
+  }
+  for (; j < nb; j += 16) acc += __ldcg(part(j));
+  red[warp][lane] = acc;
+  __syncthreads();
+  if (warp == 0) {
+    double v = 0.0;
+#pragma unroll
+    for (int w = 0; w < 16; ++w) v += red[w][lane];
+    const int r = b * 32 + lane;
+    if (r < nc) u[r] = v;
   }
 }
 
