@@ -186,6 +186,20 @@ struct DBuf {
 
 static inline int round_up(int v, int a) { return (v + a - 1) / a * a; }
 
+// cudaFuncAttributeMaxDynamicSharedMemorySize is per function and process-wide:
+// contexts of different sizes may be alive at once, so it is only ever raised.
+template <class K>
+static void raise_smem_limit(K* func, size_t bytes) {
+  static std::mutex mu;
+  static std::unordered_map<const void*, size_t> cur;
+  std::lock_guard<std::mutex> lk(mu);
+  size_t& c = cur[(const void*)func];
+  if (bytes > c) {
+    CK(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    c = bytes;
+  }
+}
+
 // FETIGPU_TIMING=1: host wall-clock marks of the build phases on stderr
 struct PhaseTimer {
   bool on;
@@ -942,10 +956,8 @@ struct Ctx {
       }
       d_sym.upload(ss, st);
       sym_smem = nbmax * 32 * (1 + kSymWarps) * 8;
-      if (sym_smem > 48 * 1024) {
-        CK(cudaFuncSetAttribute(k_sym_gemv_scatter<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sym_smem));
-        CK(cudaFuncSetAttribute(k_sym_gemv_scatter<3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sym_smem));
-      }
+      raise_smem_limit(k_sym_gemv_scatter<1, true>, sym_smem);
+      raise_smem_limit(k_sym_gemv_scatter<3, false>, sym_smem);
       CK(cudaStreamSynchronize(st));
       use_sym = true;
       // same packing for the (symmetric) preconditioner blocks S~_s / K_TT
@@ -975,12 +987,8 @@ struct Ctx {
       }
       d_pcsym.upload(pss, st);
       pc_sym_smem = pnbmax * 32 * (1 + kSymWarps) * 8;
-      if (pc_sym_smem > 48 * 1024) {
-        CK(cudaFuncSetAttribute(k_sym_gemv_scatter<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                pc_sym_smem));
-        CK(cudaFuncSetAttribute(k_sym_gemv_scatter<3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                std::max(pc_sym_smem, sym_smem)));
-      }
+      raise_smem_limit(k_sym_gemv_scatter<1, false>, pc_sym_smem);
+      raise_smem_limit(k_sym_gemv_scatter<3, false>, pc_sym_smem);
       CK(cudaStreamSynchronize(st));
       pc_sym = true;
     }
@@ -1279,8 +1287,12 @@ struct Ctx {
       for (auto& S : su.subs) tot_c += (int)S.c.size();
       if (blk_t.n < (size_t)tot_c * k) blk_t.alloc((size_t)tot_c * k);
       if (blk_T.n < (size_t)Nc * k) { blk_T.alloc((size_t)Nc * k); blk_U.alloc((size_t)Nc * k); }
-      k_block_dp_t<<<dim3((k + 63) / 64, Ns), 256, 0, st>>>(d_op.p, d_dp.p, d_oprows.p, d_opcoef_apply.p, d_abc.p, W,
-                                                             ldw, k, blk_t.p, k);
+      {
+        const size_t smem = ((size_t)std::max(max_ns * 8, 4 * 8 * kDpTCols) + max_ns) * 8 + (size_t)max_ns * 4;
+        raise_smem_limit(k_block_dp_t, smem);
+        k_block_dp_t<<<dim3((k + kDpTCols - 1) / kDpTCols, Ns), 256, smem, st>>>(
+            d_op.p, d_dp.p, d_oprows.p, d_opcoef_apply.p, d_abc.p, W, ldw, k, blk_t.p, k);
+      }
       k_coarse_gather_block<<<dim3((k + 255) / 256, Nc), 256, 0, st>>>(d_optr.p, d_oidx.p, blk_t.p, k, Nc, k,
                                                                        blk_T.p, k);
       const double one = 1.0, zero = 0.0;

@@ -321,7 +321,14 @@ __global__ void __launch_bounds__(256, 2) k_block_apply_dp(BlockApplyArgs a) {
   }
 }
 
-// FETI-DP coarse pre-pass for a block: T_s = A_bc^T (B_s^T W)   (n_c x k)
+// FETI-DP coarse pre-pass for a block: T_s = A_bc^T (B_s^T W)   (n_c x k).
+// One CTA per (128-column slab, subdomain): the subdomain's A_bc rows (padded
+// to 8), row ids and coefficients are staged in shared memory once, so the
+// only global stream is W (two adjacent columns per thread, 16-byte loads).
+// 4 thread groups split the rows; per column the partial sums are combined
+// in group order -- the accumulation order of the 64-column version, so
+// results are unchanged.
+constexpr int kDpTCols = 128;
 __global__ void __launch_bounds__(256) k_block_dp_t(const OpSub* __restrict__ subs,
                                                     const DpSub* __restrict__ dps,
                                                     const int* __restrict__ rows,
@@ -330,30 +337,67 @@ __global__ void __launch_bounds__(256) k_block_dp_t(const OpSub* __restrict__ su
                                                     const double* __restrict__ W, int ldw, int k,
                                                     double* __restrict__ tbuf, int ldt) {
   // (coefs are the apply coefficients: unit when the operators are sign-folded)
+  extern __shared__ double dsm[];
   const int s = blockIdx.y;
   const OpSub d = subs[s];
   const DpSub p = dps[s];
-  const int col = blockIdx.x * 64 + (threadIdx.x & 63);
-  const int grp = threadIdx.x >> 6;  // 4 groups split the inner range
-  __shared__ double red[4][8][64];
-  double acc[8] = {};
+  const int ns = d.ns;
+  double* As = dsm;                                   // max(ns * 8, 4 * 8 * kDpTCols): A, then partials
+  double* cs = As + max(ns * 8, 4 * 8 * kDpTCols);    // ns coefficients
+  int* rs = reinterpret_cast<int*>(cs + ns);          // ns row ids
   const double* Ab = abc + p.abc_off;
+  for (int idx = threadIdx.x; idx < ns * 8; idx += blockDim.x) {
+    const int j = idx >> 3, c = idx & 7;
+    As[idx] = c < p.nc ? Ab[(size_t)j * p.nc + c] : 0.0;
+  }
+  for (int j = threadIdx.x; j < ns; j += blockDim.x) {
+    rs[j] = rows[d.map_off + j];
+    cs[j] = coefs[d.map_off + j];
+  }
+  __syncthreads();
+  const int lc = 2 * (threadIdx.x & 63);             // local column pair
+  const int col = blockIdx.x * kDpTCols + lc;
+  const int grp = threadIdx.x >> 6;                  // 4 groups split the rows
+  const bool vec = (ldw & 1) == 0 && col + 1 < k;
+  double a0[8] = {}, a1[8] = {};
   if (col < k) {
-    for (int j = grp; j < d.ns; j += 4) {
-      const int r = rows[d.map_off + j];
-      const double x = r >= 0 ? coefs[d.map_off + j] * W[(size_t)r * ldw + col] : 0.0;
+    for (int j = grp; j < ns; j += 4) {
+      const int r = rs[j];
+      double w0 = 0.0, w1 = 0.0;
+      if (r >= 0) {
+        const double* wr = W + (size_t)r * ldw + col;
+        if (vec) {
+          const double2 w = __ldg(reinterpret_cast<const double2*>(wr));
+          w0 = w.x;
+          w1 = w.y;
+        } else {
+          w0 = wr[0];
+          w1 = col + 1 < k ? wr[1] : 0.0;
+        }
+      }
+      const double x0 = cs[j] * w0, x1 = cs[j] * w1;
 #pragma unroll
-      for (int c = 0; c < 8; ++c)
-        if (c < p.nc) acc[c] = fma(Ab[(size_t)j * p.nc + c], x, acc[c]);
+      for (int c = 0; c < 8; ++c) {
+        const double av = As[j * 8 + c];
+        a0[c] = fma(av, x0, a0[c]);
+        a1[c] = fma(av, x1, a1[c]);
+      }
     }
   }
+  __syncthreads();  // A no longer needed: its space holds the group partials
+  double* red = As;  // [4][8][kDpTCols]
 #pragma unroll
-  for (int c = 0; c < 8; ++c) red[grp][c][threadIdx.x & 63] = acc[c];
+  for (int c = 0; c < 8; ++c) {
+    red[(grp * 8 + c) * kDpTCols + lc] = a0[c];
+    red[(grp * 8 + c) * kDpTCols + lc + 1] = a1[c];
+  }
   __syncthreads();
-  if (grp == 0 && col < k) {
-    for (int c = 0; c < p.nc; ++c)
-      tbuf[(size_t)(p.t_off + c) * ldt + col] =
-          red[0][c][threadIdx.x] + red[1][c][threadIdx.x] + red[2][c][threadIdx.x] + red[3][c][threadIdx.x];
+  for (int idx = threadIdx.x; idx < p.nc * kDpTCols; idx += blockDim.x) {
+    const int c = idx / kDpTCols, l = idx - c * kDpTCols;
+    const int gc = blockIdx.x * kDpTCols + l;
+    if (gc < k)
+      tbuf[(size_t)(p.t_off + c) * ldt + gc] = red[(0 * 8 + c) * kDpTCols + l] + red[(1 * 8 + c) * kDpTCols + l] +
+                                                red[(2 * 8 + c) * kDpTCols + l] + red[(3 * 8 + c) * kDpTCols + l];
   }
 }
 
