@@ -1773,7 +1773,7 @@ int Ctx::solve(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_trace* 
   CK(cudaMemcpyAsync(w.p, z.p, m * 8, cudaMemcpyDeviceToDevice, st));
   const double target = o.rel ? o.tol * eps0 : o.tol;
   // one PCG / FO iteration (everything on the stream, no host work)
-  auto body = [&]() {
+  auto body = [&](bool readback) {
     apply_F(w.p, q.p, 1, m, m);
     dots({{w.p, q.p}, {w.p, r.p}}, &sc.p->delta);
     if (tf) proj_corr(q.p, m, corr.p, m, 1);
@@ -1794,32 +1794,98 @@ int Ctx::solve(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_trace* 
       k_cg_dir2<<<grid_for(m), kThreads, 0, st>>>(m, sc.p, z.p, w.p);
       k_shift_rz<<<1, 1, 0, st>>>(sc.p);
     }
-    CK(cudaMemcpyAsync(hs, sc.p, sizeof(Scal), cudaMemcpyDeviceToHost, st));
+    if (readback) CK(cudaMemcpyAsync(hs, sc.p, sizeof(Scal), cudaMemcpyDeviceToHost, st));
     LAUNCH_CHECK();
   };
-  cudaGraph_t graph = nullptr;
-  cudaGraphExec_t exec = nullptr;
-  bool use_graph = true;
-  if (use_graph) {
+  struct GraphGuard {
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    ~GraphGuard() {
+      if (exec) cudaGraphExecDestroy(exec);
+      if (graph) cudaGraphDestroy(graph);
+    }
+  } gg;
+  cudaGraph_t& graph = gg.graph;
+  cudaGraphExec_t& exec = gg.exec;
+  // Preferred: the whole loop on the device -- the iteration body plus
+  // k_iter_control under a `while` conditional node, one graph launch per
+  // solve, no host round trip per iteration.  Fallback (no conditional nodes,
+  // or FETIGPU_HOST_LOOP=1): one graph launch + a 64-byte readback per iteration.
+  const char* hl = getenv("FETIGPU_HOST_LOOP");
+  bool device_loop = !(hl && hl[0] == '1') && eps > target && o.max_it > 0;
+  if (device_loop) {
+    DBuf<IterCtl> dctl;
+    DBuf<double> dtrace;
+    const int tcap = tr && tr->eps ? std::min(tr->cap, o.max_it + 1) : 1;
+    dctl.alloc(1);
+    dtrace.alloc(std::max(1, tcap));
+    IterCtl h0{0, FETIGPU_MAX_ITER, 0, tcap, o.max_it, 0, eps0, target};
+    CK(cudaMemcpyAsync(dctl.p, &h0, sizeof(IterCtl), cudaMemcpyHostToDevice, st));
+    CK(cudaStreamSynchronize(st));
+    bool built_ok = false;
+    if (cudaGraphCreate(&graph, 0) == cudaSuccess) {
+      cudaGraphConditionalHandle hcond;
+      cudaGraphNodeParams cp = {};
+      cudaGraphNode_t cnode;
+      if (cudaGraphConditionalHandleCreate(&hcond, graph, 1, cudaGraphCondAssignDefault) == cudaSuccess) {
+        cp.type = cudaGraphNodeTypeConditional;
+        cp.conditional.handle = hcond;
+        cp.conditional.type = cudaGraphCondTypeWhile;
+        cp.conditional.size = 1;
+        if (cudaGraphAddNode(&cnode, graph, nullptr, 0, &cp) == cudaSuccess) {
+          cudaGraph_t bodyg = cp.conditional.phGraph_out[0];
+          if (cudaStreamBeginCaptureToGraph(st, bodyg, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal) ==
+              cudaSuccess) {
+            body(false);
+            k_iter_control<<<1, 1, 0, st>>>(sc.p, dctl.p, dtrace.p, hcond);
+            cudaGraph_t captured = nullptr;
+            built_ok = cudaStreamEndCapture(st, &captured) == cudaSuccess &&
+                       cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess;
+          }
+        }
+      }
+    }
+    if (!built_ok) {  // fall back to the host-driven loop
+      cudaGetLastError();
+      if (exec) { cudaGraphExecDestroy(exec); exec = nullptr; }
+      if (graph) { cudaGraphDestroy(graph); graph = nullptr; }
+      device_loop = false;
+    } else {
+      CK(cudaGraphLaunch(exec, st));
+      IterCtl hc;
+      CK(cudaMemcpyAsync(&hc, dctl.p, sizeof(IterCtl), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      std::vector<double> ht(std::max(1, tcap));
+      if (tcap > 1) CK(cudaMemcpy(ht.data(), dtrace.p, (size_t)tcap * 8, cudaMemcpyDeviceToHost));
+      if (hc.err) fail(FETIGPU_E_NEGATIVE_INNER_PRODUCT, "r^T z < 0: preconditioner is not symmetric positive");
+      for (int i = 1; i <= hc.it; ++i) {
+        it = i;
+        fapp = 1 + i;
+        push(i < tcap ? ht[i] : hc.eps, 1);
+      }
+      it = hc.it;
+      fapp = 1 + hc.it;
+      eps = hc.it > 0 ? hc.eps : eps0;
+      status = hc.status;
+    }
+  }
+  if (!device_loop) {
     CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-    body();
+    body(true);
     CK(cudaStreamEndCapture(st, &graph));
     CK(cudaGraphInstantiate(&exec, graph, 0));
+    while (true) {
+      if (eps <= target) { status = FETIGPU_CONVERGED; break; }
+      if (it >= o.max_it) { status = FETIGPU_MAX_ITER; break; }
+      CK(cudaGraphLaunch(exec, st));
+      CK(cudaStreamSynchronize(st));
+      if (hs->breakdown != 0.0) { status = FETIGPU_BREAKDOWN; break; }
+      ++fapp;
+      eps = metric(*hs);
+      ++it;
+      push(eps, 1);
+    }
   }
-  while (true) {
-    if (eps <= target) { status = FETIGPU_CONVERGED; break; }
-    if (it >= o.max_it) { status = FETIGPU_MAX_ITER; break; }
-    if (use_graph) CK(cudaGraphLaunch(exec, st));
-    else body();
-    CK(cudaStreamSynchronize(st));
-    if (hs->breakdown != 0.0) { status = FETIGPU_BREAKDOWN; break; }
-    ++fapp;
-    eps = metric(*hs);
-    ++it;
-    push(eps, 1);
-  }
-  if (exec) cudaGraphExecDestroy(exec);
-  if (graph) cudaGraphDestroy(graph);
   CK(cudaEventRecord(ev1, st));
   const double ms = elapsed(ev0, ev1);
   CK(cudaMemcpyAsync(lambda_host, lam.p, m * 8, cudaMemcpyDeviceToHost, st));

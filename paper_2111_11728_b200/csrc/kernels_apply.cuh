@@ -724,6 +724,36 @@ __global__ void k_cg_dir2(int n, Scal* sc, const double* __restrict__ z, double*
 }
 __global__ void k_shift_rz(Scal* sc) { sc->rz_old = sc->rz; }
 
+// Device-side loop control of PCG / FO (runs as the last node of the
+// iteration body under a CUDA-graph `while` conditional): the host loop's
+// tests in the same order -- breakdown, NegativeInnerProduct (residual_metric,
+// SPEC.md:420-423), eps = sqrt(max(r^T z, 0)), convergence, iteration cap --
+// with the trace written to device memory.
+struct IterCtl {
+  int it, status, err, trace_cap;
+  int max_it, pad;
+  double eps, target;
+};
+__global__ void k_iter_control(const Scal* __restrict__ sc, IterCtl* __restrict__ c, double* __restrict__ trace,
+                               cudaGraphConditionalHandle h) {
+  unsigned int go = 0;
+  if (sc->breakdown != 0.0) {
+    c->status = 2;  // FETIGPU_BREAKDOWN
+  } else if (sc->rz < -1e-14 * sqrt(sc->rr) * sqrt(sc->zz)) {
+    c->err = 14;    // FETIGPU_E_NEGATIVE_INNER_PRODUCT
+  } else {
+    const double eps = sqrt(fmax(sc->rz, 0.0));
+    const int it = c->it + 1;
+    c->it = it;
+    c->eps = eps;
+    if (it < c->trace_cap) trace[it] = eps;
+    if (eps <= c->target) c->status = 0;      // FETIGPU_CONVERGED
+    else if (it >= c->max_it) c->status = 1;  // FETIGPU_MAX_ITER
+    else go = 1;
+  }
+  cudaGraphSetConditional(h, go);
+}
+
 // ------------------------------------------------------- vector updates --
 
 __global__ void k_axpy(int n, double a, const double* __restrict__ x, double* __restrict__ y) {
