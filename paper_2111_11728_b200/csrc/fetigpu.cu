@@ -423,12 +423,13 @@ struct Ctx {
     int ne_max = 0, nf_max = 0;
     for (auto& f : fs) { ne_max = std::max(ne_max, f.ne); nf_max = std::max(nf_max, f.nf); }
     const int B = (int)fs.size();
-    for (int k0 = 0; k0 < ne_max; k0 += kNB) {
+    raise_smem_limit(k_bpc_update, kBpcUpdateSmem);
+    for (int k0 = 0; k0 < ne_max; k0 += kBpcNB) {
       k_bpc_diag<<<B, kThreads, 0, st>>>(d, base, k0, d_status.p);
       const int rows = std::max(1, nf_max - k0 - 1);
       k_bpc_trsm<<<dim3((rows + kThreads - 1) / kThreads, B), kThreads, 0, st>>>(d, base, k0);
       const int nt = (rows + kTile - 1) / kTile;
-      k_bpc_update<<<dim3(nt * (nt + 1) / 2, B), kThreads, 0, st>>>(d, base, k0);
+      k_bpc_update<<<dim3(nt * (nt + 1) / 2, B), kThreads, kBpcUpdateSmem, st>>>(d, base, k0);
       LAUNCH_CHECK();
     }
   }

@@ -279,52 +279,77 @@ __device__ __forceinline__ void dmma_884b(double& d0, double& d1, double a, doub
                : "d"(a), "d"(b));
 }
 constexpr int kBpcPad = kTile + 4;
+// panel width of the batched elimination: 64 columns halve the number of
+// read-modify-write passes over the trailing matrices (the update is memory
+// bound: 64 x 64 tile, 2 * 64 * 64 * kBpcNB flop per 3 * 32 KB moved)
+constexpr int kBpcNB = 64;
+constexpr size_t kBpcUpdateSmem = (size_t)2 * kBpcNB * kBpcPad * sizeof(double);
 
 __global__ void __launch_bounds__(kThreads) k_bpc_diag(const FrontDesc* fds, double* base, int k0,
                                                        int* status) {
   const FrontDesc f = fds[blockIdx.x];
   if (k0 >= f.ne) return;
-  __shared__ double D[kNB * (kNB + 1)];
+  __shared__ double D[kBpcNB * (kBpcNB + 1)];
   double* A = base + f.off;
-  const int kb = min(kNB, f.ne - k0), ld = f.ld;
+  const int kb = min(kBpcNB, f.ne - k0), ld = f.ld;
   for (int idx = threadIdx.x; idx < kb * kb; idx += kThreads) {
     const int j = idx / kb, i = idx - j * kb;
-    if (i >= j) D[j * (kNB + 1) + i] = A[(size_t)(k0 + j) * ld + k0 + i];
+    if (i >= j) D[j * (kBpcNB + 1) + i] = A[(size_t)(k0 + j) * ld + k0 + i];
   }
   __syncthreads();
-  eliminate_smem(D, kb, kb, kNB + 1, status, f.code);
+  eliminate_smem(D, kb, kb, kBpcNB + 1, status, f.code);
   for (int idx = threadIdx.x; idx < kb * kb; idx += kThreads) {
     const int j = idx / kb, i = idx - j * kb;
-    if (i >= j) A[(size_t)(k0 + j) * ld + k0 + i] = D[j * (kNB + 1) + i];
+    if (i >= j) A[(size_t)(k0 + j) * ld + k0 + i] = D[j * (kBpcNB + 1) + i];
   }
 }
 
 __global__ void __launch_bounds__(kThreads) k_bpc_trsm(const FrontDesc* fds, double* base, int k0) {
   const FrontDesc f = fds[blockIdx.y];
   if (k0 >= f.ne) return;
-  const int kb = min(kNB, f.ne - k0), k1 = k0 + kb, ld = f.ld;
+  const int kb = min(kBpcNB, f.ne - k0), k1 = k0 + kb, ld = f.ld;
   const int r = k1 + blockIdx.x * kThreads + threadIdx.x;
   if (k1 + blockIdx.x * kThreads >= f.nf) return;
-  __shared__ double D[kNB * (kNB + 1)];
+  __shared__ double D[kBpcNB * (kBpcNB + 1)];
   double* A = base + f.off;
   for (int idx = threadIdx.x; idx < kb * kb; idx += kThreads) {
     const int j = idx / kb, i = idx - j * kb;
-    if (i >= j) D[j * (kNB + 1) + i] = A[(size_t)(k0 + j) * ld + k0 + i];
+    if (i >= j) D[j * (kBpcNB + 1) + i] = A[(size_t)(k0 + j) * ld + k0 + i];
   }
   __syncthreads();
   if (r >= f.nf) return;
-  double x[kNB];
+  // row r of the panel: x L^T = a, in two 32-column halves so at most 64
+  // values are live (first half solved, second half updated from it, solved)
+  constexpr int H = kBpcNB / 2;
+  double lo[H], hi[H];
 #pragma unroll
-  for (int c = 0; c < kNB; ++c)
-    if (c < kb) x[c] = A[(size_t)(k0 + c) * ld + r];
+  for (int c = 0; c < H; ++c) lo[c] = c < kb ? A[(size_t)(k0 + c) * ld + r] : 0.0;
 #pragma unroll
-  for (int c = 0; c < kNB; ++c) {
+  for (int c = 0; c < H; ++c) {
     if (c < kb) {
-      double v = x[c];
+      double v = lo[c];
 #pragma unroll
-      for (int c2 = 0; c2 < c; ++c2) v -= x[c2] * D[c2 * (kNB + 1) + c];
-      x[c] = v / D[c * (kNB + 1) + c];
-      A[(size_t)(k0 + c) * ld + r] = x[c];
+      for (int c2 = 0; c2 < c; ++c2) v -= lo[c2] * D[c2 * (kBpcNB + 1) + c];
+      lo[c] = v / D[c * (kBpcNB + 1) + c];
+      A[(size_t)(k0 + c) * ld + r] = lo[c];
+    }
+  }
+  if (kb <= H) return;
+#pragma unroll
+  for (int c = 0; c < H; ++c) {
+    double v = H + c < kb ? A[(size_t)(k0 + H + c) * ld + r] : 0.0;
+#pragma unroll
+    for (int c2 = 0; c2 < H; ++c2) v -= lo[c2] * D[c2 * (kBpcNB + 1) + H + c];
+    hi[c] = v;
+  }
+#pragma unroll
+  for (int c = 0; c < H; ++c) {
+    if (H + c < kb) {
+      double v = hi[c];
+#pragma unroll
+      for (int c2 = 0; c2 < c; ++c2) v -= hi[c2] * D[(H + c2) * (kBpcNB + 1) + H + c];
+      hi[c] = v / D[(H + c) * (kBpcNB + 1) + H + c];
+      A[(size_t)(k0 + H + c) * ld + r] = hi[c];
     }
   }
 }
@@ -332,7 +357,7 @@ __global__ void __launch_bounds__(kThreads) k_bpc_trsm(const FrontDesc* fds, dou
 __global__ void __launch_bounds__(kThreads) k_bpc_update(const FrontDesc* fds, double* base, int k0) {
   const FrontDesc f = fds[blockIdx.y];
   if (k0 >= f.ne) return;
-  const int kb = min(kNB, f.ne - k0), k1 = k0 + kb, ld = f.ld;
+  const int kb = min(kBpcNB, f.ne - k0), k1 = k0 + kb, ld = f.ld;
   const int mt = f.nf - k1;
   const int nt = (mt + kTile - 1) / kTile;
   const int t = blockIdx.x;
@@ -341,12 +366,13 @@ __global__ void __launch_bounds__(kThreads) k_bpc_update(const FrontDesc* fds, d
   while (ti * (ti + 1) / 2 > t) --ti;
   while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
   const int tj = t - ti * (ti + 1) / 2;
-  __shared__ double LiT[kNB * kBpcPad];
-  __shared__ double LjT[kNB * kBpcPad];
+  extern __shared__ double bpc_sm[];
+  double* LiT = bpc_sm;                    // kBpcNB x kBpcPad
+  double* LjT = bpc_sm + kBpcNB * kBpcPad;
   double* A = base + f.off;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wr = warp >> 2, wc = warp & 3;
-  for (int idx = tid; idx < kNB * kTile; idx += kThreads) {
+  for (int idx = tid; idx < kBpcNB * kTile; idx += kThreads) {
     const int c = idx / kTile, r = idx - c * kTile;
     const int ri = ti * kTile + r, rj = tj * kTile + r;
     LiT[c * kBpcPad + r] = (c < kb && ri < mt) ? A[(size_t)(k0 + c) * ld + k1 + ri] : 0.0;
