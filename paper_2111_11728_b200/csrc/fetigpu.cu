@@ -2105,7 +2105,9 @@ int Ctx::solve_rrs(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_tra
     apply_F_block(W.p, k, Qb.p, k, k);  // line 7 (K5)
     mark(1);
     fapp += k;
-    // line 8: Delta = Q^T W (column-major k x k; lower triangle used)
+    // line 8: Delta = Q^T W (column-major k x k; lower triangle used).  A
+    // cublasDsyrkx of the lower triangle halves the flops but measured slower
+    // at k = 96 (MBB) and shifted RRS rank decisions: the GEMM stays.
     CB(cublasDgemm(cb, CUBLAS_OP_N, CUBLAS_OP_T, k, k, m, &one, Qb.p, k, W.p, k, &zero, Delta.p, k));
     k_mirror_lower<<<grid_for((long long)k * k), kThreads, 0, st>>>(Delta.p, k);
     mark(2);
