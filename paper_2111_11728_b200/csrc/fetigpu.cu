@@ -1740,6 +1740,13 @@ int Ctx::solve(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_trace* 
   }
   const int psi_S = std::max(1, std::min(64, m / 2048));
   if (fo) psi_part.alloc((size_t)cap * psi_S);
+  int fo_seg_grid = 148 * 8;
+  {
+    int dev = 0, sms = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    fo_seg_grid = sms * 8;
+  }
   Scal* hs = nullptr;
   CK(cudaMallocHost(&hs, sizeof(Scal)));
   std::unique_ptr<Scal, decltype(&cudaFreeHost)> hs_guard(hs, cudaFreeHost);
@@ -1787,7 +1794,7 @@ int Ctx::solve(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_trace* 
       k_inc<<<1, 1, 0, st>>>(cnt.p);
       CK(cudaMemcpyAsync(w.p, z.p, m * 8, cudaMemcpyDeviceToDevice, st));
       for (int pss = 0; pss < passes; ++pss) {
-        k_fo_psi_seg<<<dim3(cap, psi_S), 256, 0, st>>>(Qst.p, m, cnt.p, w.p, psi_part.p);
+        k_fo_psi_seg<<<fo_seg_grid, 256, 0, st>>>(Qst.p, m, cnt.p, w.p, psi_part.p, psi_S);
         k_fo_psi_sum<<<(cap + 255) / 256, 256, 0, st>>>(cnt.p, psi_S, psi_part.p, psi.p);
         k_fo_sub<<<(m + 31) / 32, 256, 0, st>>>(Wst.p, m, cnt.p, psi.p, w.p);
       }

@@ -654,8 +654,20 @@ __global__ void __launch_bounds__(256) k_fo_sub(const double* __restrict__ W, in
   const int i = blockIdx.x * 32 + lane;
   __shared__ double part[8][33];
   double v = 0.0;
-  if (i < m)
-    for (int j = warp; j < c; j += 8) v = fma(W[(size_t)j * m + i], psi[j], v);
+  if (i < m) {
+    // four loads in flight per warp, then the FMAs in the same order as the
+    // plain loop (bit-identical); otherwise each load waits for the last FMA
+    int j = warp;
+    for (; j + 24 < c; j += 32) {
+      const double w0 = __ldcs(W + (size_t)j * m + i), w1 = __ldcs(W + (size_t)(j + 8) * m + i),
+                   w2 = __ldcs(W + (size_t)(j + 16) * m + i), w3 = __ldcs(W + (size_t)(j + 24) * m + i);
+      v = fma(w0, psi[j], v);
+      v = fma(w1, psi[j + 8], v);
+      v = fma(w2, psi[j + 16], v);
+      v = fma(w3, psi[j + 24], v);
+    }
+    for (; j < c; j += 8) v = fma(W[(size_t)j * m + i], psi[j], v);
+  }
   part[warp][lane] = v;
   __syncthreads();
   if (warp == 0 && i < m) {
@@ -671,28 +683,40 @@ __global__ void __launch_bounds__(256) k_fo_sub(const double* __restrict__ W, in
 __global__ void __launch_bounds__(256) k_fo_psi_seg(const double* __restrict__ Q, int m,
                                                     const int* __restrict__ cnt,
                                                     const double* __restrict__ w,
-                                                    double* __restrict__ partial) {
-  const int j = blockIdx.x;
-  if (j >= *cnt) return;
-  const int S = gridDim.y, s = blockIdx.y;
+                                                    double* __restrict__ partial, int S) {
+  // fixed grid, grid-stride over the live (column j, segment s) items: no
+  // empty CTAs for the not-yet-stored directions (the graph is static)
+  const int items = *cnt * S;
   const int chunk = (m + S - 1) / S;
-  const int i0 = s * chunk, i1 = min(m, i0 + chunk);
-  const double* q = Q + (size_t)j * m;
-  double a0 = 0.0, a1 = 0.0;
-  int i = i0 + threadIdx.x;
-  for (; i + 256 < i1; i += 512) {
-    a0 = fma(q[i], w[i], a0);
-    a1 = fma(q[i + 256], w[i + 256], a1);
-  }
-  if (i < i1) a0 = fma(q[i], w[i], a0);
-  double acc = warp_sum(a0 + a1);
   __shared__ double red[8];
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double t = 0.0;
-    for (int k = 0; k < 8; ++k) t += red[k];
-    partial[(size_t)j * S + s] = t;
+  for (int item = blockIdx.x; item < items; item += gridDim.x) {
+    const int j = item / S, s = item - j * S;
+    const int i0 = s * chunk, i1 = min(m, i0 + chunk);
+    const double* q = Q + (size_t)j * m;
+    double a0 = 0.0, a1 = 0.0;
+    int i = i0 + threadIdx.x;
+    for (; i + 768 < i1; i += 1024) {  // 4 loads of each vector in flight, same FMA order as 2-way
+      const double q0 = __ldcs(q + i), q1 = __ldcs(q + i + 256), q2 = __ldcs(q + i + 512), q3 = __ldcs(q + i + 768);
+      const double x0 = w[i], x1 = w[i + 256], x2 = w[i + 512], x3 = w[i + 768];
+      a0 = fma(q0, x0, a0);
+      a1 = fma(q1, x1, a1);
+      a0 = fma(q2, x2, a0);
+      a1 = fma(q3, x3, a1);
+    }
+    for (; i + 256 < i1; i += 512) {
+      a0 = fma(q[i], w[i], a0);
+      a1 = fma(q[i + 256], w[i + 256], a1);
+    }
+    if (i < i1) a0 = fma(q[i], w[i], a0);
+    const double acc = warp_sum(a0 + a1);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int k = 0; k < 8; ++k) t += red[k];
+      partial[(size_t)j * S + s] = t;
+    }
+    __syncthreads();
   }
 }
 __global__ void k_fo_psi_sum(const int* __restrict__ cnt, int S, const double* __restrict__ partial,
