@@ -189,12 +189,36 @@ def cpu_sample(steps=3, warmup=1, sample=(8, 4)):
                       f"extrapolated x{scale:.0f} in subdomains"}
 
 
-def cpu_solves():
-    """The oracle's full PCG solves (implicit per-subdomain solves, all host
-    cores) for the two configs whose CPU solve fits a bounded budget."""
+def cpu_applies(steps=3):
+    """the oracle's build time and single F-apply time (median of
+    `steps` after one warm-up, all host cores) for C1-C3 and C5."""
     from oracle import pyoracle
     out = {}
-    for name, fn, dirs in (("C2", pb.config2, 1), ("C3-fetidp", lambda: pb.config3(method=1), 1)):
+    for name, fn in (("C1", pb.config1), ("C2", pb.config2), ("C3-tfeti", lambda: pb.config3(method=0)),
+                     ("C3-fetidp", lambda: pb.config3(method=1)), ("C5", pb.config5)):
+        t0 = time.perf_counter()
+        o = pyoracle.Oracle(fn())
+        tb = time.perf_counter() - t0
+        x = np.random.default_rng(0).standard_normal(o.m)
+        o.apply_F(x)
+        ts = []
+        for _ in range(steps):
+            t0 = time.perf_counter()
+            o.apply_F(x)
+            ts.append(time.perf_counter() - t0)
+        out[name] = {"build_s": round(tb, 4), "apply_ms": round(statistics.median(ts) * 1e3, 3), "m": o.m}
+        log("cpu apply", name, out[name])
+    return out
+
+
+def cpu_solves():
+    """The oracle's full PCG solves (implicit per-subdomain solves, all host
+    cores) for the configs whose CPU solve fits a bounded budget; the C3 T-FETI
+    FO (44 s) and C5 RRS (~700 s) CPU solves are recorded in
+    profiles/r01_solves_full_vs_oracle.jsonl and profiles/r01_parity_C5_full.json."""
+    from oracle import pyoracle
+    out = {}
+    for name, fn, dirs in (("C1", pb.config1, 0), ("C2", pb.config2, 1), ("C3-fetidp", lambda: pb.config3(method=1), 1)):
         t0 = time.perf_counter()
         o = pyoracle.Oracle(fn())
         tb = time.perf_counter() - t0
@@ -446,6 +470,7 @@ def main():
                    "cores": r["cores"], "kind": "port", "sample": r["sample"],
                    "cpu_model": cpu_model(), "t_apply_c4_s": r["t_apply_c4_s"]}
             if not args.no_solves:
+                cpu["applies"] = cpu_applies()
                 cpu["solves"] = cpu_solves()
         except Exception as e:  # the checker is optional for the GPU number
             log("cpu baseline failed:", e)
