@@ -186,6 +186,33 @@ struct DBuf {
 
 static inline int round_up(int v, int a) { return (v + a - 1) / a * a; }
 
+// Launch with programmatic dependent launch (PDL): the kernel may be scheduled
+// while its predecessor in the stream finishes and waits in pdl_wait() (every
+// kernel launched this way calls it first), which hides the launch latency
+// between the small dependent kernels of a solver iteration.  FETIGPU_NO_PDL=1
+// launches them normally.
+static bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("FETIGPU_NO_PDL");
+    return !(e && e[0] == '1');
+  }();
+  return on;
+}
+template <class... KArgs, class... Args>
+static void launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  CK(cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...));
+}
+
 // cudaFuncAttributeMaxDynamicSharedMemorySize is per function and process-wide:
 // contexts of different sizes may be alive at once, so it is only ever raised.
 template <class K>
@@ -1096,24 +1123,29 @@ struct Ctx {
   // zero_y: output still to be zeroed (the gather kernel does it when it runs)
   void coarse_solve_packed(bool g_ready, double* zero_y = nullptr) {
     if (!g_ready || su.Nc == 0) {
-      k_coarse_gather<<<grid_for(std::max(su.Nc, zero_y ? su.m : 0)), kThreads, 0, st>>>(
-          d_optr.p, d_oidx.p, d_tbuf.p, su.Nc, d_gc.p, 1.0, nullptr, zero_y, zero_y ? su.m : 0);
+      launch_pdl(k_coarse_gather, grid_for(std::max(su.Nc, zero_y ? su.m : 0)), kThreads, 0, st,
+                 (const int*)d_optr.p, (const int*)d_oidx.p, (const double*)d_tbuf.p, su.Nc, d_gc.p, 1.0,
+                 (const double*)nullptr, zero_y, zero_y ? su.m : 0);
       LAUNCH_CHECK();
     }
     if (su.Nc == 0) return;
     if (!use_csym) {  // small coarse problem: dense L2-resident inverse, one launch
-      k_dense_gemv<<<grid_for((long long)su.Nc * 32), kThreads, 0, st>>>(d_Kinv.p, su.Nc, d_gc.p, d_h.p);
+      launch_pdl(k_dense_gemv, grid_for((long long)su.Nc * 32), kThreads, 0, st, (const double*)d_Kinv.p, su.Nc,
+                 (const double*)d_gc.p, d_h.p);
       LAUNCH_CHECK();
       return;
     }
-    k_csym_tiles<<<csym_grid, 128, 0, st>>>(d_kinv_tiles.p, kinv_nb, su.Nc, d_gc.p, d_crow.p, d_ccol.p);
-    k_csym_reduce<<<kinv_nb, 512, 0, st>>>(d_crow.p, d_ccol.p, kinv_nb, su.Nc, d_h.p);
+    launch_pdl(k_csym_tiles, csym_grid, 128, 0, st, (const double*)d_kinv_tiles.p, kinv_nb, su.Nc,
+               (const double*)d_gc.p, d_crow.p, d_ccol.p);
+    launch_pdl(k_csym_reduce, kinv_nb, 512, 0, st, (const double*)d_crow.p, (const double*)d_ccol.p, kinv_nb,
+               su.Nc, d_h.p);
     LAUNCH_CHECK();
   }
   // phase 2: y = sum_s B_s (v_s + A''_s u_s)
   void launch_phase2_csym(double* y) {
-    k_dp_phase2<<<su.Ns, kThreads, 0, st>>>(d_op.p, d_dp.p, d_oprows.p, d_opcoef_apply.p, d_abc.p, d_cmap.p, d_h.p,
-                                            d_vbuf.p, y, 1.0);
+    launch_pdl(k_dp_phase2, su.Ns, kThreads, 0, st, (const OpSub*)d_op.p, (const DpSub*)d_dp.p,
+               (const int*)d_oprows.p, (const double*)d_opcoef_apply.p, (const double*)d_abc.p,
+               (const int*)d_cmap.p, (const double*)d_h.p, (const double*)d_vbuf.p, y, 1.0);
     LAUNCH_CHECK();
   }
 
@@ -1161,14 +1193,16 @@ struct Ctx {
         double* yc = y + (size_t)c * ldy;
         // phase 1: v_s = F''_s x_s and t_s = A''^T x_s (one kernel; it also zeroes y)
         if (use_sym) {
-          k_sym_gemv_scatter<1, true><<<Ns, 256, sym_smem, st>>>(d_sym.p, d_symtiles.p, d_oprows.p,
-                                                                 d_opcoef_apply.p, xc, nullptr, d_vbuf.p, d_voff.p,
-                                                                 d_dp.p, d_abc.p, d_tbuf.p, 0, yc, su.m, Ns,
-                                                                 su.Nc ? d_cgather.p : nullptr);
+          launch_pdl(k_sym_gemv_scatter<1, true>, Ns, 256, sym_smem, st, (const SymSub*)d_sym.p,
+                     (const double*)d_symtiles.p, (const int*)d_oprows.p, (const double*)d_opcoef_apply.p, xc,
+                     (double*)nullptr, d_vbuf.p, (const int*)d_voff.p, (const DpSub*)d_dp.p,
+                     (const double*)d_abc.p, d_tbuf.p, 0, yc, su.m, Ns,
+                     (const CoarseGather*)(su.Nc ? d_cgather.p : nullptr));
         } else {
-          k_gather_gemv_scatter<1, true><<<dim3(Ns, 1, rsplit), kThreads, max_ld * 8, st>>>(
-              d_op.p, d_opmat.p, d_oprows.p, d_opcoef_apply.p, xc, nullptr, nullptr, 0, d_vbuf.p, d_voff.p, ldx, 0,
-              1, d_dp.p, d_abc.p, d_tbuf.p);
+          launch_pdl(k_gather_gemv_scatter<1, true>, dim3(Ns, 1, rsplit), kThreads, max_ld * 8, st,
+                     (const OpSub*)d_op.p, (const double*)d_opmat.p, (const int*)d_oprows.p,
+                     (const double*)d_opcoef_apply.p, xc, (double*)nullptr, (double*)nullptr, 0, d_vbuf.p,
+                     (const int*)d_voff.p, ldx, 0, 1, (const DpSub*)d_dp.p, (const double*)d_abc.p, d_tbuf.p);
         }
         // coarse: u = Kbar^{-1} (sum_s B_c^T t_s), fixed order (y zeroed here on the non-symmetric path)
         coarse_solve_packed(use_sym, use_sym ? nullptr : yc);
@@ -1471,7 +1505,7 @@ struct Ctx {
     a.npairs = k;
     a.n = su.m;
     const int nblk = std::max(1, std::min(kDotBlocks, (su.m + 1023) / 1024));
-    k_dot_fused<<<nblk, kThreads, 0, st>>>(a, d_partial.p, d_counter.p, out);
+    launch_pdl(k_dot_fused, nblk, kThreads, 0, st, a, d_partial.p, d_counter.p, out);
     LAUNCH_CHECK();
   }
 
@@ -1785,22 +1819,26 @@ int Ctx::solve(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_trace* 
     apply_F(w.p, q.p, 1, m, m);
     dots({{w.p, q.p}, {w.p, r.p}}, &sc.p->delta);
     if (tf) proj_corr(q.p, m, corr.p, m, 1);
-    k_pcg_update<<<grid_for(m), kThreads, 0, st>>>(m, sc.p, fo ? 1 : 0, w.p, q.p, tf ? corr.p : nullptr, lam.p,
-                                                   r.p);
+    launch_pdl(k_pcg_update, grid_for(m), kThreads, 0, st, m, sc.p, fo ? 1 : 0, (const double*)w.p,
+               (const double*)q.p, (const double*)(tf ? corr.p : nullptr), lam.p, r.p);
     precond_projected(r.p, z.p, nullptr);
     dots({{r.p, z.p}, {r.p, r.p}, {z.p, z.p}}, &sc.p->rz);
     if (fo) {
-      k_fo_store2<<<grid_for(m), kThreads, 0, st>>>(m, sc.p, cnt.p, w.p, q.p, Wst.p, Qst.p);
-      k_inc<<<1, 1, 0, st>>>(cnt.p);
+      launch_pdl(k_fo_store2, grid_for(m), kThreads, 0, st, m, (const Scal*)sc.p, (const int*)cnt.p,
+                 (const double*)w.p, (const double*)q.p, Wst.p, Qst.p);
+      launch_pdl(k_inc, 1, 1, 0, st, cnt.p);
       CK(cudaMemcpyAsync(w.p, z.p, m * 8, cudaMemcpyDeviceToDevice, st));
       for (int pss = 0; pss < passes; ++pss) {
-        k_fo_psi_seg<<<fo_seg_grid, 256, 0, st>>>(Qst.p, m, cnt.p, w.p, psi_part.p, psi_S);
-        k_fo_psi_sum<<<(cap + 255) / 256, 256, 0, st>>>(cnt.p, psi_S, psi_part.p, psi.p);
-        k_fo_sub<<<(m + 31) / 32, 256, 0, st>>>(Wst.p, m, cnt.p, psi.p, w.p);
+        launch_pdl(k_fo_psi_seg, fo_seg_grid, 256, 0, st, (const double*)Qst.p, m, (const int*)cnt.p,
+                   (const double*)w.p, psi_part.p, psi_S);
+        launch_pdl(k_fo_psi_sum, (cap + 255) / 256, 256, 0, st, (const int*)cnt.p, psi_S,
+                   (const double*)psi_part.p, psi.p);
+        launch_pdl(k_fo_sub, (m + 31) / 32, 256, 0, st, (const double*)Wst.p, m, (const int*)cnt.p,
+                   (const double*)psi.p, w.p);
       }
     } else {
-      k_cg_dir2<<<grid_for(m), kThreads, 0, st>>>(m, sc.p, z.p, w.p);
-      k_shift_rz<<<1, 1, 0, st>>>(sc.p);
+      launch_pdl(k_cg_dir2, grid_for(m), kThreads, 0, st, m, sc.p, (const double*)z.p, w.p);
+      launch_pdl(k_shift_rz, 1, 1, 0, st, sc.p);
     }
     if (readback) CK(cudaMemcpyAsync(hs, sc.p, sizeof(Scal), cudaMemcpyDeviceToHost, st));
     LAUNCH_CHECK();
@@ -1845,7 +1883,7 @@ int Ctx::solve(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_trace* 
           if (cudaStreamBeginCaptureToGraph(st, bodyg, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal) ==
               cudaSuccess) {
             body(false);
-            k_iter_control<<<1, 1, 0, st>>>(sc.p, dctl.p, dtrace.p, hcond);
+            launch_pdl(k_iter_control, 1, 1, 0, st, (const Scal*)sc.p, dctl.p, dtrace.p, hcond);
             cudaGraph_t captured = nullptr;
             built_ok = cudaStreamEndCapture(st, &captured) == cudaSuccess &&
                        cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess;

@@ -20,6 +20,16 @@
 
 namespace fg {
 
+// Programmatic dependent launch: a kernel launched with the PDL attribute may
+// be scheduled while its predecessor in the stream is still finishing; it
+// waits here (griddepcontrol.wait) until the predecessor has completed and its
+// writes are visible.  A no-op for ordinary launches.
+__device__ __forceinline__ void pdl_wait() {
+#if __CUDA_ARCH__ >= 900
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+
 // ------------------------------------------------------------ the F-apply --
 // KR = max dual rows touching one local DOF (1 FETI-DP, <= 3 T-FETI cross points)
 // FETI-DP coarse pre-pass fused into the GEMV CTA (x_s already in smem):
@@ -83,6 +93,7 @@ __global__ void __launch_bounds__(kThreads) k_gather_gemv_scatter(
     double* __restrict__ zcols, int ldz, double* __restrict__ vbuf, const int* __restrict__ voff,
     int ldx, int ldy, int zrs = 1, const DpSub* __restrict__ dps = nullptr,
     const double* __restrict__ abc = nullptr, double* __restrict__ tbuf = nullptr) {
+  pdl_wait();
   extern __shared__ double xs[];
   const int s = blockIdx.x;
   const int col = blockIdx.y;
@@ -169,6 +180,7 @@ __global__ void __launch_bounds__(256) k_sym_gemv_scatter(
     double* __restrict__ vbuf, const int* __restrict__ voff, const DpSub* __restrict__ dps = nullptr,
     const double* __restrict__ abc = nullptr, double* __restrict__ tbuf = nullptr, int s0 = 0,
     double* __restrict__ zero_y = nullptr, int ny = 0, int nsub = 1, const CoarseGather* cgp = nullptr) {
+  pdl_wait();
   extern __shared__ double shm[];
   const int s = s0 + blockIdx.x;   // subdomain (s0: first subdomain of a pipelined chunk)
   const SymSub d = subs[s];
@@ -307,6 +319,7 @@ __global__ void k_coarse_gather(const int* __restrict__ optr, const int* __restr
                                 const double* __restrict__ tbuf, int nc, double* __restrict__ out,
                                 double sign, const double* __restrict__ add,
                                 double* __restrict__ zero_y = nullptr, int ny = 0) {
+  pdl_wait();
   if (zero_y)  // the apply's output is zeroed here, between phase 1 and phase 2
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ny; i += gridDim.x * blockDim.x) zero_y[i] = 0.0;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nc; i += gridDim.x * blockDim.x) {
@@ -328,6 +341,7 @@ __global__ void k_coarse_gather(const int* __restrict__ optr, const int* __restr
 __global__ void __launch_bounds__(128) k_csym_tiles(const double* __restrict__ tiles, int nb, int nc,
                                                     const double* __restrict__ g, double* __restrict__ rowp,
                                                     double* __restrict__ colp) {
+  pdl_wait();
   const int lane = threadIdx.x & 31;
   const int ntiles = nb * (nb + 1) / 2;
   const int nw = (gridDim.x * blockDim.x) >> 5;
@@ -370,6 +384,7 @@ __global__ void __launch_bounds__(128) k_csym_tiles(const double* __restrict__ t
 __global__ void __launch_bounds__(512) k_csym_reduce(const double* __restrict__ rowp,
                                                      const double* __restrict__ colp, int nb, int nc,
                                                      double* __restrict__ u) {
+  pdl_wait();
   __shared__ double red[16][32];
   const int b = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const size_t rb = (size_t)b * (b + 1) / 2;
@@ -403,6 +418,7 @@ __global__ void __launch_bounds__(512) k_csym_reduce(const double* __restrict__ 
 __global__ void __launch_bounds__(256) k_dense_gemv(const double* __restrict__ M, int n,
                                                     const double* __restrict__ x,
                                                     double* __restrict__ y) {
+  pdl_wait();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
   for (int i = warp; i < n; i += nwarps) {
@@ -439,6 +455,7 @@ __global__ void k_dp_phase2(const OpSub* __restrict__ subs, const DpSub* __restr
                             const double* __restrict__ abc, const int* __restrict__ cmap,
                             const double* __restrict__ u, const double* __restrict__ vbuf,
                             double* __restrict__ y, double vscale) {
+  pdl_wait();
   const int s = blockIdx.x;
   const OpSub d = subs[s];
   const DpSub p = dps[s];
@@ -470,6 +487,7 @@ __global__ void k_proj_gather(const OpSub* __restrict__ psubs, const int* __rest
                               const double* __restrict__ coefs, const double* __restrict__ RT,
                               const int* __restrict__ rt_off, const double* __restrict__ v, int ldv,
                               double* __restrict__ g, int ldg, double sign, int rs = 1) {
+  pdl_wait();
   const int s = blockIdx.x, col = blockIdx.y;
   const OpSub d = psubs[s];
   const double* vc = v + (size_t)col * ldv;
@@ -513,6 +531,7 @@ __global__ void k_proj_scatter(const OpSub* __restrict__ psubs, const int* __res
                                const double* __restrict__ coefs, const double* __restrict__ RT,
                                const int* __restrict__ rt_off, const double* __restrict__ h, int ldh,
                                double* __restrict__ corr, int ldc, int rs = 1) {
+  pdl_wait();
   const int s = blockIdx.x, col = blockIdx.y;
   const OpSub d = psubs[s];
   const double* R = RT + rt_off[s];
@@ -584,6 +603,7 @@ __global__ void k_dot_final(const double* partial, int npairs, double* out) {
 // fixed slot, the last block to finish sums them in fixed order.
 __global__ void __launch_bounds__(kThreads) k_dot_fused(DotArgs args, double* partial,
                                                         unsigned int* counter, double* out) {
+  pdl_wait();
   double acc[4] = {0, 0, 0, 0};
   const int stride = gridDim.x * blockDim.x;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < args.n; i += stride) {
@@ -649,6 +669,7 @@ __global__ void __launch_bounds__(256) k_fo_sub(const double* __restrict__ W, in
                                                 const int* __restrict__ cnt,
                                                 const double* __restrict__ psi,
                                                 double* __restrict__ w) {
+  pdl_wait();
   const int c = *cnt;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int i = blockIdx.x * 32 + lane;
@@ -684,6 +705,7 @@ __global__ void __launch_bounds__(256) k_fo_psi_seg(const double* __restrict__ Q
                                                     const int* __restrict__ cnt,
                                                     const double* __restrict__ w,
                                                     double* __restrict__ partial, int S) {
+  pdl_wait();
   // fixed grid, grid-stride over the live (column j, segment s) items: no
   // empty CTAs for the not-yet-stored directions (the graph is static)
   const int items = *cnt * S;
@@ -721,6 +743,7 @@ __global__ void __launch_bounds__(256) k_fo_psi_seg(const double* __restrict__ Q
 }
 __global__ void k_fo_psi_sum(const int* __restrict__ cnt, int S, const double* __restrict__ partial,
                              double* __restrict__ psi) {
+  pdl_wait();
   const int c = *cnt;
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < c; j += gridDim.x * blockDim.x) {
     double t = 0.0;
@@ -732,6 +755,7 @@ __global__ void k_fo_psi_sum(const int* __restrict__ cnt, int S, const double* _
 __global__ void k_fo_store2(int n, const Scal* sc, const int* __restrict__ cnt,
                             const double* __restrict__ w, const double* __restrict__ q,
                             double* __restrict__ Wst, double* __restrict__ Qst) {
+  pdl_wait();
   const double inv = 1.0 / sqrt(sc->delta);
   const int j = *cnt;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
@@ -739,14 +763,17 @@ __global__ void k_fo_store2(int n, const Scal* sc, const int* __restrict__ cnt,
     Qst[(size_t)j * n + i] = q[i] * inv;
   }
 }
-__global__ void k_inc(int* cnt) { *cnt += 1; }
+__global__ void k_inc(int* cnt) {
+  pdl_wait(); *cnt += 1; }
 // w = z + beta w with beta = rz / rz_old from device scalars; then rz_old = rz
 __global__ void k_cg_dir2(int n, Scal* sc, const double* __restrict__ z, double* __restrict__ w) {
+  pdl_wait();
   const double beta = sc->rz / sc->rz_old;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
     w[i] = fma(beta, w[i], z[i]);
 }
-__global__ void k_shift_rz(Scal* sc) { sc->rz_old = sc->rz; }
+__global__ void k_shift_rz(Scal* sc) {
+  pdl_wait(); sc->rz_old = sc->rz; }
 
 // Device-side loop control of PCG / FO (runs as the last node of the
 // iteration body under a CUDA-graph `while` conditional): the host loop's
@@ -760,6 +787,7 @@ struct IterCtl {
 };
 __global__ void k_iter_control(const Scal* __restrict__ sc, IterCtl* __restrict__ c, double* __restrict__ trace,
                                cudaGraphConditionalHandle h) {
+  pdl_wait();
   unsigned int go = 0;
   if (sc->breakdown != 0.0) {
     c->status = 2;  // FETIGPU_BREAKDOWN
@@ -781,11 +809,13 @@ __global__ void k_iter_control(const Scal* __restrict__ sc, IterCtl* __restrict_
 // ------------------------------------------------------- vector updates --
 
 __global__ void k_axpy(int n, double a, const double* __restrict__ x, double* __restrict__ y) {
+  pdl_wait();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
     y[i] = fma(a, x[i], y[i]);
 }
 // v += corr (projector finish)
 __global__ void k_add(int n, const double* __restrict__ c, double* __restrict__ v, int ldc, int ldv) {
+  pdl_wait();
   const int col = blockIdx.y;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
     v[(size_t)col * ldv + i] += c[(size_t)col * ldc + i];
@@ -794,6 +824,7 @@ __global__ void k_add(int n, const double* __restrict__ c, double* __restrict__ 
 __global__ void k_pcg_update(int n, Scal* sc, int fo, const double* __restrict__ w,
                              const double* __restrict__ q, const double* __restrict__ corr,
                              double* __restrict__ lambda, double* __restrict__ r) {
+  pdl_wait();
   if (!(sc->delta > 0.0)) {  // breakdown: leave lambda, r untouched
     if (blockIdx.x == 0 && threadIdx.x == 0) sc->breakdown = 1.0;
     return;
