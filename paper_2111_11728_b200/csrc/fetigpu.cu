@@ -361,7 +361,7 @@ struct Ctx {
   // a copy stream; the subdomains of chunk c (rows < pipe_need[c]) start their
   // phase-1 GEMV on their own stream as soon as that prefix has landed, so the
   // H2D copy overlaps the operator stream and the chunks fill the GPU together.
-  static constexpr int kPipe = 4;
+  static constexpr int kPipe = 8;
   cudaStream_t pipe_st[kPipe] = {}, pipe_cp = nullptr;
   cudaEvent_t pipe_in[kPipe] = {}, pipe_done[kPipe] = {}, pipe_start = nullptr;
   int pipe_s0[kPipe + 1] = {}, pipe_need[kPipe] = {};
