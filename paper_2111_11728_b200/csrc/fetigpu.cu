@@ -18,6 +18,7 @@
 #include <unordered_map>
 #include <numeric>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "common.cuh"
@@ -211,6 +212,24 @@ static void launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, 
   cfg.attrs = at;
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
   CK(cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...));
+}
+
+// f(i) for i in [0, n) over up to 16 host threads (contiguous ranges); f must
+// write disjoint outputs.  Serial for small n.
+template <class F>
+static void parallel_for(int n, F&& f) {
+  const int nt = std::min<int>(16, std::max(1u, std::thread::hardware_concurrency()));
+  if (n < 64 || nt <= 1) {
+    for (int i = 0; i < n; ++i) f(i);
+    return;
+  }
+  std::vector<std::thread> th;
+  for (int t = 0; t < nt; ++t)
+    th.emplace_back([&, t] {
+      const int a = (int)((long long)n * t / nt), b = (int)((long long)n * (t + 1) / nt);
+      for (int i = a; i < b; ++i) f(i);
+    });
+  for (auto& x : th) x.join();
 }
 
 // cudaFuncAttributeMaxDynamicSharedMemorySize is per function and process-wide:
@@ -674,6 +693,7 @@ struct Ctx {
       d_fac_ne.upload(fne, st);
       d_fac_off.upload(so.fac_off, st);
     }
+    ptimer.mark("slot src/ext lists", st);
     // ---- per-subdomain operator maps
     // flat (subdomain, perimeter position) -> up to 3 (row, sign, weight) entries
     struct Ent { int row; double coef; double w; };
@@ -692,20 +712,28 @@ struct Ctx {
       add_ent(r.sp, su.dpos[r.dp], {i, 1.0, su.wplus[i]});
       if (r.kind == 0) add_ent(r.sm, su.dpos[r.dm], {i, -1.0, su.wminus[i]});
     }
+    ptimer.mark("maps: row entries", st);
     std::vector<OpSub> ops(Ns), pcs(Ns), pjs(Ns);
     std::vector<int> slot_of(Ns), top_off(Ns), design(Ns), rt_off(Ns);
+    std::vector<size_t> ip_off(Ns);
     size_t ntop = 0, nT = 0;
-    for (int s = 0; s < Ns; ++s) { ntop += su.subs[s].Top.size(); nT += su.subs[s].T.size(); }
+    for (int s = 0; s < Ns; ++s) {  // output offsets first, so subdomains can be filled in parallel
+      top_off[s] = (int)ntop;
+      ip_off[s] = nT;
+      ntop += su.subs[s].Top.size();
+      nT += su.subs[s].T.size();
+    }
     std::vector<int> rows(ntop * KR), prow(nT * KRp), top_pos(ntop);
     std::vector<double> coef(ntop * KR), pcoef(nT * KRp), pjcoef(nT * KRp), RT(nT * 3);
-    size_t io = 0, ip = 0;
-    for (int s = 0; s < Ns; ++s) {
+    sub_maxrow.assign(Ns, -1);
+    parallel_for(Ns, [&](int s) {
       const SubPlan& S = su.subs[s];
       const int sl = S.op_slot;
+      size_t io = (size_t)top_off[s], ip = ip_off[s];
       slot_of[s] = sl;
       design[s] = S.design;
       ops[s] = {op_moff[sl], op_ns[sl], op_ld[sl], (int)(io * KR), 0};
-      top_off[s] = (int)io;
+      int mx = -1;
       for (int t : S.Top) {
         const size_t k = (size_t)s * nb + t;
         top_pos[io] = t;
@@ -713,9 +741,11 @@ struct Ctx {
           const bool has = q < ecnt[k];
           rows[io * KR + q] = has ? ent[k * KR + q].row : -1;
           coef[io * KR + q] = has ? ent[k * KR + q].coef : 0.0;
+          mx = std::max(mx, rows[io * KR + q]);
         }
         ++io;
       }
+      sub_maxrow[s] = mx;
       // preconditioner / projector maps over T
       pcs[s] = {0, (int)S.T.size(), 0, (int)(ip * KRp), 0};
       pjs[s] = pcs[s];
@@ -731,12 +761,8 @@ struct Ctx {
         for (int q = 0; q < 3; ++q) RT[ip * 3 + q] = su.Rb[(size_t)q * nb + t];
         ++ip;
       }
-    }
-    sub_maxrow.assign(Ns, -1);
-    for (int s = 0; s < Ns; ++s) {
-      const size_t b = (size_t)top_off[s] * KR, e = b + su.subs[s].Top.size() * (size_t)KR;
-      for (size_t q = b; q < e; ++q) sub_maxrow[s] = std::max(sub_maxrow[s], rows[q]);
-    }
+    });
+    ptimer.mark("maps: host loops", st);
     d_oprows.upload(rows, st); d_opcoef.upload(coef, st);
     d_slot_of.upload(slot_of, st); d_design.upload(design, st);
     d_top_pos.upload(top_pos, st); d_top_off.upload(top_off, st);
