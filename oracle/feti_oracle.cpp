@@ -364,8 +364,8 @@ static void q4_unit(const Material& m, double hx, double hy, double* k /*8x8 cm*
 // assemble_subdomain (fem.cpp:86-119): element loop ey-major, ex-minor,
 // contributions e_mod * k_unit(i,j) summed in insertion order (Eigen
 // setFromTriplets collapses duplicates in insertion order).
-static Csr assemble(int n, double hx, double hy, const double* rho, const Material& mat,
-                    const double* k_unit) {
+static Csr assemble(int n, double /*hx*/, double /*hy*/, const double* rho, const Material& mat,
+                    const double* k_unit) {  // element size is already in k_unit
   const int nn = n + 1, ndof = 2 * nn * nn;
   Csr K;
   K.n = ndof;
