@@ -328,6 +328,9 @@ def solve_table(engine, configs):
                      "iterations": tr["iterations"], "status": ["converged", "max_iter", "breakdown"][tr["status"]],
                      "rel_residual": tr["eps_final"] / tr["eps0"] if tr["eps0"] > 0 else 0.0,
                      "m": st["m"], "directions": ["single", "fo", "rrs"][kw.get("directions", 0)]}
+        ops = g.time_ops(reps=200 if not name.startswith("C4") else 20)
+        out[name]["per_iteration_ops_us"] = {k.replace("_ms", ""): round(v * 1e3, 2) for k, v in ops.items()}
+        out[name]["us_per_iteration"] = round(tr["solve_ms"] * 1e3 / max(1, tr["iterations"]), 1)
         if not name.startswith("C4"):
             # C1-C3 and C5 operators are L2-resident -- time per apply and
             # effective GB/s of the formula bytes, labelled as such (no HBM-fraction claim)

@@ -223,6 +223,11 @@ int fetigpu_host_free(void* ptr);
 int fetigpu_memcpy(fetigpu_ctx* ctx, void* dst, const void* src, size_t bytes, int kind);
 int fetigpu_fill_random(fetigpu_ctx* ctx, double* d_ptr, size_t count, unsigned long long seed);
 int fetigpu_synchronize(fetigpu_ctx* ctx);
+/* Device time per call (CUDA events, `reps` back-to-back calls after 3
+ * warm-up, no L2 flush) of the three per-iteration operators: ms[0] F-apply,
+ * ms[1] preconditioner, ms[2] projector (identity for
+ * FETI-DP; decomposition.hpp:136 for T-FETI). */
+int fetigpu_time_ops(fetigpu_ctx* ctx, int reps, double* ms);
 /* Times `reps` device-resident applies of F on ncols columns with CUDA
  * events on the context stream; ms[0] = mean per apply, ms[1] = mean of the
  * dominant kernel, ms[2] = its share; launches[0] = kernels per apply. */

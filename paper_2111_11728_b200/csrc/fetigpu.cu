@@ -2692,6 +2692,40 @@ int fetigpu_synchronize(fetigpu_ctx* ctx) {
   return guarded([&] { CK(cudaStreamSynchronize(ctx->c.st)); });
 }
 
+int fetigpu_time_ops(fetigpu_ctx* ctx, int reps, double* ms) {
+  return guarded([&] {
+    NEED_BUILT(ctx);
+    Ctx& c = ctx->c;
+    const int m = std::max(1, c.su.m);
+    DBuf<double> x, y;
+    x.alloc(m);
+    y.alloc(m);
+    k_fill_random<<<grid_for(m), kThreads, 0, c.st>>>(x.p, (size_t)m, 11ull);
+    LAUNCH_CHECK();
+    cudaEvent_t a, b;
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+    for (int op = 0; op < 3; ++op) {
+      auto run = [&] {
+        if (c.su.m == 0) return;
+        if (op == 0) c.apply_F(x.p, y.p, 1, c.su.m, c.su.m);
+        else if (op == 1) c.apply_precond(x.p, y.p, nullptr);
+        else c.project(y.p, 1, c.su.m);
+      };
+      for (int w = 0; w < 3; ++w) run();
+      CK(cudaEventRecord(a, c.st));
+      for (int r = 0; r < reps; ++r) run();
+      CK(cudaEventRecord(b, c.st));
+      CK(cudaEventSynchronize(b));
+      float t = 0;
+      CK(cudaEventElapsedTime(&t, a, b));
+      ms[op] = t / std::max(1, reps);
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+  });
+}
+
 int fetigpu_time_apply(fetigpu_ctx* ctx, const double* x, double* y, int ncols, int reps, int flush_l2,
                        double* ms, int* launches) {
   return guarded([&] {

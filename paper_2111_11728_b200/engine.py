@@ -79,7 +79,7 @@ EXPORTED = ["fetigpu_set_device", "fetigpu_create", "fetigpu_build", "fetigpu_de
             "fetigpu_host_alloc", "fetigpu_host_free", "fetigpu_memcpy", "fetigpu_fill_random",
             "fetigpu_synchronize", "fetigpu_time_apply", "fetigpu_apply_F_block_device",
             "fetigpu_time_apply_block", "fetigpu_fp64_peak", "fetigpu_selftest_dmma",
-            "fetigpu_pivoted_cholesky", "fetigpu_pivoted_compress"]
+            "fetigpu_pivoted_cholesky", "fetigpu_pivoted_compress", "fetigpu_time_ops"]
 
 
 class FgProblem(C.Structure):
@@ -324,6 +324,12 @@ class FetiSystem:
             L.fetigpu_device_free(self.h, dW)
             L.fetigpu_device_free(self.h, dQ)
         return Q
+
+    def time_ops(self, reps: int = 200) -> dict:
+        """Device time per call of F, the preconditioner and the projector (ms)."""
+        ms = (C.c_double * 3)()
+        check(lib().fetigpu_time_ops(self.h, reps, ms))
+        return {"F_ms": ms[0], "precond_ms": ms[1], "project_ms": ms[2]}
 
     def local_operator(self, s: int):
         cap = 8 * self.prob.n
