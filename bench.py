@@ -117,8 +117,11 @@ def dist_setup(n_gpus):
     if ws > 1:
         import torch
         import torch.distributed as td
-        torch.cuda.set_device(local)
-        td.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if torch.cuda.is_available():
+            torch.cuda.set_device(local)
+            td.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:  # no GPU (e.g. the CPU reference arm): plumbing over gloo
+            td.init_process_group("gloo")
         dist = td
     return ws, rank, local, dist
 
@@ -271,6 +274,7 @@ def run_reference(args, ws, rank, dist):
         return
     from oracle import pyoracle
     pyoracle.build()
+    cores = pyoracle.lib().fo_set_threads(os.cpu_count() or 1)  # torchrun sets OMP_NUM_THREADS=1
     sx, sy = 8, 4
     prob = pb.config4(sx=sx, sy=sy)
     o = pyoracle.Oracle(prob)
@@ -293,7 +297,7 @@ def run_reference(args, ws, rank, dist):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded U(0,1) densities, C4 law)",
             "config": {"workload": "C4 FETI-DP F-apply (single direction)", "flush_l2": False},
-            "cpu_baseline": {"value": v, "unit": "GB/s", "cores": os.cpu_count(), "kind": "port",
+            "cpu_baseline": {"value": v, "unit": "GB/s", "cores": cores, "kind": "port",
                              "sample": sample, "cpu_model": cpu_model()},
             "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -359,7 +363,14 @@ def main():
         args.warmup = 3
     ws, rank, local, dist = dist_setup(args.gpus)
     if args.impl == "reference":
+        # The other ranks wait until rank 0 has measured, in a blocking gloo
+        # barrier: exiting early left them polling in the process-group
+        # teardown (and an NCCL barrier would spin a host thread each), which
+        # halved the CPU baseline's throughput.
+        cpu_group = dist.new_group(backend="gloo") if dist is not None else None
         run_reference(args, ws, rank, dist)
+        if dist is not None:
+            dist.barrier(group=cpu_group)
         return
     from paper_2111_11728_b200 import engine
     engine.check(engine.lib().fetigpu_set_device(local))
@@ -468,6 +479,9 @@ def main():
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
         try:
+            from oracle import pyoracle
+            pyoracle.build()
+            pyoracle.lib().fo_set_threads(os.cpu_count() or 1)
             r = cpu_sample()
             cpu = {"value": st["op_bytes"] / r["t_apply_c4_s"] / 1e9, "unit": "GB/s",
                    "cores": r["cores"], "kind": "port", "sample": r["sample"],

@@ -1398,6 +1398,12 @@ extern "C" {
 
 const char* fo_last_error(void) { return g_err.c_str(); }
 void fo_set_refine(int on) { g_refine = on != 0; }
+// host threads for the OpenMP loops (the CPU baseline uses every core even
+// under torchrun, which sets OMP_NUM_THREADS=1); returns the count in force
+int fo_set_threads(int n) {
+  if (n > 0) omp_set_num_threads(n);
+  return omp_get_max_threads();
+}
 
 int fo_create(const fo_problem* p, void** out) {
   *out = nullptr;

@@ -82,6 +82,7 @@ const char* fo_last_error(void);
  * iterative refinement with long-double residuals (affects objects created
  * afterwards for the Phi / Kbar_cc build, and all later applications) */
 void fo_set_refine(int on);
+int fo_set_threads(int n);
 void fo_destroy(void* h);
 /* info[0]=m, [1]=N_s, [2]=local DOFs, [3]=N_c (FETI-DP), [4]=kept coarse rows,
  * [5]=interface rows, [6]=max n_s (touched DOFs per subdomain) */
