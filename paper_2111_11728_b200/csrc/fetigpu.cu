@@ -848,6 +848,24 @@ struct Ctx {
       d_pjcoef.upload(pjcoef, st);
       d_RT.upload(RT, st);
       d_rt_off.upload(rt_off, st);
+      {  // invert the (subdomain, touched DOF) -> rows maps: per row its <= 2 entries
+        std::vector<int2> sr((size_t)2 * std::max(1, su.m), make_int2(-1, 0));
+        std::vector<double2> cc((size_t)std::max(1, su.m), make_double2(0.0, 0.0));
+        for (int s = 0; s < Ns; ++s)
+          for (size_t j = 0; j < su.subs[s].T.size(); ++j)
+            for (int q = 0; q < KRp; ++q) {
+              const size_t e = (ip_off[s] + j) * KRp + q;
+              const int r = prow[e];
+              if (r < 0) continue;
+              const int slot = sr[2 * (size_t)r].x < 0 ? 0 : 1;
+              if (slot == 1 && sr[2 * (size_t)r + 1].x >= 0)
+                fail(FETIGPU_E_STATE, "projector: more than two entries in a dual row");
+              sr[2 * (size_t)r + slot] = make_int2(s, rt_off[s] + (int)j * 3);
+              (slot == 0 ? cc[r].x : cc[r].y) = pjcoef[e];
+            }
+        d_pjrow_sr.upload(sr, st);
+        d_pjrow_c.upload(cc, st);
+      }
       d_H.upload(su.H, st);
       std::vector<double> e(3 * Ns, 0.0);  // e = -R^T f (decomposition.hpp:127)
       for (int s = 0; s < Ns; ++s)
@@ -1372,6 +1390,10 @@ struct Ctx {
   }
 
   // v <- P v for a row-major block (m x ncols, ld = ncols), T-FETI only
+  // single-vector projector finish: per dual row its <= 2 (s, RT offset) / signs
+  DBuf<int2> d_pjrow_sr;
+  DBuf<double2> d_pjrow_c;
+
   // grow-only scratch for the multi-column projector paths: no cudaMalloc /
   // cudaFree (both device-synchronising) inside solver iterations once warm
   DBuf<double> ws_g, ws_h, ws_corr;
@@ -1409,7 +1431,24 @@ struct Ctx {
   }
 
   // corr = P v - v for ncols columns (T-FETI); caller adds
+  // single vector: g = gsign R^T B^T v; h = H g; out = B R h (accumulate: out += B R h)
+  void proj_single(const double* v, double* out, int accumulate, double gsign) {
+    const int nc = 3 * su.Ns;
+    launch_pdl(k_proj_gather, dim3(su.Ns, 1), kThreads, 0, st, (const OpSub*)d_pj.p, (const int*)d_pcrows.p,
+               (const double*)d_pjcoef.p, (const double*)d_RT.p, (const int*)d_rt_off.p, v, su.m, d_g.p, nc, gsign,
+               1);
+    launch_pdl(k_dense_gemv, grid_for((long long)nc * 32), kThreads, 0, st, (const double*)d_H.p, nc,
+               (const double*)d_g.p, d_h.p);
+    launch_pdl(k_proj_rows, grid_for(su.m), kThreads, 0, st, su.m, (const int2*)d_pjrow_sr.p,
+               (const double2*)d_pjrow_c.p, (const double*)d_RT.p, (const double*)d_h.p, out, accumulate);
+    LAUNCH_CHECK();
+  }
+
   void proj_corr(const double* v, int ldv, double* corr, int ldc, int ncols, double gsign = -1.0) {
+    if (ncols == 1 && su.m > 0) {
+      proj_single(v, corr, 0, gsign);
+      return;
+    }
     const int nc = 3 * su.Ns;
     double* gp = d_g.p;
     double* hp = d_h.p;
@@ -1431,6 +1470,10 @@ struct Ctx {
 
   void project(double* v, int ncols, int ld) {
     if (su.method != FETIGPU_TFETI) return;
+    if (ncols == 1 && su.m > 0) {
+      proj_single(v, v, 1, -1.0);
+      return;
+    }
     double* cp = d_v3.p;
     if (ncols > 1) cp = grow(ws_corr, (size_t)su.m * ncols);
     proj_corr(v, ld, cp, su.m, ncols);

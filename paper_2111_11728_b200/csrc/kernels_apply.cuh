@@ -527,6 +527,30 @@ __global__ void k_small_gemm(const double* __restrict__ H, int n, const double* 
 }
 
 // corr[row] += sign_entry * (R_T h_s)_j into a zeroed buffer (2 contributions per row)
+// R_T h_s at one touched DOF (the value k_proj_scatter spreads over its rows)
+__device__ __forceinline__ double proj_rh(const double* __restrict__ R, const double* __restrict__ hs) {
+  return R[0] * hs[0] + R[1] * hs[1] + R[2] * hs[2];
+}
+
+// Single-vector projector finish, row-wise: every dual row has at most two
+// (subdomain, R row, sign) entries, so corr_r = c_plus + c_minus is formed in
+// place (0 + a + b == a + b in either order: bit-identical to the zeroed
+// buffer + atomic scatter it replaces) and either stored (proj_corr) or added
+// to v (project) -- no memset, no atomics, one launch.
+__global__ void k_proj_rows(int m, const int2* __restrict__ ent_sr, const double2* __restrict__ ent_c,
+                            const double* __restrict__ RT, const double* __restrict__ h, double* __restrict__ out,
+                            int accumulate) {
+  pdl_wait();
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < m; r += gridDim.x * blockDim.x) {
+    const int2 sr0 = ent_sr[2 * r], sr1 = ent_sr[2 * r + 1];   // (s, RT offset) or s < 0
+    const double2 c = ent_c[r];
+    double corr = 0.0;
+    if (sr0.x >= 0) corr = c.x * proj_rh(RT + sr0.y, h + 3 * sr0.x);
+    if (sr1.x >= 0) corr = corr + c.y * proj_rh(RT + sr1.y, h + 3 * sr1.x);
+    out[r] = accumulate ? out[r] + corr : corr;
+  }
+}
+
 __global__ void k_proj_scatter(const OpSub* __restrict__ psubs, const int* __restrict__ rows,
                                const double* __restrict__ coefs, const double* __restrict__ RT,
                                const int* __restrict__ rt_off, const double* __restrict__ h, int ldh,
@@ -538,8 +562,9 @@ __global__ void k_proj_scatter(const OpSub* __restrict__ psubs, const int* __res
   const double* hc = h + (size_t)col * ldh + 3 * s;
   const double h0 = hc[0], h1 = hc[1], h2 = hc[2];
   double* cc = corr + (size_t)col * ldc;
+  const double hh[3] = {h0, h1, h2};
   for (int j = threadIdx.x; j < d.ns; j += blockDim.x) {
-    const double v = R[j * 3] * h0 + R[j * 3 + 1] * h1 + R[j * 3 + 2] * h2;
+    const double v = proj_rh(R + j * 3, hh);
     for (int k = 0; k < 3; ++k) {
       const int r = rows[d.map_off + j * 3 + k];
       if (r >= 0) atomicAdd(cc + (size_t)r * rs, coefs[d.map_off + j * 3 + k] * v);
