@@ -1327,26 +1327,24 @@ struct Ctx {
 
   // Zcols: per-subdomain columns, column-major m x N_s (row_major = false)
   // or row-major m x N_s (row_major = true)
-  void apply_precond(const double* r, double* z, double* Zcols, bool row_major = false) {
-    CK(cudaMemsetAsync(z, 0, su.m * 8, st));
+  void apply_precond(const double* r, double* z, double* Zcols, bool row_major = false, bool z_zeroed = false) {
+    if (!z_zeroed) CK(cudaMemsetAsync(z, 0, su.m * 8, st));
     if (Zcols) CK(cudaMemsetAsync(Zcols, 0, (size_t)su.m * su.Ns * 8, st));
     const int ldz = row_major ? 1 : su.m, zrs = row_major ? su.Ns : 1;
     if (pc_sym && !Zcols) {
-      if (KRp == 1)
-        k_sym_gemv_scatter<1, false><<<su.Ns, 256, pc_sym_smem, st>>>(d_pcsym.p, d_pcsymtiles.p, d_pcrows.p,
-                                                                      d_pccoef.p, r, z, nullptr, nullptr);
-      else
-        k_sym_gemv_scatter<3, false><<<su.Ns, 256, pc_sym_smem, st>>>(d_pcsym.p, d_pcsymtiles.p, d_pcrows.p,
-                                                                      d_pccoef.p, r, z, nullptr, nullptr);
+      auto k = KRp == 1 ? k_sym_gemv_scatter<1, false> : k_sym_gemv_scatter<3, false>;
+      launch_pdl(k, su.Ns, 256, pc_sym_smem, st, (const SymSub*)d_pcsym.p, (const double*)d_pcsymtiles.p,
+                 (const int*)d_pcrows.p, (const double*)d_pccoef.p, r, z, (double*)nullptr, (const int*)nullptr,
+                 (const DpSub*)nullptr, (const double*)nullptr, (double*)nullptr, 0, (double*)nullptr, 0, 1,
+                 (const CoarseGather*)nullptr);
       LAUNCH_CHECK();
       return;
     }
-    if (KRp == 1)
-      k_gather_gemv_scatter<1, false><<<dim3(su.Ns, 1, pc_rsplit), kThreads, max_pc_ld * 8, st>>>(
-          d_pc.p, d_pcmat.p, d_pcrows.p, d_pccoef.p, r, z, Zcols, ldz, nullptr, nullptr, 0, 0, zrs);
-    else
-      k_gather_gemv_scatter<3, false><<<dim3(su.Ns, 1, pc_rsplit), kThreads, max_pc_ld * 8, st>>>(
-          d_pc.p, d_pcmat.p, d_pcrows.p, d_pccoef.p, r, z, Zcols, ldz, nullptr, nullptr, 0, 0, zrs);
+    auto k = KRp == 1 ? k_gather_gemv_scatter<1, false> : k_gather_gemv_scatter<3, false>;
+    launch_pdl(k, dim3(su.Ns, 1, pc_rsplit), kThreads, max_pc_ld * 8, st, (const OpSub*)d_pc.p,
+               (const double*)d_pcmat.p, (const int*)d_pcrows.p, (const double*)d_pccoef.p, r, z, Zcols, ldz,
+               (double*)nullptr, (const int*)nullptr, 0, 0, zrs, (const DpSub*)nullptr, (const double*)nullptr,
+               (double*)nullptr);
     LAUNCH_CHECK();
   }
 
@@ -1889,8 +1887,9 @@ int Ctx::solve(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_trace* 
     dots({{w.p, q.p}, {w.p, r.p}}, &sc.p->delta);
     if (tf) proj_corr(q.p, m, corr.p, m, 1);
     launch_pdl(k_pcg_update, grid_for(m), kThreads, 0, st, m, sc.p, fo ? 1 : 0, (const double*)w.p,
-               (const double*)q.p, (const double*)(tf ? corr.p : nullptr), lam.p, r.p);
-    precond_projected(r.p, z.p, nullptr);
+               (const double*)q.p, (const double*)(tf ? corr.p : nullptr), lam.p, r.p, z.p);
+    apply_precond(r.p, z.p, nullptr, false, /*z_zeroed=*/true);
+    project(z.p, 1, m);
     dots({{r.p, z.p}, {r.p, r.p}, {z.p, z.p}}, &sc.p->rz);
     if (fo) {
       launch_pdl(k_fo_store2, grid_for(m), kThreads, 0, st, m, (const Scal*)sc.p, (const int*)cnt.p,

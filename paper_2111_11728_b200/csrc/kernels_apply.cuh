@@ -848,8 +848,10 @@ __global__ void k_add(int n, const double* __restrict__ c, double* __restrict__ 
 // alpha from device scalars; lambda += alpha w; r -= alpha * Pq  (Pq = q + corr or q)
 __global__ void k_pcg_update(int n, Scal* sc, int fo, const double* __restrict__ w,
                              const double* __restrict__ q, const double* __restrict__ corr,
-                             double* __restrict__ lambda, double* __restrict__ r) {
+                             double* __restrict__ lambda, double* __restrict__ r, double* __restrict__ zero_z) {
   pdl_wait();
+  if (zero_z)  // the preconditioner output of this iteration, zeroed here instead of a memset node
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) zero_z[i] = 0.0;
   if (!(sc->delta > 0.0)) {  // breakdown: leave lambda, r untouched
     if (blockIdx.x == 0 && threadIdx.x == 0) sc->breakdown = 1.0;
     return;
