@@ -16,13 +16,15 @@ Each case draws:
 
 GPU and oracle see identical inputs.  The accuracy yardstick is the
 problem's own sensitivity to last-bit rounding: a third oracle runs on
-densities perturbed by ~2^-50 relative noise, and the GPU's distance to the
+densities perturbed by 2^-47..2^-45 relative noise, and the GPU's distance to the
 oracle must stay within SENS_FACTOR x that perturbed oracle's distance (plus
 a small floor).  The refined-oracle policy of test_gpu_parity.py is not used
 here: its reference shares the oracle's own K assembly, so on anisotropic
 elements or non-unit moduli it favours the oracle by the conditioning-amplified
 assembly rounding, which an ND-Schur assembly cannot reproduce bit for bit.
 FO and RRS iteration counts must agree within +-1."""
+import os
+
 import numpy as np
 import pytest
 
@@ -30,7 +32,7 @@ from paper_2111_11728_b200 import problems as pb
 
 pytestmark = pytest.mark.gpu
 SENS_FACTOR = 100.0
-SEEDS = list(range(64))
+SEEDS = list(range(int(os.environ.get("FETIGPU_FUZZ_SEEDS", "64"))))  # longer sweeps: raise the count
 
 
 def random_problem(seed):
@@ -75,7 +77,7 @@ def rel(a, b):
     return np.linalg.norm(np.asarray(a) - np.asarray(b)) / (nb if nb > 0 else 1.0)
 
 
-def close(got, dbl, pert, what, floor=1e-12):
+def close(got, dbl, pert, what, floor=5e-11):
     """|got - dbl| within SENS_FACTOR x the rounding sensitivity |pert - dbl|."""
     eg, es = rel(got, dbl), rel(pert, dbl)
     assert eg <= max(SENS_FACTOR * es, floor), (what, eg, es)
@@ -83,7 +85,8 @@ def close(got, dbl, pert, what, floor=1e-12):
 
 def perturbed(prob, seed):
     rng = np.random.default_rng(10_000 + seed)
-    d = prob.densities * (1.0 - rng.uniform(0.0, 2.0 ** -50, prob.densities.shape))
+    # a few ulps (2^-47..2^-45 relative): large enough never to round away
+    d = prob.densities * (1.0 - rng.uniform(2.0 ** -47, 2.0 ** -45, prob.densities.shape))
     return prob.replace(densities=d)
 
 
