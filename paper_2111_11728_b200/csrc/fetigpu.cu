@@ -1216,9 +1216,26 @@ struct Ctx {
   }
 
   // -------------------------------------------------------- operators --
-  void apply_F(const double* x, double* y, int ncols, int ldx, int ldy) {
+  // y_zeroed: the caller already zeroed y (T-FETI scatters into it); lets the
+  // solver loop drop the memset node and chain the GEMV with PDL
+  void apply_F(const double* x, double* y, int ncols, int ldx, int ldy, bool y_zeroed = false) {
     const int Ns = su.Ns;
     if (su.method == FETIGPU_TFETI) {
+      if (ncols == 1 && y_zeroed) {
+        if (use_sym)
+          launch_pdl(k_sym_gemv_scatter<3, false>, Ns, 256, sym_smem, st, (const SymSub*)d_sym.p,
+                     (const double*)d_symtiles.p, (const int*)d_oprows.p, (const double*)d_opcoef_apply.p, x, y,
+                     (double*)nullptr, (const int*)nullptr, (const DpSub*)nullptr, (const double*)nullptr,
+                     (double*)nullptr, 0, (double*)nullptr, 0, 1, (const CoarseGather*)nullptr);
+        else
+          launch_pdl(k_gather_gemv_scatter<3, false>, dim3(Ns, 1, rsplit), kThreads, max_ld * 8, st,
+                     (const OpSub*)d_op.p, (const double*)d_opmat.p, (const int*)d_oprows.p,
+                     (const double*)d_opcoef_apply.p, x, y, (double*)nullptr, 0, (double*)nullptr,
+                     (const int*)nullptr, ldx, ldy, 1, (const DpSub*)nullptr, (const double*)nullptr,
+                     (double*)nullptr);
+        LAUNCH_CHECK();
+        return;
+      }
       for (int c = 0; c < ncols; ++c) CK(cudaMemsetAsync(y + (size_t)c * ldy, 0, su.m * 8, st));
       if (use_sym) {
         for (int c = 0; c < ncols; ++c)
@@ -1880,10 +1897,11 @@ int Ctx::solve(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_trace* 
   };
   push(eps0, 1);
   CK(cudaMemcpyAsync(w.p, z.p, m * 8, cudaMemcpyDeviceToDevice, st));
+  CK(cudaMemsetAsync(q.p, 0, m * 8, st));  // then re-zeroed each iteration by its last reader of q
   const double target = o.rel ? o.tol * eps0 : o.tol;
   // one PCG / FO iteration (everything on the stream, no host work)
   auto body = [&](bool readback) {
-    apply_F(w.p, q.p, 1, m, m);
+    apply_F(w.p, q.p, 1, m, m, /*y_zeroed=*/true);
     dots({{w.p, q.p}, {w.p, r.p}}, &sc.p->delta);
     if (tf) proj_corr(q.p, m, corr.p, m, 1);
     launch_pdl(k_pcg_update, grid_for(m), kThreads, 0, st, m, sc.p, fo ? 1 : 0, (const double*)w.p,
@@ -1893,7 +1911,7 @@ int Ctx::solve(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_trace* 
     dots({{r.p, z.p}, {r.p, r.p}, {z.p, z.p}}, &sc.p->rz);
     if (fo) {
       launch_pdl(k_fo_store2, grid_for(m), kThreads, 0, st, m, (const Scal*)sc.p, (const int*)cnt.p,
-                 (const double*)w.p, (const double*)q.p, Wst.p, Qst.p);
+                 (const double*)w.p, q.p, Wst.p, Qst.p);
       launch_pdl(k_inc, 1, 1, 0, st, cnt.p);
       CK(cudaMemcpyAsync(w.p, z.p, m * 8, cudaMemcpyDeviceToDevice, st));
       for (int pss = 0; pss < passes; ++pss) {
@@ -1905,7 +1923,7 @@ int Ctx::solve(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_trace* 
                    (const double*)psi.p, w.p);
       }
     } else {
-      launch_pdl(k_cg_dir2, grid_for(m), kThreads, 0, st, m, sc.p, (const double*)z.p, w.p);
+      launch_pdl(k_cg_dir2, grid_for(m), kThreads, 0, st, m, sc.p, (const double*)z.p, w.p, q.p);
       launch_pdl(k_shift_rz, 1, 1, 0, st, sc.p);
     }
     if (readback) CK(cudaMemcpyAsync(hs, sc.p, sizeof(Scal), cudaMemcpyDeviceToHost, st));

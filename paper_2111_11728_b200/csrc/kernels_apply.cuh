@@ -777,8 +777,9 @@ __global__ void k_fo_psi_sum(const int* __restrict__ cnt, int S, const double* _
   }
 }
 
+// also re-zeroes q (last reader this iteration) for the next apply's scatter
 __global__ void k_fo_store2(int n, const Scal* sc, const int* __restrict__ cnt,
-                            const double* __restrict__ w, const double* __restrict__ q,
+                            const double* __restrict__ w, double* __restrict__ q,
                             double* __restrict__ Wst, double* __restrict__ Qst) {
   pdl_wait();
   const double inv = 1.0 / sqrt(sc->delta);
@@ -786,16 +787,21 @@ __global__ void k_fo_store2(int n, const Scal* sc, const int* __restrict__ cnt,
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     Wst[(size_t)j * n + i] = w[i] * inv;
     Qst[(size_t)j * n + i] = q[i] * inv;
+    q[i] = 0.0;
   }
 }
 __global__ void k_inc(int* cnt) {
   pdl_wait(); *cnt += 1; }
 // w = z + beta w with beta = rz / rz_old from device scalars; then rz_old = rz
-__global__ void k_cg_dir2(int n, Scal* sc, const double* __restrict__ z, double* __restrict__ w) {
+// (zero_q: re-zeroed for the next apply's scatter; q is dead after k_pcg_update)
+__global__ void k_cg_dir2(int n, Scal* sc, const double* __restrict__ z, double* __restrict__ w,
+                          double* __restrict__ zero_q) {
   pdl_wait();
   const double beta = sc->rz / sc->rz_old;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     w[i] = fma(beta, w[i], z[i]);
+    if (zero_q) zero_q[i] = 0.0;
+  }
 }
 __global__ void k_shift_rz(Scal* sc) {
   pdl_wait(); sc->rz_old = sc->rz; }
