@@ -1,5 +1,6 @@
 """Full-size GPU vs oracle solve parity for one config (one-off evidence run).
-python tools/parity_full.py C5 > profiles/r01_parity_C5.json"""
+python tools/parity_full.py C5 > profiles/r01_parity_C5.json
+python tools/parity_full.py C4 400 1e-6 1   (max_it, tol, directions override: FO)"""
 import json
 import os
 import sys
@@ -15,6 +16,8 @@ name = sys.argv[1]
 max_it = int(sys.argv[2]) if len(sys.argv) > 2 else 200
 tol = float(sys.argv[3]) if len(sys.argv) > 3 else 1e-6
 prob = pb.CONFIGS[name]()
+if len(sys.argv) > 4:  # directions override (C4's RRS exceeds one GPU: run it with FO / single)
+    prob = prob.replace(directions=int(sys.argv[4]))
 out = {"config": name, "method": prob.method, "directions": prob.directions, "tol": tol,
        "host_cores": os.cpu_count()}
 g = engine.FetiSystem(prob)
@@ -44,13 +47,15 @@ out["u_rel_energy_gpu_vs_oracle"] = float(np.sqrt(max(num, 0.0) / den))
 # L2 restricted to nodes that touch a solid element (rho > 0.5)
 n = prob.n
 mask = np.zeros((o.n_sub, o.local_dofs), bool)
-for s_ in range(o.n_sub):
-    rho = prob.densities[prob.module_type[s_]]
-    for ey in range(n):
-        for ex in range(n):
-            if rho[ey, ex] > 0.5:
-                for a in (ey * (n + 1) + ex, ey * (n + 1) + ex + 1, (ey + 1) * (n + 1) + ex, (ey + 1) * (n + 1) + ex + 1):
-                    mask[s_, 2 * a:2 * a + 2] = True
+for d in range(prob.densities.shape[0]):  # per design: nodes touching a solid element
+    solid = prob.densities[d] > 0.5
+    node = np.zeros((n + 1, n + 1), bool)
+    node[:-1, :-1] |= solid
+    node[:-1, 1:] |= solid
+    node[1:, :-1] |= solid
+    node[1:, 1:] |= solid
+    dof = np.repeat(node.reshape(-1), 2)
+    mask[np.asarray(prob.module_type) == d] = dof
 out["u_rel_l2_solid_nodes"] = float(np.linalg.norm((ug - uo)[mask]) / np.linalg.norm(uo[mask]))
 out["iteration_diff"] = tg["iterations"] - to["iterations"]
 print(json.dumps(out))
