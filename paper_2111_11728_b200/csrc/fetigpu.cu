@@ -8,6 +8,7 @@
 #include <cublas_v2.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -2042,13 +2043,15 @@ static bool pivchol_cluster_try(double* A, int n, double tol, int* perm, int* ra
   const int R = (n + CL - 1) / CL;
   const size_t smem = ((size_t)R * n + 3 * (size_t)n) * 8;
   if (smem > 225 * 1024) return false;
-  static int ok = -1;  // per instantiation: attributes set and cluster schedulable
-  if (ok < 0) {
-    ok = 0;
+  // per instantiation: attributes set and cluster schedulable (-1 unknown).
+  // Atomic: contexts may be driven from several host threads; a duplicated
+  // first probe is harmless (same attribute values).
+  static std::atomic<int> ok{-1};
+  if (ok.load() < 0) {
     if (cudaFuncSetAttribute(k_pivchol_cl<CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, 225 * 1024) !=
-        cudaSuccess) { cudaGetLastError(); return false; }
+        cudaSuccess) { cudaGetLastError(); ok.store(0); return false; }
     if (CL > 8 && cudaFuncSetAttribute(k_pivchol_cl<CL>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
-                      cudaSuccess) { cudaGetLastError(); return false; }
+                      cudaSuccess) { cudaGetLastError(); ok.store(0); return false; }
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute at[1];
     cfg.gridDim = dim3(CL);
@@ -2065,9 +2068,9 @@ static bool pivchol_cluster_try(double* A, int n, double tol, int* perm, int* ra
       cudaGetLastError();
       nclusters = 0;
     }
-    ok = nclusters > 0 ? 1 : 0;
+    ok.store(nclusters > 0 ? 1 : 0);
   }
-  if (!ok) return false;
+  if (!ok.load()) return false;
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute at[1];
   cfg.gridDim = dim3(CL);
@@ -2100,8 +2103,8 @@ static bool launch_pivchol_cluster(double* A, int n, double tol, int* perm, int*
 static void launch_pivchol(double* A, int n, double tol, int* perm, int* rank, int* status, int* ctl, double* gx,
                            cudaStream_t st) {
   if (launch_pivchol_cluster(A, n, tol, perm, rank, status, gx, st)) return;
-  static int coop_blocks = 0;
-  if (!coop_blocks) {
+  static std::atomic<int> coop_blocks{0};  // (see pivchol_cluster_try: benign duplicated init)
+  if (!coop_blocks.load()) {
     int dev = 0, sms = 0, per_sm = 0;
     CK(cudaGetDevice(&dev));
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -2109,7 +2112,7 @@ static void launch_pivchol(double* A, int n, double tol, int* perm, int* rank, i
     coop_blocks = sms * std::max(1, std::min(per_sm, 2));
   }
   void* args[] = {&A, &n, &tol, &perm, &rank, &status, &ctl};
-  CK(cudaLaunchCooperativeKernel((void*)k_pivchol_coop, coop_blocks, 512, args, 0, st));
+  CK(cudaLaunchCooperativeKernel((void*)k_pivchol_coop, dim3(coop_blocks.load()), dim3(512), args, 0, st));
 }
 
 // Rank-Revealing Simultaneous FETI, Alg. 1 of PAPER.md:302-351:

@@ -422,3 +422,37 @@ def test_host_pipelined_apply(oracle_mod, monkeypatch):
     o = oracle_mod.Oracle(prob)
     assert rel(y_host, o.apply_F(x)) <= 1e-8
     g.close()
+
+
+def test_concurrent_contexts_from_two_threads():
+    """SURVEY 8b threading contract: a context owns its stream, distinct
+    contexts may be driven from different host threads, and results do not
+    depend on concurrency (fixed reduction orders).  Two FO solves and two
+    applies run at the same time from two threads must be bit-identical to
+    the same calls made one after the other."""
+    import threading
+    from paper_2111_11728_b200 import engine
+    probs = [CASES["C2s"](), CASES["C3tf_s"]()]
+    sys_ = [engine.FetiSystem(p) for p in probs]
+    xs = [np.random.default_rng(40 + i).standard_normal(g.m) for i, g in enumerate(sys_)]
+    ref = [(g.solve(tol=1e-8, max_it=500, directions=1)[0], g.apply_F(x)) for g, x in zip(sys_, xs)]
+    out = [None, None]
+
+    def work(i):
+        g, x = sys_[i], xs[i]
+        res = []
+        for _ in range(3):
+            res.append((g.solve(tol=1e-8, max_it=500, directions=1)[0], g.apply_F(x)))
+        out[i] = res
+
+    th = [threading.Thread(target=work, args=(i,)) for i in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for i in range(2):
+        for lam, y in out[i]:
+            assert np.array_equal(lam, ref[i][0])
+            assert np.array_equal(y, ref[i][1])
+    for g in sys_:
+        g.close()
