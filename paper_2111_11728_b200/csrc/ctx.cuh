@@ -1,0 +1,290 @@
+// ctx.cuh -- the per-problem context: device-resident operators and their metadata.
+// Method bodies: ctx_build.cuh (K1-K3, coarse), ctx_ops.cuh (K4/K5, projector,
+// preconditioner, rhs, recovery), solve_pcg.cuh, solve_rrs.cuh.
+// Part of the libfetigpu unity build (fetigpu.cu includes it); namespace fg.
+#pragma once
+#include "runtime.cuh"
+#include "setup.hpp"
+#include "kernels_apply.cuh"
+#include "kernels_build.cuh"
+#include "kernels_dmma.cuh"
+
+namespace fg {
+
+struct Ctx {
+  Setup su;
+  Scratch scratch;
+  cudaStream_t st = nullptr;
+  cublasHandle_t cb = nullptr;
+  bool built = false;
+  DBuf<int> d_status;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr;
+  double build_ms = 0, nd_ms = 0, slot_ms = 0, coarse_ms = 0;
+  bool keep_factors = true;
+
+  // ND tree
+  DBuf<NdDev> d_nodes;
+  DBuf<int> d_elem_ids, d_emap, d_cmaps, d_nd_dofs, d_topdown, d_design;
+  DBuf<double> d_dens, d_S, d_ndfac;
+  // operator (F_s) per subdomain
+  int KR = 1;
+  DBuf<OpSub> d_op;
+  DBuf<double> d_opmat, d_opcoef, d_opfac;
+  // coefficients used with the explicit operators: all ones once the +-1
+  // constraint signs are folded into F_s / A_bc (FETI-DP), else d_opcoef
+  DBuf<double> d_opcoef_apply;
+  bool folded = false;
+  // symmetric-packed operator tiles for the GEMV (used when rsplit == 1)
+  bool use_sym = false;
+  DBuf<double> d_symtiles;
+  DBuf<SymSub> d_sym;
+  double sym_bytes = 0;
+  int sym_smem = 0;
+  bool pc_sym = false;
+  DBuf<double> d_pcsymtiles;
+  DBuf<SymSub> d_pcsym;
+  int pc_sym_smem = 0;
+  std::vector<std::vector<double>> slot_sign;
+  DBuf<int> d_oprows, d_slot_of, d_fac_ne, d_top_pos, d_top_off;
+  DBuf<long long> d_fac_off;
+  std::vector<int> op_ns, op_ld;
+  std::vector<long long> op_moff, op_foff;
+  int max_ld = 0, max_ne = 0;
+  int rsplit = 1;     // CTAs per subdomain in the GEMV kernels (few subdomains)
+  int pc_rsplit = 1;
+  // slot src/ext lists
+  DBuf<int> d_op_src, d_op_ext, d_op_src_off, d_op_ext_off;
+  // preconditioner
+  int KRp = 1;
+  DBuf<OpSub> d_pc;
+  DBuf<double> d_pcmat, d_pccoef;
+  DBuf<int> d_pcrows;
+  int max_pc_ld = 0;
+  // projector (T-FETI)
+  DBuf<OpSub> d_pj;
+  DBuf<double> d_pjcoef, d_RT, d_H, d_e;
+  DBuf<int> d_rt_off;
+  // FETI-DP
+  DBuf<DpSub> d_dp;
+  DBuf<double> d_abc, d_kccs, d_Kinv, d_vbuf, d_tbuf, d_fbar_loc, d_fbar;
+  DBuf<int> d_cmap, d_voff, d_optr, d_oidx;
+  // boundary data for rhs / recovery
+  DBuf<double> d_fb, d_gD;
+  DBuf<int> d_D, d_D_off, d_D_cnt, d_c_pos, d_c_off, d_xoff;
+  DBuf<double> d_xb;
+  // scratch vectors
+  DBuf<double> d_v1, d_v2, d_v3, d_g, d_h, d_partial;
+  DBuf<double> d_d, d_lam0;
+  DBuf<unsigned int> d_counter, d_counter2;
+  bool have_rhs = false;
+  // stats
+  double op_bytes = 0, op_flops = 0, main_bytes = 0;
+  // grow-only staging buffers of the host-pointer entry points
+  DBuf<double> stage_x, stage_y;
+  void stage(size_t n) {
+    if (stage_x.n < n) { stage_x.alloc(n); stage_y.alloc(n); }
+  }
+
+  // FETI-DP coarse inverse in symmetric-packed 32x32 tiles (+ per-tile partials)
+  DBuf<double> d_kinv_tiles, d_crow, d_ccol, d_gc;
+  DBuf<unsigned int> d_gcnt;
+  DBuf<CoarseGather> d_cgather;
+  int kinv_nb = 0, csym_grid = 1;
+  bool use_csym = false;  // packed inverse only where the dense one leaves L2 (N_c > 2048)
+
+  // Host-buffer F-apply pipeline (fetigpu_apply_F with host pointers, FETI-DP
+  // on the symmetric path): lambda goes over PCIe in kPipe row-prefix chunks on
+  // a copy stream; the subdomains of chunk c (rows < pipe_need[c]) start their
+  // phase-1 GEMV on their own stream as soon as that prefix has landed, so the
+  // H2D copy overlaps the operator stream and the chunks fill the GPU together.
+  static constexpr int kPipe = 8;
+  cudaStream_t pipe_st[kPipe] = {}, pipe_cp = nullptr;
+  cudaEvent_t pipe_in[kPipe] = {}, pipe_done[kPipe] = {}, pipe_start = nullptr;
+  int pipe_s0[kPipe + 1] = {}, pipe_need[kPipe] = {};
+  bool pipe_ready = false;
+  std::vector<int> sub_maxrow;  // per subdomain: largest dual row it touches (-1: none)
+
+  ~Ctx() {
+    for (auto& e : pipe_in) if (e) cudaEventDestroy(e);
+    for (auto& e : pipe_done) if (e) cudaEventDestroy(e);
+    if (pipe_start) cudaEventDestroy(pipe_start);
+    for (auto& q : pipe_st) if (q) cudaStreamDestroy(q);
+    if (pipe_cp) cudaStreamDestroy(pipe_cp);
+    if (cb) cublasDestroy(cb);
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev1) cudaEventDestroy(ev1);
+    if (ev2) cudaEventDestroy(ev2);
+    if (st) cudaStreamDestroy(st);
+  }
+
+  void check_status() {
+    int h = 0;
+    CK(cudaMemcpyAsync(&h, d_status.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (h != 0) {
+      CK(cudaMemsetAsync(d_status.p, 0, sizeof(int), st));
+      fail(h, "device factorization failed (nonpositive pivot)");
+    }
+  }
+
+  void init_device();
+
+  double elapsed(cudaEvent_t a, cudaEvent_t b) {
+    float ms = 0;
+    CK(cudaEventSynchronize(b));
+    CK(cudaEventElapsedTime(&ms, a, b));
+    return ms;
+  }
+
+  // ------------------------------------------------------------ build --
+  void eliminate(const std::vector<FrontDesc>& fds, double* base);
+
+  // batched blocked partial Cholesky over all frontals in `fs` (device copy `d`)
+  void bpc(const FrontDesc* d, const std::vector<FrontDesc>& fs, double* base);
+
+  void build_nd();
+
+  // batched slot processing: assemble [[S[src,src],E],[E^T,0]], eliminate,
+  // extract; processed in chunks bounded by a workspace budget
+  struct SlotOut {
+    std::vector<long long> mat_off;
+    std::vector<int> mat_ld;
+    std::vector<long long> abc_off, kcc_off, fac_off;
+  };
+  void run_slots(const std::vector<SlotFront>& slots, const SlotOut& out, double* mats, double sign,
+                 bool nc_first, double* abc, double* kcc, double* fac, int errcode);
+
+  PhaseTimer ptimer;
+  void build_ops();
+
+  void build_coarse(const SlotOut& so, const std::vector<int>& osub, const std::vector<int>& oloc);
+
+  // u = Kbar^{-1} (sum_s B_c^T t_s) into d_h (stages A + B on the packed inverse)
+  // g_ready: phase 1 already formed g in d_gc (fused gather of the symmetric
+  // GEMV); otherwise gather it here
+  // zero_y: output still to be zeroed (the gather kernel does it when it runs)
+  void coarse_solve_packed(bool g_ready, double* zero_y = nullptr);
+  // phase 2: y = sum_s B_s (v_s + A''_s u_s)
+  void launch_phase2_csym(double* y) {
+    launch_pdl(k_dp_phase2, su.Ns, kThreads, 0, st, (const OpSub*)d_op.p, (const DpSub*)d_dp.p,
+               (const int*)d_oprows.p, (const double*)d_opcoef_apply.p, (const double*)d_abc.p,
+               (const int*)d_cmap.p, (const double*)d_h.p, (const double*)d_vbuf.p, y, 1.0);
+    LAUNCH_CHECK();
+  }
+
+  void launch_kcc_assemble(const int* optr, const int* osub, const int* oloc, const long long* kco,
+                           const int* ncs, const double* kccs, int Nc, double* K);
+  void launch_identity(double* X, int n);
+  void launch_symmetrize(double* A, int n);
+
+  void build();
+
+  // -------------------------------------------------------- operators --
+  // y_zeroed: the caller already zeroed y (T-FETI scatters into it); lets the
+  // solver loop drop the memset node and chain the GEMV with PDL
+  void apply_F(const double* x, double* y, int ncols, int ldx, int ldy, bool y_zeroed = false);
+
+  void setup_pipe();
+
+  // y = F x with x, y in (pinned) host memory; the result is identical to
+  // the device path (same kernels per subdomain, same phase-2 order)
+  void apply_F_host(const double* xh, double* yh);
+
+  // Zcols: per-subdomain columns, column-major m x N_s (row_major = false)
+  // or row-major m x N_s (row_major = true)
+  void apply_precond(const double* r, double* z, double* Zcols, bool row_major = false, bool z_zeroed = false);
+
+  // ---- K5: Q = F W for k columns, row-major blocks (W(i,c) = W[i*ldw + c])
+  DBuf<double> blk_t, blk_T, blk_U;
+  void apply_F_block(const double* W, int ldw, double* Q, int ldq, int k);
+
+  // single-vector projector finish: per dual row its <= 2 (s, RT offset) / signs
+  DBuf<int2> d_pjrow_sr;
+  DBuf<double2> d_pjrow_c;
+
+  // grow-only scratch for the multi-column projector paths: no cudaMalloc /
+  // cudaFree (both device-synchronising) inside solver iterations once warm
+  DBuf<double> ws_g, ws_h, ws_corr;
+  static double* grow(DBuf<double>& b, size_t n) {
+    if (b.n < n) b.alloc(n);
+    return b.p;
+  }
+
+  // v <- P v for a row-major block (m x ncols, ld = ncols), T-FETI only
+  void project_rm(double* v, int ncols);
+
+  // h = H g for ncols columns of length 3N_s (H symmetric, column-major)
+  void small_gemm(const double* g, double* h, int ncols) {
+    const int nc = 3 * su.Ns;
+    if (ncols == 1) {
+      k_dense_gemv<<<grid_for((long long)nc * 32), kThreads, 0, st>>>(d_H.p, nc, g, h);
+    } else {
+      const double one = 1.0, zero = 0.0;
+      CB(cublasDgemm(cb, CUBLAS_OP_N, CUBLAS_OP_N, nc, ncols, nc, &one, d_H.p, nc, g, nc, &zero, h, nc));
+    }
+    LAUNCH_CHECK();
+  }
+
+  // single vector: g = gsign R^T B^T v; h = H g; out = B R h (accumulate: out += B R h)
+  void proj_single(const double* v, double* out, int accumulate, double gsign) {
+    const int nc = 3 * su.Ns;
+    launch_pdl(k_proj_gather, dim3(su.Ns, 1), kThreads, 0, st, (const OpSub*)d_pj.p, (const int*)d_pcrows.p,
+               (const double*)d_pjcoef.p, (const double*)d_RT.p, (const int*)d_rt_off.p, v, su.m, d_g.p, nc, gsign,
+               1);
+    launch_pdl(k_dense_gemv, grid_for((long long)nc * 32), kThreads, 0, st, (const double*)d_H.p, nc,
+               (const double*)d_g.p, d_h.p);
+    launch_pdl(k_proj_rows, grid_for(su.m), kThreads, 0, st, su.m, (const int2*)d_pjrow_sr.p,
+               (const double2*)d_pjrow_c.p, (const double*)d_RT.p, (const double*)d_h.p, out, accumulate);
+    LAUNCH_CHECK();
+  }
+
+  // corr = P v - v for ncols columns (T-FETI); caller adds
+  void proj_corr(const double* v, int ldv, double* corr, int ldc, int ncols, double gsign = -1.0);
+
+  void project(double* v, int ncols, int ld) {
+    if (su.method != FETIGPU_TFETI) return;
+    if (ncols == 1 && su.m > 0) {
+      proj_single(v, v, 1, -1.0);
+      return;
+    }
+    double* cp = d_v3.p;
+    if (ncols > 1) cp = grow(ws_corr, (size_t)su.m * ncols);
+    proj_corr(v, ld, cp, su.m, ncols);
+    k_add<<<dim3(grid_for(su.m), ncols), kThreads, 0, st>>>(su.m, cp, v, su.m, ld);
+    LAUNCH_CHECK();
+  }
+
+  // per-subdomain boundary rhs b = (f - B^T lambda)[src] - S[src,D] gD - S[src,c] u_c
+  void launch_bnd_rhs(const double* lambda, const double* uc);
+  void launch_bnd_u(const double* uc, double* ub_all);
+  void launch_dp_fbar();
+  void launch_rhs_scatter(double* out);
+  void launch_add_rigid(double* u, const double* alpha);
+  void launch_scatter_perim(const double* ub_all, double* u);
+
+  void rhs();
+
+  void recover(const double* lambda_dev, double* u_dev);
+
+  // ------------------------------------------------------------ engine --
+  void dots(std::initializer_list<std::pair<const double*, const double*>> pairs, double* out) {
+    DotArgs a{};
+    int k = 0;
+    for (auto& p : pairs) { a.a[k] = p.first; a.b[k] = p.second; ++k; }
+    a.npairs = k;
+    a.n = su.m;
+    const int nblk = std::max(1, std::min(kDotBlocks, (su.m + 1023) / 1024));
+    launch_pdl(k_dot_fused, nblk, kThreads, 0, st, a, d_partial.p, d_counter.p, out);
+    LAUNCH_CHECK();
+  }
+
+  void precond_projected(const double* r, double* z, double* Zcols) {
+    apply_precond(r, z, Zcols);
+    project(z, 1, su.m);
+  }
+
+  int solve(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_trace* tr);
+  int solve_rrs(const fetigpu_solve_opts& o, double* lam, fetigpu_trace* tr);
+};
+
+}  // namespace fg

@@ -1,0 +1,511 @@
+// ctx_ops.cuh -- operator applications: F (K4 single column, K5 block, host-pipelined),
+// preconditioner, T-FETI projector, right-hand side and primal recovery.
+// Part of the libfetigpu unity build (fetigpu.cu includes it); namespace fg.
+#pragma once
+#include "ctx.cuh"
+
+namespace fg {
+
+// b_i = p[src_i] - sum_D S[src_i, D] g - sum_c S[src_i, c] u_c  with
+// p = f - B_s^T lambda on the perimeter
+__global__ void k_bnd_rhs(int nb, const double* __restrict__ fb, const double* __restrict__ lambda,
+                          const OpSub* __restrict__ ops, const int* __restrict__ rows,
+                          const double* __restrict__ coefs, int KR, const int* __restrict__ top_pos,
+                          const int* __restrict__ top_off, const int* __restrict__ D,
+                          const int* __restrict__ D_off, const int* __restrict__ D_cnt,
+                          const double* __restrict__ gD, const int* __restrict__ c_pos,
+                          const int* __restrict__ c_off, const int* __restrict__ cmap,
+                          const DpSub* __restrict__ dps, const double* __restrict__ uc,
+                          const double* __restrict__ S, const int* __restrict__ design,
+                          const int* __restrict__ slot_of, const int* __restrict__ src,
+                          const int* __restrict__ src_off, const int* __restrict__ nes,
+                          double* __restrict__ xb, const int* __restrict__ xoff) {
+  extern __shared__ double p[];
+  const int s = blockIdx.x;
+  for (int i = threadIdx.x; i < nb; i += blockDim.x) p[i] = fb[(size_t)s * nb + i];
+  __syncthreads();
+  if (lambda) {
+    const OpSub d = ops[s];
+    for (int a = threadIdx.x; a < d.ns; a += blockDim.x) {
+      double v = 0.0;
+      for (int k = 0; k < KR; ++k) {
+        const int r = rows[d.map_off + a * KR + k];
+        if (r >= 0) v += coefs[d.map_off + a * KR + k] * lambda[r];
+      }
+      p[top_pos[top_off[s] + a]] -= v;
+    }
+    __syncthreads();
+  }
+  const int sl = slot_of[s];
+  const int ne = nes[sl];
+  const int* sr = src + src_off[sl];
+  const double* Sd = S + (size_t)design[s] * nb * nb;
+  const int nD = D_cnt[s];
+  const int nc = (uc && dps) ? dps[s].nc : 0;
+  for (int i = threadIdx.x; i < ne; i += blockDim.x) {
+    const int pi = sr[i];
+    double v = p[pi];
+    for (int k = 0; k < nD; ++k) v -= Sd[(size_t)D[D_off[s] + k] * nb + pi] * gD[D_off[s] + k];
+    for (int k = 0; k < nc; ++k)
+      v -= Sd[(size_t)c_pos[c_off[s] + k] * nb + pi] * uc[cmap[dps[s].cmap_off + k]];
+    xb[xoff[s] + i] = v;
+  }
+}
+void Ctx::launch_bnd_rhs(const double* lambda, const double* uc) {
+  k_bnd_rhs<<<su.Ns, kThreads, su.nb * 8, st>>>(
+      su.nb, d_fb.p, lambda, d_op.p, d_oprows.p, d_opcoef.p, KR, d_top_pos.p, d_top_off.p, d_D.p, d_D_off.p,
+      d_D_cnt.p, d_gD.p, d_c_pos.p, d_c_off.p, d_cmap.p, su.method == FETIGPU_FETIDP ? d_dp.p : nullptr, uc,
+      d_S.p, d_design.p, d_slot_of.p, d_op_src.p, d_op_src_off.p, d_fac_ne.p, d_xb.p, d_xoff.p);
+  LAUNCH_CHECK();
+}
+
+// d[row] += sign * x[ext[a]] over the operator support (B K^+ f)
+__global__ void k_rhs_scatter(const OpSub* __restrict__ ops, const int* __restrict__ rows,
+                              const double* __restrict__ coefs, int KR, const int* __restrict__ slot_of,
+                              const int* __restrict__ ext, const int* __restrict__ ext_off,
+                              const double* __restrict__ xb, const int* __restrict__ xoff,
+                              double* __restrict__ out) {
+  const int s = blockIdx.x;
+  const OpSub d = ops[s];
+  const int* e = ext + ext_off[slot_of[s]];
+  for (int a = threadIdx.x; a < d.ns; a += blockDim.x) {
+    const double v = xb[xoff[s] + e[a]];
+    for (int k = 0; k < KR; ++k) {
+      const int r = rows[d.map_off + a * KR + k];
+      if (r >= 0) atomicAdd(out + r, coefs[d.map_off + a * KR + k] * v);
+    }
+  }
+}
+void Ctx::launch_rhs_scatter(double* out) {
+  k_rhs_scatter<<<su.Ns, kThreads, 0, st>>>(d_op.p, d_oprows.p, d_opcoef.p, KR, d_slot_of.p, d_op_ext.p,
+                                            d_op_ext_off.p, d_xb.p, d_xoff.p, out);
+  LAUNCH_CHECK();
+}
+
+// fbar_c^s = f_c - S[c,D] g - S[c, r] x   (x = S_rr^{-1} b on r)
+__global__ void k_dp_fbar(int nb, const double* __restrict__ fb, const int* __restrict__ D,
+                          const int* __restrict__ D_off, const int* __restrict__ D_cnt,
+                          const double* __restrict__ gD, const int* __restrict__ c_pos,
+                          const int* __restrict__ c_off, const DpSub* __restrict__ dps,
+                          const double* __restrict__ S, const int* __restrict__ design,
+                          const int* __restrict__ slot_of, const int* __restrict__ src,
+                          const int* __restrict__ src_off, const int* __restrict__ nes,
+                          const double* __restrict__ xb, const int* __restrict__ xoff,
+                          double* __restrict__ fbar) {
+  const int s = blockIdx.x;
+  const DpSub dp = dps[s];
+  const int sl = slot_of[s];
+  const int ne = nes[sl];
+  const int* sr = src + src_off[sl];
+  const double* Sd = S + (size_t)design[s] * nb * nb;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int k = warp; k < dp.nc; k += blockDim.x >> 5) {
+    const int cp = c_pos[c_off[s] + k];
+    double v = 0.0;
+    for (int i = lane; i < ne; i += 32) v += Sd[(size_t)sr[i] * nb + cp] * xb[xoff[s] + i];
+    for (int q = lane; q < D_cnt[s]; q += 32) v += Sd[(size_t)D[D_off[s] + q] * nb + cp] * gD[D_off[s] + q];
+    v = warp_sum(v);
+    if (lane == 0) fbar[dp.t_off + k] = fb[(size_t)s * nb + cp] - v;
+  }
+}
+void Ctx::launch_dp_fbar() {
+  k_dp_fbar<<<su.Ns, kThreads, 0, st>>>(su.nb, d_fb.p, d_D.p, d_D_off.p, d_D_cnt.p, d_gD.p, d_c_pos.p,
+                                        d_c_off.p, d_dp.p, d_S.p, d_design.p, d_slot_of.p, d_op_src.p,
+                                        d_op_src_off.p, d_fac_ne.p, d_xb.p, d_xoff.p, d_fbar_loc.p);
+  LAUNCH_CHECK();
+}
+
+// perimeter displacement: ub[src_i] = x_i; FETI-DP adds corners and supports
+__global__ void k_bnd_u(int nb, const int* __restrict__ slot_of, const int* __restrict__ src,
+                        const int* __restrict__ src_off, const int* __restrict__ nes,
+                        const double* __restrict__ xb, const int* __restrict__ xoff,
+                        const int* __restrict__ D, const int* __restrict__ D_off,
+                        const int* __restrict__ D_cnt, const double* __restrict__ gD,
+                        const int* __restrict__ c_pos, const int* __restrict__ c_off,
+                        const DpSub* __restrict__ dps, const int* __restrict__ cmap,
+                        const double* __restrict__ uc, double* __restrict__ ub) {
+  const int s = blockIdx.x;
+  double* u = ub + (size_t)s * nb;
+  for (int i = threadIdx.x; i < nb; i += blockDim.x) u[i] = 0.0;
+  __syncthreads();
+  const int sl = slot_of[s];
+  const int* sr = src + src_off[sl];
+  for (int i = threadIdx.x; i < nes[sl]; i += blockDim.x) u[sr[i]] = xb[xoff[s] + i];
+  for (int k = threadIdx.x; k < D_cnt[s]; k += blockDim.x) u[D[D_off[s] + k]] = gD[D_off[s] + k];
+  if (dps && uc)
+    for (int k = threadIdx.x; k < dps[s].nc; k += blockDim.x)
+      u[c_pos[c_off[s] + k]] = uc[cmap[dps[s].cmap_off + k]];
+}
+void Ctx::launch_bnd_u(const double* uc, double* ub_all) {
+  k_bnd_u<<<su.Ns, kThreads, 0, st>>>(su.nb, d_slot_of.p, d_op_src.p, d_op_src_off.p, d_fac_ne.p, d_xb.p,
+                                      d_xoff.p, d_D.p, d_D_off.p, d_D_cnt.p, d_gD.p, d_c_pos.p, d_c_off.p,
+                                      su.method == FETIGPU_FETIDP ? d_dp.p : nullptr, d_cmap.p, uc, ub_all);
+  LAUNCH_CHECK();
+}
+__global__ void k_scatter_perim(int nb, int nloc, const int* __restrict__ pdof, const double* __restrict__ ub,
+                                double* __restrict__ u) {
+  const int s = blockIdx.x;
+  for (int i = threadIdx.x; i < nb; i += blockDim.x) u[(size_t)s * nloc + pdof[i]] = ub[(size_t)s * nb + i];
+}
+void Ctx::launch_scatter_perim(const double* ub_all, double* u) {
+  DBuf<int> pd;
+  pd.upload(su.perim_dof, st);
+  k_scatter_perim<<<su.Ns, kThreads, 0, st>>>(su.nb, su.nloc, pd.p, ub_all, u);
+  LAUNCH_CHECK();
+  CK(cudaStreamSynchronize(st));
+}
+__global__ void k_add_rigid(int nloc, const double* __restrict__ R, const double* __restrict__ alpha,
+                            double* __restrict__ u) {
+  const int s = blockIdx.x;
+  const double a0 = alpha[3 * s], a1 = alpha[3 * s + 1], a2 = alpha[3 * s + 2];
+  for (int i = threadIdx.x; i < nloc; i += blockDim.x)
+    u[(size_t)s * nloc + i] += R[i] * a0 + R[nloc + i] * a1 + R[2 * nloc + i] * a2;
+}
+void Ctx::launch_add_rigid(double* u, const double* alpha) {
+  DBuf<double> R;
+  R.upload(su.Rfull, st);
+  k_add_rigid<<<su.Ns, kThreads, 0, st>>>(su.nloc, R.p, alpha, u);
+  LAUNCH_CHECK();
+  CK(cudaStreamSynchronize(st));
+}
+
+void Ctx::init_device() {
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    fail(FETIGPU_E_NO_DEVICE, "no CUDA device available");
+  CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  CB(cublasCreate(&cb));
+  CB(cublasSetStream(cb, st));
+  CK(cudaEventCreate(&ev0));
+  CK(cudaEventCreate(&ev1));
+  CK(cudaEventCreate(&ev2));
+  d_status.alloc(1);
+  d_status.zero(st);
+  CK(cudaFuncSetAttribute(k_nd_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          kSmallFront * kSmallFront * 8));
+  CK(cudaFuncSetAttribute(k_front_elim_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          kSmallFront * kSmallFront * 8));
+  CK(cudaFuncSetAttribute(k_block_apply<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBlockSmem));
+  CK(cudaFuncSetAttribute(k_block_apply<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBlockSmem));
+  CK(cudaFuncSetAttribute(k_block_apply_dp, cudaFuncAttributeMaxDynamicSharedMemorySize, kAsyncSmem));
+}
+
+void Ctx::coarse_solve_packed(bool g_ready, double* zero_y) {
+  if (!g_ready || su.Nc == 0) {
+    launch_pdl(k_coarse_gather, grid_for(std::max(su.Nc, zero_y ? su.m : 0)), kThreads, 0, st,
+               (const int*)d_optr.p, (const int*)d_oidx.p, (const double*)d_tbuf.p, su.Nc, d_gc.p, 1.0,
+               (const double*)nullptr, zero_y, zero_y ? su.m : 0);
+    LAUNCH_CHECK();
+  }
+  if (su.Nc == 0) return;
+  if (!use_csym) {  // small coarse problem: dense L2-resident inverse, one launch
+    launch_pdl(k_dense_gemv, grid_for((long long)su.Nc * 32), kThreads, 0, st, (const double*)d_Kinv.p, su.Nc,
+               (const double*)d_gc.p, d_h.p);
+    LAUNCH_CHECK();
+    return;
+  }
+  launch_pdl(k_csym_tiles, csym_grid, 128, 0, st, (const double*)d_kinv_tiles.p, kinv_nb, su.Nc,
+             (const double*)d_gc.p, d_crow.p, d_ccol.p);
+  launch_pdl(k_csym_reduce, kinv_nb, 512, 0, st, (const double*)d_crow.p, (const double*)d_ccol.p, kinv_nb,
+             su.Nc, d_h.p);
+  LAUNCH_CHECK();
+}
+
+void Ctx::apply_F(const double* x, double* y, int ncols, int ldx, int ldy, bool y_zeroed) {
+  const int Ns = su.Ns;
+  if (su.method == FETIGPU_TFETI) {
+    if (ncols == 1 && y_zeroed) {
+      if (use_sym)
+        launch_pdl(k_sym_gemv_scatter<3, false>, Ns, 256, sym_smem, st, (const SymSub*)d_sym.p,
+                   (const double*)d_symtiles.p, (const int*)d_oprows.p, (const double*)d_opcoef_apply.p, x, y,
+                   (double*)nullptr, (const int*)nullptr, (const DpSub*)nullptr, (const double*)nullptr,
+                   (double*)nullptr, 0, (double*)nullptr, 0, 1, (const CoarseGather*)nullptr);
+      else
+        launch_pdl(k_gather_gemv_scatter<3, false>, dim3(Ns, 1, rsplit), kThreads, max_ld * 8, st,
+                   (const OpSub*)d_op.p, (const double*)d_opmat.p, (const int*)d_oprows.p,
+                   (const double*)d_opcoef_apply.p, x, y, (double*)nullptr, 0, (double*)nullptr,
+                   (const int*)nullptr, ldx, ldy, 1, (const DpSub*)nullptr, (const double*)nullptr,
+                   (double*)nullptr);
+      LAUNCH_CHECK();
+      return;
+    }
+    for (int c = 0; c < ncols; ++c) CK(cudaMemsetAsync(y + (size_t)c * ldy, 0, su.m * 8, st));
+    if (use_sym) {
+      for (int c = 0; c < ncols; ++c)
+        k_sym_gemv_scatter<3, false><<<Ns, 256, sym_smem, st>>>(d_sym.p, d_symtiles.p, d_oprows.p,
+                                                                d_opcoef_apply.p, x + (size_t)c * ldx,
+                                                                y + (size_t)c * ldy, nullptr, nullptr);
+    } else {
+      dim3 grid(Ns, ncols, rsplit);
+      k_gather_gemv_scatter<3, false><<<grid, kThreads, max_ld * 8, st>>>(
+          d_op.p, d_opmat.p, d_oprows.p, d_opcoef_apply.p, x, y, nullptr, 0, nullptr, nullptr, ldx, ldy);
+    }
+    LAUNCH_CHECK();
+  } else {
+    for (int c = 0; c < ncols; ++c) {
+      const double* xc = x + (size_t)c * ldx;
+      double* yc = y + (size_t)c * ldy;
+      // phase 1: v_s = F''_s x_s and t_s = A''^T x_s (one kernel; it also zeroes y)
+      if (use_sym) {
+        launch_pdl(k_sym_gemv_scatter<1, true>, Ns, 256, sym_smem, st, (const SymSub*)d_sym.p,
+                   (const double*)d_symtiles.p, (const int*)d_oprows.p, (const double*)d_opcoef_apply.p, xc,
+                   (double*)nullptr, d_vbuf.p, (const int*)d_voff.p, (const DpSub*)d_dp.p,
+                   (const double*)d_abc.p, d_tbuf.p, 0, yc, su.m, Ns,
+                   (const CoarseGather*)(su.Nc ? d_cgather.p : nullptr));
+      } else {
+        launch_pdl(k_gather_gemv_scatter<1, true>, dim3(Ns, 1, rsplit), kThreads, max_ld * 8, st,
+                   (const OpSub*)d_op.p, (const double*)d_opmat.p, (const int*)d_oprows.p,
+                   (const double*)d_opcoef_apply.p, xc, (double*)nullptr, (double*)nullptr, 0, d_vbuf.p,
+                   (const int*)d_voff.p, ldx, 0, 1, (const DpSub*)d_dp.p, (const double*)d_abc.p, d_tbuf.p);
+      }
+      // coarse: u = Kbar^{-1} (sum_s B_c^T t_s), fixed order (y zeroed here on the non-symmetric path)
+      coarse_solve_packed(use_sym, use_sym ? nullptr : yc);
+      // phase 2: y = sum_s B_s (v_s + A''_s u_s)
+      launch_phase2_csym(yc);
+      LAUNCH_CHECK();
+    }
+  }
+}
+
+void Ctx::setup_pipe() {
+  pipe_ready = false;
+  const char* off = getenv("FETIGPU_NO_PIPE");
+  if ((off && off[0] == '1') || !use_sym || su.method != FETIGPU_FETIDP || su.Ns < 4 * kPipe) return;
+  int run = -1;
+  for (int c = 0; c < kPipe; ++c) {
+    pipe_s0[c] = (int)((long long)su.Ns * c / kPipe);
+    pipe_s0[c + 1] = (int)((long long)su.Ns * (c + 1) / kPipe);
+    for (int s = pipe_s0[c]; s < pipe_s0[c + 1]; ++s) run = std::max(run, sub_maxrow[s]);
+    pipe_need[c] = run + 1;  // rows [0, need) cover every row chunks 0..c gather
+  }
+  // worthwhile only if the first chunks need a real prefix of lambda
+  if (pipe_need[kPipe / 2 - 1] > (long long)su.m * 3 / 4) return;
+  if (!pipe_cp) {
+    CK(cudaStreamCreateWithFlags(&pipe_cp, cudaStreamNonBlocking));
+    for (int c = 0; c < kPipe; ++c) {
+      CK(cudaStreamCreateWithFlags(&pipe_st[c], cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&pipe_in[c], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&pipe_done[c], cudaEventDisableTiming));
+    }
+    CK(cudaEventCreateWithFlags(&pipe_start, cudaEventDisableTiming));
+  }
+  pipe_ready = true;
+}
+
+void Ctx::apply_F_host(const double* xh, double* yh) {
+  const int m = su.m;
+  stage(m);
+  double* x = stage_x.p;
+  double* y = stage_y.p;
+  if (!pipe_ready) {
+    CK(cudaMemcpyAsync(x, xh, (size_t)m * 8, cudaMemcpyHostToDevice, st));
+    apply_F(x, y, 1, m, m);
+  } else {
+    CK(cudaEventRecord(pipe_start, st));  // after everything already queued on st
+    CK(cudaStreamWaitEvent(pipe_cp, pipe_start, 0));
+    int done = 0;
+    for (int c = 0; c < kPipe; ++c) {
+      const int need = c == kPipe - 1 ? m : pipe_need[c];
+      if (need > done) {
+        CK(cudaMemcpyAsync(x + done, xh + done, (size_t)(need - done) * 8, cudaMemcpyHostToDevice, pipe_cp));
+        done = need;
+      }
+      CK(cudaEventRecord(pipe_in[c], pipe_cp));
+    }
+    for (int c = 0; c < kPipe; ++c) {
+      cudaStream_t q = pipe_st[c];
+      CK(cudaStreamWaitEvent(q, pipe_in[c], 0));
+      const int nblk = pipe_s0[c + 1] - pipe_s0[c];
+      k_sym_gemv_scatter<1, true><<<nblk, 256, sym_smem, q>>>(d_sym.p, d_symtiles.p, d_oprows.p,
+                                                               d_opcoef_apply.p, x, nullptr, d_vbuf.p, d_voff.p,
+                                                               d_dp.p, d_abc.p, d_tbuf.p, pipe_s0[c], y, m,
+                                                               su.Ns, su.Nc ? d_cgather.p : nullptr);
+      LAUNCH_CHECK();
+      CK(cudaEventRecord(pipe_done[c], q));
+      CK(cudaStreamWaitEvent(st, pipe_done[c], 0));
+    }
+    // coarse u = Kbar^{-1} (sum_s B_c^T t_s) on the packed inverse; phase 2
+    coarse_solve_packed(true);
+    launch_phase2_csym(y);
+    LAUNCH_CHECK();
+  }
+  CK(cudaMemcpyAsync(yh, y, (size_t)m * 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+}
+
+void Ctx::apply_precond(const double* r, double* z, double* Zcols, bool row_major, bool z_zeroed) {
+  if (!z_zeroed) CK(cudaMemsetAsync(z, 0, su.m * 8, st));
+  if (Zcols) CK(cudaMemsetAsync(Zcols, 0, (size_t)su.m * su.Ns * 8, st));
+  const int ldz = row_major ? 1 : su.m, zrs = row_major ? su.Ns : 1;
+  if (pc_sym && !Zcols) {
+    auto k = KRp == 1 ? k_sym_gemv_scatter<1, false> : k_sym_gemv_scatter<3, false>;
+    launch_pdl(k, su.Ns, 256, pc_sym_smem, st, (const SymSub*)d_pcsym.p, (const double*)d_pcsymtiles.p,
+               (const int*)d_pcrows.p, (const double*)d_pccoef.p, r, z, (double*)nullptr, (const int*)nullptr,
+               (const DpSub*)nullptr, (const double*)nullptr, (double*)nullptr, 0, (double*)nullptr, 0, 1,
+               (const CoarseGather*)nullptr);
+    LAUNCH_CHECK();
+    return;
+  }
+  auto k = KRp == 1 ? k_gather_gemv_scatter<1, false> : k_gather_gemv_scatter<3, false>;
+  launch_pdl(k, dim3(su.Ns, 1, pc_rsplit), kThreads, max_pc_ld * 8, st, (const OpSub*)d_pc.p,
+             (const double*)d_pcmat.p, (const int*)d_pcrows.p, (const double*)d_pccoef.p, r, z, Zcols, ldz,
+             (double*)nullptr, (const int*)nullptr, 0, 0, zrs, (const DpSub*)nullptr, (const double*)nullptr,
+             (double*)nullptr);
+  LAUNCH_CHECK();
+}
+
+void Ctx::apply_F_block(const double* W, int ldw, double* Q, int ldq, int k) {
+  const int Ns = su.Ns, m = su.m;
+  if (ldq == k) CK(cudaMemsetAsync(Q, 0, (size_t)m * k * 8, st));
+  else CK(cudaMemset2DAsync(Q, (size_t)ldq * 8, 0, (size_t)k * 8, m, st));
+  BlockApplyArgs a{d_op.p, d_opmat.p, d_oprows.p, d_opcoef_apply.p, KR, nullptr, nullptr, nullptr, nullptr, 0,
+                   W, ldw, Q, ldq, k};
+  int max_ns = 0;
+  for (int n : op_ns) max_ns = std::max(max_ns, n);
+  if (su.method == FETIGPU_FETIDP) {
+    const int Nc = su.Nc;
+    int tot_c = 0;
+    for (auto& S : su.subs) tot_c += (int)S.c.size();
+    if (blk_t.n < (size_t)tot_c * k) blk_t.alloc((size_t)tot_c * k);
+    if (blk_T.n < (size_t)Nc * k) { blk_T.alloc((size_t)Nc * k); blk_U.alloc((size_t)Nc * k); }
+    {
+      const size_t smem = ((size_t)std::max(max_ns * 8, 4 * 8 * kDpTCols) + max_ns) * 8 + (size_t)max_ns * 4;
+      raise_smem_limit(k_block_dp_t, smem);
+      k_block_dp_t<<<dim3((k + kDpTCols - 1) / kDpTCols, Ns), 256, smem, st>>>(
+          d_op.p, d_dp.p, d_oprows.p, d_opcoef_apply.p, d_abc.p, W, ldw, k, blk_t.p, k);
+    }
+    k_coarse_gather_block<<<dim3((k + 255) / 256, Nc), 256, 0, st>>>(d_optr.p, d_oidx.p, blk_t.p, k, Nc, k,
+                                                                     blk_T.p, k);
+    const double one = 1.0, zero = 0.0;
+    // U = Kbar^{-1} T  (row-major N_c x k == column-major k x N_c: U^T = T^T Kinv)
+    CB(cublasDgemm(cb, CUBLAS_OP_N, CUBLAS_OP_N, k, Nc, Nc, &one, blk_T.p, k, d_Kinv.p, Nc, &zero, blk_U.p, k));
+    a.dps = d_dp.p; a.abc = d_abc.p; a.cmap = d_cmap.p; a.U = blk_U.p; a.ldu = k;
+    max_ns += 8;
+  }
+  dim3 grid((k + kBN - 1) / kBN, (max_ns + kBM - 1) / kBM, Ns);
+  const bool fast = folded && (k % 2 == 0) && (ldw % 2 == 0) && (ldq % 2 == 0) &&
+                    ((uintptr_t)W % 16 == 0) && ((uintptr_t)Q % 16 == 0);
+  if (fast) k_block_apply_dp<<<grid, 256, kAsyncSmem, st>>>(a);
+  else if (KR == 1) k_block_apply<1><<<grid, 256, kBlockSmem, st>>>(a);
+  else k_block_apply<3><<<grid, 256, kBlockSmem, st>>>(a);
+  LAUNCH_CHECK();
+}
+
+void Ctx::project_rm(double* v, int ncols) {
+  if (su.method != FETIGPU_TFETI) return;
+  const int nc = 3 * su.Ns;
+  double* g = grow(ws_g, (size_t)nc * ncols);
+  double* h = grow(ws_h, (size_t)nc * ncols);
+  double* corr = grow(ws_corr, (size_t)su.m * ncols);
+  CK(cudaMemsetAsync(corr, 0, (size_t)su.m * ncols * 8, st));
+  k_proj_gather<<<dim3(su.Ns, ncols), kThreads, 0, st>>>(d_pj.p, d_pcrows.p, d_pjcoef.p, d_RT.p, d_rt_off.p, v, 1,
+                                                        g, nc, -1.0, ncols);
+  small_gemm(g, h, ncols);
+  k_proj_scatter<<<dim3(su.Ns, ncols), kThreads, 0, st>>>(d_pj.p, d_pcrows.p, d_pjcoef.p, d_RT.p, d_rt_off.p,
+                                                         h, nc, corr, 1, ncols);
+  k_add<<<grid_for((long long)su.m * ncols), kThreads, 0, st>>>(su.m * ncols, corr, v, 0, 0);
+  LAUNCH_CHECK();
+}
+
+void Ctx::proj_corr(const double* v, int ldv, double* corr, int ldc, int ncols, double gsign) {
+  if (ncols == 1 && su.m > 0) {
+    proj_single(v, corr, 0, gsign);
+    return;
+  }
+  const int nc = 3 * su.Ns;
+  double* gp = d_g.p;
+  double* hp = d_h.p;
+  if (ncols > 1) {
+    gp = grow(ws_g, (size_t)nc * ncols);
+    hp = grow(ws_h, (size_t)nc * ncols);
+  }
+  k_proj_gather<<<dim3(su.Ns, ncols), kThreads, 0, st>>>(d_pj.p, d_pcrows.p, d_pjcoef.p, d_RT.p,
+                                                        d_rt_off.p, v, ldv, gp, nc, gsign);
+  small_gemm(gp, hp, ncols);
+  if (ldc == su.m)
+    CK(cudaMemsetAsync(corr, 0, (size_t)su.m * ncols * 8, st));
+  else
+    for (int c = 0; c < ncols; ++c) CK(cudaMemsetAsync(corr + (size_t)c * ldc, 0, su.m * 8, st));
+  k_proj_scatter<<<dim3(su.Ns, ncols), kThreads, 0, st>>>(d_pj.p, d_pcrows.p, d_pjcoef.p, d_RT.p,
+                                                         d_rt_off.p, hp, nc, corr, ldc);
+  LAUNCH_CHECK();
+}
+
+void Ctx::rhs() {
+  const int m = su.m;
+  // x_s = S_kk^{-1} f_k (T-FETI) or S_rr^{-1} (f_r - S_rD g) (FETI-DP)
+  launch_bnd_rhs(nullptr, nullptr);
+  k_chol_solve<<<su.Ns, kThreads, max_ne * 8, st>>>(d_opfac.p, d_fac_off.p, d_slot_of.p, d_fac_ne.p, d_xb.p,
+                                                     d_xoff.p);
+  LAUNCH_CHECK();
+  CK(cudaMemsetAsync(d_v1.p, 0, m * 8, st));
+  launch_rhs_scatter(d_v1.p);  // B K^+ f
+  if (su.method == FETIGPU_TFETI) {
+    DBuf<double> gap;
+    gap.upload(su.gap, st);
+    k_sub<<<grid_for(m), kThreads, 0, st>>>(m, d_v1.p, gap.p, d_d.p);
+    // lambda0 = G^T (G G^T)^{-1} e = -B R H e
+    small_gemm(d_e.p, d_h.p, 1);
+    CK(cudaMemsetAsync(d_v2.p, 0, m * 8, st));
+    k_proj_scatter<<<su.Ns, kThreads, 0, st>>>(d_pj.p, d_pcrows.p, d_pjcoef.p, d_RT.p, d_rt_off.p, d_h.p,
+                                               3 * su.Ns, d_v2.p, m);
+    CK(cudaMemsetAsync(d_lam0.p, 0, m * 8, st));
+    k_axpy<<<grid_for(m), kThreads, 0, st>>>(m, -1.0, d_v2.p, d_lam0.p);
+    CK(cudaStreamSynchronize(st));
+    gap.release();
+  } else {
+    // fbar_c = sum B_c^T (f_c - S_cD g - S_cr x); d = d_r - F_rc Kbar^{-1} fbar_c
+    launch_dp_fbar();
+    k_coarse_gather<<<grid_for(su.Nc), kThreads, 0, st>>>(d_optr.p, d_oidx.p, d_fbar_loc.p, su.Nc, d_fbar.p,
+                                                         1.0, nullptr);
+    k_dense_gemv<<<grid_for((long long)su.Nc * 32), kThreads, 0, st>>>(d_Kinv.p, su.Nc, d_fbar.p, d_h.p);
+    CK(cudaMemsetAsync(d_v2.p, 0, m * 8, st));
+    k_dp_phase2<<<su.Ns, kThreads, 0, st>>>(d_op.p, d_dp.p, d_oprows.p, d_opcoef_apply.p, d_abc.p, d_cmap.p, d_h.p,
+                                            nullptr, d_v2.p, 0.0);
+    k_sub<<<grid_for(m), kThreads, 0, st>>>(m, d_v1.p, d_v2.p, d_d.p);
+    CK(cudaMemsetAsync(d_lam0.p, 0, m * 8, st));
+    LAUNCH_CHECK();
+  }
+  CK(cudaStreamSynchronize(st));
+  have_rhs = true;
+}
+
+void Ctx::recover(const double* lambda_dev, double* u_dev) {
+  const int m = su.m, Ns = su.Ns;
+  if (!have_rhs) rhs();
+  DBuf<double> ub, alpha, uc;
+  ub.alloc((size_t)Ns * su.nb);
+  if (su.method == FETIGPU_TFETI) {
+    // rho = d - F lambda; alpha = (G G^T)^{-1} G rho (least squares, decomposition.hpp:143)
+    apply_F(lambda_dev, d_v1.p, 1, m, m);
+    k_sub<<<grid_for(m), kThreads, 0, st>>>(m, d_d.p, d_v1.p, d_v2.p);
+    k_proj_gather<<<su.Ns, kThreads, 0, st>>>(d_pj.p, d_pcrows.p, d_pjcoef.p, d_RT.p, d_rt_off.p, d_v2.p, m,
+                                              d_g.p, 3 * Ns, -1.0);
+    alpha.alloc(3 * (size_t)Ns);
+    small_gemm(d_g.p, alpha.p, 1);
+    launch_bnd_rhs(lambda_dev, nullptr);
+  } else {
+    // u_c = Kbar^{-1} (fbar_c + F_rc^T lambda)
+    k_dp_t<<<Ns, kThreads, 0, st>>>(d_op.p, d_dp.p, d_oprows.p, d_opcoef_apply.p, d_abc.p, lambda_dev, d_tbuf.p);
+    k_coarse_gather<<<grid_for(su.Nc), kThreads, 0, st>>>(d_optr.p, d_oidx.p, d_tbuf.p, su.Nc, d_g.p, 1.0,
+                                                         d_fbar.p);
+    uc.alloc(std::max(1, su.Nc));
+    k_dense_gemv<<<grid_for((long long)su.Nc * 32), kThreads, 0, st>>>(d_Kinv.p, su.Nc, d_g.p, uc.p);
+    launch_bnd_rhs(lambda_dev, uc.p);
+  }
+  k_chol_solve<<<Ns, kThreads, max_ne * 8, st>>>(d_opfac.p, d_fac_off.p, d_slot_of.p, d_fac_ne.p, d_xb.p,
+                                                  d_xoff.p);
+  launch_bnd_u(uc.p, ub.p);
+  CK(cudaMemsetAsync(u_dev, 0, (size_t)Ns * su.nloc * 8, st));
+  launch_scatter_perim(ub.p, u_dev);
+  if (!keep_factors) fail(FETIGPU_E_STATE, "recovery needs the ND factors");
+  int shm = 0;
+  for (auto& nd : su.nd.nodes) shm = std::max(shm, nd.nf);
+  k_nd_backsub<<<Ns, kThreads, shm * 8, st>>>(d_nodes.p, d_topdown.p, (int)su.nd.topdown.size(), d_nd_dofs.p,
+                                              d_ndfac.p, su.nd.factor_stride, d_design.p, u_dev, su.nloc);
+  LAUNCH_CHECK();
+  if (su.method == FETIGPU_TFETI) launch_add_rigid(u_dev, alpha.p);
+  CK(cudaStreamSynchronize(st));
+}
+
+}  // namespace fg

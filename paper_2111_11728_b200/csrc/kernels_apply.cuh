@@ -725,7 +725,8 @@ __global__ void __launch_bounds__(256) k_fo_sub(const double* __restrict__ W, in
 }
 // psi_j = q_j^T w for j < *cnt on a (column x row-segment) grid: CTA (j, s)
 // reduces rows [s*chunk, (s+1)*chunk) of column j into partial[j*S + s];
-// k_fo_psi_sum adds the S partials of each column in fixed order.
+// k_fo_psi_sum adds the S partials of each column in fixed order (skipped
+// when S == 1, where the caller passes psi itself as the partial buffer).
 __global__ void __launch_bounds__(256) k_fo_psi_seg(const double* __restrict__ Q, int m,
                                                     const int* __restrict__ cnt,
                                                     const double* __restrict__ w,
@@ -761,7 +762,7 @@ __global__ void __launch_bounds__(256) k_fo_psi_seg(const double* __restrict__ Q
     if (threadIdx.x == 0) {
       double t = 0.0;
       for (int k = 0; k < 8; ++k) t += red[k];
-      partial[(size_t)j * S + s] = t;
+      partial[(size_t)j * S + s] = t;  // S == 1: partial is psi itself
     }
     __syncthreads();
   }

@@ -1,0 +1,292 @@
+// runtime.cuh -- error macros, device allocation (block cache), launch helpers (PDL,
+// shared-memory opt-in), host parallel_for, phase timer and scratch buffers.
+// Part of the libfetigpu unity build (fetigpu.cu includes it); namespace fg.
+#pragma once
+#include <cublas_v2.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <numeric>
+#include <string>
+#include <thread>
+#include <unordered_map>
+#include <vector>
+
+#include "common.cuh"
+#include "fetigpu.h"
+#include "setup.hpp"  // fg::Error / fail
+
+namespace fg {
+
+#define CK(x)                                                                                  \
+  do {                                                                                         \
+    cudaError_t e_ = (x);                                                                      \
+    if (e_ != cudaSuccess)                                                                     \
+      fail(e_ == cudaErrorMemoryAllocation ? FETIGPU_E_OUT_OF_MEMORY : FETIGPU_E_CUDA,         \
+           std::string(#x) + ": " + cudaGetErrorString(e_));                                   \
+  } while (0)
+#define CB(x)                                                                                  \
+  do {                                                                                         \
+    cublasStatus_t s_ = (x);                                                                   \
+    if (s_ != CUBLAS_STATUS_SUCCESS)                                                           \
+      fail(FETIGPU_E_CUDA, std::string(#x) + " failed (cuBLAS status " + std::to_string((int)s_) + \
+                               ", line " + std::to_string(__LINE__) + ")");                    \
+  } while (0)
+#define LAUNCH_CHECK()                                                                         \
+  do {                                                                                         \
+    cudaError_t e_ = cudaGetLastError();                                                       \
+    if (e_ != cudaSuccess)                                                                     \
+      fail(e_ == cudaErrorMemoryAllocation ? FETIGPU_E_OUT_OF_MEMORY : FETIGPU_E_CUDA,         \
+           std::string("kernel launch before ") + __FILE__ + ":" + std::to_string(__LINE__) + ": " +  \
+               cudaGetErrorString(e_));                                                        \
+  } while (0)
+
+static size_t g_device_bytes = 0;
+
+// Device memory: cudaMalloc behind a per-device cache of large blocks.  A freed
+// block is kept and handed to a later request it fits (at most 2x larger), so
+// repeated builds and solves in one process (SIMP loops, the bench's config
+// table) reuse memory instead of paying variable cudaMalloc / cudaFree costs.
+// A release first synchronises the device (cudaFree semantics: buffers freed
+// at scope end are never still in use).  On OOM the cache is returned to the
+// driver and the allocation retried.  FETIGPU_NO_CACHE=1 disables the cache.
+struct BlockCache {
+  std::mutex mu;
+  std::multimap<size_t, void*> free_blocks;      // capacity -> block
+  std::unordered_map<void*, size_t> capacity;    // every live or cached block
+  size_t cached = 0;
+};
+static BlockCache& block_cache() {
+  static BlockCache caches[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return caches[dev & 63];
+}
+static bool cache_on() {
+  static const bool on = [] {
+    const char* e = getenv("FETIGPU_NO_CACHE");
+    return !(e && e[0] == '1');
+  }();
+  return on;
+}
+// Only the RRS direction store goes through the cache: its multi-GB chunks are
+// allocated and freed per solve, and that is where driver allocation cost
+// varied (up to ~0.9 s per C5 solve).  Everything else keeps a fresh
+// cudaMalloc placement -- measured: caching the build workspace or operator
+// storage made the L2-resident applies of C2 / C3 6-10% slower.
+static void* dev_alloc(size_t bytes, bool cached) {
+  bytes = (bytes + 511) & ~size_t(511);
+  BlockCache& C = block_cache();
+  if (!cached) {
+    void* p = nullptr;
+    CK(cudaMalloc(&p, bytes));
+    return p;
+  }
+  if (cache_on()) {
+    std::lock_guard<std::mutex> lk(C.mu);
+    auto it = C.free_blocks.lower_bound(bytes);
+    if (it != C.free_blocks.end() && it->first <= 2 * bytes) {
+      void* p = it->second;
+      C.cached -= it->first;
+      C.free_blocks.erase(it);
+      return p;
+    }
+  }
+  void* p = nullptr;
+  cudaError_t e = cudaMalloc(&p, bytes);
+  if (e == cudaErrorMemoryAllocation && cache_on()) {  // give the cache back, retry
+    cudaGetLastError();
+    std::lock_guard<std::mutex> lk(C.mu);
+    cudaDeviceSynchronize();
+    for (auto& f : C.free_blocks) {
+      cudaFree(f.second);
+      C.capacity.erase(f.second);
+    }
+    C.free_blocks.clear();
+    C.cached = 0;
+    e = cudaMalloc(&p, bytes);
+  }
+  CK(e);
+  if (cache_on()) {
+    std::lock_guard<std::mutex> lk(C.mu);
+    C.capacity[p] = bytes;
+  }
+  return p;
+}
+static void dev_free(void* p) {
+  if (!cache_on()) {
+    cudaFree(p);
+    return;
+  }
+  BlockCache& C = block_cache();
+  std::unique_lock<std::mutex> lk(C.mu);
+  auto it = C.capacity.find(p);
+  if (it == C.capacity.end()) {  // small block: plain cudaFree
+    lk.unlock();
+    cudaFree(p);
+    return;
+  }
+  cudaDeviceSynchronize();  // cudaFree semantics: nothing still uses the buffer
+  C.free_blocks.emplace(it->second, p);
+  C.cached += it->second;
+}
+// free device memory including the cached blocks
+static size_t dev_free_bytes() {
+  size_t freeb = 0, total = 0;
+  CK(cudaMemGetInfo(&freeb, &total));
+  if (cache_on()) {
+    BlockCache& C = block_cache();
+    std::lock_guard<std::mutex> lk(C.mu);
+    freeb += C.cached;
+  }
+  return freeb;
+}
+
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  ~DBuf() { release(); }
+  void release() {
+    if (p) {
+      dev_free(p);
+      g_device_bytes -= n * sizeof(T);
+    }
+    p = nullptr;
+    n = 0;
+  }
+  bool cached = false;  // recycled scratch: allocate through the block cache
+  void alloc(size_t count) {
+    release();
+    if (count == 0) count = 1;
+    p = static_cast<T*>(dev_alloc(count * sizeof(T), cached));
+    n = count;
+    g_device_bytes += n * sizeof(T);
+  }
+  void upload(const std::vector<T>& v, cudaStream_t st) {
+    alloc(v.size());
+    if (!v.empty()) CK(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, st));
+  }
+  void zero(cudaStream_t st) { CK(cudaMemsetAsync(p, 0, n * sizeof(T), st)); }
+};
+
+static inline int round_up(int v, int a) { return (v + a - 1) / a * a; }
+
+// Launch with programmatic dependent launch (PDL): the kernel may be scheduled
+// while its predecessor in the stream finishes and waits in pdl_wait() (every
+// kernel launched this way calls it first), which hides the launch latency
+// between the small dependent kernels of a solver iteration.  FETIGPU_NO_PDL=1
+// launches them normally.
+static bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("FETIGPU_NO_PDL");
+    return !(e && e[0] == '1');
+  }();
+  return on;
+}
+template <class... KArgs, class... Args>
+static void launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  CK(cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...));
+}
+
+// f(i) for i in [0, n) over up to 16 host threads (contiguous ranges); f must
+// write disjoint outputs.  Serial for small n.
+template <class F>
+static void parallel_for(int n, F&& f) {
+  const int nt = std::min<int>(16, std::max(1u, std::thread::hardware_concurrency()));
+  if (n < 64 || nt <= 1) {
+    for (int i = 0; i < n; ++i) f(i);
+    return;
+  }
+  std::vector<std::thread> th;
+  for (int t = 0; t < nt; ++t)
+    th.emplace_back([&, t] {
+      const int a = (int)((long long)n * t / nt), b = (int)((long long)n * (t + 1) / nt);
+      for (int i = a; i < b; ++i) f(i);
+    });
+  for (auto& x : th) x.join();
+}
+
+// cudaFuncAttributeMaxDynamicSharedMemorySize is per function and process-wide:
+// contexts of different sizes may be alive at once, so it is only ever raised.
+template <class K>
+static void raise_smem_limit(K* func, size_t bytes) {
+  static std::mutex mu;
+  static std::unordered_map<const void*, size_t> cur;
+  std::lock_guard<std::mutex> lk(mu);
+  size_t& c = cur[(const void*)func];
+  if (bytes > c) {
+    CK(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    c = bytes;
+  }
+}
+
+// FETIGPU_TIMING=1: host wall-clock marks of the build phases on stderr
+struct PhaseTimer {
+  bool on;
+  std::chrono::steady_clock::time_point t0, last;
+  PhaseTimer() {
+    const char* e = getenv("FETIGPU_TIMING");
+    on = e && e[0] == '1';
+    t0 = last = std::chrono::steady_clock::now();
+  }
+  void mark(const char* what, cudaStream_t st) {
+    if (!on) return;
+    cudaStreamSynchronize(st);
+    const auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "[fetigpu] %-28s %8.2f ms (total %8.2f)\n", what,
+            std::chrono::duration<double, std::milli>(now - last).count(),
+            std::chrono::duration<double, std::milli>(now - t0).count());
+    last = now;
+  }
+};
+static inline int grid_for(long long n, int threads = kThreads, int cap = 148 * 16) {
+  long long g = (n + threads - 1) / threads;
+  return (int)std::max<long long>(1, std::min<long long>(g, cap));
+}
+
+// Grow-only device scratch buffers keyed by slot: build temporaries reuse
+// them instead of cudaMalloc/cudaFree per level / chunk (cudaFree is a
+// device-wide synchronization).
+struct Scratch {
+  std::vector<std::unique_ptr<DBuf<char>>> bufs;
+  void* get(int id, size_t bytes) {
+    if ((int)bufs.size() <= id) bufs.resize(id + 1);
+    if (!bufs[id]) bufs[id] = std::make_unique<DBuf<char>>();
+    if (bufs[id]->n < bytes) bufs[id]->alloc(bytes + bytes / 4);
+    return bufs[id]->p;
+  }
+  template <class T>
+  T* upload(int id, const std::vector<T>& v, cudaStream_t st) {
+    T* p = static_cast<T*>(get(id, std::max<size_t>(1, v.size()) * sizeof(T)));
+    if (!v.empty()) CK(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, st));
+    return p;
+  }
+  void release(int id) {
+    if (id < (int)bufs.size() && bufs[id]) bufs[id]->release();
+  }
+};
+enum ScratchId { kScWs = 0, kScDescA, kScDescB, kScSlots, kScSrc, kScExt, kScMo, kScMl, kScAo, kScKo, kScFo,
+                 kScMisc };
+
+}  // namespace fg
