@@ -107,13 +107,34 @@ __device__ __forceinline__ void nd_assemble(const NdArgs& a, const NdDev& nd, in
       const double* S = a.ws + a.hbase[ch.height] + (long long)dl * a.hstride[ch.height] + ch.off;
       const int nbc = ch.nf - ch.ne;
       const int* cm = a.cmaps + nd.cmap_off[c];
-      for (int idx = tid; idx < nbc * nbc; idx += nt) {
-        const int j = idx / nbc, i = idx - j * nbc;
-        if (i < j) continue;
-        const double v = S[(size_t)(ch.ne + j) * ch.nf + ch.ne + i];
-        int pr = cm[i], pc = cm[j];
-        if (pr < pc) { const int t = pr; pr = pc; pc = t; }
-        F[(size_t)pc * ld + pr] += v;
+      // U independent (child entry, target) pairs per thread in flight: the
+      // targets of one child are distinct, and each target still receives
+      // zero + child 0 + child 1 in that order
+      constexpr int U = 4;
+      const int tot = nbc * nbc;
+      for (int base = tid; base < tot; base += U * nt) {
+        double v[U], f[U];
+        int pos[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int idx = base + u * nt;
+          pos[u] = -1;
+          v[u] = 0.0;
+          if (idx < tot) {
+            const int j = idx / nbc, i = idx - j * nbc;
+            if (i >= j) {
+              v[u] = S[(size_t)(ch.ne + j) * ch.nf + ch.ne + i];
+              int pr = cm[i], pc = cm[j];
+              if (pr < pc) { const int t = pr; pr = pc; pc = t; }
+              pos[u] = pc * ld + pr;
+            }
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) f[u] = pos[u] >= 0 ? F[pos[u]] : 0.0;
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (pos[u] >= 0) F[pos[u]] = f[u] + v[u];
       }
       __syncthreads();
     }
@@ -354,7 +375,7 @@ __global__ void __launch_bounds__(kThreads) k_bpc_trsm(const FrontDesc* fds, dou
   }
 }
 
-__global__ void __launch_bounds__(kThreads) k_bpc_update(const FrontDesc* fds, double* base, int k0) {
+__global__ void __launch_bounds__(kThreads, 2) k_bpc_update(const FrontDesc* fds, double* base, int k0) {
   const FrontDesc f = fds[blockIdx.y];
   if (k0 >= f.ne) return;
   const int kb = min(kBpcNB, f.ne - k0), k1 = k0 + kb, ld = f.ld;
@@ -372,12 +393,32 @@ __global__ void __launch_bounds__(kThreads) k_bpc_update(const FrontDesc* fds, d
   double* A = base + f.off;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wr = warp >> 2, wc = warp & 3;
-  for (int idx = tid; idx < kBpcNB * kTile; idx += kThreads) {
+  // panels by cp.async: all 2 x 16 copies per thread in flight at once (a
+  // register-staged loop serialises one L2 round trip per iteration)
+#pragma unroll 4
+  for (int q = 0; q < kBpcNB * kTile / kThreads; ++q) {
+    const int idx = tid + q * kThreads;
     const int c = idx / kTile, r = idx - c * kTile;
     const int ri = ti * kTile + r, rj = tj * kTile + r;
-    LiT[c * kBpcPad + r] = (c < kb && ri < mt) ? A[(size_t)(k0 + c) * ld + k1 + ri] : 0.0;
-    LjT[c * kBpcPad + r] = (c < kb && rj < mt) ? A[(size_t)(k0 + c) * ld + k1 + rj] : 0.0;
+    const double* col = A + (size_t)(k0 + c) * ld + k1;
+    cp_async8(LiT + c * kBpcPad + r, (c < kb && ri < mt) ? col + ri : A, c < kb && ri < mt);
+    cp_async8(LjT + c * kBpcPad + r, (c < kb && rj < mt) ? col + rj : A, c < kb && rj < mt);
   }
+  cp_async_commit();
+  // the trailing tile this thread updates, loaded while the panels land
+  double cpre[4][2][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int ri = ti * kTile + wr * 32 + i * 8 + (lane >> 2);
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int cj = tj * kTile + wc * 16 + j * 8 + 2 * (lane & 3);
+      const bool ok0 = ri < mt && cj < mt && ri >= cj, ok1 = ri < mt && cj + 1 < mt && ri >= cj + 1;
+      cpre[i][j][0] = ok0 ? A[(size_t)(k1 + cj) * ld + k1 + ri] : 0.0;
+      cpre[i][j][1] = ok1 ? A[(size_t)(k1 + cj + 1) * ld + k1 + ri] : 0.0;
+    }
+  }
+  cp_async_wait<0>();
   __syncthreads();
   double acc[4][2][2];
 #pragma unroll
@@ -403,8 +444,8 @@ __global__ void __launch_bounds__(kThreads) k_bpc_update(const FrontDesc* fds, d
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
       const int cj = tj * kTile + wc * 16 + j * 8 + 2 * (lane & 3);
-      if (cj < mt && ri >= cj) A[(size_t)(k1 + cj) * ld + k1 + ri] -= acc[i][j][0];
-      if (cj + 1 < mt && ri >= cj + 1) A[(size_t)(k1 + cj + 1) * ld + k1 + ri] -= acc[i][j][1];
+      if (cj < mt && ri >= cj) A[(size_t)(k1 + cj) * ld + k1 + ri] = cpre[i][j][0] - acc[i][j][0];
+      if (cj + 1 < mt && ri >= cj + 1) A[(size_t)(k1 + cj + 1) * ld + k1 + ri] = cpre[i][j][1] - acc[i][j][1];
     }
   }
 }

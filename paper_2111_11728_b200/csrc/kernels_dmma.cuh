@@ -219,15 +219,6 @@ __global__ void __launch_bounds__(256) k_block_apply(BlockApplyArgs a) {
 constexpr int kStages = 3;
 constexpr int kAsyncSmem = (kStages * (kBM * kApad + kBK * kBpad)) * 8 + (512 + 16) * 4;
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  const int n = valid ? 16 : 0;
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(n));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
-
 __global__ void __launch_bounds__(256, 2) k_block_apply_dp(BlockApplyArgs a) {
   extern __shared__ __align__(16) double dsm[];
   double* As = dsm;                                   // kStages x (kBM x kApad)
