@@ -313,10 +313,12 @@ __global__ void __launch_bounds__(kThreads) k_bpc_diag(const FrontDesc* fds, dou
   __shared__ double D[kBpcNB * (kBpcNB + 1)];
   double* A = base + f.off;
   const int kb = min(kBpcNB, f.ne - k0), ld = f.ld;
-  for (int idx = threadIdx.x; idx < kb * kb; idx += kThreads) {
+  for (int idx = threadIdx.x; idx < kb * kb; idx += kThreads) {  // cp.async: all copies in flight
     const int j = idx / kb, i = idx - j * kb;
-    if (i >= j) D[j * (kBpcNB + 1) + i] = A[(size_t)(k0 + j) * ld + k0 + i];
+    if (i >= j) cp_async8(D + j * (kBpcNB + 1) + i, A + (size_t)(k0 + j) * ld + k0 + i, true);
   }
+  cp_async_commit();
+  cp_async_wait<0>();
   __syncthreads();
   eliminate_smem(D, kb, kb, kBpcNB + 1, status, f.code);
   for (int idx = threadIdx.x; idx < kb * kb; idx += kThreads) {
@@ -333,10 +335,12 @@ __global__ void __launch_bounds__(kThreads) k_bpc_trsm(const FrontDesc* fds, dou
   if (k1 + blockIdx.x * kThreads >= f.nf) return;
   __shared__ double D[kBpcNB * (kBpcNB + 1)];
   double* A = base + f.off;
-  for (int idx = threadIdx.x; idx < kb * kb; idx += kThreads) {
+  for (int idx = threadIdx.x; idx < kb * kb; idx += kThreads) {  // cp.async: all copies in flight
     const int j = idx / kb, i = idx - j * kb;
-    if (i >= j) D[j * (kBpcNB + 1) + i] = A[(size_t)(k0 + j) * ld + k0 + i];
+    if (i >= j) cp_async8(D + j * (kBpcNB + 1) + i, A + (size_t)(k0 + j) * ld + k0 + i, true);
   }
+  cp_async_commit();
+  cp_async_wait<0>();
   __syncthreads();
   if (r >= f.nf) return;
   // row r of the panel: x L^T = a, in two 32-column halves so at most 64
