@@ -81,10 +81,30 @@ static bool cache_on() {
 // varied (up to ~0.9 s per C5 solve).  Everything else keeps a fresh
 // cudaMalloc placement -- measured: caching the build workspace or operator
 // storage made the L2-resident applies of C2 / C3 6-10% slower.
+// FETIGPU_TIMING=1 also reports every allocation / free of >= 64 MB
+// (FETIGPU_TIMING=2: only those, without the synchronising phase marks)
+static bool alloc_trace() {
+  static const bool on = [] {
+    const char* e = getenv("FETIGPU_TIMING");
+    return e && (e[0] == '1' || e[0] == '2');
+  }();
+  return on;
+}
+struct AllocTrace {
+  const char* what;
+  size_t bytes;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  ~AllocTrace() {
+    if (!alloc_trace() || bytes < (64u << 20)) return;
+    fprintf(stderr, "[fetigpu]   %s %8.1f MB %8.2f ms\n", what, bytes / 1048576.0,
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+  }
+};
 static void* dev_alloc(size_t bytes, bool cached) {
   bytes = (bytes + 511) & ~size_t(511);
   BlockCache& C = block_cache();
   if (!cached) {
+    AllocTrace tr{"cudaMalloc", bytes};
     void* p = nullptr;
     CK(cudaMalloc(&p, bytes));
     return p;
@@ -120,16 +140,18 @@ static void* dev_alloc(size_t bytes, bool cached) {
   }
   return p;
 }
-static void dev_free(void* p) {
+static void dev_free(void* p, size_t bytes = 0) {
   if (!cache_on()) {
+    AllocTrace tr{"cudaFree  ", bytes};
     cudaFree(p);
     return;
   }
   BlockCache& C = block_cache();
   std::unique_lock<std::mutex> lk(C.mu);
   auto it = C.capacity.find(p);
-  if (it == C.capacity.end()) {  // small block: plain cudaFree
+  if (it == C.capacity.end()) {  // not a cached block: plain cudaFree
     lk.unlock();
+    AllocTrace tr{"cudaFree  ", bytes};
     cudaFree(p);
     return;
   }
@@ -159,7 +181,7 @@ struct DBuf {
   ~DBuf() { release(); }
   void release() {
     if (p) {
-      dev_free(p);
+      dev_free(p, n * sizeof(T));
       g_device_bytes -= n * sizeof(T);
     }
     p = nullptr;
@@ -245,14 +267,16 @@ static void raise_smem_limit(K* func, size_t bytes) {
 struct PhaseTimer {
   bool on;
   std::chrono::steady_clock::time_point t0, last;
+  bool sync = true;  // FETIGPU_TIMING=3: host timestamps only (no stream synchronisation)
   PhaseTimer() {
     const char* e = getenv("FETIGPU_TIMING");
-    on = e && e[0] == '1';
+    on = e && (e[0] == '1' || e[0] == '3');
+    sync = !(e && e[0] == '3');
     t0 = last = std::chrono::steady_clock::now();
   }
   void mark(const char* what, cudaStream_t st) {
     if (!on) return;
-    cudaStreamSynchronize(st);
+    if (sync) cudaStreamSynchronize(st);
     const auto now = std::chrono::steady_clock::now();
     fprintf(stderr, "[fetigpu] %-28s %8.2f ms (total %8.2f)\n", what,
             std::chrono::duration<double, std::milli>(now - last).count(),
