@@ -11,6 +11,25 @@
 
 namespace fg {
 
+// host-side index maps produced by Ctx::host_maps (see ctx_build.cuh)
+struct HostMaps {
+  std::vector<int> src, ext, src_off, ext_off, fac_ne;           // slot src/ext lists
+  std::vector<OpSub> ops, pcs, pjs;                              // per subdomain
+  std::vector<int> slot_of, top_off, design, rt_off, sub_maxrow;
+  std::vector<size_t> ip_off;
+  std::vector<int> rows, top_pos, prow;                          // gather / scatter entries
+  std::vector<double> coef, pcoef, pjcoef, RT;
+  std::vector<int2> pj_sr;                                       // T-FETI projector rows
+  std::vector<double2> pj_c;
+  std::vector<double> e;
+  std::vector<double> fb, gD;                                    // rhs / recovery
+  std::vector<int> Dl, Doff, Dcnt, cpos, coff, xoff;
+  int xo = 0;
+  std::vector<DpSub> dps;                                        // FETI-DP coarse lists
+  std::vector<int> cmap, voff, optr, oidx, osub, oloc;
+  int vo = 0, to = 0;
+};
+
 struct Ctx {
   Setup su;
   Scratch scratch;
@@ -150,12 +169,16 @@ struct Ctx {
     std::vector<long long> mat_off;
     std::vector<int> mat_ld;
     std::vector<long long> abc_off, kcc_off, fac_off;
+    long long mat_total = 0, abc_total = 0, kcc_total = 0, fac_total = 0;
   };
   void run_slots(const std::vector<SlotFront>& slots, const SlotOut& out, double* mats, double sign,
                  bool nc_first, double* abc, double* kcc, double* fac, int errcode);
 
   PhaseTimer ptimer;
-  void build_ops();
+  // operator slot layout (offsets of F_s / A_bc / Kcc^s / factors per slot)
+  void plan_op_slots(SlotOut& so);
+  HostMaps host_maps(const SlotOut& so) const;
+  void build_ops(const SlotOut& so, std::future<HostMaps>& maps);
 
   void build_coarse(const SlotOut& so, const std::vector<int>& osub, const std::vector<int>& oloc);
 

@@ -255,13 +255,10 @@ void Ctx::run_slots(const std::vector<SlotFront>& slots, const SlotOut& out, dou
   check_status();
 }
 
-void Ctx::build_ops() {
-  const int Ns = su.Ns, nb = su.nb;
-  const bool dp = su.method == FETIGPU_FETIDP;
-  ptimer.mark("build_ops start", st);
-  // ---- operator slots
+void Ctx::plan_op_slots(SlotOut& so) {
   const int nslot = (int)su.op_slots.size();
-  SlotOut so;
+  KR = su.method == FETIGPU_FETIDP ? 1 : 3;
+  KRp = KR;
   long long mo = 0, ao = 0, ko = 0, fo = 0;
   op_ns.resize(nslot); op_ld.resize(nslot); op_moff.resize(nslot); op_foff.resize(nslot);
   for (int i = 0; i < nslot; ++i) {
@@ -276,34 +273,34 @@ void Ctx::build_ops() {
     max_ld = std::max(max_ld, ld);
     max_ne = std::max(max_ne, s.ne);
   }
-  d_opmat.alloc(mo);
-  d_opfac.alloc(fo);
-  if (dp) { d_abc.alloc(ao); d_kccs.alloc(ko); }
-  ptimer.mark("op slot planning", st);
-  run_slots(su.op_slots, so, d_opmat.p, -1.0, dp, dp ? d_abc.p : nullptr, dp ? d_kccs.p : nullptr,
-            d_opfac.p, dp ? FETIGPU_E_SINGULAR_REMAINDER : FETIGPU_E_NOT_POSITIVE_DEFINITE);
-  ptimer.mark("op slots (device)", st);
-  // slot src/ext lists for rhs / recovery
-  {
-    std::vector<int> src, ext, so_, eo_, fne;
-    for (auto& s : su.op_slots) {
-      so_.push_back((int)src.size());
-      eo_.push_back((int)ext.size());
-      src.insert(src.end(), s.src.begin(), s.src.end());
-      ext.insert(ext.end(), s.ext.begin(), s.ext.end());
-      fne.push_back(s.ne);
-    }
-    d_op_src.upload(src, st); d_op_ext.upload(ext, st);
-    d_op_src_off.upload(so_, st); d_op_ext_off.upload(eo_, st);
-    d_fac_ne.upload(fne, st);
-    d_fac_off.upload(so.fac_off, st);
+  so.mat_total = mo; so.abc_total = ao; so.kcc_total = ko; so.fac_total = fo;
+}
+
+// Host-only index maps of the operators, preconditioner, projector, rhs /
+// recovery and coarse problem.  They depend on the setup and the slot plan
+// only, so build() computes them on a worker thread while the device runs
+// the ND tree, and build_ops uploads them.
+// threads for the maps: they run beside the thread driving the ND launches,
+// so leave it (and the driver's threads) a share of the cores
+static int map_threads() {
+  return std::max(1, (int)std::thread::hardware_concurrency() / 2 - 1);
+}
+
+HostMaps Ctx::host_maps(const SlotOut& so) const {
+  const int Ns = su.Ns, nb = su.nb;
+  const bool dp = su.method == FETIGPU_FETIDP;
+  HostMaps h;
+  // ---- slot src/ext lists for rhs / recovery
+  for (auto& s : su.op_slots) {
+    h.src_off.push_back((int)h.src.size());
+    h.ext_off.push_back((int)h.ext.size());
+    h.src.insert(h.src.end(), s.src.begin(), s.src.end());
+    h.ext.insert(h.ext.end(), s.ext.begin(), s.ext.end());
+    h.fac_ne.push_back(s.ne);
   }
-  ptimer.mark("slot src/ext lists", st);
   // ---- per-subdomain operator maps
   // flat (subdomain, perimeter position) -> up to 3 (row, sign, weight) entries
   struct Ent { int row; double coef; double w; };
-  KR = dp ? 1 : 3;
-  KRp = KR;
   // entries are read only below ecnt[k]: no zero fill (Ns x nb x KR of them)
   std::unique_ptr<Ent[]> ent(new Ent[(size_t)Ns * nb * KR]);
   std::vector<unsigned char> ecnt((size_t)Ns * nb, 0);
@@ -317,63 +314,151 @@ void Ctx::build_ops() {
     add_ent(r.sp, su.dpos[r.dp], {i, 1.0, su.wplus[i]});
     if (r.kind == 0) add_ent(r.sm, su.dpos[r.dm], {i, -1.0, su.wminus[i]});
   }
-  ptimer.mark("maps: row entries", st);
-  std::vector<OpSub> ops(Ns), pcs(Ns), pjs(Ns);
-  std::vector<int> slot_of(Ns), top_off(Ns), design(Ns), rt_off(Ns);
-  std::vector<size_t> ip_off(Ns);
+  h.ops.resize(Ns); h.pcs.resize(Ns); h.pjs.resize(Ns);
+  h.slot_of.resize(Ns); h.top_off.resize(Ns); h.design.resize(Ns); h.rt_off.resize(Ns);
+  h.ip_off.resize(Ns);
   size_t ntop = 0, nT = 0;
   for (int s = 0; s < Ns; ++s) {  // output offsets first, so subdomains can be filled in parallel
-    top_off[s] = (int)ntop;
-    ip_off[s] = nT;
+    h.top_off[s] = (int)ntop;
+    h.ip_off[s] = nT;
     ntop += su.subs[s].Top.size();
     nT += su.subs[s].T.size();
   }
-  std::vector<int> rows(ntop * KR), prow(nT * KRp), top_pos(ntop);
-  std::vector<double> coef(ntop * KR), pcoef(nT * KRp), pjcoef(nT * KRp), RT(nT * 3);
-  sub_maxrow.assign(Ns, -1);
+  h.rows.resize(ntop * KR); h.prow.resize(nT * KRp); h.top_pos.resize(ntop);
+  h.coef.resize(ntop * KR); h.pcoef.resize(nT * KRp); h.pjcoef.resize(nT * KRp); h.RT.resize(nT * 3);
+  h.sub_maxrow.assign(Ns, -1);
   parallel_for(Ns, [&](int s) {
     const SubPlan& S = su.subs[s];
     const int sl = S.op_slot;
-    size_t io = (size_t)top_off[s], ip = ip_off[s];
-    slot_of[s] = sl;
-    design[s] = S.design;
-    ops[s] = {op_moff[sl], op_ns[sl], op_ld[sl], (int)(io * KR), 0};
+    size_t io = (size_t)h.top_off[s], ip = h.ip_off[s];
+    h.slot_of[s] = sl;
+    h.design[s] = S.design;
+    h.ops[s] = {op_moff[sl], op_ns[sl], op_ld[sl], (int)(io * KR), 0};
     int mx = -1;
     for (int t : S.Top) {
       const size_t k = (size_t)s * nb + t;
-      top_pos[io] = t;
+      h.top_pos[io] = t;
       for (int q = 0; q < KR; ++q) {
         const bool has = q < ecnt[k];
-        rows[io * KR + q] = has ? ent[k * KR + q].row : -1;
-        coef[io * KR + q] = has ? ent[k * KR + q].coef : 0.0;
-        mx = std::max(mx, rows[io * KR + q]);
+        h.rows[io * KR + q] = has ? ent[k * KR + q].row : -1;
+        h.coef[io * KR + q] = has ? ent[k * KR + q].coef : 0.0;
+        mx = std::max(mx, h.rows[io * KR + q]);
       }
       ++io;
     }
-    sub_maxrow[s] = mx;
+    h.sub_maxrow[s] = mx;
     // preconditioner / projector maps over T
-    pcs[s] = {0, (int)S.T.size(), 0, (int)(ip * KRp), 0};
-    pjs[s] = pcs[s];
-    rt_off[s] = (int)(ip * 3);
+    h.pcs[s] = {0, (int)S.T.size(), 0, (int)(ip * KRp), 0};
+    h.pjs[s] = h.pcs[s];
+    h.rt_off[s] = (int)(ip * 3);
     for (int t : S.T) {
       const size_t k = (size_t)s * nb + t;
       for (int q = 0; q < KRp; ++q) {
         const bool has = q < ecnt[k];
-        prow[ip * KRp + q] = has ? ent[k * KR + q].row : -1;
-        pcoef[ip * KRp + q] = has ? ent[k * KR + q].coef * ent[k * KR + q].w : 0.0;
-        pjcoef[ip * KRp + q] = has ? ent[k * KR + q].coef : 0.0;
+        h.prow[ip * KRp + q] = has ? ent[k * KR + q].row : -1;
+        h.pcoef[ip * KRp + q] = has ? ent[k * KR + q].coef * ent[k * KR + q].w : 0.0;
+        h.pjcoef[ip * KRp + q] = has ? ent[k * KR + q].coef : 0.0;
       }
-      for (int q = 0; q < 3; ++q) RT[ip * 3 + q] = su.Rb[(size_t)q * nb + t];
+      for (int q = 0; q < 3; ++q) h.RT[ip * 3 + q] = su.Rb[(size_t)q * nb + t];
       ++ip;
     }
-  });
-  ptimer.mark("maps: host loops", st);
-  d_oprows.upload(rows, st); d_opcoef.upload(coef, st);
-  d_slot_of.upload(slot_of, st); d_design.upload(design, st);
-  d_top_pos.upload(top_pos, st); d_top_off.upload(top_off, st);
-  d_pcrows.upload(prow, st); d_pccoef.upload(pcoef, st);
+  }, map_threads());
+  // ---- T-FETI projector: per dual row its <= 2 (subdomain, RT offset) entries, and e
+  if (!dp) {
+    h.pj_sr.assign((size_t)2 * std::max(1, su.m), make_int2(-1, 0));
+    h.pj_c.assign((size_t)std::max(1, su.m), make_double2(0.0, 0.0));
+    for (int s = 0; s < Ns; ++s)
+      for (size_t j = 0; j < su.subs[s].T.size(); ++j)
+        for (int q = 0; q < KRp; ++q) {
+          const size_t e = (h.ip_off[s] + j) * KRp + q;
+          const int r = h.prow[e];
+          if (r < 0) continue;
+          const int slot = h.pj_sr[2 * (size_t)r].x < 0 ? 0 : 1;
+          if (slot == 1 && h.pj_sr[2 * (size_t)r + 1].x >= 0)
+            fail(FETIGPU_E_STATE, "projector: more than two entries in a dual row");
+          h.pj_sr[2 * (size_t)r + slot] = make_int2(s, h.rt_off[s] + (int)j * 3);
+          (slot == 0 ? h.pj_c[r].x : h.pj_c[r].y) = h.pjcoef[e];
+        }
+    h.e.assign(3 * Ns, 0.0);  // e = -R^T f (decomposition.hpp:127)
+    for (int s = 0; s < Ns; ++s)
+      for (int k = 0; k < 3; ++k) {
+        double v = 0.0;
+        for (int i = 0; i < nb; ++i) v += su.Rb[(size_t)k * nb + i] * su.subs[s].f[i];
+        h.e[3 * s + k] = -v;
+      }
+  }
+  // ---- boundary data for rhs / recovery
+  h.xo = 0;
+  for (int s = 0; s < Ns; ++s) {
+    const SubPlan& S = su.subs[s];
+    h.fb.insert(h.fb.end(), S.f.begin(), S.f.end());
+    h.Doff.push_back((int)h.Dl.size());
+    h.Dcnt.push_back((int)S.D.size());
+    h.Dl.insert(h.Dl.end(), S.D.begin(), S.D.end());
+    h.gD.insert(h.gD.end(), S.gD.begin(), S.gD.end());
+    h.coff.push_back((int)h.cpos.size());
+    h.cpos.insert(h.cpos.end(), S.c.begin(), S.c.end());
+    h.xoff.push_back(h.xo);
+    h.xo += su.op_slots[S.op_slot].ne;
+  }
+  // ---- FETI-DP coarse index lists
+  if (dp) {
+    h.dps.resize(Ns);
+    h.optr.push_back(0);
+    std::vector<int> toff(Ns);
+    h.vo = 0;
+    h.to = 0;
+    for (int s = 0; s < Ns; ++s) {
+      const SubPlan& S = su.subs[s];
+      const int sl = S.op_slot;
+      h.dps[s].abc_off = so.abc_off[sl];
+      h.dps[s].nc = (int)S.c.size();
+      if (h.dps[s].nc > 8) fail(FETIGPU_E_STATE, "more than 8 primal DOFs per subdomain");
+      h.dps[s].cmap_off = (int)h.cmap.size();
+      h.cmap.insert(h.cmap.end(), S.cg.begin(), S.cg.end());
+      h.dps[s].v_off = h.vo;
+      h.voff.push_back(h.vo);
+      h.vo += (int)S.Top.size();
+      h.dps[s].t_off = h.to;
+      toff[s] = h.to;
+      h.to += (int)S.c.size();
+    }
+    for (int i = 0; i < su.Nc; ++i) {
+      for (auto& o : su.c_owners[i]) {
+        h.oidx.push_back(toff[o.first] + o.second);
+        h.osub.push_back(o.first);
+        h.oloc.push_back(o.second);
+      }
+      h.optr.push_back((int)h.oidx.size());
+    }
+  }
+  return h;
+}
 
-  ptimer.mark("per-subdomain maps (host)", st);
+void Ctx::build_ops(const SlotOut& so, std::future<HostMaps>& maps) {
+  const int Ns = su.Ns, nb = su.nb;
+  const bool dp = su.method == FETIGPU_FETIDP;
+  ptimer.mark("build_ops start", st);
+  // ---- operator slots
+  d_opmat.alloc(so.mat_total);
+  d_opfac.alloc(so.fac_total);
+  if (dp) { d_abc.alloc(so.abc_total); d_kccs.alloc(so.kcc_total); }
+  ptimer.mark("op slot allocation", st);
+  run_slots(su.op_slots, so, d_opmat.p, -1.0, dp, dp ? d_abc.p : nullptr, dp ? d_kccs.p : nullptr,
+            d_opfac.p, dp ? FETIGPU_E_SINGULAR_REMAINDER : FETIGPU_E_NOT_POSITIVE_DEFINITE);
+  ptimer.mark("op slots (device)", st);
+  HostMaps h = maps.get();  // normally finished long before (overlapped with the ND tree)
+  ptimer.mark("host maps (join)", st);
+  d_op_src.upload(h.src, st); d_op_ext.upload(h.ext, st);
+  d_op_src_off.upload(h.src_off, st); d_op_ext_off.upload(h.ext_off, st);
+  d_fac_ne.upload(h.fac_ne, st);
+  d_fac_off.upload(so.fac_off, st);
+  sub_maxrow = h.sub_maxrow;
+  d_oprows.upload(h.rows, st); d_opcoef.upload(h.coef, st);
+  d_slot_of.upload(h.slot_of, st); d_design.upload(h.design, st);
+  d_top_pos.upload(h.top_pos, st); d_top_off.upload(h.top_off, st);
+  d_pcrows.upload(h.prow, st); d_pccoef.upload(h.pcoef, st);
+  ptimer.mark("per-subdomain maps (upload)", st);
   // ---- preconditioner matrices
   std::vector<long long> pc_moff;
   std::vector<int> pc_ld;
@@ -441,114 +526,45 @@ void Ctx::build_ops() {
   ptimer.mark("preconditioner slots", st);
   for (int s = 0; s < Ns; ++s) {
     const int sl = su.subs[s].pc_slot;
-    pcs[s].moff = pc_moff[sl];
-    pcs[s].ld = pc_ld[sl];
+    h.pcs[s].moff = pc_moff[sl];
+    h.pcs[s].ld = pc_ld[sl];
   }
-  d_pc.upload(pcs, st);
-  d_op.upload(ops, st);
+  d_pc.upload(h.pcs, st);
+  d_op.upload(h.ops, st);
 
   // ---- T-FETI projector data
   if (!dp) {
-    d_pj.upload(pjs, st);
-    d_pjcoef.upload(pjcoef, st);
-    d_RT.upload(RT, st);
-    d_rt_off.upload(rt_off, st);
-    {  // invert the (subdomain, touched DOF) -> rows maps: per row its <= 2 entries
-      std::vector<int2> sr((size_t)2 * std::max(1, su.m), make_int2(-1, 0));
-      std::vector<double2> cc((size_t)std::max(1, su.m), make_double2(0.0, 0.0));
-      for (int s = 0; s < Ns; ++s)
-        for (size_t j = 0; j < su.subs[s].T.size(); ++j)
-          for (int q = 0; q < KRp; ++q) {
-            const size_t e = (ip_off[s] + j) * KRp + q;
-            const int r = prow[e];
-            if (r < 0) continue;
-            const int slot = sr[2 * (size_t)r].x < 0 ? 0 : 1;
-            if (slot == 1 && sr[2 * (size_t)r + 1].x >= 0)
-              fail(FETIGPU_E_STATE, "projector: more than two entries in a dual row");
-            sr[2 * (size_t)r + slot] = make_int2(s, rt_off[s] + (int)j * 3);
-            (slot == 0 ? cc[r].x : cc[r].y) = pjcoef[e];
-          }
-      d_pjrow_sr.upload(sr, st);
-      d_pjrow_c.upload(cc, st);
-    }
+    d_pj.upload(h.pjs, st);
+    d_pjcoef.upload(h.pjcoef, st);
+    d_RT.upload(h.RT, st);
+    d_rt_off.upload(h.rt_off, st);
+    d_pjrow_sr.upload(h.pj_sr, st);
+    d_pjrow_c.upload(h.pj_c, st);
     d_H.upload(su.H, st);
-    std::vector<double> e(3 * Ns, 0.0);  // e = -R^T f (decomposition.hpp:127)
-    for (int s = 0; s < Ns; ++s)
-      for (int k = 0; k < 3; ++k) {
-        double v = 0.0;
-        for (int i = 0; i < nb; ++i) v += su.Rb[(size_t)k * nb + i] * su.subs[s].f[i];
-        e[3 * s + k] = -v;
-      }
-    d_e.upload(e, st);
+    d_e.upload(h.e, st);
   }
-
   // ---- boundary data for rhs / recovery
-  {
-    std::vector<double> fb, gD;
-    std::vector<int> Dl, Doff, Dcnt, cpos, coff, xoff;
-    int xo = 0;
-    for (int s = 0; s < Ns; ++s) {
-      const SubPlan& S = su.subs[s];
-      fb.insert(fb.end(), S.f.begin(), S.f.end());
-      Doff.push_back((int)Dl.size());
-      Dcnt.push_back((int)S.D.size());
-      Dl.insert(Dl.end(), S.D.begin(), S.D.end());
-      gD.insert(gD.end(), S.gD.begin(), S.gD.end());
-      coff.push_back((int)cpos.size());
-      cpos.insert(cpos.end(), S.c.begin(), S.c.end());
-      xoff.push_back(xo);
-      xo += su.op_slots[S.op_slot].ne;
-    }
-    d_fb.upload(fb, st); d_gD.upload(gD, st);
-    d_D.upload(Dl, st); d_D_off.upload(Doff, st); d_D_cnt.upload(Dcnt, st);
-    d_c_pos.upload(cpos, st); d_c_off.upload(coff, st);
-    d_xoff.upload(xoff, st);
-    d_xb.alloc(xo);
-  }
-
+  d_fb.upload(h.fb, st); d_gD.upload(h.gD, st);
+  d_D.upload(h.Dl, st); d_D_off.upload(h.Doff, st); d_D_cnt.upload(h.Dcnt, st);
+  d_c_pos.upload(h.cpos, st); d_c_off.upload(h.coff, st);
+  d_xoff.upload(h.xoff, st);
+  d_xb.alloc(h.xo);
   // ---- FETI-DP coarse problem
   if (dp) {
-    std::vector<DpSub> dps(Ns);
-    std::vector<int> cmap, voff, optr{0}, oidx, osub, oloc;
-    int vo = 0, to = 0;
-    std::vector<int> toff(Ns);
-    for (int s = 0; s < Ns; ++s) {
-      const SubPlan& S = su.subs[s];
-      const int sl = S.op_slot;
-      dps[s].abc_off = so.abc_off[sl];
-      dps[s].nc = (int)S.c.size();
-      if (dps[s].nc > 8) fail(FETIGPU_E_STATE, "more than 8 primal DOFs per subdomain");
-      dps[s].cmap_off = (int)cmap.size();
-      cmap.insert(cmap.end(), S.cg.begin(), S.cg.end());
-      dps[s].v_off = vo;
-      voff.push_back(vo);
-      vo += (int)S.Top.size();
-      dps[s].t_off = to;
-      toff[s] = to;
-      to += (int)S.c.size();
-    }
-    for (int i = 0; i < su.Nc; ++i) {
-      for (auto& o : su.c_owners[i]) {
-        oidx.push_back(toff[o.first] + o.second);
-        osub.push_back(o.first);
-        oloc.push_back(o.second);
-      }
-      optr.push_back((int)oidx.size());
-    }
-    d_dp.upload(dps, st);
-    d_cmap.upload(cmap, st);
-    d_voff.upload(voff, st);
-    d_optr.upload(optr, st);
-    d_oidx.upload(oidx, st);
-    d_vbuf.alloc(vo);
-    d_tbuf.alloc(std::max(1, to));
-    d_fbar_loc.alloc(std::max(1, to));
+    d_dp.upload(h.dps, st);
+    d_cmap.upload(h.cmap, st);
+    d_voff.upload(h.voff, st);
+    d_optr.upload(h.optr, st);
+    d_oidx.upload(h.oidx, st);
+    d_vbuf.alloc(h.vo);
+    d_tbuf.alloc(std::max(1, h.to));
+    d_fbar_loc.alloc(std::max(1, h.to));
     d_fbar.alloc(std::max(1, su.Nc));
-    build_coarse(so, osub, oloc);
+    build_coarse(so, h.osub, h.oloc);
   }
   ptimer.mark("projector/boundary data", st);
   // ---- fold the +-1 signs of the FETI-DP constraint rows into F_s and A_bc
-  d_opcoef_apply.upload(coef, st);
+  d_opcoef_apply.upload(h.coef, st);
   if (dp) {
     const int nsl = (int)su.op_slots.size();
     slot_sign.assign(nsl, {});
@@ -556,7 +572,7 @@ void Ctx::build_ops() {
     for (int s = 0; s < Ns && ok; ++s) {
       const int sl = su.subs[s].op_slot;
       std::vector<double> sg(op_ns[sl]);
-      for (int a = 0; a < op_ns[sl]; ++a) sg[a] = coef[ops[s].map_off + a];
+      for (int a = 0; a < op_ns[sl]; ++a) sg[a] = h.coef[h.ops[s].map_off + a];
       if (slot_sign[sl].empty()) slot_sign[sl] = sg;
       else if (slot_sign[sl] != sg) ok = false;
     }
@@ -579,9 +595,9 @@ void Ctx::build_ops() {
       k_fold_signs<<<dim3(64, nsl), kThreads, 0, st>>>(dmo.p, dns.p, dld.p, dao.p, dnc.p, dso.p, dsg.p,
                                                       d_opmat.p, d_abc.p);
       LAUNCH_CHECK();
-      std::vector<double> ones(coef.size(), 1.0);
-      for (size_t i = 0; i < rows.size(); ++i)
-        if (rows[i] < 0) ones[i] = 0.0;
+      std::vector<double> ones(h.coef.size(), 1.0);
+      for (size_t i = 0; i < h.rows.size(); ++i)
+        if (h.rows[i] < 0) ones[i] = 0.0;
       d_opcoef_apply.upload(ones, st);
       CK(cudaStreamSynchronize(st));
       folded = true;
@@ -628,7 +644,7 @@ void Ctx::build_ops() {
     for (int s = 0; s < Ns; ++s) {
       const int sl = su.subs[s].op_slot;
       const int nb = (op_ns[sl] + 31) / 32;
-      ss[s] = {toff[sl], op_ns[sl], nb, ops[s].map_off, 0};
+      ss[s] = {toff[sl], op_ns[sl], nb, h.ops[s].map_off, 0};
       sym_bytes += (double)nb * (nb + 1) / 2 * 1024 * 8;
     }
     d_sym.upload(ss, st);
@@ -660,7 +676,7 @@ void Ctx::build_ops() {
     std::vector<SymSub> pss(Ns);
     for (int s = 0; s < Ns; ++s) {
       const int sl = su.subs[s].pc_slot;
-      pss[s] = {ptoff[sl], pns[sl], (pns[sl] + 31) / 32, pcs[s].map_off, 0};
+      pss[s] = {ptoff[sl], pns[sl], (pns[sl] + 31) / 32, h.pcs[s].map_off, 0};
     }
     d_pcsym.upload(pss, st);
     pc_sym_smem = pnbmax * 32 * (1 + kSymWarps) * 8;
@@ -768,13 +784,21 @@ void Ctx::build_coarse(const SlotOut& so, const std::vector<int>& osub, const st
 
 void Ctx::build() {
   ptimer = PhaseTimer();
+  SlotOut so;
+  plan_op_slots(so);
+  // host index maps on a worker thread, overlapped with the device ND tree
+  std::future<HostMaps> maps = std::async(std::launch::async, [this, &so] { return host_maps(so); });
+  struct Join {  // never leave the worker running past this frame (e.g. on a build error)
+    std::future<HostMaps>& f;
+    ~Join() { if (f.valid()) f.wait(); }
+  } join{maps};
   CK(cudaEventRecord(ev0, st));
   CK(cudaMemcpyToSymbolAsync(c_kunit, su.kunit, sizeof(su.kunit), 0, cudaMemcpyHostToDevice, st));
   build_nd();
   ptimer.mark("nested dissection", st);
   CK(cudaEventRecord(ev1, st));
   nd_ms = elapsed(ev0, ev1);
-  build_ops();
+  build_ops(so, maps);
   CK(cudaEventRecord(ev2, st));
   CK(cudaStreamSynchronize(st));
   scratch.release(kScWs);

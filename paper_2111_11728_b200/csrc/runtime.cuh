@@ -10,6 +10,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <future>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -231,11 +232,12 @@ static void launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, 
   CK(cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...));
 }
 
-// f(i) for i in [0, n) over up to 16 host threads (contiguous ranges); f must
-// write disjoint outputs.  Serial for small n.
+// f(i) for i in [0, n) over up to max_threads host threads (contiguous
+// ranges, at most the core count); f must write disjoint outputs.  Serial for
+// small n.
 template <class F>
-static void parallel_for(int n, F&& f) {
-  const int nt = std::min<int>(16, std::max(1u, std::thread::hardware_concurrency()));
+static void parallel_for(int n, F&& f, int max_threads = 16) {
+  const int nt = std::min<int>(max_threads, std::max(1u, std::thread::hardware_concurrency()));
   if (n < 64 || nt <= 1) {
     for (int i = 0; i < n; ++i) f(i);
     return;
