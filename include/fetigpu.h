@@ -228,6 +228,12 @@ int fetigpu_synchronize(fetigpu_ctx* ctx);
  * ms[1] preconditioner, ms[2] projector (identity for
  * FETI-DP; decomposition.hpp:136 for T-FETI). */
 int fetigpu_time_ops(fetigpu_ctx* ctx, int reps, double* ms);
+/* Device memory of the current device: free and total bytes (cudaMemGetInfo),
+ * and the bytes `ctx` (nullable) holds in its cache of freed RRS
+ * direction-store chunks -- reused by its next solve, returned to the driver
+ * by fetigpu_destroy.  Memory planning for the RRS store (SPEC.md:435-443:
+ * two m x k blocks per iteration). */
+int fetigpu_device_memory(fetigpu_ctx* ctx, size_t* free_bytes, size_t* total_bytes, size_t* cached_bytes);
 /* Times `reps` device-resident applies of F on ncols columns with CUDA
  * events on the context stream; ms[0] = mean per apply, ms[1] = mean of the
  * dominant kernel, ms[2] = its share; launches[0] = kernels per apply. */

@@ -123,6 +123,9 @@ struct Ctx {
   bool pipe_ready = false;
   std::vector<int> sub_maxrow;  // per subdomain: largest dual row it touches (-1: none)
 
+  // freed RRS direction-store chunks, reused by this context's next solve;
+  // returned to the driver with the context
+  BlockCache rrs_cache;
   ~Ctx() {
     for (auto& e : pipe_in) if (e) cudaEventDestroy(e);
     for (auto& e : pipe_done) if (e) cudaEventDestroy(e);

@@ -417,6 +417,14 @@ int fetigpu_synchronize(fetigpu_ctx* ctx) {
   return guarded([&] { CK(cudaStreamSynchronize(ctx->c.st)); });
 }
 
+int fetigpu_device_memory(fetigpu_ctx* ctx, size_t* free_bytes, size_t* total_bytes, size_t* cached_bytes) {
+  return guarded([&] {
+    if (!free_bytes || !total_bytes || !cached_bytes) fail(FETIGPU_E_INVALID_ARGUMENT, "null output");
+    CK(cudaMemGetInfo(free_bytes, total_bytes));
+    *cached_bytes = ctx ? ctx->c.rrs_cache.cached_bytes() : 0;
+  });
+}
+
 int fetigpu_time_ops(fetigpu_ctx* ctx, int reps, double* ms) {
   return guarded([&] {
     NEED_BUILT(ctx);

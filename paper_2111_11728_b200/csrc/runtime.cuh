@@ -49,27 +49,19 @@ namespace fg {
                cudaGetErrorString(e_));                                                        \
   } while (0)
 
-static size_t g_device_bytes = 0;
+static std::atomic<size_t> g_device_bytes{0};  // live DBuf bytes, all contexts (stats)
 
-// Device memory: cudaMalloc behind a per-device cache of large blocks.  A freed
-// block is kept and handed to a later request it fits (at most 2x larger), so
-// repeated builds and solves in one process (SIMP loops, the bench's config
-// table) reuse memory instead of paying variable cudaMalloc / cudaFree costs.
-// A release first synchronises the device (cudaFree semantics: buffers freed
-// at scope end are never still in use).  On OOM the cache is returned to the
-// driver and the allocation retried.  FETIGPU_NO_CACHE=1 disables the cache.
-struct BlockCache {
-  std::mutex mu;
-  std::multimap<size_t, void*> free_blocks;      // capacity -> block
-  std::unordered_map<void*, size_t> capacity;    // every live or cached block
-  size_t cached = 0;
-};
-static BlockCache& block_cache() {
-  static BlockCache caches[64];
-  int dev = 0;
-  cudaGetDevice(&dev);
-  return caches[dev & 63];
-}
+// Device memory.  Plain cudaMalloc / cudaFree, except for buffers that name a
+// BlockCache: a freed block is kept there and handed to a later request it
+// fits (at most 2x larger).  Only the RRS direction store uses one (each
+// context owns its cache): its multi-GB chunks are allocated per solve, and
+// that is where driver allocation cost varied (up to ~0.9 s per C5 solve).
+// Everything else keeps a fresh cudaMalloc placement -- measured: caching the
+// build workspace or operator storage made the L2-resident applies of C2 / C3
+// 6-10% slower.  A release into the cache first synchronises the device
+// (cudaFree semantics: buffers freed at scope end are never still in use).
+// On OOM the cache is returned to the driver and the allocation retried.
+// FETIGPU_NO_CACHE=1 disables caching.
 static bool cache_on() {
   static const bool on = [] {
     const char* e = getenv("FETIGPU_NO_CACHE");
@@ -77,11 +69,6 @@ static bool cache_on() {
   }();
   return on;
 }
-// Only the RRS direction store goes through the cache: its multi-GB chunks are
-// allocated and freed per solve, and that is where driver allocation cost
-// varied (up to ~0.9 s per C5 solve).  Everything else keeps a fresh
-// cudaMalloc placement -- measured: caching the build workspace or operator
-// storage made the L2-resident applies of C2 / C3 6-10% slower.
 // FETIGPU_TIMING=1 also reports every allocation / free of >= 64 MB
 // (FETIGPU_TIMING=2: only those, without the synchronising phase marks)
 static bool alloc_trace() {
@@ -101,74 +88,83 @@ struct AllocTrace {
             std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
   }
 };
-static void* dev_alloc(size_t bytes, bool cached) {
+struct BlockCache {
+  std::mutex mu;
+  std::multimap<size_t, void*> free_blocks;      // capacity -> block
+  std::unordered_map<void*, size_t> capacity;    // every live or cached block
+  size_t cached = 0;
+  // return every cached block to the driver
+  void trim() {
+    std::lock_guard<std::mutex> lk(mu);
+    if (free_blocks.empty()) return;
+    cudaDeviceSynchronize();
+    for (auto& f : free_blocks) {
+      AllocTrace tr{"cudaFree  ", f.first};
+      cudaFree(f.second);
+      capacity.erase(f.second);
+    }
+    free_blocks.clear();
+    cached = 0;
+  }
+  size_t cached_bytes() {
+    std::lock_guard<std::mutex> lk(mu);
+    return cached;
+  }
+  ~BlockCache() { trim(); }
+};
+static void* dev_alloc(size_t bytes, BlockCache* cache) {
   bytes = (bytes + 511) & ~size_t(511);
-  BlockCache& C = block_cache();
-  if (!cached) {
+  if (!cache || !cache_on()) {
     AllocTrace tr{"cudaMalloc", bytes};
     void* p = nullptr;
     CK(cudaMalloc(&p, bytes));
     return p;
   }
-  if (cache_on()) {
-    std::lock_guard<std::mutex> lk(C.mu);
-    auto it = C.free_blocks.lower_bound(bytes);
-    if (it != C.free_blocks.end() && it->first <= 2 * bytes) {
+  {
+    std::lock_guard<std::mutex> lk(cache->mu);
+    auto it = cache->free_blocks.lower_bound(bytes);
+    if (it != cache->free_blocks.end() && it->first <= 2 * bytes) {
       void* p = it->second;
-      C.cached -= it->first;
-      C.free_blocks.erase(it);
+      cache->cached -= it->first;
+      cache->free_blocks.erase(it);
       return p;
     }
   }
   void* p = nullptr;
-  cudaError_t e = cudaMalloc(&p, bytes);
-  if (e == cudaErrorMemoryAllocation && cache_on()) {  // give the cache back, retry
+  cudaError_t e;
+  {
+    AllocTrace tr{"cudaMalloc", bytes};
+    e = cudaMalloc(&p, bytes);
+  }
+  if (e == cudaErrorMemoryAllocation) {  // give the cache back, retry
     cudaGetLastError();
-    std::lock_guard<std::mutex> lk(C.mu);
-    cudaDeviceSynchronize();
-    for (auto& f : C.free_blocks) {
-      cudaFree(f.second);
-      C.capacity.erase(f.second);
-    }
-    C.free_blocks.clear();
-    C.cached = 0;
+    cache->trim();
     e = cudaMalloc(&p, bytes);
   }
   CK(e);
-  if (cache_on()) {
-    std::lock_guard<std::mutex> lk(C.mu);
-    C.capacity[p] = bytes;
-  }
+  std::lock_guard<std::mutex> lk(cache->mu);
+  cache->capacity[p] = bytes;
   return p;
 }
-static void dev_free(void* p, size_t bytes = 0) {
-  if (!cache_on()) {
-    AllocTrace tr{"cudaFree  ", bytes};
-    cudaFree(p);
-    return;
+static void dev_free(void* p, size_t bytes, BlockCache* cache) {
+  if (cache && cache_on()) {
+    std::lock_guard<std::mutex> lk(cache->mu);
+    auto it = cache->capacity.find(p);
+    if (it != cache->capacity.end()) {
+      cudaDeviceSynchronize();  // cudaFree semantics: nothing still uses the buffer
+      cache->free_blocks.emplace(it->second, p);
+      cache->cached += it->second;
+      return;
+    }
   }
-  BlockCache& C = block_cache();
-  std::unique_lock<std::mutex> lk(C.mu);
-  auto it = C.capacity.find(p);
-  if (it == C.capacity.end()) {  // not a cached block: plain cudaFree
-    lk.unlock();
-    AllocTrace tr{"cudaFree  ", bytes};
-    cudaFree(p);
-    return;
-  }
-  cudaDeviceSynchronize();  // cudaFree semantics: nothing still uses the buffer
-  C.free_blocks.emplace(it->second, p);
-  C.cached += it->second;
+  AllocTrace tr{"cudaFree  ", bytes};
+  cudaFree(p);
 }
-// free device memory including the cached blocks
-static size_t dev_free_bytes() {
+// free device memory including the blocks held in `cache`
+static size_t dev_free_bytes(BlockCache* cache = nullptr) {
   size_t freeb = 0, total = 0;
   CK(cudaMemGetInfo(&freeb, &total));
-  if (cache_on()) {
-    BlockCache& C = block_cache();
-    std::lock_guard<std::mutex> lk(C.mu);
-    freeb += C.cached;
-  }
+  if (cache) freeb += cache->cached_bytes();
   return freeb;
 }
 
@@ -182,17 +178,17 @@ struct DBuf {
   ~DBuf() { release(); }
   void release() {
     if (p) {
-      dev_free(p, n * sizeof(T));
+      dev_free(p, n * sizeof(T), cache);
       g_device_bytes -= n * sizeof(T);
     }
     p = nullptr;
     n = 0;
   }
-  bool cached = false;  // recycled scratch: allocate through the block cache
+  BlockCache* cache = nullptr;  // recycled storage: allocate through this block cache
   void alloc(size_t count) {
     release();
     if (count == 0) count = 1;
-    p = static_cast<T*>(dev_alloc(count * sizeof(T), cached));
+    p = static_cast<T*>(dev_alloc(count * sizeof(T), cache));
     n = count;
     g_device_bytes += n * sizeof(T);
   }

@@ -136,7 +136,7 @@ int Ctx::solve_rrs(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_tra
   auto append_slot = [&](int rank, double** wn, double** qn) {
     if (chunks.empty() || chunks.back().used + rank > chunks.back().cap) {
       const auto t0 = tnow();
-      size_t freeb = dev_free_bytes(), total = 0, fr0 = 0;
+      size_t freeb = dev_free_bytes(&rrs_cache), total = 0, fr0 = 0;
       CK(cudaMemGetInfo(&fr0, &total));
       const auto t1 = tnow();
       const size_t margin = std::max<size_t>(size_t(1) << 30, total / 64);
@@ -148,7 +148,7 @@ int Ctx::solve_rrs(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_tra
                                           ")");
       Chunk ch{std::unique_ptr<DBuf<double>>(new DBuf<double>), std::unique_ptr<DBuf<double>>(new DBuf<double>),
                std::unique_ptr<DBuf<double>>(new DBuf<double>), c, 0, K};
-      ch.w->cached = ch.q->cached = ch.psi->cached = true;
+      ch.w->cache = ch.q->cache = ch.psi->cache = &rrs_cache;
       ch.w->alloc((size_t)m * c);
       const auto t2 = tnow();
       ch.q->alloc((size_t)m * c);

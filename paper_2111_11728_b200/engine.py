@@ -79,7 +79,8 @@ EXPORTED = ["fetigpu_set_device", "fetigpu_create", "fetigpu_build", "fetigpu_de
             "fetigpu_host_alloc", "fetigpu_host_free", "fetigpu_memcpy", "fetigpu_fill_random",
             "fetigpu_synchronize", "fetigpu_time_apply", "fetigpu_apply_F_block_device",
             "fetigpu_time_apply_block", "fetigpu_fp64_peak", "fetigpu_selftest_dmma",
-            "fetigpu_pivoted_cholesky", "fetigpu_pivoted_compress", "fetigpu_time_ops"]
+            "fetigpu_pivoted_cholesky", "fetigpu_pivoted_compress", "fetigpu_time_ops",
+            "fetigpu_device_memory"]
 
 
 class FgProblem(C.Structure):
@@ -149,6 +150,16 @@ def fp64_peak():
     a, b = C.c_double(), C.c_double()
     check(lib().fetigpu_fp64_peak(C.byref(a), C.byref(b)))
     return a.value, b.value
+
+
+def device_memory(system=None) -> dict:
+    """Free / total device bytes, and the bytes `system` (a FetiSystem, or
+    None) holds in its cache of freed RRS direction-store chunks
+    (fetigpu_device_memory)."""
+    f, t, c = C.c_size_t(), C.c_size_t(), C.c_size_t()
+    check(lib().fetigpu_device_memory(system.h if system is not None else None, C.byref(f), C.byref(t),
+                                      C.byref(c)))
+    return {"free": f.value, "total": t.value, "cached": c.value}
 
 
 def pivoted_cholesky(a: np.ndarray, tol: float = 1e-12):

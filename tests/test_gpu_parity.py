@@ -456,3 +456,24 @@ def test_concurrent_contexts_from_two_threads():
             assert np.array_equal(y, ref[i][1])
     for g in sys_:
         g.close()
+
+
+def test_rrs_store_cache_owned_by_context():
+    """The RRS direction store is recycled through a per-context block cache:
+    a second solve on the same context reuses the chunks (same results), and
+    destroying the context returns them to the driver."""
+    from paper_2111_11728_b200 import engine
+    before = engine.device_memory()
+    g = engine.FetiSystem(pb.config5(sx=16, sy=8))     # m ~ 22k, k = 128: store chunks of ~100 MB
+    assert engine.device_memory(g)["cached"] == 0
+    lam, tr = g.solve(tol=1e-6, max_it=100, directions=2)
+    assert tr["status"] == 0
+    held = engine.device_memory(g)["cached"]
+    assert held > 0                                    # the solve's chunks went to the cache
+    lam2, _ = g.solve(tol=1e-6, max_it=100, directions=2)
+    assert np.array_equal(lam, lam2)
+    assert engine.device_memory(g)["cached"] == held   # reused, not grown
+    g.close()
+    after = engine.device_memory()
+    assert after["cached"] == 0
+    assert after["free"] >= before["free"] - (64 << 20)
