@@ -221,12 +221,13 @@ def cpu_solves():
     profiles/r01_solves_full_vs_oracle.jsonl and profiles/r01_parity_C5_full.json."""
     from oracle import pyoracle
     out = {}
-    for name, fn, dirs in (("C1", pb.config1, 0), ("C2", pb.config2, 1), ("C3-fetidp", lambda: pb.config3(method=1), 1)):
+    for name, fn, dirs in (("C1", pb.config1, 0), ("C2", pb.config2, 0), ("C2-fo", pb.config2, 1),
+                           ("C3-fetidp", lambda: pb.config3(method=1), 1)):
         t0 = time.perf_counter()
         o = pyoracle.Oracle(fn())
         tb = time.perf_counter() - t0
         t0 = time.perf_counter()
-        _, tr = o.solve(tol=1e-6, max_it=2000, directions=dirs)
+        _, tr = o.solve(tol=1e-6, max_it=6000, directions=dirs)
         out[name] = {"build_s": tb, "solve_s": time.perf_counter() - t0, "iterations": tr["iterations"],
                      "status": ["converged", "max_iter", "breakdown"][tr["status"]],
                      "directions": ["single", "fo", "rrs"][dirs]}
@@ -467,7 +468,7 @@ def main():
         g.close()
         solves = solve_table(engine, [
             ("C1", pb.config1, dict(tol=1e-6, max_it=2000, directions=0)),
-            ("C2", pb.config2, dict(tol=1e-6, max_it=2000, directions=0)),
+            ("C2", pb.config2, dict(tol=1e-6, max_it=6000, directions=0)),
             ("C2-fo", pb.config2, dict(tol=1e-6, max_it=2000, directions=1)),
             ("C3-tfeti", lambda: pb.config3(method=0), dict(tol=1e-6, max_it=2000, directions=1)),
             ("C3-fetidp", lambda: pb.config3(method=1), dict(tol=1e-6, max_it=2000, directions=1)),

@@ -21,6 +21,7 @@
 namespace fg {
 
 __constant__ double c_kunit[64];   // unit-modulus Q4 stiffness (col-major)
+constexpr int kLeafElems = 64;     // element moduli staged per pass in a leaf
 
 // Unblocked right-looking partial Cholesky of a column-major matrix in
 // shared memory: eliminates the first ne of nf DOFs (lower triangle).
@@ -65,6 +66,68 @@ __device__ void eliminate_smem(double* F, int nf, int ne, int ld, int* status, i
   }
 }
 
+// Same elimination, trailing update walked per column instead of per entry:
+// a work item is a folded column pair (p, m-1-p) (or the middle column) cut
+// into S contiguous segments, so the inner loop is a plain column run
+// (LDS c_i, LDS F, DFMA, STS) with c_j in a register and no per-entry index
+// arithmetic.  Every entry still receives F_ij - c_i c_j once per pivot in
+// pivot order, so results are bit-identical to eliminate_smem.  Lanes of a
+// warp sit in different columns: an even ld (ld + 1 odd) keeps them on
+// distinct shared-memory banks.
+__device__ void eliminate_smem_cols(double* F, int nf, int ne, int ld, int* status, int code) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int k = 0; k < ne; ++k) {
+    double* ck = F + (size_t)k * ld;
+    if (tid == 0) {
+      double d = ck[k];
+      if (!(d > 0.0)) {
+        atomicExch(status, code);
+        d = 1.0;
+      }
+      ck[k] = sqrt(d);
+    }
+    __syncthreads();
+    const double l = ck[k];
+    for (int i = k + 1 + tid; i < nf; i += nt) ck[i] = ck[i] / l;
+    __syncthreads();
+    const int m = nf - k - 1;
+    const int P = m / 2, npairs = P + (m & 1);
+    const int S = npairs > 0 ? max(1, nt / npairs) : 1;
+    const double* cc = ck + k + 1;            // trailing part of the pivot column
+    double* T = F + (size_t)(k + 1) * ld + k + 1;   // trailing block, T[jj*ld + ii]
+    for (int w = tid; w < npairs * S; w += nt) {
+      const int p = w % npairs, s = w / npairs;
+      const int len = p < P ? m + 1 : m - p;
+      const int L = (len + S - 1) / S;
+      const int q0 = s * L, q1 = min(len, q0 + L);
+      // column p: rows p + q for q < m - p
+      {
+        const int a = q0, b = min(q1, m - p);
+        if (a < b) {
+          const double cj = cc[p];
+          double* col = T + (size_t)p * ld + p;
+          const double* ci = cc + p;
+#pragma unroll 4
+          for (int q = a; q < b; ++q) col[q] = fma(-ci[q], cj, col[q]);
+        }
+      }
+      // column m-1-p: rows (m-1-p) + (q - (m-p)) for q >= m - p
+      {
+        const int a = max(q0, m - p), b = q1;
+        if (a < b) {
+          const int jj = m - 1 - p;
+          const double cj = cc[jj];
+          double* col = T + (size_t)jj * ld + jj - (m - p);
+          const double* ci = cc + jj - (m - p);
+#pragma unroll 4
+          for (int q = a; q < b; ++q) col[q] = fma(-ci[q], cj, col[q]);
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // ---------------------------------------------------------------- ND tree --
 struct NdArgs {
   const NdDev* nodes;
@@ -89,10 +152,16 @@ __device__ __forceinline__ void nd_assemble(const NdArgs& a, const NdDev& nd, in
   const int tid = threadIdx.x, nt = blockDim.x;
   if (nd.leaf) {
     const double* rho = a.dens + (size_t)(a.d0 + dl) * a.n * a.n;
-    for (int e = 0; e < nd.elem_cnt; ++e) {
-      const int eid = a.elem_ids[nd.elem_off + e];
-      // simp_modulus (fem.cpp:19-24)
-      const double E = a.Emin + pow(rho[eid], a.p) * (a.E0 - a.Emin);
+    // simp_modulus (fem.cpp:19-24), one pow per element (not per thread)
+    __shared__ double Es[kLeafElems];
+    for (int e0 = 0; e0 < nd.elem_cnt; e0 += kLeafElems) {
+    const int ecnt = min(kLeafElems, nd.elem_cnt - e0);
+    __syncthreads();
+    for (int e = tid; e < ecnt; e += nt)
+      Es[e] = a.Emin + pow(rho[a.elem_ids[nd.elem_off + e0 + e]], a.p) * (a.E0 - a.Emin);
+    __syncthreads();
+    for (int e = e0; e < e0 + ecnt; ++e) {
+      const double E = Es[e - e0];
       const int* em = a.emap + (size_t)(nd.elem_off + e) * 8;
       for (int idx = tid; idx < 64; idx += nt) {
         const int r = idx & 7, c = idx >> 3;
@@ -100,6 +169,7 @@ __device__ __forceinline__ void nd_assemble(const NdArgs& a, const NdDev& nd, in
         if (pr >= pc) F[(size_t)pc * ld + pr] += E * c_kunit[c * 8 + r];
       }
       __syncthreads();
+    }
     }
   } else {
     for (int c = 0; c < 2; ++c) {
@@ -151,7 +221,7 @@ __global__ void __launch_bounds__(kThreads) k_nd_small(NdArgs a) {
   for (int i = threadIdx.x; i < nf * nf; i += blockDim.x) F[i] = 0.0;
   __syncthreads();
   nd_assemble(a, nd, dl, F, nf);
-  eliminate_smem(F, nf, nd.ne, nf, a.status, kNotSPD);
+  eliminate_smem_cols(F, nf, nd.ne, nf, a.status, kNotSPD);
   double* out = a.ws + a.hbase[nd.height] + (long long)dl * a.hstride[nd.height] + nd.off;
   for (int i = threadIdx.x; i < nf * nf; i += blockDim.x) out[i] = F[i];
   if (a.factors) {
@@ -466,7 +536,7 @@ __global__ void __launch_bounds__(kThreads) k_front_elim_small(const FrontDesc* 
     F[idx] = A[(size_t)j * f.ld + i];
   }
   __syncthreads();
-  eliminate_smem(F, nf, f.ne, nf, status, f.code);
+  eliminate_smem_cols(F, nf, f.ne, nf, status, f.code);
   for (int idx = threadIdx.x; idx < nf * nf; idx += blockDim.x) {
     const int j = idx / nf, i = idx - j * nf;
     A[(size_t)j * f.ld + i] = F[idx];
