@@ -74,19 +74,21 @@ __device__ void eliminate_smem(double* F, int nf, int ne, int ld, int* status, i
 // pivot order, so results are bit-identical to eliminate_smem.  Lanes of a
 // warp sit in different columns: an even ld (ld + 1 odd) keeps them on
 // distinct shared-memory banks.
+__device__ __forceinline__ void pivot_sqrt(double* akk, int* status, int code) {
+  double d = *akk;
+  if (!(d > 0.0)) {
+    atomicExch(status, code);
+    d = 1.0;
+  }
+  *akk = sqrt(d);
+}
+
 __device__ void eliminate_smem_cols(double* F, int nf, int ne, int ld, int* status, int code) {
   const int tid = threadIdx.x, nt = blockDim.x;
+  if (ne > 0 && tid == 0) pivot_sqrt(F, status, code);
+  __syncthreads();
   for (int k = 0; k < ne; ++k) {
     double* ck = F + (size_t)k * ld;
-    if (tid == 0) {
-      double d = ck[k];
-      if (!(d > 0.0)) {
-        atomicExch(status, code);
-        d = 1.0;
-      }
-      ck[k] = sqrt(d);
-    }
-    __syncthreads();
     const double l = ck[k];
     for (int i = k + 1 + tid; i < nf; i += nt) ck[i] = ck[i] / l;
     __syncthreads();
@@ -95,35 +97,34 @@ __device__ void eliminate_smem_cols(double* F, int nf, int ne, int ld, int* stat
     const int S = npairs > 0 ? max(1, nt / npairs) : 1;
     const double* cc = ck + k + 1;            // trailing part of the pivot column
     double* T = F + (size_t)(k + 1) * ld + k + 1;   // trailing block, T[jj*ld + ii]
+    // thread 0 owns work item 0, whose first entry is the next pivot
+    // A[k+1][k+1]: it takes the square root right after its own updates, so
+    // one barrier per pivot is saved
     for (int w = tid; w < npairs * S; w += nt) {
       const int p = w % npairs, s = w / npairs;
       const int len = p < P ? m + 1 : m - p;
       const int L = (len + S - 1) / S;
       const int q0 = s * L, q1 = min(len, q0 + L);
-      // column p: rows p + q for q < m - p
-      {
-        const int a = q0, b = min(q1, m - p);
-        if (a < b) {
-          const double cj = cc[p];
-          double* col = T + (size_t)p * ld + p;
-          const double* ci = cc + p;
-#pragma unroll 4
-          for (int q = a; q < b; ++q) col[q] = fma(-ci[q], cj, col[q]);
+      // entries q < m - p: column p, rows p + q; then column m-1-p, rows
+      // (m-1-p) + (q - (m-p)).  One loop with a pointer switch, so lanes
+      // whose segments straddle the fold do not serialise two loops.
+      const int split = m - p;
+      int jj = q0 < split ? p : m - 1 - p;
+      int sh = q0 < split ? 0 : split;
+      double cj = cc[jj];
+      double* col = T + (size_t)jj * ld + jj - sh;
+      const double* ci = cc + jj - sh;
+      for (int q = q0; q < q1; ++q) {
+        if (q == split) {
+          jj = m - 1 - p;
+          cj = cc[jj];
+          col = T + (size_t)jj * ld + jj - split;
+          ci = cc + jj - split;
         }
-      }
-      // column m-1-p: rows (m-1-p) + (q - (m-p)) for q >= m - p
-      {
-        const int a = max(q0, m - p), b = q1;
-        if (a < b) {
-          const int jj = m - 1 - p;
-          const double cj = cc[jj];
-          double* col = T + (size_t)jj * ld + jj - (m - p);
-          const double* ci = cc + jj - (m - p);
-#pragma unroll 4
-          for (int q = a; q < b; ++q) col[q] = fma(-ci[q], cj, col[q]);
-        }
+        col[q] = fma(-ci[q], cj, col[q]);
       }
     }
+    if (tid == 0 && k + 1 < ne) pivot_sqrt(T, status, code);
     __syncthreads();
   }
 }
@@ -154,6 +155,30 @@ __device__ __forceinline__ void nd_assemble(const NdArgs& a, const NdDev& nd, in
     const double* rho = a.dens + (size_t)(a.d0 + dl) * a.n * a.n;
     // simp_modulus (fem.cpp:19-24), one pow per element (not per thread)
     __shared__ double Es[kLeafElems];
+    if (nd.elem_cnt <= kLeafElems) {
+      for (int e = tid; e < nd.elem_cnt; e += nt)
+        Es[e] = a.Emin + pow(rho[a.elem_ids[nd.elem_off + e]], a.p) * (a.E0 - a.Emin);
+      // wavefront rounds t = lx + 2 ly over the leaf's w x h elements (ey-major):
+      // elements of one round share no node, and every earlier neighbour of
+      // an element in ey-major order lies in an earlier round, so each entry
+      // still receives its element contributions in element order
+      const int e0id = a.elem_ids[nd.elem_off], eLid = a.elem_ids[nd.elem_off + nd.elem_cnt - 1];
+      const int w = eLid % a.n - e0id % a.n + 1, h = eLid / a.n - e0id / a.n + 1;
+      __syncthreads();
+      for (int t = 0; t < w + 2 * h - 2; ++t) {
+        const int ly0 = max(0, (t - w + 2) / 2), ly1 = min(h - 1, t / 2);
+        for (int idx = tid; idx < (ly1 - ly0 + 1) * 64; idx += nt) {
+          const int ly = ly0 + (idx >> 6), lx = t - 2 * ly;
+          const int e = ly * w + lx;
+          const double E = Es[e];
+          const int* em = a.emap + (size_t)(nd.elem_off + e) * 8;
+          const int r = idx & 7, c = (idx >> 3) & 7;
+          const int pr = em[r], pc = em[c];
+          if (pr >= pc) F[(size_t)pc * ld + pr] += E * c_kunit[c * 8 + r];
+        }
+        __syncthreads();
+      }
+    } else {
     for (int e0 = 0; e0 < nd.elem_cnt; e0 += kLeafElems) {
     const int ecnt = min(kLeafElems, nd.elem_cnt - e0);
     __syncthreads();
@@ -169,6 +194,7 @@ __device__ __forceinline__ void nd_assemble(const NdArgs& a, const NdDev& nd, in
         if (pr >= pc) F[(size_t)pc * ld + pr] += E * c_kunit[c * 8 + r];
       }
       __syncthreads();
+    }
     }
     }
   } else {
@@ -222,8 +248,14 @@ __global__ void __launch_bounds__(kThreads) k_nd_small(NdArgs a) {
   __syncthreads();
   nd_assemble(a, nd, dl, F, nf);
   eliminate_smem_cols(F, nf, nd.ne, nf, a.status, kNotSPD);
+  // the parent (nd_assemble) and k_nd_extract_root read only the lower
+  // triangle of the trailing (perimeter) block: write just that
   double* out = a.ws + a.hbase[nd.height] + (long long)dl * a.hstride[nd.height] + nd.off;
-  for (int i = threadIdx.x; i < nf * nf; i += blockDim.x) out[i] = F[i];
+  {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    for (int j = nd.ne + warp; j < nf; j += nw)
+      for (int i = j + lane; i < nf; i += 32) out[(size_t)j * nf + i] = F[(size_t)j * nf + i];
+  }
   if (a.factors) {
     double* fo = a.factors + (size_t)(a.d0 + dl) * a.fstride + nd.foff;
     for (int i = threadIdx.x; i < nf * nd.ne; i += blockDim.x) fo[i] = F[i];
