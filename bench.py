@@ -333,6 +333,15 @@ def solve_table(engine, configs):
                      "iterations": tr["iterations"], "status": ["converged", "max_iter", "breakdown"][tr["status"]],
                      "rel_residual": tr["eps_final"] / tr["eps0"] if tr["eps0"] > 0 else 0.0,
                      "m": st["m"], "directions": ["single", "fo", "rrs"][kw.get("directions", 0)]}
+        if kw.get("directions", 0) == 2:
+            # FETI-DP auto store (solve_rrs.cuh): the implicit store applies F to
+            # three k-column blocks per iteration, the explicit one to one
+            k = st["n_sub"]
+            out[name]["f_applies"] = tr["f_applies"]
+            out[name]["store"] = "implicit" if tr["f_applies"] > 2 * k * tr["iterations"] + 1 else "explicit"
+            out[name]["kept"] = [int(x) for x in tr["kept"][1:]]
+            out[name]["phase_ms"] = {p: round(v, 1) for p, v in zip(
+                ("FW", "gram", "pivchol", "compress", "update", "precond", "pack", "reorth"), tr["phase_ms"])}
         ops = g.time_ops(reps=200 if not name.startswith("C4") else 20)
         out[name]["per_iteration_ops_us"] = {k.replace("_ms", ""): round(v * 1e3, 2) for k, v in ops.items()}
         out[name]["us_per_iteration"] = round(tr["solve_ms"] * 1e3 / max(1, tr["iterations"]), 1)
@@ -475,6 +484,7 @@ def main():
             ("C5", pb.config5, dict(tol=1e-6, max_it=200, directions=2)),
             ("C4-cg", pb.config4, dict(tol=1e-6, max_it=3000, directions=0)),
             ("C4-fo", pb.config4, dict(tol=1e-6, max_it=3000, directions=1)),
+            ("C4-rrs", pb.config4, dict(tol=1e-6, max_it=100, directions=2)),
         ])
 
     cpu = None

@@ -311,6 +311,9 @@ struct Ctx {
 
   int solve(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_trace* tr);
   int solve_rrs(const fetigpu_solve_opts& o, double* lam, fetigpu_trace* tr);
+  int solve_rrs_implicit(const fetigpu_solve_opts& o, double* lam, fetigpu_trace* tr);
+  bool use_implicit_store(const fetigpu_solve_opts& o);
+  int rrs_store = 0;   // FETIGPU_RRS_STORE_AUTO / _EXPLICIT / _IMPLICIT
 };
 
 }  // namespace fg

@@ -212,6 +212,17 @@ int fetigpu_solve(fetigpu_ctx* ctx, const fetigpu_solve_opts* o, double* lambda,
   });
 }
 
+int fetigpu_set_rrs_store(fetigpu_ctx* ctx, int mode) {
+  return guarded([&] {
+    if (!ctx) fail(FETIGPU_E_INVALID_ARGUMENT, "null context");
+    if (mode < FETIGPU_RRS_STORE_AUTO || mode > FETIGPU_RRS_STORE_IMPLICIT)
+      fail(FETIGPU_E_INVALID_ARGUMENT, "unknown RRS store mode");
+    if (mode == FETIGPU_RRS_STORE_IMPLICIT && ctx->c.su.method != FETIGPU_FETIDP)
+      fail(FETIGPU_E_CONFIG, "the implicit RRS store needs FETI-DP (T-FETI directions are projected, dense)");
+    ctx->c.rrs_store = mode;
+  });
+}
+
 int fetigpu_recover(fetigpu_ctx* ctx, const double* lambda, double* u) {
   return guarded([&] {
     NEED_BUILT(ctx);

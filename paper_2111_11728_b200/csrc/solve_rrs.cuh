@@ -6,6 +6,142 @@
 
 namespace fg {
 
+// ------------------------------------------------ implicit direction store --
+// FETI-DP RRS with the stored directions kept as coefficients over the
+// preconditioner blocks Z_l (solve_rrs_implicit).  Z_l column s lives on the
+// dual rows of subdomain s only (the preconditioner's map), so it is stored
+// packed: ZV[l * nz + t] for the map position t of (s, a).
+
+// ZV[l * nz + t] = Z (row-major m x k) at the map positions t of each
+// subdomain's column (packed block l, column-major: appending a block never
+// moves the earlier ones)
+__global__ void k_rrs_zpack(const OpSub* __restrict__ pc, const int* __restrict__ rows,
+                            const double* __restrict__ Z, int k, double* __restrict__ ZV, long long nz, int l) {
+  const int s = blockIdx.x;
+  const OpSub d = pc[s];
+  double* zl = ZV + (size_t)l * nz;
+  for (int a = threadIdx.x; a < d.ns; a += blockDim.x) {
+    const int r = rows[d.map_off + a];
+    zl[d.map_off + a] = r >= 0 ? Z[(size_t)r * k + s] : 0.0;
+  }
+}
+
+constexpr int kZL = 16;          // Z blocks per pass of k_rrs_zgather
+constexpr int kZC = 32;          // Z blocks per register chunk of k_rrs_zscatter
+constexpr int kZRows = 64;       // map rows staged per tile in k_rrs_zscatter
+
+// X^T(c, l*k + s) = sum_a ZV[l nz + off_s + a] Y(r_a, c): the coordinates of
+// Z_l^T Y, for l in [l0, l0 + kZL) ∩ [0, nl).  Y row-major m x k, X^T column-major
+// k x (nl k).  One CTA per (column tile, subdomain, l chunk).
+__global__ void __launch_bounds__(256) k_rrs_zgather(const OpSub* __restrict__ pc, const int* __restrict__ rows,
+                                                     const double* __restrict__ ZV, long long nz, int nl,
+                                                     const double* __restrict__ Y, int k,
+                                                     double* __restrict__ XT) {
+  extern __shared__ double zs[];   // ns x kZL
+  const int s = blockIdx.y, l0 = blockIdx.z * kZL;
+  const OpSub d = pc[s];
+  const int nlc = min(kZL, nl - l0);
+  for (int idx = threadIdx.x; idx < d.ns * kZL; idx += blockDim.x) {
+    const int j = idx / d.ns, a = idx - j * d.ns;
+    zs[a * kZL + j] = j < nlc ? ZV[(size_t)(l0 + j) * nz + d.map_off + a] : 0.0;
+  }
+  __syncthreads();
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= k) return;
+  double acc[kZL];
+#pragma unroll
+  for (int j = 0; j < kZL; ++j) acc[j] = 0.0;
+  for (int a = 0; a < d.ns; ++a) {
+    const int r = rows[d.map_off + a];
+    if (r < 0) continue;
+    const double y = Y[(size_t)r * k + c];
+#pragma unroll
+    for (int j = 0; j < kZL; ++j) acc[j] = fma(zs[a * kZL + j], y, acc[j]);
+  }
+#pragma unroll
+  for (int j = 0; j < kZL; ++j)
+    if (j < nlc) XT[(size_t)((size_t)(l0 + j) * k + s) * k + c] = acc[j];
+}
+
+// D(r_a, c) += sum_l ZV[l nz + off_s + a] N^T(c, l*k + s) over the map rows of
+// subdomain s.  Per (row, column) the sum over l runs in a fixed order (chunks
+// of kZC coordinates in registers, partial sums in shared memory) and lands in
+// D with one atomic; D is zeroed and each dual row has exactly two owners, so
+// the two contributions commute exactly and D is deterministic.
+// N^T column-major k x (nl k).  Dynamic smem: kZRows x (kZC + 128) doubles.
+__global__ void __launch_bounds__(128) k_rrs_zscatter(const OpSub* __restrict__ pc, const int* __restrict__ rows,
+                                                      const double* __restrict__ ZV, long long nz, int nl,
+                                                      const double* __restrict__ NT, int k,
+                                                      double* __restrict__ D) {
+  extern __shared__ double sm[];
+  double* zs = sm;                         // kZRows x kZC
+  double* vacc = sm + kZRows * kZC;        // kZRows x 128 (row a, thread)
+  const int s = blockIdx.y;
+  const OpSub d = pc[s];
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  for (int a0 = 0; a0 < d.ns; a0 += kZRows) {
+    const int na = min(kZRows, d.ns - a0);
+    for (int a = 0; a < na; ++a) vacc[a * 128 + threadIdx.x] = 0.0;
+    for (int l0 = 0; l0 < nl; l0 += kZC) {
+      const int nlc = min(kZC, nl - l0);
+      double nr[kZC];
+#pragma unroll
+      for (int j = 0; j < kZC; ++j)
+        nr[j] = (c < k && j < nlc) ? NT[(size_t)((size_t)(l0 + j) * k + s) * k + c] : 0.0;
+      __syncthreads();
+      for (int idx = threadIdx.x; idx < na * kZC; idx += blockDim.x) {
+        const int j = idx / na, a = idx - j * na;
+        zs[a * kZC + j] = j < nlc ? ZV[(size_t)(l0 + j) * nz + d.map_off + a0 + a] : 0.0;
+      }
+      __syncthreads();
+      for (int a = 0; a < na; ++a) {
+        double v = vacc[a * 128 + threadIdx.x];
+#pragma unroll
+        for (int j = 0; j < kZC; ++j) v = fma(zs[a * kZC + j], nr[j], v);
+        vacc[a * 128 + threadIdx.x] = v;
+      }
+    }
+    if (c < k)
+      for (int a = 0; a < na; ++a) {
+        const int r = rows[d.map_off + a0 + a];
+        if (r >= 0) atomicAdd(D + (size_t)r * k + c, vacc[a * 128 + threadIdx.x]);
+      }
+    __syncthreads();
+  }
+}
+constexpr size_t kZScatterSmem = (size_t)kZRows * (kZC + 128) * 8;
+
+// column-major n x n block at ld: identity
+__global__ void k_identity_ld(double* X, int n, int ld) {
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < (long long)n * n;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int j = (int)(idx / n), i = (int)(idx - (long long)j * n);
+    X[(size_t)j * ld + i] = i == j ? 1.0 : 0.0;
+  }
+}
+
+// out(:, c) = in(:, perm[c]) for column-major blocks (rows x cols)
+__global__ void k_gather_cols_cm(const double* __restrict__ in, int ldi, const int* __restrict__ perm, int rows,
+                                 int cols, double* __restrict__ out, int ldo) {
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < (long long)rows * cols;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int c = (int)(idx / rows), i = (int)(idx - (long long)c * rows);
+    out[(size_t)c * ldo + i] = in[(size_t)perm[c] * ldi + i];
+  }
+}
+
+// yh = 0; yh[perm[c]] = y[c] for c < rank; also tp[c] = t[perm[c]] (gather)
+__global__ void k_perm_gather(const double* __restrict__ t, const int* __restrict__ perm, int rank,
+                              double* __restrict__ tp) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < rank; c += gridDim.x * blockDim.x) tp[c] = t[perm[c]];
+}
+__global__ void k_perm_scatter(const double* __restrict__ y, const int* __restrict__ perm, int rank, int k,
+                               double* __restrict__ yh) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < k; c += gridDim.x * blockDim.x) yh[c] = 0.0;
+  __syncthreads();
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < rank; c += gridDim.x * blockDim.x) yh[perm[c]] = y[c];
+}
+
 // Launch the cluster pivoted Cholesky with the smallest cluster whose
 // distributed shared memory holds the n x n Gram matrix; false if none fits
 // (n > kPivcholClusterMaxN or the cluster cannot be scheduled).
@@ -94,6 +230,7 @@ static void launch_pivchol(double* A, int n, double tol, int* perm, int* rank, i
 // Blocks are row-major (m x k, k fastest) so the K5 block apply gathers and
 // scatters whole contiguous rows; cuBLAS sees them as column-major k x m.
 int Ctx::solve_rrs(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_trace* tr) {
+  if (use_implicit_store(o)) return solve_rrs_implicit(o, lambda_host, tr);
   const int m = su.m, Ns = su.Ns;
   const int passes = std::max(1, o.reorth_passes);
   PhaseTimer pt;
@@ -324,6 +461,278 @@ int Ctx::solve_rrs(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_tra
   }
   chunks.clear();
   pt.mark("rrs store release", st);
+  return 0;
+}
+
+
+// Direction-store choice for FETI-DP RRS.  Explicit (Alg. 1 as written):
+// W_j and Q_j = F W_j stored densely, 2 m rank_j doubles per iteration, and
+// each CGS pass costs ~4 m k K flops (K stored columns).  Implicit (see
+// solve_rrs_implicit): per iteration sum_s n_s packed values plus (i+1) k
+// rank_i coefficients; each pass costs one block F-apply plus ~2 k^3 i^2
+// flops of coefficient GEMMs.  Per iteration the explicit reorthogonalization is
+// ~m k^2 i and the implicit one ~k^3 i^2, so the implicit store is cheaper
+// while i < m / k; auto takes it when m > 32 k (C2, C3, C5, paper MBB) or when
+// 32 iterations of the explicit store would not fit in free memory (C4:
+// 16.5 GB per iteration).  T-FETI always uses the explicit store (its
+// projected directions are dense).
+bool Ctx::use_implicit_store(const fetigpu_solve_opts& o) {
+  if (su.method != FETIGPU_FETIDP) return false;
+  if (rrs_store == FETIGPU_RRS_STORE_EXPLICIT) return false;
+  if (rrs_store == FETIGPU_RRS_STORE_IMPLICIT) return true;
+  const char* e = getenv("FETIGPU_RRS_STORE");
+  if (e && !strcmp(e, "explicit")) return false;
+  if (e && !strcmp(e, "implicit")) return true;
+  constexpr int kAutoIters = 32;
+  if ((long long)su.m > (long long)kAutoIters * su.Ns) return true;
+  const double need = 16.0 * su.m * (double)su.Ns * std::min(o.max_it, kAutoIters);
+  return need > 0.8 * (double)dev_free_bytes(&rrs_cache);
+}
+
+// Alg. 1 for FETI-DP (identity projector) with an implicit direction store.
+//
+// Every stored block is W_j = sum_{l<=j} Z_l M_j[l] where Z_l is the block of
+// per-subdomain preconditioned residual columns of iteration l: column s is
+// nonzero only on subdomain s's dual rows, so Z_l is kept packed (sum_s n_s
+// values instead of m k).  The re-orthogonalization coefficient of Alg. 1,
+// Psi_j = Q_j^T V with Q_j = F W_j, is formed as W_j^T (F V) (F symmetric),
+// so Q_j is never stored either: each CGS pass applies F to the current block
+// once (K5) and works on the Z coordinates,
+//     X = Zhat^T (F V)            (packed gather GEMM, k_rrs_zgather)
+//     Psi_j = M_j^T X,  N = sum_j M_j Psi_j        (cuBLAS)
+//     V <- V - Zhat N             (packed scatter GEMM, k_rrs_zscatter)
+// and the coordinates of V over Z_0..Z_{i+1} are [-sum N ; I].  The line-10/11
+// compression acts on those coordinates: M_i = C_W[:, perm] L~^{-T}; the
+// lambda / r updates use W, F W and the pivoted factor directly.
+// Memory per iteration: sum_s n_s packed values + (i+1) k x rank_i
+// coefficients, against 2 m rank_i for the explicit store (C4: 8 MB + 34 MB
+// x (i+1) against 16.5 GB).  Three K5 applies per iteration instead of one.
+// Same arithmetic as Alg. 1 up to rounding (the coefficient form of the CGS
+// products); iteration and kept-direction counts are checked against the
+// oracle in tests/test_gpu_parity.py.
+int Ctx::solve_rrs_implicit(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_trace* tr) {
+  const int m = su.m, Ns = su.Ns, k = Ns;
+  const int passes = std::max(1, o.reorth_passes);
+  PhaseTimer pt;
+  rhs();
+  std::vector<OpSub> hpc(Ns);
+  CK(cudaMemcpyAsync(hpc.data(), d_pc.p, Ns * sizeof(OpSub), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (KRp != 1) fail(FETIGPU_E_STATE, "implicit RRS store needs a one-row-per-DOF preconditioner map");
+  long long nz = 0;
+  int max_pcn = 0;
+  for (auto& d : hpc) { nz = std::max<long long>(nz, (long long)d.map_off + d.ns); max_pcn = std::max(max_pcn, d.ns); }
+  DBuf<double> lam, r, z, q, W, Qb, Dd, Delta, Linv, tvec, tp, gam, yh, ZV, XT, NT, NTot, CW, CT;
+  DBuf<int> perm, rank_d, ctl;
+  DBuf<Scal> sc;
+  DBuf<double> pivx;
+  lam.alloc(m); r.alloc(m); z.alloc(m); q.alloc(m);
+  W.alloc((size_t)m * k); Qb.alloc((size_t)m * k); Dd.alloc((size_t)m * k);
+  Delta.alloc((size_t)k * k); Linv.alloc((size_t)k * k);
+  tvec.alloc(k); tp.alloc(k); gam.alloc(k); yh.alloc(k);
+  perm.alloc(k); rank_d.alloc(1); ctl.alloc(4); pivx.alloc((size_t)k + 64);
+  sc.alloc(1);
+  sc.zero(st);
+  // packed Z blocks (column-major nz x zcap, grown by doubling) and the
+  // per-iteration coordinate scratch, grown to (i+1) k x k as i increases
+  int zcap = std::max(1, std::min(o.max_it, 8));
+  ZV.alloc((size_t)nz * zcap);
+  auto zv_block = [&](int l) {
+    if (l >= zcap) {
+      const int nc = std::max(l + 1, 2 * zcap);
+      DBuf<double> z2;
+      z2.alloc((size_t)nz * nc);
+      CK(cudaMemcpyAsync(z2.p, ZV.p, (size_t)nz * zcap * 8, cudaMemcpyDeviceToDevice, st));
+      std::swap(z2.p, ZV.p);
+      std::swap(z2.n, ZV.n);
+      zcap = nc;
+    }
+  };
+  grow(CW, (size_t)k * k);
+  std::vector<std::unique_ptr<DBuf<double>>> Mb;   // M_j: (j+1)k x rank_j, column-major
+  std::vector<int> Mrank;
+  Scal* hs = nullptr;
+  CK(cudaMallocHost(&hs, sizeof(Scal)));
+  std::unique_ptr<Scal, decltype(&cudaFreeHost)> hs_guard(hs, cudaFreeHost);
+  const double one = 1.0, mone = -1.0, zero = 0.0;
+  raise_smem_limit(k_rrs_zgather, (size_t)max_pcn * kZL * 8);
+  raise_smem_limit(k_rrs_zscatter, kZScatterSmem);
+  pt.mark("rrs-implicit setup", st);
+  CK(cudaEventRecord(ev0, st));
+  CK(cudaMemcpyAsync(lam.p, d_lam0.p, m * 8, cudaMemcpyDeviceToDevice, st));
+  apply_F(lam.p, q.p, 1, m, m);
+  int fapp = 1;
+  k_sub<<<grid_for(m), kThreads, 0, st>>>(m, d_d.p, q.p, r.p);
+  apply_precond(r.p, z.p, W.p, true);  // Alg. 1 line 2: W = Z_0
+  dots({{r.p, z.p}, {r.p, r.p}, {z.p, z.p}}, &sc.p->rz);
+  k_rrs_zpack<<<Ns, kThreads, 0, st>>>(d_pc.p, d_pcrows.p, W.p, k, ZV.p, nz, 0);
+  k_identity_ld<<<grid_for((long long)k * k), kThreads, 0, st>>>(CW.p, k, k);  // C_W = I over Z_0
+  LAUNCH_CHECK();
+  CK(cudaMemcpyAsync(hs, sc.p, sizeof(Scal), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  auto metric = [&](const Scal& sv) {
+    if (sv.rz < -1e-14 * std::sqrt(sv.rr) * std::sqrt(sv.zz))
+      fail(FETIGPU_E_NEGATIVE_INNER_PRODUCT, "r^T z < 0: preconditioner is not symmetric positive");
+    return std::sqrt(std::max(sv.rz, 0.0));
+  };
+  const double eps0 = metric(*hs);
+  double eps = eps0;
+  int it = 0, status = FETIGPU_MAX_ITER, K = 0;
+  auto push = [&](double e, int kept) {
+    if (tr && it < tr->cap) {
+      if (tr->eps) tr->eps[it] = e;
+      if (tr->kept) tr->kept[it] = kept;
+      if (tr->f_app) tr->f_app[it] = fapp;
+    }
+  };
+  push(eps0, Ns);
+  const double target = o.rel ? o.tol * eps0 : o.tol;
+  cudaEvent_t pev[9];
+  for (auto& e : pev) CK(cudaEventCreate(&e));
+  double phase[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  auto mark = [&](int i) { CK(cudaEventRecord(pev[i], st)); };
+  const char* tenv = getenv("FETIGPU_TRACE");
+  const bool trace_on = tenv && tenv[0] == '1';
+  const dim3 ggrid((k + 255) / 256, Ns, 1), sgrid((k + 127) / 128, Ns);
+  while (true) {
+    if (eps <= target) { status = FETIGPU_CONVERGED; break; }
+    if (it >= o.max_it) { status = FETIGPU_MAX_ITER; break; }
+    const int i = it;              // stored blocks 0..i-1; W has coordinates CW over Z_0..Z_i
+    const int kzi = (i + 1) * k;   // rows of CW
+    mark(0);
+    apply_F_block(W.p, k, Qb.p, k, k);  // line 7
+    fapp += k;
+    mark(1);
+    CB(cublasDgemm(cb, CUBLAS_OP_N, CUBLAS_OP_T, k, k, m, &one, Qb.p, k, W.p, k, &zero, Delta.p, k));  // line 8
+    k_mirror_lower<<<grid_for((long long)k * k), kThreads, 0, st>>>(Delta.p, k);
+    mark(2);
+    launch_pivchol(Delta.p, k, o.pivot_tol, perm.p, rank_d.p, d_status.p, ctl.p, pivx.p, st);  // line 9
+    LAUNCH_CHECK();
+    mark(3);
+    int rank = 0;
+    CK(cudaMemcpyAsync(&rank, rank_d.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    int hstat = 0;
+    CK(cudaMemcpy(&hstat, d_status.p, sizeof(int), cudaMemcpyDeviceToHost));
+    if (hstat) {
+      CK(cudaMemset(d_status.p, 0, sizeof(int)));
+      fail(FETIGPU_E_INDEFINITE_INPUT, "pivoted Cholesky: negative pivot");
+    }
+    if (rank == 0) { status = FETIGPU_BREAKDOWN; break; }
+    // lines 10-11 on the coordinates: M_i = CW[:, perm] L~^{-T}
+    launch_identity(Linv.p, rank);
+    CB(cublasDtrsm(cb, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, rank, rank,
+                   &one, Delta.p, k, Linv.p, rank));
+    Mb.emplace_back(new DBuf<double>);
+    Mb.back()->alloc((size_t)kzi * rank);
+    Mrank.push_back(rank);
+    grow(CT, (size_t)kzi * k);
+    k_gather_cols_cm<<<grid_for((long long)kzi * rank), kThreads, 0, st>>>(CW.p, kzi, perm.p, kzi, rank, CT.p,
+                                                                           kzi);
+    CB(cublasDtrmm(cb, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, kzi, rank,
+                   &one, Linv.p, rank, CT.p, kzi, Mb.back()->p, kzi));
+    K += rank;
+    mark(4);
+    // lines 13-15: gamma = L~^{-1} (W^T r)[perm], y = L~^{-T} gamma,
+    // lambda += W yh, r -= (F W) yh with yh = y scattered to perm
+    CB(cublasDgemv(cb, CUBLAS_OP_N, k, m, &one, W.p, k, r.p, 1, &zero, tvec.p, 1));
+    k_perm_gather<<<1, 1024, 0, st>>>(tvec.p, perm.p, rank, tp.p);
+    CB(cublasDgemv(cb, CUBLAS_OP_N, rank, rank, &one, Linv.p, rank, tp.p, 1, &zero, gam.p, 1));
+    CB(cublasDgemv(cb, CUBLAS_OP_T, rank, rank, &one, Linv.p, rank, gam.p, 1, &zero, tp.p, 1));
+    k_perm_scatter<<<1, 1024, 0, st>>>(tp.p, perm.p, rank, k, yh.p);
+    CB(cublasDgemv(cb, CUBLAS_OP_T, k, m, &one, W.p, k, yh.p, 1, &one, lam.p, 1));
+    CB(cublasDgemv(cb, CUBLAS_OP_T, k, m, &mone, Qb.p, k, yh.p, 1, &one, r.p, 1));
+    mark(5);
+    // line 16: Z_{i+1}
+    apply_precond(r.p, z.p, W.p, true);
+    dots({{r.p, z.p}, {r.p, r.p}, {z.p, z.p}}, &sc.p->rz);
+    mark(6);
+    CK(cudaMemcpyAsync(hs, sc.p, sizeof(Scal), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    eps = metric(*hs);
+    ++it;
+    push(eps, rank);
+    if (trace_on) {
+      float te = 0;
+      CK(cudaEventElapsedTime(&te, ev0, pev[6]));
+      fprintf(stderr, "[fetigpu] rrs-implicit it %4d  eps/eps0 %.3e  rank %5d  K %7d  t %9.1f ms\n", it,
+              eps / eps0, rank, K, te);
+    }
+    if (eps <= target || it >= o.max_it) {  // no next block needed
+      mark(7);
+      mark(8);
+    } else {
+      zv_block(it);
+      k_rrs_zpack<<<Ns, kThreads, 0, st>>>(d_pc.p, d_pcrows.p, W.p, k, ZV.p, nz, it);
+      LAUNCH_CHECK();
+      mark(7);
+      // lines 18-21 in coordinates over Z_0..Z_{it-1} (the stored blocks use
+      // Z_0..Z_{it-1}; Z_it is the new block itself)
+      const int nl = it, kz = nl * k;
+      grow(XT, (size_t)kz * k); grow(NT, (size_t)kz * k); grow(NTot, (size_t)kz * k);
+      grow(CT, (size_t)kz * k); grow(CW, (size_t)(kz + k) * k);
+      for (int p = 0; p < passes; ++p) {
+        apply_F_block(W.p, k, Qb.p, k, k);  // Y = F V
+        fapp += k;
+        k_rrs_zgather<<<dim3(ggrid.x, Ns, (nl + kZL - 1) / kZL), 256, (size_t)max_pcn * kZL * 8, st>>>(
+            d_pc.p, d_pcrows.p, ZV.p, nz, nl, Qb.p, k, XT.p);
+        LAUNCH_CHECK();
+        // Psi_j^T = X^T[:, 0:(j+1)k] M_j (k x rank_j, stored in CT at column offset sum rank),
+        // N^T = sum_j Psi_j^T M_j^T (k x (j+1)k prefixes), largest j first with beta 0
+        int off = 0;
+        std::vector<int> poff(Mb.size());
+        for (size_t j = 0; j < Mb.size(); ++j) {
+          poff[j] = off;
+          const int kj = (int)(j + 1) * k;
+          CB(cublasDgemm(cb, CUBLAS_OP_N, CUBLAS_OP_N, k, Mrank[j], kj, &one, XT.p, k, Mb[j]->p, kj, &zero,
+                         CT.p + (size_t)off * k, k));
+          off += Mrank[j];
+        }
+        for (int j = (int)Mb.size() - 1; j >= 0; --j) {
+          const int kj = (j + 1) * k;
+          const double beta = j == (int)Mb.size() - 1 ? 0.0 : 1.0;
+          CB(cublasDgemm(cb, CUBLAS_OP_N, CUBLAS_OP_T, k, kj, Mrank[j], &one, CT.p + (size_t)poff[j] * k, k,
+                         Mb[j]->p, kj, &beta, NT.p, k));
+        }
+        CK(cudaMemsetAsync(Dd.p, 0, (size_t)m * k * 8, st));
+        k_rrs_zscatter<<<sgrid, 128, kZScatterSmem, st>>>(d_pc.p, d_pcrows.p, ZV.p, nz, nl, NT.p, k, Dd.p);
+        LAUNCH_CHECK();
+        CB(cublasDaxpy(cb, (int)std::min<size_t>((size_t)m * k, (size_t)INT_MAX), &mone, Dd.p, 1, W.p, 1));
+        if ((size_t)m * k > (size_t)INT_MAX)
+          CB(cublasDaxpy(cb, (int)((size_t)m * k - INT_MAX), &mone, Dd.p + INT_MAX, 1, W.p + INT_MAX, 1));
+        if (p == 0) CK(cudaMemcpyAsync(NTot.p, NT.p, (size_t)kz * k * 8, cudaMemcpyDeviceToDevice, st));
+        else CB(cublasDaxpy(cb, kz * k, &one, NT.p, 1, NTot.p, 1));
+      }
+      // coordinates of the new W over Z_0..Z_it: [-NTot^T ; I]
+      const int kzn = (it + 1) * k;
+      CB(cublasDgeam(cb, CUBLAS_OP_T, CUBLAS_OP_N, kz, k, &mone, NTot.p, k, &zero, CW.p, kzn, CW.p, kzn));
+      k_identity_ld<<<grid_for((long long)k * k), kThreads, 0, st>>>(CW.p + kz, k, kzn);
+      LAUNCH_CHECK();
+      mark(8);
+    }
+    CK(cudaEventSynchronize(pev[8]));
+    float t = 0;
+    for (int qi = 0; qi < 8; ++qi) {
+      CK(cudaEventElapsedTime(&t, pev[qi], pev[qi + 1]));
+      phase[qi] += t;
+    }
+  }
+  for (auto& e : pev) cudaEventDestroy(e);
+  if (tr)
+    for (int qi = 0; qi < 8; ++qi) tr->phase_ms[qi] = phase[qi];
+  CK(cudaEventRecord(ev1, st));
+  const double ms = elapsed(ev0, ev1);
+  CK(cudaMemcpyAsync(lambda_host, lam.p, m * 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  pt.mark("rrs-implicit loop + readback", st);
+  if (tr) {
+    tr->status = status;
+    tr->iterations = it;
+    tr->f_applies = fapp;
+    tr->eps0 = eps0;
+    tr->eps_final = eps;
+    tr->solve_ms = ms;
+  }
   return 0;
 }
 

@@ -80,7 +80,7 @@ EXPORTED = ["fetigpu_set_device", "fetigpu_create", "fetigpu_build", "fetigpu_de
             "fetigpu_synchronize", "fetigpu_time_apply", "fetigpu_apply_F_block_device",
             "fetigpu_time_apply_block", "fetigpu_fp64_peak", "fetigpu_selftest_dmma",
             "fetigpu_pivoted_cholesky", "fetigpu_pivoted_compress", "fetigpu_time_ops",
-            "fetigpu_device_memory"]
+            "fetigpu_device_memory", "fetigpu_set_rrs_store"]
 
 
 class FgProblem(C.Structure):
@@ -308,6 +308,14 @@ class FetiSystem:
                          eps0=tr.eps0, eps_final=tr.eps_final, eps=eps[:n].copy(),
                          kept=kept[:n].copy(), f_app=fap[:n].copy(), solve_ms=tr.solve_ms,
                          phase_ms=list(tr.phase_ms))
+
+    RRS_STORE = {"auto": 0, "explicit": 1, "implicit": 2}
+
+    def set_rrs_store(self, mode: str = "auto"):
+        """Direction store of RRS solves (fetigpu_set_rrs_store): "explicit"
+        (W_j, F W_j dense, Alg. 1 as written), "implicit" (FETI-DP: W_j as
+        coefficients over the packed preconditioner blocks) or "auto"."""
+        check(lib().fetigpu_set_rrs_store(self.h, self.RRS_STORE[mode]))
 
     def recover(self, lam: np.ndarray) -> np.ndarray:
         lam = np.ascontiguousarray(lam, dtype=np.float64)

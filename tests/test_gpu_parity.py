@@ -154,6 +154,48 @@ def test_solve(name, directions, oracle_mod):
         np.testing.assert_array_equal(tg["kept"], to["kept"])
 
 
+@pytest.mark.parametrize("name", ["C2s", "C3dp_s", "C5s", "C4s", "C2_lumped"])
+def test_solve_rrs_implicit_store(name, oracle_mod):
+    """FETI-DP RRS with the implicit direction store (W_j as coefficients over
+    the packed preconditioner blocks, Q_j never stored; solve_rrs.cuh) against
+    the oracle's dense-store Alg. 1: same status, iterations +-1, identical
+    kept-direction counts, residual and displacements as close as the
+    explicit store's."""
+    g, o, r = systems(name, oracle_mod)
+    kw = dict(tol=1e-6, max_it=60, directions=2)
+    g.set_rrs_store("explicit")
+    le, te = g.solve(**kw)
+    g.set_rrs_store("implicit")
+    try:
+        li, ti = g.solve(**kw)
+    finally:
+        g.set_rrs_store("auto")
+    lo, to = o.solve(**kw)
+    print(name, "iters implicit", ti["iterations"], "explicit", te["iterations"], "oracle", to["iterations"])
+    assert ti["status"] == to["status"] == 0
+    assert abs(ti["iterations"] - to["iterations"]) <= 1
+    np.testing.assert_array_equal(ti["kept"], to["kept"])
+    assert ti["f_applies"] > te["f_applies"]           # three block applies per iteration
+    d, _ = o.rhs()
+    res_i = np.linalg.norm(d - o.apply_F(li))
+    res_o = np.linalg.norm(d - o.apply_F(lo))
+    assert res_i <= 10 * res_o + 1e-14
+    ui, ue, uo = g.recover(li), g.recover(le), o.recover(lo)
+    assert rel(ui, uo) <= 10 * rel(ue, uo) + 1e-12
+
+
+def test_rrs_store_modes(oracle_mod):
+    """The implicit store is FETI-DP only; unknown modes are rejected."""
+    from paper_2111_11728_b200 import engine
+    g, _, _ = systems("C3tf_s", oracle_mod)
+    with pytest.raises(engine.ConfigError):
+        g.set_rrs_store("implicit")
+    with pytest.raises(KeyError):
+        g.set_rrs_store("bogus")
+    g.set_rrs_store("explicit")
+    g.set_rrs_store("auto")
+
+
 @pytest.mark.parametrize("name", list(CASES))
 def test_recover(name, oracle_mod):
     g, o, r = systems(name, oracle_mod)
@@ -465,6 +507,7 @@ def test_rrs_store_cache_owned_by_context():
     from paper_2111_11728_b200 import engine
     before = engine.device_memory()
     g = engine.FetiSystem(pb.config5(sx=16, sy=8))     # m ~ 22k, k = 128: store chunks of ~100 MB
+    g.set_rrs_store("explicit")                        # auto would pick the implicit store (m > 32 k)
     assert engine.device_memory(g)["cached"] == 0
     lam, tr = g.solve(tol=1e-6, max_it=100, directions=2)
     assert tr["status"] == 0
@@ -477,3 +520,20 @@ def test_rrs_store_cache_owned_by_context():
     after = engine.device_memory()
     assert after["cached"] == 0
     assert after["free"] >= before["free"] - (64 << 20)
+
+
+def test_rrs_implicit_store_deterministic():
+    """Two implicit-store RRS solves on one context are bitwise identical (the
+    packed scatter sums each row's two owner contributions in a zeroed buffer),
+    use no cached direction chunks, and leave no device memory behind."""
+    from paper_2111_11728_b200 import engine
+    before = engine.device_memory()
+    g = engine.FetiSystem(pb.config5(sx=16, sy=8))
+    g.set_rrs_store("implicit")
+    lam, tr = g.solve(tol=1e-6, max_it=100, directions=2)
+    lam2, tr2 = g.solve(tol=1e-6, max_it=100, directions=2)
+    assert tr["status"] == 0 and tr["iterations"] == tr2["iterations"]
+    assert np.array_equal(lam, lam2)
+    assert engine.device_memory(g)["cached"] == 0
+    g.close()
+    assert engine.device_memory()["free"] >= before["free"] - (64 << 20)
