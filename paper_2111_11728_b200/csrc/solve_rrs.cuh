@@ -28,7 +28,7 @@ __global__ void k_rrs_zpack(const OpSub* __restrict__ pc, const int* __restrict_
 
 constexpr int kZL = 16;          // Z blocks per pass of k_rrs_zgather
 constexpr int kZC = 32;          // Z blocks per register chunk of k_rrs_zscatter
-constexpr int kZRows = 64;       // map rows staged per tile in k_rrs_zscatter
+constexpr int kZRows = 32;       // map rows staged per tile in k_rrs_zscatter
 
 // X^T(c, l*k + s) = sum_a ZV[l nz + off_s + a] Y(r_a, c): the coordinates of
 // Z_l^T Y, for l in [l0, l0 + kZL) ∩ [0, nl).  Y row-major m x k, X^T column-major
@@ -37,24 +37,36 @@ __global__ void __launch_bounds__(256) k_rrs_zgather(const OpSub* __restrict__ p
                                                      const double* __restrict__ ZV, long long nz, int nl,
                                                      const double* __restrict__ Y, int k,
                                                      double* __restrict__ XT) {
-  extern __shared__ double zs[];   // ns x kZL
+  extern __shared__ double zs[];   // ns x kZL, then ns row ids
   const int s = blockIdx.y, l0 = blockIdx.z * kZL;
   const OpSub d = pc[s];
+  int* rs = reinterpret_cast<int*>(zs + (size_t)d.ns * kZL);
   const int nlc = min(kZL, nl - l0);
   for (int idx = threadIdx.x; idx < d.ns * kZL; idx += blockDim.x) {
     const int j = idx / d.ns, a = idx - j * d.ns;
     zs[a * kZL + j] = j < nlc ? ZV[(size_t)(l0 + j) * nz + d.map_off + a] : 0.0;
   }
+  for (int a = threadIdx.x; a < d.ns; a += blockDim.x) rs[a] = rows[d.map_off + a];
   __syncthreads();
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= k) return;
   double acc[kZL];
 #pragma unroll
   for (int j = 0; j < kZL; ++j) acc[j] = 0.0;
-  for (int a = 0; a < d.ns; ++a) {
-    const int r = rows[d.map_off + a];
-    if (r < 0) continue;
-    const double y = Y[(size_t)r * k + c];
+  // four row loads in flight per step; rows with r < 0 contribute y = 0, which
+  // leaves acc unchanged (fma(z, 0, acc) == acc for finite z)
+  int a = 0;
+  for (; a + 4 <= d.ns; a += 4) {
+    double y[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) y[u] = rs[a + u] >= 0 ? Y[(size_t)rs[a + u] * k + c] : 0.0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int j = 0; j < kZL; ++j) acc[j] = fma(zs[(a + u) * kZL + j], y[u], acc[j]);
+  }
+  for (; a < d.ns; ++a) {
+    const double y = rs[a] >= 0 ? Y[(size_t)rs[a] * k + c] : 0.0;
 #pragma unroll
     for (int j = 0; j < kZL; ++j) acc[j] = fma(zs[a * kZL + j], y, acc[j]);
   }
@@ -555,7 +567,7 @@ int Ctx::solve_rrs_implicit(const fetigpu_solve_opts& o, double* lambda_host, fe
   CK(cudaMallocHost(&hs, sizeof(Scal)));
   std::unique_ptr<Scal, decltype(&cudaFreeHost)> hs_guard(hs, cudaFreeHost);
   const double one = 1.0, mone = -1.0, zero = 0.0;
-  raise_smem_limit(k_rrs_zgather, (size_t)max_pcn * kZL * 8);
+  raise_smem_limit(k_rrs_zgather, (size_t)max_pcn * (kZL * 8 + 4));
   raise_smem_limit(k_rrs_zscatter, kZScatterSmem);
   pt.mark("rrs-implicit setup", st);
   CK(cudaEventRecord(ev0, st));
@@ -674,7 +686,7 @@ int Ctx::solve_rrs_implicit(const fetigpu_solve_opts& o, double* lambda_host, fe
       for (int p = 0; p < passes; ++p) {
         apply_F_block(W.p, k, Qb.p, k, k);  // Y = F V
         fapp += k;
-        k_rrs_zgather<<<dim3(ggrid.x, Ns, (nl + kZL - 1) / kZL), 256, (size_t)max_pcn * kZL * 8, st>>>(
+        k_rrs_zgather<<<dim3(ggrid.x, Ns, (nl + kZL - 1) / kZL), 256, (size_t)max_pcn * (kZL * 8 + 4), st>>>(
             d_pc.p, d_pcrows.p, ZV.p, nz, nl, Qb.p, k, XT.p);
         LAUNCH_CHECK();
         // Psi_j^T = X^T[:, 0:(j+1)k] M_j (k x rank_j, stored in CT at column offset sum rank),
