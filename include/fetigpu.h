@@ -186,9 +186,9 @@ int fetigpu_solve(fetigpu_ctx* ctx, const fetigpu_solve_opts* o, double* lambda,
  * dense store, 2 m rank_j doubles per iteration.  IMPLICIT (FETI-DP only):
  * each W_j kept as coefficients over the packed per-subdomain preconditioner
  * blocks, Q_j never stored, three block F-applies per iteration.  AUTO
- * (default): implicit for FETI-DP when m > 32 N_s or when 32 iterations of
- * the explicit store would not fit in free device memory; explicit otherwise
- * and always for T-FETI.  Env override FETIGPU_RRS_STORE=explicit|implicit
+ * (default): implicit for FETI-DP when N_s >= 256 and m > 32 N_s, or when 32
+ * iterations of the explicit store would not fit in free device memory;
+ * explicit otherwise and always for T-FETI.  Env override FETIGPU_RRS_STORE=explicit|implicit
  * applies under AUTO. */
 enum { FETIGPU_RRS_STORE_AUTO = 0, FETIGPU_RRS_STORE_EXPLICIT = 1, FETIGPU_RRS_STORE_IMPLICIT = 2 };
 int fetigpu_set_rrs_store(fetigpu_ctx* ctx, int mode);

@@ -484,10 +484,14 @@ int Ctx::solve_rrs(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_tra
 // rank_i coefficients; each pass costs one block F-apply plus ~2 k^3 i^2
 // flops of coefficient GEMMs.  Per iteration the explicit reorthogonalization is
 // ~m k^2 i and the implicit one ~k^3 i^2, so the implicit store is cheaper
-// while i < m / k; auto takes it when m > 32 k (C2, C3, C5, paper MBB) or when
-// 32 iterations of the explicit store would not fit in free memory (C4:
-// 16.5 GB per iteration).  T-FETI always uses the explicit store (its
-// projected directions are dense).
+// while i < m / k -- once k is large enough that the implicit store's extra
+// launches (2 block applies and ~4i coefficient GEMMs per iteration) do not
+// dominate.  Measured (warm, tools/rrs_store_rep.py): C5 (k = 512) 176-200 ms
+// implicit vs 446 ms explicit; C2 (k = 32) 37 vs 17-23 ms; C3 FETI-DP (k = 128)
+// 21 vs 17.5 ms.  Auto therefore takes the implicit store when k >= 256 and
+// m > 32 k, or when 32 iterations of the explicit store would not fit in free
+// memory (C4: 16.5 GB per iteration).  T-FETI always uses the explicit store
+// (its projected directions are dense).
 bool Ctx::use_implicit_store(const fetigpu_solve_opts& o) {
   if (su.method != FETIGPU_FETIDP) return false;
   if (rrs_store == FETIGPU_RRS_STORE_EXPLICIT) return false;
@@ -496,7 +500,7 @@ bool Ctx::use_implicit_store(const fetigpu_solve_opts& o) {
   if (e && !strcmp(e, "explicit")) return false;
   if (e && !strcmp(e, "implicit")) return true;
   constexpr int kAutoIters = 32;
-  if ((long long)su.m > (long long)kAutoIters * su.Ns) return true;
+  if (su.Ns >= 256 && (long long)su.m > (long long)kAutoIters * su.Ns) return true;
   const double need = 16.0 * su.m * (double)su.Ns * std::min(o.max_it, kAutoIters);
   return need > 0.8 * (double)dev_free_bytes(&rrs_cache);
 }
@@ -561,8 +565,29 @@ int Ctx::solve_rrs_implicit(const fetigpu_solve_opts& o, double* lambda_host, fe
     }
   };
   grow(CW, (size_t)k * k);
-  std::vector<std::unique_ptr<DBuf<double>>> Mb;   // M_j: (j+1)k x rank_j, column-major
+  // M_j ((j+1)k x rank_j, column-major) carved from arena chunks whose sizes
+  // double, and coordinate scratch grown geometrically: no device allocation
+  // (and none of the driver's occasional 100 ms cudaMalloc stalls) in most
+  // iterations
+  std::vector<std::unique_ptr<DBuf<double>>> Mchunks;
+  size_t mc_used = 0;
+  std::vector<double*> Mb;
   std::vector<int> Mrank;
+  auto m_alloc = [&](size_t n) {
+    if (Mchunks.empty() || mc_used + n > Mchunks.back()->n) {
+      const size_t cap_n = std::max(n, Mchunks.empty() ? n * 4 : 2 * Mchunks.back()->n);
+      Mchunks.emplace_back(new DBuf<double>);
+      Mchunks.back()->alloc(cap_n);
+      mc_used = 0;
+    }
+    double* p0 = Mchunks.back()->p + mc_used;
+    mc_used += (n + 31) & ~size_t(31);
+    return p0;
+  };
+  auto grow2 = [](DBuf<double>& b, size_t n) {
+    if (b.n < n) b.alloc(std::max(n, 2 * b.n));
+    return b.p;
+  };
   Scal* hs = nullptr;
   CK(cudaMallocHost(&hs, sizeof(Scal)));
   std::unique_ptr<Scal, decltype(&cudaFreeHost)> hs_guard(hs, cudaFreeHost);
@@ -615,7 +640,14 @@ int Ctx::solve_rrs_implicit(const fetigpu_solve_opts& o, double* lambda_host, fe
     apply_F_block(W.p, k, Qb.p, k, k);  // line 7
     fapp += k;
     mark(1);
-    CB(cublasDgemm(cb, CUBLAS_OP_N, CUBLAS_OP_T, k, k, m, &one, Qb.p, k, W.p, k, &zero, Delta.p, k));  // line 8
+    // line 8 on coordinates: Delta = Q^T W = (Zhat^T Q)^T C_W over Z_0..Z_i --
+    // a packed gather plus a (i+1)k-deep GEMM instead of an m-deep one (C4:
+    // 2 (i+1) k^3 against 2 m k^2 flops)
+    grow2(XT, (size_t)kzi * k);
+    k_rrs_zgather<<<dim3(ggrid.x, Ns, (i + 1 + kZL - 1) / kZL), 256, (size_t)max_pcn * (kZL * 8 + 4), st>>>(
+        d_pc.p, d_pcrows.p, ZV.p, nz, i + 1, Qb.p, k, XT.p);
+    LAUNCH_CHECK();
+    CB(cublasDgemm(cb, CUBLAS_OP_N, CUBLAS_OP_N, k, k, kzi, &one, XT.p, k, CW.p, kzi, &zero, Delta.p, k));
     k_mirror_lower<<<grid_for((long long)k * k), kThreads, 0, st>>>(Delta.p, k);
     mark(2);
     launch_pivchol(Delta.p, k, o.pivot_tol, perm.p, rank_d.p, d_status.p, ctl.p, pivx.p, st);  // line 9
@@ -635,14 +667,13 @@ int Ctx::solve_rrs_implicit(const fetigpu_solve_opts& o, double* lambda_host, fe
     launch_identity(Linv.p, rank);
     CB(cublasDtrsm(cb, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, rank, rank,
                    &one, Delta.p, k, Linv.p, rank));
-    Mb.emplace_back(new DBuf<double>);
-    Mb.back()->alloc((size_t)kzi * rank);
+    Mb.push_back(m_alloc((size_t)kzi * rank));
     Mrank.push_back(rank);
-    grow(CT, (size_t)kzi * k);
+    grow2(CT, (size_t)kzi * k);
     k_gather_cols_cm<<<grid_for((long long)kzi * rank), kThreads, 0, st>>>(CW.p, kzi, perm.p, kzi, rank, CT.p,
                                                                            kzi);
     CB(cublasDtrmm(cb, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, kzi, rank,
-                   &one, Linv.p, rank, CT.p, kzi, Mb.back()->p, kzi));
+                   &one, Linv.p, rank, CT.p, kzi, Mb.back(), kzi));
     K += rank;
     mark(4);
     // lines 13-15: gamma = L~^{-1} (W^T r)[perm], y = L~^{-T} gamma,
@@ -681,8 +712,8 @@ int Ctx::solve_rrs_implicit(const fetigpu_solve_opts& o, double* lambda_host, fe
       // lines 18-21 in coordinates over Z_0..Z_{it-1} (the stored blocks use
       // Z_0..Z_{it-1}; Z_it is the new block itself)
       const int nl = it, kz = nl * k;
-      grow(XT, (size_t)kz * k); grow(NT, (size_t)kz * k); grow(NTot, (size_t)kz * k);
-      grow(CT, (size_t)kz * k); grow(CW, (size_t)(kz + k) * k);
+      grow2(XT, (size_t)kz * k); grow2(NT, (size_t)kz * k); grow2(NTot, (size_t)kz * k);
+      grow2(CT, (size_t)kz * k); grow2(CW, (size_t)(kz + k) * k);
       for (int p = 0; p < passes; ++p) {
         apply_F_block(W.p, k, Qb.p, k, k);  // Y = F V
         fapp += k;
@@ -696,7 +727,7 @@ int Ctx::solve_rrs_implicit(const fetigpu_solve_opts& o, double* lambda_host, fe
         for (size_t j = 0; j < Mb.size(); ++j) {
           poff[j] = off;
           const int kj = (int)(j + 1) * k;
-          CB(cublasDgemm(cb, CUBLAS_OP_N, CUBLAS_OP_N, k, Mrank[j], kj, &one, XT.p, k, Mb[j]->p, kj, &zero,
+          CB(cublasDgemm(cb, CUBLAS_OP_N, CUBLAS_OP_N, k, Mrank[j], kj, &one, XT.p, k, Mb[j], kj, &zero,
                          CT.p + (size_t)off * k, k));
           off += Mrank[j];
         }
@@ -704,7 +735,7 @@ int Ctx::solve_rrs_implicit(const fetigpu_solve_opts& o, double* lambda_host, fe
           const int kj = (j + 1) * k;
           const double beta = j == (int)Mb.size() - 1 ? 0.0 : 1.0;
           CB(cublasDgemm(cb, CUBLAS_OP_N, CUBLAS_OP_T, k, kj, Mrank[j], &one, CT.p + (size_t)poff[j] * k, k,
-                         Mb[j]->p, kj, &beta, NT.p, k));
+                         Mb[j], kj, &beta, NT.p, k));
         }
         CK(cudaMemsetAsync(Dd.p, 0, (size_t)m * k * 8, st));
         k_rrs_zscatter<<<sgrid, 128, kZScatterSmem, st>>>(d_pc.p, d_pcrows.p, ZV.p, nz, nl, NT.p, k, Dd.p);
