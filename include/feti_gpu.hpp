@@ -139,6 +139,9 @@ class DualSystem {
     }
     return lam;
   }
+  // RRS direction store (FETIGPU_RRS_STORE_AUTO / _EXPLICIT / _IMPLICIT, fetigpu.h);
+  // the reference has no counterpart (it always stores W_j, Q_j densely)
+  void set_rrs_store(int mode) { check(fetigpu_set_rrs_store(ctx_, mode)); }
   // recover_primal: per-subdomain displacements
   std::vector<std::vector<double>> recover_primal(const std::vector<double>& lambda) const {
     std::vector<double> u((size_t)n_sub_ * local_dofs_);

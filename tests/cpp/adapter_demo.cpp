@@ -29,6 +29,7 @@ int main() {
     fetigpu::DualSystem sys(p);
     std::printf("dual size %d\n", sys.dual_size());
     sys.build();
+    sys.set_rrs_store(FETIGPU_RRS_STORE_AUTO);  // T-FETI: the explicit (reference) store
     std::vector<double> x(sys.dual_size(), 1.0);
     auto y = sys.apply(x);
     fetigpu::SolveOptions o;
