@@ -691,11 +691,11 @@ __global__ void __launch_bounds__(kThreads) k_fo_psi(const double* __restrict__ 
 // 32 rows per CTA (lane <-> row, coalesced per column), the 8 warps split the
 // columns j = warp, warp+8, ...; partial sums reduced over warps in fixed order.
 __global__ void __launch_bounds__(256) k_fo_sub(const double* __restrict__ W, int m,
-                                                const int* __restrict__ cnt,
+                                                const int* __restrict__ cnt, int plus,
                                                 const double* __restrict__ psi,
                                                 double* __restrict__ w) {
   pdl_wait();
-  const int c = *cnt;
+  const int c = *cnt + plus;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int i = blockIdx.x * 32 + lane;
   __shared__ double part[8][33];
@@ -728,13 +728,13 @@ __global__ void __launch_bounds__(256) k_fo_sub(const double* __restrict__ W, in
 // k_fo_psi_sum adds the S partials of each column in fixed order (skipped
 // when S == 1, where the caller passes psi itself as the partial buffer).
 __global__ void __launch_bounds__(256) k_fo_psi_seg(const double* __restrict__ Q, int m,
-                                                    const int* __restrict__ cnt,
+                                                    const int* __restrict__ cnt, int plus,
                                                     const double* __restrict__ w,
                                                     double* __restrict__ partial, int S) {
   pdl_wait();
   // fixed grid, grid-stride over the live (column j, segment s) items: no
   // empty CTAs for the not-yet-stored directions (the graph is static)
-  const int items = *cnt * S;
+  const int items = (*cnt + plus) * S;
   const int chunk = (m + S - 1) / S;
   __shared__ double red[8];
   for (int item = blockIdx.x; item < items; item += gridDim.x) {
@@ -767,10 +767,10 @@ __global__ void __launch_bounds__(256) k_fo_psi_seg(const double* __restrict__ Q
     __syncthreads();
   }
 }
-__global__ void k_fo_psi_sum(const int* __restrict__ cnt, int S, const double* __restrict__ partial,
+__global__ void k_fo_psi_sum(const int* __restrict__ cnt, int plus, int S, const double* __restrict__ partial,
                              double* __restrict__ psi) {
   pdl_wait();
-  const int c = *cnt;
+  const int c = *cnt + plus;
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < c; j += gridDim.x * blockDim.x) {
     double t = 0.0;
     for (int s = 0; s < S; ++s) t += partial[(size_t)j * S + s];
@@ -778,10 +778,15 @@ __global__ void k_fo_psi_sum(const int* __restrict__ cnt, int S, const double* _
   }
 }
 
-// also re-zeroes q (last reader this iteration) for the next apply's scatter
+// also re-zeroes q (last reader this iteration) for the next apply's scatter,
+// and starts the next direction: w <- z (element-wise after its store, so no
+// separate copy node).  Column *cnt is written; the count itself is advanced
+// at the end of the iteration (k_iter_control or k_inc), so the CGS kernels in
+// between read *cnt + 1.
 __global__ void k_fo_store2(int n, const Scal* sc, const int* __restrict__ cnt,
-                            const double* __restrict__ w, double* __restrict__ q,
-                            double* __restrict__ Wst, double* __restrict__ Qst) {
+                            double* __restrict__ w, double* __restrict__ q,
+                            double* __restrict__ Wst, double* __restrict__ Qst,
+                            const double* __restrict__ z) {
   pdl_wait();
   const double inv = 1.0 / sqrt(sc->delta);
   const int j = *cnt;
@@ -789,6 +794,7 @@ __global__ void k_fo_store2(int n, const Scal* sc, const int* __restrict__ cnt,
     Wst[(size_t)j * n + i] = w[i] * inv;
     Qst[(size_t)j * n + i] = q[i] * inv;
     q[i] = 0.0;
+    w[i] = z[i];
   }
 }
 __global__ void k_inc(int* cnt) {
@@ -818,8 +824,9 @@ struct IterCtl {
   double eps, target;
 };
 __global__ void k_iter_control(const Scal* __restrict__ sc, IterCtl* __restrict__ c, double* __restrict__ trace,
-                               cudaGraphConditionalHandle h) {
+                               cudaGraphConditionalHandle h, int* fo_cnt) {
   pdl_wait();
+  if (fo_cnt) *fo_cnt += 1;   // FO: the direction stored this iteration
   unsigned int go = 0;
   if (sc->breakdown != 0.0) {
     c->status = 2;  // FETIGPU_BREAKDOWN

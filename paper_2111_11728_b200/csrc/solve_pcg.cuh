@@ -103,19 +103,18 @@ int Ctx::solve(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_trace* 
     project(z.p, 1, m);
     dots({{r.p, z.p}, {r.p, r.p}, {z.p, z.p}}, &sc.p->rz);
     if (fo) {
-      launch_pdl(k_fo_store2, grid_for(m), kThreads, 0, st, m, (const Scal*)sc.p, (const int*)cnt.p,
-                 (const double*)w.p, q.p, Wst.p, Qst.p);
-      launch_pdl(k_inc, 1, 1, 0, st, cnt.p);
-      CK(cudaMemcpyAsync(w.p, z.p, m * 8, cudaMemcpyDeviceToDevice, st));
+      launch_pdl(k_fo_store2, grid_for(m), kThreads, 0, st, m, (const Scal*)sc.p, (const int*)cnt.p, w.p, q.p,
+                 Wst.p, Qst.p, (const double*)z.p);
       for (int pss = 0; pss < passes; ++pss) {
-        launch_pdl(k_fo_psi_seg, fo_seg_grid, 256, 0, st, (const double*)Qst.p, m, (const int*)cnt.p,
+        launch_pdl(k_fo_psi_seg, fo_seg_grid, 256, 0, st, (const double*)Qst.p, m, (const int*)cnt.p, 1,
                    (const double*)w.p, psi_S == 1 ? psi.p : psi_part.p, psi_S);
         if (psi_S > 1)
-          launch_pdl(k_fo_psi_sum, (cap + 255) / 256, 256, 0, st, (const int*)cnt.p, psi_S,
+          launch_pdl(k_fo_psi_sum, (cap + 255) / 256, 256, 0, st, (const int*)cnt.p, 1, psi_S,
                      (const double*)psi_part.p, psi.p);
-        launch_pdl(k_fo_sub, (m + 31) / 32, 256, 0, st, (const double*)Wst.p, m, (const int*)cnt.p,
+        launch_pdl(k_fo_sub, (m + 31) / 32, 256, 0, st, (const double*)Wst.p, m, (const int*)cnt.p, 1,
                    (const double*)psi.p, w.p);
       }
+      if (readback) launch_pdl(k_inc, 1, 1, 0, st, cnt.p);   // host loop; the device loop's k_iter_control advances it
     } else {
       launch_pdl(k_cg_dir2, grid_for(m), kThreads, 0, st, m, sc.p, (const double*)z.p, w.p, q.p);
       launch_pdl(k_shift_rz, 1, 1, 0, st, sc.p);
@@ -163,7 +162,8 @@ int Ctx::solve(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_trace* 
           if (cudaStreamBeginCaptureToGraph(st, bodyg, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal) ==
               cudaSuccess) {
             body(false);
-            launch_pdl(k_iter_control, 1, 1, 0, st, (const Scal*)sc.p, dctl.p, dtrace.p, hcond);
+            launch_pdl(k_iter_control, 1, 1, 0, st, (const Scal*)sc.p, dctl.p, dtrace.p, hcond,
+                       fo ? cnt.p : (int*)nullptr);
             cudaGraph_t captured = nullptr;
             built_ok = cudaStreamEndCapture(st, &captured) == cudaSuccess &&
                        cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess;
