@@ -161,7 +161,7 @@ void Ctx::build_nd() {
         a.level_nodes = dsm[h].p;
         dim3 grid((unsigned)hsmall[h].size(), dc);
         const int thr = hnfmax[h] <= 64 ? 64 : (hnfmax[h] <= 96 ? 128 : kThreads);
-        k_nd_small<<<grid, thr, hnfmax[h] * hnfmax[h] * 8, st>>>(a);
+        k_nd_small<<<grid, thr, hnfmax[h] * (hnfmax[h] + 1) / 2 * 8, st>>>(a);
         LAUNCH_CHECK();
       }
       if (!hlarge[h].empty()) {

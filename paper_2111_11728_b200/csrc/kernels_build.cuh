@@ -83,20 +83,29 @@ __device__ __forceinline__ void pivot_sqrt(double* akk, int* status, int code) {
   *akk = sqrt(d);
 }
 
+// Column c of a lower-triangular frontal, from its diagonal down: full
+// column-major storage (leading dimension ld), or packed (PK: the columns'
+// lower parts back to back, ld = nf -- half the shared memory, so twice the
+// resident CTAs for the ND small levels).
+template <bool PK>
+__device__ __forceinline__ double* diag_ptr(double* F, int c, int ld) {
+  return PK ? F + ((size_t)c * ld - ((size_t)c * (c - 1)) / 2) : F + (size_t)c * ld + c;
+}
+
+template <bool PK>
 __device__ void eliminate_smem_cols(double* F, int nf, int ne, int ld, int* status, int code) {
   const int tid = threadIdx.x, nt = blockDim.x;
-  if (ne > 0 && tid == 0) pivot_sqrt(F, status, code);
+  if (ne > 0 && tid == 0) pivot_sqrt(diag_ptr<PK>(F, 0, ld), status, code);
   __syncthreads();
   for (int k = 0; k < ne; ++k) {
-    double* ck = F + (size_t)k * ld;
-    const double l = ck[k];
-    for (int i = k + 1 + tid; i < nf; i += nt) ck[i] = ck[i] / l;
+    double* dk = diag_ptr<PK>(F, k, ld);      // dk[i - k] = A[i][k]
+    const double l = dk[0];
+    for (int i = k + 1 + tid; i < nf; i += nt) dk[i - k] = dk[i - k] / l;
     __syncthreads();
     const int m = nf - k - 1;
     const int P = m / 2, npairs = P + (m & 1);
     const int S = npairs > 0 ? max(1, nt / npairs) : 1;
-    const double* cc = ck + k + 1;            // trailing part of the pivot column
-    double* T = F + (size_t)(k + 1) * ld + k + 1;   // trailing block, T[jj*ld + ii]
+    const double* cc = dk + 1;                // trailing part of the pivot column
     // thread 0 owns work item 0, whose first entry is the next pivot
     // A[k+1][k+1]: it takes the square root right after its own updates, so
     // one barrier per pivot is saved
@@ -106,25 +115,26 @@ __device__ void eliminate_smem_cols(double* F, int nf, int ne, int ld, int* stat
       const int L = (len + S - 1) / S;
       const int q0 = s * L, q1 = min(len, q0 + L);
       // entries q < m - p: column p, rows p + q; then column m-1-p, rows
-      // (m-1-p) + (q - (m-p)).  One loop with a pointer switch, so lanes
-      // whose segments straddle the fold do not serialise two loops.
+      // (m-1-p) + (q - (m-p)) (trailing coordinates).  One loop with a pointer
+      // switch, so lanes whose segments straddle the fold do not serialise
+      // two loops.
       const int split = m - p;
       int jj = q0 < split ? p : m - 1 - p;
       int sh = q0 < split ? 0 : split;
       double cj = cc[jj];
-      double* col = T + (size_t)jj * ld + jj - sh;
+      double* col = diag_ptr<PK>(F, k + 1 + jj, ld) - sh;
       const double* ci = cc + jj - sh;
       for (int q = q0; q < q1; ++q) {
         if (q == split) {
           jj = m - 1 - p;
           cj = cc[jj];
-          col = T + (size_t)jj * ld + jj - split;
+          col = diag_ptr<PK>(F, k + 1 + jj, ld) - split;
           ci = cc + jj - split;
         }
         col[q] = fma(-ci[q], cj, col[q]);
       }
     }
-    if (tid == 0 && k + 1 < ne) pivot_sqrt(T, status, code);
+    if (tid == 0 && k + 1 < ne) pivot_sqrt(diag_ptr<PK>(F, k + 1, ld), status, code);
     __syncthreads();
   }
 }
@@ -148,6 +158,7 @@ struct NdArgs {
   int* status;
 };
 
+template <bool PK>
 __device__ __forceinline__ void nd_assemble(const NdArgs& a, const NdDev& nd, int dl, double* F,
                                             int ld) {
   const int tid = threadIdx.x, nt = blockDim.x;
@@ -174,7 +185,7 @@ __device__ __forceinline__ void nd_assemble(const NdArgs& a, const NdDev& nd, in
           const int* em = a.emap + (size_t)(nd.elem_off + e) * 8;
           const int r = idx & 7, c = (idx >> 3) & 7;
           const int pr = em[r], pc = em[c];
-          if (pr >= pc) F[(size_t)pc * ld + pr] += E * c_kunit[c * 8 + r];
+          if (pr >= pc) diag_ptr<PK>(F, pc, ld)[pr - pc] += E * c_kunit[c * 8 + r];
         }
         __syncthreads();
       }
@@ -191,7 +202,7 @@ __device__ __forceinline__ void nd_assemble(const NdArgs& a, const NdDev& nd, in
       for (int idx = tid; idx < 64; idx += nt) {
         const int r = idx & 7, c = idx >> 3;
         const int pr = em[r], pc = em[c];
-        if (pr >= pc) F[(size_t)pc * ld + pr] += E * c_kunit[c * 8 + r];
+        if (pr >= pc) diag_ptr<PK>(F, pc, ld)[pr - pc] += E * c_kunit[c * 8 + r];
       }
       __syncthreads();
     }
@@ -222,7 +233,7 @@ __device__ __forceinline__ void nd_assemble(const NdArgs& a, const NdDev& nd, in
               v[u] = S[(size_t)(ch.ne + j) * ch.nf + ch.ne + i];
               int pr = cm[i], pc = cm[j];
               if (pr < pc) { const int t = pr; pr = pc; pc = t; }
-              pos[u] = pc * ld + pr;
+              pos[u] = (int)(diag_ptr<PK>(F, pc, ld) - F) + pr - pc;
             }
           }
         }
@@ -237,28 +248,32 @@ __device__ __forceinline__ void nd_assemble(const NdArgs& a, const NdDev& nd, in
   }
 }
 
-// small tree nodes: assemble + eliminate in shared memory, one CTA per (node, design)
+// small tree nodes: assemble + eliminate in shared memory (packed lower
+// triangle, nf (nf + 1) / 2 doubles), one CTA per (node, design)
 __global__ void __launch_bounds__(kThreads) k_nd_small(NdArgs a) {
   extern __shared__ double F[];
   const int t = a.level_nodes[blockIdx.x];
   const int dl = blockIdx.y;
   const NdDev nd = a.nodes[t];
   const int nf = nd.nf;
-  for (int i = threadIdx.x; i < nf * nf; i += blockDim.x) F[i] = 0.0;
+  for (int i = threadIdx.x; i < nf * (nf + 1) / 2; i += blockDim.x) F[i] = 0.0;
   __syncthreads();
-  nd_assemble(a, nd, dl, F, nf);
-  eliminate_smem_cols(F, nf, nd.ne, nf, a.status, kNotSPD);
+  nd_assemble<true>(a, nd, dl, F, nf);
+  eliminate_smem_cols<true>(F, nf, nd.ne, nf, a.status, kNotSPD);
   // the parent (nd_assemble) and k_nd_extract_root read only the lower
   // triangle of the trailing (perimeter) block: write just that
   double* out = a.ws + a.hbase[nd.height] + (long long)dl * a.hstride[nd.height] + nd.off;
-  {
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-    for (int j = nd.ne + warp; j < nf; j += nw)
-      for (int i = j + lane; i < nf; i += 32) out[(size_t)j * nf + i] = F[(size_t)j * nf + i];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int j = nd.ne + warp; j < nf; j += nw) {
+    const double* cj = diag_ptr<true>(F, j, nf);
+    for (int i = j + lane; i < nf; i += 32) out[(size_t)j * nf + i] = cj[i - j];
   }
-  if (a.factors) {
+  if (a.factors) {   // first ne columns, full height (zeros above the diagonal)
     double* fo = a.factors + (size_t)(a.d0 + dl) * a.fstride + nd.foff;
-    for (int i = threadIdx.x; i < nf * nd.ne; i += blockDim.x) fo[i] = F[i];
+    for (int j = warp; j < nd.ne; j += nw) {
+      const double* cj = diag_ptr<true>(F, j, nf);
+      for (int i = lane; i < nf; i += 32) fo[(size_t)j * nf + i] = i >= j ? cj[i - j] : 0.0;
+    }
   }
 }
 
@@ -271,7 +286,7 @@ __global__ void __launch_bounds__(kThreads) k_nd_assemble(NdArgs a) {
   double* F = a.ws + a.hbase[nd.height] + (long long)dl * a.hstride[nd.height] + nd.off;
   for (long long i = threadIdx.x; i < (long long)nf * nf; i += blockDim.x) F[i] = 0.0;
   __syncthreads();
-  nd_assemble(a, nd, dl, F, nf);
+  nd_assemble<false>(a, nd, dl, F, nf);
 }
 
 __global__ void k_nd_copy_factors(NdArgs a) {
@@ -568,7 +583,7 @@ __global__ void __launch_bounds__(kThreads) k_front_elim_small(const FrontDesc* 
     F[idx] = A[(size_t)j * f.ld + i];
   }
   __syncthreads();
-  eliminate_smem_cols(F, nf, f.ne, nf, status, f.code);
+  eliminate_smem_cols<false>(F, nf, f.ne, nf, status, f.code);
   for (int idx = threadIdx.x; idx < nf * nf; idx += blockDim.x) {
     const int j = idx / nf, i = idx - j * nf;
     A[(size_t)j * f.ld + i] = F[idx];
