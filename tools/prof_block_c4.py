@@ -11,6 +11,7 @@ from paper_2111_11728_b200 import engine, problems as pb  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--k", type=int, default=2048)
 ap.add_argument("--reps", type=int, default=3)
+ap.add_argument("--hash", action="store_true", help="also print sha1 of Q (bit-identity probe)")
 args = ap.parse_args()
 g = engine.FetiSystem(pb.config4())
 L, m, k = engine.lib(), g.m, args.k
@@ -23,3 +24,9 @@ ms = (C.c_double * 1)()
 engine.check(L.fetigpu_time_apply_block(g.h, Wp, Qp, k, 1, ms))
 engine.check(L.fetigpu_time_apply_block(g.h, Wp, Qp, k, args.reps, ms))
 print(f"k {k}: {ms[0]:.2f} ms per block apply")
+if args.hash:
+    import hashlib
+    import numpy as np
+    q = np.empty(m * k)
+    engine.check(L.fetigpu_memcpy(g.h, q.ctypes.data_as(C.c_void_p), dQ, C.c_size_t(8 * m * k), 2))
+    print("Q sha1", hashlib.sha1(q.tobytes()).hexdigest()[:16])
