@@ -352,9 +352,10 @@ __global__ void __launch_bounds__(256) k_block_dp_t(const OpSub* __restrict__ su
   const bool vec = (ldw & 1) == 0 && col + 1 < k;
   double a0[8] = {}, a1[8] = {};
   if (col < k) {
-    for (int j = grp; j < ns; j += 4) {
+    auto loadw = [&](int j, double& w0, double& w1) {
       const int r = rs[j];
-      double w0 = 0.0, w1 = 0.0;
+      w0 = 0.0;
+      w1 = 0.0;
       if (r >= 0) {
         const double* wr = W + (size_t)r * ldw + col;
         if (vec) {
@@ -366,6 +367,8 @@ __global__ void __launch_bounds__(256) k_block_dp_t(const OpSub* __restrict__ su
           w1 = col + 1 < k ? wr[1] : 0.0;
         }
       }
+    };
+    auto accum = [&](int j, double w0, double w1) {
       const double x0 = cs[j] * w0, x1 = cs[j] * w1;
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
@@ -373,6 +376,21 @@ __global__ void __launch_bounds__(256) k_block_dp_t(const OpSub* __restrict__ su
         a0[c] = fma(av, x0, a0[c]);
         a1[c] = fma(av, x1, a1[c]);
       }
+    };
+    // four W rows in flight per thread, accumulated in row order (the
+    // single-row loop's order: bit-identical; it waited on every load)
+    int j = grp;
+    for (; j + 12 < ns; j += 16) {
+      double w[4][2];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) loadw(j + 4 * u, w[u][0], w[u][1]);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) accum(j + 4 * u, w[u][0], w[u][1]);
+    }
+    for (; j < ns; j += 4) {
+      double w0, w1;
+      loadw(j, w0, w1);
+      accum(j, w0, w1);
     }
   }
   __syncthreads();  // A no longer needed: its space holds the group partials
