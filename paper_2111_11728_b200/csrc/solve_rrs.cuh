@@ -154,6 +154,20 @@ __global__ void k_perm_scatter(const double* __restrict__ y, const int* __restri
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < rank; c += gridDim.x * blockDim.x) yh[perm[c]] = y[c];
 }
 
+// the nine per-phase timing events of an RRS solve
+struct PhaseEvents {
+  cudaEvent_t ev[9] = {};
+  PhaseEvents() {
+    for (auto& e : ev) CK(cudaEventCreate(&e));
+  }
+  ~PhaseEvents() {
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+  }
+  PhaseEvents(const PhaseEvents&) = delete;
+  PhaseEvents& operator=(const PhaseEvents&) = delete;
+};
+
 // Launch the cluster pivoted Cholesky with the smallest cluster whose
 // distributed shared memory holds the n x n Gram matrix; false if none fits
 // (n > kPivcholClusterMaxN or the cluster cannot be scheduled).
@@ -346,8 +360,8 @@ int Ctx::solve_rrs(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_tra
   push(eps0, Ns);
   project_rm(W.p, Ns);  // line 3
   const double target = o.rel ? o.tol * eps0 : o.tol;
-  cudaEvent_t pev[9];
-  for (auto& e : pev) CK(cudaEventCreate(&e));
+  PhaseEvents pe;   // destroyed on every exit path (errors throw out of the loop)
+  cudaEvent_t* pev = pe.ev;
   double phase[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   auto mark = [&](int i) { CK(cudaEventRecord(pev[i], st)); };
   const char* tenv = getenv("FETIGPU_TRACE");  // per-iteration RRS line on stderr
@@ -455,7 +469,6 @@ int Ctx::solve_rrs(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_tra
       phase[q] += t;
     }
   }
-  for (auto& e : pev) cudaEventDestroy(e);
   if (tr)
     for (int q = 0; q < 8; ++q) tr->phase_ms[q] = phase[q];
   CK(cudaEventRecord(ev1, st));
@@ -624,8 +637,8 @@ int Ctx::solve_rrs_implicit(const fetigpu_solve_opts& o, double* lambda_host, fe
   };
   push(eps0, Ns);
   const double target = o.rel ? o.tol * eps0 : o.tol;
-  cudaEvent_t pev[9];
-  for (auto& e : pev) CK(cudaEventCreate(&e));
+  PhaseEvents pe;   // destroyed on every exit path (errors throw out of the loop)
+  cudaEvent_t* pev = pe.ev;
   double phase[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   auto mark = [&](int i) { CK(cudaEventRecord(pev[i], st)); };
   const char* tenv = getenv("FETIGPU_TRACE");
@@ -760,7 +773,6 @@ int Ctx::solve_rrs_implicit(const fetigpu_solve_opts& o, double* lambda_host, fe
       phase[qi] += t;
     }
   }
-  for (auto& e : pev) cudaEventDestroy(e);
   if (tr)
     for (int qi = 0; qi < 8; ++qi) tr->phase_ms[qi] = phase[qi];
   CK(cudaEventRecord(ev1, st));
