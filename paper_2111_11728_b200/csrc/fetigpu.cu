@@ -328,11 +328,13 @@ int fetigpu_pivoted_cholesky(const double* a, int n, double tol, int* perm, doub
     DBuf<int> p, r, status, ctl;
     DBuf<double> gx;
     A.alloc((size_t)n * n);
-    p.alloc(n); r.alloc(1); status.alloc(1); ctl.alloc(4); gx.alloc((size_t)n + 64);
+    p.alloc(n); r.alloc(1); status.alloc(1); ctl.alloc(4); gx.alloc(2 * (size_t)n + 64);
     status.zero(st);
     CK(cudaMemcpyAsync(A.p, a, (size_t)n * n * 8, cudaMemcpyHostToDevice, st));
     k_mirror_lower<<<grid_for((long long)n * n), kThreads, 0, st>>>(A.p, n);
-    launch_pivchol(A.p, n, tol, p.p, r.p, status.p, ctl.p, gx.p, st);
+    DBuf<double> lc;
+    lc.alloc((size_t)n * n);
+    launch_pivchol(A.p, n, tol, p.p, r.p, status.p, ctl.p, gx.p, st, lc.p);
     LAUNCH_CHECK();
     int hstat = 0;
     std::vector<double> full((size_t)n * n);

@@ -1188,6 +1188,115 @@ __global__ void __launch_bounds__(512) k_pivchol_cl(double* Ag, int n, double to
 // Same algorithm and per-element arithmetic as k_pivchol, spread over a
 // cooperative grid: block 0 selects the pivot, swaps and scales column k; all
 // blocks share the rank-1 trailing update; two grid syncs per pivot.
+// Cooperative-grid pivoted Cholesky with ONE grid barrier per pivot (k > 640).
+// Rows and columns are never swapped: A stays in original index order and
+// every CTA keeps the position -> index map in shared memory, choosing the
+// next pivot itself (same scan and reduction tree in every CTA, so all agree)
+// and forming the scaled pivot column in shared memory before its share of
+// the trailing update.  The pivot scan of step k may overlap faster CTAs'
+// updates of step k, so it reads the diagonal from a ping-pong copy dd[k & 1]
+// that step k writes only into dd[(k + 1) & 1]; the pivot column itself is
+// never touched by its own step's update.  Per pivot the values are those of
+// k_pivchol_coop (the same division for L, the same fma(-L_i, L_j, A_ij) per
+// entry, ties to the lowest position), so rank, permutation and L are
+// bit-identical; the serial block-0 phase and one grid barrier are gone.  L is
+// collected by original row in `lc` (n x n) and written to A in pivot order
+// at the end.  Dynamic shared memory: n doubles + n ints.  dd: 2n doubles.
+__global__ void __launch_bounds__(512) k_pivchol_coop1(double* A, int n, double tol, int* perm,
+                                                       int* rank_out, int* status, double* lc, double* dd) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ double psm[];
+  double* Ls = psm;                                   // scaled pivot column, by position
+  int* at = reinterpret_cast<int*>(Ls + n);           // original index at position
+  __shared__ double sv[16];
+  __shared__ int si[16];
+  __shared__ double s_scale;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int lane = tid & 31, warp = tid >> 5, nwarp = nt >> 5;
+  for (int i = tid; i < n; i += nt) at[i] = i;
+  for (long long i = blockIdx.x * (long long)nt + tid; i < n; i += (long long)gridDim.x * nt)
+    dd[i] = A[(size_t)i * n + i];
+  grid.sync();
+  {
+    double mx = -1e300;
+    for (int i = tid; i < n; i += nt) mx = fmax(mx, dd[i]);
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 0) sv[warp] = mx;
+    __syncthreads();
+    if (tid == 0) {
+      double m2 = sv[0];
+      for (int w = 1; w < nwarp; ++w) m2 = fmax(m2, sv[w]);
+      s_scale = m2;
+    }
+    __syncthreads();
+  }
+  const double stop_tol = tol * s_scale;
+  const double neg_tol = -tol * fmax(s_scale, 1e-300);
+  int k = 0;
+  for (; k < n; ++k) {
+    const double* dcur = dd + (size_t)(k & 1) * n;
+    double* dnext = dd + (size_t)((k + 1) & 1) * n;
+    // pivot: largest remaining diagonal, ties -> lowest position
+    double bv = -1e300;
+    int bi = n;
+    for (int j = k + tid; j < n; j += nt) {
+      const double v = dcur[at[j]];
+      if (v > bv || (v == bv && j < bi)) { bv = v; bi = j; }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+    }
+    if (lane == 0) { sv[warp] = bv; si[warp] = bi; }
+    __syncthreads();
+    double v = sv[0];
+    int b = si[0];
+    for (int w = 1; w < nwarp; ++w)
+      if (sv[w] > v || (sv[w] == v && si[w] < b)) { v = sv[w]; b = si[w]; }
+    if (!(v > stop_tol)) {
+      if (blockIdx.x == 0)
+        for (int j = k + tid; j < n; j += nt)
+          if (dcur[at[j]] < neg_tol) atomicExch(status, 2);
+      break;
+    }
+    const int q = at[b], qk = at[k];
+    __syncthreads();   // every thread has read sv/si and at[b], at[k] before the swap
+    if (tid == 0) { at[k] = q; at[b] = qk; }
+    __syncthreads();
+    const double l = sqrt(A[(size_t)q * n + q]);
+    // scaled pivot column by position (the old kernel's ck[i] /= l)
+    for (int p = k + 1 + tid; p < n; p += nt) Ls[p] = A[(size_t)q * n + at[p]] / l;
+    if (blockIdx.x == 0) {
+      for (int p = k + 1 + tid; p < n; p += nt) lc[(size_t)k * n + at[p]] = Ls[p];
+      if (tid == 0) lc[(size_t)k * n + q] = l;
+    }
+    __syncthreads();
+    const int r = n - k - 1;
+    const long long tot = (long long)r * r;
+    for (long long idx = blockIdx.x * (long long)nt + tid; idx < tot; idx += (long long)gridDim.x * nt) {
+      const int pj = k + 1 + (int)(idx / r), pi = k + 1 + (int)(idx % r);
+      double* e = A + (size_t)at[pj] * n + at[pi];
+      const double nv = *e - Ls[pi] * Ls[pj];
+      *e = nv;
+      if (pi == pj) dnext[at[pi]] = nv;
+    }
+    grid.sync();
+  }
+  grid.sync();   // (break path) every CTA is done reading A before it is overwritten
+  // L in pivot order: column c < k holds rows p >= c (the layout of k_pivchol_coop)
+  for (long long idx = blockIdx.x * (long long)nt + tid; idx < (long long)k * n;
+       idx += (long long)gridDim.x * nt) {
+    const int c = (int)(idx / n), p = (int)(idx % n);
+    if (p >= c) A[(size_t)c * n + p] = lc[(size_t)c * n + at[p]];
+  }
+  if (blockIdx.x == 0) {
+    for (int i = tid; i < n; i += nt) perm[i] = at[i];
+    if (tid == 0) *rank_out = k;
+  }
+}
+
 __global__ void __launch_bounds__(512) k_pivchol_coop(double* A, int n, double tol, int* perm,
                                                       int* rank_out, int* status, int* ctl) {
   namespace cg = cooperative_groups;

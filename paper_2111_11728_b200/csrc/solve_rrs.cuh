@@ -233,15 +233,31 @@ static bool launch_pivchol_cluster(double* A, int n, double tol, int* perm, int*
 
 // Alg. 1 line 9 on a symmetric n x n matrix already in device memory (full
 // storage): the cluster kernel when the matrix fits distributed shared memory,
-// else the cooperative-grid kernel.  Scratch: ctl 4 ints, gx n + 64 doubles.
+// else a cooperative-grid kernel -- k_pivchol_coop1 (one grid barrier per
+// pivot) when an n x n scratch `lc` is given, k_pivchol_coop otherwise
+// (FETIGPU_PIVCHOL_COOP0=1 forces it).  Scratch: ctl 4 ints, gx 2n + 64 doubles.
 static void launch_pivchol(double* A, int n, double tol, int* perm, int* rank, int* status, int* ctl, double* gx,
-                           cudaStream_t st) {
+                           cudaStream_t st, double* lc = nullptr) {
   if (launch_pivchol_cluster(A, n, tol, perm, rank, status, gx, st)) return;
+  int dev = 0, sms = 0;
+  CK(cudaGetDevice(&dev));
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const char* e = getenv("FETIGPU_PIVCHOL_COOP0");
+  const size_t smem = (size_t)n * 12;
+  if (lc && !(e && e[0] == '1') && smem <= 200 * 1024) {
+    raise_smem_limit(k_pivchol_coop1, smem);
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pivchol_coop1, 512, smem));
+    if (per_sm > 0) {
+      const int blocks = sms * std::min(per_sm, 2);
+      void* args[] = {&A, &n, &tol, &perm, &rank, &status, &lc, &gx};
+      CK(cudaLaunchCooperativeKernel((void*)k_pivchol_coop1, dim3(blocks), dim3(512), args, smem, st));
+      return;
+    }
+  }
   static std::atomic<int> coop_blocks{0};  // (see pivchol_cluster_try: benign duplicated init)
   if (!coop_blocks.load()) {
-    int dev = 0, sms = 0, per_sm = 0;
-    CK(cudaGetDevice(&dev));
-    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    int per_sm = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pivchol_coop, 512, 0));
     coop_blocks = sms * std::max(1, std::min(per_sm, 2));
   }
@@ -273,7 +289,7 @@ int Ctx::solve_rrs(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_tra
   W.alloc((size_t)m * Ns); Qb.alloc((size_t)m * Ns);
   ctl.alloc(4);
   DBuf<double> pivx;
-  pivx.alloc((size_t)Ns + 64);
+  pivx.alloc(2 * (size_t)Ns + 64);
   Linv.alloc((size_t)Ns * Ns);
   Delta.alloc((size_t)Ns * Ns); gamma.alloc(Ns);
   perm.alloc(Ns); rank_d.alloc(1);
@@ -381,7 +397,7 @@ int Ctx::solve_rrs(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_tra
     k_mirror_lower<<<grid_for((long long)k * k), kThreads, 0, st>>>(Delta.p, k);
     mark(2);
     // line 9
-    launch_pivchol(Delta.p, k, o.pivot_tol, perm.p, rank_d.p, d_status.p, ctl.p, pivx.p, st);
+    launch_pivchol(Delta.p, k, o.pivot_tol, perm.p, rank_d.p, d_status.p, ctl.p, pivx.p, st, Linv.p);
     LAUNCH_CHECK();
     mark(3);
     int rank = 0;
@@ -559,7 +575,7 @@ int Ctx::solve_rrs_implicit(const fetigpu_solve_opts& o, double* lambda_host, fe
   W.alloc((size_t)m * k); Qb.alloc((size_t)m * k); Dd.alloc((size_t)m * k);
   Delta.alloc((size_t)k * k); Linv.alloc((size_t)k * k);
   tvec.alloc(k); tp.alloc(k); gam.alloc(k); yh.alloc(k);
-  perm.alloc(k); rank_d.alloc(1); ctl.alloc(4); pivx.alloc((size_t)k + 64);
+  perm.alloc(k); rank_d.alloc(1); ctl.alloc(4); pivx.alloc(2 * (size_t)k + 64);
   sc.alloc(1);
   sc.zero(st);
   // packed Z blocks (column-major nz x zcap, grown by doubling) and the
@@ -663,7 +679,7 @@ int Ctx::solve_rrs_implicit(const fetigpu_solve_opts& o, double* lambda_host, fe
     CB(cublasDgemm(cb, CUBLAS_OP_N, CUBLAS_OP_N, k, k, kzi, &one, XT.p, k, CW.p, kzi, &zero, Delta.p, k));
     k_mirror_lower<<<grid_for((long long)k * k), kThreads, 0, st>>>(Delta.p, k);
     mark(2);
-    launch_pivchol(Delta.p, k, o.pivot_tol, perm.p, rank_d.p, d_status.p, ctl.p, pivx.p, st);  // line 9
+    launch_pivchol(Delta.p, k, o.pivot_tol, perm.p, rank_d.p, d_status.p, ctl.p, pivx.p, st, Linv.p);  // line 9
     LAUNCH_CHECK();
     mark(3);
     int rank = 0;
