@@ -152,6 +152,12 @@ typedef struct fetigpu_stats {
   double device_bytes;       /* device memory held by the context */
   int host_pipeline;         /* 1: fetigpu_apply_F overlaps the H2D of x with the GEMV */
   int reserved_;
+  /* bytes one F-apply must stream with symmetric operator storage: the
+   * symmetric-packed F_s tiles when the packed kernel runs (else 8 n_s^2),
+   * A_bc read in both phases, the coarse inverse (packed tiles or dense),
+   * lambda read + y written and the gather lists -- the roofline bytes of
+   * the apply actually executed (op_bytes counts full F_s storage). */
+  double stream_bytes;
 } fetigpu_stats;
 
 /* Select the CUDA device used by contexts built afterwards from this host

@@ -53,6 +53,7 @@ struct Ctx {
   // constraint signs are folded into F_s / A_bc (FETI-DP), else d_opcoef
   DBuf<double> d_opcoef_apply;
   bool folded = false;
+  bool blk_aligned = false;  // every slot's F'' / A'' rows admit 16-byte chunks (K5 fast path)
   // symmetric-packed operator tiles for the GEMV (used when rsplit == 1)
   bool use_sym = false;
   DBuf<double> d_symtiles;

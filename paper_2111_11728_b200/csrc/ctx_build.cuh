@@ -601,6 +601,14 @@ void Ctx::build_ops(const SlotOut& so, std::future<HostMaps>& maps) {
       d_opcoef_apply.upload(ones, st);
       CK(cudaStreamSynchronize(st));
       folded = true;
+      // K5's cp.async fast path copies 16-byte chunks of F'' and A'' rows:
+      // every slot needs even n_s (no chunk straddles F'' and its padding),
+      // even n_c and an even A'' offset (16-byte aligned A'' rows).  A
+      // one-direction support at a partition vertex (odd n_c) or on an edge
+      // (odd n_s) takes the general kernel.
+      blk_aligned = true;
+      for (int i = 0; i < nsl; ++i)
+        if ((nsv[i] & 1) || (ncv[i] & 1) || (ao[i] & 1) || (op_moff[i] & 1) || (op_ld[i] & 1)) blk_aligned = false;
     }
   }
   ptimer.mark("coarse problem + folding", st);

@@ -383,7 +383,7 @@ void Ctx::apply_F_block(const double* W, int ldw, double* Q, int ldq, int k) {
     max_ns += 8;
   }
   dim3 grid((k + kBN - 1) / kBN, (max_ns + kBM - 1) / kBM, Ns);
-  const bool fast = folded && (k % 2 == 0) && (ldw % 2 == 0) && (ldq % 2 == 0) &&
+  const bool fast = folded && blk_aligned && (k % 2 == 0) && (ldw % 2 == 0) && (ldq % 2 == 0) &&
                     ((uintptr_t)W % 16 == 0) && ((uintptr_t)Q % 16 == 0);
   if (fast) k_block_apply_dp<<<grid, 256, kAsyncSmem, st>>>(a);
   else if (KR == 1) k_block_apply<1><<<grid, 256, kBlockSmem, st>>>(a);

@@ -103,6 +103,12 @@ int fetigpu_stats_get(const fetigpu_ctx* ctx, fetigpu_stats* s) {
     s->op_bytes = 8 * sn2 + (dp ? 16 * snc + 8.0 * c.su.Nc * c.su.Nc : 0) + 16.0 * c.su.m + 8 * sns;
     s->op_flops_per_col = 2 * sn2 + (dp ? 4 * snc + 2.0 * c.su.Nc * c.su.Nc : 0);
     s->main_kernel_bytes = c.use_sym ? c.sym_bytes : 8 * sn2;
+    double coarse = 0;
+    if (dp) {
+      const double nbc = (c.su.Nc + 31) / 32;
+      coarse = c.use_csym ? nbc * (nbc + 1) / 2 * 1024 * 8 : 8.0 * c.su.Nc * c.su.Nc;
+    }
+    s->stream_bytes = s->main_kernel_bytes + (dp ? 16 * snc : 0) + coarse + 16.0 * c.su.m + 8 * sns;
     s->build_ms = c.build_ms; s->nd_ms = c.nd_ms; s->slot_ms = c.slot_ms; s->coarse_ms = c.coarse_ms;
     s->device_bytes = (double)g_device_bytes;
   });

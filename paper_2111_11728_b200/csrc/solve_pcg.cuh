@@ -42,7 +42,18 @@ int Ctx::solve(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_trace* 
   sc.zero(st);
   cnt.alloc(1);
   cnt.zero(st);
-  const int cap = std::max(1, o.max_it);
+  // FO keeps two m-vectors per iteration.  The store is sized for max_it
+  // iterations but clamped to the free device memory (a generous max_it must
+  // not fail a solve that converges early); a solve that fills a clamped
+  // store without converging fails with FETIGPU_E_OUT_OF_MEMORY.
+  int cap = std::max(1, o.max_it);
+  if (fo) {
+    const size_t freeb = dev_free_bytes(), margin = size_t(1) << 30;
+    const long long fit = freeb > margin ? (long long)((freeb - margin) / (16.0 * m + 8)) : 0;
+    if (fit < 1) fail(FETIGPU_E_OUT_OF_MEMORY, "FO: no device memory for the direction store");
+    cap = (int)std::min<long long>(cap, fit);
+  }
+  const int max_it = fo ? cap : o.max_it;
   DBuf<double> psi_part;
   if (fo) {
     Wst.alloc((size_t)m * cap);
@@ -137,14 +148,14 @@ int Ctx::solve(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_trace* 
   // solve, no host round trip per iteration.  Fallback (no conditional nodes,
   // or FETIGPU_HOST_LOOP=1): one graph launch + a 64-byte readback per iteration.
   const char* hl = getenv("FETIGPU_HOST_LOOP");
-  bool device_loop = !(hl && hl[0] == '1') && eps > target && o.max_it > 0;
+  bool device_loop = !(hl && hl[0] == '1') && eps > target && max_it > 0;
   if (device_loop) {
     DBuf<IterCtl> dctl;
     DBuf<double> dtrace;
-    const int tcap = tr && tr->eps ? std::min(tr->cap, o.max_it + 1) : 1;
+    const int tcap = tr && tr->eps ? std::min(tr->cap, max_it + 1) : 1;
     dctl.alloc(1);
     dtrace.alloc(std::max(1, tcap));
-    IterCtl h0{0, FETIGPU_MAX_ITER, 0, tcap, o.max_it, 0, eps0, target};
+    IterCtl h0{0, FETIGPU_MAX_ITER, 0, tcap, max_it, 0, eps0, target};
     CK(cudaMemcpyAsync(dctl.p, &h0, sizeof(IterCtl), cudaMemcpyHostToDevice, st));
     CK(cudaStreamSynchronize(st));
     bool built_ok = false;
@@ -202,7 +213,7 @@ int Ctx::solve(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_trace* 
     CK(cudaGraphInstantiate(&exec, graph, 0));
     while (true) {
       if (eps <= target) { status = FETIGPU_CONVERGED; break; }
-      if (it >= o.max_it) { status = FETIGPU_MAX_ITER; break; }
+      if (it >= max_it) { status = FETIGPU_MAX_ITER; break; }
       CK(cudaGraphLaunch(exec, st));
       CK(cudaStreamSynchronize(st));
       if (hs->breakdown != 0.0) { status = FETIGPU_BREAKDOWN; break; }
@@ -212,6 +223,9 @@ int Ctx::solve(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_trace* 
       push(eps, 1);
     }
   }
+  if (status == FETIGPU_MAX_ITER && max_it < o.max_it)
+    fail(FETIGPU_E_OUT_OF_MEMORY, "FO: direction store full after " + std::to_string(max_it) +
+                                      " iterations (device memory), max_it = " + std::to_string(o.max_it));
   CK(cudaEventRecord(ev1, st));
   const double ms = elapsed(ev0, ev1);
   CK(cudaMemcpyAsync(lambda_host, lam.p, m * 8, cudaMemcpyDeviceToHost, st));

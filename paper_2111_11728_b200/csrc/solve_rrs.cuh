@@ -400,13 +400,13 @@ int Ctx::solve_rrs(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_tra
     launch_pivchol(Delta.p, k, o.pivot_tol, perm.p, rank_d.p, d_status.p, ctl.p, pivx.p, st, Linv.p);
     LAUNCH_CHECK();
     mark(3);
-    int rank = 0;
+    int rank = 0, hstat = 0;
     CK(cudaMemcpyAsync(&rank, rank_d.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&hstat, d_status.p, sizeof(int), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    int hstat = 0;
-    CK(cudaMemcpy(&hstat, d_status.p, sizeof(int), cudaMemcpyDeviceToHost));
     if (hstat) {
-      CK(cudaMemset(d_status.p, 0, sizeof(int)));
+      CK(cudaMemsetAsync(d_status.p, 0, sizeof(int), st));
+      CK(cudaStreamSynchronize(st));
       fail(FETIGPU_E_INDEFINITE_INPUT, "pivoted Cholesky: negative pivot");
     }
     if (rank == 0) { status = FETIGPU_BREAKDOWN; break; }
@@ -682,13 +682,13 @@ int Ctx::solve_rrs_implicit(const fetigpu_solve_opts& o, double* lambda_host, fe
     launch_pivchol(Delta.p, k, o.pivot_tol, perm.p, rank_d.p, d_status.p, ctl.p, pivx.p, st, Linv.p);  // line 9
     LAUNCH_CHECK();
     mark(3);
-    int rank = 0;
+    int rank = 0, hstat = 0;
     CK(cudaMemcpyAsync(&rank, rank_d.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&hstat, d_status.p, sizeof(int), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    int hstat = 0;
-    CK(cudaMemcpy(&hstat, d_status.p, sizeof(int), cudaMemcpyDeviceToHost));
     if (hstat) {
-      CK(cudaMemset(d_status.p, 0, sizeof(int)));
+      CK(cudaMemsetAsync(d_status.p, 0, sizeof(int), st));
+      CK(cudaStreamSynchronize(st));
       fail(FETIGPU_E_INDEFINITE_INPUT, "pivoted Cholesky: negative pivot");
     }
     if (rank == 0) { status = FETIGPU_BREAKDOWN; break; }
