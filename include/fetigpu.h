@@ -208,6 +208,11 @@ int fetigpu_local_operator(fetigpu_ctx* ctx, int s, int* ns, int* dofs, double* 
 /* Block F-apply (K5, FP64 tensor cores): Q = F W for k columns stored
  * row-major (W(i,c) = W[i*ldw + c]), device pointers, ctx stream. */
 int fetigpu_apply_F_block_device(fetigpu_ctx* ctx, const double* W, int ldw, double* Q, int ldq, int k);
+/* Test hook: Q = F Z for a fresh per-subdomain preconditioner block Z
+ * (row-major m x N_s, column s supported on subdomain s's dual rows) through
+ * the sparse-aware K5z path the RRS solver uses on Alg. 1 lines 2/16 blocks;
+ * host buffers.  FETIGPU_E_CONFIG when the problem lacks that structure. */
+int fetigpu_apply_F_zblock(fetigpu_ctx* ctx, const double* Z, double* Q);
 int fetigpu_time_apply_block(fetigpu_ctx* ctx, const double* W, double* Q, int k, int reps, double* ms);
 /* Rank-revealing pivoted Cholesky, Alg. 1 line 9 -- replaces
  * feti::pivoted_cholesky (proj/include/feti/linalg.hpp:80, linalg.cpp:83-138)
@@ -227,6 +232,18 @@ int fetigpu_pivoted_cholesky(const double* a, int n, double tol, int* perm, doub
  * on the identity, column gather, triangular multiply). */
 int fetigpu_pivoted_compress(const int* perm, const double* lower, int n, int rank, const double* w, int rows,
                              double* out);
+/* Dense FP64 algebra of the engine (hand-written DMMA kernels, no cuBLAS):
+ * C = alpha op(A) op(B) + beta C, column-major BLAS dgemm semantics on host
+ * buffers (test hook).  flags: 1 lower-triangle tiles only (i >= j stored),
+ * 2 / 4 / 8 triangular-operand K ranges (see csrc/dla.cuh GemmFlags), 256
+ * deterministic split-K path. */
+int fetigpu_dla_gemm(int ta, int tb, int M, int N, int K, double alpha, const double* A, long long lda,
+                     const double* B, long long ldb, double beta, double* C, long long ldc, int flags);
+/* X = L^{-1} (n x n, column-major, lower triangle of L read; X lower with
+ * zeros above the diagonal): the L~^{-1} of Alg. 1 lines 10-11. */
+int fetigpu_dla_tri_inv(const double* L, int n, long long ldl, double* X);
+/* mean device time (ms) of `reps` M x N x K GEMMs on device-resident random operands */
+int fetigpu_dla_time_gemm(int ta, int tb, int M, int N, int K, int reps, double* ms);
 /* Measured FP64 issue peaks of this device (DMMA m8n8k4 and DFMA), TFLOP/s. */
 int fetigpu_fp64_peak(double* tflops_dmma, double* tflops_dfma);
 /* DMMA fragment-layout self test: C (8x8 row-major) = A (8x4) B (4x8). */

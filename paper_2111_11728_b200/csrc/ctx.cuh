@@ -8,6 +8,7 @@
 #include "kernels_apply.cuh"
 #include "kernels_build.cuh"
 #include "kernels_dmma.cuh"
+#include "dla.cuh"
 
 namespace fg {
 
@@ -34,7 +35,6 @@ struct Ctx {
   Setup su;
   Scratch scratch;
   cudaStream_t st = nullptr;
-  cublasHandle_t cb = nullptr;
   bool built = false;
   DBuf<int> d_status;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr;
@@ -133,7 +133,6 @@ struct Ctx {
     if (pipe_start) cudaEventDestroy(pipe_start);
     for (auto& q : pipe_st) if (q) cudaStreamDestroy(q);
     if (pipe_cp) cudaStreamDestroy(pipe_cp);
-    if (cb) cublasDestroy(cb);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
     if (ev2) cudaEventDestroy(ev2);
@@ -224,6 +223,25 @@ struct Ctx {
   // ---- K5: Q = F W for k columns, row-major blocks (W(i,c) = W[i*ldw + c])
   DBuf<double> blk_t, blk_T, blk_U;
   void apply_F_block(const double* W, int ldw, double* Q, int ldq, int k);
+  // ---- K5z: Q = F Z for a fresh per-subdomain preconditioner block Z
+  // (row-major m x N_s, column s supported on subdomain s's dual rows):
+  // 5 local columns per subdomain instead of N_s (kernels_dmma.cuh).  false
+  // when the problem does not have that structure (then use apply_F_block).
+  int bz_state = 0;   // 0 unknown, 1 ready, -1 not applicable
+  DBuf<int> bz_other, bz_j, bz_nbr, bz_erow, bz_eb1, bz_eb2, bz_ez1, bz_ez2;
+  DBuf<BzEdge> bz_edges;
+  DBuf<double> bz_Y;
+  int bz_nedges = 0, bz_maxns = 0;
+  bool bz_prepare();
+  // coarse scratch of the block applies (K5 / K5z) for k columns
+  void ensure_block_buffers(int k) {
+    if (su.method != FETIGPU_FETIDP) return;
+    int tot_c = 0;
+    for (auto& S : su.subs) tot_c += (int)S.c.size();
+    if (blk_t.n < (size_t)tot_c * k) blk_t.alloc((size_t)tot_c * k);
+    if (blk_T.n < (size_t)su.Nc * k) { blk_T.alloc((size_t)su.Nc * k); blk_U.alloc((size_t)su.Nc * k); }
+  }
+  bool apply_F_block_z(const double* Z, double* Q, int k);
 
   // single-vector projector finish: per dual row its <= 2 (s, RT offset) / signs
   DBuf<int2> d_pjrow_sr;
@@ -231,11 +249,14 @@ struct Ctx {
 
   // grow-only scratch for the multi-column projector paths: no cudaMalloc /
   // cudaFree (both device-synchronising) inside solver iterations once warm
-  DBuf<double> ws_g, ws_h, ws_corr;
+  DBuf<double> ws_g, ws_h, ws_corr, ws_dla;
   static double* grow(DBuf<double>& b, size_t n) {
     if (b.n < n) b.alloc(n);
     return b.p;
   }
+  // grow-only workspace of the dense algebra (split-K partials, triangular
+  // inverse, GEMV segment partials)
+  double* dla_ws(size_t n) { return grow(ws_dla, std::max<size_t>(n, 1)); }
 
   // v <- P v for a row-major block (m x ncols, ld = ncols), T-FETI only
   void project_rm(double* v, int ncols);
@@ -246,8 +267,7 @@ struct Ctx {
     if (ncols == 1) {
       k_dense_gemv<<<grid_for((long long)nc * 32), kThreads, 0, st>>>(d_H.p, nc, g, h);
     } else {
-      const double one = 1.0, zero = 0.0;
-      CB(cublasDgemm(cb, CUBLAS_OP_N, CUBLAS_OP_N, nc, ncols, nc, &one, d_H.p, nc, g, nc, &zero, h, nc));
+      gemm(st, false, false, nc, ncols, nc, 1.0, d_H.p, nc, g, nc, 0.0, h, nc);
     }
     LAUNCH_CHECK();
   }

@@ -727,9 +727,14 @@ void Ctx::build_coarse(const SlotOut& so, const std::vector<int>& osub, const st
   DBuf<double> K;
   K.alloc((size_t)Nc * Nc);
   launch_kcc_assemble(d_optr.p, dos.p, dol.p, dkco.p, dncs.p, d_kccs.p, Nc, K.p);
-  // blocked Cholesky: diagonal blocks by k_front_elim_large, panels by cuBLAS
+  // blocked right-looking Cholesky: diagonal blocks by k_front_elim_large,
+  // panel L21 = A21 L11^{-T} through the inverted diagonal block, trailing
+  // update A22 -= L21 L21^T on the lower tiles (DMMA GEMMs, dla.cuh)
   const int NBc = 256;
-  const double one = 1.0, mone = -1.0, zero = 0.0;
+  DBuf<double> Xd, Pt, Tw;
+  Xd.alloc((size_t)NBc * NBc);
+  Pt.alloc((size_t)std::max(1, Nc - std::min(NBc, Nc)) * NBc);
+  Tw.alloc(tri_inv_workspace(std::max(Nc, NBc)));
   for (int k0 = 0; k0 < Nc; k0 += NBc) {
     const int kb = std::min(NBc, Nc - k0);
     std::vector<FrontDesc> f{{(long long)k0 * Nc + k0, kb, kb, Nc, FETIGPU_E_SINGULAR_COARSE}};
@@ -740,21 +745,24 @@ void Ctx::build_coarse(const SlotOut& so, const std::vector<int>& osub, const st
     CK(cudaStreamSynchronize(st));
     const int rest = Nc - k0 - kb;
     if (rest > 0) {
-      CB(cublasDtrsm(cb, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT,
-                     rest, kb, &one, K.p + (size_t)k0 * Nc + k0, Nc, K.p + (size_t)k0 * Nc + k0 + kb, Nc));
-      CB(cublasDsyrk(cb, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, rest, kb, &mone,
-                     K.p + (size_t)k0 * Nc + k0 + kb, Nc, &one, K.p + (size_t)(k0 + kb) * Nc + k0 + kb, Nc));
+      double* L11 = K.p + (size_t)k0 * Nc + k0;
+      double* A21 = L11 + kb;
+      tri_inv_lower(st, L11, Nc, kb, Xd.p, kb, Tw.p);
+      CK(cudaMemcpy2DAsync(Pt.p, (size_t)rest * 8, A21, (size_t)Nc * 8, (size_t)rest * 8, kb,
+                           cudaMemcpyDeviceToDevice, st));
+      // L21 = A21 X11^T (X11 lower: column c of X11^T ends at row c)
+      gemm(st, false, true, rest, kb, kb, 1.0, Pt.p, rest, Xd.p, kb, 0.0, A21, Nc, kGemmKEndByCol);
+      gemm(st, false, true, rest, rest, kb, -1.0, A21, Nc, A21, Nc, 1.0, A21 + (size_t)kb * Nc, Nc,
+           kGemmLowerTiles);
     }
   }
   check_status();
-  // inverse: X = L^{-1}, Kinv = X^T X
+  // inverse: X = L^{-1}, Kinv = X^T X (lower tiles, then mirrored)
   DBuf<double> X;
   X.alloc((size_t)Nc * Nc);
-  launch_identity(X.p, Nc);
-  CB(cublasDtrsm(cb, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, Nc, Nc,
-                 &one, K.p, Nc, X.p, Nc));
+  tri_inv_lower(st, K.p, Nc, Nc, X.p, Nc, Tw.p);
   d_Kinv.alloc((size_t)Nc * Nc);
-  CB(cublasDsyrk(cb, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, Nc, Nc, &one, X.p, Nc, &zero, d_Kinv.p, Nc));
+  gemm(st, true, false, Nc, Nc, Nc, 1.0, X.p, Nc, X.p, Nc, 0.0, d_Kinv.p, Nc, kGemmLowerTiles | kGemmKStartByCol);
   launch_symmetrize(d_Kinv.p, Nc);
   // fused-gather target + arrival counters (always); symmetric-packed copy
   // of the inverse for the single-vector apply when it is large

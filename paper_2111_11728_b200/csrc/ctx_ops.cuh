@@ -174,8 +174,6 @@ void Ctx::init_device() {
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
     fail(FETIGPU_E_NO_DEVICE, "no CUDA device available");
   CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-  CB(cublasCreate(&cb));
-  CB(cublasSetStream(cb, st));
   CK(cudaEventCreate(&ev0));
   CK(cudaEventCreate(&ev1));
   CK(cudaEventCreate(&ev2));
@@ -364,10 +362,7 @@ void Ctx::apply_F_block(const double* W, int ldw, double* Q, int ldq, int k) {
   for (int n : op_ns) max_ns = std::max(max_ns, n);
   if (su.method == FETIGPU_FETIDP) {
     const int Nc = su.Nc;
-    int tot_c = 0;
-    for (auto& S : su.subs) tot_c += (int)S.c.size();
-    if (blk_t.n < (size_t)tot_c * k) blk_t.alloc((size_t)tot_c * k);
-    if (blk_T.n < (size_t)Nc * k) { blk_T.alloc((size_t)Nc * k); blk_U.alloc((size_t)Nc * k); }
+    ensure_block_buffers(k);
     {
       const size_t smem = ((size_t)std::max(max_ns * 8, 4 * 8 * kDpTCols) + max_ns) * 8 + (size_t)max_ns * 4;
       raise_smem_limit(k_block_dp_t, smem);
@@ -376,9 +371,8 @@ void Ctx::apply_F_block(const double* W, int ldw, double* Q, int ldq, int k) {
     }
     k_coarse_gather_block<<<dim3((k + 255) / 256, Nc), 256, 0, st>>>(d_optr.p, d_oidx.p, blk_t.p, k, Nc, k,
                                                                      blk_T.p, k);
-    const double one = 1.0, zero = 0.0;
     // U = Kbar^{-1} T  (row-major N_c x k == column-major k x N_c: U^T = T^T Kinv)
-    CB(cublasDgemm(cb, CUBLAS_OP_N, CUBLAS_OP_N, k, Nc, Nc, &one, blk_T.p, k, d_Kinv.p, Nc, &zero, blk_U.p, k));
+    gemm(st, false, false, k, Nc, Nc, 1.0, blk_T.p, k, d_Kinv.p, Nc, 0.0, blk_U.p, k);
     a.dps = d_dp.p; a.abc = d_abc.p; a.cmap = d_cmap.p; a.U = blk_U.p; a.ldu = k;
     max_ns += 8;
   }
@@ -389,6 +383,133 @@ void Ctx::apply_F_block(const double* W, int ldw, double* Q, int ldq, int k) {
   else if (KR == 1) k_block_apply<1><<<grid, 256, kBlockSmem, st>>>(a);
   else k_block_apply<3><<<grid, 256, kBlockSmem, st>>>(a);
   LAUNCH_CHECK();
+}
+
+bool Ctx::bz_prepare() {
+  if (bz_state) return bz_state > 0;
+  bz_state = -1;
+  if (su.method != FETIGPU_FETIDP || !folded || KR != 1 || su.m == 0 || su.Nc == 0) return false;
+  const int Ns = su.Ns, m = su.m;
+  std::vector<OpSub> ops(Ns);
+  CK(cudaMemcpyAsync(ops.data(), d_op.p, Ns * sizeof(OpSub), cudaMemcpyDeviceToHost, st));
+  long long nmap = 0;
+  for (auto& d : ops) nmap = std::max<long long>(nmap, (long long)d.map_off + d.ns);
+  std::vector<int> rows(nmap);
+  CK(cudaMemcpyAsync(rows.data(), d_oprows.p, nmap * sizeof(int), cudaMemcpyDeviceToHost, st));
+  std::vector<DpSub> dps(Ns);
+  CK(cudaMemcpyAsync(dps.data(), d_dp.p, Ns * sizeof(DpSub), cudaMemcpyDeviceToHost, st));
+  // Z column s lives on the preconditioner map rows of s: they must be the
+  // operator map rows of s (as sets) for X_t to have the 2-column structure
+  std::vector<OpSub> pcs(Ns);
+  CK(cudaMemcpyAsync(pcs.data(), d_pc.p, Ns * sizeof(OpSub), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (KRp != 1) return false;
+  long long npc = 0;
+  for (auto& d : pcs) npc = std::max<long long>(npc, (long long)d.map_off + d.ns);
+  std::vector<int> prow(npc);
+  CK(cudaMemcpyAsync(prow.data(), d_pcrows.p, npc * sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  for (int t = 0; t < Ns; ++t) {
+    if (dps[t].nc > 8) return false;
+    std::vector<int> a(rows.begin() + ops[t].map_off, rows.begin() + ops[t].map_off + ops[t].ns);
+    std::vector<int> b(prow.begin() + pcs[t].map_off, prow.begin() + pcs[t].map_off + pcs[t].ns);
+    a.erase(std::remove(a.begin(), a.end(), -1), a.end());
+    b.erase(std::remove(b.begin(), b.end(), -1), b.end());
+    std::sort(a.begin(), a.end());
+    std::sort(b.begin(), b.end());
+    if (a != b) return false;
+  }
+  // owners of each dual row (ascending subdomain order) and their local positions
+  std::vector<int> t1(m, -1), t2(m, -1), b1(m, -1), b2(m, -1);
+  for (int t = 0; t < Ns; ++t)
+    for (int a = 0; a < ops[t].ns; ++a) {
+      const int r = rows[ops[t].map_off + a];
+      if (r < 0) continue;
+      if (t1[r] < 0) { t1[r] = t; b1[r] = a; }
+      else if (t2[r] < 0) { t2[r] = t; b2[r] = a; }
+      else return false;   // more than two owners
+    }
+  // neighbour slots: 0 = itself, then the other owners in first-seen order
+  std::vector<int> nbr((size_t)Ns * kZNb, -1), other(nmap, -1), jslot(nmap, 0);
+  for (int t = 0; t < Ns; ++t) {
+    nbr[(size_t)t * kZNb] = t;
+    int cnt = 1;
+    for (int a = 0; a < ops[t].ns; ++a) {
+      const int r = rows[ops[t].map_off + a];
+      if (r < 0) continue;
+      const int o = t1[r] == t ? t2[r] : t1[r];
+      if (o < 0) continue;
+      int j = 1;
+      while (j < cnt && nbr[(size_t)t * kZNb + j] != o) ++j;
+      if (j == cnt) {
+        if (cnt == kZNb) return false;   // more than 4 neighbours: not this structure
+        nbr[(size_t)t * kZNb + cnt++] = o;
+      }
+      other[ops[t].map_off + a] = o;
+      jslot[ops[t].map_off + a] = j;
+    }
+  }
+  // positions of each row in its owners' preconditioner maps (the packed Z
+  // blocks of the implicit RRS store are laid out on those maps)
+  std::vector<long long> pz1(m, -1), pz2(m, -1);
+  for (int t = 0; t < Ns; ++t)
+    for (int a = 0; a < pcs[t].ns; ++a) {
+      const int r = prow[pcs[t].map_off + a];
+      if (r < 0) continue;
+      if (t == t1[r]) pz1[r] = pcs[t].map_off + a;
+      else if (t == t2[r]) pz2[r] = pcs[t].map_off + a;
+    }
+  // interface edges: rows grouped by their owner pair, chunks of kBzRows
+  std::map<std::pair<int, int>, std::vector<int>> groups;
+  for (int r = 0; r < m; ++r) {
+    if (t1[r] < 0) return false;
+    groups[{t1[r], t2[r]}].push_back(r);
+  }
+  std::vector<BzEdge> edges;
+  std::vector<int> erow, eb1, eb2, ez1, ez2;
+  for (auto& g : groups)
+    for (size_t i0 = 0; i0 < g.second.size(); i0 += kBzRows) {
+      const int cnt = (int)std::min<size_t>(kBzRows, g.second.size() - i0);
+      edges.push_back({g.first.first, g.first.second, (int)erow.size(), cnt});
+      for (int i = 0; i < cnt; ++i) {
+        const int r = g.second[i0 + i];
+        erow.push_back(r);
+        eb1.push_back(b1[r]);
+        eb2.push_back(t2[r] >= 0 ? b2[r] : 0);
+        ez1.push_back((int)pz1[r]);
+        ez2.push_back(t2[r] >= 0 ? (int)pz2[r] : 0);
+      }
+    }
+  for (auto& d : ops) bz_maxns = std::max(bz_maxns, d.ns);
+  bz_other.upload(other, st); bz_j.upload(jslot, st); bz_nbr.upload(nbr, st);
+  bz_erow.upload(erow, st); bz_eb1.upload(eb1, st); bz_eb2.upload(eb2, st);
+  bz_ez1.upload(ez1, st); bz_ez2.upload(ez2, st);
+  bz_edges.upload(edges, st);
+  bz_nedges = (int)edges.size();
+  bz_Y.alloc((size_t)std::max<long long>(1, nmap) * kZNb);
+  CK(cudaStreamSynchronize(st));
+  bz_state = 1;
+  return true;
+}
+
+bool Ctx::apply_F_block_z(const double* Z, double* Q, int k) {
+  if (k != su.Ns || !bz_prepare()) return false;
+  const int Ns = su.Ns, Nc = su.Nc;
+  int tot_c = 0;
+  for (auto& S : su.subs) tot_c += (int)S.c.size();
+  ensure_block_buffers(k);
+  CK(cudaMemsetAsync(blk_t.p, 0, (size_t)tot_c * k * 8, st));
+  const size_t smem = (size_t)bz_maxns * 20;
+  raise_smem_limit(k_bz_local, smem);
+  k_bz_local<<<Ns, 256, smem, st>>>(d_op.p, d_dp.p, d_opmat.p, d_oprows.p, d_abc.p, bz_other.p, bz_j.p, bz_nbr.p, Z,
+                                    k, bz_Y.p, blk_t.p, k);
+  LAUNCH_CHECK();
+  k_coarse_gather_block<<<dim3((k + 255) / 256, Nc), 256, 0, st>>>(d_optr.p, d_oidx.p, blk_t.p, k, Nc, k, blk_T.p, k);
+  gemm(st, false, false, k, Nc, Nc, 1.0, blk_T.p, k, d_Kinv.p, Nc, 0.0, blk_U.p, k);
+  k_bz_edges<<<dim3((k + kBzCols - 1) / kBzCols, bz_nedges), kBzCols, 0, st>>>(
+      bz_edges.p, bz_erow.p, bz_eb1.p, bz_eb2.p, d_op.p, d_dp.p, d_abc.p, d_cmap.p, bz_nbr.p, bz_Y.p, blk_U.p, k, Q);
+  LAUNCH_CHECK();
+  return true;
 }
 
 void Ctx::project_rm(double* v, int ncols) {

@@ -1,0 +1,599 @@
+// dla.cuh -- hand-written FP64 dense linear algebra on the DMMA tensor pipe.
+//
+// Everything the RRS iteration (Alg. 1), the coarse block
+// term of K5 and the FETI-DP coarse factorization need beyond the operator
+// kernels: GEMM in all four transpose combinations (optionally batched,
+// lower-triangle-only, or with a triangular operand whose zero region is
+// skipped), the inverse of a lower-triangular matrix (Alg. 1 lines 10-11,
+// the compression of PivotedCholesky::compress, proj/src/linalg.cpp:131-138),
+// block GEMVs over row-major m x k direction blocks (lines 13-15), AXPY and
+// transpose-scale.  All results are deterministic: every output element is
+// one thread's fixed-order sum (no split-K atomics).
+//
+// GEMM: column-major operands as in BLAS.  A CTA computes a BM x BN tile of
+// C with DMMA m8n8k4 (the only FP64 tensor-core instruction on sm_100a;
+// tcgen05 has no f64 kind).  Operand tiles BM x 16 / 16 x BN are
+// staged by 16-byte cp.async in an ST-stage ring.  Each operand tile is kept
+// in shared memory in the layout its global memory is contiguous in:
+//   "k-rows"  [16][BMN + 8]   (A not transposed, B transposed)
+//   "mn-rows" [BMN][16 + 4]   (A transposed, B not transposed)
+// Both paddings make the 8x4 / 4x8 DMMA fragment loads conflict-free (two
+// shared-memory wavefronts per 256-byte warp load).
+#pragma once
+
+#include "runtime.cuh"
+
+namespace fg {
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// cp.async of `bytes` (0, 8 or 16) bytes into a 16-byte smem slot, zero-filling the rest
+__device__ __forceinline__ void cp_async_n16(void* smem, const void* gmem, int bytes) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(bytes));
+}
+
+enum GemmFlags : int {
+  kGemmLowerTiles = 1,   // C symmetric-result use: skip tiles strictly above the diagonal, store i >= j only
+  kGemmKEndByCol = 2,    // op(B)(j, c) = 0 for j > c (lower-triangular B^T): K range ends at the tile's last column
+  kGemmKStartByCol = 4,  // op(B)(j, c) = 0 for j < c (lower-triangular B): K range starts at the tile's first column
+  kGemmKEndByRow = 8,    // op(A)(i, j) = 0 for j > i (lower-triangular A): K range ends at the tile's last row
+};
+
+struct GemmArgs {
+  int M, N, K;
+  double alpha, beta;
+  const double* A;
+  long long lda, sA;
+  const double* B;
+  long long ldb, sB;
+  double* C;
+  long long ldc, sC;
+  int flags;
+  int vec;   // 1: every operand row/column start is 16-byte aligned (16-byte cp.async)
+  int Ktot;  // split-K: batch z covers K indices [z K, min((z+1) K, Ktot)) (0: plain batch)
+};
+
+template <int BM, int BN, int WM, int WN>
+struct GemmShape {
+  static constexpr int THREADS = (BM / WM) * (BN / WN) * 32;
+};
+
+template <int BMN, int BK, bool KROWS>
+__host__ __device__ constexpr int tile_doubles() {
+  return KROWS ? BK * (BMN + 8) : BMN * (BK + 4);
+}
+
+template <int BM, int BN, int BK, int ST, bool TA, bool TB>
+constexpr size_t gemm_smem_bytes() {
+  return (size_t)ST * (tile_doubles<BM, BK, !TA>() + tile_doubles<BN, BK, TB>()) * 8;
+}
+
+// Issue the cp.async copies of one operand tile.  KROWS: the tile's global
+// memory is contiguous along the M/N index (rows of the smem tile are k).
+//   KROWS:  element (mn, kk) at P[mn + kk * ld]
+//   !KROWS: element (mn, kk) at P[kk + mn * ld]
+template <int BMN, int BK, int THREADS, bool KROWS>
+__device__ __forceinline__ void gemm_load_tile(double* sm, const double* P, long long ld, int mn0, int MN, int k0,
+                                               int kend, bool vec, int tid) {
+  if (KROWS) {
+    constexpr int CPR = BMN / 2;                  // 16-byte chunks per k-row
+    constexpr int NCH = BK * CPR;
+#pragma unroll
+    for (int q = 0; q < (NCH + THREADS - 1) / THREADS; ++q) {
+      const int idx = tid + q * THREADS;
+      if (NCH % THREADS == 0 || idx < NCH) {
+        const int kr = idx / CPR, c2 = (idx - kr * CPR) * 2;
+        const int mn = mn0 + c2, kk = k0 + kr;
+        double* dst = sm + kr * (BMN + 8) + c2;
+        const bool ok = kk < kend && mn < MN;
+        const double* src = ok ? P + (size_t)mn + (size_t)kk * ld : P;
+        if (vec) {
+          cp_async_n16(dst, src, ok ? (mn + 1 < MN ? 16 : 8) : 0);
+        } else {
+          cp_async8(dst, src, ok);
+          cp_async8(dst + 1, ok && mn + 1 < MN ? src + 1 : P, ok && mn + 1 < MN);
+        }
+      }
+    }
+  } else {
+    constexpr int CPR = BK / 2;                   // chunks per mn-row
+    constexpr int NCH = BMN * CPR;
+#pragma unroll
+    for (int q = 0; q < (NCH + THREADS - 1) / THREADS; ++q) {
+      const int idx = tid + q * THREADS;
+      if (NCH % THREADS == 0 || idx < NCH) {
+        const int r = idx / CPR, c2 = (idx - r * CPR) * 2;
+        const int mn = mn0 + r, kk = k0 + c2;
+        double* dst = sm + r * (BK + 4) + c2;
+        const bool ok = kk < kend && mn < MN;
+        const double* src = ok ? P + (size_t)kk + (size_t)mn * ld : P;
+        if (vec) {
+          cp_async_n16(dst, src, ok ? (kk + 1 < kend ? 16 : 8) : 0);
+        } else {
+          cp_async8(dst, src, ok);
+          cp_async8(dst + 1, ok && kk + 1 < kend ? src + 1 : P, ok && kk + 1 < kend);
+        }
+      }
+    }
+  }
+}
+
+// VAR 0: plain; 1: operands swapped in the mma (accumulates C^T fragments);
+// 2: fragments of the next k4 step loaded before the current step's DMMAs
+template <int BM, int BN, int BK, int WM, int WN, int ST, bool TA, bool TB, int VAR = 0>
+__global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32) k_gemm(GemmArgs g) {
+  constexpr int THREADS = GemmShape<BM, BN, WM, WN>::THREADS;
+  constexpr int FM = WM / 8, FN = WN / 8;
+  constexpr bool AK = !TA, BKR = TB;      // smem layout: k-rows?
+  constexpr int TA_D = tile_doubles<BM, BK, AK>(), TB_D = tile_doubles<BN, BK, BKR>();
+  extern __shared__ __align__(16) double gsm[];
+  const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
+  if ((g.flags & kGemmLowerTiles) && m0 + BM <= n0) return;
+  const int z = blockIdx.z;
+  const double* A = g.A + (size_t)z * g.sA;
+  const double* B = g.B + (size_t)z * g.sB;
+  double* C = g.C + (size_t)z * g.sC;
+  int kbeg = 0, kend = g.Ktot > 0 ? min(g.K, g.Ktot - z * g.K) : g.K;
+  if (g.flags & kGemmKEndByCol) kend = min(kend, n0 + BN);
+  if (g.flags & kGemmKEndByRow) kend = min(kend, m0 + BM);
+  if (g.flags & kGemmKStartByCol) kbeg = (n0 / BK) * BK;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int WGN = BN / WN;
+  const int wm = warp / WGN, wn = warp % WGN;
+  const bool vec = g.vec != 0;
+  const int nk = kend > kbeg ? (kend - kbeg + BK - 1) / BK : 0;
+
+  double acc[FM][FN][2];
+#pragma unroll
+  for (int i = 0; i < FM; ++i)
+#pragma unroll
+    for (int j = 0; j < FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  auto issue = [&](int t) {
+    const int k0 = kbeg + t * BK, s = t % ST;
+    gemm_load_tile<BM, BK, THREADS, AK>(gsm + s * (TA_D + TB_D), A, g.lda, m0, g.M, k0, kend, vec, tid);
+    gemm_load_tile<BN, BK, THREADS, BKR>(gsm + s * (TA_D + TB_D) + TA_D, B, g.ldb, n0, g.N, k0, kend, vec, tid);
+  };
+#pragma unroll
+  for (int t = 0; t < ST - 1; ++t) {
+    if (t < nk) issue(t);
+    cp_async_commit();
+  }
+  for (int t = 0; t < nk; ++t) {
+    cp_async_wait<ST - 2>();
+    __syncthreads();
+    if (t + ST - 1 < nk) issue(t + ST - 1);
+    cp_async_commit();
+    const double* As = gsm + (t % ST) * (TA_D + TB_D);
+    const double* Bs = As + TA_D;
+    auto lda_ = [&](int i, int k4) {
+      const int r = wm * WM + i * 8 + (lane >> 2), c = k4 + (lane & 3);
+      return AK ? As[c * (BM + 8) + r] : As[r * (BK + 4) + c];
+    };
+    auto ldb_ = [&](int j, int k4) {
+      const int cidx = wn * WN + j * 8 + (lane >> 2), kk = k4 + (lane & 3);
+      return BKR ? Bs[kk * (BN + 8) + cidx] : Bs[cidx * (BK + 4) + kk];
+    };
+    if (VAR == 2) {
+      double af[2][FM], bf[2][FN];
+#pragma unroll
+      for (int i = 0; i < FM; ++i) af[0][i] = lda_(i, 0);
+#pragma unroll
+      for (int j = 0; j < FN; ++j) bf[0][j] = ldb_(j, 0);
+#pragma unroll
+      for (int k4 = 0; k4 < BK; k4 += 4) {
+        const int cur = (k4 / 4) & 1;
+        if (k4 + 4 < BK) {
+#pragma unroll
+          for (int i = 0; i < FM; ++i) af[cur ^ 1][i] = lda_(i, k4 + 4);
+#pragma unroll
+          for (int j = 0; j < FN; ++j) bf[cur ^ 1][j] = ldb_(j, k4 + 4);
+        }
+#pragma unroll
+        for (int i = 0; i < FM; ++i)
+#pragma unroll
+          for (int j = 0; j < FN; ++j) dmma(acc[i][j][0], acc[i][j][1], af[cur][i], bf[cur][j]);
+      }
+    } else {
+#pragma unroll
+      for (int k4 = 0; k4 < BK; k4 += 4) {
+        double af[FM], bf[FN];
+#pragma unroll
+        for (int i = 0; i < FM; ++i) af[i] = lda_(i, k4);
+#pragma unroll
+        for (int j = 0; j < FN; ++j) bf[j] = ldb_(j, k4);
+#pragma unroll
+        for (int i = 0; i < FM; ++i)
+#pragma unroll
+          for (int j = 0; j < FN; ++j) {
+            if (VAR == 1) dmma(acc[i][j][0], acc[i][j][1], bf[j], af[i]);
+            else dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+          }
+      }
+    }
+  }
+  cp_async_wait<0>();
+  // epilogue: C = alpha acc + beta C (beta == 0: C not read)
+  const bool lower = (g.flags & kGemmLowerTiles) != 0;
+#pragma unroll
+  for (int i = 0; i < FM; ++i) {
+#pragma unroll
+    for (int j = 0; j < FN; ++j) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int r = m0 + wm * WM + i * 8 + (VAR == 1 ? 2 * (lane & 3) + h : (lane >> 2));
+        const int c = n0 + wn * WN + j * 8 + (VAR == 1 ? (lane >> 2) : 2 * (lane & 3) + h);
+        if (r >= g.M || c >= g.N || (lower && c > r)) continue;
+        double* p = C + (size_t)r + (size_t)c * g.ldc;
+        const double v = g.alpha * acc[i][j][h];
+        *p = g.beta == 0.0 ? v : fma(g.beta, *p, v);
+      }
+    }
+  }
+}
+
+template <int BM, int BN, int BK, int WM, int WN, int ST, bool TA, bool TB, int VAR = 0>
+static void gemm_launch(const GemmArgs& a, int batch, cudaStream_t st) {
+  constexpr size_t smem = gemm_smem_bytes<BM, BN, BK, ST, TA, TB>();
+  constexpr int threads = GemmShape<BM, BN, WM, WN>::THREADS;
+  auto kern = k_gemm<BM, BN, BK, WM, WN, ST, TA, TB, VAR>;
+  static std::atomic<int> raised{0};   // benign duplicated first call (same attribute value)
+  if (!raised.load()) {
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    raised.store(1);
+  }
+  const dim3 grid((a.M + BM - 1) / BM, (a.N + BN - 1) / BN, batch);
+  kern<<<grid, threads, smem, st>>>(a);
+}
+
+// tile configurations (BM, BN, BK, warp tile, stages); FETIGPU_GEMM_CFG
+// forces one (sweeps), otherwise chosen by the number of output tiles
+static int gemm_forced_cfg() {
+  static std::atomic<int> v{-2};
+  if (v.load() == -2) {
+    const char* e = getenv("FETIGPU_GEMM_CFG");
+    v.store(e ? atoi(e) : -1);
+  }
+  return v.load();
+}
+
+// Measured on a B200 (tools/gemm_sweep.py, profiles/r02_gemm_sweep.log):
+// small 64 x 64 tiles with 4 warps (32 x 32 warp tiles) and 3-4 resident
+// CTAs per SM keep the DMMA pipe busiest (30-32 TFLOP/s = 81-87% of the
+// measured DMMA peak at 2048^3 .. 4096^3); 128 x 128 tiles with one CTA per
+// SM stall on the k-tile barrier (24-28 TFLOP/s).
+template <bool TA, bool TB>
+static void gemm_cfg(int cfg, const GemmArgs& a, int batch, cudaStream_t st) {
+  switch (cfg) {
+    case 1: gemm_launch<128, 64, 16, 32, 32, 3, TA, TB>(a, batch, st); break;
+    case 2: gemm_launch<64, 64, 16, 32, 32, 3, TA, TB>(a, batch, st); break;
+    case 3: gemm_launch<64, 64, 16, 32, 32, 2, TA, TB>(a, batch, st); break;
+    default: gemm_launch<64, 64, 32, 32, 32, 2, TA, TB>(a, batch, st); break;
+  }
+}
+
+template <bool TA, bool TB>
+static void gemm_dispatch(const GemmArgs& a, int batch, cudaStream_t st) {
+  gemm_cfg<TA, TB>(gemm_forced_cfg(), a, batch, st);
+}
+
+// C = alpha op(A) op(B) + beta C, column-major (BLAS dgemm semantics), with
+// `batch` strided instances and the GemmFlags above.
+static void gemm(cudaStream_t st, bool ta, bool tb, int M, int N, int K, double alpha, const double* A,
+                 long long lda, const double* B, long long ldb, double beta, double* C, long long ldc, int flags = 0,
+                 int batch = 1, long long sA = 0, long long sB = 0, long long sC = 0) {
+  if (M <= 0 || N <= 0 || batch <= 0) return;
+  const bool vec = ((uintptr_t)A % 16 == 0) && ((uintptr_t)B % 16 == 0) && (lda % 2 == 0) && (ldb % 2 == 0) &&
+                   (sA % 2 == 0) && (sB % 2 == 0);
+  GemmArgs a{M, N, std::max(K, 0), alpha, beta, A, lda, sA, B, ldb, sB, C, ldc, sC, flags, vec ? 1 : 0, 0};
+  if (!ta && !tb) gemm_dispatch<false, false>(a, batch, st);
+  else if (!ta && tb) gemm_dispatch<false, true>(a, batch, st);
+  else if (ta && !tb) gemm_dispatch<true, false>(a, batch, st);
+  else gemm_dispatch<true, true>(a, batch, st);
+  LAUNCH_CHECK();
+}
+
+// Deterministic split-K for small outputs with a long inner dimension (the
+// m-deep Grams and CGS coefficients of the explicit RRS store): S fixed
+// segments (a function of M, N, K only) into a workspace, summed in segment
+// order.  `ws` must hold gemm_splitk_ws(M, N, K) doubles; falls back to the
+// plain GEMM when splitting does not pay.
+__global__ void k_splitk_sum(int M, int N, int S, const double* __restrict__ part, double alpha, double beta,
+                             double* __restrict__ C, long long ldc, int lower) {
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < (long long)M * N;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int c = (int)(idx / M), r = (int)(idx - (long long)c * M);
+    if (lower && c > r) continue;
+    double s = 0.0;
+    for (int q = 0; q < S; ++q) s += part[(size_t)q * M * N + idx];
+    double* p = C + (size_t)r + (size_t)c * ldc;
+    *p = beta == 0.0 ? alpha * s : fma(beta, *p, alpha * s);
+  }
+}
+// Split count: the fewest fixed K segments (each >= 512 deep) that fill the
+// last wave of 64 x 64 tiles (about 3 resident CTAs on each of 148 SMs) within
+// 8%; 1 when the plain tile grid already does.
+static int gemm_splitk_segments(int M, int N, int K) {
+  const long long tiles = (long long)((M + 63) / 64) * ((N + 63) / 64), slots = 3 * 148;
+  auto eff = [&](long long units) { return (double)units / (double)(((units + slots - 1) / slots) * slots); };
+  if (eff(tiles) >= 0.92 || K < 1024) return 1;
+  int best = 1;
+  double be = eff(tiles);
+  for (int S = 2; S <= 16 && K / S >= 512; ++S) {
+    const double e = eff(tiles * S);
+    if (e > be + 0.03) { best = S; be = e; }
+    if (be >= 0.92) break;
+  }
+  return best;
+}
+static size_t gemm_splitk_ws(int M, int N, int K) {
+  const int S = gemm_splitk_segments(M, N, K);
+  return S > 1 ? (size_t)S * M * N : 0;
+}
+static void gemm_splitk(cudaStream_t st, bool ta, bool tb, int M, int N, int K, double alpha, const double* A,
+                        long long lda, const double* B, long long ldb, double beta, double* C, long long ldc,
+                        double* ws, int flags = 0) {
+  const int S = gemm_splitk_segments(M, N, K);
+  if (S <= 1 || M <= 0 || N <= 0) {
+    gemm(st, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, flags);
+    return;
+  }
+  const int kseg = (((K + S - 1) / S) + 15) / 16 * 16;
+  const int nseg = (K + kseg - 1) / kseg;
+  const long long sA = ta ? kseg : (long long)kseg * lda;
+  const long long sB = tb ? (long long)kseg * ldb : kseg;
+  const bool vec = ((uintptr_t)A % 16 == 0) && ((uintptr_t)B % 16 == 0) && (lda % 2 == 0) && (ldb % 2 == 0);
+  GemmArgs a{M, N, kseg, 1.0, 0.0, A, lda, sA, B, ldb, sB, ws, M, (long long)M * N,
+             flags & ~(kGemmKEndByCol | kGemmKStartByCol | kGemmKEndByRow), vec ? 1 : 0, K};
+  if (!ta && !tb) gemm_dispatch<false, false>(a, nseg, st);
+  else if (!ta && tb) gemm_dispatch<false, true>(a, nseg, st);
+  else if (ta && !tb) gemm_dispatch<true, false>(a, nseg, st);
+  else gemm_dispatch<true, true>(a, nseg, st);
+  LAUNCH_CHECK();
+  k_splitk_sum<<<grid_for((long long)M * N), kThreads, 0, st>>>(M, N, nseg, ws, alpha, beta, C, ldc,
+                                                                 (flags & kGemmLowerTiles) ? 1 : 0);
+  LAUNCH_CHECK();
+}
+
+// ------------------------------------------- lower-triangular inverse --
+// X = L^{-1} for the 64 x 64 (or smaller, last) diagonal blocks: one CTA per
+// block, column j of X by forward substitution on e_j (the per-column
+// arithmetic of a triangular solve on the identity).
+constexpr int kTriNB = 64;
+__global__ void __launch_bounds__(kTriNB) k_tri_inv_diag(const double* __restrict__ L, long long ldl, int n,
+                                                         double* __restrict__ X, long long ldx) {
+  __shared__ double Ls[kTriNB][kTriNB + 1];
+  const int b0 = blockIdx.x * kTriNB;
+  const int nb = min(kTriNB, n - b0);
+  for (int idx = threadIdx.x; idx < nb * nb; idx += blockDim.x) {
+    const int c = idx / nb, r = idx - c * nb;
+    Ls[r][c] = r >= c ? L[(size_t)(b0 + r) + (size_t)(b0 + c) * ldl] : 0.0;
+  }
+  __syncthreads();
+  const int j = threadIdx.x;
+  if (j >= nb) return;
+  double x[kTriNB];
+#pragma unroll
+  for (int i = 0; i < kTriNB; ++i) x[i] = 0.0;
+#pragma unroll
+  for (int i = 0; i < kTriNB; ++i) {
+    if (i < nb && i >= j) {
+      double s = i == j ? 1.0 : 0.0;
+#pragma unroll
+      for (int q = 0; q < kTriNB; ++q)
+        if (q < i) s -= Ls[i][q] * x[q];
+      x[i] = s / Ls[i][i];
+    }
+  }
+  // column j of the inverse (zeros above the diagonal)
+#pragma unroll
+  for (int i = 0; i < kTriNB; ++i)
+    if (i < nb) X[(size_t)(b0 + i) + (size_t)(b0 + j) * ldx] = x[i];
+}
+
+// X = L^{-1} (n x n lower; X lower with explicit zeros above the diagonal).
+// Diagonal 64-blocks by substitution, then the blocked recursion
+//   X21 = -X22 (L21 X11)
+// on splits at multiples of 64.  Workspace T: >= (n/2 + 64)^2 doubles.
+static void tri_inv_rec(cudaStream_t st, const double* L, long long ldl, int n, double* X, long long ldx, double* T) {
+  if (n <= kTriNB) return;
+  const int n1 = ((n / 2 + kTriNB - 1) / kTriNB) * kTriNB, n2 = n - n1;
+  tri_inv_rec(st, L, ldl, n1, X, ldx, T);
+  tri_inv_rec(st, L + (size_t)n1 + (size_t)n1 * ldl, ldl, n2, X + (size_t)n1 + (size_t)n1 * ldx, ldx, T);
+  // T = L21 X11 (n2 x n1; X11 lower: K range of column c starts at c)
+  gemm(st, false, false, n2, n1, n1, 1.0, L + n1, ldl, X, ldx, 0.0, T, n2, kGemmKStartByCol);
+  // X21 = -X22 T (X22 lower: K range of row r ends at r)
+  gemm(st, false, false, n2, n1, n2, -1.0, X + (size_t)n1 + (size_t)n1 * ldx, ldx, T, n2, 0.0, X + n1, ldx,
+       kGemmKEndByRow);
+}
+
+__global__ void k_zero_upper(double* X, long long ldx, int n) {
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < (long long)n * n;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int c = (int)(idx / n), r = (int)(idx - (long long)c * n);
+    if (r < c) X[(size_t)r + (size_t)c * ldx] = 0.0;
+  }
+}
+
+static size_t tri_inv_workspace(int n) {
+  const size_t h = (size_t)n / 2 + kTriNB;
+  return h * h;
+}
+
+static void tri_inv_lower(cudaStream_t st, const double* L, long long ldl, int n, double* X, long long ldx, double* T) {
+  if (n <= 0) return;
+  k_zero_upper<<<grid_for((long long)n * n), kThreads, 0, st>>>(X, ldx, n);
+  k_tri_inv_diag<<<(n + kTriNB - 1) / kTriNB, kTriNB, 0, st>>>(L, ldl, n, X, ldx);
+  LAUNCH_CHECK();
+  tri_inv_rec(st, L, ldl, n, X, ldx, T);
+}
+
+// ----------------------------------------------------------- GEMVs --
+// Row-major m x k blocks W(i, c) = W[i * ldw + c] (the RRS direction blocks).
+// t = W^T r (length k), deterministic two-stage reduction: stage 1 sums a
+// fixed row segment per CTA (columns over threads, two per thread), stage 2
+// adds the segment partials in segment order.
+constexpr int kGvSeg = 296;     // row segments (2 per SM)
+__global__ void __launch_bounds__(256) k_gemv_rm_t_part(const double* __restrict__ W, long long ldw, int m, int k,
+                                                        const double* __restrict__ r, double* __restrict__ part) {
+  const int c = (blockIdx.x * 256 + threadIdx.x) * 2;
+  const int seg = blockIdx.y, nseg = gridDim.y;
+  const long long i0 = (long long)m * seg / nseg, i1 = (long long)m * (seg + 1) / nseg;
+  if (c >= k) return;
+  const bool two = c + 1 < k;
+  const bool vec = two && (ldw % 2 == 0) && ((uintptr_t)W % 16 == 0);
+  double s0 = 0.0, s1 = 0.0;
+  long long i = i0;
+  for (; i + 4 <= i1; i += 4) {
+    double w0[4], w1[4], rv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const double* p = W + (size_t)(i + u) * ldw + c;
+      if (vec) {
+        const double2 v = __ldg(reinterpret_cast<const double2*>(p));
+        w0[u] = v.x; w1[u] = v.y;
+      } else {
+        w0[u] = p[0]; w1[u] = two ? p[1] : 0.0;
+      }
+      rv[u] = r[i + u];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) { s0 = fma(w0[u], rv[u], s0); s1 = fma(w1[u], rv[u], s1); }
+  }
+  for (; i < i1; ++i) {
+    const double* p = W + (size_t)i * ldw + c;
+    s0 = fma(p[0], r[i], s0);
+    if (two) s1 = fma(p[1], r[i], s1);
+  }
+  part[(size_t)seg * k + c] = s0;
+  if (two) part[(size_t)seg * k + c + 1] = s1;
+}
+__global__ void k_gemv_seg_sum(const double* __restrict__ part, int nseg, int k, double alpha,
+                               double* __restrict__ t) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= k) return;
+  double s = 0.0;
+  for (int q = 0; q < nseg; ++q) s += part[(size_t)q * k + c];
+  t[c] = alpha * s;
+}
+static void gemv_rm_t(cudaStream_t st, const double* W, long long ldw, int m, int k, const double* r, double* t,
+                      double* part /* kGvSeg * k */) {
+  if (k <= 0) return;
+  k_gemv_rm_t_part<<<dim3((k + 511) / 512, kGvSeg), 256, 0, st>>>(W, ldw, m, k, r, part);
+  k_gemv_seg_sum<<<(k + 255) / 256, 256, 0, st>>>(part, kGvSeg, k, 1.0, t);
+  LAUNCH_CHECK();
+}
+
+// Alg. 1 lines 14-15 fused: lambda += W yh, r -= Q yh (one warp per row,
+// lanes over the k columns, fixed shuffle order)
+__global__ void __launch_bounds__(256) k_rrs_update(const double* __restrict__ W, const double* __restrict__ Q,
+                                                    long long ld, int m, int k, const double* __restrict__ yh,
+                                                    double* __restrict__ lam, double* __restrict__ r) {
+  extern __shared__ double ys[];
+  for (int c = threadIdx.x; c < k; c += blockDim.x) ys[c] = yh[c];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  for (long long i = (long long)blockIdx.x * 8 + (threadIdx.x >> 5); i < m; i += (long long)gridDim.x * 8) {
+    const double* w = W + (size_t)i * ld;
+    const double* q = Q + (size_t)i * ld;
+    double a = 0.0, b = 0.0;
+    for (int c = lane; c < k; c += 32) {
+      a = fma(w[c], ys[c], a);
+      b = fma(q[c], ys[c], b);
+    }
+    a = warp_sum(a);
+    b = warp_sum(b);
+    if (lane == 0) {
+      lam[i] += a;
+      r[i] -= b;
+    }
+  }
+}
+
+// small column-major GEMV: y = alpha op(A) x + beta y (A: M x N)
+__global__ void k_gemv_cm_n(int M, int N, double alpha, const double* __restrict__ A, long long lda,
+                            const double* __restrict__ x, double beta, double* __restrict__ y) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= M) return;
+  double s = 0.0;
+  for (int j = 0; j < N; ++j) s = fma(A[(size_t)i + (size_t)j * lda], x[j], s);
+  y[i] = beta == 0.0 ? alpha * s : fma(beta, y[i], alpha * s);
+}
+__global__ void k_gemv_cm_t(int M, int N, double alpha, const double* __restrict__ A, long long lda,
+                            const double* __restrict__ x, double beta, double* __restrict__ y) {
+  const int j = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (j >= N) return;
+  double s = 0.0;
+  for (int i = lane; i < M; i += 32) s = fma(A[(size_t)i + (size_t)j * lda], x[i], s);
+  s = warp_sum(s);
+  if (lane == 0) y[j] = beta == 0.0 ? alpha * s : fma(beta, y[j], alpha * s);
+}
+static void gemv_cm(cudaStream_t st, bool trans, int M, int N, double alpha, const double* A, long long lda,
+                    const double* x, double beta, double* y) {
+  if (!trans && M > 0) k_gemv_cm_n<<<(M + 255) / 256, 256, 0, st>>>(M, N, alpha, A, lda, x, beta, y);
+  if (trans && N > 0) k_gemv_cm_t<<<(N + 7) / 8, 256, 0, st>>>(M, N, alpha, A, lda, x, beta, y);
+  LAUNCH_CHECK();
+}
+// y = A^T x for a tall column-major A (M >> N): fixed row segments per warp,
+// partials summed in segment order (part: kGvSeg * N doubles)
+__global__ void k_gemv_cm_t_part(int M, int N, const double* __restrict__ A, long long lda,
+                                 const double* __restrict__ x, double* __restrict__ part) {
+  const int j = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  const int seg = blockIdx.y, nseg = gridDim.y;
+  if (j >= N) return;
+  const long long i0 = (long long)M * seg / nseg, i1 = (long long)M * (seg + 1) / nseg;
+  double s = 0.0;
+  for (long long i = i0 + lane; i < i1; i += 32) s = fma(A[(size_t)i + (size_t)j * lda], x[i], s);
+  s = warp_sum(s);
+  if (lane == 0) part[(size_t)seg * N + j] = s;
+}
+static void gemv_cm_t_tall(cudaStream_t st, int M, int N, const double* A, long long lda, const double* x, double* y,
+                           double* part) {
+  if (N <= 0) return;
+  k_gemv_cm_t_part<<<dim3((N + 7) / 8, kGvSeg), 256, 0, st>>>(M, N, A, lda, x, part);
+  k_gemv_seg_sum<<<(N + 255) / 256, 256, 0, st>>>(part, kGvSeg, N, 1.0, y);
+  LAUNCH_CHECK();
+}
+
+// y += a x over size_t lengths
+__global__ void k_axpy_n(size_t n, double a, const double* __restrict__ x, double* __restrict__ y) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    y[i] = fma(a, x[i], y[i]);
+}
+static void axpy(cudaStream_t st, size_t n, double a, const double* x, double* y) {
+  if (!n) return;
+  const size_t blocks = std::min<size_t>((n + 255) / 256, (size_t)148 * 16);
+  k_axpy_n<<<(unsigned)blocks, 256, 0, st>>>(n, a, x, y);
+  LAUNCH_CHECK();
+}
+
+// C (rows x cols, ldc) = alpha A^T with A cols x rows (lda), column-major;
+// both sides coalesced through a 32 x 33 shared tile
+__global__ void k_transpose_scale(int rows, int cols, double alpha, const double* __restrict__ A, long long lda,
+                                  double* __restrict__ C, long long ldc) {
+  __shared__ double t[32][33];
+  const int r0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
+  for (int q = threadIdx.y; q < 32; q += blockDim.y) {   // t[x][q] = A(c0 + x, r0 + q)
+    const int ac = c0 + threadIdx.x, ar = r0 + q;
+    if (ac < cols && ar < rows) t[threadIdx.x][q] = A[(size_t)ac + (size_t)ar * lda];
+  }
+  __syncthreads();
+  for (int q = threadIdx.y; q < 32; q += blockDim.y) {   // C(r0 + x, c0 + q) = A(c0 + q, r0 + x)
+    const int rr = r0 + threadIdx.x, cc = c0 + q;
+    if (rr < rows && cc < cols) C[(size_t)rr + (size_t)cc * ldc] = alpha * t[q][threadIdx.x];
+  }
+}
+static void transpose_scale(cudaStream_t st, int rows, int cols, double alpha, const double* A, long long lda,
+                            double* C, long long ldc) {
+  if (rows <= 0 || cols <= 0) return;
+  k_transpose_scale<<<dim3((rows + 31) / 32, (cols + 31) / 32), dim3(32, 8), 0, st>>>(rows, cols, alpha, A, lda, C,
+                                                                                      ldc);
+  LAUNCH_CHECK();
+}
+
+}  // namespace fg

@@ -271,6 +271,22 @@ int fetigpu_apply_F_block_device(fetigpu_ctx* ctx, const double* W, int ldw, dou
   });
 }
 
+// test hook: Q = F Z through K5z for a per-subdomain preconditioner block
+// (row-major m x N_s host buffers); FETIGPU_E_CONFIG when not applicable
+int fetigpu_apply_F_zblock(fetigpu_ctx* ctx, const double* Z, double* Q) {
+  return guarded([&] {
+    NEED_BUILT(ctx);
+    Ctx& c = ctx->c;
+    const size_t n = (size_t)c.su.m * c.su.Ns;
+    DBuf<double> dz, dq;
+    dz.alloc(std::max<size_t>(n, 1)); dq.alloc(std::max<size_t>(n, 1));
+    CK(cudaMemcpyAsync(dz.p, Z, n * 8, cudaMemcpyHostToDevice, c.st));
+    if (!c.apply_F_block_z(dz.p, dq.p, c.su.Ns)) fail(FETIGPU_E_CONFIG, "K5z: not a FETI-DP block with that structure");
+    CK(cudaMemcpyAsync(Q, dq.p, n * 8, cudaMemcpyDeviceToHost, c.st));
+    CK(cudaStreamSynchronize(c.st));
+  });
+}
+
 int fetigpu_time_apply_block(fetigpu_ctx* ctx, const double* W, double* Q, int k, int reps, double* ms) {
   return guarded([&] {
     NEED_BUILT(ctx);
@@ -322,6 +338,75 @@ int fetigpu_fp64_peak(double* tflops_dmma, double* tflops_dfma) {
   });
 }
 
+// ---- dense algebra hooks (dla.cuh): host-buffer GEMM / triangular inverse
+// for the parity tests, device-resident GEMM timing for the bench
+int fetigpu_dla_gemm(int ta, int tb, int M, int N, int K, double alpha, const double* A, long long lda,
+                     const double* B, long long ldb, double beta, double* C, long long ldc, int flags) {
+  return guarded([&] {
+    if (M < 0 || N < 0 || K < 0) fail(FETIGPU_E_INVALID_ARGUMENT, "bad dimensions");
+    if (!M || !N) return;
+    cudaStream_t st;
+    CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    std::unique_ptr<CUstream_st, decltype(&cudaStreamDestroy)> st_guard(st, cudaStreamDestroy);
+    const size_t na = (size_t)lda * (ta ? M : K), nb = (size_t)ldb * (tb ? K : N), nc = (size_t)ldc * N;
+    DBuf<double> dA, dB, dC, ws;
+    dA.alloc(std::max<size_t>(na, 1)); dB.alloc(std::max<size_t>(nb, 1)); dC.alloc(nc);
+    if (na) CK(cudaMemcpyAsync(dA.p, A, na * 8, cudaMemcpyHostToDevice, st));
+    if (nb) CK(cudaMemcpyAsync(dB.p, B, nb * 8, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(dC.p, C, nc * 8, cudaMemcpyHostToDevice, st));
+    if (flags & 256) {   // split-K path of the same product
+      ws.alloc(std::max<size_t>(1, gemm_splitk_ws(M, N, K)));
+      gemm_splitk(st, ta, tb, M, N, K, alpha, dA.p, lda, dB.p, ldb, beta, dC.p, ldc, ws.p, flags & 255);
+    } else {
+      gemm(st, ta, tb, M, N, K, alpha, dA.p, lda, dB.p, ldb, beta, dC.p, ldc, flags);
+    }
+    CK(cudaMemcpyAsync(C, dC.p, nc * 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  });
+}
+
+int fetigpu_dla_tri_inv(const double* L, int n, long long ldl, double* X) {
+  return guarded([&] {
+    if (n <= 0) return;
+    cudaStream_t st;
+    CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    std::unique_ptr<CUstream_st, decltype(&cudaStreamDestroy)> st_guard(st, cudaStreamDestroy);
+    DBuf<double> dL, dX, ws;
+    dL.alloc((size_t)ldl * n); dX.alloc((size_t)n * n); ws.alloc(tri_inv_workspace(n));
+    CK(cudaMemcpyAsync(dL.p, L, (size_t)ldl * n * 8, cudaMemcpyHostToDevice, st));
+    tri_inv_lower(st, dL.p, ldl, n, dX.p, n, ws.p);
+    CK(cudaMemcpyAsync(X, dX.p, (size_t)n * n * 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  });
+}
+
+int fetigpu_dla_time_gemm(int ta, int tb, int M, int N, int K, int reps, double* ms) {
+  return guarded([&] {
+    if (M <= 0 || N <= 0 || K <= 0 || reps <= 0) fail(FETIGPU_E_INVALID_ARGUMENT, "bad dimensions");
+    cudaStream_t st;
+    CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    std::unique_ptr<CUstream_st, decltype(&cudaStreamDestroy)> st_guard(st, cudaStreamDestroy);
+    const long long lda = ta ? K : M, ldb = tb ? N : K;
+    DBuf<double> dA, dB, dC;
+    dA.alloc((size_t)M * K); dB.alloc((size_t)K * N); dC.alloc((size_t)M * N);
+    k_fill_random<<<grid_for((long long)M * K), kThreads, 0, st>>>(dA.p, (size_t)M * K, 1);
+    k_fill_random<<<grid_for((long long)K * N), kThreads, 0, st>>>(dB.p, (size_t)K * N, 2);
+    gemm(st, ta, tb, M, N, K, 1.0, dA.p, lda, dB.p, ldb, 0.0, dC.p, M);   // warm-up
+    cudaEvent_t a, b;
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+    CK(cudaEventRecord(a, st));
+    for (int r = 0; r < reps; ++r) gemm(st, ta, tb, M, N, K, 1.0, dA.p, lda, dB.p, ldb, 0.0, dC.p, M);
+    CK(cudaEventRecord(b, st));
+    CK(cudaEventSynchronize(b));
+    float t = 0;
+    CK(cudaEventElapsedTime(&t, a, b));
+    *ms = t / reps;
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+  });
+}
+
 int fetigpu_pivoted_cholesky(const double* a, int n, double tol, int* perm, double* lower, int* rank) {
   return guarded([&] {
     if (n < 0 || (n > 0 && (!a || !perm || !lower || !rank))) fail(FETIGPU_E_INVALID_ARGUMENT, "bad arguments");
@@ -366,11 +451,7 @@ int fetigpu_pivoted_compress(const int* perm, const double* lower, int n, int ra
     cudaStream_t st;
     CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
     std::unique_ptr<CUstream_st, decltype(&cudaStreamDestroy)> st_guard(st, cudaStreamDestroy);
-    cublasHandle_t h;
-    CB(cublasCreate(&h));
-    std::unique_ptr<cublasContext, decltype(&cublasDestroy)> h_guard(h, cublasDestroy);
-    CB(cublasSetStream(h, st));
-    DBuf<double> L, Linv, W, Wsel, O;
+    DBuf<double> L, Linv, W, Wsel, O, Tw;
     DBuf<int> p;
     L.alloc((size_t)n * n); Linv.alloc((size_t)rank * rank);
     W.alloc((size_t)rows * n); Wsel.alloc((size_t)rows * rank); O.alloc((size_t)rows * rank);
@@ -378,15 +459,12 @@ int fetigpu_pivoted_compress(const int* perm, const double* lower, int n, int ra
     CK(cudaMemcpyAsync(L.p, lower, (size_t)n * n * 8, cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(W.p, w, (size_t)rows * n * 8, cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(p.p, perm, (size_t)n * 4, cudaMemcpyHostToDevice, st));
-    // L~^{-1} by a triangular solve on the identity, W_sel = W N^T[:, :rank],
+    // L~^{-1} (dla.cuh tri_inv_lower), W_sel = W N^T[:, :rank],
     // out = W_sel L~^{-T}: the solver's compression (Alg. 1 lines 10-11)
-    k_identity<<<grid_for((long long)rank * rank), kThreads, 0, st>>>(Linv.p, rank);
-    const double one = 1.0;
-    CB(cublasDtrsm(h, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, rank, rank, &one,
-                   L.p, n, Linv.p, rank));
+    Tw.alloc(tri_inv_workspace(rank));
+    tri_inv_lower(st, L.p, n, rank, Linv.p, rank, Tw.p);
     k_gather_cols<<<dim3(grid_for(rows), rank), kThreads, 0, st>>>(W.p, rows, p.p, rank, Wsel.p);
-    CB(cublasDtrmm(h, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, rows, rank, &one,
-                   Linv.p, rank, Wsel.p, rows, O.p, rows));
+    gemm(st, false, true, rows, rank, rank, 1.0, Wsel.p, rows, Linv.p, rank, 0.0, O.p, rows, kGemmKEndByCol);
     LAUNCH_CHECK();
     CK(cudaMemcpyAsync(out, O.p, (size_t)rows * rank * 8, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));

@@ -423,3 +423,198 @@ __global__ void k_coarse_gather_block(const int* __restrict__ optr, const int* _
 }
 
 }  // namespace fg
+
+namespace fg {
+
+// ---------------- K5z: block F-apply of a fresh preconditioner block ------
+// Q = F Z where Z (row-major m x k, k = N_s) holds the per-subdomain
+// preconditioner columns of Alg. 1 lines 2/16: column s is nonzero only on
+// the dual rows of subdomain s.  B_t^T Z therefore has, per local row a of
+// subdomain t, exactly two nonzero columns: t itself and the other owner o(a)
+// of that row -- at most 5 distinct columns per subdomain (itself and its
+// edge neighbours; FETI-DP corners are primal).  The local products shrink
+// from n_t x k to n_t x 5 (K5z-1), the coarse term keeps its dense form
+// (U = Kbar^{-1} T, DMMA GEMM), and Q is written once per dual row from both
+// owners' contributions in a fixed order (K5z-2): no memset, no atomics.
+constexpr int kZNb = 5;   // neighbour slots per subdomain (slot 0: itself)
+
+// K5z-1, one CTA per subdomain t: Y_t = F''_t X_t (n_t x 5, packed at the
+// op-map positions) and the coarse pre-pass T_t = A''_t^T X_t into the tbuf
+// rows of t at the 5 neighbour columns (tbuf zeroed by the caller).
+__global__ void __launch_bounds__(256) k_bz_local(const OpSub* __restrict__ subs, const DpSub* __restrict__ dps,
+                                                  const double* __restrict__ mats, const int* __restrict__ rows,
+                                                  const double* __restrict__ abc, const int* __restrict__ other,
+                                                  const int* __restrict__ jslot, const int* __restrict__ nbr,
+                                                  const double* __restrict__ Z, int k, double* __restrict__ Y,
+                                                  double* __restrict__ tbuf, int ldt) {
+  extern __shared__ double bzs[];
+  const int t = blockIdx.x;
+  const OpSub d = subs[t];
+  const DpSub p = dps[t];
+  const int ns = d.ns;
+  double* xt = bzs;                 // Z(r_a, t)
+  double* xo = bzs + ns;            // Z(r_a, o(a))
+  int* jo = reinterpret_cast<int*>(bzs + 2 * ns);
+  for (int a = threadIdx.x; a < ns; a += blockDim.x) {
+    const int r = rows[d.map_off + a];
+    const int o = other[d.map_off + a];
+    xt[a] = r >= 0 ? Z[(size_t)r * k + t] : 0.0;
+    xo[a] = (r >= 0 && o >= 0) ? Z[(size_t)r * k + o] : 0.0;
+    jo[a] = jslot[d.map_off + a];
+  }
+  __syncthreads();
+  const double* F = mats + d.moff;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int b = warp; b < ns; b += 8) {
+    const double* fr = F + (size_t)b * d.ld;      // row b of the symmetric F''_t = column b
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0, a4 = 0.0;
+    for (int a = lane; a < ns; a += 32) {
+      const double f = fr[a];
+      a0 = fma(f, xt[a], a0);
+      const double v = f * xo[a];
+      const int j = jo[a];
+      if (j == 1) a1 += v;
+      else if (j == 2) a2 += v;
+      else if (j == 3) a3 += v;
+      else if (j == 4) a4 += v;
+    }
+    a0 = warp_sum(a0); a1 = warp_sum(a1); a2 = warp_sum(a2); a3 = warp_sum(a3); a4 = warp_sum(a4);
+    if (lane == 0) {
+      double* y = Y + (size_t)(d.map_off + b) * kZNb;
+      y[0] = a0; y[1] = a1; y[2] = a2; y[3] = a3; y[4] = a4;
+    }
+  }
+  // T_t(c, j) = sum_a A''(a, c) X(a, j), one thread per (c, j)
+  const double* A = abc + p.abc_off;
+  for (int q = threadIdx.x; q < p.nc * kZNb; q += blockDim.x) {
+    const int c = q / kZNb, j = q - c * kZNb;
+    const int s = nbr[t * kZNb + j];
+    if (s < 0) continue;
+    double acc = 0.0;
+    for (int a = 0; a < ns; ++a) {
+      const double x = j == 0 ? xt[a] : (jo[a] == j ? xo[a] : 0.0);
+      acc = fma(A[(size_t)a * p.nc + c], x, acc);
+    }
+    tbuf[(size_t)(p.t_off + c) * ldt + s] = acc;
+  }
+}
+
+// One group of dual rows shared by the same two subdomains (an interface
+// edge), at most kBzRows rows: entry e of the group is dual row rows[e] at
+// local position b1[e] of t1 and b2[e] of t2 (t2 < 0: single owner).
+struct BzEdge {
+  int t1, t2, e0, cnt;
+};
+constexpr int kBzRows = 128;
+constexpr int kBzCols = 256;
+
+// K5z-2: Q(r, s) = [Y_t1(b1, j1(s)) + A''_t1(b1, :) U_t1(:, s)]
+//                + [Y_t2(b2, j2(s)) + A''_t2(b2, :) U_t2(:, s)]
+// for every column s; one CTA per (edge group, 256-column tile), one column
+// per thread, Q rows written once (coalesced, no atomics).
+__global__ void __launch_bounds__(kBzCols) k_bz_edges(const BzEdge* __restrict__ edges, const int* __restrict__ erow,
+                                                      const int* __restrict__ eb1, const int* __restrict__ eb2,
+                                                      const OpSub* __restrict__ subs, const DpSub* __restrict__ dps,
+                                                      const double* __restrict__ abc, const int* __restrict__ cmap,
+                                                      const int* __restrict__ nbr, const double* __restrict__ Y,
+                                                      const double* __restrict__ U, int k, double* __restrict__ Q) {
+  __shared__ double A1[kBzRows][8], A2[kBzRows][8], Y1[kBzRows][kZNb], Y2[kBzRows][kZNb];
+  __shared__ int R[kBzRows];
+  const BzEdge e = edges[blockIdx.y];
+  const DpSub p1 = dps[e.t1];
+  const DpSub p2 = e.t2 >= 0 ? dps[e.t2] : DpSub{0, 0, 0, 0, 0};
+  const OpSub d1 = subs[e.t1];
+  const OpSub d2 = e.t2 >= 0 ? subs[e.t2] : OpSub{0, 0, 0, 0, 0};
+  for (int q = threadIdx.x; q < e.cnt * 8; q += blockDim.x) {
+    const int i = q >> 3, c = q & 7;
+    const int b1 = eb1[e.e0 + i], b2 = eb2[e.e0 + i];
+    A1[i][c] = c < p1.nc ? abc[p1.abc_off + (size_t)b1 * p1.nc + c] : 0.0;
+    A2[i][c] = (e.t2 >= 0 && c < p2.nc) ? abc[p2.abc_off + (size_t)b2 * p2.nc + c] : 0.0;
+  }
+  for (int q = threadIdx.x; q < e.cnt * kZNb; q += blockDim.x) {
+    const int i = q / kZNb, j = q - i * kZNb;
+    Y1[i][j] = Y[(size_t)(d1.map_off + eb1[e.e0 + i]) * kZNb + j];
+    Y2[i][j] = e.t2 >= 0 ? Y[(size_t)(d2.map_off + eb2[e.e0 + i]) * kZNb + j] : 0.0;
+  }
+  for (int i = threadIdx.x; i < e.cnt; i += blockDim.x) R[i] = erow[e.e0 + i];
+  __syncthreads();
+  const int s = blockIdx.x * kBzCols + threadIdx.x;
+  if (s >= k) return;
+  int j1 = -1, j2 = -1;
+#pragma unroll
+  for (int j = 0; j < kZNb; ++j) {
+    if (nbr[e.t1 * kZNb + j] == s) j1 = j;
+    if (e.t2 >= 0 && nbr[e.t2 * kZNb + j] == s) j2 = j;
+  }
+  double u1[8], u2[8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    u1[c] = c < p1.nc ? U[(size_t)cmap[p1.cmap_off + c] * k + s] : 0.0;
+    u2[c] = (e.t2 >= 0 && c < p2.nc) ? U[(size_t)cmap[p2.cmap_off + c] * k + s] : 0.0;
+  }
+  for (int i = 0; i < e.cnt; ++i) {
+    double v1 = j1 >= 0 ? Y1[i][j1] : 0.0;
+    double v2 = j2 >= 0 ? Y2[i][j2] : 0.0;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      v1 = fma(A1[i][c], u1[c], v1);
+      v2 = fma(A2[i][c], u2[c], v2);
+    }
+    Q[(size_t)R[i] * k + s] = v1 + v2;
+  }
+}
+
+}  // namespace fg
+
+namespace fg {
+
+// CGS update of the implicit RRS store (Alg. 1 line 20 on coordinates),
+// V(r, c) -= sum_l ZV_l(r) N^T(c, l k + t1) + sum_l ZV_l(r) N^T(c, l k + t2)
+// for dual row r shared by t1 < t2, computed once per row (interface-edge
+// groups as in K5z-2): no zeroed m x k buffer, no atomics, no separate AXPY.
+// The arithmetic is that of the zero / atomic-scatter / AXPY sequence it
+// replaces: each owner's sum over l is one fma chain in ascending l, the two
+// owner sums are added (0 + a + b == a + b), and V = fma(-1, D, V).
+// Requires nl <= kZsMax coordinates blocks (the caller falls back otherwise).
+constexpr int kZsMax = 32;
+__global__ void __launch_bounds__(kBzCols) k_rrs_zsub_edges(const BzEdge* __restrict__ edges,
+                                                            const int* __restrict__ erow,
+                                                            const int* __restrict__ ez1, const int* __restrict__ ez2,
+                                                            const double* __restrict__ ZV, long long nz, int nl,
+                                                            const double* __restrict__ NT, int k,
+                                                            double* __restrict__ V) {
+  extern __shared__ double zsm[];            // [cnt][nl] owner 1, then [cnt][nl] owner 2
+  __shared__ int R[kBzRows];
+  const BzEdge e = edges[blockIdx.y];
+  double* z1 = zsm;
+  double* z2 = zsm + (size_t)e.cnt * nl;
+  for (int q = threadIdx.x; q < e.cnt * nl; q += blockDim.x) {
+    const int i = q / nl, l = q - i * nl;
+    z1[i * nl + l] = ZV[(size_t)l * nz + ez1[e.e0 + i]];
+    z2[i * nl + l] = e.t2 >= 0 ? ZV[(size_t)l * nz + ez2[e.e0 + i]] : 0.0;
+  }
+  for (int i = threadIdx.x; i < e.cnt; i += blockDim.x) R[i] = erow[e.e0 + i];
+  __syncthreads();
+  const int c = blockIdx.x * kBzCols + threadIdx.x;
+  if (c >= k) return;
+  double n1[kZsMax], n2[kZsMax];
+#pragma unroll
+  for (int l = 0; l < kZsMax; ++l) {
+    n1[l] = l < nl ? NT[((size_t)l * k + e.t1) * k + c] : 0.0;
+    n2[l] = (l < nl && e.t2 >= 0) ? NT[((size_t)l * k + e.t2) * k + c] : 0.0;
+  }
+  for (int i = 0; i < e.cnt; ++i) {
+    double p1 = 0.0, p2 = 0.0;
+#pragma unroll
+    for (int l = 0; l < kZsMax; ++l) {
+      if (l < nl) {
+        p1 = fma(z1[i * nl + l], n1[l], p1);
+        p2 = fma(z2[i * nl + l], n2[l], p2);
+      }
+    }
+    double* v = V + (size_t)R[i] * k + c;
+    *v = fma(-1.0, p1 + p2, *v);
+  }
+}
+
+}  // namespace fg

@@ -2,8 +2,6 @@
 // shared-memory opt-in), host parallel_for, phase timer and scratch buffers.
 // Part of the libfetigpu unity build (fetigpu.cu includes it); namespace fg.
 #pragma once
-#include <cublas_v2.h>
-
 #include <algorithm>
 #include <atomic>
 #include <chrono>
@@ -32,13 +30,6 @@ namespace fg {
     if (e_ != cudaSuccess)                                                                     \
       fail(e_ == cudaErrorMemoryAllocation ? FETIGPU_E_OUT_OF_MEMORY : FETIGPU_E_CUDA,         \
            std::string(#x) + ": " + cudaGetErrorString(e_));                                   \
-  } while (0)
-#define CB(x)                                                                                  \
-  do {                                                                                         \
-    cublasStatus_t s_ = (x);                                                                   \
-    if (s_ != CUBLAS_STATUS_SUCCESS)                                                           \
-      fail(FETIGPU_E_CUDA, std::string(#x) + " failed (cuBLAS status " + std::to_string((int)s_) + \
-                               ", line " + std::to_string(__LINE__) + ")");                    \
   } while (0)
 #define LAUNCH_CHECK()                                                                         \
   do {                                                                                         \

@@ -346,7 +346,6 @@ int Ctx::solve_rrs(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_tra
   Scal* hs = nullptr;
   CK(cudaMallocHost(&hs, sizeof(Scal)));
   std::unique_ptr<Scal, decltype(&cudaFreeHost)> hs_guard(hs, cudaFreeHost);
-  const double one = 1.0, mone = -1.0, zero = 0.0;
   pt.mark("rrs setup", st);
   CK(cudaEventRecord(ev0, st));
   CK(cudaMemcpyAsync(lam.p, d_lam0.p, m * 8, cudaMemcpyDeviceToDevice, st));
@@ -390,10 +389,10 @@ int Ctx::solve_rrs(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_tra
     apply_F_block(W.p, k, Qb.p, k, k);  // line 7 (K5)
     mark(1);
     fapp += k;
-    // line 8: Delta = Q^T W (column-major k x k; lower triangle used).  A
-    // cublasDsyrkx of the lower triangle halves the flops but measured slower
-    // at k = 96 (MBB) and shifted RRS rank decisions: the GEMM stays.
-    CB(cublasDgemm(cb, CUBLAS_OP_N, CUBLAS_OP_T, k, k, m, &one, Qb.p, k, W.p, k, &zero, Delta.p, k));
+    // line 8: Delta = Q^T W (column-major k x k): the lower tiles of the
+    // m-deep product (split-K with a fixed segment sum), mirrored.
+    gemm_splitk(st, false, true, k, k, m, 1.0, Qb.p, k, W.p, k, 0.0, Delta.p, k, dla_ws(gemm_splitk_ws(k, k, m)),
+                kGemmLowerTiles);
     k_mirror_lower<<<grid_for((long long)k * k), kThreads, 0, st>>>(Delta.p, k);
     mark(2);
     // line 9
@@ -421,18 +420,15 @@ int Ctx::solve_rrs(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_tra
               std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - ta).count(),
               chunks.size());
     }
-    launch_identity(Linv.p, rank);
-    CB(cublasDtrsm(cb, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, rank, rank,
-                   &one, Delta.p, k, Linv.p, rank));
+    tri_inv_lower(st, Delta.p, k, rank, Linv.p, rank, dla_ws(tri_inv_workspace(rank)));
     // W_sel lands in Q's (still free) arena slot, W_new = W_sel L~^{-T} in W's;
     // then Q_sel lands in W (no longer needed) and Q_new = Q_sel L~^{-T}.
+    // (L~^{-T} is upper triangular: column c of the product ends at index c.)
     const dim3 tgrid((m + 31) / 32, (rank + 31) / 32);
     k_gather_cols_t<<<tgrid, dim3(32, 8), 0, st>>>(W.p, k, perm.p, rank, m, Qn, m);
-    CB(cublasDtrmm(cb, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, m, rank, &one,
-                   Linv.p, rank, Qn, m, Wn, m));
+    gemm(st, false, true, m, rank, rank, 1.0, Qn, m, Linv.p, rank, 0.0, Wn, m, kGemmKEndByCol);
     k_gather_cols_t<<<tgrid, dim3(32, 8), 0, st>>>(Qb.p, k, perm.p, rank, m, W.p, m);
-    CB(cublasDtrmm(cb, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, m, rank, &one,
-                   Linv.p, rank, W.p, m, Qn, m));
+    gemm(st, false, true, m, rank, rank, 1.0, W.p, m, Linv.p, rank, 0.0, Qn, m, kGemmKEndByCol);
     K += rank;
     if (trace_on) {
       const auto tb = std::chrono::steady_clock::now();
@@ -442,9 +438,9 @@ int Ctx::solve_rrs(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_tra
     }
     mark(4);
     // lines 13-15
-    CB(cublasDgemv(cb, CUBLAS_OP_T, m, rank, &one, Wn, m, r.p, 1, &zero, gamma.p, 1));
-    CB(cublasDgemv(cb, CUBLAS_OP_N, m, rank, &one, Wn, m, gamma.p, 1, &one, lam.p, 1));
-    CB(cublasDgemv(cb, CUBLAS_OP_N, m, rank, &one, Qn, m, gamma.p, 1, &zero, tmp.p, 1));
+    gemv_cm_t_tall(st, m, rank, Wn, m, r.p, gamma.p, dla_ws((size_t)kGvSeg * rank));
+    gemv_cm(st, false, m, rank, 1.0, Wn, m, gamma.p, 1.0, lam.p);
+    gemv_cm(st, false, m, rank, 1.0, Qn, m, gamma.p, 0.0, tmp.p);
     project(tmp.p, 1, m);
     k_axpy<<<grid_for(m), kThreads, 0, st>>>(m, -1.0, tmp.p, r.p);
     mark(5);
@@ -470,11 +466,10 @@ int Ctx::solve_rrs(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_tra
     // `passes` passes.  W is row-major m x Ns (= column-major Ns x m).
     for (int p = 0; p < passes; ++p) {
       for (const Chunk& ch : chunks)  // Psi_c = Q_c^T W   (used x Ns, ld cap)
-        CB(cublasDgemm(cb, CUBLAS_OP_T, CUBLAS_OP_T, ch.used, Ns, m, &one, ch.q->p, m, W.p, Ns, &zero,
-                       ch.psi->p, ch.cap));
+        gemm_splitk(st, true, true, ch.used, Ns, m, 1.0, ch.q->p, m, W.p, Ns, 0.0, ch.psi->p, ch.cap,
+                    dla_ws(gemm_splitk_ws(ch.used, Ns, m)));
       for (const Chunk& ch : chunks)  // W -= W_c Psi_c   ==   W^T -= Psi_c^T W_c^T
-        CB(cublasDgemm(cb, CUBLAS_OP_T, CUBLAS_OP_T, Ns, m, ch.used, &mone, ch.psi->p, ch.cap, ch.w->p, m, &one,
-                       W.p, Ns));
+        gemm(st, true, true, Ns, m, ch.used, -1.0, ch.psi->p, ch.cap, ch.w->p, m, 1.0, W.p, Ns);
     }
     mark(8);
     CK(cudaEventSynchronize(pev[8]));
@@ -572,15 +567,32 @@ int Ctx::solve_rrs_implicit(const fetigpu_solve_opts& o, double* lambda_host, fe
   DBuf<Scal> sc;
   DBuf<double> pivx;
   lam.alloc(m); r.alloc(m); z.alloc(m); q.alloc(m);
-  W.alloc((size_t)m * k); Qb.alloc((size_t)m * k); Dd.alloc((size_t)m * k);
+  W.alloc((size_t)m * k); Qb.alloc((size_t)m * k);
   Delta.alloc((size_t)k * k); Linv.alloc((size_t)k * k);
   tvec.alloc(k); tp.alloc(k); gam.alloc(k); yh.alloc(k);
   perm.alloc(k); rank_d.alloc(1); ctl.alloc(4); pivx.alloc(2 * (size_t)k + 64);
   sc.alloc(1);
   sc.zero(st);
+  // Everything the first nl_pre iterations need is allocated here, before
+  // the timed loop: a multi-GB cudaMalloc / cudaFree inside an iteration
+  // synchronises the device and occasionally stalls for 100+ ms in the
+  // driver.  nl_pre = min(max_it, 32), reduced until the
+  // coordinate scratch and the M_j arena fit in 40% of free memory; beyond
+  // it the buffers grow by doubling.
+  const char* nbz = getenv("FETIGPU_NO_BZ");   // A/B switch: dense K5 / scatter+AXPY paths
+  const bool use_bz = !(nbz && nbz[0] == '1') && bz_prepare();
+  int nl_pre = std::max(1, std::min(o.max_it, 32));
+  {
+    const size_t freeb = dev_free_bytes(&rrs_cache);
+    auto need = [&](int nlp) {
+      const double kk = (double)k * k;
+      return 8.0 * (5.0 * (nlp + 1) * kk + kk * nlp * (nlp + 1) / 2.0 + (double)nz * (nlp + 1));
+    };
+    while (nl_pre > 1 && need(nl_pre) > 0.4 * (double)freeb) --nl_pre;
+  }
   // packed Z blocks (column-major nz x zcap, grown by doubling) and the
   // per-iteration coordinate scratch, grown to (i+1) k x k as i increases
-  int zcap = std::max(1, std::min(o.max_it, 8));
+  int zcap = nl_pre + 1;
   ZV.alloc((size_t)nz * zcap);
   auto zv_block = [&](int l) {
     if (l >= zcap) {
@@ -593,11 +605,8 @@ int Ctx::solve_rrs_implicit(const fetigpu_solve_opts& o, double* lambda_host, fe
       zcap = nc;
     }
   };
-  grow(CW, (size_t)k * k);
-  // M_j ((j+1)k x rank_j, column-major) carved from arena chunks whose sizes
-  // double, and coordinate scratch grown geometrically: no device allocation
-  // (and none of the driver's occasional 100 ms cudaMalloc stalls) in most
-  // iterations
+  // M_j ((j+1)k x rank_j, column-major) carved from arena chunks: the
+  // first holds nl_pre iterations, later ones double
   std::vector<std::unique_ptr<DBuf<double>>> Mchunks;
   size_t mc_used = 0;
   std::vector<double*> Mb;
@@ -617,10 +626,17 @@ int Ctx::solve_rrs_implicit(const fetigpu_solve_opts& o, double* lambda_host, fe
     if (b.n < n) b.alloc(std::max(n, 2 * b.n));
     return b.p;
   };
+  {
+    const size_t kk = (size_t)k * k, kzmax = (size_t)(nl_pre + 1) * k;
+    grow2(CW, kzmax * k); grow2(XT, kzmax * k); grow2(NT, kzmax * k); grow2(NTot, kzmax * k); grow2(CT, kzmax * k);
+    Mchunks.emplace_back(new DBuf<double>);
+    Mchunks.back()->alloc(kk * (size_t)nl_pre * (nl_pre + 1) / 2 + 32 * (size_t)nl_pre);
+    dla_ws(std::max({gemm_splitk_ws(k, k, (int)kzmax), tri_inv_workspace(k), (size_t)kGvSeg * k}));
+    ensure_block_buffers(k);
+  }
   Scal* hs = nullptr;
   CK(cudaMallocHost(&hs, sizeof(Scal)));
   std::unique_ptr<Scal, decltype(&cudaFreeHost)> hs_guard(hs, cudaFreeHost);
-  const double one = 1.0, mone = -1.0, zero = 0.0;
   raise_smem_limit(k_rrs_zgather, (size_t)max_pcn * (kZL * 8 + 4));
   raise_smem_limit(k_rrs_zscatter, kZScatterSmem);
   pt.mark("rrs-implicit setup", st);
@@ -666,7 +682,8 @@ int Ctx::solve_rrs_implicit(const fetigpu_solve_opts& o, double* lambda_host, fe
     const int i = it;              // stored blocks 0..i-1; W has coordinates CW over Z_0..Z_i
     const int kzi = (i + 1) * k;   // rows of CW
     mark(0);
-    apply_F_block(W.p, k, Qb.p, k, k);  // line 7
+    // line 7 (at i = 0, W = Z_0 is a fresh preconditioner block: K5z)
+    if (!(i == 0 && use_bz && apply_F_block_z(W.p, Qb.p, k))) apply_F_block(W.p, k, Qb.p, k, k);
     fapp += k;
     mark(1);
     // line 8 on coordinates: Delta = Q^T W = (Zhat^T Q)^T C_W over Z_0..Z_i --
@@ -676,7 +693,8 @@ int Ctx::solve_rrs_implicit(const fetigpu_solve_opts& o, double* lambda_host, fe
     k_rrs_zgather<<<dim3(ggrid.x, Ns, (i + 1 + kZL - 1) / kZL), 256, (size_t)max_pcn * (kZL * 8 + 4), st>>>(
         d_pc.p, d_pcrows.p, ZV.p, nz, i + 1, Qb.p, k, XT.p);
     LAUNCH_CHECK();
-    CB(cublasDgemm(cb, CUBLAS_OP_N, CUBLAS_OP_N, k, k, kzi, &one, XT.p, k, CW.p, kzi, &zero, Delta.p, k));
+    gemm_splitk(st, false, false, k, k, kzi, 1.0, XT.p, k, CW.p, kzi, 0.0, Delta.p, k,
+                dla_ws(gemm_splitk_ws(k, k, kzi)), kGemmLowerTiles);
     k_mirror_lower<<<grid_for((long long)k * k), kThreads, 0, st>>>(Delta.p, k);
     mark(2);
     launch_pivchol(Delta.p, k, o.pivot_tol, perm.p, rank_d.p, d_status.p, ctl.p, pivx.p, st, Linv.p);  // line 9
@@ -693,27 +711,25 @@ int Ctx::solve_rrs_implicit(const fetigpu_solve_opts& o, double* lambda_host, fe
     }
     if (rank == 0) { status = FETIGPU_BREAKDOWN; break; }
     // lines 10-11 on the coordinates: M_i = CW[:, perm] L~^{-T}
-    launch_identity(Linv.p, rank);
-    CB(cublasDtrsm(cb, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, rank, rank,
-                   &one, Delta.p, k, Linv.p, rank));
+    tri_inv_lower(st, Delta.p, k, rank, Linv.p, rank, dla_ws(tri_inv_workspace(rank)));
     Mb.push_back(m_alloc((size_t)kzi * rank));
     Mrank.push_back(rank);
     grow2(CT, (size_t)kzi * k);
     k_gather_cols_cm<<<grid_for((long long)kzi * rank), kThreads, 0, st>>>(CW.p, kzi, perm.p, kzi, rank, CT.p,
                                                                            kzi);
-    CB(cublasDtrmm(cb, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, kzi, rank,
-                   &one, Linv.p, rank, CT.p, kzi, Mb.back(), kzi));
+    gemm(st, false, true, kzi, rank, rank, 1.0, CT.p, kzi, Linv.p, rank, 0.0, Mb.back(), kzi, kGemmKEndByCol);
     K += rank;
     mark(4);
     // lines 13-15: gamma = L~^{-1} (W^T r)[perm], y = L~^{-T} gamma,
     // lambda += W yh, r -= (F W) yh with yh = y scattered to perm
-    CB(cublasDgemv(cb, CUBLAS_OP_N, k, m, &one, W.p, k, r.p, 1, &zero, tvec.p, 1));
+    gemv_rm_t(st, W.p, k, m, k, r.p, tvec.p, dla_ws((size_t)kGvSeg * k));
     k_perm_gather<<<1, 1024, 0, st>>>(tvec.p, perm.p, rank, tp.p);
-    CB(cublasDgemv(cb, CUBLAS_OP_N, rank, rank, &one, Linv.p, rank, tp.p, 1, &zero, gam.p, 1));
-    CB(cublasDgemv(cb, CUBLAS_OP_T, rank, rank, &one, Linv.p, rank, gam.p, 1, &zero, tp.p, 1));
+    gemv_cm(st, false, rank, rank, 1.0, Linv.p, rank, tp.p, 0.0, gam.p);
+    gemv_cm(st, true, rank, rank, 1.0, Linv.p, rank, gam.p, 0.0, tp.p);
     k_perm_scatter<<<1, 1024, 0, st>>>(tp.p, perm.p, rank, k, yh.p);
-    CB(cublasDgemv(cb, CUBLAS_OP_T, k, m, &one, W.p, k, yh.p, 1, &one, lam.p, 1));
-    CB(cublasDgemv(cb, CUBLAS_OP_T, k, m, &mone, Qb.p, k, yh.p, 1, &one, r.p, 1));
+    raise_smem_limit(k_rrs_update, (size_t)k * 8);
+    k_rrs_update<<<148 * 8, 256, (size_t)k * 8, st>>>(W.p, Qb.p, k, m, k, yh.p, lam.p, r.p);
+    LAUNCH_CHECK();
     mark(5);
     // line 16: Z_{i+1}
     apply_precond(r.p, z.p, W.p, true);
@@ -744,7 +760,8 @@ int Ctx::solve_rrs_implicit(const fetigpu_solve_opts& o, double* lambda_host, fe
       grow2(XT, (size_t)kz * k); grow2(NT, (size_t)kz * k); grow2(NTot, (size_t)kz * k);
       grow2(CT, (size_t)kz * k); grow2(CW, (size_t)(kz + k) * k);
       for (int p = 0; p < passes; ++p) {
-        apply_F_block(W.p, k, Qb.p, k, k);  // Y = F V
+        // Y = F V; the first pass sees V = Z_it itself (K5z)
+        if (!(p == 0 && use_bz && apply_F_block_z(W.p, Qb.p, k))) apply_F_block(W.p, k, Qb.p, k, k);
         fapp += k;
         k_rrs_zgather<<<dim3(ggrid.x, Ns, (nl + kZL - 1) / kZL), 256, (size_t)max_pcn * (kZL * 8 + 4), st>>>(
             d_pc.p, d_pcrows.p, ZV.p, nz, nl, Qb.p, k, XT.p);
@@ -756,28 +773,34 @@ int Ctx::solve_rrs_implicit(const fetigpu_solve_opts& o, double* lambda_host, fe
         for (size_t j = 0; j < Mb.size(); ++j) {
           poff[j] = off;
           const int kj = (int)(j + 1) * k;
-          CB(cublasDgemm(cb, CUBLAS_OP_N, CUBLAS_OP_N, k, Mrank[j], kj, &one, XT.p, k, Mb[j], kj, &zero,
-                         CT.p + (size_t)off * k, k));
+          gemm_splitk(st, false, false, k, Mrank[j], kj, 1.0, XT.p, k, Mb[j], kj, 0.0, CT.p + (size_t)off * k, k,
+                      dla_ws(gemm_splitk_ws(k, Mrank[j], kj)));
           off += Mrank[j];
         }
         for (int j = (int)Mb.size() - 1; j >= 0; --j) {
           const int kj = (j + 1) * k;
           const double beta = j == (int)Mb.size() - 1 ? 0.0 : 1.0;
-          CB(cublasDgemm(cb, CUBLAS_OP_N, CUBLAS_OP_T, k, kj, Mrank[j], &one, CT.p + (size_t)poff[j] * k, k,
-                         Mb[j], kj, &beta, NT.p, k));
+          gemm(st, false, true, k, kj, Mrank[j], 1.0, CT.p + (size_t)poff[j] * k, k, Mb[j], kj, beta, NT.p, k);
         }
-        CK(cudaMemsetAsync(Dd.p, 0, (size_t)m * k * 8, st));
-        k_rrs_zscatter<<<sgrid, 128, kZScatterSmem, st>>>(d_pc.p, d_pcrows.p, ZV.p, nz, nl, NT.p, k, Dd.p);
-        LAUNCH_CHECK();
-        CB(cublasDaxpy(cb, (int)std::min<size_t>((size_t)m * k, (size_t)INT_MAX), &mone, Dd.p, 1, W.p, 1));
-        if ((size_t)m * k > (size_t)INT_MAX)
-          CB(cublasDaxpy(cb, (int)((size_t)m * k - INT_MAX), &mone, Dd.p + INT_MAX, 1, W.p + INT_MAX, 1));
+        if (use_bz && nl <= kZsMax) {   // V -= Zhat N, once per dual row (interface-edge groups)
+          const size_t zs = (size_t)kBzRows * nl * 2 * 8;
+          raise_smem_limit(k_rrs_zsub_edges, zs);
+          k_rrs_zsub_edges<<<dim3((k + kBzCols - 1) / kBzCols, bz_nedges), kBzCols, zs, st>>>(
+              bz_edges.p, bz_erow.p, bz_ez1.p, bz_ez2.p, ZV.p, nz, nl, NT.p, k, W.p);
+          LAUNCH_CHECK();
+        } else {
+          if (Dd.n < (size_t)m * k) Dd.alloc((size_t)m * k);
+          CK(cudaMemsetAsync(Dd.p, 0, (size_t)m * k * 8, st));
+          k_rrs_zscatter<<<sgrid, 128, kZScatterSmem, st>>>(d_pc.p, d_pcrows.p, ZV.p, nz, nl, NT.p, k, Dd.p);
+          LAUNCH_CHECK();
+          axpy(st, (size_t)m * k, -1.0, Dd.p, W.p);
+        }
         if (p == 0) CK(cudaMemcpyAsync(NTot.p, NT.p, (size_t)kz * k * 8, cudaMemcpyDeviceToDevice, st));
-        else CB(cublasDaxpy(cb, kz * k, &one, NT.p, 1, NTot.p, 1));
+        else axpy(st, (size_t)kz * k, 1.0, NT.p, NTot.p);
       }
       // coordinates of the new W over Z_0..Z_it: [-NTot^T ; I]
       const int kzn = (it + 1) * k;
-      CB(cublasDgeam(cb, CUBLAS_OP_T, CUBLAS_OP_N, kz, k, &mone, NTot.p, k, &zero, CW.p, kzn, CW.p, kzn));
+      transpose_scale(st, kz, k, -1.0, NTot.p, k, CW.p, kzn);
       k_identity_ld<<<grid_for((long long)k * k), kThreads, 0, st>>>(CW.p + kz, k, kzn);
       LAUNCH_CHECK();
       mark(8);

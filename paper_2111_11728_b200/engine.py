@@ -23,7 +23,7 @@ import numpy as np
 from .problems import Problem
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libfetigpu.so")
+LIB_PATH = os.environ.get("FETIGPU_LIB") or os.path.join(_HERE, "lib", "libfetigpu.so")
 _lib = None
 
 D = C.POINTER(C.c_double)
@@ -80,7 +80,8 @@ EXPORTED = ["fetigpu_set_device", "fetigpu_create", "fetigpu_build", "fetigpu_de
             "fetigpu_synchronize", "fetigpu_time_apply", "fetigpu_apply_F_block_device",
             "fetigpu_time_apply_block", "fetigpu_fp64_peak", "fetigpu_selftest_dmma",
             "fetigpu_pivoted_cholesky", "fetigpu_pivoted_compress", "fetigpu_time_ops",
-            "fetigpu_device_memory", "fetigpu_set_rrs_store"]
+            "fetigpu_device_memory", "fetigpu_set_rrs_store", "fetigpu_dla_gemm", "fetigpu_dla_tri_inv",
+            "fetigpu_dla_time_gemm", "fetigpu_apply_F_zblock"]
 
 
 class FgProblem(C.Structure):
@@ -191,6 +192,38 @@ def compress(perm, lower, rank: int, w: np.ndarray) -> np.ndarray:
     check(lib().fetigpu_pivoted_compress(_p(pv), _p(lowf), n, rank, W.ctypes.data_as(D), w.shape[0],
                                          out.ctypes.data_as(D)))
     return np.ascontiguousarray(out[:, :rank])
+
+
+def dla_gemm(A: np.ndarray, B: np.ndarray, ta: bool = False, tb: bool = False, alpha: float = 1.0,
+             beta: float = 0.0, C0: np.ndarray = None, flags: int = 0) -> np.ndarray:
+    """alpha op(A) op(B) + beta C0 through the engine's DMMA GEMM (dla.cuh),
+    column-major like BLAS dgemm."""
+    A = np.asfortranarray(A, dtype=np.float64)
+    B = np.asfortranarray(B, dtype=np.float64)
+    M = A.shape[1] if ta else A.shape[0]
+    K = A.shape[0] if ta else A.shape[1]
+    N = B.shape[0] if tb else B.shape[1]
+    Cm = np.asfortranarray(np.zeros((M, N)) if C0 is None else C0, dtype=np.float64).copy(order="F")
+    check(lib().fetigpu_dla_gemm(int(ta), int(tb), M, N, K, C.c_double(alpha), A.ctypes.data_as(D),
+                                 C.c_longlong(max(1, A.shape[0])), B.ctypes.data_as(D),
+                                 C.c_longlong(max(1, B.shape[0])), C.c_double(beta), Cm.ctypes.data_as(D),
+                                 C.c_longlong(max(1, M)), flags))
+    return Cm
+
+
+def dla_tri_inv(L: np.ndarray) -> np.ndarray:
+    """L^{-1} of the lower triangle of L through the engine's kernels."""
+    Lf = np.asfortranarray(L, dtype=np.float64)
+    n = Lf.shape[0]
+    X = np.zeros((n, n), order="F")
+    check(lib().fetigpu_dla_tri_inv(Lf.ctypes.data_as(D), n, C.c_longlong(n), X.ctypes.data_as(D)))
+    return X
+
+
+def dla_time_gemm(M: int, N: int, K: int, ta: bool = False, tb: bool = False, reps: int = 5) -> float:
+    ms = C.c_double()
+    check(lib().fetigpu_dla_time_gemm(int(ta), int(tb), M, N, K, reps, C.byref(ms)))
+    return ms.value
 
 
 def dmma_selftest(A: np.ndarray, B: np.ndarray) -> np.ndarray:
@@ -342,6 +375,14 @@ class FetiSystem:
         finally:
             L.fetigpu_device_free(self.h, dW)
             L.fetigpu_device_free(self.h, dQ)
+        return Q
+
+    def apply_F_zblock(self, Z: np.ndarray) -> np.ndarray:
+        """Q = F Z through the sparse-aware K5z path (Z: m x N_s per-subdomain
+        preconditioner columns, as apply_precond(columns=True) returns)."""
+        Z = np.ascontiguousarray(Z, dtype=np.float64)
+        Q = np.empty_like(Z)
+        check(lib().fetigpu_apply_F_zblock(self.h, Z.ctypes.data_as(D), Q.ctypes.data_as(D)))
         return Q
 
     def time_ops(self, reps: int = 200) -> dict:
