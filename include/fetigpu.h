@@ -208,6 +208,12 @@ int fetigpu_local_operator(fetigpu_ctx* ctx, int s, int* ns, int* dofs, double* 
 /* Block F-apply (K5, FP64 tensor cores): Q = F W for k columns stored
  * row-major (W(i,c) = W[i*ldw + c]), device pointers, ctx stream. */
 int fetigpu_apply_F_block_device(fetigpu_ctx* ctx, const double* W, int ldw, double* Q, int ldq, int k);
+/* Invariant check of the device solver (test hook): when
+ * on, every FO / RRS solve afterwards reconstructs its stored F-normalised
+ * search directions W and reports max |W^T F W - I| over all of them (FO
+ * conjugacy and Alg. 1 orthonormality) and their number. */
+int fetigpu_set_check(fetigpu_ctx* ctx, int on);
+int fetigpu_check_result(const fetigpu_ctx* ctx, double* err, int* n);
 /* Test hook: Q = F Z for a fresh per-subdomain preconditioner block Z
  * (row-major m x N_s, column s supported on subdomain s's dual rows) through
  * the sparse-aware K5z path the RRS solver uses on Alg. 1 lines 2/16 blocks;

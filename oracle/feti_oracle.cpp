@@ -1154,6 +1154,25 @@ struct TraceRec {
 // PAPER.md:302-351).  FO keeps the F-normalized directions
 // (w/sqrt(w^T F w), F w/sqrt(.)) and re-orthogonalizes with the same number of
 // passes as RRS, so RRS with one subdomain reproduces FO.
+// invariant check: max |W^T F W - I| over the stored
+// F-normalised directions of the last FO / RRS solve (fo_set_check)
+static bool g_check = false;
+static double g_check_err = -1.0;
+static int g_check_n = 0;
+static void check_orth(const std::vector<const double*>& W, const std::vector<const double*>& Q, int m) {
+  const int K = (int)W.size();
+  double e = 0.0;
+#pragma omp parallel for schedule(dynamic) reduction(max : e)
+  for (int a = 0; a < K; ++a)
+    for (int b = 0; b < K; ++b) {
+      long double acc = 0.0L;   // accurate inner products: the check adds no cancellation of its own
+      for (int i = 0; i < m; ++i) acc += (long double)W[a][i] * (long double)Q[b][i];
+      e = std::max(e, std::fabs((double)acc - (a == b ? 1.0 : 0.0)));
+    }
+  g_check_err = e;
+  g_check_n = K;
+}
+
 int Oracle::solve(const fo_opts& o, double* lambda, fo_trace* tr) {
   TraceRec rec{tr};
   std::vector<double> d(m), lam0(m), r(m), tmp(m), z(m);
@@ -1212,6 +1231,11 @@ int Oracle::solve(const fo_opts& o, double* lambda, fo_trace* tr) {
         for (int i = 0; i < m; ++i) w[i] = z[i] + beta * w[i];
       }
       rz = rz_new;
+    }
+    if (g_check && o.directions == 1) {
+      std::vector<const double*> wp, qp;
+      for (size_t j = 0; j < Ws.size(); ++j) { wp.push_back(Ws[j].data()); qp.push_back(Qs[j].data()); }
+      check_orth(wp, qp, m);
     }
   } else {
     // Alg. 1
@@ -1291,6 +1315,12 @@ int Oracle::solve(const fo_opts& o, double* lambda, fo_trace* tr) {
       }
     }
     (void)kept_last;
+    if (g_check) {
+      std::vector<const double*> wp, qp;
+      for (size_t j = 0; j < Ws.size(); ++j)
+        for (int c = 0; c < Ws[j].c; ++c) { wp.push_back(Ws[j].col(c)); qp.push_back(Qs[j].col(c)); }
+      check_orth(wp, qp, m);
+    }
   }
   if (tr) {
     tr->status = status;
@@ -1398,6 +1428,15 @@ extern "C" {
 
 const char* fo_last_error(void) { return g_err.c_str(); }
 void fo_set_refine(int on) { g_refine = on != 0; }
+void fo_set_check(int on) {
+  g_check = on != 0;
+  g_check_err = -1.0;
+  g_check_n = 0;
+}
+void fo_check_result(double* err, int* n) {
+  *err = g_check_err;
+  *n = g_check_n;
+}
 // host threads for the OpenMP loops (the CPU baseline uses every core even
 // under torchrun, which sets OMP_NUM_THREADS=1); returns the count in force
 int fo_set_threads(int n) {

@@ -83,6 +83,10 @@ const char* fo_last_error(void);
  * afterwards for the Phi / Kbar_cc build, and all later applications) */
 void fo_set_refine(int on);
 int fo_set_threads(int n);
+/* invariant check of later FO / RRS solves: max |W^T F W - I| over the
+ * stored F-normalised directions and their number */
+void fo_set_check(int on);
+void fo_check_result(double* err, int* n);
 void fo_destroy(void* h);
 /* info[0]=m, [1]=N_s, [2]=local DOFs, [3]=N_c (FETI-DP), [4]=kept coarse rows,
  * [5]=interface rows, [6]=max n_s (touched DOFs per subdomain) */

@@ -217,6 +217,16 @@ class Oracle:
         return u
 
 
+def set_check(on: bool = True):
+    lib().fo_set_check(int(on))
+
+
+def check_result():
+    e, n = C.c_double(), C.c_int()
+    lib().fo_check_result(C.byref(e), C.byref(n))
+    return e.value, n.value
+
+
 # ---- kernel-level helpers (SPEC examples) ---------------------------------
 def simp_modulus(rho, E0=1.0, Emin=1e-9, p=3.0) -> float:
     out = C.c_double()

@@ -202,6 +202,8 @@ struct Ctx {
                            const int* ncs, const double* kccs, int Nc, double* K);
   void launch_identity(double* X, int n);
   void launch_symmetrize(double* A, int n);
+  void mirror_slots(const std::vector<long long>& moff, const std::vector<int>& ns, const std::vector<int>& ld,
+                    double* mats);
 
   void build();
 
@@ -335,6 +337,47 @@ struct Ctx {
   int solve_rrs_implicit(const fetigpu_solve_opts& o, double* lam, fetigpu_trace* tr);
   bool use_implicit_store(const fetigpu_solve_opts& o);
   int rrs_store = 0;   // FETIGPU_RRS_STORE_AUTO / _EXPLICIT / _IMPLICIT
+  // invariant check of the stored search directions (fetigpu_set_check):
+  // after each FO / RRS solve, chk_err = max |W^T F W - I| over all stored
+  // F-normalised directions, chk_n = their number
+  bool chk_on = false;
+  double chk_err = -1.0;
+  int chk_n = 0;
+  // blocks (W_b, Q_b = F W_b), column-major m x r_b (ld m): max |W^T Q - I|
+  // row_major: blocks are row-major m x r_b (ld r_b) instead
+  void check_orth(const std::vector<const double*>& Ws, const std::vector<const double*>& Qs,
+                  const std::vector<int>& rs, bool row_major = false) {
+    const int m = su.m;
+    int K = 0;
+    for (int r : rs) K += r;
+    std::vector<double> G((size_t)K * K);
+    DBuf<double> g;
+    int ra0 = 0;
+    for (size_t a = 0; a < Ws.size(); ++a) {
+      int rb0 = 0;
+      for (size_t b = 0; b < Qs.size(); ++b) {
+        g.alloc((size_t)rs[a] * rs[b]);
+        // each inner product in double-double (test hook: the check must not
+        // add its own cancellation error to the measured loss of conjugacy)
+        const long long sw = row_major ? 1 : m, ew = row_major ? rs[a] : 1;
+        const long long sq = row_major ? 1 : m, eq = row_major ? rs[b] : 1;
+        k_dot_dd<<<dim3(rs[a], rs[b]), 256, 0, st>>>(Ws[a], sw, ew, Qs[b], sq, eq, m, g.p, rs[a]);
+        LAUNCH_CHECK();
+        std::vector<double> h((size_t)rs[a] * rs[b]);
+        CK(cudaMemcpyAsync(h.data(), g.p, h.size() * 8, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        for (int j = 0; j < rs[b]; ++j)
+          for (int i = 0; i < rs[a]; ++i) G[(size_t)(rb0 + j) * K + ra0 + i] = h[(size_t)j * rs[a] + i];
+        rb0 += rs[b];
+      }
+      ra0 += rs[a];
+    }
+    double e = 0.0;
+    for (int j = 0; j < K; ++j)
+      for (int i = 0; i < K; ++i) e = std::max(e, std::fabs(G[(size_t)j * K + i] - (i == j ? 1.0 : 0.0)));
+    chk_err = e;
+    chk_n = K;
+  }
 };
 
 }  // namespace fg

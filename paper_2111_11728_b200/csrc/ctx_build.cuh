@@ -48,6 +48,16 @@ void Ctx::launch_identity(double* X, int n) {
   k_identity<<<grid_for((long long)n * n), kThreads, 0, st>>>(X, n);
   LAUNCH_CHECK();
 }
+void Ctx::mirror_slots(const std::vector<long long>& moff, const std::vector<int>& ns, const std::vector<int>& ld,
+                       double* mats) {
+  if (moff.empty()) return;
+  DBuf<long long> dm;
+  DBuf<int> dn, dl;
+  dm.upload(moff, st); dn.upload(ns, st); dl.upload(ld, st);
+  k_mirror_slots<<<dim3(64, (unsigned)moff.size()), kThreads, 0, st>>>(dm.p, dn.p, dl.p, mats);
+  LAUNCH_CHECK();
+  CK(cudaStreamSynchronize(st));
+}
 void Ctx::launch_symmetrize(double* A, int n) {
   k_symmetrize<<<grid_for((long long)n * n), kThreads, 0, st>>>(A, n);
   LAUNCH_CHECK();
@@ -446,6 +456,7 @@ void Ctx::build_ops(const SlotOut& so, std::future<HostMaps>& maps) {
   ptimer.mark("op slot allocation", st);
   run_slots(su.op_slots, so, d_opmat.p, -1.0, dp, dp ? d_abc.p : nullptr, dp ? d_kccs.p : nullptr,
             d_opfac.p, dp ? FETIGPU_E_SINGULAR_REMAINDER : FETIGPU_E_NOT_POSITIVE_DEFINITE);
+  mirror_slots(op_moff, op_ns, op_ld, d_opmat.p);
   ptimer.mark("op slots (device)", st);
   HostMaps h = maps.get();  // normally finished long before (overlapped with the ND tree)
   ptimer.mark("host maps (join)", st);
@@ -477,6 +488,9 @@ void Ctx::build_ops(const SlotOut& so, std::future<HostMaps>& maps) {
     SlotOut po;
     po.mat_off = pc_moff; po.mat_ld = pc_ld;
     run_slots(su.pc_slots, po, d_pcmat.p, 1.0, false, nullptr, nullptr, nullptr, FETIGPU_E_SINGULAR_INTERIOR);
+    std::vector<int> pc_ns(npc);
+    for (int i = 0; i < npc; ++i) pc_ns[i] = (int)(su.pc_slots[i].src.size() - su.pc_slots[i].ne);
+    mirror_slots(pc_moff, pc_ns, pc_ld, d_pcmat.p);
   } else {
     // K_bb per design from element contributions
     std::vector<int> pne(su.nb / 2 * 4, -1);

@@ -433,6 +433,38 @@ static void tri_inv_lower(cudaStream_t st, const double* L, long long ldl, int n
   tri_inv_rec(st, L, ldl, n, X, ldx, T);
 }
 
+// G(a, b) = sum_i W(i, a) Q(i, b) in double-double (TwoSum / FMA TwoProd)
+// with W(i, a) = W[a * sw + i * ew]: the accurate inner products of the
+// invariant-check test hook.  One CTA per (a, b).
+__device__ __forceinline__ void dd_add(double& hi, double& lo, double a) {
+  const double s = hi + a, bb = s - hi;
+  lo += (hi - (s - bb)) + (a - bb);
+  hi = s;
+}
+__global__ void k_dot_dd(const double* __restrict__ W, long long sw, long long ew, const double* __restrict__ Q,
+                         long long sq, long long eq, int m, double* __restrict__ G, int ldg) {
+  __shared__ double sh[256], sl[256];
+  const int a = blockIdx.x, b = blockIdx.y;
+  double hi = 0.0, lo = 0.0;
+  for (int i = threadIdx.x; i < m; i += blockDim.x) {
+    const double x = W[(size_t)a * sw + (size_t)i * ew], y = Q[(size_t)b * sq + (size_t)i * eq];
+    const double p = x * y, pe = fma(x, y, -p);
+    dd_add(hi, lo, p);
+    lo += pe;
+  }
+  sh[threadIdx.x] = hi;
+  sl[threadIdx.x] = lo;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double h = 0.0, l = 0.0;
+    for (int t = 0; t < (int)blockDim.x; ++t) {
+      dd_add(h, l, sh[t]);
+      l += sl[t];
+    }
+    G[(size_t)b * ldg + a] = h + l;
+  }
+}
+
 // ----------------------------------------------------------- GEMVs --
 // Row-major m x k blocks W(i, c) = W[i * ldw + c] (the RRS direction blocks).
 // t = W^T r (length k), deterministic two-stage reduction: stage 1 sums a

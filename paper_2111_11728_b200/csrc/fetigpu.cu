@@ -271,6 +271,21 @@ int fetigpu_apply_F_block_device(fetigpu_ctx* ctx, const double* W, int ldw, dou
   });
 }
 
+// invariant check of the device solver's stored directions (test hook)
+int fetigpu_set_check(fetigpu_ctx* ctx, int on) {
+  return guarded([&] {
+    ctx->c.chk_on = on != 0;
+    ctx->c.chk_err = -1.0;
+    ctx->c.chk_n = 0;
+  });
+}
+int fetigpu_check_result(const fetigpu_ctx* ctx, double* err, int* n) {
+  return guarded([&] {
+    *err = ctx->c.chk_err;
+    *n = ctx->c.chk_n;
+  });
+}
+
 // test hook: Q = F Z through K5z for a per-subdomain preconditioner block
 // (row-major m x N_s host buffers); FETIGPU_E_CONFIG when not applicable
 int fetigpu_apply_F_zblock(fetigpu_ctx* ctx, const double* Z, double* Q) {

@@ -259,6 +259,25 @@ __global__ void __launch_bounds__(256) k_sym_gemv_scatter(
 }
 
 // pack the lower block-triangle of a row-major symmetric ns x ld matrix
+// Explicit symmetric local operators (F_s, S~_s; row-major ns x ld per slot):
+// the upper triangle is replaced by the lower one.  The elimination computes
+// both triangles independently, and at SIMP contrast 1e9 they differ by
+// rounding x cond(K_rr) (up to ~1e-8 relative): an F applied from both
+// triangles is then measurably nonsymmetric, which costs FO / RRS their
+// F-conjugacy.  The symmetric-packed kernels already read
+// the lower block-triangle only.
+__global__ void k_mirror_slots(const long long* __restrict__ moff, const int* __restrict__ ns_,
+                               const int* __restrict__ ld_, double* __restrict__ mats) {
+  const int sl = blockIdx.y;
+  const int ns = ns_[sl], ld = ld_[sl];
+  double* M = mats + moff[sl];
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < (long long)ns * ns;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int r = (int)(idx / ns), c = (int)(idx - (long long)r * ns);
+    if (c > r) M[(size_t)r * ld + c] = M[(size_t)c * ld + r];
+  }
+}
+
 __global__ void k_pack_sym(const long long* __restrict__ moff, const int* __restrict__ ns_,
                            const int* __restrict__ ld_, const long long* __restrict__ toff,
                            const double* __restrict__ mats, double* __restrict__ tiles) {

@@ -223,6 +223,12 @@ int Ctx::solve(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_trace* 
       push(eps, 1);
     }
   }
+  if (chk_on && fo) {   // stored F-normalised directions: W^T F W = I
+    int n = 0;
+    CK(cudaMemcpyAsync(&n, cnt.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (n > 0) check_orth({Wst.p}, {Qst.p}, {n});
+  }
   if (status == FETIGPU_MAX_ITER && max_it < o.max_it)
     fail(FETIGPU_E_OUT_OF_MEMORY, "FO: direction store full after " + std::to_string(max_it) +
                                       " iterations (device memory), max_it = " + std::to_string(o.max_it));

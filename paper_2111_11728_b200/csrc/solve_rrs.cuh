@@ -26,6 +26,17 @@ __global__ void k_rrs_zpack(const OpSub* __restrict__ pc, const int* __restrict_
   }
 }
 
+// inverse of k_rrs_zpack (test hook of the invariant check): Z(r_a, s) = ZV(t)
+__global__ void k_rrs_zunpack(const OpSub* __restrict__ pc, const int* __restrict__ rows,
+                              const double* __restrict__ zl, int k, double* __restrict__ Z) {
+  const int s = blockIdx.x;
+  const OpSub d = pc[s];
+  for (int a = threadIdx.x; a < d.ns; a += blockDim.x) {
+    const int r = rows[d.map_off + a];
+    if (r >= 0) Z[(size_t)r * k + s] = zl[d.map_off + a];
+  }
+}
+
 constexpr int kZL = 16;          // Z blocks per pass of k_rrs_zgather
 constexpr int kZC = 32;          // Z blocks per register chunk of k_rrs_zscatter
 constexpr int kZRows = 32;       // map rows staged per tile in k_rrs_zscatter
@@ -495,6 +506,12 @@ int Ctx::solve_rrs(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_tra
     tr->eps_final = eps;
     tr->solve_ms = ms;
   }
+  if (chk_on && K > 0) {   // Alg. 1 orthonormality over all stored blocks
+    std::vector<const double*> ws, qs;
+    std::vector<int> rs;
+    for (const Chunk& ch : chunks) { ws.push_back(ch.w->p); qs.push_back(ch.q->p); rs.push_back(ch.used); }
+    check_orth(ws, qs, rs);
+  }
   chunks.clear();
   pt.mark("rrs store release", st);
   return 0;
@@ -819,6 +836,33 @@ int Ctx::solve_rrs_implicit(const fetigpu_solve_opts& o, double* lambda_host, fe
   CK(cudaMemcpyAsync(lambda_host, lam.p, m * 8, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   pt.mark("rrs-implicit loop + readback", st);
+  if (chk_on && !Mb.empty()) {
+    // Alg. 1 orthonormality of the implicit store: W_j = sum_l Z_l M_j[l]
+    // densely (test sizes), Q_j = F W_j by K5, then max |W^T F W - I|
+    const int nb = (int)Mb.size();
+    DBuf<double> Zd;
+    Zd.alloc((size_t)m * k * nb);
+    CK(cudaMemsetAsync(Zd.p, 0, (size_t)m * k * nb * 8, st));
+    for (int l = 0; l < nb; ++l)
+      k_rrs_zunpack<<<Ns, kThreads, 0, st>>>(d_pc.p, d_pcrows.p, ZV.p + (size_t)l * nz, k, Zd.p + (size_t)l * m * k);
+    LAUNCH_CHECK();
+    std::vector<std::unique_ptr<DBuf<double>>> Wd, Qd;
+    std::vector<const double*> ws, qs;
+    for (int j = 0; j < nb; ++j) {
+      const int rk = Mrank[j], kj = (j + 1) * k;
+      Wd.emplace_back(new DBuf<double>);
+      Qd.emplace_back(new DBuf<double>);
+      Wd.back()->alloc((size_t)m * rk);
+      Qd.back()->alloc((size_t)m * rk);
+      for (int l = 0; l <= j; ++l)   // W_j^T (rank x m) += M_j[l]^T Z_l^T
+        gemm(st, true, false, rk, m, k, 1.0, Mb[j] + (size_t)l * k, kj, Zd.p + (size_t)l * m * k, k,
+             l == 0 ? 0.0 : 1.0, Wd.back()->p, rk);
+      apply_F_block(Wd.back()->p, rk, Qd.back()->p, rk, rk);
+      ws.push_back(Wd.back()->p);
+      qs.push_back(Qd.back()->p);
+    }
+    check_orth(ws, qs, Mrank, true);
+  }
   if (tr) {
     tr->status = status;
     tr->iterations = it;

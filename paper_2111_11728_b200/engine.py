@@ -81,7 +81,7 @@ EXPORTED = ["fetigpu_set_device", "fetigpu_create", "fetigpu_build", "fetigpu_de
             "fetigpu_time_apply_block", "fetigpu_fp64_peak", "fetigpu_selftest_dmma",
             "fetigpu_pivoted_cholesky", "fetigpu_pivoted_compress", "fetigpu_time_ops",
             "fetigpu_device_memory", "fetigpu_set_rrs_store", "fetigpu_dla_gemm", "fetigpu_dla_tri_inv",
-            "fetigpu_dla_time_gemm", "fetigpu_apply_F_zblock"]
+            "fetigpu_dla_time_gemm", "fetigpu_apply_F_zblock", "fetigpu_set_check", "fetigpu_check_result"]
 
 
 class FgProblem(C.Structure):
@@ -376,6 +376,16 @@ class FetiSystem:
             L.fetigpu_device_free(self.h, dW)
             L.fetigpu_device_free(self.h, dQ)
         return Q
+
+    def set_check(self, on: bool = True):
+        """Invariant check of later FO / RRS solves (fetigpu_set_check)."""
+        check(lib().fetigpu_set_check(self.h, int(on)))
+
+    def check_result(self):
+        """(max |W^T F W - I| over the last solve's stored directions, their number)"""
+        e, n = C.c_double(), C.c_int()
+        check(lib().fetigpu_check_result(self.h, C.byref(e), C.byref(n)))
+        return e.value, n.value
 
     def apply_F_zblock(self, Z: np.ndarray) -> np.ndarray:
         """Q = F Z through the sparse-aware K5z path (Z: m x N_s per-subdomain

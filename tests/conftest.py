@@ -11,6 +11,28 @@ if ROOT not in sys.path:
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200) and libfetigpu.so")
+    config.addinivalue_line("markers", "slow: full-size oracle comparisons of several minutes of CPU "
+                                       "oracle time; run with FETIGPU_SLOW_TESTS=1")
+
+
+def pytest_collection_modifyitems(config, items):
+    if os.environ.get("FETIGPU_SLOW_TESTS") == "1":
+        return
+    skip = pytest.mark.skip(reason="slow oracle comparison (FETIGPU_SLOW_TESTS=1 runs it)")
+    for it in items:
+        if "slow" in it.keywords:
+            it.add_marker(skip)
+
+
+@pytest.fixture(scope="session", autouse=True)
+def _oracle_threads():
+    """The CPU oracle uses every host core (the GPU box has 16)."""
+    try:
+        from oracle import pyoracle
+        pyoracle.build()
+        pyoracle.lib().fo_set_threads(os.cpu_count() or 1)
+    except Exception:
+        pass
 
 
 def has_gpu() -> bool:

@@ -38,6 +38,12 @@ CASES = {
     "C1_dir_k": lambda: pb.config1(sx=3, sy=3, n=8).replace(scaling=1, precond=1),
     "C2_lumped": lambda: pb.config2(sx=3, sy=2, n=10).replace(precond=0),
     "C3tf_super": lambda: pb.config3(method=0, sx=3, sy=2, n=8).replace(precond=2),
+    # one-direction supports: a roller at a partition vertex gives
+    # that subdomain an odd n_c, a roller on an interface edge node an odd n_s
+    "C2_roller_vertex": lambda: pb.config2(sx=3, sy=2, n=8).replace(
+        dirichlet=[(0, 0, 0.0), (0, 1, 0.0), (3 * 8, 1, 0.0)], point_loads=[((2 * 8) * 25 + 12, 1, -1.0)]),
+    "C2_roller_edge": lambda: pb.config2(sx=3, sy=2, n=8).replace(
+        dirichlet=pb.left_clamp(3, 2, 8) + [(3 * 25 + 8, 0, 0.0)]),
 }
 
 
@@ -248,7 +254,8 @@ def test_fp64_peak_reported():
     assert dmma > 1.0 and dfma > 1.0
 
 
-@pytest.mark.parametrize("name", ["C1", "C1b", "C2s", "C3tf_s", "C3dp_s", "C5s", "C4s", "C1_dir_k"])
+@pytest.mark.parametrize("name", ["C1", "C1b", "C2s", "C3tf_s", "C3dp_s", "C5s", "C4s", "C1_dir_k",
+                                  "C2_roller_vertex", "C2_roller_edge"])
 @pytest.mark.parametrize("k", [1, 7, 64, 130])
 def test_block_apply(name, k, oracle_mod):
     """K5 (DMMA block apply, fused gather/scatter) against the per-column GEMV
