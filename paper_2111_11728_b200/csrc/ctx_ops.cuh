@@ -379,7 +379,25 @@ void Ctx::apply_F_block(const double* W, int ldw, double* Q, int ldq, int k) {
   dim3 grid((k + kBN - 1) / kBN, (max_ns + kBM - 1) / kBM, Ns);
   const bool fast = folded && blk_aligned && (k % 2 == 0) && (ldw % 2 == 0) && (ldq % 2 == 0) &&
                     ((uintptr_t)W % 16 == 0) && ((uintptr_t)Q % 16 == 0);
-  if (fast) k_block_apply_dp<<<grid, 256, kAsyncSmem, st>>>(a);
+  // tile of the fast path (FETIGPU_K5_CFG, C4 k = 2048 block apply on a
+  // B200, bit-identical results): 0 = 128 x 64 x 16 / 3 stages / 2 CTAs per
+  // SM 75.4 ms; 1 = 64 x 64 x 16 / 3 76.6; 2 = 64 x 64 x 32 / 2 74.1;
+  // 3 = 64 x 64 x 16 / 2 (4 CTAs per SM) 72.8 (default); 4 = 128 x 64 x 16 /
+  // 3 (templated) 75.3; 5 = 64 x 128 x 16 / 3 74.7
+  static const int k5cfg = [] {
+    const char* e = getenv("FETIGPU_K5_CFG");
+    return e ? atoi(e) : 3;
+  }();
+  auto launch2 = [&](auto kern, int BM, int BN, size_t smem, int threads) {
+    raise_smem_limit(kern, smem);
+    kern<<<dim3((k + BN - 1) / BN, (max_ns + BM - 1) / BM, Ns), threads, smem, st>>>(a);
+  };
+  if (fast && k5cfg == 1) launch2(k_block_apply_dp2<64, 64, 16, 3>, 64, 64, k5_smem<64, 64, 16, 3>(max_ns + 8), 128);
+  else if (fast && k5cfg == 2) launch2(k_block_apply_dp2<64, 64, 32, 2>, 64, 64, k5_smem<64, 64, 32, 2>(max_ns + 8), 128);
+  else if (fast && k5cfg == 3) launch2(k_block_apply_dp2<64, 64, 16, 2>, 64, 64, k5_smem<64, 64, 16, 2>(max_ns + 8), 128);
+  else if (fast && k5cfg == 4) launch2(k_block_apply_dp2<128, 64, 16, 3>, 128, 64, k5_smem<128, 64, 16, 3>(max_ns + 8), 256);
+  else if (fast && k5cfg == 5) launch2(k_block_apply_dp2<64, 128, 16, 3>, 64, 128, k5_smem<64, 128, 16, 3>(max_ns + 8), 256);
+  else if (fast) k_block_apply_dp<<<grid, 256, kAsyncSmem, st>>>(a);
   else if (KR == 1) k_block_apply<1><<<grid, 256, kBlockSmem, st>>>(a);
   else k_block_apply<3><<<grid, 256, kBlockSmem, st>>>(a);
   LAUNCH_CHECK();

@@ -312,6 +312,117 @@ __global__ void __launch_bounds__(256, 2) k_block_apply_dp(BlockApplyArgs a) {
   }
 }
 
+// K5, FETI-DP fast path, templated tile: BM x BN CTA tile of 32 x 32 warp
+// tiles, BK-deep k steps in an ST-stage cp.async ring (same operand layouts
+// and arithmetic order per output element as k_block_apply_dp: the k loop
+// runs over [F''_s | A''_s] columns in ascending order).  The dense-algebra
+// sweep (profiles/r02_gemm_sweep.log) found 64 x 64 tiles with 3-4 resident
+// CTAs per SM keep the DMMA pipe busiest.
+template <int BM, int BN, int BK, int ST>
+__global__ void __launch_bounds__((BM / 32) * (BN / 32) * 32) k_block_apply_dp2(BlockApplyArgs a) {
+  constexpr int THREADS = (BM / 32) * (BN / 32) * 32;
+  constexpr int AP = BK + 4, BP = BN + 8;
+  extern __shared__ __align__(16) double dsm[];
+  double* As = dsm;                                   // ST x (BM x AP)
+  double* Bs = dsm + ST * BM * AP;                    // ST x (BK x BP)
+  int* srow = reinterpret_cast<int*>(Bs + ST * BK * BP);
+  const int s = blockIdx.z;
+  const OpSub d = a.subs[s];
+  const int ns = d.ns;
+  const int row0 = blockIdx.y * BM;
+  if (row0 >= ns) return;
+  const DpSub p = a.dps[s];
+  const int nc = p.nc;
+  const int kin = ns + nc;
+  const int col0 = blockIdx.x * BN;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int WGN = BN / 32;
+  const int wr = warp / WGN, wc = warp % WGN;
+  const double* F = a.mats + d.moff;
+  const double* Abc = a.abc + p.abc_off;
+  const int* rw = a.rows + d.map_off;
+  for (int j = tid; j < kin; j += THREADS) srow[j] = j < ns ? rw[j] : a.cmap[p.cmap_off + j - ns];
+  __syncthreads();
+  const int nk = (kin + BK - 1) / BK;
+  auto issue = [&](int t) {
+    const int kk = t * BK, st = t % ST;
+    double* A_ = As + st * BM * AP;
+    double* B_ = Bs + st * BK * BP;
+    constexpr int ACH = BM * (BK / 2), BCH = BK * (BN / 2);
+#pragma unroll
+    for (int q = 0; q < (ACH + THREADS - 1) / THREADS; ++q) {
+      const int idx = tid + q * THREADS;
+      if (ACH % THREADS == 0 || idx < ACH) {
+        const int r = idx / (BK / 2), c2 = (idx % (BK / 2)) * 2;
+        const int gi = row0 + r, gj = kk + c2;
+        const double* src = F;
+        const bool ok = gi < ns && gj < kin;
+        if (ok) src = gj < ns ? F + (size_t)gi * d.ld + gj : Abc + (size_t)gi * nc + (gj - ns);
+        cp_async16(A_ + r * AP + c2, src, ok);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < (BCH + THREADS - 1) / THREADS; ++q) {
+      const int idx = tid + q * THREADS;
+      if (BCH % THREADS == 0 || idx < BCH) {
+        const int r = idx / (BN / 2), c2 = (idx % (BN / 2)) * 2;
+        const int gj = kk + r, gc = col0 + c2;
+        const double* src = a.W;
+        const bool ok = gj < kin && gc < a.k;
+        if (ok) src = gj < ns ? a.W + (size_t)srow[gj] * a.ldw + gc : a.U + (size_t)srow[gj] * a.ldu + gc;
+        cp_async16(B_ + r * BP + c2, src, ok);
+      }
+    }
+  };
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+#pragma unroll
+  for (int t = 0; t < ST - 1; ++t) {
+    if (t < nk) issue(t);
+    cp_async_commit();
+  }
+  for (int t = 0; t < nk; ++t) {
+    cp_async_wait<ST - 2>();
+    __syncthreads();
+    if (t + ST - 1 < nk) issue(t + ST - 1);
+    cp_async_commit();
+    const double* A_ = As + (t % ST) * BM * AP;
+    const double* B_ = Bs + (t % ST) * BK * BP;
+#pragma unroll
+    for (int k4 = 0; k4 < BK; k4 += 4) {
+      double af[4], bf[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) af[i] = A_[(wr * 32 + i * 8 + (lane >> 2)) * AP + k4 + (lane & 3)];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bf[j] = B_[(k4 + (lane & 3)) * BP + wc * 32 + j * 8 + (lane >> 2)];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+  }
+  cp_async_wait<0>();
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int li = row0 + wr * 32 + i * 8 + (lane >> 2);
+    if (li >= ns) continue;
+    double* qrow = a.Q + (size_t)srow[li] * a.ldq;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int gc = col0 + wc * 32 + j * 8 + 2 * (lane & 3);
+      if (gc < a.k) atomicAdd(qrow + gc, acc[i][j][0]);
+      if (gc + 1 < a.k) atomicAdd(qrow + gc + 1, acc[i][j][1]);
+    }
+  }
+}
+template <int BM, int BN, int BK, int ST>
+constexpr size_t k5_smem(int kin_max) {
+  return (size_t)ST * (BM * (BK + 4) + BK * (BN + 8)) * 8 + (size_t)kin_max * 4;
+}
+
 // FETI-DP coarse pre-pass for a block: T_s = A_bc^T (B_s^T W)   (n_c x k).
 // One CTA per (128-column slab, subdomain): the subdomain's A_bc rows (padded
 // to 8), row ids and coefficients are staged in shared memory once, so the
