@@ -526,7 +526,7 @@ def main():
         tf = flops / (t_blk * 1e-3) / 1e12
         block = {"k": k, "ms": t_blk, "flops": flops, "tflops": tf * ws, "peak_dmma_tflops": dmma,
                  "peak_dfma_tflops": dfma, "frac": tf / dmma, "peak_kind": "measured (fetigpu_fp64_peak)",
-                 "kernel": "k_block_apply<1> (DMMA m8n8k4) + coarse pre-pass + cuBLAS DGEMM"}
+                 "kernel": "k_block_apply_dp2<64,64,16,2> (DMMA m8n8k4, fused W-row gather and Q scatter) + coarse pre-pass + DMMA GEMM (dla.cuh) for U = Kbar^-1 T"}
         L.fetigpu_device_free(g.h, dW)
         L.fetigpu_device_free(g.h, dQ)
         log("block", block)

@@ -208,6 +208,21 @@ int fetigpu_local_operator(fetigpu_ctx* ctx, int s, int* ns, int* dofs, double* 
 /* Block F-apply (K5, FP64 tensor cores): Q = F W for k columns stored
  * row-major (W(i,c) = W[i*ldw + c]), device pointers, ctx stream. */
 int fetigpu_apply_F_block_device(fetigpu_ctx* ctx, const double* W, int ldw, double* Q, int ldq, int k);
+/* Subdomain-sharded apply (one rank of a row-band partition
+ * of the module grid, exchanges done by the caller: paper_2111_11728_b200/
+ * shard.py over torch.distributed).  The context applies only subdomains
+ * [s0, s1).  phase1: y := partial sum over the owned subdomains (T-FETI F or
+ * the preconditioner: complete except on rows shared with another rank;
+ * FETI-DP F: nothing yet) and, for FETI-DP F, the owned t_s = A''_s^T x_s
+ * written into the zeroed tot_c vector tout.  After the caller sums tout over
+ * ranks, phase2 adds the coarse correction and the local parts for the owned
+ * subdomains; summing y over ranks on the shared rows completes F x.  Every
+ * dual row has two owners, so the N-rank result equals the 1-GPU apply bit
+ * for bit.  Device pointers, context stream. */
+int fetigpu_shard_set_range(fetigpu_ctx* ctx, int s0, int s1);
+int fetigpu_shard_info(const fetigpu_ctx* ctx, int* tot_c);
+int fetigpu_shard_phase1_device(fetigpu_ctx* ctx, const double* x, double* y, double* tout, int precond);
+int fetigpu_shard_phase2_device(fetigpu_ctx* ctx, const double* tall, double* y);
 /* Invariant check of the device solver (test hook): when
  * on, every FO / RRS solve afterwards reconstructs its stored F-normalised
  * search directions W and reports max |W^T F W - I| over all of them (FO

@@ -235,6 +235,18 @@ struct Ctx {
   DBuf<double> bz_Y;
   int bz_nedges = 0, bz_maxns = 0;
   bool bz_prepare();
+  // ---- subdomain-sharded apply: this context applies only the
+  // subdomains [shard_s0, shard_s1) of the full problem (one rank of a
+  // row-band partition of the module grid); exchanges are the caller's
+  // (shard.py: NCCL / gloo, or an in-process emulation)
+  int shard_s0 = 0, shard_s1 = -1;
+  int tot_c() const {
+    int t = 0;
+    for (auto& S : su.subs) t += (int)S.c.size();
+    return t;
+  }
+  void shard_phase1(const double* x, double* y, double* tout, bool precond);
+  void shard_phase2(const double* tall, double* y);
   // coarse scratch of the block applies (K5 / K5z) for k columns
   void ensure_block_buffers(int k) {
     if (su.method != FETIGPU_FETIDP) return;

@@ -403,6 +403,80 @@ void Ctx::apply_F_block(const double* W, int ldw, double* Q, int ldq, int k) {
   LAUNCH_CHECK();
 }
 
+// Sharded F (or preconditioner) apply, phase 1 over the owned subdomains:
+// y := 0, then T-FETI / preconditioner: y += sum_{s owned} B_s M_s B_s^T x
+// (M = F_s or S~_s, complete for rows with both owners owned); FETI-DP F:
+// v_s = F''_s x_s and t_s = A''_s^T x_s for the owned s, t copied into the
+// zeroed tot_c vector `tout` at the owned offsets.  The kernels and their
+// per-subdomain arithmetic are those of the single-context apply (the
+// symmetric-packed / full-matrix choice included), so after the exchanges
+// the result equals the 1-GPU apply bit for bit: every dual row has exactly
+// two owners (0 + a + b == a + b in any order) and the coarse gather runs on
+// the complete t in the fixed owner order.
+void Ctx::shard_phase1(const double* x, double* y, double* tout, bool precond) {
+  const int s0 = shard_s0, s1 = shard_s1 < 0 ? su.Ns : shard_s1, n = s1 - s0;
+  CK(cudaMemsetAsync(y, 0, (size_t)su.m * 8, st));
+  if (n <= 0 || su.m == 0) return;
+  if (precond) {
+    if (pc_sym) {
+      auto k = KRp == 1 ? k_sym_gemv_scatter<1, false> : k_sym_gemv_scatter<3, false>;
+      k<<<n, 256, pc_sym_smem, st>>>(d_pcsym.p, d_pcsymtiles.p, d_pcrows.p, d_pccoef.p, x, y, nullptr, nullptr,
+                                     nullptr, nullptr, nullptr, s0, nullptr, 0, 1, nullptr);
+    } else {
+      auto k = KRp == 1 ? k_gather_gemv_scatter<1, false> : k_gather_gemv_scatter<3, false>;
+      k<<<dim3(n, 1, pc_rsplit), kThreads, max_pc_ld * 8, st>>>(d_pc.p + s0, d_pcmat.p, d_pcrows.p, d_pccoef.p, x,
+                                                                  y, nullptr, 0, nullptr, nullptr, su.m, su.m, 1,
+                                                                  nullptr, nullptr, nullptr);
+    }
+    LAUNCH_CHECK();
+    return;
+  }
+  if (su.method == FETIGPU_TFETI) {
+    if (use_sym)
+      k_sym_gemv_scatter<3, false><<<n, 256, sym_smem, st>>>(d_sym.p, d_symtiles.p, d_oprows.p, d_opcoef_apply.p,
+                                                             x, y, nullptr, nullptr, nullptr, nullptr, nullptr, s0,
+                                                             nullptr, 0, 1, nullptr);
+    else
+      k_gather_gemv_scatter<3, false><<<dim3(n, 1, rsplit), kThreads, max_ld * 8, st>>>(
+          d_op.p + s0, d_opmat.p, d_oprows.p, d_opcoef_apply.p, x, y, nullptr, 0, nullptr, nullptr, su.m, su.m, 1,
+          nullptr, nullptr, nullptr);
+    LAUNCH_CHECK();
+    return;
+  }
+  if (use_sym)
+    k_sym_gemv_scatter<1, true><<<n, 256, sym_smem, st>>>(d_sym.p, d_symtiles.p, d_oprows.p, d_opcoef_apply.p, x,
+                                                          nullptr, d_vbuf.p, d_voff.p, d_dp.p, d_abc.p, d_tbuf.p, s0,
+                                                          nullptr, 0, 1, nullptr);
+  else
+    k_gather_gemv_scatter<1, true><<<dim3(n, 1, rsplit), kThreads, max_ld * 8, st>>>(
+        d_op.p + s0, d_opmat.p, d_oprows.p, d_opcoef_apply.p, x, nullptr, nullptr, 0, d_vbuf.p, d_voff.p + s0,
+        su.m, 0, 1, d_dp.p + s0, d_abc.p, d_tbuf.p);
+  LAUNCH_CHECK();
+  int t0 = 0, t1 = 0;
+  for (int s = 0; s < s1; ++s) {
+    const int c = (int)su.subs[s].c.size();
+    if (s < s0) t0 += c;
+    t1 += c;
+  }
+  if (t1 > t0) CK(cudaMemcpyAsync(tout + t0, d_tbuf.p + t0, (size_t)(t1 - t0) * 8, cudaMemcpyDeviceToDevice, st));
+}
+
+// Phase 2 (FETI-DP F only): t complete on every rank -> the coarse gather in
+// fixed owner order, u = Kbar^{-1} g (redundant on every rank), then
+// y += B_s (v_s + A''_s u_s) for the owned subdomains.
+void Ctx::shard_phase2(const double* tall, double* y) {
+  if (su.method != FETIGPU_FETIDP || su.m == 0) return;
+  const int s0 = shard_s0, s1 = shard_s1 < 0 ? su.Ns : shard_s1, n = s1 - s0;
+  const int tc = tot_c();
+  if (tc) CK(cudaMemcpyAsync(d_tbuf.p, tall, (size_t)tc * 8, cudaMemcpyDeviceToDevice, st));
+  coarse_solve_packed(false, nullptr);
+  if (n > 0) {
+    k_dp_phase2<<<n, kThreads, 0, st>>>(d_op.p + s0, d_dp.p + s0, d_oprows.p, d_opcoef_apply.p, d_abc.p, d_cmap.p,
+                                        d_h.p, d_vbuf.p, y, 1.0);
+    LAUNCH_CHECK();
+  }
+}
+
 bool Ctx::bz_prepare() {
   if (bz_state) return bz_state > 0;
   bz_state = -1;

@@ -271,6 +271,32 @@ int fetigpu_apply_F_block_device(fetigpu_ctx* ctx, const double* W, int ldw, dou
   });
 }
 
+// ---- subdomain-sharded apply, device pointers on the ctx stream
+int fetigpu_shard_set_range(fetigpu_ctx* ctx, int s0, int s1) {
+  return guarded([&] {
+    NEED_BUILT(ctx);
+    Ctx& c = ctx->c;
+    if (s0 < 0 || s1 < s0 || s1 > c.su.Ns) fail(FETIGPU_E_INVALID_ARGUMENT, "bad subdomain range");
+    c.shard_s0 = s0;
+    c.shard_s1 = s1;
+  });
+}
+int fetigpu_shard_info(const fetigpu_ctx* ctx, int* tot_c) {
+  return guarded([&] { *tot_c = ctx->c.tot_c(); });
+}
+int fetigpu_shard_phase1_device(fetigpu_ctx* ctx, const double* x, double* y, double* tout, int precond) {
+  return guarded([&] {
+    NEED_BUILT(ctx);
+    ctx->c.shard_phase1(x, y, tout, precond != 0);
+  });
+}
+int fetigpu_shard_phase2_device(fetigpu_ctx* ctx, const double* tall, double* y) {
+  return guarded([&] {
+    NEED_BUILT(ctx);
+    ctx->c.shard_phase2(tall, y);
+  });
+}
+
 // invariant check of the device solver's stored directions (test hook)
 int fetigpu_set_check(fetigpu_ctx* ctx, int on) {
   return guarded([&] {

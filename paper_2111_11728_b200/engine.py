@@ -81,7 +81,9 @@ EXPORTED = ["fetigpu_set_device", "fetigpu_create", "fetigpu_build", "fetigpu_de
             "fetigpu_time_apply_block", "fetigpu_fp64_peak", "fetigpu_selftest_dmma",
             "fetigpu_pivoted_cholesky", "fetigpu_pivoted_compress", "fetigpu_time_ops",
             "fetigpu_device_memory", "fetigpu_set_rrs_store", "fetigpu_dla_gemm", "fetigpu_dla_tri_inv",
-            "fetigpu_dla_time_gemm", "fetigpu_apply_F_zblock", "fetigpu_set_check", "fetigpu_check_result"]
+            "fetigpu_dla_time_gemm", "fetigpu_apply_F_zblock", "fetigpu_set_check", "fetigpu_check_result",
+            "fetigpu_shard_set_range", "fetigpu_shard_info", "fetigpu_shard_phase1_device",
+            "fetigpu_shard_phase2_device"]
 
 
 class FgProblem(C.Structure):
