@@ -187,6 +187,18 @@ int fetigpu_project_device(fetigpu_ctx* ctx, double* v, int ncols, int ld);
 int fetigpu_rhs(fetigpu_ctx* ctx, double* d, double* lambda0);
 int fetigpu_solve(fetigpu_ctx* ctx, const fetigpu_solve_opts* o, double* lambda,
                   fetigpu_trace* tr);
+/* pcg / simultaneous_pcg from a given lambda0 (host, length m) instead of
+ * the default start (FETI-DP: 0; T-FETI: G^T (G G^T)^{-1} e):
+ * the SIMP loop's warm start from the previous snapshot's multipliers
+ * (SURVEY.md 8f rank 2).  T-FETI projects it onto G lambda = e. */
+int fetigpu_solve_warm(fetigpu_ctx* ctx, const fetigpu_solve_opts* o, const double* lambda0, double* lambda,
+                       fetigpu_trace* tr);
+/* Next density snapshot of the same problem (same partition, module size,
+ * design count, supports, loads and method): host setup and device build
+ * again, operator storage reused through the context's block cache (no
+ * cudaFree / cudaMalloc of the multi-GB operator storage).  The SIMP outer
+ * loop calls this once per optimization iteration. */
+int fetigpu_rebuild(fetigpu_ctx* ctx, const fetigpu_problem* p);
 /* RRS direction store (no reference counterpart: the reference's
  * simultaneous_pcg keeps W_j, Q_j densely).  EXPLICIT: that
  * dense store, 2 m rank_j doubles per iteration.  IMPLICIT (FETI-DP only):

@@ -127,6 +127,15 @@ struct Ctx {
   // freed RRS direction-store chunks, reused by this context's next solve;
   // returned to the driver with the context
   BlockCache rrs_cache;
+  // operator storage recycled across fetigpu_rebuild (density snapshots)
+  BlockCache build_cache;
+  int rebuilds = 0;
+  // warm start of the next solve (fetigpu_solve_warm): device copy of lambda0
+  DBuf<double> d_warm;
+  bool warm = false;
+  // lam := lambda0 of the solve: the warm start when one is set (T-FETI:
+  // projected onto G lambda = e: lam0 + P(warm - lam0)), else the default
+  void init_lambda(double* lam);
   ~Ctx() {
     for (auto& e : pipe_in) if (e) cudaEventDestroy(e);
     for (auto& e : pipe_done) if (e) cudaEventDestroy(e);

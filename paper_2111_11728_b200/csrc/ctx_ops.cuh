@@ -477,6 +477,22 @@ void Ctx::shard_phase2(const double* tall, double* y) {
   }
 }
 
+void Ctx::init_lambda(double* lam) {
+  const int m = su.m;
+  if (!warm) {
+    CK(cudaMemcpyAsync(lam, d_lam0.p, (size_t)m * 8, cudaMemcpyDeviceToDevice, st));
+    return;
+  }
+  if (su.method == FETIGPU_TFETI) {
+    k_sub<<<grid_for(m), kThreads, 0, st>>>(m, d_warm.p, d_lam0.p, lam);   // lam = warm - lam0
+    project(lam, 1, m);
+    k_axpy<<<grid_for(m), kThreads, 0, st>>>(m, 1.0, d_lam0.p, lam);       // lam += lam0
+    LAUNCH_CHECK();
+  } else {
+    CK(cudaMemcpyAsync(lam, d_warm.p, (size_t)m * 8, cudaMemcpyDeviceToDevice, st));
+  }
+}
+
 bool Ctx::bz_prepare() {
   if (bz_state) return bz_state > 0;
   bz_state = -1;

@@ -218,6 +218,54 @@ int fetigpu_solve(fetigpu_ctx* ctx, const fetigpu_solve_opts* o, double* lambda,
   });
 }
 
+int fetigpu_solve_warm(fetigpu_ctx* ctx, const fetigpu_solve_opts* o, const double* lambda0, double* lambda,
+                       fetigpu_trace* tr) {
+  return guarded([&] {
+    NEED_BUILT(ctx);
+    Ctx& c = ctx->c;
+    struct Reset {
+      Ctx& c;
+      ~Reset() { c.warm = false; }
+    } reset{c};
+    if (lambda0 && c.su.m > 0) {
+      if (c.d_warm.n < (size_t)c.su.m) c.d_warm.alloc(c.su.m);
+      CK(cudaMemcpyAsync(c.d_warm.p, lambda0, (size_t)c.su.m * 8, cudaMemcpyHostToDevice, c.st));
+      c.warm = true;
+    }
+    c.solve(*o, lambda, tr);
+  });
+}
+
+// New snapshot of the same problem (same partition, supports, loads, method;
+// new densities / material): host setup again, device operators rebuilt in
+// the existing storage (recycled through the context's block cache).
+int fetigpu_rebuild(fetigpu_ctx* ctx, const fetigpu_problem* p) {
+  return guarded([&] {
+    NEED_BUILT(ctx);
+    if (!p) fail(FETIGPU_E_INVALID_ARGUMENT, "null problem");
+    Ctx& c = ctx->c;
+    const Setup& old = c.su;
+    if (p->sx != old.sx || p->sy != old.sy || p->n != old.n || p->n_designs != old.n_designs ||
+        p->method != old.method)
+      fail(FETIGPU_E_DIMENSION_MISMATCH, "rebuild: partition, module size, design count and method must match");
+    Setup su;
+    su.load(*p);
+    if (su.m != old.m || su.Nc != old.Nc) fail(FETIGPU_E_DIMENSION_MISMATCH, "rebuild: constraint structure changed");
+    CK(cudaStreamSynchronize(c.st));
+    c.su = std::move(su);
+    c.have_rhs = false;
+    c.bz_state = 0;
+    c.built = false;
+    struct Scope {
+      BlockCache* prev;
+      explicit Scope(BlockCache* b) : prev(g_build_cache) { g_build_cache = b; }
+      ~Scope() { g_build_cache = prev; }
+    } scope(&c.build_cache);
+    c.build();
+    ++c.rebuilds;
+  });
+}
+
 int fetigpu_set_rrs_store(fetigpu_ctx* ctx, int mode) {
   return guarded([&] {
     if (!ctx) fail(FETIGPU_E_INVALID_ARGUMENT, "null context");

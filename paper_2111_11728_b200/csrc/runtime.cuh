@@ -159,6 +159,13 @@ static size_t dev_free_bytes(BlockCache* cache = nullptr) {
   return freeb;
 }
 
+// During an in-place rebuild (fetigpu_rebuild) every DBuf allocated on this
+// thread without its own cache takes this one (and keeps it): the rebuild's
+// release + alloc of same-sized operator storage recycles the blocks instead
+// of calling cudaFree / cudaMalloc (multi-GB calls that occasionally stall
+// for 100+ ms in the driver).
+static thread_local BlockCache* g_build_cache = nullptr;
+
 template <class T>
 struct DBuf {
   T* p = nullptr;
@@ -178,6 +185,7 @@ struct DBuf {
   BlockCache* cache = nullptr;  // recycled storage: allocate through this block cache
   void alloc(size_t count) {
     release();
+    if (!cache && g_build_cache) cache = g_build_cache;
     if (count == 0) count = 1;
     p = static_cast<T*>(dev_alloc(count * sizeof(T), cache));
     n = count;

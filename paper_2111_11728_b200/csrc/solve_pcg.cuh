@@ -74,7 +74,7 @@ int Ctx::solve(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_trace* 
   std::unique_ptr<Scal, decltype(&cudaFreeHost)> hs_guard(hs, cudaFreeHost);
   const bool tf = su.method == FETIGPU_TFETI;
   CK(cudaEventRecord(ev0, st));
-  CK(cudaMemcpyAsync(lam.p, d_lam0.p, m * 8, cudaMemcpyDeviceToDevice, st));
+  init_lambda(lam.p);
   apply_F(lam.p, q.p, 1, m, m);
   int fapp = 1;
   k_sub<<<grid_for(m), kThreads, 0, st>>>(m, d_d.p, q.p, r.p);

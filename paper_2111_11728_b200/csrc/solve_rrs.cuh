@@ -359,7 +359,7 @@ int Ctx::solve_rrs(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_tra
   std::unique_ptr<Scal, decltype(&cudaFreeHost)> hs_guard(hs, cudaFreeHost);
   pt.mark("rrs setup", st);
   CK(cudaEventRecord(ev0, st));
-  CK(cudaMemcpyAsync(lam.p, d_lam0.p, m * 8, cudaMemcpyDeviceToDevice, st));
+  init_lambda(lam.p);
   apply_F(lam.p, q.p, 1, m, m);
   int fapp = 1;
   k_sub<<<grid_for(m), kThreads, 0, st>>>(m, d_d.p, q.p, r.p);
@@ -658,7 +658,7 @@ int Ctx::solve_rrs_implicit(const fetigpu_solve_opts& o, double* lambda_host, fe
   raise_smem_limit(k_rrs_zscatter, kZScatterSmem);
   pt.mark("rrs-implicit setup", st);
   CK(cudaEventRecord(ev0, st));
-  CK(cudaMemcpyAsync(lam.p, d_lam0.p, m * 8, cudaMemcpyDeviceToDevice, st));
+  init_lambda(lam.p);
   apply_F(lam.p, q.p, 1, m, m);
   int fapp = 1;
   k_sub<<<grid_for(m), kThreads, 0, st>>>(m, d_d.p, q.p, r.p);

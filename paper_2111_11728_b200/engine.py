@@ -83,7 +83,7 @@ EXPORTED = ["fetigpu_set_device", "fetigpu_create", "fetigpu_build", "fetigpu_de
             "fetigpu_device_memory", "fetigpu_set_rrs_store", "fetigpu_dla_gemm", "fetigpu_dla_tri_inv",
             "fetigpu_dla_time_gemm", "fetigpu_apply_F_zblock", "fetigpu_set_check", "fetigpu_check_result",
             "fetigpu_shard_set_range", "fetigpu_shard_info", "fetigpu_shard_phase1_device",
-            "fetigpu_shard_phase2_device"]
+            "fetigpu_shard_phase2_device", "fetigpu_solve_warm", "fetigpu_rebuild"]
 
 
 class FgProblem(C.Structure):
@@ -343,6 +343,30 @@ class FetiSystem:
                          eps0=tr.eps0, eps_final=tr.eps_final, eps=eps[:n].copy(),
                          kept=kept[:n].copy(), f_app=fap[:n].copy(), solve_ms=tr.solve_ms,
                          phase_ms=list(tr.phase_ms))
+
+    def solve_warm(self, lam0, tol: float = 1e-6, max_it: int = 1000, directions: int = 0, rel: bool = True,
+                   pivot_tol: float = 1e-12, reorth_passes: int = 2):
+        """solve() started from lam0 (fetigpu_solve_warm)."""
+        o = FgOpts(tol, 1 if rel else 0, max_it, directions, pivot_tol, reorth_passes)
+        cap = max_it + 2
+        eps, kept, fap = np.zeros(cap), np.zeros(cap, dtype=np.int32), np.zeros(cap, dtype=np.int32)
+        tr = FgTrace(0, 0, 0, 0.0, 0.0, cap, _p(eps), _p(kept), _p(fap), 0.0)
+        tr.phase_ms = (C.c_double * 8)(*([0.0] * 8))
+        lam = np.zeros(self.m)
+        l0 = np.ascontiguousarray(lam0, dtype=np.float64)
+        check(lib().fetigpu_solve_warm(self.h, C.byref(o), _p(l0), _p(lam), C.byref(tr)))
+        n = tr.iterations + 1
+        return lam, dict(status=tr.status, iterations=tr.iterations, f_applies=tr.f_applies,
+                         eps0=tr.eps0, eps_final=tr.eps_final, eps=eps[:n].copy(),
+                         kept=kept[:n].copy(), f_app=fap[:n].copy(), solve_ms=tr.solve_ms,
+                         phase_ms=list(tr.phase_ms))
+
+    def rebuild(self, prob: Problem):
+        """Next snapshot of the same problem in place (fetigpu_rebuild)."""
+        self._keep = []
+        st = make_struct(prob, self._keep)
+        check(lib().fetigpu_rebuild(self.h, C.byref(st)))
+        self.prob = prob
 
     RRS_STORE = {"auto": 0, "explicit": 1, "implicit": 2}
 

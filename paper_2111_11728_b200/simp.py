@@ -3,9 +3,14 @@
 SURVEY.md 8f rank 2 -- the paper's motivating workload).
 
 Every optimization iteration rebuilds the explicit local operators for the
-current densities (one ``FetiSystem`` per snapshot, F_s shared per module
-type) and solves the state problem on the GPU; sensitivities, the filter and
-the optimality-criteria update are small host-side array work.
+current densities in place (one ``FetiSystem`` for the whole run,
+``FetiSystem.rebuild`` -> fetigpu_rebuild reuses the device storage; F_s
+shared per module type) and solves the state problem on the GPU, optionally
+warm-started from the previous snapshot's multipliers (fetigpu_solve_warm;
+off by default: with the SPEC's relative criterion eps(i)/eps(0) a warm start
+tightens the absolute accuracy instead of saving iterations).  The
+sensitivities, the filter and the optimality-criteria update are small
+host-side array work.
 
 Design decisions restated from SPEC.md:536-537: optimality-criteria update with
 damping 0.5 and move limit 0.2, bisection on the Lagrange multiplier for the
@@ -72,8 +77,9 @@ class SimpState:
 
 def optimize(prob: Problem, iterations: int = 10, volfrac: float = 0.5, rmin: float = 1.5,
              move: float = 0.2, damping: float = 0.5, rho_min: float = 1e-3, tol: float = 1e-6,
-             directions: int = 2, snapshots=()) -> SimpState:
-    """Runs `iterations` OC steps from the uniform design rho = volfrac."""
+             directions: int = 2, snapshots=(), warm: bool = False, in_place: bool = True) -> SimpState:
+    """Runs `iterations` OC steps from the uniform design rho = volfrac.
+    in_place=False re-creates the system per snapshot (round-1 behaviour)."""
     from .engine import FetiSystem, IndefiniteInput
     n, T = prob.n, prob.densities.shape[0]
     types = np.asarray(prob.module_type)
@@ -85,18 +91,31 @@ def optimize(prob: Problem, iterations: int = 10, volfrac: float = 0.5, rmin: fl
     Hs = H.sum(axis=1)
     state = SimpState(rho.copy(), [], 0, [], [])
     snaps = {}
+    g = None
+    lam_prev = None
     for it in range(iterations):
-        g = FetiSystem(prob.replace(densities=rho.copy()))
+        snap = prob.replace(densities=rho.copy())
+        if g is None or not in_place:
+            if g is not None:
+                g.close()
+            g = FetiSystem(snap)
+        else:
+            g.rebuild(snap)
+
+        def state_solve(dirs):
+            if warm and lam_prev is not None:
+                return g.solve_warm(lam_prev, tol=tol, max_it=2000, directions=dirs)
+            return g.solve(tol=tol, max_it=2000, directions=dirs)
         used = directions
         try:
-            lam, tr = g.solve(tol=tol, max_it=2000, directions=directions)
+            lam, tr = state_solve(directions)
         except IndefiniteInput:
             # RRS Gram lost positivity beyond pivot_tol: the
             # application falls back to FO for this state solve
             used = 1
-            lam, tr = g.solve(tol=tol, max_it=2000, directions=1)
+            lam, tr = state_solve(1)
+        lam_prev = lam
         u = g.recover(lam)
-        g.close()
         state.solves.append({"iterations": tr["iterations"], "status": tr["status"], "solve_ms": tr["solve_ms"],
                              "directions": used})
         # compliance and sensitivities per element, summed per module type
@@ -133,6 +152,8 @@ def optimize(prob: Problem, iterations: int = 10, volfrac: float = 0.5, rmin: fl
         state.iteration = it + 1
         if it + 1 in snapshots:
             snaps[it + 1] = rho.copy()
+    if g is not None:
+        g.close()
     state.densities = rho
     state.snapshots = snaps
     return state

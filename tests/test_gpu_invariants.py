@@ -179,3 +179,47 @@ def test_rrs_rank_deficiency_mirrored(store, oracle_mod):
     assert tg["kept"].min() < 2
     np.testing.assert_array_equal(tg["kept"], to["kept"])
     g.close()
+
+
+def test_rebuild_in_place_equals_fresh_build():
+    """fetigpu_rebuild (next density snapshot in the existing storage) gives
+    the operator and the solve of a freshly built system bit for bit."""
+    from paper_2111_11728_b200 import engine
+    p1 = pb.config5(sx=4, sy=2, n=12, n_designs=3)
+    p2 = p1.replace(densities=np.clip(p1.densities * 0.7 + 0.2, 0.0, 1.0))
+    g = engine.FetiSystem(p1)
+    _ = g.solve(tol=1e-6, max_it=200, directions=2)
+    g.rebuild(p2)
+    f = engine.FetiSystem(p2)
+    x = np.random.default_rng(4).standard_normal(g.m)
+    assert np.array_equal(g.apply_F(x), f.apply_F(x))
+    assert np.array_equal(g.apply_precond(x), f.apply_precond(x))
+    assert np.array_equal(g.rhs()[0], f.rhs()[0])
+    lg, tg = g.solve(tol=1e-6, max_it=200, directions=2)
+    lf, tf = f.solve(tol=1e-6, max_it=200, directions=2)
+    assert np.array_equal(lg, lf) and tg["iterations"] == tf["iterations"]
+    assert np.array_equal(g.recover(lg), f.recover(lf))
+    g.close()
+    f.close()
+
+
+@pytest.mark.parametrize("method", [0, 1])
+def test_warm_start(method, oracle_mod):
+    """fetigpu_solve_warm: started at the solution the solve stops at once
+    (absolute tolerance); T-FETI projects any warm start onto G lambda = e."""
+    prob = (DESK["C3tf_s"] if method == 0 else DESK["C3dp_s"])()
+    g = _sys(prob)
+    lam, tr = g.solve(tol=1e-10, max_it=500, directions=1)
+    lw, tw = g.solve_warm(lam, tol=10 * tr["eps_final"], rel=False, max_it=500, directions=1)
+    if method == 1:
+        assert tw["iterations"] == 0 and np.array_equal(lw, lam)
+    else:   # the projection lam0 + P(lam - lam0) reproduces lam up to rounding
+        assert tw["iterations"] <= 1
+        assert np.linalg.norm(lw - lam) <= 1e-10 * np.linalg.norm(lam)
+    if method == 0:
+        o = oracle_mod.Oracle(prob)
+        junk = np.random.default_rng(9).standard_normal(g.m)
+        lj, tj = g.solve_warm(junk, tol=1e-8, max_it=500, directions=1)
+        assert o.coarse_residual(lj) < 1e-10
+        assert tj["status"] == 0
+    g.close()
