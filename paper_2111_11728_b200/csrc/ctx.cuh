@@ -264,7 +264,12 @@ struct Ctx {
     if (blk_t.n < (size_t)tot_c * k) blk_t.alloc((size_t)tot_c * k);
     if (blk_T.n < (size_t)su.Nc * k) { blk_T.alloc((size_t)su.Nc * k); blk_U.alloc((size_t)su.Nc * k); }
   }
-  bool apply_F_block_z(const double* Z, double* Q, int k);
+  // Yout / Tout (optional): keep the sparse part Y (nmap x 5) and the coarse
+  // pre-pass T (N_c x k row-major) of F Z for the line-7 correction
+  bool apply_F_block_z(const double* Z, double* Q, int k, double* Yout = nullptr, double* Tout = nullptr);
+  long long bz_nmap = 0;
+  double* bz_tt = nullptr;   // compact T output of the next K5z (set by the solver)
+  DBuf<int> fz_osub, fz_orow;   // coarse-gather owners: subdomain, tbuf row (d_optr order)
 
   // single-vector projector finish: per dual row its <= 2 (s, RT offset) / signs
   DBuf<int2> d_pjrow_sr;

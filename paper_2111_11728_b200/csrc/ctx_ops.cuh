@@ -595,12 +595,23 @@ bool Ctx::bz_prepare() {
   bz_edges.upload(edges, st);
   bz_nedges = (int)edges.size();
   bz_Y.alloc((size_t)std::max<long long>(1, nmap) * kZNb);
+  bz_nmap = nmap;
+  {   // owners of each primal in the coarse gather's order: subdomain and tbuf row
+    std::vector<int> os, orw;
+    for (int pc = 0; pc < su.Nc; ++pc)
+      for (auto& ow : su.c_owners[pc]) {
+        os.push_back(ow.first);
+        orw.push_back(dps[ow.first].t_off + ow.second);
+      }
+    fz_osub.upload(os, st);
+    fz_orow.upload(orw, st);
+  }
   CK(cudaStreamSynchronize(st));
   bz_state = 1;
   return true;
 }
 
-bool Ctx::apply_F_block_z(const double* Z, double* Q, int k) {
+bool Ctx::apply_F_block_z(const double* Z, double* Q, int k, double* Yout, double* Tout) {
   if (k != su.Ns || !bz_prepare()) return false;
   const int Ns = su.Ns, Nc = su.Nc;
   int tot_c = 0;
@@ -609,13 +620,15 @@ bool Ctx::apply_F_block_z(const double* Z, double* Q, int k) {
   CK(cudaMemsetAsync(blk_t.p, 0, (size_t)tot_c * k * 8, st));
   const size_t smem = (size_t)bz_maxns * 20;
   raise_smem_limit(k_bz_local, smem);
+  double* Y = Yout ? Yout : bz_Y.p;
+  double* T = blk_T.p;
   k_bz_local<<<Ns, 256, smem, st>>>(d_op.p, d_dp.p, d_opmat.p, d_oprows.p, d_abc.p, bz_other.p, bz_j.p, bz_nbr.p, Z,
-                                    k, bz_Y.p, blk_t.p, k);
+                                    k, Y, blk_t.p, k, Tout);
   LAUNCH_CHECK();
-  k_coarse_gather_block<<<dim3((k + 255) / 256, Nc), 256, 0, st>>>(d_optr.p, d_oidx.p, blk_t.p, k, Nc, k, blk_T.p, k);
-  gemm(st, false, false, k, Nc, Nc, 1.0, blk_T.p, k, d_Kinv.p, Nc, 0.0, blk_U.p, k);
+  k_coarse_gather_block<<<dim3((k + 255) / 256, Nc), 256, 0, st>>>(d_optr.p, d_oidx.p, blk_t.p, k, Nc, k, T, k);
+  gemm(st, false, false, k, Nc, Nc, 1.0, T, k, d_Kinv.p, Nc, 0.0, blk_U.p, k);
   k_bz_edges<<<dim3((k + kBzCols - 1) / kBzCols, bz_nedges), kBzCols, 0, st>>>(
-      bz_edges.p, bz_erow.p, bz_eb1.p, bz_eb2.p, d_op.p, d_dp.p, d_abc.p, d_cmap.p, bz_nbr.p, bz_Y.p, blk_U.p, k, Q);
+      bz_edges.p, bz_erow.p, bz_eb1.p, bz_eb2.p, d_op.p, d_dp.p, d_abc.p, d_cmap.p, bz_nbr.p, Y, blk_U.p, k, Q);
   LAUNCH_CHECK();
   return true;
 }

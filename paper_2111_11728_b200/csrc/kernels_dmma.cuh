@@ -557,7 +557,7 @@ __global__ void __launch_bounds__(256) k_bz_local(const OpSub* __restrict__ subs
                                                   const double* __restrict__ abc, const int* __restrict__ other,
                                                   const int* __restrict__ jslot, const int* __restrict__ nbr,
                                                   const double* __restrict__ Z, int k, double* __restrict__ Y,
-                                                  double* __restrict__ tbuf, int ldt) {
+                                                  double* __restrict__ tbuf, int ldt, double* __restrict__ tt) {
   extern __shared__ double bzs[];
   const int t = blockIdx.x;
   const OpSub d = subs[t];
@@ -607,6 +607,7 @@ __global__ void __launch_bounds__(256) k_bz_local(const OpSub* __restrict__ subs
       acc = fma(A[(size_t)a * p.nc + c], x, acc);
     }
     tbuf[(size_t)(p.t_off + c) * ldt + s] = acc;
+    if (tt) tt[(size_t)(p.t_off + c) * kZNb + j] = acc;   // compact copy (line-7 correction)
   }
 }
 
@@ -688,6 +689,7 @@ namespace fg {
 // owner sums are added (0 + a + b == a + b), and V = fma(-1, D, V).
 // Requires nl <= kZsMax coordinates blocks (the caller falls back otherwise).
 constexpr int kZsMax = 32;
+constexpr int kZsChunk = 8;     // rows accumulated in registers at a time
 __global__ void __launch_bounds__(kBzCols) k_rrs_zsub_edges(const BzEdge* __restrict__ edges,
                                                             const int* __restrict__ erow,
                                                             const int* __restrict__ ez1, const int* __restrict__ ez2,
@@ -708,23 +710,194 @@ __global__ void __launch_bounds__(kBzCols) k_rrs_zsub_edges(const BzEdge* __rest
   __syncthreads();
   const int c = blockIdx.x * kBzCols + threadIdx.x;
   if (c >= k) return;
-  double n1[kZsMax], n2[kZsMax];
+  const double* N1 = NT + (size_t)e.t1 * k + c;
+  const double* N2 = e.t2 >= 0 ? NT + (size_t)e.t2 * k + c : nullptr;
+  const size_t lstep = (size_t)k * k;
+  // chunks of kZsChunk rows: accumulators in registers, l outer (each
+  // owner's sum stays one fma chain in ascending l), then the rows' V loads
+  // are issued together and V = fma(-1, p1 + p2, V)
+  for (int i0 = 0; i0 < e.cnt; i0 += kZsChunk) {
+    double a1[kZsChunk], a2[kZsChunk];
 #pragma unroll
-  for (int l = 0; l < kZsMax; ++l) {
-    n1[l] = l < nl ? NT[((size_t)l * k + e.t1) * k + c] : 0.0;
-    n2[l] = (l < nl && e.t2 >= 0) ? NT[((size_t)l * k + e.t2) * k + c] : 0.0;
-  }
-  for (int i = 0; i < e.cnt; ++i) {
-    double p1 = 0.0, p2 = 0.0;
+    for (int u = 0; u < kZsChunk; ++u) a1[u] = a2[u] = 0.0;
+    for (int l = 0; l < nl; ++l) {
+      const double n1 = N1[l * lstep], n2 = N2 ? N2[l * lstep] : 0.0;
 #pragma unroll
-    for (int l = 0; l < kZsMax; ++l) {
-      if (l < nl) {
-        p1 = fma(z1[i * nl + l], n1[l], p1);
-        p2 = fma(z2[i * nl + l], n2[l], p2);
+      for (int u = 0; u < kZsChunk; ++u) {
+        const int i = min(i0 + u, e.cnt - 1);
+        a1[u] = fma(z1[i * nl + l], n1, a1[u]);
+        a2[u] = fma(z2[i * nl + l], n2, a2[u]);
       }
     }
-    double* v = V + (size_t)R[i] * k + c;
-    *v = fma(-1.0, p1 + p2, *v);
+    double v[kZsChunk];
+#pragma unroll
+    for (int u = 0; u < kZsChunk; ++u) v[u] = i0 + u < e.cnt ? V[(size_t)R[i0 + u] * k + c] : 0.0;
+#pragma unroll
+    for (int u = 0; u < kZsChunk; ++u)
+      if (i0 + u < e.cnt) V[(size_t)R[i0 + u] * k + c] = fma(-1.0, a1[u] + a2[u], v[u]);
+  }
+}
+
+}  // namespace fg
+
+namespace fg {
+
+// Alg. 1 line 7 without a block F-apply.  After the two CGS passes the new
+// block is V2 = V1 - Zhat N2, and the second pass already applied F to V1
+// (Qb = F V1).  With F Z_l kept from each Z block's K5z apply -- its sparse
+// part Y_l (n_t x 5 per subdomain) and its coarse pre-pass T_l -- linearity
+// gives F V2 = F V1 - sum_l (F Z_l) N2[l], where N2 is the second pass's
+// (roundoff-sized) correction, so the subtraction costs no accuracy.  The
+// coarse part enters as U_c = Kbar^{-1} sum_l T_l N2[l] (GEMMs, caller);
+// this kernel subtracts, per dual row r shared by t1 < t2 (interface-edge
+// groups), the two owners' terms
+//   p_o(c) = sum_l sum_j Y_l,to(b_o, j) N2^T(c, l k + nbr_to(j)) + A''_to(b_o, :) U_c(cmap_to, c)
+// as Q(r, c) = fma(-1, p1 + p2, Q(r, c)).  CTA = (edge group, 32 columns),
+// warp w takes rows w, w + 8, ..; the N2 values of the two owners' five
+// neighbour columns and the U_c rows are staged in shared memory.
+// Coarse part of the correction: T_c^T(c, p) = sum_l sum_{owners t of p}
+// sum_j tt_l(t_off(t) + cp, j) N2^T(c, l k + nbr_t(j)) -- T_l kept in its
+// compact per-subdomain form (n_c x 5 per t: A''_t^T X_l,t) instead of the
+// dense N_c x k matrix.  Owners in the fixed (ascending) order of the coarse
+// gather.  Grid (column tiles, N_c); output column-major k x N_c.
+__global__ void k_fz_coarse(const int* __restrict__ optr, const int* __restrict__ osub,
+                            const int* __restrict__ orow, const int* __restrict__ nbr, const double* __restrict__ tt,
+                            long long ttstride, int nl, const double* __restrict__ NT, int k,
+                            double* __restrict__ TcT) {
+  const int p = blockIdx.y;
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= k) return;
+  double acc = 0.0;
+  for (int q = optr[p]; q < optr[p + 1]; ++q) {
+    const int t = osub[q], row = orow[q];
+    for (int l = 0; l < nl; ++l) {
+      const double* tl = tt + (size_t)l * ttstride + (size_t)row * kZNb;
+#pragma unroll
+      for (int j = 0; j < kZNb; ++j) {
+        const int s = nbr[t * kZNb + j];
+        if (s >= 0) acc = fma(tl[j], NT[((size_t)l * k + s) * k + c], acc);
+      }
+    }
+  }
+  TcT[(size_t)p * k + c] = acc;
+}
+
+constexpr int kFzCols = 64;     // columns per CTA
+constexpr int kFzRows = 64;     // rows per CTA (edge groups are split over grid.z)
+constexpr int kFzL = 2;         // coordinate blocks staged per step
+// 256 threads: thread (column c = tid % 64, row slice q = tid / 64) owns the
+// rows q, q + 4, .. (16 accumulators per owner); per staged coordinate
+// column the two N2 values sit in registers and the Y entries of the rows
+// come from shared memory (warp broadcast).  The coarse rows A''(b, :) and
+// the U_c columns are staged as well.
+__global__ void __launch_bounds__(256) k_fz_correct(const BzEdge* __restrict__ edges, const int* __restrict__ erow,
+                                                    const int* __restrict__ eb1, const int* __restrict__ eb2,
+                                                    const OpSub* __restrict__ subs, const DpSub* __restrict__ dps,
+                                                    const double* __restrict__ abc, const int* __restrict__ cmap,
+                                                    const int* __restrict__ nbr, const double* __restrict__ Yst,
+                                                    long long ystride, int nl, const double* __restrict__ NT,
+                                                    const double* __restrict__ Uc, int k, double* __restrict__ Q) {
+  __shared__ double ys[2][kFzRows][kFzL * kZNb];      // 10 KB
+  __shared__ double ns[2][kFzL * kZNb][kFzCols];      // 10 KB
+  __shared__ double as[2][kFzRows][8], us[2][8][kFzCols];
+  __shared__ int rb[2][kFzRows];
+  const BzEdge e = edges[blockIdx.y];
+  const int r0 = blockIdx.z * kFzRows;
+  if (r0 >= e.cnt) return;
+  const int cnt = min(kFzRows, e.cnt - r0);
+  const int c0 = blockIdx.x * kFzCols;
+  const int tt[2] = {e.t1, e.t2};
+  const OpSub d1 = subs[e.t1];
+  const OpSub d2 = e.t2 >= 0 ? subs[e.t2] : OpSub{0, 0, 0, 0, 0};
+  const DpSub p1d = dps[e.t1];
+  const DpSub p2d = e.t2 >= 0 ? dps[e.t2] : DpSub{0, 0, 0, 0, 0};
+  const int tid = threadIdx.x, tc = tid % kFzCols, tq = tid / kFzCols;
+  for (int i = tid; i < kFzRows; i += blockDim.x) {
+    rb[0][i] = i < cnt ? d1.map_off + eb1[e.e0 + r0 + i] : 0;
+    rb[1][i] = (i < cnt && e.t2 >= 0) ? d2.map_off + eb2[e.e0 + r0 + i] : 0;
+  }
+  for (int q = tid; q < 2 * kFzRows * 8; q += blockDim.x) {
+    const int cc = q % 8, i = (q / 8) % kFzRows, o = q / (8 * kFzRows);
+    const DpSub pd = o == 0 ? p1d : p2d;
+    const int b = (o == 0 ? (i < cnt ? eb1[e.e0 + r0 + i] : 0) : (i < cnt && e.t2 >= 0 ? eb2[e.e0 + r0 + i] : 0));
+    as[o][i][cc] = (i < cnt && cc < pd.nc && (o == 0 || e.t2 >= 0)) ? abc[pd.abc_off + (size_t)b * pd.nc + cc] : 0.0;
+  }
+  for (int q = tid; q < 2 * 8 * kFzCols; q += blockDim.x) {
+    const int c = q % kFzCols, cc = (q / kFzCols) % 8, o = q / (kFzCols * 8);
+    const DpSub pd = o == 0 ? p1d : p2d;
+    us[o][cc][c] = ((o == 0 || e.t2 >= 0) && cc < pd.nc && c0 + c < k)
+                       ? Uc[(size_t)cmap[pd.cmap_off + cc] * k + c0 + c] : 0.0;
+  }
+  double a1[kFzRows / 4], a2[kFzRows / 4];
+#pragma unroll
+  for (int u = 0; u < kFzRows / 4; ++u) a1[u] = a2[u] = 0.0;
+  for (int l0 = 0; l0 < nl; l0 += kFzL) {
+    const int lc = min(kFzL, nl - l0);
+    __syncthreads();
+    // staging with all of a thread's loads in flight before its stores
+    constexpr int NY = 2 * kFzRows * kFzL * kZNb / 256, NN = 2 * kFzL * kZNb * kFzCols / 256;
+    double yv[NY], nv[NN];
+#pragma unroll
+    for (int w = 0; w < NY; ++w) {
+      const int q = tid + w * 256;
+      const int j = q % kZNb, l = (q / kZNb) % kFzL, i = (q / (kZNb * kFzL)) % kFzRows,
+                o = q / (kZNb * kFzL * kFzRows);
+      yv[w] = (i < cnt && l < lc && (o == 0 || e.t2 >= 0))
+                  ? __ldg(Yst + (size_t)(l0 + l) * ystride + (size_t)rb[o][i] * kZNb + j) : 0.0;
+    }
+#pragma unroll
+    for (int w = 0; w < NN; ++w) {
+      const int q = tid + w * 256;
+      const int c = q % kFzCols, j = (q / kFzCols) % kZNb, l = (q / (kFzCols * kZNb)) % kFzL,
+                o = q / (kFzCols * kZNb * kFzL);
+      const int t = tt[o];
+      const int sdm = t >= 0 ? nbr[t * kZNb + j] : -1;
+      nv[w] = (sdm >= 0 && l < lc && c0 + c < k) ? __ldg(NT + ((size_t)(l0 + l) * k + sdm) * k + c0 + c) : 0.0;
+    }
+#pragma unroll
+    for (int w = 0; w < NY; ++w) {
+      const int q = tid + w * 256;
+      const int j = q % kZNb, l = (q / kZNb) % kFzL, i = (q / (kZNb * kFzL)) % kFzRows,
+                o = q / (kZNb * kFzL * kFzRows);
+      ys[o][i][l * kZNb + j] = yv[w];
+    }
+#pragma unroll
+    for (int w = 0; w < NN; ++w) {
+      const int q = tid + w * 256;
+      const int c = q % kFzCols, j = (q / kFzCols) % kZNb, l = (q / (kFzCols * kZNb)) % kFzL,
+                o = q / (kFzCols * kZNb * kFzL);
+      ns[o][l * kZNb + j][c] = nv[w];
+    }
+    __syncthreads();
+    for (int q = 0; q < lc * kZNb; ++q) {
+      const double n1 = ns[0][q][tc], n2 = ns[1][q][tc];
+#pragma unroll
+      for (int u = 0; u < kFzRows / 4; ++u) {
+        a1[u] = fma(ys[0][tq + 4 * u][q], n1, a1[u]);
+        a2[u] = fma(ys[1][tq + 4 * u][q], n2, a2[u]);
+      }
+    }
+  }
+  __syncthreads();
+  const int c = c0 + tc;
+  if (c >= k) return;
+  double qv[kFzRows / 4];
+#pragma unroll
+  for (int u = 0; u < kFzRows / 4; ++u) {
+    const int i = tq + 4 * u;
+    qv[u] = i < cnt ? Q[(size_t)erow[e.e0 + r0 + i] * k + c] : 0.0;
+  }
+#pragma unroll
+  for (int u = 0; u < kFzRows / 4; ++u) {
+    const int i = tq + 4 * u;
+    if (i >= cnt) continue;
+    double x1 = a1[u], x2 = a2[u];
+#pragma unroll
+    for (int cc = 0; cc < 8; ++cc) {
+      x1 = fma(as[0][i][cc], us[0][cc][tc], x1);
+      x2 = fma(as[1][i][cc], us[1][cc][tc], x2);
+    }
+    Q[(size_t)erow[e.e0 + r0 + i] * k + c] = fma(-1.0, x1 + x2, qv[u]);
   }
 }
 

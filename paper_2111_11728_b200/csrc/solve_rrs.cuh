@@ -598,12 +598,18 @@ int Ctx::solve_rrs_implicit(const fetigpu_solve_opts& o, double* lambda_host, fe
   // it the buffers grow by doubling.
   const char* nbz = getenv("FETIGPU_NO_BZ");   // A/B switch: dense K5 / scatter+AXPY paths
   const bool use_bz = !(nbz && nbz[0] == '1') && bz_prepare();
+  // line 7 from the kept F Z_l (k_fz_correct) after two CGS passes
+  const char* nfz = getenv("FETIGPU_NO_FZ");
+  const bool use_fz = use_bz && passes >= 2 && !(nfz && nfz[0] == '1');
+  const long long ystride = use_fz ? bz_nmap * kZNb : 0;
+  const size_t tstride = use_fz ? (size_t)tot_c() * kZNb : 0;   // compact A''^T X per Z block
   int nl_pre = std::max(1, std::min(o.max_it, 32));
   {
     const size_t freeb = dev_free_bytes(&rrs_cache);
     auto need = [&](int nlp) {
       const double kk = (double)k * k;
-      return 8.0 * (5.0 * (nlp + 1) * kk + kk * nlp * (nlp + 1) / 2.0 + (double)nz * (nlp + 1));
+      return 8.0 * (5.0 * (nlp + 1) * kk + kk * nlp * (nlp + 1) / 2.0 + (double)nz * (nlp + 1) +
+                    (double)(ystride + tstride) * (nlp + 1));
     };
     while (nl_pre > 1 && need(nl_pre) > 0.4 * (double)freeb) --nl_pre;
   }
@@ -611,14 +617,21 @@ int Ctx::solve_rrs_implicit(const fetigpu_solve_opts& o, double* lambda_host, fe
   // per-iteration coordinate scratch, grown to (i+1) k x k as i increases
   int zcap = nl_pre + 1;
   ZV.alloc((size_t)nz * zcap);
+  DBuf<double> Yst, Tst;   // F Z_l kept for the line-7 correction (use_fz)
+  if (use_fz) { Yst.alloc((size_t)ystride * zcap); Tst.alloc(tstride * zcap); }
+  auto regrow = [&](DBuf<double>& b, size_t per, int oldc, int newc) {
+    if (!per) return;
+    DBuf<double> b2;
+    b2.alloc(per * newc);
+    CK(cudaMemcpyAsync(b2.p, b.p, per * oldc * 8, cudaMemcpyDeviceToDevice, st));
+    std::swap(b2.p, b.p);
+    std::swap(b2.n, b.n);
+  };
   auto zv_block = [&](int l) {
     if (l >= zcap) {
       const int nc = std::max(l + 1, 2 * zcap);
-      DBuf<double> z2;
-      z2.alloc((size_t)nz * nc);
-      CK(cudaMemcpyAsync(z2.p, ZV.p, (size_t)nz * zcap * 8, cudaMemcpyDeviceToDevice, st));
-      std::swap(z2.p, ZV.p);
-      std::swap(z2.n, ZV.n);
+      regrow(ZV, (size_t)nz, zcap, nc);
+      if (use_fz) { regrow(Yst, (size_t)ystride, zcap, nc); regrow(Tst, tstride, zcap, nc); }
       zcap = nc;
     }
   };
@@ -699,8 +712,22 @@ int Ctx::solve_rrs_implicit(const fetigpu_solve_opts& o, double* lambda_host, fe
     const int i = it;              // stored blocks 0..i-1; W has coordinates CW over Z_0..Z_i
     const int kzi = (i + 1) * k;   // rows of CW
     mark(0);
-    // line 7 (at i = 0, W = Z_0 is a fresh preconditioner block: K5z)
-    if (!(i == 0 && use_bz && apply_F_block_z(W.p, Qb.p, k))) apply_F_block(W.p, k, Qb.p, k, k);
+    // line 7: at i = 0, W = Z_0 is a fresh preconditioner block (K5z); later
+    // F V2 = F V1 - (F Zhat) N2 from the kept F Z_l (k_fz_correct), else K5
+    if (i == 0 && use_bz && apply_F_block_z(W.p, Qb.p, k, use_fz ? Yst.p : nullptr, use_fz ? Tst.p : nullptr)) {
+    } else if (use_fz && i >= 1 && i <= kZsMax) {
+      const int Nc = su.Nc;
+      k_fz_coarse<<<dim3((k + 255) / 256, Nc), 256, 0, st>>>(d_optr.p, fz_osub.p, fz_orow.p, bz_nbr.p, Tst.p,
+                                                             (long long)tstride, i, NT.p, k, blk_T.p);
+      LAUNCH_CHECK();
+      gemm(st, false, false, k, Nc, Nc, 1.0, blk_T.p, k, d_Kinv.p, Nc, 0.0, blk_U.p, k);   // U_c
+      k_fz_correct<<<dim3((k + kFzCols - 1) / kFzCols, bz_nedges, (kBzRows + kFzRows - 1) / kFzRows), 256, 0, st>>>(
+          bz_edges.p, bz_erow.p, bz_eb1.p, bz_eb2.p, d_op.p, d_dp.p, d_abc.p, d_cmap.p, bz_nbr.p, Yst.p, ystride, i,
+          NT.p, blk_U.p, k, Qb.p);
+      LAUNCH_CHECK();
+    } else {
+      apply_F_block(W.p, k, Qb.p, k, k);
+    }
     fapp += k;
     mark(1);
     // line 8 on coordinates: Delta = Q^T W = (Zhat^T Q)^T C_W over Z_0..Z_i --
@@ -777,8 +804,11 @@ int Ctx::solve_rrs_implicit(const fetigpu_solve_opts& o, double* lambda_host, fe
       grow2(XT, (size_t)kz * k); grow2(NT, (size_t)kz * k); grow2(NTot, (size_t)kz * k);
       grow2(CT, (size_t)kz * k); grow2(CW, (size_t)(kz + k) * k);
       for (int p = 0; p < passes; ++p) {
-        // Y = F V; the first pass sees V = Z_it itself (K5z)
-        if (!(p == 0 && use_bz && apply_F_block_z(W.p, Qb.p, k))) apply_F_block(W.p, k, Qb.p, k, k);
+        // Y = F V; the first pass sees V = Z_it itself (K5z, F Z_it kept for line 7)
+        if (!(p == 0 && use_bz &&
+              apply_F_block_z(W.p, Qb.p, k, use_fz ? Yst.p + (size_t)it * ystride : nullptr,
+                              use_fz ? Tst.p + (size_t)it * tstride : nullptr)))
+          apply_F_block(W.p, k, Qb.p, k, k);
         fapp += k;
         k_rrs_zgather<<<dim3(ggrid.x, Ns, (nl + kZL - 1) / kZL), 256, (size_t)max_pcn * (kZL * 8 + 4), st>>>(
             d_pc.p, d_pcrows.p, ZV.p, nz, nl, Qb.p, k, XT.p);
