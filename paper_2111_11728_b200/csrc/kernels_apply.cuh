@@ -1494,3 +1494,185 @@ __global__ void k_fill_random(double* p, size_t n, unsigned long long seed) {
 }
 
 }  // namespace fg
+
+namespace fg {
+
+// ------------------------------- blocked pivoted Cholesky (k > 640) --
+// The right-looking algorithm of k_pivchol_coop1 reorganised into panels of
+// kPcNB pivots without changing a single operation: every entry still
+// receives fma(-L_i, L_j, a) once per pivot, in pivot order.
+//   * panel phase (one CTA, k_pc_panel): for each pivot of the panel, the
+//     largest remaining diagonal (ties -> lowest position) from the running
+//     diagonal d, and the pivot row's current entries computed on the fly:
+//     the stored entry (updated up to the panel start) followed by the
+//     in-panel updates in pivot order -- exactly the values the right-looking
+//     kernel would hold; L column = row / sqrt(d_q), d updated by the same fma;
+//   * trailing phase (grid, k_pc_trailing): every remaining entry of the lower
+//     triangle takes the panel's updates as one fma chain in pivot order.
+// The symmetric matrix is updated in its lower triangle only (the two
+// triangles received identical updates before).  One grid-wide phase per
+// kPcNB pivots instead of a grid barrier per pivot.
+constexpr int kPcNB = 32;
+struct PcCtl {
+  int k;         // pivots done
+  int stop;      // 1: rank found
+  double stop_tol, neg_tol;
+};
+
+__global__ void k_pc_init(const double* __restrict__ A, int n, double tol, int* __restrict__ at,
+                          double* __restrict__ d, PcCtl* ctl) {
+  __shared__ double sv[32];
+  double mx = -1e300;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    at[i] = i;
+    d[i] = A[(size_t)i * n + i];
+    mx = fmax(mx, d[i]);
+  }
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) sv[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m2 = sv[0];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m2 = fmax(m2, sv[w]);
+    ctl->k = 0;
+    ctl->stop = 0;
+    ctl->stop_tol = tol * m2;
+    ctl->neg_tol = -tol * fmax(m2, 1e-300);
+  }
+}
+
+__global__ void __launch_bounds__(1024) k_pc_panel(const double* __restrict__ A, int n, int* __restrict__ atg,
+                                                   double* __restrict__ dg, double* __restrict__ lc, PcCtl* ctl,
+                                                   int* status) {
+  extern __shared__ double pcs[];
+  double* d = pcs;                                    // running diagonal by original index
+  int* at = reinterpret_cast<int*>(d + n);            // original index at position
+  __shared__ double sv[32];
+  __shared__ int si[32];
+  if (ctl->stop) return;
+  const int k0 = ctl->k;
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nwarp = nt >> 5;
+  for (int i = tid; i < n; i += nt) { d[i] = dg[i]; at[i] = atg[i]; }
+  __syncthreads();
+  const double stop_tol = ctl->stop_tol, neg_tol = ctl->neg_tol;
+  const int kend = min(n, k0 + kPcNB);
+  int k = k0;
+  bool stopped = false;
+  for (; k < kend; ++k) {
+    double bv = -1e300;
+    int bi = n;
+    for (int j = k + tid; j < n; j += nt) {
+      const double v = d[at[j]];
+      if (v > bv || (v == bv && j < bi)) { bv = v; bi = j; }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+    }
+    if (lane == 0) { sv[warp] = bv; si[warp] = bi; }
+    __syncthreads();
+    double v = sv[0];
+    int b = si[0];
+    for (int w = 1; w < nwarp; ++w)
+      if (sv[w] > v || (sv[w] == v && si[w] < b)) { v = sv[w]; b = si[w]; }
+    if (!(v > stop_tol)) {
+      for (int j = k + tid; j < n; j += nt)
+        if (d[at[j]] < neg_tol) atomicExch(status, 2);
+      stopped = true;
+      break;
+    }
+    const int q = at[b], qk = at[k];
+    __syncthreads();
+    if (tid == 0) { at[k] = q; at[b] = qk; }
+    __syncthreads();
+    const double l = sqrt(d[q]);
+    const double* lq = lc + q;                        // L(q, k') at lc[k' n + q]
+    for (int p = k + 1 + tid; p < n; p += nt) {
+      const int a = at[p];
+      double x = a > q ? A[(size_t)a * n + q] : A[(size_t)q * n + a];
+      for (int kk = k0; kk < k; ++kk) x = fma(-lc[(size_t)kk * n + a], lq[(size_t)kk * n], x);
+      const double Ls = x / l;
+      lc[(size_t)k * n + a] = Ls;
+      d[a] = fma(-Ls, Ls, d[a]);
+    }
+    if (tid == 0) lc[(size_t)k * n + q] = l;
+    __syncthreads();
+  }
+  for (int i = tid; i < n; i += nt) { dg[i] = d[i]; atg[i] = at[i]; }
+  if (tid == 0) {
+    ctl->k = k;
+    if (stopped || k == n) ctl->stop = 1;
+  }
+}
+
+// trailing update of the remaining lower triangle with the panel [k0, k1):
+// 64 x 64 tiles in ORIGINAL index space (coalesced), 4 x 4 entries per
+// thread; entries of already pivoted rows/columns are skipped (done[] by
+// original index, maintained here from at[]).
+__global__ void __launch_bounds__(256) k_pc_trailing(double* __restrict__ A, int n, const int* __restrict__ at,
+                                                     const double* __restrict__ lc, const PcCtl* ctl, int k0) {
+  __shared__ double Lr[kPcNB][64], Lcs[kPcNB][64];
+  __shared__ unsigned char done_r[64], done_c[64];
+  const int k1 = ctl->k;               // pivots done after the panel
+  if (k1 <= k0) return;                // nothing new (stopped before this panel)
+  const int bi = blockIdx.y, bj = blockIdx.x;
+  if (bj > bi) return;
+  const int r0 = bi * 64, c0 = bj * 64;
+  const int tid = threadIdx.x;
+  // pivoted originals: positions < k1
+  for (int i = tid; i < 64; i += blockDim.x) { done_r[i] = 0; done_c[i] = 0; }
+  __syncthreads();
+  for (int p = tid; p < k1; p += blockDim.x) {
+    const int a = at[p];
+    if (a >= r0 && a < r0 + 64) done_r[a - r0] = 1;
+    if (a >= c0 && a < c0 + 64) done_c[a - c0] = 1;
+  }
+  const int np = k1 - k0;
+  for (int q = tid; q < kPcNB * 64; q += blockDim.x) {
+    const int kk = q >> 6, i = q & 63;
+    Lr[kk][i] = (kk < np && r0 + i < n) ? lc[(size_t)(k0 + kk) * n + r0 + i] : 0.0;
+    Lcs[kk][i] = (kk < np && c0 + i < n) ? lc[(size_t)(k0 + kk) * n + c0 + i] : 0.0;
+  }
+  __syncthreads();
+  const int tr = (tid >> 4) * 4, tcl = (tid & 15) * 4;
+  double e[4][4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int a = r0 + tr + u, b = c0 + tcl + v;
+      e[u][v] = (a < n && b < n && a > b) ? A[(size_t)a * n + b] : 0.0;
+    }
+  for (int kk = 0; kk < np; ++kk) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) e[u][v] = fma(-Lr[kk][tr + u], Lcs[kk][tcl + v], e[u][v]);
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int a = r0 + tr + u, b = c0 + tcl + v;
+      if (a < n && b < n && a > b && !done_r[tr + u] && !done_c[tcl + v]) A[(size_t)a * n + b] = e[u][v];
+    }
+}
+
+// L in pivot order (column c < rank holds rows p >= c), perm and rank: the
+// output layout of k_pivchol_coop1
+__global__ void k_pc_finish(double* __restrict__ A, int n, const int* __restrict__ at, const double* __restrict__ lc,
+                            const PcCtl* ctl, int* perm, int* rank_out) {
+  const int k = ctl->k;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < (long long)k * n;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int c = (int)(idx / n), p = (int)(idx % n);
+    if (p >= c) A[(size_t)c * n + p] = lc[(size_t)c * n + at[p]];
+  }
+  if (blockIdx.x == 0) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) perm[i] = at[i];
+    if (threadIdx.x == 0) *rank_out = k;
+  }
+}
+
+}  // namespace fg

@@ -250,6 +250,27 @@ static bool launch_pivchol_cluster(double* A, int n, double tol, int* perm, int*
 static void launch_pivchol(double* A, int n, double tol, int* perm, int* rank, int* status, int* ctl, double* gx,
                            cudaStream_t st, double* lc = nullptr) {
   if (launch_pivchol_cluster(A, n, tol, perm, rank, status, gx, st)) return;
+  // blocked (panels of kPcNB pivots, one grid-wide trailing phase per panel;
+  // the per-entry arithmetic of k_pivchol_coop1): at[] lives in perm, the
+  // running diagonal and the control block in gx (2n + 64 doubles)
+  static const bool blocked = [] {
+    const char* e = getenv("FETIGPU_PIVCHOL_BLOCKED");
+    return !(e && e[0] == '0');
+  }();
+  if (lc && blocked && (size_t)n * 12 <= 200 * 1024) {
+    double* d = gx;
+    PcCtl* pc = reinterpret_cast<PcCtl*>(gx + n + 8);
+    k_pc_init<<<1, 1024, 0, st>>>(A, n, tol, perm, d, pc);
+    raise_smem_limit(k_pc_panel, (size_t)n * 12);
+    const int nb = (n + 63) / 64;
+    for (int k0 = 0; k0 < n; k0 += kPcNB) {
+      k_pc_panel<<<1, 1024, (size_t)n * 12, st>>>(A, n, perm, d, lc, pc, status);
+      k_pc_trailing<<<dim3(nb, nb), 256, 0, st>>>(A, n, perm, lc, pc, k0);
+    }
+    k_pc_finish<<<grid_for((long long)n * n), kThreads, 0, st>>>(A, n, perm, lc, pc, perm, rank);
+    LAUNCH_CHECK();
+    return;
+  }
   int dev = 0, sms = 0;
   CK(cudaGetDevice(&dev));
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));

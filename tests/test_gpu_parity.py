@@ -392,7 +392,7 @@ def test_floating_tfeti_rank_deficient_coarse(oracle_mod):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("n,deficit", [(1, 0), (5, 0), (32, 3), (96, 7), (160, 0), (161, 3), (300, 20),
-                                       (512, 0), (640, 11), (700, 5), (1024, 0)])
+                                       (512, 0), (640, 11), (700, 5), (1024, 0), (2048, 40)])
 def test_pivoted_cholesky_device(n, deficit, oracle_mod):
     """fetigpu_pivoted_cholesky (linalg.hpp:80) vs the oracle on
     graded PSD Gram matrices of rank n - deficit.  Covers the cluster kernel
@@ -418,6 +418,30 @@ def test_pivoted_cholesky_device(n, deficit, oracle_mod):
     assert cg.shape == co.shape == (257, r)
     # W L~^{-T} amplifies the rounding difference of L by cond(L~) ~ 1e3 here
     assert np.linalg.norm(cg - co) <= 1e-6 * np.linalg.norm(co)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,deficit", [(700, 5), (1500, 0), (2048, 300)])
+def test_pivoted_cholesky_blocked_bitwise(n, deficit):
+    """The blocked panel / trailing pivoted Cholesky (n > 640) reorganises the
+    right-looking k_pivchol_coop1 without changing any per-entry operation:
+    rank, permutation and L are identical bit for bit (one process per
+    variant: FETIGPU_PIVCHOL_BLOCKED is read once)."""
+    import subprocess
+    import sys
+    code = ("import sys, hashlib, numpy as np; sys.path.insert(0, %r);"
+            "from paper_2111_11728_b200 import engine;"
+            "rng = np.random.default_rng(%d); X = rng.standard_normal((%d, %d)) * np.logspace(0, -3, %d);"
+            "A = X @ X.T; p, L, r = engine.pivoted_cholesky(A);"
+            "print(r, hashlib.sha1(p.tobytes() + L.tobytes()).hexdigest())"
+            % (os.path.dirname(os.path.dirname(os.path.abspath(__file__))), n, n, n - deficit, n - deficit))
+    out = {}
+    for v in ("0", "1"):
+        env = dict(os.environ, FETIGPU_PIVCHOL_BLOCKED=v)
+        out[v] = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                                check=True).stdout.split()
+    assert int(out["1"][0]) == n - deficit
+    assert out["0"] == out["1"]
 
 
 @pytest.mark.gpu
