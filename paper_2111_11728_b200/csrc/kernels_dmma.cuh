@@ -785,12 +785,12 @@ __global__ void k_fz_coarse(const int* __restrict__ optr, const int* __restrict_
 constexpr int kFzCols = 64;     // columns per CTA
 constexpr int kFzRows = 64;     // rows per CTA (edge groups are split over grid.z)
 constexpr int kFzL = 2;         // coordinate blocks staged per step
-// 256 threads: thread (column c = tid % 64, row slice q = tid / 64) owns the
-// rows q, q + 4, .. (16 accumulators per owner); per staged coordinate
-// column the two N2 values sit in registers and the Y entries of the rows
-// come from shared memory (warp broadcast).  The coarse rows A''(b, :) and
+// 256 threads: thread (columns tc, tc + 32; row slice tq = tid / 32) owns the
+// rows tq, tq + 8, .. (8 rows x 2 columns per owner); per staged coordinate
+// column the four N2 values sit in registers and the Y entries of the rows
+// come from shared memory (warp broadcast): 20 shared loads per 32 FMAs.  The coarse rows A''(b, :) and
 // the U_c columns are staged as well.
-__global__ void __launch_bounds__(256) k_fz_correct(const BzEdge* __restrict__ edges, const int* __restrict__ erow,
+__global__ void __launch_bounds__(256, 2) k_fz_correct(const BzEdge* __restrict__ edges, const int* __restrict__ erow,
                                                     const int* __restrict__ eb1, const int* __restrict__ eb2,
                                                     const OpSub* __restrict__ subs, const DpSub* __restrict__ dps,
                                                     const double* __restrict__ abc, const int* __restrict__ cmap,
@@ -811,7 +811,7 @@ __global__ void __launch_bounds__(256) k_fz_correct(const BzEdge* __restrict__ e
   const OpSub d2 = e.t2 >= 0 ? subs[e.t2] : OpSub{0, 0, 0, 0, 0};
   const DpSub p1d = dps[e.t1];
   const DpSub p2d = e.t2 >= 0 ? dps[e.t2] : DpSub{0, 0, 0, 0, 0};
-  const int tid = threadIdx.x, tc = tid % kFzCols, tq = tid / kFzCols;
+  const int tid = threadIdx.x, tc = tid % 32, tq = tid / 32;
   for (int i = tid; i < kFzRows; i += blockDim.x) {
     rb[0][i] = i < cnt ? d1.map_off + eb1[e.e0 + r0 + i] : 0;
     rb[1][i] = (i < cnt && e.t2 >= 0) ? d2.map_off + eb2[e.e0 + r0 + i] : 0;
@@ -828,9 +828,9 @@ __global__ void __launch_bounds__(256) k_fz_correct(const BzEdge* __restrict__ e
     us[o][cc][c] = ((o == 0 || e.t2 >= 0) && cc < pd.nc && c0 + c < k)
                        ? Uc[(size_t)cmap[pd.cmap_off + cc] * k + c0 + c] : 0.0;
   }
-  double a1[kFzRows / 4], a2[kFzRows / 4];
+  double a1[kFzRows / 8][2], a2[kFzRows / 8][2];
 #pragma unroll
-  for (int u = 0; u < kFzRows / 4; ++u) a1[u] = a2[u] = 0.0;
+  for (int u = 0; u < kFzRows / 8; ++u) a1[u][0] = a1[u][1] = a2[u][0] = a2[u][1] = 0.0;
   for (int l0 = 0; l0 < nl; l0 += kFzL) {
     const int lc = min(kFzL, nl - l0);
     __syncthreads();
@@ -870,34 +870,40 @@ __global__ void __launch_bounds__(256) k_fz_correct(const BzEdge* __restrict__ e
     }
     __syncthreads();
     for (int q = 0; q < lc * kZNb; ++q) {
-      const double n1 = ns[0][q][tc], n2 = ns[1][q][tc];
+      const double n1a = ns[0][q][tc], n1b = ns[0][q][tc + 32], n2a = ns[1][q][tc], n2b = ns[1][q][tc + 32];
 #pragma unroll
-      for (int u = 0; u < kFzRows / 4; ++u) {
-        a1[u] = fma(ys[0][tq + 4 * u][q], n1, a1[u]);
-        a2[u] = fma(ys[1][tq + 4 * u][q], n2, a2[u]);
+      for (int u = 0; u < kFzRows / 8; ++u) {
+        const double y1 = ys[0][tq + 8 * u][q], y2 = ys[1][tq + 8 * u][q];
+        a1[u][0] = fma(y1, n1a, a1[u][0]);
+        a1[u][1] = fma(y1, n1b, a1[u][1]);
+        a2[u][0] = fma(y2, n2a, a2[u][0]);
+        a2[u][1] = fma(y2, n2b, a2[u][1]);
       }
     }
   }
   __syncthreads();
-  const int c = c0 + tc;
-  if (c >= k) return;
-  double qv[kFzRows / 4];
 #pragma unroll
-  for (int u = 0; u < kFzRows / 4; ++u) {
-    const int i = tq + 4 * u;
-    qv[u] = i < cnt ? Q[(size_t)erow[e.e0 + r0 + i] * k + c] : 0.0;
-  }
+  for (int h = 0; h < 2; ++h) {
+    const int cl = tc + 32 * h, c = c0 + cl;
+    if (c >= k) continue;
+    double qv[kFzRows / 8];
 #pragma unroll
-  for (int u = 0; u < kFzRows / 4; ++u) {
-    const int i = tq + 4 * u;
-    if (i >= cnt) continue;
-    double x1 = a1[u], x2 = a2[u];
-#pragma unroll
-    for (int cc = 0; cc < 8; ++cc) {
-      x1 = fma(as[0][i][cc], us[0][cc][tc], x1);
-      x2 = fma(as[1][i][cc], us[1][cc][tc], x2);
+    for (int u = 0; u < kFzRows / 8; ++u) {
+      const int i = tq + 8 * u;
+      qv[u] = i < cnt ? Q[(size_t)erow[e.e0 + r0 + i] * k + c] : 0.0;
     }
-    Q[(size_t)erow[e.e0 + r0 + i] * k + c] = fma(-1.0, x1 + x2, qv[u]);
+#pragma unroll
+    for (int u = 0; u < kFzRows / 8; ++u) {
+      const int i = tq + 8 * u;
+      if (i >= cnt) continue;
+      double x1 = a1[u][h], x2 = a2[u][h];
+#pragma unroll
+      for (int cc = 0; cc < 8; ++cc) {
+        x1 = fma(as[0][i][cc], us[0][cc][cl], x1);
+        x2 = fma(as[1][i][cc], us[1][cc][cl], x2);
+      }
+      Q[(size_t)erow[e.e0 + r0 + i] * k + c] = fma(-1.0, x1 + x2, qv[u]);
+    }
   }
 }
 
