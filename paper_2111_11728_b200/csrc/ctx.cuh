@@ -285,6 +285,15 @@ struct Ctx {
   // grow-only workspace of the dense algebra (split-K partials, triangular
   // inverse, GEMV segment partials)
   double* dla_ws(size_t n) { return grow(ws_dla, std::max<size_t>(n, 1)); }
+  // ||x||^2 of a long block into the device scalar out (k_norm2)
+  DBuf<double> nrm_part;
+  DBuf<unsigned int> nrm_cnt;
+  void block_norm2(const double* x, size_t n, double* out) {
+    constexpr int kBlocks = 148 * 4;
+    if (nrm_part.n < kBlocks) { nrm_part.alloc(kBlocks); nrm_cnt.alloc(1); nrm_cnt.zero(st); }
+    k_norm2<<<kBlocks, 256, 0, st>>>(x, n, nrm_part.p, nrm_cnt.p, out);
+    LAUNCH_CHECK();
+  }
 
   // v <- P v for a row-major block (m x ncols, ld = ncols), T-FETI only
   void project_rm(double* v, int ncols);

@@ -592,6 +592,34 @@ static void gemv_cm_t_tall(cudaStream_t st, int M, int N, const double* A, long 
   LAUNCH_CHECK();
 }
 
+// out = sum_i x_i^2 over size_t lengths, deterministic (fixed grid, block
+// partials summed in order by the last block)
+__global__ void __launch_bounds__(256) k_norm2(const double* __restrict__ x, size_t n, double* __restrict__ part,
+                                               unsigned int* __restrict__ cnt, double* __restrict__ out) {
+  __shared__ double red[8];
+  __shared__ bool last;
+  double s = 0.0;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    s = fma(x[i], x[i], s);
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < 8; ++w) t += red[w];
+    part[blockIdx.x] = t;
+    __threadfence();
+    last = atomicAdd(cnt, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    double t = 0.0;
+    for (unsigned b = 0; b < gridDim.x; ++b) t += __ldcg(part + b);
+    *out = t;
+    *cnt = 0;
+  }
+}
+
 // y += a x over size_t lengths
 __global__ void k_axpy_n(size_t n, double a, const double* __restrict__ x, double* __restrict__ y) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)

@@ -654,6 +654,11 @@ int Ctx::solve_rrs_implicit(const fetigpu_solve_opts& o, double* lambda_host, fe
   const char* nfz = getenv("FETIGPU_NO_FZ");
   const bool use_fz = use_bz && passes >= 2 && !(nfz && nfz[0] == '1');
   const long long ystride = use_fz ? bz_nmap * kZNb : 0;
+  const char* nfz2 = getenv("FETIGPU_NO_FZ2");
+  const bool use_fz2 = use_fz && !(nfz2 && nfz2[0] == '1');
+  DBuf<double> dnorm;
+  dnorm.alloc(2);
+  int n_fz2 = 0, n_k5_2 = 0;
   const size_t tstride = use_fz ? (size_t)tot_c() * kZNb : 0;   // compact A''^T X per Z block
   int nl_pre = std::max(1, std::min(o.max_it, 32));
   {
@@ -839,8 +844,8 @@ int Ctx::solve_rrs_implicit(const fetigpu_solve_opts& o, double* lambda_host, fe
     if (trace_on) {
       float te = 0;
       CK(cudaEventElapsedTime(&te, ev0, pev[6]));
-      fprintf(stderr, "[fetigpu] rrs-implicit it %4d  eps/eps0 %.3e  rank %5d  K %7d  t %9.1f ms\n", it,
-              eps / eps0, rank, K, te);
+      fprintf(stderr, "[fetigpu] rrs-implicit it %4d  eps/eps0 %.3e  rank %5d  K %7d  t %9.1f ms  (pass-2 F: %d kept-FZ, %d K5)\n",
+              it, eps / eps0, rank, K, te, n_fz2, n_k5_2);
     }
     if (eps <= target || it >= o.max_it) {  // no next block needed
       mark(7);
@@ -856,12 +861,34 @@ int Ctx::solve_rrs_implicit(const fetigpu_solve_opts& o, double* lambda_host, fe
       grow2(XT, (size_t)kz * k); grow2(NT, (size_t)kz * k); grow2(NTot, (size_t)kz * k);
       grow2(CT, (size_t)kz * k); grow2(CW, (size_t)(kz + k) * k);
       for (int p = 0; p < passes; ++p) {
-        // Y = F V; the first pass sees V = Z_it itself (K5z, F Z_it kept for line 7)
-        if (!(p == 0 && use_bz &&
-              apply_F_block_z(W.p, Qb.p, k, use_fz ? Yst.p + (size_t)it * ystride : nullptr,
-                              use_fz ? Tst.p + (size_t)it * tstride : nullptr)))
+        // Y = F V; the first pass sees V = Z_it itself (K5z, F Z_it kept for line 7).
+        // Later passes: F V_p = F V_{p-1} - (F Zhat) N_{p-1} from the kept F Z_l
+        // when the previous pass removed at most 3/4 of the block's norm
+        // (||V_p|| >= ||V_{p-1}|| / 2, so the subtraction's rounding stays at
+        // the level of a direct apply); otherwise the block apply (K5).
+        bool fz_pass = false;
+        if (p > 0 && use_fz && use_fz2 && nl <= kZsMax) {
+          double hn[2];
+          CK(cudaMemcpyAsync(hn, dnorm.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+          CK(cudaStreamSynchronize(st));
+          fz_pass = hn[1] >= 0.25 * hn[0];
+          ++(fz_pass ? n_fz2 : n_k5_2);
+        }
+        if (fz_pass) {
+          k_fz_coarse<<<dim3((k + 255) / 256, su.Nc), 256, 0, st>>>(d_optr.p, fz_osub.p, fz_orow.p, bz_nbr.p, Tst.p,
+                                                                    (long long)tstride, nl, NT.p, k, blk_T.p);
+          gemm(st, false, false, k, su.Nc, su.Nc, 1.0, blk_T.p, k, d_Kinv.p, su.Nc, 0.0, blk_U.p, k);
+          k_fz_correct<<<dim3((k + kFzCols - 1) / kFzCols, bz_nedges, (kBzRows + kFzRows - 1) / kFzRows), 256, 0,
+                         st>>>(bz_edges.p, bz_erow.p, bz_eb1.p, bz_eb2.p, d_op.p, d_dp.p, d_abc.p, d_cmap.p,
+                               bz_nbr.p, Yst.p, ystride, nl, NT.p, blk_U.p, k, Qb.p);
+          LAUNCH_CHECK();
+        } else if (!(p == 0 && use_bz &&
+                     apply_F_block_z(W.p, Qb.p, k, use_fz ? Yst.p + (size_t)it * ystride : nullptr,
+                                     use_fz ? Tst.p + (size_t)it * tstride : nullptr))) {
           apply_F_block(W.p, k, Qb.p, k, k);
+        }
         fapp += k;
+        if (use_fz2 && p + 1 < passes) block_norm2(W.p, (size_t)m * k, dnorm.p);   // ||V_p||^2
         k_rrs_zgather<<<dim3(ggrid.x, Ns, (nl + kZL - 1) / kZL), 128, (size_t)max_pcn * (kZL * 8 + 4), st>>>(
             d_pc.p, d_pcrows.p, ZV.p, nz, nl, Qb.p, k, XT.p);
         LAUNCH_CHECK();
@@ -894,6 +921,7 @@ int Ctx::solve_rrs_implicit(const fetigpu_solve_opts& o, double* lambda_host, fe
           LAUNCH_CHECK();
           axpy(st, (size_t)m * k, -1.0, Dd.p, W.p);
         }
+        if (use_fz2 && p + 1 < passes) block_norm2(W.p, (size_t)m * k, dnorm.p + 1);   // ||V_{p+1}||^2
         if (p == 0) CK(cudaMemcpyAsync(NTot.p, NT.p, (size_t)kz * k * 8, cudaMemcpyDeviceToDevice, st));
         else axpy(st, (size_t)kz * k, 1.0, NT.p, NTot.p);
       }
