@@ -139,6 +139,31 @@ class DualSystem {
     }
     return lam;
   }
+  // pcg / simultaneous_pcg from lambda0 (the SIMP loop's warm start)
+  std::vector<double> solve_warm(const SolveOptions& o, const std::vector<double>& lambda0,
+                                 ConvergenceTrace* tr = nullptr) {
+    fetigpu_solve_opts so{o.tol, o.relative ? 1 : 0, o.max_iterations, o.directions, o.pivot_tol,
+                          o.reorth_passes};
+    std::vector<double> lam(m_);
+    const int cap = o.max_iterations + 2;
+    std::vector<double> eps(cap);
+    std::vector<int> kept(cap), fap(cap);
+    fetigpu_trace t{0, 0, 0, 0.0, 0.0, cap, eps.data(), kept.data(), fap.data(), 0.0, {}};
+    check(fetigpu_solve_warm(ctx_, &so, lambda0.data(), lam.data(), &t));
+    if (tr) {
+      tr->status = t.status;
+      tr->iterations = t.iterations;
+      tr->f_applies = t.f_applies;
+      tr->eps_r.assign(eps.begin(), eps.begin() + t.iterations + 1);
+      tr->kept_dirs.assign(kept.begin(), kept.begin() + t.iterations + 1);
+      tr->cum_f_applies.assign(fap.begin(), fap.begin() + t.iterations + 1);
+      tr->solve_ms = t.solve_ms;
+    }
+    return lam;
+  }
+  // next density snapshot of the same problem in place (mbb_modular_snapshot
+  // loop): operators rebuilt in the existing device storage
+  void rebuild(const fetigpu_problem& p) { check(fetigpu_rebuild(ctx_, &p)); }
   // RRS direction store (FETIGPU_RRS_STORE_AUTO / _EXPLICIT / _IMPLICIT, fetigpu.h);
   // the reference has no counterpart (it always stores W_j, Q_j densely)
   void set_rrs_store(int mode) { check(fetigpu_set_rrs_store(ctx_, mode)); }

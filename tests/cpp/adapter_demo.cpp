@@ -38,6 +38,15 @@ int main() {
     auto lam = sys.solve(o, &tr);
     auto u = sys.recover_primal(lam);
     std::printf("solve status %d iterations %d tip uy %.6e\n", tr.status, tr.iterations, u[1][2 * n + 1]);
+    // SIMP-loop use: next density snapshot in place, warm-started solve
+    std::vector<double> rho2(rho.size());
+    for (size_t i = 0; i < rho.size(); ++i) rho2[i] = 0.5 * rho[i] + 0.25;
+    fetigpu_problem p2 = p;
+    p2.densities = rho2.data();
+    sys.rebuild(p2);
+    fetigpu::ConvergenceTrace tr2;
+    auto lam2 = sys.solve_warm(o, lam, &tr2);
+    std::printf("rebuild + warm solve status %d iterations %d\n", tr2.status, tr2.iterations);
     // pivoted_cholesky / PivotedCholesky::compress (linalg.hpp:72-89)
     std::vector<double> a{1.0, 2.0, 2.0, 4.0 + 1e-3};  // 2x2 column-major, pivot 1 first
     auto pc = fetigpu::pivoted_cholesky(a, 2);
@@ -45,7 +54,7 @@ int main() {
     auto c = pc.compress(w, 2);
     std::printf("pivchol rank %d perm %d %d L00 %.6f compress %zu\n", pc.rank, pc.permutation[0],
                 pc.permutation[1], pc.lower[0], c.size());
-    return tr.status == 0 && pc.rank == 2 && pc.permutation[0] == 1 ? 0 : 3;
+    return tr.status == 0 && tr2.status == 0 && pc.rank == 2 && pc.permutation[0] == 1 ? 0 : 3;
   } catch (const std::exception& e) {
     std::printf("exception: %s\n", e.what());
     return 2;

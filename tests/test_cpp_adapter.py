@@ -34,4 +34,5 @@ def test_adapter_gpu(tmp_path):
     r = subprocess.run([str(exe)], capture_output=True, text=True)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "solve status 0" in r.stdout
+    assert "rebuild + warm solve status 0" in r.stdout
     assert "pivchol rank 2 perm 1 0 L00 2.000250" in r.stdout
