@@ -267,6 +267,24 @@ struct Ctx {
   // Yout / Tout (optional): keep the sparse part Y (nmap x 5) and the coarse
   // pre-pass T (N_c x k row-major) of F Z for the line-7 correction
   bool apply_F_block_z(const double* Z, double* Q, int k, double* Yout = nullptr, double* Tout = nullptr);
+  // Q -= (F Zhat) N from the kept F Z_l (K14): DMMA form by default,
+  // FETIGPU_FZ_FMA=1 selects the fma-chain kernel
+  void launch_fz_correct(const double* Yst, long long ystride, int nl, const double* NT, const double* Uc, int k,
+                         double* Q) {
+    static const bool fma_form = [] {
+      const char* e = getenv("FETIGPU_FZ_FMA");
+      return e && e[0] == '1';
+    }();
+    if (fma_form || (k & 1))   // the DMMA form's 16-byte B rows need an even k
+      k_fz_correct<<<dim3((k + kFzCols - 1) / kFzCols, bz_nedges, (kBzRows + kFzRows - 1) / kFzRows), 256, 0, st>>>(
+          bz_edges.p, bz_erow.p, bz_eb1.p, bz_eb2.p, d_op.p, d_dp.p, d_abc.p, d_cmap.p, bz_nbr.p, Yst, ystride, nl, NT,
+          Uc, k, Q);
+    else
+      k_fz_correct_mma<<<dim3((k + kFmBN - 1) / kFmBN, bz_nedges, (kBzRows + kFmBM - 1) / kFmBM), 128, 0, st>>>(
+          bz_edges.p, bz_erow.p, bz_eb1.p, bz_eb2.p, d_op.p, d_dp.p, d_abc.p, d_cmap.p, bz_nbr.p, Yst, ystride, nl,
+          NT, Uc, k, Q);
+    LAUNCH_CHECK();
+  }
   long long bz_nmap = 0;
   double* bz_tt = nullptr;   // compact T output of the next K5z (set by the solver)
   DBuf<int> fz_osub, fz_orow;   // coarse-gather owners: subdomain, tbuf row (d_optr order)

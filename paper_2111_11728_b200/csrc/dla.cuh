@@ -273,6 +273,10 @@ static void gemm_cfg(int cfg, const GemmArgs& a, int batch, cudaStream_t st) {
     case 1: gemm_launch<128, 64, 16, 32, 32, 3, TA, TB>(a, batch, st); break;
     case 2: gemm_launch<64, 64, 16, 32, 32, 3, TA, TB>(a, batch, st); break;
     case 3: gemm_launch<64, 64, 16, 32, 32, 2, TA, TB>(a, batch, st); break;
+    case 4: gemm_launch<64, 64, 32, 32, 64, 2, TA, TB>(a, batch, st); break;
+    case 5: gemm_launch<64, 128, 32, 32, 64, 2, TA, TB>(a, batch, st); break;
+    case 6: gemm_launch<128, 64, 32, 64, 32, 2, TA, TB>(a, batch, st); break;
+    case 7: gemm_launch<64, 64, 16, 32, 64, 3, TA, TB>(a, batch, st); break;
     default: gemm_launch<64, 64, 32, 32, 32, 2, TA, TB>(a, batch, st); break;
   }
 }

@@ -907,4 +907,137 @@ __global__ void __launch_bounds__(256, 2) k_fz_correct(const BzEdge* __restrict_
   }
 }
 
+// DMMA form of k_fz_correct: per (edge group, 64 rows, 64 columns) the
+// correction is a small GEMM  Q[rows, cols] -= A (rows x K) B (K x cols) with
+// K = 10 nl (both owners' Y_l entries against the N2 rows of their neighbour
+// slots) + 16 (A''(b, :) against the U_c rows of their primal DOFs).  A is
+// gathered element-wise and B row-wise (16-byte) with cp.async into a 2-stage
+// ring; 4 warps of 32 x 32 on mma.sync.m8n8k4.f64.  The sum over K runs in DMMA
+// order (not the fma chain of k_fz_correct): equal to it up to rounding.
+constexpr int kFmBM = 64, kFmBN = 64, kFmBK = 16;
+__global__ void __launch_bounds__(128) k_fz_correct_mma(const BzEdge* __restrict__ edges,
+                                                        const int* __restrict__ erow, const int* __restrict__ eb1,
+                                                        const int* __restrict__ eb2, const OpSub* __restrict__ subs,
+                                                        const DpSub* __restrict__ dps, const double* __restrict__ abc,
+                                                        const int* __restrict__ cmap, const int* __restrict__ nbr,
+                                                        const double* __restrict__ Yst, long long ystride, int nl,
+                                                        const double* __restrict__ NT, const double* __restrict__ Uc,
+                                                        int k, double* __restrict__ Q) {
+  constexpr int AP = kFmBK + 4, BP = kFmBN + 8;
+  __shared__ __align__(16) double As[2][kFmBM * AP];
+  __shared__ __align__(16) double Bs[2][kFmBK * BP];
+  __shared__ long long arow[2][kFmBM];     // Y row offsets (map_off + b) * 5 per owner, -1 if none
+  __shared__ long long aabc[2][kFmBM];     // A'' row offsets per owner
+  __shared__ int R[kFmBM];
+  const BzEdge e = edges[blockIdx.y];
+  const int r0 = blockIdx.z * kFmBM;
+  if (r0 >= e.cnt) return;
+  const int cnt = min(kFmBM, e.cnt - r0);
+  const int c0 = blockIdx.x * kFmBN;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wr = warp >> 1, wc = warp & 1;
+  const int tt[2] = {e.t1, e.t2};
+  DpSub pd[2];
+  pd[0] = dps[e.t1];
+  pd[1] = e.t2 >= 0 ? dps[e.t2] : DpSub{0, 0, 0, 0, 0};
+  for (int i = tid; i < kFmBM; i += blockDim.x) {
+    const bool ok = i < cnt;
+    const int b1 = ok ? eb1[e.e0 + r0 + i] : 0, b2 = ok ? eb2[e.e0 + r0 + i] : 0;
+    arow[0][i] = ok ? (long long)(subs[e.t1].map_off + b1) * kZNb : -1;
+    arow[1][i] = (ok && e.t2 >= 0) ? (long long)(subs[e.t2].map_off + b2) * kZNb : -1;
+    aabc[0][i] = ok ? pd[0].abc_off + (long long)b1 * pd[0].nc : -1;
+    aabc[1][i] = (ok && e.t2 >= 0) ? pd[1].abc_off + (long long)b2 * pd[1].nc : -1;
+    R[i] = ok ? erow[e.e0 + r0 + i] : 0;
+  }
+  __syncthreads();
+  const int Ky = 2 * kZNb * nl;                     // K index q < Ky: (l, o, j) = (q / 10, (q / 5) % 2, q % 5)
+  const int Kt = Ky + 16;                           // then 16 coarse columns (o, cc)
+  const int nk = (Kt + kFmBK - 1) / kFmBK;
+  auto issue = [&](int t) {
+    const int k0 = t * kFmBK, st = t & 1;
+    // A: 64 rows x 16 K, element-wise
+#pragma unroll
+    for (int w = 0; w < kFmBM * kFmBK / 128; ++w) {
+      const int idx = tid + w * 128, i = idx / kFmBK, kk = idx % kFmBK, q = k0 + kk;
+      const double* src = Yst;
+      bool ok = false;
+      if (q < Ky) {
+        const int l = q / (2 * kZNb), o = (q / kZNb) & 1, j = q % kZNb;
+        const long long ro = arow[o][i];
+        ok = ro >= 0;
+        if (ok) src = Yst + (size_t)l * ystride + ro + j;
+      } else if (q < Kt) {
+        const int o = (q - Ky) >> 3, cc = (q - Ky) & 7;
+        const long long ao = aabc[o][i];
+        ok = ao >= 0 && cc < pd[o].nc;
+        if (ok) src = abc + ao + cc;
+      }
+      cp_async8(&As[st][i * AP + kk], src, ok);
+    }
+    // B: 16 K rows x 64 columns, 16-byte chunks
+#pragma unroll
+    for (int w = 0; w < kFmBK * (kFmBN / 2) / 128; ++w) {
+      const int idx = tid + w * 128, kk = idx / (kFmBN / 2), c2 = (idx % (kFmBN / 2)) * 2, q = k0 + kk;
+      const int c = c0 + c2;
+      const double* src = NT;
+      bool ok = false;
+      if (c < k) {
+        if (q < Ky) {
+          const int l = q / (2 * kZNb), o = (q / kZNb) & 1, j = q % kZNb;
+          const int t = tt[o];
+          const int sdm = t >= 0 ? nbr[t * kZNb + j] : -1;
+          ok = sdm >= 0;
+          if (ok) src = NT + ((size_t)l * k + sdm) * k + c;
+        } else if (q < Kt) {
+          const int o = (q - Ky) >> 3, cc = (q - Ky) & 7;
+          ok = tt[o] >= 0 && cc < pd[o].nc;
+          if (ok) src = Uc + (size_t)cmap[pd[o].cmap_off + cc] * k + c;
+        }
+      }
+      cp_async16(&Bs[st][kk * BP + c2], src, ok);
+    }
+  };
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  issue(0);
+  cp_async_commit();
+  for (int t = 0; t < nk; ++t) {
+    if (t + 1 < nk) issue(t + 1);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    const double* A_ = As[t & 1];
+    const double* B_ = Bs[t & 1];
+#pragma unroll
+    for (int k4 = 0; k4 < kFmBK; k4 += 4) {
+      double af[4], bf[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) af[i] = A_[(wr * 32 + i * 8 + (lane >> 2)) * AP + k4 + (lane & 3)];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bf[j] = B_[(k4 + (lane & 3)) * BP + wc * 32 + j * 8 + (lane >> 2)];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+    __syncthreads();
+  }
+  cp_async_wait<0>();
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int li = wr * 32 + i * 8 + (lane >> 2);
+    if (li >= cnt) continue;
+    double* qrow = Q + (size_t)R[li] * k;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int c = c0 + wc * 32 + j * 8 + 2 * (lane & 3);
+      if (c < k) qrow[c] -= acc[i][j][0];
+      if (c + 1 < k) qrow[c + 1] -= acc[i][j][1];
+    }
+  }
+}
+
 }  // namespace fg

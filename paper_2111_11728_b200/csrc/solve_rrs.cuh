@@ -778,9 +778,7 @@ int Ctx::solve_rrs_implicit(const fetigpu_solve_opts& o, double* lambda_host, fe
                                                              (long long)tstride, i, NT.p, k, blk_T.p);
       LAUNCH_CHECK();
       gemm(st, false, false, k, Nc, Nc, 1.0, blk_T.p, k, d_Kinv.p, Nc, 0.0, blk_U.p, k);   // U_c
-      k_fz_correct<<<dim3((k + kFzCols - 1) / kFzCols, bz_nedges, (kBzRows + kFzRows - 1) / kFzRows), 256, 0, st>>>(
-          bz_edges.p, bz_erow.p, bz_eb1.p, bz_eb2.p, d_op.p, d_dp.p, d_abc.p, d_cmap.p, bz_nbr.p, Yst.p, ystride, i,
-          NT.p, blk_U.p, k, Qb.p);
+      launch_fz_correct(Yst.p, ystride, i, NT.p, blk_U.p, k, Qb.p);
       LAUNCH_CHECK();
     } else {
       apply_F_block(W.p, k, Qb.p, k, k);
@@ -878,9 +876,7 @@ int Ctx::solve_rrs_implicit(const fetigpu_solve_opts& o, double* lambda_host, fe
           k_fz_coarse<<<dim3((k + 255) / 256, su.Nc), 256, 0, st>>>(d_optr.p, fz_osub.p, fz_orow.p, bz_nbr.p, Tst.p,
                                                                     (long long)tstride, nl, NT.p, k, blk_T.p);
           gemm(st, false, false, k, su.Nc, su.Nc, 1.0, blk_T.p, k, d_Kinv.p, su.Nc, 0.0, blk_U.p, k);
-          k_fz_correct<<<dim3((k + kFzCols - 1) / kFzCols, bz_nedges, (kBzRows + kFzRows - 1) / kFzRows), 256, 0,
-                         st>>>(bz_edges.p, bz_erow.p, bz_eb1.p, bz_eb2.p, d_op.p, d_dp.p, d_abc.p, d_cmap.p,
-                               bz_nbr.p, Yst.p, ystride, nl, NT.p, blk_U.p, k, Qb.p);
+          launch_fz_correct(Yst.p, ystride, nl, NT.p, blk_U.p, k, Qb.p);
           LAUNCH_CHECK();
         } else if (!(p == 0 && use_bz &&
                      apply_F_block_z(W.p, Qb.p, k, use_fz ? Yst.p + (size_t)it * ystride : nullptr,

@@ -58,3 +58,16 @@ def test_presets():
     assert (inc.sx, inc.sy) == (4, 4) and d[0].sum() == 0 and d[:, 0].sum() == 0   # inclusion off the boundary
     with pytest.raises(ValueError):
         pb.laminated_beam(n=10)
+
+
+def test_bench_stream_bytes_and_shared_config():
+    """bench.py: the headline byte count (symmetric storage, SURVEY 8d layout)
+    and the config dict both arms print (same workload, same constant)."""
+    import bench
+    w = bench.c4_work()
+    assert w["bytes"] == 4279246848.0                 # SURVEY App. A full-storage formula
+    assert w["packed_main_bytes"] == 2190999552.0     # the packed kernel's bytes per launch
+    assert w["stream_bytes"] == 2407302912.0
+    assert w["m"] == 504000 and w["n_c"] == 4224
+    c1, c2 = bench.c4_config(), bench.c4_config()
+    assert c1 == c2 and c1["value_bytes_per_apply"] == w["stream_bytes"]

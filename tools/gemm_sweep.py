@@ -18,6 +18,6 @@ if len(sys.argv) > 1:   # child: one config
     print(json.dumps(out), flush=True)
 else:
     env = dict(os.environ)
-    for cfg in range(4):
+    for cfg in range(8):
         env["FETIGPU_GEMM_CFG"] = str(cfg)
         subprocess.run([sys.executable, __file__, str(cfg)], env=env)
