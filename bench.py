@@ -519,13 +519,17 @@ def main():
         bms = (C.c_double * 1)()
         engine.check(L.fetigpu_time_apply_block(g.h, Wp, Qp, k, 1, bms))      # warm-up
         barrier(dist)
-        engine.check(L.fetigpu_time_apply_block(g.h, Wp, Qp, k, args.block_reps, bms))
+        with ClockSampler(local) as bclk:
+            engine.check(L.fetigpu_time_apply_block(g.h, Wp, Qp, k, args.block_reps, bms))
         t_blk = max_over_ranks(dist, bms[0])
         dmma, dfma = engine.fp64_peak()
         flops = st["op_flops_per_col"] * k
         tf = flops / (t_blk * 1e-3) / 1e12
         block = {"k": k, "ms": t_blk, "flops": flops, "tflops": tf * ws, "peak_dmma_tflops": dmma,
-                 "peak_dfma_tflops": dfma, "frac": tf / dmma, "peak_kind": "measured (fetigpu_fp64_peak)",
+                 "peak_dfma_tflops": dfma, "frac": tf / dmma,
+                 "peak_kind": "measured on this device by fetigpu_fp64_peak (independent DMMA.8x8x4 from "
+                              "registers, all SMs); MEASURED_PEAKS.json has no FP64 figure; datasheet 40",
+                 "clocks": bclk.summary(),
                  "kernel": "k_block_apply_dp2<64,64,16,2> (DMMA m8n8k4, fused W-row gather and Q scatter) + coarse pre-pass + DMMA GEMM (dla.cuh) for U = Kbar^-1 T"}
         L.fetigpu_device_free(g.h, dW)
         L.fetigpu_device_free(g.h, dQ)
