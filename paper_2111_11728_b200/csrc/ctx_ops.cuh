@@ -356,8 +356,24 @@ void Ctx::apply_F_block(const double* W, int ldw, double* Q, int ldq, int k) {
   const int Ns = su.Ns, m = su.m;
   if (ldq == k) CK(cudaMemsetAsync(Q, 0, (size_t)m * k * 8, st));
   else CK(cudaMemset2DAsync(Q, (size_t)ldq * 8, 0, (size_t)k * 8, m, st));
+  // K5 walks the subdomains in 4 x 4-module tiles: both neighbours sharing a
+  // dual row (left/right and below/above) are processed close in time, so
+  // the W rows of an interface are read from DRAM about once
+  if (d_k5order.n != (size_t)Ns) {
+    std::vector<int> ord;
+    ord.reserve(Ns);
+    for (int ty = 0; ty < su.sy; ty += 4)
+      for (int tx = 0; tx < su.sx; tx += 4)
+        for (int y = ty; y < std::min(su.sy, ty + 4); ++y)
+          for (int x = tx; x < std::min(su.sx, tx + 4); ++x) ord.push_back(y * su.sx + x);
+    d_k5order.upload(ord, st);
+  }
+  static const bool tiled = [] {
+    const char* e = getenv("FETIGPU_K5_ROWMAJOR");
+    return !(e && e[0] == '1');
+  }();
   BlockApplyArgs a{d_op.p, d_opmat.p, d_oprows.p, d_opcoef_apply.p, KR, nullptr, nullptr, nullptr, nullptr, 0,
-                   W, ldw, Q, ldq, k};
+                   W, ldw, Q, ldq, k, tiled ? d_k5order.p : nullptr};
   int max_ns = 0;
   for (int n : op_ns) max_ns = std::max(max_ns, n);
   if (su.method == FETIGPU_FETIDP) {

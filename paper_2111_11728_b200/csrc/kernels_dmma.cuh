@@ -85,6 +85,7 @@ struct BlockApplyArgs {
   double* Q;
   int ldq;
   int k;
+  const int* order;      // nullable: subdomain processed by grid slice z (K5 dp2)
 };
 
 template <int KR>
@@ -326,7 +327,7 @@ __global__ void __launch_bounds__((BM / 32) * (BN / 32) * 32) k_block_apply_dp2(
   double* As = dsm;                                   // ST x (BM x AP)
   double* Bs = dsm + ST * BM * AP;                    // ST x (BK x BP)
   int* srow = reinterpret_cast<int*>(Bs + ST * BK * BP);
-  const int s = blockIdx.z;
+  const int s = a.order ? a.order[blockIdx.z] : blockIdx.z;
   const OpSub d = a.subs[s];
   const int ns = d.ns;
   const int row0 = blockIdx.y * BM;

@@ -9,10 +9,12 @@ displacements GPU-vs-oracle 5.5e-4 against oracle-vs-refined 5.3e-3.
 * C2 (BASELINE configs[1], single direction as configured): the GPU's
   iteration count lies within the oracle's own last-bit spread of the
   oracle's median (see the test);
-* C3 FETI-DP FO, C3 T-FETI FO and C5 RRS: ||u_gpu - u_oracle|| <=
+* C3 FETI-DP FO and C3 T-FETI FO: ||u_gpu - u_oracle|| <=
   max(||u_oracle - u_refined||, 1e-8) (relative L2), and iteration counts
-  within +-1 of the oracle (FO / RRS).
-C3 T-FETI (about 3 min of CPU oracle time) and C5 (about 25 min) are marked
+  within +-1 of the oracle;
+* C5 RRS: the dual energy of the GPU's lambda is at least as low as the
+  oracle's (the refined oracle's RRS breaks down on C5).
+C3 T-FETI (about 4 min of CPU oracle time) and C5 (about 12 min) are marked
 slow (FETIGPU_SLOW_TESTS=1).
 """
 import numpy as np
@@ -94,5 +96,26 @@ def test_c3_tfeti_fo_displacements_within_spread(oracle_mod):
 
 
 @pytest.mark.slow
-def test_c5_rrs_displacements_within_spread(oracle_mod):
-    _displacement_spread("C5 RRS", pb.config5(), oracle_mod, 2, 200)
+def test_c5_rrs_energy_vs_oracle(oracle_mod):
+    """Full C5 (1e9 contrast, 0/1 designs) with RRS.  The refined oracle's RRS
+    breaks down there (a roundoff-negative pivot: IndefiniteInput), so the
+    yardstick is the quantity the iteration minimises: the dual energy
+    J(lambda) = 1/2 lambda^T F lambda - d^T lambda, evaluated with the ORACLE's
+    operator for both solutions.  The GPU's lambda must be at least as close
+    to the minimiser as the oracle's own (to 1e-6 relative), with the same
+    iteration count +-1 (measured round 1: 11 = 11; J closer by 14x on a C5-law
+    diagnostic, profiles/r01_c5_conditioning_diag.json)."""
+    from paper_2111_11728_b200 import engine
+    prob = pb.config5()
+    o = oracle_mod.Oracle(prob)
+    lo, to = o.solve(tol=1e-6, max_it=200, directions=2)
+    g = engine.FetiSystem(prob)
+    lg, tg = g.solve(tol=1e-6, max_it=200, directions=2)
+    g.close()
+    d, _ = o.rhs()
+    J = lambda lam: 0.5 * lam @ o.apply_F(lam) - d @ lam   # noqa: E731
+    jg, jo = J(lg), J(lo)
+    print("C5 RRS its gpu", tg["iterations"], "oracle", to["iterations"], "J gpu %.10e oracle %.10e" % (jg, jo))
+    assert tg["status"] == to["status"] == 0
+    assert abs(tg["iterations"] - to["iterations"]) <= 1
+    assert jg <= jo + 1e-6 * abs(jo)
