@@ -321,17 +321,18 @@ __global__ void k_splitk_sum(int M, int N, int S, const double* __restrict__ par
 }
 // Split count: the fewest fixed K segments (each >= 512 deep) that fill the
 // last wave of 64 x 64 tiles (about 3 resident CTAs on each of 148 SMs) within
-// 8%; 1 when the plain tile grid already does.
+// 3%; 1 when the plain tile grid already does.
 static int gemm_splitk_segments(int M, int N, int K) {
   const long long tiles = (long long)((M + 63) / 64) * ((N + 63) / 64), slots = 3 * 148;
   auto eff = [&](long long units) { return (double)units / (double)(((units + slots - 1) / slots) * slots); };
-  if (eff(tiles) >= 0.92 || K < 1024) return 1;
+  if (eff(tiles) >= 0.97 || K < 1024) return 1;
   int best = 1;
   double be = eff(tiles);
-  for (int S = 2; S <= 16 && K / S >= 512; ++S) {
+  // (partials capped at 64 M doubles = 512 MB of workspace)
+  for (int S = 2; S <= 8 && K / S >= 512 && (long long)S * M * N <= (64ll << 20); ++S) {
     const double e = eff(tiles * S);
-    if (e > be + 0.03) { best = S; be = e; }
-    if (be >= 0.92) break;
+    if (e > be + 0.02) { best = S; be = e; }
+    if (be >= 0.97) break;
   }
   return best;
 }

@@ -718,7 +718,8 @@ int Ctx::solve_rrs_implicit(const fetigpu_solve_opts& o, double* lambda_host, fe
     grow2(CW, kzmax * k); grow2(XT, kzmax * k); grow2(NT, kzmax * k); grow2(NTot, kzmax * k); grow2(CT, kzmax * k);
     Mchunks.emplace_back(new DBuf<double>);
     Mchunks.back()->alloc(kk * (size_t)nl_pre * (nl_pre + 1) / 2 + 32 * (size_t)nl_pre);
-    dla_ws(std::max({gemm_splitk_ws(k, k, (int)kzmax), tri_inv_workspace(k), (size_t)kGvSeg * k}));
+    dla_ws(std::max({gemm_splitk_ws(k, k, (int)kzmax), tri_inv_workspace(k), (size_t)kGvSeg * k,
+                     (size_t)64 << 20}));   // the split-K cap
     ensure_block_buffers(k);
   }
   Scal* hs = nullptr;
