@@ -398,6 +398,54 @@ def solve_table(engine, configs):
     return out
 
 
+class _SoloComm:
+    """world size 1 without torchrun: the exchanges are identities"""
+
+    def allreduce_sum(self, t):
+        return t
+
+
+def run_shard(args, ws, rank, local, dist):
+    """--shard: the C4 apply sharded over the ranks by module row bands
+    (paper_2111_11728_b200/shard.py): halo rows and the coarse t exchanged by
+    NCCL allreduce, the coarse problem solved redundantly.  Strong scaling:
+    every rank applies 1/N of the subdomains to the same multiplier vector.
+    The apply synchronises the host around its exchanges, so the time is the
+    host wall clock of `steps` applies after a device synchronisation, max
+    over ranks."""
+    import torch
+    from paper_2111_11728_b200 import engine, shard
+    torch.cuda.set_device(local)
+    prob = pb.config4()
+    g = engine.FetiSystem(prob)
+    ranges = shard.row_bands(prob.sx, prob.sy, ws)
+    comm = shard.TorchComm(dist, "cuda") if dist is not None else _SoloComm()
+    sh = shard.ShardedSystem(g, rank, ranges, comm)
+    x = torch.as_tensor(np.random.default_rng(1234).standard_normal(g.m), device="cuda")
+    for _ in range(args.warmup):
+        sh.apply(x)
+    torch.cuda.synchronize()
+    barrier(dist)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        y = sh.apply(x)
+    torch.cuda.synchronize()
+    t = max_over_ranks(dist, (time.perf_counter() - t0) / args.steps)
+    ref = g.apply_F(x.cpu().numpy())
+    tt = sh.plan.touched(rank)
+    exact = bool(np.array_equal(y.cpu().numpy()[tt], ref[tt]))
+    if rank == 0:
+        vbytes = c4_work()["stream_bytes"]
+        cfg = dict(c4_config(), parallelism=f"subdomain-sharded x{ws} (row bands)")
+        print(json.dumps({"metric": METRIC, "value": vbytes / t / 1e9, "unit": "GB/s", "n_gpus": ws,
+                          "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+                          "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                          "data": "synthetic (seeded U(0,1) densities, C4 law)", "config": cfg,
+                          "sharded_equals_1gpu_bitwise": exact,
+                          "timing": "host wall clock per sharded apply (exchanges synchronise), max over ranks"}),
+              flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -409,6 +457,9 @@ def main():
     ap.add_argument("--no-block", action="store_true")
     ap.add_argument("--block-k", type=int, default=2048)
     ap.add_argument("--block-reps", type=int, default=3)
+    ap.add_argument("--shard", action="store_true",
+                    help="strong scaling: one C4 apply sharded over the ranks (shard.py, NCCL exchanges) "
+                         "instead of N replicas")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -426,6 +477,9 @@ def main():
     from paper_2111_11728_b200 import engine
     engine.check(engine.lib().fetigpu_set_device(local))
     L = engine.lib()
+    if args.shard:
+        run_shard(args, ws, rank, local, dist)
+        return
 
     prob = pb.config4()
     t0 = time.perf_counter()
