@@ -151,7 +151,10 @@ typedef struct fetigpu_stats {
   double nd_ms, slot_ms, coarse_ms;
   double device_bytes;       /* device memory held by the context */
   int host_pipeline;         /* 1: fetigpu_apply_F overlaps the H2D of x with the GEMV */
-  int reserved_;
+  /* loop of the last PCG / FO solve: 0 host-driven, 1 CUDA-graph while loop,
+   * 2 persistent kernel with a grid barrier, 3 persistent kernel as one
+   * thread-block cluster (K15) */
+  int solve_loop;
   /* bytes one F-apply must stream with symmetric operator storage: the
    * symmetric-packed F_s tiles when the packed kernel runs (else 8 n_s^2),
    * A_bc read in both phases, the coarse inverse (packed tiles or dense),

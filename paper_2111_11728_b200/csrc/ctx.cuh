@@ -6,6 +6,7 @@
 #include "runtime.cuh"
 #include "setup.hpp"
 #include "kernels_apply.cuh"
+#include "kernels_persist.cuh"
 #include "kernels_build.cuh"
 #include "kernels_dmma.cuh"
 #include "dla.cuh"
@@ -370,14 +371,16 @@ struct Ctx {
   void recover(const double* lambda_dev, double* u_dev);
 
   // ------------------------------------------------------------ engine --
+  // fixed partition of the deterministic dot products: one row per thread
+  // (the persistent loop forms each row's operands on the fly in its CTA)
+  int dot_blocks() const { return std::max(1, std::min(kDotBlocks, (su.m + kThreads - 1) / kThreads)); }
   void dots(std::initializer_list<std::pair<const double*, const double*>> pairs, double* out) {
     DotArgs a{};
     int k = 0;
     for (auto& p : pairs) { a.a[k] = p.first; a.b[k] = p.second; ++k; }
     a.npairs = k;
     a.n = su.m;
-    const int nblk = std::max(1, std::min(kDotBlocks, (su.m + 1023) / 1024));
-    launch_pdl(k_dot_fused, nblk, kThreads, 0, st, a, d_partial.p, d_counter.p, out);
+    launch_pdl(k_dot_fused, dot_blocks(), kThreads, 0, st, a, d_partial.p, d_counter.p, out);
     LAUNCH_CHECK();
   }
 
@@ -386,6 +389,32 @@ struct Ctx {
     project(z, 1, su.m);
   }
 
+  // K15 persistent PCG / FO loop (kernels_persist.cuh): grid size (0 = not
+  // applicable / disabled), barrier kind, launch
+  bool persist_cluster = false;
+  int solve_loop = 0;   // fetigpu_stats::solve_loop of the last PCG / FO solve
+  int p_state = 0;   // 0 unknown, 1 ready, -1 not applicable (a row without one or two owners)
+  DBuf<int4> p_op_ent, p_pc_ent;
+  DBuf<double2> p_op_c, p_pc_c;
+  DBuf<unsigned char> p_pc_wr;
+  DBuf<int> p_voff_op, p_voff_pc;
+  DBuf<double> p_vop, p_vpc, p_w2, p_r2;
+  DBuf<unsigned int> p_bar;
+  bool persist_prepare();
+  size_t persist_smem() const;
+  // FETIGPU_PERSIST_RED=1: small coarse operators applied redundantly by the
+  // CTAs that need them instead of in their own grid phase (measured slower)
+  static bool persist_red() {
+    static const bool on = [] {
+      const char* e = getenv("FETIGPU_PERSIST_RED");
+      return e && e[0] == '1';
+    }();
+    return on;
+  }
+  int persist_grid(bool fo);
+  void launch_persist(int G, bool fo, int passes, int psi_S, double* lam, double* r, double* z, double* w, double* q,
+                      Scal* sc, double* Wst, double* Qst, double* psi, double* psi_part, int* cnt, IterCtl* ctl,
+                      double* trace);
   int solve(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_trace* tr);
   int solve_rrs(const fetigpu_solve_opts& o, double* lam, fetigpu_trace* tr);
   int solve_rrs_implicit(const fetigpu_solve_opts& o, double* lam, fetigpu_trace* tr);

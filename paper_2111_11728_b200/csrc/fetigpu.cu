@@ -89,7 +89,7 @@ int fetigpu_stats_get(const fetigpu_ctx* ctx, fetigpu_stats* s) {
     s->n_kept = c.su.n_kept; s->n_iface = c.su.n_iface; s->max_ns = mx; s->n_designs = c.su.n_designs;
     s->n_op_slots = (int)c.su.op_slots.size();
     s->host_pipeline = c.pipe_ready ? 1 : 0;
-    s->reserved_ = 0;
+    s->solve_loop = c.solve_loop;
     s->n_pc_slots = (int)(c.su.precond == FETIGPU_DIRICHLET ? c.su.pc_slots.size() : c.su.pc_lumped_T.size());
     // algorithmic work per apply, pure index counts
     double sn2 = 0, snc = 0, sns = 0;
@@ -711,3 +711,16 @@ int fetigpu_time_apply(fetigpu_ctx* ctx, const double* x, double* y, int ncols, 
 }
 
 }  // extern "C"
+
+#ifdef FG_PERSIST_PROF
+// tools/persist_prof.py: the K15 phase stamps of the last persistent solve
+extern "C" int fetigpu_pprof(unsigned long long* out, int cap) {
+  unsigned int n = 0;
+  if (cudaMemcpyFromSymbol(&n, fg::g_pprof_n, sizeof(n)) != cudaSuccess) return -1;
+  n = std::min<unsigned int>(n, (unsigned int)cap);
+  if (n && cudaMemcpyFromSymbol(out, fg::g_pprof, n * sizeof(unsigned long long)) != cudaSuccess) return -1;
+  const unsigned int z = 0;
+  cudaMemcpyToSymbol(fg::g_pprof_n, &z, sizeof(z));
+  return (int)n;
+}
+#endif

@@ -15,6 +15,7 @@
 #pragma once
 
 #include <cooperative_groups.h>
+#include <type_traits>
 
 #include "common.cuh"
 
@@ -86,6 +87,136 @@ __device__ __forceinline__ void fused_dp_t(const DpSub& p, const double* __restr
   }
 }
 
+// One CTA of the K4/K7 GEMV: subdomain s, column col, row slice zi of nz
+// (rows i = warp + 8 zi, + 8 nz, ...).  A row's dot product does not depend on
+// the slicing, and every dual row receives its two contributions in either
+// order (0 + a + b), so any nz gives bit-identical results.  Shared by the
+// kernel below and the persistent solver loop (kernels_persist.cuh); x is
+// read through L2 (__ldcg) because the persistent loop writes it in-kernel.
+// x_s = B_s^T x into shared memory (ld entries, zero padded): xval(r, e)
+// returns the dual-vector value at row r for map entry e (a plain L2 load, or
+// a value the persistent loop forms on the fly)
+template <int KR, class XV>
+__device__ __forceinline__ void gather_xs(const OpSub& d, const int* __restrict__ rows,
+                                          const double* __restrict__ coefs, double* xs, XV&& xval) {
+  const int* rw = rows + d.map_off;
+  const double* cf = coefs + d.map_off;
+  for (int j = threadIdx.x; j < d.ld; j += blockDim.x) {
+    double acc = 0.0;
+    if (j < d.ns) {
+#pragma unroll
+      for (int k = 0; k < KR; ++k) {
+        const int r = rw[j * KR + k];
+        if (r >= 0) acc += cf[j * KR + k] * xval(r, d.map_off + j * KR + k);
+      }
+    }
+    xs[j] = acc;
+  }
+}
+
+// the row part of the K4/K7 GEMV for one CTA (rows i = warp + 8 zi, + 8 nz,
+// ...): v_i = F_s[i,:] x_s, stored (STORE_V) or scattered with the map's signs
+template <int KR, bool STORE_V>
+__device__ __forceinline__ void gemv_rows_cta(int s, int col, int zi, int nz, const double* xs, const OpSub& d,
+                                              const double* __restrict__ mats, const int* __restrict__ rows,
+                                              const double* __restrict__ coefs, double* y, double* zcols, int ldz,
+                                              double* vbuf, const int* __restrict__ voff, int ldy, int zrs) {
+  const int* rw = rows + d.map_off;
+  const double* cf = coefs + d.map_off;
+  const double* A = mats + d.moff;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // rows are split over nz CTAs when there are few subdomains; each warp
+  // streams two of its rows at a time (independent chains, same arithmetic
+  // per row as one at a time)
+  const int nw = (blockDim.x >> 5) * nz;
+  auto emit = [&](int i, double v) {
+    if (STORE_V) {
+      vbuf[voff[s] + i] = v;
+    } else {
+      double* yc = y + (size_t)col * ldy;
+#pragma unroll
+      for (int k = 0; k < KR; ++k) {
+        const int r = rw[i * KR + k];
+        if (r >= 0) {
+          const double c = cf[i * KR + k] * v;
+          atomicAdd(yc + r, c);
+          if (zcols) zcols[(size_t)s * ldz + (size_t)r * zrs] = c;
+        }
+      }
+    }
+  };
+  const int n2 = d.ld >> 1;
+  // R rows i, i + nw, ... streamed together: each row keeps its own two
+  // lane-strided chains (acc0 even / acc1 odd columns), exactly as one at a time
+  auto rowblk = [&](int i, auto rc) {
+    constexpr int R = decltype(rc)::value;
+    const double2* Ar[R];
+    double acc0[R], acc1[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      Ar[r] = reinterpret_cast<const double2*>(A + (size_t)(i + r * nw) * d.ld);
+      acc0[r] = 0.0;
+      acc1[r] = 0.0;
+    }
+    int j = lane;
+    for (; j + 32 < n2; j += 64) {
+      double2 a0[R], a1[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        a0[r] = __ldcs(Ar[r] + j);
+        a1[r] = __ldcs(Ar[r] + j + 32);
+      }
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        acc0[r] = fma(a0[r].x, xs[2 * j], acc0[r]);
+        acc1[r] = fma(a0[r].y, xs[2 * j + 1], acc1[r]);
+        acc0[r] = fma(a1[r].x, xs[2 * j + 64], acc0[r]);
+        acc1[r] = fma(a1[r].y, xs[2 * j + 65], acc1[r]);
+      }
+    }
+    for (; j < n2; j += 32) {
+      double2 a0[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) a0[r] = __ldcs(Ar[r] + j);
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        acc0[r] = fma(a0[r].x, xs[2 * j], acc0[r]);
+        acc1[r] = fma(a0[r].y, xs[2 * j + 1], acc1[r]);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const double v = warp_sum(acc0[r] + acc1[r]);
+      if (lane == 0) emit(i + r * nw, v);
+    }
+  };
+  int i = warp + (blockDim.x >> 5) * zi;
+  for (; i + 3 * nw < d.ns; i += 4 * nw) rowblk(i, std::integral_constant<int, 4>{});
+  if (i + nw < d.ns) {
+    rowblk(i, std::integral_constant<int, 2>{});
+    i += 2 * nw;
+  }
+  if (i < d.ns) rowblk(i, std::integral_constant<int, 1>{});
+}
+
+// One CTA of the K4/K7 GEMV: subdomain s, column col, row slice zi of nz.
+// A row's dot product does not depend on the slicing, and every dual row
+// receives its two contributions in either order (0 + a + b), so any nz gives
+// bit-identical results.  x is read through L2 (__ldcg).
+template <int KR, bool STORE_V>
+__device__ __forceinline__ void gemv_scatter_cta(
+    int s, int col, int zi, int nz, double* xs, const OpSub* __restrict__ subs, const double* __restrict__ mats,
+    const int* __restrict__ rows, const double* __restrict__ coefs, const double* x, double* y, double* zcols,
+    int ldz, double* vbuf, const int* __restrict__ voff, int ldx, int ldy, int zrs, const DpSub* __restrict__ dps,
+    const double* __restrict__ abc, double* tbuf) {
+  const OpSub d = subs[s];
+  const double* xc = x + (size_t)col * ldx;
+  gather_xs<KR>(d, rows, coefs, xs, [&](int r, int) { return __ldcg(xc + r); });
+  __syncthreads();
+  if (STORE_V && dps && zi == 0) fused_dp_t(dps[s], abc, xs, d.ns, tbuf);
+  gemv_rows_cta<KR, STORE_V>(s, col, zi, nz, xs, d, mats, rows, coefs, y, zcols, ldz, vbuf, voff, ldy, zrs);
+}
+
 template <int KR, bool STORE_V>
 __global__ void __launch_bounds__(kThreads) k_gather_gemv_scatter(
     const OpSub* __restrict__ subs, const double* __restrict__ mats, const int* __restrict__ rows,
@@ -95,66 +226,8 @@ __global__ void __launch_bounds__(kThreads) k_gather_gemv_scatter(
     const double* __restrict__ abc = nullptr, double* __restrict__ tbuf = nullptr) {
   pdl_wait();
   extern __shared__ double xs[];
-  const int s = blockIdx.x;
-  const int col = blockIdx.y;
-  const OpSub d = subs[s];
-  const double* xc = x + (size_t)col * ldx;
-  const int* rw = rows + d.map_off;
-  const double* cf = coefs + d.map_off;
-  for (int j = threadIdx.x; j < d.ld; j += blockDim.x) {
-    double acc = 0.0;
-    if (j < d.ns) {
-#pragma unroll
-      for (int k = 0; k < KR; ++k) {
-        const int r = rw[j * KR + k];
-        if (r >= 0) acc += cf[j * KR + k] * xc[r];
-      }
-    }
-    xs[j] = acc;
-  }
-  __syncthreads();
-  if (STORE_V && dps && blockIdx.z == 0) fused_dp_t(dps[s], abc, xs, d.ns, tbuf);
-  const double* A = mats + d.moff;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // rows are split over gridDim.z CTAs when there are few subdomains
-  const int nw = (blockDim.x >> 5) * gridDim.z;
-  for (int i = warp + (blockDim.x >> 5) * blockIdx.z; i < d.ns; i += nw) {
-    const double2* Ai = reinterpret_cast<const double2*>(A + (size_t)i * d.ld);
-    double acc0 = 0.0, acc1 = 0.0;
-    const int n2 = d.ld >> 1;
-    int j = lane;
-#pragma unroll 4
-    for (; j + 32 < n2; j += 64) {
-      const double2 a0 = __ldcs(Ai + j);
-      const double2 a1 = __ldcs(Ai + j + 32);
-      acc0 = fma(a0.x, xs[2 * j], acc0);
-      acc1 = fma(a0.y, xs[2 * j + 1], acc1);
-      acc0 = fma(a1.x, xs[2 * j + 64], acc0);
-      acc1 = fma(a1.y, xs[2 * j + 65], acc1);
-    }
-    for (; j < n2; j += 32) {
-      const double2 a0 = __ldcs(Ai + j);
-      acc0 = fma(a0.x, xs[2 * j], acc0);
-      acc1 = fma(a0.y, xs[2 * j + 1], acc1);
-    }
-    const double v = warp_sum(acc0 + acc1);
-    if (lane == 0) {
-      if (STORE_V) {
-        vbuf[voff[s] + i] = v;
-      } else {
-        double* yc = y + (size_t)col * ldy;
-#pragma unroll
-        for (int k = 0; k < KR; ++k) {
-          const int r = rw[i * KR + k];
-          if (r >= 0) {
-            const double c = cf[i * KR + k] * v;
-            atomicAdd(yc + r, c);
-            if (zcols) zcols[(size_t)s * ldz + (size_t)r * zrs] = c;
-          }
-        }
-      }
-    }
-  }
+  gemv_scatter_cta<KR, STORE_V>(blockIdx.x, blockIdx.y, blockIdx.z, gridDim.z, xs, subs, mats, rows, coefs, x, y,
+                                zcols, ldz, vbuf, voff, ldx, ldy, zrs, dps, abc, tbuf);
 }
 
 // ------------------------------------ K4 on symmetric-packed F_s (C4 path) --
@@ -432,15 +505,14 @@ __global__ void __launch_bounds__(512) k_csym_reduce(const double* __restrict__ 
   }
 }
 
-// dense row-major GEMV y = M x (one warp per row), n x n; 128-bit loads and
-// four independent accumulators keep ~4 KB in flight per warp
-__global__ void __launch_bounds__(256) k_dense_gemv(const double* __restrict__ M, int n,
-                                                    const double* __restrict__ x,
-                                                    double* __restrict__ y) {
-  pdl_wait();
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  const int nwarps = (gridDim.x * blockDim.x) >> 5;
-  for (int i = warp; i < n; i += nwarps) {
+// rows i = warp0, warp0 + nwarps, ... of y = M x (one warp per row; a row's
+// result does not depend on the warp count).  x through L2 (__ldcg): the
+// persistent solver loop produces it in-kernel.
+__device__ __forceinline__ void dense_gemv_warps(const double* __restrict__ M, int n, const double* x,
+                                                 double* y, int warp0, int nwarps) {
+  const int lane = threadIdx.x & 31;
+  // one row's chains (a0..a3 over lane-strided double2 pairs, then warp_sum)
+  auto row = [&](int i) {
     const double* Mi = M + (size_t)i * n;
     double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
     if ((n & 1) == 0) {
@@ -449,42 +521,60 @@ __global__ void __launch_bounds__(256) k_dense_gemv(const double* __restrict__ M
       int j = lane;
       for (; j + 32 < n2; j += 64) {
         const double2 u = __ldcs(M2 + j), v = __ldcs(M2 + j + 32);
-        a0 = fma(u.x, x[2 * j], a0);
-        a1 = fma(u.y, x[2 * j + 1], a1);
-        a2 = fma(v.x, x[2 * j + 64], a2);
-        a3 = fma(v.y, x[2 * j + 65], a3);
+        a0 = fma(u.x, __ldcg(x + 2 * j), a0);
+        a1 = fma(u.y, __ldcg(x + 2 * j + 1), a1);
+        a2 = fma(v.x, __ldcg(x + 2 * j + 64), a2);
+        a3 = fma(v.y, __ldcg(x + 2 * j + 65), a3);
       }
       for (; j < n2; j += 32) {
         const double2 u = __ldcs(M2 + j);
-        a0 = fma(u.x, x[2 * j], a0);
-        a1 = fma(u.y, x[2 * j + 1], a1);
+        a0 = fma(u.x, __ldcg(x + 2 * j), a0);
+        a1 = fma(u.y, __ldcg(x + 2 * j + 1), a1);
       }
     } else {
-      for (int j = lane; j < n; j += 32) a0 = fma(Mi[j], x[j], a0);
+      for (int j = lane; j < n; j += 32) a0 = fma(Mi[j], __ldcg(x + j), a0);
     }
-    const double acc = warp_sum((a0 + a1) + (a2 + a3));
-    if (lane == 0) y[i] = acc;
+    return warp_sum((a0 + a1) + (a2 + a3));
+  };
+  int i = warp0;
+  for (; i + 3 * nwarps < n; i += 4 * nwarps) {   // four rows in flight per warp
+    const double v0 = row(i), v1 = row(i + nwarps), v2 = row(i + 2 * nwarps), v3 = row(i + 3 * nwarps);
+    if (lane == 0) {
+      y[i] = v0;
+      y[i + nwarps] = v1;
+      y[i + 2 * nwarps] = v2;
+      y[i + 3 * nwarps] = v3;
+    }
   }
+  for (; i < n; i += nwarps) {
+    const double v = row(i);
+    if (lane == 0) y[i] = v;
+  }
+}
+// dense row-major GEMV y = M x (one warp per row), n x n; 128-bit loads and
+// four independent accumulators keep ~4 KB in flight per warp
+__global__ void __launch_bounds__(256) k_dense_gemv(const double* __restrict__ M, int n,
+                                                    const double* __restrict__ x,
+                                                    double* __restrict__ y) {
+  pdl_wait();
+  dense_gemv_warps(M, n, x, y, (blockIdx.x * blockDim.x + threadIdx.x) >> 5, (gridDim.x * blockDim.x) >> 5);
 }
 
 // FETI-DP phase 2: v_s += A_bc u[cmap]; scatter sign * v_s.  A_bc rows are
 // n_c (4 or 8) contiguous doubles, read as 128-bit pairs.
-__global__ void k_dp_phase2(const OpSub* __restrict__ subs, const DpSub* __restrict__ dps,
-                            const int* __restrict__ rows, const double* __restrict__ coefs,
-                            const double* __restrict__ abc, const int* __restrict__ cmap,
-                            const double* __restrict__ u, const double* __restrict__ vbuf,
-                            double* __restrict__ y, double vscale) {
-  pdl_wait();
-  const int s = blockIdx.x;
+__device__ __forceinline__ void dp_phase2_cta(int s, const OpSub* __restrict__ subs, const DpSub* __restrict__ dps,
+                                              const int* __restrict__ rows, const double* __restrict__ coefs,
+                                              const double* __restrict__ abc, const int* __restrict__ cmap,
+                                              const double* u, const double* vbuf, double* y, double vscale) {
   const OpSub d = subs[s];
   const DpSub p = dps[s];
   __shared__ double uc[8];
-  if (threadIdx.x < 8) uc[threadIdx.x] = threadIdx.x < p.nc ? u[cmap[p.cmap_off + threadIdx.x]] : 0.0;
+  if (threadIdx.x < 8) uc[threadIdx.x] = threadIdx.x < p.nc ? __ldcg(u + cmap[p.cmap_off + threadIdx.x]) : 0.0;
   __syncthreads();
   const double* Ab = abc + p.abc_off;
   const bool vec = (p.nc & 1) == 0 && (p.abc_off & 1) == 0;
   for (int j = threadIdx.x; j < d.ns; j += blockDim.x) {
-    double v = vbuf ? vscale * vbuf[p.v_off + j] : 0.0;
+    double v = vbuf ? vscale * __ldcg(vbuf + p.v_off + j) : 0.0;
     if (vec) {
       const double2* A2 = reinterpret_cast<const double2*>(Ab + (size_t)j * p.nc);
       for (int c = 0; c < (p.nc >> 1); ++c) {
@@ -499,24 +589,32 @@ __global__ void k_dp_phase2(const OpSub* __restrict__ subs, const DpSub* __restr
     if (r >= 0) atomicAdd(y + r, coefs[d.map_off + j] * v);
   }
 }
+__global__ void k_dp_phase2(const OpSub* __restrict__ subs, const DpSub* __restrict__ dps,
+                            const int* __restrict__ rows, const double* __restrict__ coefs,
+                            const double* __restrict__ abc, const int* __restrict__ cmap,
+                            const double* __restrict__ u, const double* __restrict__ vbuf,
+                            double* __restrict__ y, double vscale) {
+  pdl_wait();
+  dp_phase2_cta(blockIdx.x, subs, dps, rows, coefs, abc, cmap, u, vbuf, y, vscale);
+}
 
 // ------------------------------------------------------ T-FETI projector --
 // g_s = -R_T^T (B_s^T v): per subdomain 3 values (K8, decomposition.hpp:136)
-__global__ void k_proj_gather(const OpSub* __restrict__ psubs, const int* __restrict__ rows,
-                              const double* __restrict__ coefs, const double* __restrict__ RT,
-                              const int* __restrict__ rt_off, const double* __restrict__ v, int ldv,
-                              double* __restrict__ g, int ldg, double sign, int rs = 1) {
-  pdl_wait();
-  const int s = blockIdx.x, col = blockIdx.y;
+// g_s = sign R_T^T (B_s^T v) for one subdomain; vval(r) yields v at dual row r
+// (an L2 load, or a value the persistent loop forms on the fly)
+template <class VV>
+__device__ __forceinline__ void proj_gather_fn(int s, int col, const OpSub* __restrict__ psubs,
+                                               const int* __restrict__ rows, const double* __restrict__ coefs,
+                                               const double* __restrict__ RT, const int* __restrict__ rt_off,
+                                               double* g, int ldg, double sign, VV&& vval) {
   const OpSub d = psubs[s];
-  const double* vc = v + (size_t)col * ldv;
   const double* R = RT + rt_off[s];
   double a0 = 0, a1 = 0, a2 = 0;
   for (int j = threadIdx.x; j < d.ns; j += blockDim.x) {
     double xj = 0.0;
     for (int k = 0; k < 3; ++k) {
       const int r = rows[d.map_off + j * 3 + k];
-      if (r >= 0) xj += coefs[d.map_off + j * 3 + k] * vc[(size_t)r * rs];
+      if (r >= 0) xj += coefs[d.map_off + j * 3 + k] * vval(r);
     }
     a0 += R[j * 3] * xj;
     a1 += R[j * 3 + 1] * xj;
@@ -532,6 +630,21 @@ __global__ void k_proj_gather(const OpSub* __restrict__ psubs, const int* __rest
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[threadIdx.x][w];
     g[(size_t)col * ldg + 3 * s + threadIdx.x] = sign * t;
   }
+}
+__device__ __forceinline__ void proj_gather_cta(int s, int col, const OpSub* __restrict__ psubs,
+                                                const int* __restrict__ rows, const double* __restrict__ coefs,
+                                                const double* __restrict__ RT, const int* __restrict__ rt_off,
+                                                const double* v, int ldv, double* g, int ldg, double sign, int rs) {
+  const double* vc = v + (size_t)col * ldv;
+  proj_gather_fn(s, col, psubs, rows, coefs, RT, rt_off, g, ldg, sign,
+                 [&](int r) { return __ldcg(vc + (size_t)r * rs); });
+}
+__global__ void k_proj_gather(const OpSub* __restrict__ psubs, const int* __restrict__ rows,
+                              const double* __restrict__ coefs, const double* __restrict__ RT,
+                              const int* __restrict__ rt_off, const double* __restrict__ v, int ldv,
+                              double* __restrict__ g, int ldg, double sign, int rs = 1) {
+  pdl_wait();
+  proj_gather_cta(blockIdx.x, blockIdx.y, psubs, rows, coefs, RT, rt_off, v, ldv, g, ldg, sign, rs);
 }
 
 // dense column-major H (n x n) times g columns: h = H g
@@ -551,6 +664,29 @@ __device__ __forceinline__ double proj_rh(const double* __restrict__ R, const do
   return R[0] * hs[0] + R[1] * hs[1] + R[2] * hs[2];
 }
 
+// corr_r = c_plus + c_minus of dual row r (h read through L2 -- produced
+// in-kernel by the persistent solver loop -- or from shared memory, SH)
+template <bool SH = false>
+__device__ __forceinline__ double proj_row_corr(int r, const int2* __restrict__ ent_sr,
+                                                const double2* __restrict__ ent_c, const double* __restrict__ RT,
+                                                const double* h) {
+  auto ld = [&](const double* p) { return SH ? *p : __ldcg(p); };
+  const int2 sr0 = ent_sr[2 * r], sr1 = ent_sr[2 * r + 1];   // (s, RT offset) or s < 0
+  const double2 c = ent_c[r];
+  double corr = 0.0;
+  if (sr0.x >= 0) {
+    const double* hs = h + 3 * sr0.x;
+    const double hh[3] = {ld(hs), ld(hs + 1), ld(hs + 2)};
+    corr = c.x * proj_rh(RT + sr0.y, hh);
+  }
+  if (sr1.x >= 0) {
+    const double* hs = h + 3 * sr1.x;
+    const double hh[3] = {ld(hs), ld(hs + 1), ld(hs + 2)};
+    corr = corr + c.y * proj_rh(RT + sr1.y, hh);
+  }
+  return corr;
+}
+
 // Single-vector projector finish, row-wise: every dual row has at most two
 // (subdomain, R row, sign) entries, so corr_r = c_plus + c_minus is formed in
 // place (0 + a + b == a + b in either order: bit-identical to the zeroed
@@ -561,12 +697,8 @@ __global__ void k_proj_rows(int m, const int2* __restrict__ ent_sr, const double
                             int accumulate) {
   pdl_wait();
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < m; r += gridDim.x * blockDim.x) {
-    const int2 sr0 = ent_sr[2 * r], sr1 = ent_sr[2 * r + 1];   // (s, RT offset) or s < 0
-    const double2 c = ent_c[r];
-    double corr = 0.0;
-    if (sr0.x >= 0) corr = c.x * proj_rh(RT + sr0.y, h + 3 * sr0.x);
-    if (sr1.x >= 0) corr = corr + c.y * proj_rh(RT + sr1.y, h + 3 * sr1.x);
-    out[r] = accumulate ? out[r] + corr : corr;
+    const double corr = proj_row_corr(r, ent_sr, ent_c, RT, h);
+    out[r] = accumulate ? __dadd_rn(out[r], corr) : corr;   // no contraction into corr's product
   }
 }
 
@@ -643,44 +775,80 @@ __global__ void k_dot_final(const double* partial, int npairs, double* out) {
   if (lane == 0) out[k] = acc;
 }
 
+// Per-block partial of the deterministic multi-dot: block vb of nvb (stride
+// nvb * blockDim), written to partial[k * kDotBlocks + vb].  f(i, x, y) yields
+// the NP operand pairs of row i (loads, or values the persistent loop forms
+// on the fly); each pair accumulates fma(x, y, acc) in row order.
+template <int NP, class F>
+__device__ __forceinline__ void dot_partial_rows(int vb, int nvb, int n, double* partial, F&& f) {
+  double acc[NP];
+#pragma unroll
+  for (int k = 0; k < NP; ++k) acc[k] = 0.0;
+  const int stride = nvb * blockDim.x;
+  for (int i = vb * blockDim.x + threadIdx.x; i < n; i += stride) {
+    double x[NP], y[NP];
+    f(i, x, y);
+#pragma unroll
+    for (int k = 0; k < NP; ++k) acc[k] = fma(x[k], y[k], acc[k]);
+  }
+  __shared__ double red[4][kThreads / 32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+  for (int k = 0; k < NP; ++k) {
+    const double v = warp_sum(acc[k]);
+    if (lane == 0) red[k][warp] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < NP) {
+    double v = 0.0;
+    for (int w = 0; w < kThreads / 32; ++w) v += red[threadIdx.x][w];
+    partial[threadIdx.x * kDotBlocks + vb] = v;
+  }
+}
+// operands through L2 (__ldcg)
+template <int NP>
+__device__ __forceinline__ void dot_partial_ld(const DotArgs& args, int vb, int nvb, double* partial) {
+  dot_partial_rows<NP>(vb, nvb, args.n, partial, [&](int i, double* x, double* y) {
+#pragma unroll
+    for (int k = 0; k < NP; ++k) {
+      x[k] = __ldcg(args.a[k] + i);
+      y[k] = __ldcg(args.b[k] + i);
+    }
+  });
+}
+__device__ __forceinline__ void dot_partial_cta(const DotArgs& args, int vb, int nvb, double* partial) {
+  switch (args.npairs) {
+    case 1: dot_partial_ld<1>(args, vb, nvb, partial); break;
+    case 2: dot_partial_ld<2>(args, vb, nvb, partial); break;
+    case 3: dot_partial_ld<3>(args, vb, nvb, partial); break;
+    default: dot_partial_ld<4>(args, vb, nvb, partial); break;
+  }
+}
+// final fixed-order sum of pair k over nvb partials (one warp; every lane returns it)
+__device__ __forceinline__ double dot_final_warp(const double* partial, int k, int nvb) {
+  const int lane = threadIdx.x & 31;
+  double a = 0.0;
+  for (int b = lane; b < nvb; b += 32) a += __ldcg(partial + k * kDotBlocks + b);
+  return warp_sum(a);
+}
+
 // Single-launch deterministic multi-dot: fixed grid, per-block partials in a
 // fixed slot, the last block to finish sums them in fixed order.
 __global__ void __launch_bounds__(kThreads) k_dot_fused(DotArgs args, double* partial,
                                                         unsigned int* counter, double* out) {
   pdl_wait();
-  double acc[4] = {0, 0, 0, 0};
-  const int stride = gridDim.x * blockDim.x;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < args.n; i += stride) {
-#pragma unroll
-    for (int k = 0; k < 4; ++k)
-      if (k < args.npairs) acc[k] = fma(args.a[k][i], args.b[k][i], acc[k]);
-  }
-  __shared__ double red[4][kThreads / 32];
   __shared__ bool last;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const double v = warp_sum(acc[k]);
-    if (lane == 0) red[k][warp] = v;
-  }
-  __syncthreads();
-  if (threadIdx.x < args.npairs) {
-    double v = 0.0;
-    for (int w = 0; w < kThreads / 32; ++w) v += red[threadIdx.x][w];
-    partial[threadIdx.x * kDotBlocks + blockIdx.x] = v;
-  }
+  dot_partial_cta(args, blockIdx.x, gridDim.x, partial);
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) last = (atomicAdd(counter, 1u) == gridDim.x - 1);
   __syncthreads();
   if (!last) return;
   __threadfence();
-  const int k = warp;
+  const int k = threadIdx.x >> 5;
   if (k < args.npairs) {
-    double a = 0.0;
-    for (int b = lane; b < (int)gridDim.x; b += 32) a += ((volatile double*)partial)[k * kDotBlocks + b];
-    a = warp_sum(a);
-    if (lane == 0) out[k] = a;
+    const double a = dot_final_warp(partial, k, gridDim.x);
+    if ((threadIdx.x & 31) == 0) out[k] = a;
   }
   if (threadIdx.x == 0) *counter = 0u;
 }
@@ -709,14 +877,9 @@ __global__ void __launch_bounds__(kThreads) k_fo_psi(const double* __restrict__ 
 }
 // 32 rows per CTA (lane <-> row, coalesced per column), the 8 warps split the
 // columns j = warp, warp+8, ...; partial sums reduced over warps in fixed order.
-__global__ void __launch_bounds__(256) k_fo_sub(const double* __restrict__ W, int m,
-                                                const int* __restrict__ cnt, int plus,
-                                                const double* __restrict__ psi,
-                                                double* __restrict__ w) {
-  pdl_wait();
-  const int c = *cnt + plus;
+__device__ __forceinline__ void fo_sub_cta(int vb, const double* W, int m, int c, const double* psi, double* w) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int i = blockIdx.x * 32 + lane;
+  const int i = vb * 32 + lane;
   __shared__ double part[8][33];
   double v = 0.0;
   if (i < m) {
@@ -726,12 +889,12 @@ __global__ void __launch_bounds__(256) k_fo_sub(const double* __restrict__ W, in
     for (; j + 24 < c; j += 32) {
       const double w0 = __ldcs(W + (size_t)j * m + i), w1 = __ldcs(W + (size_t)(j + 8) * m + i),
                    w2 = __ldcs(W + (size_t)(j + 16) * m + i), w3 = __ldcs(W + (size_t)(j + 24) * m + i);
-      v = fma(w0, psi[j], v);
-      v = fma(w1, psi[j + 8], v);
-      v = fma(w2, psi[j + 16], v);
-      v = fma(w3, psi[j + 24], v);
+      v = fma(w0, __ldcg(psi + j), v);
+      v = fma(w1, __ldcg(psi + j + 8), v);
+      v = fma(w2, __ldcg(psi + j + 16), v);
+      v = fma(w3, __ldcg(psi + j + 24), v);
     }
-    for (; j < c; j += 8) v = fma(W[(size_t)j * m + i], psi[j], v);
+    for (; j < c; j += 8) v = fma(__ldcg(W + (size_t)j * m + i), __ldcg(psi + j), v);
   }
   part[warp][lane] = v;
   __syncthreads();
@@ -739,8 +902,49 @@ __global__ void __launch_bounds__(256) k_fo_sub(const double* __restrict__ W, in
     double s = 0.0;
 #pragma unroll
     for (int k = 0; k < 8; ++k) s += part[k][lane];
-    w[i] -= s;
+    w[i] = __ldcg(w + i) - s;
   }
+  __syncthreads();   // part[] is reused by the next row block of a persistent CTA
+}
+__global__ void __launch_bounds__(256) k_fo_sub(const double* __restrict__ W, int m,
+                                                const int* __restrict__ cnt, int plus,
+                                                const double* __restrict__ psi,
+                                                double* __restrict__ w) {
+  pdl_wait();
+  fo_sub_cta(blockIdx.x, W, m, *cnt + plus, psi, w);
+}
+// one (column j, row segment s) item of psi = Q^T w (item = j * S + s)
+__device__ __forceinline__ void fo_psi_item(int item, const double* Q, int m, const double* w, double* partial,
+                                            int S) {
+  const int chunk = (m + S - 1) / S;
+  __shared__ double red[8];
+  const int j = item / S, s = item - j * S;
+  const int i0 = s * chunk, i1 = min(m, i0 + chunk);
+  const double* q = Q + (size_t)j * m;
+  double a0 = 0.0, a1 = 0.0;
+  int i = i0 + threadIdx.x;
+  for (; i + 768 < i1; i += 1024) {  // 4 loads of each vector in flight, same FMA order as 2-way
+    const double q0 = __ldcs(q + i), q1 = __ldcs(q + i + 256), q2 = __ldcs(q + i + 512), q3 = __ldcs(q + i + 768);
+    const double x0 = __ldcg(w + i), x1 = __ldcg(w + i + 256), x2 = __ldcg(w + i + 512), x3 = __ldcg(w + i + 768);
+    a0 = fma(q0, x0, a0);
+    a1 = fma(q1, x1, a1);
+    a0 = fma(q2, x2, a0);
+    a1 = fma(q3, x3, a1);
+  }
+  for (; i + 256 < i1; i += 512) {
+    a0 = fma(__ldcg(q + i), __ldcg(w + i), a0);
+    a1 = fma(__ldcg(q + i + 256), __ldcg(w + i + 256), a1);
+  }
+  if (i < i1) a0 = fma(__ldcg(q + i), __ldcg(w + i), a0);
+  const double acc = warp_sum(a0 + a1);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int k = 0; k < 8; ++k) t += red[k];
+    partial[(size_t)j * S + s] = t;  // S == 1: partial is psi itself
+  }
+  __syncthreads();
 }
 // psi_j = q_j^T w for j < *cnt on a (column x row-segment) grid: CTA (j, s)
 // reduces rows [s*chunk, (s+1)*chunk) of column j into partial[j*S + s];
@@ -754,37 +958,7 @@ __global__ void __launch_bounds__(256) k_fo_psi_seg(const double* __restrict__ Q
   // fixed grid, grid-stride over the live (column j, segment s) items: no
   // empty CTAs for the not-yet-stored directions (the graph is static)
   const int items = (*cnt + plus) * S;
-  const int chunk = (m + S - 1) / S;
-  __shared__ double red[8];
-  for (int item = blockIdx.x; item < items; item += gridDim.x) {
-    const int j = item / S, s = item - j * S;
-    const int i0 = s * chunk, i1 = min(m, i0 + chunk);
-    const double* q = Q + (size_t)j * m;
-    double a0 = 0.0, a1 = 0.0;
-    int i = i0 + threadIdx.x;
-    for (; i + 768 < i1; i += 1024) {  // 4 loads of each vector in flight, same FMA order as 2-way
-      const double q0 = __ldcs(q + i), q1 = __ldcs(q + i + 256), q2 = __ldcs(q + i + 512), q3 = __ldcs(q + i + 768);
-      const double x0 = w[i], x1 = w[i + 256], x2 = w[i + 512], x3 = w[i + 768];
-      a0 = fma(q0, x0, a0);
-      a1 = fma(q1, x1, a1);
-      a0 = fma(q2, x2, a0);
-      a1 = fma(q3, x3, a1);
-    }
-    for (; i + 256 < i1; i += 512) {
-      a0 = fma(q[i], w[i], a0);
-      a1 = fma(q[i + 256], w[i + 256], a1);
-    }
-    if (i < i1) a0 = fma(q[i], w[i], a0);
-    const double acc = warp_sum(a0 + a1);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double t = 0.0;
-      for (int k = 0; k < 8; ++k) t += red[k];
-      partial[(size_t)j * S + s] = t;  // S == 1: partial is psi itself
-    }
-    __syncthreads();
-  }
+  for (int item = blockIdx.x; item < items; item += gridDim.x) fo_psi_item(item, Q, m, w, partial, S);
 }
 __global__ void k_fo_psi_sum(const int* __restrict__ cnt, int plus, int S, const double* __restrict__ partial,
                              double* __restrict__ psi) {

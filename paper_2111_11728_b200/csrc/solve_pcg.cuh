@@ -5,6 +5,205 @@
 
 namespace fg {
 
+// ------------------------------------------- K15: persistent iteration ---
+// Per dual row the (subdomain, local index, coefficient) entries of a map
+// (operator or preconditioner) and one designated storing entry per row;
+// false if some row has more than two entries (or none, unless allowed: the
+// T-FETI operator maps skip the fixing DOFs).
+static bool persist_rows(const std::vector<OpSub>& subs, const std::vector<int>& rows, const std::vector<double>& cf,
+                         int KR, int m, bool allow_empty, std::vector<int4>& ent, std::vector<double2>& cc,
+                         std::vector<unsigned char>& wr) {
+  ent.assign(m, make_int4(-1, 0, -1, 0));
+  cc.assign(m, make_double2(0.0, 0.0));
+  wr.assign(rows.size(), 0);
+  std::vector<int> n(m, 0);
+  for (int s = 0; s < (int)subs.size(); ++s)
+    for (int a = 0; a < subs[s].ns; ++a)
+      for (int k = 0; k < KR; ++k) {
+        const size_t e = (size_t)subs[s].map_off + (size_t)a * KR + k;
+        const int r = rows[e];
+        if (r < 0) continue;
+        if (r >= m || n[r] == 2) return false;
+        if (n[r] == 0) { ent[r].x = s; ent[r].y = a; cc[r].x = cf[e]; wr[e] = 1; }
+        else { ent[r].z = s; ent[r].w = a; cc[r].y = cf[e]; }
+        ++n[r];
+      }
+  for (int r = 0; r < m; ++r)   // no entry: the atomic path leaves 0 there (row_combine too)
+    if (n[r] == 0 && !allow_empty) return false;
+  return true;
+}
+
+bool Ctx::persist_prepare() {
+  if (p_state) return p_state > 0;
+  p_state = -1;
+  const int Ns = su.Ns, m = su.m;
+  auto down = [&](auto& dbuf, size_t n, auto& vec) {
+    vec.resize(n);
+    if (n) CK(cudaMemcpyAsync(vec.data(), dbuf.p, n * sizeof(vec[0]), cudaMemcpyDeviceToHost, st));
+  };
+  std::vector<OpSub> ops, pcs;
+  down(d_op, Ns, ops);
+  down(d_pc, Ns, pcs);
+  CK(cudaStreamSynchronize(st));
+  size_t nop = 0, npc = 0;
+  for (auto& d : ops) nop = std::max(nop, (size_t)d.map_off + (size_t)d.ns * KR);
+  for (auto& d : pcs) npc = std::max(npc, (size_t)d.map_off + (size_t)d.ns * KRp);
+  std::vector<int> orow, prow;
+  std::vector<double> ocf, pcf;
+  down(d_oprows, nop, orow);
+  down(d_opcoef_apply, nop, ocf);
+  down(d_pcrows, npc, prow);
+  down(d_pccoef, npc, pcf);
+  CK(cudaStreamSynchronize(st));
+  std::vector<int4> oe, pe;
+  std::vector<double2> oc, pc;
+  std::vector<unsigned char> ow, pw;
+  if (!persist_rows(ops, orow, ocf, KR, m, true, oe, oc, ow) || !persist_rows(pcs, prow, pcf, KRp, m, false, pe, pc, pw))
+    return false;
+  std::vector<int> vo(Ns), vp(Ns);
+  int to = 0, tp = 0;
+  for (int s = 0; s < Ns; ++s) {
+    vo[s] = to; to += ops[s].ns;
+    vp[s] = tp; tp += pcs[s].ns;
+  }
+  if (su.method == FETIGPU_FETIDP) {
+    down(d_voff, Ns, vo);   // phase 2 reads v_s at DpSub::v_off (= d_voff) of d_vbuf
+    CK(cudaStreamSynchronize(st));
+  } else {
+    p_vop.alloc(std::max(1, to));
+    p_voff_op.upload(vo, st);
+  }
+  p_vpc.alloc(std::max(1, tp));
+  p_voff_pc.upload(vp, st);
+  p_op_ent.upload(oe, st); p_op_c.upload(oc, st);
+  p_pc_ent.upload(pe, st); p_pc_c.upload(pc, st); p_pc_wr.upload(pw, st);
+  p_w2.alloc(m);
+  p_r2.alloc(m);
+  p_bar.alloc(2);
+  CK(cudaStreamSynchronize(st));
+  p_state = 1;
+  return true;
+}
+
+// Applicable where the loop runs on the plain per-subdomain operators (no
+// symmetric-packed tiles, dense L2-resident coarse inverse): C1-C3 and C5
+// single / FO.  FETIGPU_PERSIST=0 selects the graph loop, =1 forces this one; FETIGPU_PERSIST_G
+// sets the grid; FETIGPU_PERSIST_BAR=grid|cluster the barrier (a grid of at
+// most 16 CTAs runs as one thread-block cluster by default).
+int Ctx::persist_grid(bool fo) {
+  const char* e = getenv("FETIGPU_PERSIST");
+  if (e && e[0] == '0') return 0;
+  if (su.m == 0 || use_sym || pc_sym || (KRp != 1 && KRp != 3)) return 0;
+  if (su.method == FETIGPU_FETIDP && (use_csym || KR != 1)) return 0;
+  if (su.method == FETIGPU_TFETI && KR != 3) return 0;
+  // measured policy (tools/persist_ab.py): the persistent loop
+  // wins where an iteration is latency-bound -- operators of a few MB (C1:
+  // 25 vs 34 us, C2: 30 vs 35 us per iteration) and FO with short vectors
+  // (C1-fo 35 vs 43 us); where the operators stream tens of MB (C3) or the
+  // CGS sweeps dominate (C2-fo: equal), the graph's many-CTA kernels keep
+  // more loads in flight than one CTA per SM and stay faster.
+  // FETIGPU_PERSIST=1 forces it wherever it applies.
+  const bool force = e && e[0] == '1';
+  if (!force && (op_bytes > 32e6 || (fo && su.m > 2048))) return 0;
+  if (!persist_prepare()) return 0;
+  int dev = 0, sms = 0;
+  CK(cudaGetDevice(&dev));
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  int occ = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_pcg_persist<GridBarrier, true, true>, kThreads,
+                                                   persist_smem()));
+  if (occ < 1) return 0;
+  int G = sms * std::min(occ, kPersistOcc);
+  const char* eg = getenv("FETIGPU_PERSIST_G");
+  if (eg && atoi(eg) > 0) G = atoi(eg);
+  G = std::min(G, sms * occ);
+  const char* eb = getenv("FETIGPU_PERSIST_BAR");
+  persist_cluster = G <= 16 && !(eb && strcmp(eb, "grid") == 0);
+  (void)fo;
+  return G;
+}
+
+size_t Ctx::persist_smem() const {
+  const bool tf = su.method == FETIGPU_TFETI;
+  const int sv = !persist_red() ? 0 : tf ? (3 * su.Ns <= kRedH ? 3 * su.Ns : 0) : (su.Nc <= kRedU ? su.Nc : 0);
+  return (size_t)(std::max(max_ld, max_pc_ld) + sv) * 8;
+}
+
+void Ctx::launch_persist(int G, bool fo, int passes, int psi_S, double* lam, double* r, double* z, double* w,
+                         double* q, Scal* sc, double* Wst, double* Qst, double* psi, double* psi_part, int* cnt,
+                         IterCtl* ctl, double* trace) {
+  const bool tf = su.method == FETIGPU_TFETI;
+  PersistArgs a{};
+  a.m = su.m;
+  a.Ns = su.Ns;
+  a.Nc = su.Nc;
+  a.KRp = KRp;
+  a.nz_op = std::max(1, std::min(8, G / su.Ns));   // one round of (subdomain, slice) items
+  a.nz_pc = a.nz_op;
+  a.ndot = dot_blocks();
+  a.psi_S = psi_S;
+  a.passes = passes;
+  a.xs_len = std::max(max_ld, max_pc_ld);
+  a.redU = !tf && persist_red() && su.Nc <= kRedU;
+  a.redH = tf && persist_red() && 3 * su.Ns <= kRedH;
+  a.op = d_op.p; a.opmat = d_opmat.p; a.oprows = d_oprows.p; a.opcoef = d_opcoef_apply.p;
+  a.vop = tf ? p_vop.p : d_vbuf.p;
+  a.voff_op = tf ? p_voff_op.p : d_voff.p;
+  a.op_ent = p_op_ent.p; a.op_c = p_op_c.p;
+  if (!tf) {
+    a.dp = d_dp.p; a.abc = d_abc.p; a.tbuf = d_tbuf.p; a.cg = su.Nc ? d_cgather.p : nullptr;
+    a.cmap = d_cmap.p; a.Kinv = d_Kinv.p; a.gc = d_gc.p;
+  } else {
+    a.pj = d_pj.p; a.pjcoef = d_pjcoef.p; a.RT = d_RT.p; a.rt_off = d_rt_off.p; a.H = d_H.p;
+    a.pj_sr = d_pjrow_sr.p; a.pj_c = d_pjrow_c.p; a.g = d_g.p;
+  }
+  a.h = d_h.p;
+  a.pc = d_pc.p; a.pcmat = d_pcmat.p; a.pcrows = d_pcrows.p; a.pccoef = d_pccoef.p;
+  a.vpc = p_vpc.p; a.voff_pc = p_voff_pc.p;
+  a.pc_ent = p_pc_ent.p; a.pc_c = p_pc_c.p; a.pc_wr = p_pc_wr.p;
+  a.lam = lam; a.r = r; a.z = z; a.w = w; a.q = q; a.w2 = p_w2.p; a.r2 = p_r2.p;
+  a.sc = sc;
+  a.partial = d_partial.p;
+  a.Wst = Wst; a.Qst = Qst; a.psi = psi; a.psi_part = psi_part; a.cnt = cnt;
+  a.ctl = ctl;
+  a.trace = trace;
+  CK(cudaMemsetAsync(p_bar.p, 0, 2 * sizeof(unsigned int), st));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(G);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = persist_smem();
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  auto go = [&](auto kern, auto barrier) {
+    if (persist_cluster) {
+      if (G > 8) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = G;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+    }
+    CK(cudaLaunchKernelEx(&cfg, kern, a, barrier));
+  };
+  const GridBarrier gb{p_bar.p, p_bar.p + 1};
+  const ClusterBarrier cb{p_bar.p, p_bar.p + 1};
+  if (persist_cluster) {
+    if (tf && fo) go(k_pcg_persist<ClusterBarrier, true, true>, cb);
+    else if (tf) go(k_pcg_persist<ClusterBarrier, true, false>, cb);
+    else if (fo) go(k_pcg_persist<ClusterBarrier, false, true>, cb);
+    else go(k_pcg_persist<ClusterBarrier, false, false>, cb);
+  } else {
+    if (tf && fo) go(k_pcg_persist<GridBarrier, true, true>, gb);
+    else if (tf) go(k_pcg_persist<GridBarrier, true, false>, gb);
+    else if (fo) go(k_pcg_persist<GridBarrier, false, true>, gb);
+    else go(k_pcg_persist<GridBarrier, false, false>, gb);
+  }
+  LAUNCH_CHECK();
+}
+
 // ----------------------------------------------------------- the engine ---
 // pcg single / FO: z = P Fbar^{-1} P r, eps_r = sqrt(r^T z)
 // (PAPER.md:384); FO keeps F-normalized directions and re-orthogonalizes by
@@ -159,7 +358,16 @@ int Ctx::solve(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_trace* 
     CK(cudaMemcpyAsync(dctl.p, &h0, sizeof(IterCtl), cudaMemcpyHostToDevice, st));
     CK(cudaStreamSynchronize(st));
     bool built_ok = false;
-    if (cudaGraphCreate(&graph, 0) == cudaSuccess) {
+    // K15: the whole loop as one persistent kernel where the operators are
+    // the plain per-subdomain ones (C1-C3, C5 single / FO); bit-identical
+    // to the graph below (kernels_persist.cuh)
+    const int pg = persist_grid(fo);
+    if (pg > 0) {
+      launch_persist(pg, fo, passes, psi_S, lam.p, r.p, z.p, w.p, q.p, sc.p, Wst.p, Qst.p, psi.p, psi_part.p, cnt.p,
+                     dctl.p, dtrace.p);
+      built_ok = true;
+      solve_loop = persist_cluster ? 3 : 2;
+    } else if (cudaGraphCreate(&graph, 0) == cudaSuccess) {
       cudaGraphConditionalHandle hcond;
       cudaGraphNodeParams cp = {};
       cudaGraphNode_t cnode;
@@ -188,7 +396,10 @@ int Ctx::solve(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_trace* 
       if (graph) { cudaGraphDestroy(graph); graph = nullptr; }
       device_loop = false;
     } else {
-      CK(cudaGraphLaunch(exec, st));
+      if (pg <= 0) {
+        CK(cudaGraphLaunch(exec, st));
+        solve_loop = 1;
+      }
       IterCtl hc;
       CK(cudaMemcpyAsync(&hc, dctl.p, sizeof(IterCtl), cudaMemcpyDeviceToHost, st));
       CK(cudaStreamSynchronize(st));
@@ -207,6 +418,7 @@ int Ctx::solve(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_trace* 
     }
   }
   if (!device_loop) {
+    solve_loop = 0;
     CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
     body(true);
     CK(cudaStreamEndCapture(st, &graph));

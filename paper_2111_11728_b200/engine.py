@@ -117,7 +117,7 @@ class FgStats(C.Structure):
                [(k, C.c_double) for k in ("op_bytes", "op_flops_per_col", "main_kernel_bytes",
                                           "build_ms", "nd_ms", "slot_ms", "coarse_ms",
                                           "device_bytes")] + \
-               [("host_pipeline", C.c_int), ("reserved_", C.c_int), ("stream_bytes", C.c_double)]
+               [("host_pipeline", C.c_int), ("solve_loop", C.c_int), ("stream_bytes", C.c_double)]
 
 
 def lib():
