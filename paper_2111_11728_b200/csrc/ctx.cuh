@@ -137,7 +137,13 @@ struct Ctx {
   // lam := lambda0 of the solve: the warm start when one is set (T-FETI:
   // projected onto G lambda = e: lam0 + P(warm - lam0)), else the default
   void init_lambda(double* lam);
+  // side stream of the block apply (Q memset overlapping the coarse GEMM)
+  cudaStream_t aux_st = nullptr;
+  cudaEvent_t aux_fork = nullptr, aux_join = nullptr;
   ~Ctx() {
+    if (aux_fork) cudaEventDestroy(aux_fork);
+    if (aux_join) cudaEventDestroy(aux_join);
+    if (aux_st) cudaStreamDestroy(aux_st);
     for (auto& e : pipe_in) if (e) cudaEventDestroy(e);
     for (auto& e : pipe_done) if (e) cudaEventDestroy(e);
     if (pipe_start) cudaEventDestroy(pipe_start);

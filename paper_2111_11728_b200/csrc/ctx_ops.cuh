@@ -354,8 +354,33 @@ void Ctx::apply_precond(const double* r, double* z, double* Zcols, bool row_majo
 
 void Ctx::apply_F_block(const double* W, int ldw, double* Q, int ldq, int k) {
   const int Ns = su.Ns, m = su.m;
-  if (ldq == k) CK(cudaMemsetAsync(Q, 0, (size_t)m * k * 8, st));
-  else CK(cudaMemset2DAsync(Q, (size_t)ldq * 8, 0, (size_t)k * 8, m, st));
+  // Q is zeroed for K5's scatter.  FETI-DP: on a side stream while the DMMA
+  // GEMM of U runs (HBM-bound memset vs FP64-bound GEMM), joined before K5
+  // (FETIGPU_K5_SERIAL=1: on the main stream)
+  static const bool serial = [] {
+    const char* e = getenv("FETIGPU_K5_SERIAL");
+    return e && e[0] == '1';
+  }();
+  const bool side = su.method == FETIGPU_FETIDP && !serial;
+  cudaStream_t zs = st;
+  if (side) {
+    if (!aux_st) {
+      CK(cudaStreamCreateWithFlags(&aux_st, cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&aux_fork, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&aux_join, cudaEventDisableTiming));
+    }
+    zs = aux_st;
+  }
+  auto zero_q = [&]() {
+    if (side) {
+      CK(cudaEventRecord(aux_fork, st));
+      CK(cudaStreamWaitEvent(aux_st, aux_fork, 0));
+    }
+    if (ldq == k) CK(cudaMemsetAsync(Q, 0, (size_t)m * k * 8, zs));
+    else CK(cudaMemset2DAsync(Q, (size_t)ldq * 8, 0, (size_t)k * 8, m, zs));
+    if (side) CK(cudaEventRecord(aux_join, aux_st));
+  };
+  if (!side) zero_q();
   // K5 walks the subdomains in 4 x 4-module tiles: both neighbours sharing a
   // dual row (left/right and below/above) are processed close in time, so
   // the W rows of an interface are read from DRAM about once
@@ -372,6 +397,10 @@ void Ctx::apply_F_block(const double* W, int ldw, double* Q, int ldq, int k) {
     const char* e = getenv("FETIGPU_K5_ROWMAJOR");
     return !(e && e[0] == '1');
   }();
+  static const bool pre_tiled = [] {   // the coarse pre-pass in the same walk (FETIGPU_DPT_TILED=0: natural)
+    const char* e = getenv("FETIGPU_DPT_TILED");
+    return tiled && !(e && e[0] == '0');
+  }();
   BlockApplyArgs a{d_op.p, d_opmat.p, d_oprows.p, d_opcoef_apply.p, KR, nullptr, nullptr, nullptr, nullptr, 0,
                    W, ldw, Q, ldq, k, tiled ? d_k5order.p : nullptr};
   int max_ns = 0;
@@ -383,15 +412,17 @@ void Ctx::apply_F_block(const double* W, int ldw, double* Q, int ldq, int k) {
       const size_t smem = ((size_t)std::max(max_ns * 8, 4 * 8 * kDpTCols) + max_ns) * 8 + (size_t)max_ns * 4;
       raise_smem_limit(k_block_dp_t, smem);
       k_block_dp_t<<<dim3((k + kDpTCols - 1) / kDpTCols, Ns), 256, smem, st>>>(
-          d_op.p, d_dp.p, d_oprows.p, d_opcoef_apply.p, d_abc.p, W, ldw, k, blk_t.p, k);
+          d_op.p, d_dp.p, d_oprows.p, d_opcoef_apply.p, d_abc.p, W, ldw, k, blk_t.p, k, pre_tiled ? d_k5order.p : nullptr);
     }
     k_coarse_gather_block<<<dim3((k + 255) / 256, Nc), 256, 0, st>>>(d_optr.p, d_oidx.p, blk_t.p, k, Nc, k,
                                                                      blk_T.p, k);
+    zero_q();   // side stream: overlaps the FP64-bound GEMM, not the HBM-bound pre-pass
     // U = Kbar^{-1} T  (row-major N_c x k == column-major k x N_c: U^T = T^T Kinv)
     gemm(st, false, false, k, Nc, Nc, 1.0, blk_T.p, k, d_Kinv.p, Nc, 0.0, blk_U.p, k);
     a.dps = d_dp.p; a.abc = d_abc.p; a.cmap = d_cmap.p; a.U = blk_U.p; a.ldu = k;
     max_ns += 8;
   }
+  if (side) CK(cudaStreamWaitEvent(st, aux_join, 0));
   dim3 grid((k + kBN - 1) / kBN, (max_ns + kBM - 1) / kBM, Ns);
   const bool fast = folded && blk_aligned && (k % 2 == 0) && (ldw % 2 == 0) && (ldq % 2 == 0) &&
                     ((uintptr_t)W % 16 == 0) && ((uintptr_t)Q % 16 == 0);

@@ -438,10 +438,13 @@ __global__ void __launch_bounds__(256) k_block_dp_t(const OpSub* __restrict__ su
                                                     const double* __restrict__ coefs,
                                                     const double* __restrict__ abc,
                                                     const double* __restrict__ W, int ldw, int k,
-                                                    double* __restrict__ tbuf, int ldt) {
-  // (coefs are the apply coefficients: unit when the operators are sign-folded)
+                                                    double* __restrict__ tbuf, int ldt,
+                                                    const int* __restrict__ order = nullptr) {
+  // (coefs are the apply coefficients: unit when the operators are sign-folded;
+  // order: K5's 4 x 4-module subdomain walk, so both owners of a dual row read
+  // its W row close in time -- the second read hits L2)
   extern __shared__ double dsm[];
-  const int s = blockIdx.y;
+  const int s = order ? order[blockIdx.y] : blockIdx.y;
   const OpSub d = subs[s];
   const DpSub p = dps[s];
   const int ns = d.ns;
