@@ -418,6 +418,10 @@ struct Ctx {
     return on;
   }
   int persist_grid(bool fo);
+  std::vector<int> pc_nsld;   // per subdomain: n_s x ld of its preconditioner matrix (K15c)
+  size_t cluster_smem() const;
+  bool cluster_ok(bool fo);
+  void launch_cluster(double* lam, double* r, double* w, Scal* sc, IterCtl* ctl, double* trace);
   void launch_persist(int G, bool fo, int passes, int psi_S, double* lam, double* r, double* z, double* w, double* q,
                       Scal* sc, double* Wst, double* Qst, double* psi, double* psi_part, int* cnt, IterCtl* ctl,
                       double* trace);

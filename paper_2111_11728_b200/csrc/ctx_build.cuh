@@ -538,10 +538,12 @@ void Ctx::build_ops(const SlotOut& so, std::future<HostMaps>& maps) {
     CK(cudaStreamSynchronize(st));
   }
   ptimer.mark("preconditioner slots", st);
+  pc_nsld.assign(Ns, 0);
   for (int s = 0; s < Ns; ++s) {
     const int sl = su.subs[s].pc_slot;
     h.pcs[s].moff = pc_moff[sl];
     h.pcs[s].ld = pc_ld[sl];
+    pc_nsld[s] = h.pcs[s].ns * h.pcs[s].ld;
   }
   d_pc.upload(h.pcs, st);
   d_op.upload(h.ops, st);

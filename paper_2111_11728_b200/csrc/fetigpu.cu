@@ -255,6 +255,7 @@ int fetigpu_rebuild(fetigpu_ctx* ctx, const fetigpu_problem* p) {
     c.su = std::move(su);
     c.have_rhs = false;
     c.bz_state = 0;
+    c.p_state = 0;   // K15 row maps are re-derived from the rebuilt operators
     c.built = false;
     struct Scope {
       BlockCache* prev;

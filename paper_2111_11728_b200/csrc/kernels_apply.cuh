@@ -116,7 +116,7 @@ __device__ __forceinline__ void gather_xs(const OpSub& d, const int* __restrict_
 
 // the row part of the K4/K7 GEMV for one CTA (rows i = warp + 8 zi, + 8 nz,
 // ...): v_i = F_s[i,:] x_s, stored (STORE_V) or scattered with the map's signs
-template <int KR, bool STORE_V>
+template <int KR, bool STORE_V, bool ASM = false>   // ASM: the matrix in shared memory
 __device__ __forceinline__ void gemv_rows_cta(int s, int col, int zi, int nz, const double* xs, const OpSub& d,
                                               const double* __restrict__ mats, const int* __restrict__ rows,
                                               const double* __restrict__ coefs, double* y, double* zcols, int ldz,
@@ -148,6 +148,7 @@ __device__ __forceinline__ void gemv_rows_cta(int s, int col, int zi, int nz, co
   const int n2 = d.ld >> 1;
   // R rows i, i + nw, ... streamed together: each row keeps its own two
   // lane-strided chains (acc0 even / acc1 odd columns), exactly as one at a time
+  auto lda = [&](const double2* p) { return ASM ? *p : __ldcs(p); };
   auto rowblk = [&](int i, auto rc) {
     constexpr int R = decltype(rc)::value;
     const double2* Ar[R];
@@ -163,8 +164,8 @@ __device__ __forceinline__ void gemv_rows_cta(int s, int col, int zi, int nz, co
       double2 a0[R], a1[R];
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        a0[r] = __ldcs(Ar[r] + j);
-        a1[r] = __ldcs(Ar[r] + j + 32);
+        a0[r] = lda(Ar[r] + j);
+        a1[r] = lda(Ar[r] + j + 32);
       }
 #pragma unroll
       for (int r = 0; r < R; ++r) {
@@ -177,7 +178,7 @@ __device__ __forceinline__ void gemv_rows_cta(int s, int col, int zi, int nz, co
     for (; j < n2; j += 32) {
       double2 a0[R];
 #pragma unroll
-      for (int r = 0; r < R; ++r) a0[r] = __ldcs(Ar[r] + j);
+      for (int r = 0; r < R; ++r) a0[r] = lda(Ar[r] + j);
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         acc0[r] = fma(a0[r].x, xs[2 * j], acc0[r]);
@@ -508,9 +509,13 @@ __global__ void __launch_bounds__(512) k_csym_reduce(const double* __restrict__ 
 // rows i = warp0, warp0 + nwarps, ... of y = M x (one warp per row; a row's
 // result does not depend on the warp count).  x through L2 (__ldcg): the
 // persistent solver loop produces it in-kernel.
+// SM: M and x in shared memory (the cluster-resident loop), plain loads
+template <bool SM = false>
 __device__ __forceinline__ void dense_gemv_warps(const double* __restrict__ M, int n, const double* x,
                                                  double* y, int warp0, int nwarps) {
   const int lane = threadIdx.x & 31;
+  auto ldm = [&](const double2* p) { return SM ? *p : __ldcs(p); };
+  auto ldx = [&](const double* p) { return SM ? *p : __ldcg(p); };
   // one row's chains (a0..a3 over lane-strided double2 pairs, then warp_sum)
   auto row = [&](int i) {
     const double* Mi = M + (size_t)i * n;
@@ -520,19 +525,19 @@ __device__ __forceinline__ void dense_gemv_warps(const double* __restrict__ M, i
       const int n2 = n >> 1;
       int j = lane;
       for (; j + 32 < n2; j += 64) {
-        const double2 u = __ldcs(M2 + j), v = __ldcs(M2 + j + 32);
-        a0 = fma(u.x, __ldcg(x + 2 * j), a0);
-        a1 = fma(u.y, __ldcg(x + 2 * j + 1), a1);
-        a2 = fma(v.x, __ldcg(x + 2 * j + 64), a2);
-        a3 = fma(v.y, __ldcg(x + 2 * j + 65), a3);
+        const double2 u = ldm(M2 + j), v = ldm(M2 + j + 32);
+        a0 = fma(u.x, ldx(x + 2 * j), a0);
+        a1 = fma(u.y, ldx(x + 2 * j + 1), a1);
+        a2 = fma(v.x, ldx(x + 2 * j + 64), a2);
+        a3 = fma(v.y, ldx(x + 2 * j + 65), a3);
       }
       for (; j < n2; j += 32) {
-        const double2 u = __ldcs(M2 + j);
-        a0 = fma(u.x, __ldcg(x + 2 * j), a0);
-        a1 = fma(u.y, __ldcg(x + 2 * j + 1), a1);
+        const double2 u = ldm(M2 + j);
+        a0 = fma(u.x, ldx(x + 2 * j), a0);
+        a1 = fma(u.y, ldx(x + 2 * j + 1), a1);
       }
     } else {
-      for (int j = lane; j < n; j += 32) a0 = fma(Mi[j], __ldcg(x + j), a0);
+      for (int j = lane; j < n; j += 32) a0 = fma(Mi[j], ldx(x + j), a0);
     }
     return warp_sum((a0 + a1) + (a2 + a3));
   };
@@ -780,7 +785,8 @@ __global__ void k_dot_final(const double* partial, int npairs, double* out) {
 // the NP operand pairs of row i (loads, or values the persistent loop forms
 // on the fly); each pair accumulates fma(x, y, acc) in row order.
 template <int NP, class F>
-__device__ __forceinline__ void dot_partial_rows(int vb, int nvb, int n, double* partial, F&& f) {
+__device__ __forceinline__ void dot_partial_rows(int vb, int nvb, int n, double* partial, F&& f,
+                                                 int pstride = kDotBlocks) {
   double acc[NP];
 #pragma unroll
   for (int k = 0; k < NP; ++k) acc[k] = 0.0;
@@ -802,7 +808,7 @@ __device__ __forceinline__ void dot_partial_rows(int vb, int nvb, int n, double*
   if (threadIdx.x < NP) {
     double v = 0.0;
     for (int w = 0; w < kThreads / 32; ++w) v += red[threadIdx.x][w];
-    partial[threadIdx.x * kDotBlocks + vb] = v;
+    partial[threadIdx.x * pstride + vb] = v;
   }
 }
 // operands through L2 (__ldcg)
@@ -825,10 +831,11 @@ __device__ __forceinline__ void dot_partial_cta(const DotArgs& args, int vb, int
   }
 }
 // final fixed-order sum of pair k over nvb partials (one warp; every lane returns it)
-__device__ __forceinline__ double dot_final_warp(const double* partial, int k, int nvb) {
+template <bool SM = false>   // SM: partials in shared memory (stride pstride)
+__device__ __forceinline__ double dot_final_warp(const double* partial, int k, int nvb, int pstride = kDotBlocks) {
   const int lane = threadIdx.x & 31;
   double a = 0.0;
-  for (int b = lane; b < nvb; b += 32) a += __ldcg(partial + k * kDotBlocks + b);
+  for (int b = lane; b < nvb; b += 32) a += SM ? partial[k * pstride + b] : __ldcg(partial + k * pstride + b);
   return warp_sum(a);
 }
 
@@ -886,6 +893,16 @@ __device__ __forceinline__ void fo_sub_cta(int vb, const double* W, int m, int c
     // four loads in flight per warp, then the FMAs in the same order as the
     // plain loop (bit-identical); otherwise each load waits for the last FMA
     int j = warp;
+    for (; j + 120 < c; j += 128) {   // 16 columns in flight
+      double wv[16], pv[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        wv[u] = __ldcs(W + (size_t)(j + 8 * u) * m + i);
+        pv[u] = __ldcg(psi + j + 8 * u);
+      }
+#pragma unroll
+      for (int u = 0; u < 16; ++u) v = fma(wv[u], pv[u], v);
+    }
     for (; j + 24 < c; j += 32) {
       const double w0 = __ldcs(W + (size_t)j * m + i), w1 = __ldcs(W + (size_t)(j + 8) * m + i),
                    w2 = __ldcs(W + (size_t)(j + 16) * m + i), w3 = __ldcs(W + (size_t)(j + 24) * m + i);

@@ -446,3 +446,273 @@ __global__ void __launch_bounds__(kThreads, kPersistOcc) k_pcg_persist(const Per
 }
 
 }  // namespace fg
+
+namespace fg {
+
+// ------------------------------------------------------------------------
+// K15c: the cluster-resident loop -- T-FETI, single direction, N_s <= 16
+// subdomains whose explicit operators fit in one thread-block cluster's
+// shared memory (C1: 8 x ~160 KB).  CTA s of the cluster keeps F_s and S~_s in
+// its shared memory for the whole solve and a replica of every dual vector
+// (m doubles each); a subdomain's GEMV result v_s stays in its CTA and the
+// others read it through distributed shared memory (DSMEM) when they form
+// the dual rows.  Scalars (dots, projector coarse vectors H g) are evaluated
+// redundantly and identically by every CTA, so an iteration needs two
+// cluster barriers and no global-memory traffic.  Same expressions, same
+// orders as the graph loop (bit-identical, tests/test_gpu_persist.py).
+// ------------------------------------------------------------------------
+struct ClusterArgs {
+  int m, Ns, ndot, KRp;
+  int fs_len, ps_len, xs_len, pad;   // shared-memory regions (uniform across the cluster)
+  const OpSub* op;
+  const double* opmat;
+  const int* oprows;
+  const double* opcoef;
+  const OpSub* pc;
+  const double* pcmat;
+  const int* pcrows;
+  const double* pccoef;
+  const int4* op_ent;
+  const double2* op_c;
+  const int4* pc_ent;
+  const double2* pc_c;
+  const OpSub* pj;
+  const double* pjcoef;
+  const double* RT;
+  const int* rt_off;
+  const double* H;
+  const int2* pj_sr;
+  const double2* pj_c;
+  double *lam, *r, *w;   // global iterates: start values in, lambda out
+  Scal* sc;
+  IterCtl* ctl;
+  double* trace;
+};
+
+// shared-memory doubles of k_pcg_cluster (every region a multiple of two
+// doubles, so the double2 loads of the GEMV rows stay 16-byte aligned)
+__host__ __device__ constexpr int even_up(int n) { return (n + 1) & ~1; }
+__host__ __device__ constexpr size_t cluster_smem_doubles(int m, int Ns, int ndot, int fs, int ps, int xs) {
+  return (size_t)even_up(fs) + even_up(ps) + 5 * (size_t)even_up(m) + 3 * (size_t)even_up(xs) +
+         3 * (size_t)even_up(3 * Ns) + (size_t)even_up(9 * Ns * Ns) + 4 * (size_t)ndot;
+}
+
+// g_s = sign R_T^T (B_s^T v) by ONE warp, emulating proj_gather_fn's CTA
+// reduction: the 8 virtual warps' lane-strided sums, warp_sum each, then the
+// fixed-order sum over virtual warps
+template <class VV>
+__device__ __forceinline__ void proj_gather_warp(int s, const OpSub* __restrict__ psubs, const int* __restrict__ rows,
+                                                 const double* __restrict__ coefs, const double* __restrict__ RT,
+                                                 const int* __restrict__ rt_off, double* g, double sign, VV&& vval) {
+  const OpSub d = psubs[s];
+  const double* R = RT + rt_off[s];
+  const int lane = threadIdx.x & 31;
+  constexpr int VW = kThreads / 32;
+  // the 8 virtual warps' chains are independent until the final ordered sum:
+  // all of them in flight at once (unrolled), each with its own accumulators
+  double a0[VW], a1[VW], a2[VW];
+#pragma unroll
+  for (int vw = 0; vw < VW; ++vw) {
+    a0[vw] = 0; a1[vw] = 0; a2[vw] = 0;
+  }
+  for (int jb = 0; jb < d.ns; jb += kThreads) {
+#pragma unroll
+    for (int vw = 0; vw < VW; ++vw) {
+      const int j = jb + vw * 32 + lane;
+      if (j < d.ns) {
+        double xj = 0.0;
+        for (int k = 0; k < 3; ++k) {
+          const int r = rows[d.map_off + j * 3 + k];
+          if (r >= 0) xj += coefs[d.map_off + j * 3 + k] * vval(r);
+        }
+        a0[vw] += R[j * 3] * xj;
+        a1[vw] += R[j * 3 + 1] * xj;
+        a2[vw] += R[j * 3 + 2] * xj;
+      }
+    }
+  }
+  double t0 = 0.0, t1 = 0.0, t2 = 0.0;
+#pragma unroll
+  for (int vw = 0; vw < VW; ++vw) {
+    t0 += warp_sum(a0[vw]);
+    t1 += warp_sum(a1[vw]);
+    t2 += warp_sum(a2[vw]);
+  }
+  if (lane < 3) g[3 * s + lane] = sign * (lane == 0 ? t0 : lane == 1 ? t1 : t2);
+}
+
+template <int KRP>
+__global__ void __launch_bounds__(kThreads, 1) k_pcg_cluster(const ClusterArgs a) {
+  namespace cgr = cooperative_groups;
+  cgr::cluster_group cl = cgr::this_cluster();
+  extern __shared__ __align__(16) double sm[];
+  const int m = a.m, Ns = a.Ns, nc3 = 3 * Ns, nd = a.ndot;
+  const int s = (int)cl.block_rank();   // this CTA's subdomain
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int mp = even_up(m), xp = even_up(a.xs_len), n3p = even_up(nc3);
+  double* Fs = sm;
+  double* Ps = Fs + even_up(a.fs_len);
+  double* w = Ps + even_up(a.ps_len);
+  double* r = w + mp;
+  double* z = r + mp;
+  double* q = z + mp;
+  double* lam = q + mp;
+  double* vop = lam + mp;             // v_s = F_s x_s (read by the other CTAs)
+  double* vpc = vop + xp;             // S~_s x_s
+  double* xs = vpc + xp;
+  double* g = xs + xp;                // this CTA's g_s (slot 3 s .. 3 s + 2), read by the others
+  double* gall = g + n3p;             // every subdomain's g, gathered over DSMEM
+  double* h = gall + n3p;
+  double* Hs = h + n3p;
+  double* part = Hs + even_up(nc3 * nc3);
+  __shared__ double s_sum[4];
+  __shared__ int zoff[16];
+  if (tid < 16) zoff[tid] = 0;
+  OpSub dop = a.op[s], dpc = a.pc[s];
+  for (int i = tid; i < dop.ns * dop.ld; i += kThreads) Fs[i] = a.opmat[dop.moff + i];
+  for (int i = tid; i < dpc.ns * dpc.ld; i += kThreads) Ps[i] = a.pcmat[dpc.moff + i];
+  for (int i = tid; i < nc3 * nc3; i += kThreads) Hs[i] = a.H[i];
+  for (int i = tid; i < m; i += kThreads) {
+    w[i] = a.w[i];
+    r[i] = a.r[i];
+    lam[i] = a.lam[i];
+  }
+  OpSub lop = dop, lpc = dpc;
+  lop.moff = 0;
+  lpc.moff = 0;
+  double rz = a.sc->rz, rz_old = a.sc->rz_old, breakdown = a.sc->breakdown;
+  int it = a.ctl->it;
+  const int max_it = a.ctl->max_it, trace_cap = a.ctl->trace_cap;
+  const double target = a.ctl->target;
+  const bool lead = s == 0 && tid == 0;
+  // y_r = c1 v_{s1}[a1] + c2 v_{s2}[a2] with v in the owners' shared memory
+  auto combine = [&](int i, const int4* __restrict__ ent, const double2* __restrict__ cc, double* vloc) {
+    const int4 e = ent[i];
+    const double2 c = cc[i];
+    double y = 0.0;
+    if (e.x >= 0) y = __dadd_rn(y, __dmul_rn(c.x, cl.map_shared_rank(vloc, e.x)[e.y]));
+    if (e.z >= 0) y = __dadd_rn(y, __dmul_rn(c.y, cl.map_shared_rank(vloc, e.z)[e.w]));
+    return y;
+  };
+  // P-correction: g_s = -R_s^T B_s^T v by this CTA (the projector kernel's
+  // CTA reduction), every g_s over DSMEM, then h = H g in every CTA
+  auto proj_h = [&](const double* v) {
+    proj_gather_fn(s, 0, a.pj, a.pcrows, a.pjcoef, a.RT, a.rt_off, g, 0, -1.0, [&](int row) { return v[row]; });
+    cl.sync();
+    for (int t = tid; t < nc3; t += kThreads) gall[t] = cl.map_shared_rank(g, t / 3)[t];
+    __syncthreads();
+    dense_gemv_warps<true>(Hs, nc3, gall, h, warp, kThreads / 32);
+    __syncthreads();
+  };
+  auto sums = [&](int np) {
+    if (warp < np) {
+      const double v = dot_final_warp<true>(part, warp, nd, nd);
+      if (lane == 0) s_sum[warp] = v;
+    }
+    __syncthreads();
+  };
+  cl.sync();
+  bool first = true;
+  for (;;) {
+    if (!first) {
+      // ---- k_iter_control on this CTA's (identical) scalars; k_cg_dir2
+      sums(3);
+      rz = s_sum[0];
+      const double rr = s_sum[1], zz = s_sum[2];
+      if (lead) { a.sc->rz = rz; a.sc->rr = rr; a.sc->zz = zz; }
+      bool go = false;
+      if (breakdown != 0.0) {
+        if (lead) a.ctl->status = 2;
+      } else if (rz < -1e-14 * sqrt(rr) * sqrt(zz)) {
+        if (lead) a.ctl->err = 14;
+      } else {
+        const double eps = sqrt(fmax(rz, 0.0));
+        ++it;
+        if (lead) {
+          a.ctl->it = it;
+          a.ctl->eps = eps;
+          if (it < trace_cap) a.trace[it] = eps;
+        }
+        if (eps <= target) {
+          if (lead) a.ctl->status = 0;
+        } else if (it >= max_it) {
+          if (lead) a.ctl->status = 1;
+        } else {
+          go = true;
+        }
+      }
+      if (!go) break;
+      const double beta = rz / rz_old;
+      rz_old = rz;
+      if (lead) a.sc->rz_old = rz;
+      for (int i = tid; i < m; i += kThreads) w[i] = fma(beta, w[i], z[i]);
+      __syncthreads();
+    }
+    // ---- v_s = F_s B_s^T w
+    gather_xs<3>(dop, a.oprows, a.opcoef, xs, [&](int row, int) { return w[row]; });
+    __syncthreads();
+    gemv_rows_cta<3, true, true>(s, 0, 0, 1, xs, lop, Fs, a.oprows, a.opcoef, nullptr, nullptr, 0, vop, zoff, 0, 1);
+    cl.sync();
+    pprof_mark();
+    // ---- q rows over DSMEM; delta, wr; P-correction of q
+    for (int i = tid; i < m; i += kThreads) q[i] = combine(i, a.op_ent, a.op_c, vop);
+    __syncthreads();
+    for (int vb = 0; vb < nd; ++vb) {
+      dot_partial_rows<2>(vb, nd, m, part, [&](int i, double* x, double* y) {
+        x[0] = w[i]; y[0] = q[i];
+        x[1] = w[i]; y[1] = r[i];
+      }, nd);
+      __syncthreads();
+    }
+    sums(2);
+    const double delta = s_sum[0], wr = s_sum[1];
+    (void)wr;
+    pprof_mark();
+    proj_h(q);
+    pprof_mark();
+    // ---- k_pcg_update (replicated), then v_s = S~_s B~_s^T r
+    if (lead) a.sc->delta = delta;
+    const bool bd = !(delta > 0.0);
+    if (bd) {
+      breakdown = 1.0;
+      if (lead) a.sc->breakdown = 1.0;
+    } else {
+      const double alpha = rz / delta;
+      if (lead) a.sc->alpha = alpha;
+      for (int i = tid; i < m; i += kThreads) {
+        lam[i] = fma(alpha, w[i], lam[i]);
+        const double pq = __dadd_rn(q[i], proj_row_corr<true>(i, a.pj_sr, a.pj_c, a.RT, h));
+        r[i] = fma(-alpha, pq, r[i]);
+      }
+    }
+    __syncthreads();
+    gather_xs<KRP>(dpc, a.pcrows, a.pccoef, xs, [&](int row, int) { return r[row]; });
+    __syncthreads();
+    gemv_rows_cta<KRP, true, true>(s, 0, 0, 1, xs, lpc, Ps, a.pcrows, a.pccoef, nullptr, nullptr, 0, vpc, zoff, 0, 1);
+    cl.sync();
+    pprof_mark();
+    // ---- z = P (M r): rows over DSMEM, P-correction; rz, rr, zz
+    for (int i = tid; i < m; i += kThreads) z[i] = combine(i, a.pc_ent, a.pc_c, vpc);
+    __syncthreads();
+    pprof_mark();
+    proj_h(z);
+    pprof_mark();
+    for (int i = tid; i < m; i += kThreads) z[i] = __dadd_rn(z[i], proj_row_corr<true>(i, a.pj_sr, a.pj_c, a.RT, h));
+    __syncthreads();
+    for (int vb = 0; vb < nd; ++vb) {
+      dot_partial_rows<3>(vb, nd, m, part, [&](int i, double* x, double* y) {
+        x[0] = r[i]; y[0] = z[i];
+        x[1] = r[i]; y[1] = r[i];
+        x[2] = z[i]; y[2] = z[i];
+      }, nd);
+      __syncthreads();
+    }
+    pprof_mark();
+    first = false;
+  }
+  if (s == 0)
+    for (int i = tid; i < m; i += kThreads) a.lam[i] = lam[i];
+  cl.sync();   // no CTA leaves while another may still read its shared memory
+}
+
+}  // namespace fg

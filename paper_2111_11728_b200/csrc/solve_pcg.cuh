@@ -97,14 +97,13 @@ int Ctx::persist_grid(bool fo) {
   if (su.method == FETIGPU_FETIDP && (use_csym || KR != 1)) return 0;
   if (su.method == FETIGPU_TFETI && KR != 3) return 0;
   // measured policy (tools/persist_ab.py): the persistent loop
-  // wins where an iteration is latency-bound -- operators of a few MB (C1:
-  // 25 vs 34 us, C2: 30 vs 35 us per iteration) and FO with short vectors
-  // (C1-fo 35 vs 43 us); where the operators stream tens of MB (C3) or the
-  // CGS sweeps dominate (C2-fo: equal), the graph's many-CTA kernels keep
+  // wins where an iteration is latency-bound -- operators of a few MB (C1-fo:
+  // 34 vs 43 us, C2: 26 vs 35 us, C2-fo: 50 vs 58 us per iteration); where
+  // the operators stream tens of MB (C3) the graph's many-CTA kernels keep
   // more loads in flight than one CTA per SM and stay faster.
   // FETIGPU_PERSIST=1 forces it wherever it applies.
   const bool force = e && e[0] == '1';
-  if (!force && (op_bytes > 32e6 || (fo && su.m > 2048))) return 0;
+  if (!force && op_bytes > 32e6) return 0;
   if (!persist_prepare()) return 0;
   int dev = 0, sms = 0;
   CK(cudaGetDevice(&dev));
@@ -201,6 +200,69 @@ void Ctx::launch_persist(int G, bool fo, int passes, int psi_S, double* lam, dou
     else if (fo) go(k_pcg_persist<GridBarrier, false, true>, gb);
     else go(k_pcg_persist<GridBarrier, false, false>, gb);
   }
+  LAUNCH_CHECK();
+}
+
+// K15c: the cluster-resident loop (T-FETI single direction, N_s <= 16
+// subdomains whose F_s and S~_s fit in one CTA's shared memory each, C1).
+// FETIGPU_CLUSTER=0 disables it.
+size_t Ctx::cluster_smem() const {
+  int fs = 0, ps = 0, xs = std::max(max_ld, max_pc_ld);
+  for (size_t s = 0; s < op_ns.size(); ++s) fs = std::max(fs, op_ns[s] * op_ld[s]);
+  for (int s = 0; s < su.Ns; ++s) ps = std::max(ps, pc_nsld[s]);
+  return cluster_smem_doubles(su.m, su.Ns, dot_blocks(), fs, ps, xs) * 8;
+}
+
+bool Ctx::cluster_ok(bool fo) {
+  const char* e = getenv("FETIGPU_CLUSTER");
+  if (e && e[0] == '0') return false;
+  if (fo || su.method != FETIGPU_TFETI || su.Ns < 1 || su.Ns > 16 || su.m == 0 || KR != 3) return false;
+  if (use_sym || pc_sym || (KRp != 1 && KRp != 3) || (int)pc_nsld.size() != su.Ns) return false;
+  int dev = 0, optin = 0;
+  CK(cudaGetDevice(&dev));
+  CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  if (cluster_smem() + 1024 > (size_t)optin) return false;
+  return persist_prepare();
+}
+
+void Ctx::launch_cluster(double* lam, double* r, double* w, Scal* sc, IterCtl* ctl, double* trace) {
+  ClusterArgs a{};
+  a.m = su.m;
+  a.Ns = su.Ns;
+  a.ndot = dot_blocks();
+  a.KRp = KRp;
+  int fs = 0, ps = 0;
+  for (size_t s = 0; s < op_ns.size(); ++s) fs = std::max(fs, op_ns[s] * op_ld[s]);
+  for (int s = 0; s < su.Ns; ++s) ps = std::max(ps, pc_nsld[s]);
+  a.fs_len = fs;
+  a.ps_len = ps;
+  a.xs_len = std::max(max_ld, max_pc_ld);
+  a.op = d_op.p; a.opmat = d_opmat.p; a.oprows = d_oprows.p; a.opcoef = d_opcoef_apply.p;
+  a.pc = d_pc.p; a.pcmat = d_pcmat.p; a.pcrows = d_pcrows.p; a.pccoef = d_pccoef.p;
+  a.op_ent = p_op_ent.p; a.op_c = p_op_c.p; a.pc_ent = p_pc_ent.p; a.pc_c = p_pc_c.p;
+  a.pj = d_pj.p; a.pjcoef = d_pjcoef.p; a.RT = d_RT.p; a.rt_off = d_rt_off.p; a.H = d_H.p;
+  a.pj_sr = d_pjrow_sr.p; a.pj_c = d_pjrow_c.p;
+  a.lam = lam; a.r = r; a.w = w;
+  a.sc = sc;
+  a.ctl = ctl;
+  a.trace = trace;
+  const size_t smem = cluster_smem();
+  auto kern = KRp == 1 ? k_pcg_cluster<1> : k_pcg_cluster<3>;
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  if (su.Ns > 8) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(su.Ns);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = su.Ns;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  CK(cudaLaunchKernelEx(&cfg, kern, a));
   LAUNCH_CHECK();
 }
 
@@ -361,8 +423,13 @@ int Ctx::solve(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_trace* 
     // K15: the whole loop as one persistent kernel where the operators are
     // the plain per-subdomain ones (C1-C3, C5 single / FO); bit-identical
     // to the graph below (kernels_persist.cuh)
-    const int pg = persist_grid(fo);
-    if (pg > 0) {
+    const bool clus = cluster_ok(fo);
+    const int pg = clus ? 1 : persist_grid(fo);
+    if (clus) {
+      launch_cluster(lam.p, r.p, w.p, sc.p, dctl.p, dtrace.p);
+      built_ok = true;
+      solve_loop = 4;
+    } else if (pg > 0) {
       launch_persist(pg, fo, passes, psi_S, lam.p, r.p, z.p, w.p, q.p, sc.p, Wst.p, Qst.p, psi.p, psi_part.p, cnt.p,
                      dctl.p, dtrace.p);
       built_ok = true;

@@ -30,7 +30,7 @@ CASES = {
     "C2_roller_edge": lambda: pb.config2(sx=3, sy=2, n=8).replace(
         dirichlet=pb.left_clamp(3, 2, 8) + [(3 * 25 + 8, 0, 0.0)]),
 }
-KEYS = ("FETIGPU_PERSIST", "FETIGPU_PERSIST_G", "FETIGPU_PERSIST_BAR", "FETIGPU_PERSIST_RED")
+KEYS = ("FETIGPU_PERSIST", "FETIGPU_PERSIST_G", "FETIGPU_PERSIST_BAR", "FETIGPU_PERSIST_RED", "FETIGPU_CLUSTER")
 
 
 def solve(g, dirs, env, max_it=3000):
@@ -59,14 +59,19 @@ def same(a, b):
 @pytest.mark.parametrize("name", list(CASES))
 def test_persistent_equals_graph(name, dirs):
     from paper_2111_11728_b200 import engine
-    g = engine.FetiSystem(CASES[name]())
+    prob = CASES[name]()
+    g = engine.FetiSystem(prob)
     try:
-        ref = solve(g, dirs, {"FETIGPU_PERSIST": "0"})
+        ref = solve(g, dirs, {"FETIGPU_PERSIST": "0", "FETIGPU_CLUSTER": "0"})
         assert ref[2] == 1, "graph loop expected"
-        got = solve(g, dirs, {"FETIGPU_PERSIST": "1"})
+        got = solve(g, dirs, {"FETIGPU_PERSIST": "1", "FETIGPU_CLUSTER": "0"})
         assert got[2] == 2, f"persistent loop did not run (solve_loop {got[2]})"
         same(ref, got)
         print(name, dirs, ref[1]["iterations"], "iterations, bit-identical")
+        if dirs == 0 and prob.method == 0 and g.stats()["n_sub"] <= 16:
+            clu = solve(g, dirs, {"FETIGPU_CLUSTER": "1"})
+            assert clu[2] == 4, f"cluster-resident loop did not run (solve_loop {clu[2]})"
+            same(ref, clu)
     finally:
         g.close()
 
@@ -80,8 +85,8 @@ def test_persistent_grid_variants(name, dirs, env):
     from paper_2111_11728_b200 import engine
     g = engine.FetiSystem(CASES[name]())
     try:
-        ref = solve(g, dirs, {"FETIGPU_PERSIST": "0"})
-        got = solve(g, dirs, dict(env, FETIGPU_PERSIST="1"))
+        ref = solve(g, dirs, {"FETIGPU_PERSIST": "0", "FETIGPU_CLUSTER": "0"})
+        got = solve(g, dirs, dict(env, FETIGPU_PERSIST="1", FETIGPU_CLUSTER="0"))
         assert got[2] == (3 if env.get("FETIGPU_PERSIST_BAR") == "cluster" else 2)
         same(ref, got)
     finally:
@@ -89,11 +94,13 @@ def test_persistent_grid_variants(name, dirs, env):
 
 
 def test_persistent_default_policy():
-    """The default picks the persistent loop where it is faster (small
-    operators) and the graph loop for C3-sized ones (K15)."""
+    """The default picks the cluster-resident loop for C1 (T-FETI single
+    direction, operators in shared memory), the persistent loop where it is
+    faster (small operators) and the graph loop for C3-sized ones (DESIGN.md
+    4, K15)."""
     from paper_2111_11728_b200 import engine
-    for prob, dirs, want in ((pb.config1(), 0, 2), (pb.config1(), 1, 2), (pb.config2(), 0, 2),
-                             (pb.config2(), 1, 1), (pb.config3(method=1), 1, 1)):
+    for prob, dirs, want in ((pb.config1(), 0, 4), (pb.config1(), 1, 2), (pb.config2(), 0, 2),
+                             (pb.config2(), 1, 2), (pb.config3(method=1), 1, 1)):
         g = engine.FetiSystem(prob)
         try:
             _, tr, loop = solve(g, dirs, {}, max_it=20)
@@ -114,6 +121,18 @@ def test_persistent_repeat_and_breakdown_free_restart():
         c = solve(g, 0, {"FETIGPU_PERSIST": "1"}, max_it=5)
         assert c[1]["iterations"] == 5 and c[1]["status"] == 1   # max_iter
         d = solve(g, 0, {"FETIGPU_PERSIST": "0"}, max_it=5)
+        same(c, d)
+    finally:
+        g.close()
+    g = engine.FetiSystem(pb.config1())
+    try:
+        a = solve(g, 0, {"FETIGPU_CLUSTER": "1"})
+        b = solve(g, 0, {"FETIGPU_CLUSTER": "1"})
+        assert a[2] == 4
+        same(a, b)
+        c = solve(g, 0, {"FETIGPU_CLUSTER": "1"}, max_it=7)
+        d = solve(g, 0, {"FETIGPU_CLUSTER": "0", "FETIGPU_PERSIST": "0"}, max_it=7)
+        assert c[1]["iterations"] == 7
         same(c, d)
     finally:
         g.close()

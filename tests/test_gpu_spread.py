@@ -12,8 +12,9 @@ displacements GPU-vs-oracle 5.5e-4 against oracle-vs-refined 5.3e-3.
 * C3 FETI-DP FO and C3 T-FETI FO: ||u_gpu - u_oracle|| <=
   max(||u_oracle - u_refined||, 1e-8) (relative L2), and iteration counts
   within +-1 of the oracle;
-* C5 RRS: the GPU's true preconditioned residual (oracle operator) within
-  10x the oracle's own (the refined oracle's RRS breaks down on C5).
+* C5 RRS: the GPU's true preconditioned residual within 10x the oracle's,
+  both measured with the accuracy reference's operator (the refined
+  oracle's RRS itself breaks down on C5).
 C3 T-FETI (about 4 min of CPU oracle time) and C5 (about 12 min) are marked
 slow (FETIGPU_SLOW_TESTS=1).
 """
@@ -101,29 +102,43 @@ def test_c5_rrs_true_residual_vs_oracle(oracle_mod):
     breaks down there (a roundoff-negative pivot: IndefiniteInput), and the
     recursively updated residual of Alg. 1 drifts from the true one at this
     conditioning (profiles/r01_c5_conditioning_diag.json), so both solutions
-    are scored by the TRUE preconditioned residual with the ORACLE's operator
-    and preconditioner, rho(lambda) = sqrt(r^T M r), r = d - F lambda,
-    relative to rho(0): the GPU's must be within ACC_FACTOR (10) of the
-    oracle's own, with the same iteration count +-1.  The dual energies
-    J = 1/2 lambda^T F lambda - d^T lambda are printed as well (measured:
-    the oracle's is lower by 1.4e-3 relative)."""
+    are scored by their TRUE preconditioned residual rho(lambda) =
+    sqrt(r^T M r), r = d - F lambda, relative to rho(0), with F, M and d of
+    the ACCURACY REFERENCE (the oracle with long-double refined local and
+    coarse solves): the GPU's must be within ACC_FACTOR (10) of the oracle's,
+    with the same iteration count +-1.  Measured with the double oracle's own
+    F instead, each solution would be scored against that operator's rounding
+    (F_oracle is 3.5e-3 from the reference on C5, F_gpu 8.1e-4: DESIGN.md 2),
+    which favours the oracle by construction (round-2 run: 3.7e-2 vs 6.9e-7).
+    Both measures and the dual energies are printed."""
     from paper_2111_11728_b200 import engine
     prob = pb.config5()
+    L = oracle_mod.lib()
+    L.fo_set_refine(0)
     o = oracle_mod.Oracle(prob)
     lo, to = o.solve(tol=1e-6, max_it=200, directions=2)
     g = engine.FetiSystem(prob)
     lg, tg = g.solve(tol=1e-6, max_it=200, directions=2)
     g.close()
-    d, _ = o.rhs()
+    L.fo_set_refine(1)
+    ref = oracle_mod.Oracle(prob)
+    L.fo_set_refine(0)
 
-    def rho(lam):
-        r = d - o.apply_F(lam)
-        return np.sqrt(max(r @ o.apply_precond(r), 0.0))
-    r0 = rho(np.zeros_like(d))
-    rg, ro = rho(lg) / r0, rho(lo) / r0
-    J = lambda lam: 0.5 * lam @ o.apply_F(lam) - d @ lam   # noqa: E731
+    def scores(sys_):
+        d, _ = sys_.rhs()
+
+        def rho(lam):
+            r = d - sys_.apply_F(lam)
+            return np.sqrt(max(r @ sys_.apply_precond(r), 0.0))
+        r0 = rho(np.zeros_like(d))
+        J = lambda lam: 0.5 * lam @ sys_.apply_F(lam) - d @ lam   # noqa: E731
+        return rho(lg) / r0, rho(lo) / r0, J(lg), J(lo)
+    rg, ro, Jg, Jo = scores(ref)
+    og, oo, _, _ = scores(o)
     print("C5 RRS its gpu", tg["iterations"], "oracle", to["iterations"],
-          "true rel residual gpu %.3e oracle %.3e" % (rg, ro), "J gpu %.10e oracle %.10e" % (J(lg), J(lo)))
+          "| true rel residual (reference operator) gpu %.3e oracle %.3e" % (rg, ro),
+          "| J gpu %.10e oracle %.10e" % (Jg, Jo),
+          "| with the double oracle's operator gpu %.3e oracle %.3e" % (og, oo))
     assert tg["status"] == to["status"] == 0
     assert abs(tg["iterations"] - to["iterations"]) <= 1
     assert rg <= 10.0 * ro

@@ -25,15 +25,15 @@ CASES = {
 
 
 def variants(grids):
-    out = [("graph", {"FETIGPU_PERSIST": "0"})]
+    out = [("graph", {"FETIGPU_PERSIST": "0", "FETIGPU_CLUSTER": "0"}), ("default", {})]
     for g in grids:
         if g == 0:
-            out.append(("persist-auto", {"FETIGPU_PERSIST": "1"}))
+            out.append(("persist-auto", {"FETIGPU_PERSIST": "1", "FETIGPU_CLUSTER": "0"}))
         else:
-            out.append((f"grid{g}", {"FETIGPU_PERSIST": "1", "FETIGPU_PERSIST_G": str(g),
+            out.append((f"grid{g}", {"FETIGPU_PERSIST": "1", "FETIGPU_CLUSTER": "0", "FETIGPU_PERSIST_G": str(g),
                                      "FETIGPU_PERSIST_BAR": "grid"}))
             if g <= 16:
-                out.append((f"cluster{g}", {"FETIGPU_PERSIST": "1", "FETIGPU_PERSIST_G": str(g),
+                out.append((f"cluster{g}", {"FETIGPU_PERSIST": "1", "FETIGPU_CLUSTER": "0", "FETIGPU_PERSIST_G": str(g),
                                             "FETIGPU_PERSIST_BAR": "cluster"}))
     return out
 
@@ -45,7 +45,7 @@ def main():
     ap.add_argument("--cases", default=",".join(CASES))
     args = ap.parse_args()
     grids = [int(x) for x in args.grids.split(",") if x]
-    keys = ("FETIGPU_PERSIST", "FETIGPU_PERSIST_G", "FETIGPU_PERSIST_BAR")
+    keys = ("FETIGPU_PERSIST", "FETIGPU_PERSIST_G", "FETIGPU_PERSIST_BAR", "FETIGPU_CLUSTER")
     for name in args.cases.split(","):
         fn, dirs = CASES[name]
         g = engine.FetiSystem(fn())
