@@ -507,15 +507,16 @@ __global__ void __launch_bounds__(512) k_csym_reduce(const double* __restrict__ 
 }
 
 // rows i = warp0, warp0 + nwarps, ... of y = M x (one warp per row; a row's
-// result does not depend on the warp count).  x through L2 (__ldcg): the
-// persistent solver loop produces it in-kernel.
-// SM: M and x in shared memory (the cluster-resident loop), plain loads
+// result does not depend on the warp count).  x by weak loads (L1-cacheable:
+// every row reads all of it); inside the persistent loop x is produced in an
+// earlier phase, and the grid / cluster barrier's acquire invalidates L1.
+// SM: M and x in shared memory (the cluster-resident loop)
 template <bool SM = false>
 __device__ __forceinline__ void dense_gemv_warps(const double* __restrict__ M, int n, const double* x,
                                                  double* y, int warp0, int nwarps) {
   const int lane = threadIdx.x & 31;
   auto ldm = [&](const double2* p) { return SM ? *p : __ldcs(p); };
-  auto ldx = [&](const double* p) { return SM ? *p : __ldcg(p); };
+  auto ldx = [&](const double* p) { return *p; };   // x is reused by every row: L1-cacheable weak loads
   // one row's chains (a0..a3 over lane-strided double2 pairs, then warp_sum)
   auto row = [&](int i) {
     const double* Mi = M + (size_t)i * n;
@@ -898,7 +899,7 @@ __device__ __forceinline__ void fo_sub_cta(int vb, const double* W, int m, int c
 #pragma unroll
       for (int u = 0; u < 16; ++u) {
         wv[u] = __ldcs(W + (size_t)(j + 8 * u) * m + i);
-        pv[u] = __ldcg(psi + j + 8 * u);
+        pv[u] = psi[j + 8 * u];
       }
 #pragma unroll
       for (int u = 0; u < 16; ++u) v = fma(wv[u], pv[u], v);
@@ -906,12 +907,12 @@ __device__ __forceinline__ void fo_sub_cta(int vb, const double* W, int m, int c
     for (; j + 24 < c; j += 32) {
       const double w0 = __ldcs(W + (size_t)j * m + i), w1 = __ldcs(W + (size_t)(j + 8) * m + i),
                    w2 = __ldcs(W + (size_t)(j + 16) * m + i), w3 = __ldcs(W + (size_t)(j + 24) * m + i);
-      v = fma(w0, __ldcg(psi + j), v);
-      v = fma(w1, __ldcg(psi + j + 8), v);
-      v = fma(w2, __ldcg(psi + j + 16), v);
-      v = fma(w3, __ldcg(psi + j + 24), v);
+      v = fma(w0, psi[j], v);
+      v = fma(w1, psi[j + 8], v);
+      v = fma(w2, psi[j + 16], v);
+      v = fma(w3, psi[j + 24], v);
     }
-    for (; j < c; j += 8) v = fma(__ldcg(W + (size_t)j * m + i), __ldcg(psi + j), v);
+    for (; j < c; j += 8) v = fma(W[(size_t)j * m + i], psi[j], v);
   }
   part[warp][lane] = v;
   __syncthreads();
@@ -942,17 +943,17 @@ __device__ __forceinline__ void fo_psi_item(int item, const double* Q, int m, co
   int i = i0 + threadIdx.x;
   for (; i + 768 < i1; i += 1024) {  // 4 loads of each vector in flight, same FMA order as 2-way
     const double q0 = __ldcs(q + i), q1 = __ldcs(q + i + 256), q2 = __ldcs(q + i + 512), q3 = __ldcs(q + i + 768);
-    const double x0 = __ldcg(w + i), x1 = __ldcg(w + i + 256), x2 = __ldcg(w + i + 512), x3 = __ldcg(w + i + 768);
+    const double x0 = w[i], x1 = w[i + 256], x2 = w[i + 512], x3 = w[i + 768];
     a0 = fma(q0, x0, a0);
     a1 = fma(q1, x1, a1);
     a0 = fma(q2, x2, a0);
     a1 = fma(q3, x3, a1);
   }
   for (; i + 256 < i1; i += 512) {
-    a0 = fma(__ldcg(q + i), __ldcg(w + i), a0);
-    a1 = fma(__ldcg(q + i + 256), __ldcg(w + i + 256), a1);
+    a0 = fma(q[i], w[i], a0);
+    a1 = fma(q[i + 256], w[i + 256], a1);
   }
-  if (i < i1) a0 = fma(__ldcg(q + i), __ldcg(w + i), a0);
+  if (i < i1) a0 = fma(q[i], w[i], a0);
   const double acc = warp_sum(a0 + a1);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
   __syncthreads();

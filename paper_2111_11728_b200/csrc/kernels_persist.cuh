@@ -28,6 +28,11 @@
 // apart), so the two paths are bit-identical (tools/persist_ab.py,
 // tests/test_gpu_persist.py).
 //
+// Coherence: data a phase reads was written in an earlier phase; it is read
+// through L2 (__ldcg) or by weak loads after a barrier whose acquire
+// invalidates L1 (CCTL.IVALL in the SASS), never through the non-coherent
+// read-only path (no LDG.CONSTANT on in-kernel data).
+//
 // Reference: pcg single / FO, residual_metric and
 // NegativeInnerProduct.
 #pragma once

@@ -471,7 +471,10 @@ int Ctx::solve(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_trace* 
       CK(cudaMemcpyAsync(&hc, dctl.p, sizeof(IterCtl), cudaMemcpyDeviceToHost, st));
       CK(cudaStreamSynchronize(st));
       std::vector<double> ht(std::max(1, tcap));
-      if (tcap > 1) CK(cudaMemcpy(ht.data(), dtrace.p, (size_t)tcap * 8, cudaMemcpyDeviceToHost));
+      if (tcap > 1) {
+        CK(cudaMemcpyAsync(ht.data(), dtrace.p, (size_t)tcap * 8, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+      }
       if (hc.err) fail(FETIGPU_E_NEGATIVE_INNER_PRODUCT, "r^T z < 0: preconditioner is not symmetric positive");
       for (int i = 1; i <= hc.it; ++i) {
         it = i;
