@@ -964,6 +964,55 @@ __device__ __forceinline__ void fo_psi_item(int item, const double* Q, int m, co
   }
   __syncthreads();
 }
+// two items of the same row segment at once (the persistent loop, where one
+// CTA works through several items): each item keeps its own chains, exactly
+// as fo_psi_item computes them, so the loads of both are in flight together
+__device__ __forceinline__ void fo_psi_item2(int itemA, int itemB, const double* Q, int m, const double* w,
+                                             double* partial, int S) {
+  const int chunk = (m + S - 1) / S;
+  __shared__ double red2[2][8];
+  const int jA = itemA / S, s = itemA - jA * S, jB = itemB / S;
+  const int i0 = s * chunk, i1 = min(m, i0 + chunk);
+  const double* qa = Q + (size_t)jA * m;
+  const double* qb = Q + (size_t)jB * m;
+  double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+  int i = i0 + threadIdx.x;
+  for (; i + 768 < i1; i += 1024) {
+    const double q0 = __ldcs(qa + i), q1 = __ldcs(qa + i + 256), q2 = __ldcs(qa + i + 512), q3 = __ldcs(qa + i + 768);
+    const double p0 = __ldcs(qb + i), p1 = __ldcs(qb + i + 256), p2 = __ldcs(qb + i + 512), p3 = __ldcs(qb + i + 768);
+    const double x0 = w[i], x1 = w[i + 256], x2 = w[i + 512], x3 = w[i + 768];
+    a0 = fma(q0, x0, a0);
+    a1 = fma(q1, x1, a1);
+    a0 = fma(q2, x2, a0);
+    a1 = fma(q3, x3, a1);
+    b0 = fma(p0, x0, b0);
+    b1 = fma(p1, x1, b1);
+    b0 = fma(p2, x2, b0);
+    b1 = fma(p3, x3, b1);
+  }
+  for (; i + 256 < i1; i += 512) {
+    a0 = fma(qa[i], w[i], a0);
+    a1 = fma(qa[i + 256], w[i + 256], a1);
+    b0 = fma(qb[i], w[i], b0);
+    b1 = fma(qb[i + 256], w[i + 256], b1);
+  }
+  if (i < i1) {
+    a0 = fma(qa[i], w[i], a0);
+    b0 = fma(qb[i], w[i], b0);
+  }
+  const double accA = warp_sum(a0 + a1), accB = warp_sum(b0 + b1);
+  if ((threadIdx.x & 31) == 0) {
+    red2[0][threadIdx.x >> 5] = accA;
+    red2[1][threadIdx.x >> 5] = accB;
+  }
+  __syncthreads();
+  if (threadIdx.x < 2) {
+    double t = 0.0;
+    for (int k = 0; k < 8; ++k) t += red2[threadIdx.x][k];
+    partial[(size_t)(threadIdx.x ? jB : jA) * S + s] = t;
+  }
+  __syncthreads();
+}
 // psi_j = q_j^T w for j < *cnt on a (column x row-segment) grid: CTA (j, s)
 // reduces rows [s*chunk, (s+1)*chunk) of column j into partial[j*S + s];
 // k_fo_psi_sum adds the S partials of each column in fixed order (skipped

@@ -282,7 +282,13 @@ __global__ void __launch_bounds__(kThreads, kPersistOcc) k_pcg_persist(const Per
         const int c = cnt, S = a.psi_S;
         for (int p = 0; p < a.passes; ++p) {
           double* part = S == 1 ? a.psi : a.psi_part;
-          for (int item = b0; item < c * S; item += G) fo_psi_item(item, a.Qst, m, wc, part, S);
+          if (S == 1) {   // two columns per round (same rows): the loads of both in flight
+            int item = b0;
+            for (; item + G < c; item += 2 * G) fo_psi_item2(item, item + G, a.Qst, m, wc, part, 1);
+            if (item < c) fo_psi_item(item, a.Qst, m, wc, part, 1);
+          } else {
+            for (int item = b0; item < c * S; item += G) fo_psi_item(item, a.Qst, m, wc, part, S);
+          }
           bar.sync(epoch);
           if (S > 1) {
             for (int jj = gtid; jj < c; jj += gstride) {   // k_fo_psi_sum
