@@ -241,6 +241,7 @@ struct Ctx {
   // ---- K5: Q = F W for k columns, row-major blocks (W(i,c) = W[i*ldw + c])
   DBuf<double> blk_t, blk_T, blk_U;
   DBuf<int> d_k5order;   // K5 subdomain order (4 x 4-module tiles)
+  DBuf<int> d_k5e_order; // K5e edge-chunk order (first owner in the K5 walk)
   void apply_F_block(const double* W, int ldw, double* Q, int ldq, int k);
   // ---- K5z: Q = F Z for a fresh per-subdomain preconditioner block Z
   // (row-major m x N_s, column s supported on subdomain s's dual rows):

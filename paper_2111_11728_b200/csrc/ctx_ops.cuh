@@ -380,7 +380,19 @@ void Ctx::apply_F_block(const double* W, int ldw, double* Q, int ldq, int k) {
     else CK(cudaMemset2DAsync(Q, (size_t)ldq * 8, 0, (size_t)k * 8, m, zs));
     if (side) CK(cudaEventRecord(aux_join, aux_st));
   };
-  if (!side) zero_q();
+  // K5e (FETIGPU_K5_EDGE=1): by interface edge -- no memset, Q written once,
+  // bit-identical.  C4 k = 2048 on one B200: DRAM 31.5 GB per kernel against
+  // 35.9 GB + the 8.3 GB memset, but 68.2 vs 65.8 ms of kernel time (the
+  // mid-tile store after the first owner stalls the MMA loop), so K5 stays
+  // the default: the block apply is FP64-bound, not HBM-bound
+  static const bool edge_on = [] {
+    const char* e = getenv("FETIGPU_K5_EDGE");
+    return e && e[0] == '1';
+  }();
+  const bool edge = edge_on && su.method == FETIGPU_FETIDP && folded && blk_aligned && (k % 2 == 0) &&
+                    (ldw % 2 == 0) && (ldq % 2 == 0) && ((uintptr_t)W % 16 == 0) && ((uintptr_t)Q % 16 == 0) &&
+                    bz_prepare();
+  if (!side && !edge) zero_q();
   // K5 walks the subdomains in 4 x 4-module tiles: both neighbours sharing a
   // dual row (left/right and below/above) are processed close in time, so
   // the W rows of an interface are read from DRAM about once
@@ -416,13 +428,35 @@ void Ctx::apply_F_block(const double* W, int ldw, double* Q, int ldq, int k) {
     }
     k_coarse_gather_block<<<dim3((k + 255) / 256, Nc), 256, 0, st>>>(d_optr.p, d_oidx.p, blk_t.p, k, Nc, k,
                                                                      blk_T.p, k);
-    zero_q();   // side stream: overlaps the FP64-bound GEMM, not the HBM-bound pre-pass
+    if (!edge) zero_q();   // side stream: overlaps the FP64-bound GEMM, not the HBM-bound pre-pass
     // U = Kbar^{-1} T  (row-major N_c x k == column-major k x N_c: U^T = T^T Kinv)
     gemm(st, false, false, k, Nc, Nc, 1.0, blk_T.p, k, d_Kinv.p, Nc, 0.0, blk_U.p, k);
     a.dps = d_dp.p; a.abc = d_abc.p; a.cmap = d_cmap.p; a.U = blk_U.p; a.ldu = k;
     max_ns += 8;
   }
-  if (side) CK(cudaStreamWaitEvent(st, aux_join, 0));
+  if (side && !edge) CK(cudaStreamWaitEvent(st, aux_join, 0));
+  if (edge) {
+    if (d_k5e_order.n != (size_t)bz_nedges) {   // edge chunks in K5's 4 x 4-module walk of their first owner
+      std::vector<BzEdge> es(bz_nedges);
+      CK(cudaMemcpyAsync(es.data(), bz_edges.p, bz_nedges * sizeof(BzEdge), cudaMemcpyDeviceToHost, st));
+      std::vector<int> ord(Ns), pos(Ns);
+      CK(cudaMemcpyAsync(ord.data(), d_k5order.p, Ns * sizeof(int), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      for (int i = 0; i < Ns; ++i) pos[ord[i]] = i;
+      std::vector<int> eo(bz_nedges);
+      std::iota(eo.begin(), eo.end(), 0);
+      std::stable_sort(eo.begin(), eo.end(), [&](int x, int y) { return pos[es[x].t1] < pos[es[y].t1]; });
+      d_k5e_order.upload(eo, st);
+    }
+    constexpr int BM = 64, BN = 64;
+    const int mt = (kBzRows + BM - 1) / BM;
+    const size_t smem = k5e_smem<64, 64, 16, 2>(max_ns);   // max_ns already counts the n_c <= 8 coarse columns
+    raise_smem_limit(k_block_apply_edge<64, 64, 16, 2>, smem);
+    EdgeApplyArgs ea{bz_edges.p, bz_erow.p, bz_eb1.p, bz_eb2.p, d_k5e_order.p, mt};
+    k_block_apply_edge<64, 64, 16, 2><<<dim3((k + BN - 1) / BN, bz_nedges * mt), 128, smem, st>>>(a, ea);
+    LAUNCH_CHECK();
+    return;
+  }
   dim3 grid((k + kBN - 1) / kBN, (max_ns + kBM - 1) / kBM, Ns);
   const bool fast = folded && blk_aligned && (k % 2 == 0) && (ldw % 2 == 0) && (ldq % 2 == 0) &&
                     ((uintptr_t)W % 16 == 0) && ((uintptr_t)Q % 16 == 0);

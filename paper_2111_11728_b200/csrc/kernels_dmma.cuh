@@ -1045,3 +1045,175 @@ __global__ void __launch_bounds__(128) k_fz_correct_mma(const BzEdge* __restrict
 }
 
 }  // namespace fg
+
+namespace fg {
+
+// ---------------------------------------------------------------------------
+// K5e: the FETI-DP block apply by interface edge instead of by subdomain.
+// A CTA owns BM dual rows of one interface edge (the rows shared by owners t1
+// and t2, K5z's edge chunks) and BN columns of Q, and runs the K5 inner loop
+// twice: over [F''_t1 | A''_t1][X_t1 ; U_t1] with the A rows taken at the
+// rows' local indices in t1, then over t2's.  After t1's range the tile is
+// stored to Q, after t2's it is added to what was stored: Q = acc_1 + acc_2,
+// the value K5's two order-free atomic contributions into a zeroed Q give
+// (0 + a + b), every element accumulated in the same k order -- so the result
+// is bit-identical to K5, without the Q memset and without the atomic
+// read-modify-write of Q (DRAM: Q is written once).
+// ---------------------------------------------------------------------------
+struct EdgeApplyArgs {
+  const BzEdge* edges;   // edge chunks (t1, t2, first entry, row count)
+  const int* erow;       // dual row of each entry
+  const int* eb1;        // local row index in t1
+  const int* eb2;        // local row index in t2
+  const int* order;      // edge-chunk walk (nullable)
+  int mt;                // BM-row tiles per chunk
+};
+
+template <int BM, int BN, int BK, int ST>
+constexpr size_t k5e_smem(int kin_max) {
+  return (size_t)ST * (BM * (BK + 4) + BK * (BN + 8)) * 8 + (size_t)(2 * kin_max + 3 * BM) * 4;
+}
+
+template <int BM, int BN, int BK, int ST>
+__global__ void __launch_bounds__((BM / 32) * (BN / 32) * 32, 4) k_block_apply_edge(BlockApplyArgs a, EdgeApplyArgs ea) {
+  constexpr int THREADS = (BM / 32) * (BN / 32) * 32;
+  constexpr int AP = BK + 4, BP = BN + 8;
+  extern __shared__ __align__(16) double dsm[];
+  double* As = dsm;                                   // ST x (BM x AP)
+  double* Bs = dsm + ST * BM * AP;                    // ST x (BK x BP)
+  int* srow = reinterpret_cast<int*>(Bs + ST * BK * BP);
+  const int ci = blockIdx.y / ea.mt;
+  const int chunk = ea.order ? ea.order[ci] : ci;
+  const BzEdge e = ea.edges[chunk];
+  const int r0 = (blockIdx.y - ci * ea.mt) * BM;
+  if (r0 >= e.cnt) return;
+  const int nrows = min(BM, e.cnt - r0);
+  const int own[2] = {e.t1, e.t2};
+  const OpSub d1 = a.subs[e.t1];
+  const DpSub p1 = a.dps[e.t1];
+  const int kin1 = d1.ns + p1.nc;
+  const bool two = e.t2 >= 0;
+  const OpSub d2 = two ? a.subs[e.t2] : d1;
+  const DpSub p2 = two ? a.dps[e.t2] : p1;
+  const int kin2 = two ? d2.ns + p2.nc : 0;
+  int* srow2 = srow + kin1;
+  int* lr1 = srow2 + kin2;     // BM local rows in t1
+  int* lr2 = lr1 + BM;         // BM local rows in t2
+  int* qr = lr2 + BM;          // BM dual rows
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int j = tid; j < kin1; j += THREADS)
+    srow[j] = j < d1.ns ? a.rows[d1.map_off + j] : a.cmap[p1.cmap_off + j - d1.ns];
+  for (int j = tid; j < kin2; j += THREADS)
+    srow2[j] = j < d2.ns ? a.rows[d2.map_off + j] : a.cmap[p2.cmap_off + j - d2.ns];
+  for (int r = tid; r < BM; r += THREADS) {
+    const bool ok = r < nrows;
+    lr1[r] = ok ? ea.eb1[e.e0 + r0 + r] : 0;
+    lr2[r] = ok && two ? ea.eb2[e.e0 + r0 + r] : 0;
+    qr[r] = ok ? ea.erow[e.e0 + r0 + r] : 0;
+  }
+  __syncthreads();
+  (void)own;
+  const int col0 = blockIdx.x * BN;
+  constexpr int WGN = BN / 32;
+  const int wr = warp / WGN, wc = warp % WGN;
+  const int nk1 = (kin1 + BK - 1) / BK, nk2 = two ? (kin2 + BK - 1) / BK : 0, nk = nk1 + nk2;
+  auto issue = [&](int t) {
+    const bool second = t >= nk1;
+    const int kk = (second ? t - nk1 : t) * BK, stg = t % ST;
+    const OpSub& d = second ? d2 : d1;
+    const DpSub& p = second ? p2 : p1;
+    const int kin = second ? kin2 : kin1, ns = d.ns, nc = p.nc;
+    const int* lr = second ? lr2 : lr1;
+    const int* sr = second ? srow2 : srow;
+    const double* F = a.mats + d.moff;
+    const double* Abc = a.abc + p.abc_off;
+    double* A_ = As + stg * BM * AP;
+    double* B_ = Bs + stg * BK * BP;
+    constexpr int ACH = BM * (BK / 2), BCH = BK * (BN / 2);
+#pragma unroll
+    for (int q = 0; q < (ACH + THREADS - 1) / THREADS; ++q) {
+      const int idx = tid + q * THREADS;
+      if (ACH % THREADS == 0 || idx < ACH) {
+        const int r = idx / (BK / 2), c2 = (idx % (BK / 2)) * 2;
+        const int gi = lr[r], gj = kk + c2;
+        const double* src = F;
+        const bool ok = r < nrows && gj < kin;
+        if (ok) src = gj < ns ? F + (size_t)gi * d.ld + gj : Abc + (size_t)gi * nc + (gj - ns);
+        cp_async16(A_ + r * AP + c2, src, ok);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < (BCH + THREADS - 1) / THREADS; ++q) {
+      const int idx = tid + q * THREADS;
+      if (BCH % THREADS == 0 || idx < BCH) {
+        const int r = idx / (BN / 2), c2 = (idx % (BN / 2)) * 2;
+        const int gj = kk + r, gc = col0 + c2;
+        const double* src = a.W;
+        const bool ok = gj < kin && gc < a.k;
+        if (ok) src = gj < ns ? a.W + (size_t)sr[gj] * a.ldw + gc : a.U + (size_t)sr[gj] * a.ldu + gc;
+        cp_async16(B_ + r * BP + c2, src, ok);
+      }
+    }
+  };
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  // tile -> Q: Q = 0 + tile (first owner) or Q += tile (the second)
+  auto flush = [&](bool add) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int li = wr * 32 + i * 8 + (lane >> 2);
+      if (li >= nrows) continue;
+      double* qrow = a.Q + (size_t)qr[li] * a.ldq;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int gc = col0 + wc * 32 + j * 8 + 2 * (lane & 3);
+        if (gc + 1 < a.k) {
+          double2* q2 = reinterpret_cast<double2*>(qrow + gc);
+          const double2 o = add ? *q2 : make_double2(0.0, 0.0);   // (0 + a) + b, as the atomics
+          *q2 = make_double2(__dadd_rn(o.x, acc[i][j][0]), __dadd_rn(o.y, acc[i][j][1]));
+        } else if (gc < a.k) {
+          qrow[gc] = __dadd_rn(add ? qrow[gc] : 0.0, acc[i][j][0]);
+        }
+      }
+    }
+  };
+#pragma unroll
+  for (int t = 0; t < ST - 1; ++t) {
+    if (t < nk) issue(t);
+    cp_async_commit();
+  }
+  for (int t = 0; t < nk; ++t) {
+    cp_async_wait<ST - 2>();
+    __syncthreads();
+    if (t + ST - 1 < nk) issue(t + ST - 1);
+    cp_async_commit();
+    if (t == nk1) {   // t1's range done: store it, start t2's from zero
+      flush(false);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    }
+    const double* A_ = As + (t % ST) * BM * AP;
+    const double* B_ = Bs + (t % ST) * BK * BP;
+#pragma unroll
+    for (int k4 = 0; k4 < BK; k4 += 4) {
+      double af[4], bf[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) af[i] = A_[(wr * 32 + i * 8 + (lane >> 2)) * AP + k4 + (lane & 3)];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bf[j] = B_[(k4 + (lane & 3)) * BP + wc * 32 + j * 8 + (lane >> 2)];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+  }
+  cp_async_wait<0>();
+  flush(two);
+}
+
+}  // namespace fg
