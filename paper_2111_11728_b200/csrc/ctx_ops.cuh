@@ -385,10 +385,8 @@ void Ctx::apply_F_block(const double* W, int ldw, double* Q, int ldq, int k) {
   // 35.9 GB + the 8.3 GB memset, but 68.2 vs 65.8 ms of kernel time (the
   // mid-tile store after the first owner stalls the MMA loop), so K5 stays
   // the default: the block apply is FP64-bound, not HBM-bound
-  static const bool edge_on = [] {
-    const char* e = getenv("FETIGPU_K5_EDGE");
-    return e && e[0] == '1';
-  }();
+  const char* ee = getenv("FETIGPU_K5_EDGE");   // read per call (tests switch it)
+  const bool edge_on = ee && ee[0] == '1';
   const bool edge = edge_on && su.method == FETIGPU_FETIDP && folded && blk_aligned && (k % 2 == 0) &&
                     (ldw % 2 == 0) && (ldq % 2 == 0) && ((uintptr_t)W % 16 == 0) && ((uintptr_t)Q % 16 == 0) &&
                     bz_prepare();

@@ -126,3 +126,25 @@ def test_zblock_apply_matches_dense_block(name):
     for c in (0, g.n_sub // 2, g.n_sub - 1):
         assert np.abs(Qz[:, c] - g.apply_F(Z[:, c])).max() <= 1e-12 * np.abs(Qd).max()
     g.close()
+
+
+@pytest.mark.parametrize("name", ["C4s", "C5s", "C2s", "C2_roller_vertex"])
+def test_edge_block_apply_bitwise(name, monkeypatch):
+    """K5e (block apply by interface edge, FETIGPU_K5_EDGE=1: both owners'
+    ranges per tile, the first stored and the second added, no memset or
+    atomics) equals K5 bit for bit."""
+    from paper_2111_11728_b200 import problems as pb
+    prob = {"C4s": lambda: pb.config4(sx=6, sy=4, n=8),
+            "C5s": lambda: pb.config5(sx=5, sy=3, n=12, n_designs=3),
+            "C2s": lambda: pb.config2(sx=4, sy=3, n=8),
+            "C2_roller_vertex": lambda: pb.config2(sx=3, sy=2, n=8).replace(
+                dirichlet=[(0, 0, 0.0), (0, 1, 0.0), (3 * 8, 1, 0.0)],
+                point_loads=[((2 * 8) * 25 + 12, 1, -1.0)])}[name]()
+    g = engine.FetiSystem(prob)
+    W = np.random.default_rng(5).standard_normal((g.m, 64))
+    monkeypatch.setenv("FETIGPU_K5_EDGE", "0")
+    Q0 = g.apply_F_block(W)
+    monkeypatch.setenv("FETIGPU_K5_EDGE", "1")
+    Q1 = g.apply_F_block(W)
+    g.close()
+    assert np.array_equal(Q0.view(np.uint64), Q1.view(np.uint64))
