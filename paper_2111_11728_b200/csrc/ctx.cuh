@@ -422,8 +422,8 @@ struct Ctx {
   std::vector<int> pc_nsld;   // per subdomain: n_s x ld of its preconditioner matrix (K15c)
   size_t cluster_smem() const;
   bool cluster_ok(bool fo);
-  void launch_cluster(double* lam, double* r, double* w, Scal* sc, IterCtl* ctl, double* trace);
-  void launch_persist(int G, bool fo, int passes, int psi_S, double* lam, double* r, double* z, double* w, double* q,
+  bool launch_cluster(double* lam, double* r, double* w, Scal* sc, IterCtl* ctl, double* trace);
+  bool launch_persist(int G, bool fo, int passes, int psi_S, double* lam, double* r, double* z, double* w, double* q,
                       Scal* sc, double* Wst, double* Qst, double* psi, double* psi_part, int* cnt, IterCtl* ctl,
                       double* trace);
   int solve(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_trace* tr);

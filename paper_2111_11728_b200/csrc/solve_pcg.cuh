@@ -128,7 +128,7 @@ size_t Ctx::persist_smem() const {
   return (size_t)(std::max(max_ld, max_pc_ld) + sv) * 8;
 }
 
-void Ctx::launch_persist(int G, bool fo, int passes, int psi_S, double* lam, double* r, double* z, double* w,
+bool Ctx::launch_persist(int G, bool fo, int passes, int psi_S, double* lam, double* r, double* z, double* w,
                          double* q, Scal* sc, double* Wst, double* Qst, double* psi, double* psi_part, int* cnt,
                          IterCtl* ctl, double* trace) {
   const bool tf = su.method == FETIGPU_TFETI;
@@ -177,6 +177,7 @@ void Ctx::launch_persist(int G, bool fo, int passes, int psi_S, double* lam, dou
   at[0].val.cooperative = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
+  bool ok = false;
   auto go = [&](auto kern, auto barrier) {
     if (persist_cluster) {
       if (G > 8) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
@@ -185,7 +186,7 @@ void Ctx::launch_persist(int G, bool fo, int passes, int psi_S, double* lam, dou
       at[0].val.clusterDim.y = 1;
       at[0].val.clusterDim.z = 1;
     }
-    CK(cudaLaunchKernelEx(&cfg, kern, a, barrier));
+    ok = cudaLaunchKernelEx(&cfg, kern, a, barrier) == cudaSuccess;
   };
   const GridBarrier gb{p_bar.p, p_bar.p + 1};
   const ClusterBarrier cb{p_bar.p, p_bar.p + 1};
@@ -200,7 +201,8 @@ void Ctx::launch_persist(int G, bool fo, int passes, int psi_S, double* lam, dou
     else if (fo) go(k_pcg_persist<GridBarrier, false, true>, gb);
     else go(k_pcg_persist<GridBarrier, false, false>, gb);
   }
-  LAUNCH_CHECK();
+  if (!ok) cudaGetLastError();   // e.g. not co-resident: the caller falls back to the graph loop
+  return ok;
 }
 
 // K15c: the cluster-resident loop (T-FETI single direction, N_s <= 16
@@ -225,7 +227,7 @@ bool Ctx::cluster_ok(bool fo) {
   return persist_prepare();
 }
 
-void Ctx::launch_cluster(double* lam, double* r, double* w, Scal* sc, IterCtl* ctl, double* trace) {
+bool Ctx::launch_cluster(double* lam, double* r, double* w, Scal* sc, IterCtl* ctl, double* trace) {
   ClusterArgs a{};
   a.m = su.m;
   a.Ns = su.Ns;
@@ -262,8 +264,11 @@ void Ctx::launch_cluster(double* lam, double* r, double* w, Scal* sc, IterCtl* c
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  CK(cudaLaunchKernelEx(&cfg, kern, a));
-  LAUNCH_CHECK();
+  if (cudaLaunchKernelEx(&cfg, kern, a) != cudaSuccess) {   // e.g. the cluster cannot be scheduled
+    cudaGetLastError();
+    return false;
+  }
+  return true;
 }
 
 // ----------------------------------------------------------- the engine ---
@@ -423,17 +428,21 @@ int Ctx::solve(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_trace* 
     // K15: the whole loop as one persistent kernel where the operators are
     // the plain per-subdomain ones (C1-C3, C5 single / FO); bit-identical
     // to the graph below (kernels_persist.cuh)
-    const bool clus = cluster_ok(fo);
-    const int pg = clus ? 1 : persist_grid(fo);
-    if (clus) {
-      launch_cluster(lam.p, r.p, w.p, sc.p, dctl.p, dtrace.p);
-      built_ok = true;
+    // (a launch that cannot be scheduled falls back to the next loop)
+    bool single_kernel = false;
+    if (cluster_ok(fo) && launch_cluster(lam.p, r.p, w.p, sc.p, dctl.p, dtrace.p)) {
+      single_kernel = true;
       solve_loop = 4;
-    } else if (pg > 0) {
-      launch_persist(pg, fo, passes, psi_S, lam.p, r.p, z.p, w.p, q.p, sc.p, Wst.p, Qst.p, psi.p, psi_part.p, cnt.p,
-                     dctl.p, dtrace.p);
+    } else {
+      const int pg = persist_grid(fo);
+      if (pg > 0 && launch_persist(pg, fo, passes, psi_S, lam.p, r.p, z.p, w.p, q.p, sc.p, Wst.p, Qst.p, psi.p,
+                                   psi_part.p, cnt.p, dctl.p, dtrace.p)) {
+        single_kernel = true;
+        solve_loop = persist_cluster ? 3 : 2;
+      }
+    }
+    if (single_kernel) {
       built_ok = true;
-      solve_loop = persist_cluster ? 3 : 2;
     } else if (cudaGraphCreate(&graph, 0) == cudaSuccess) {
       cudaGraphConditionalHandle hcond;
       cudaGraphNodeParams cp = {};
@@ -463,7 +472,7 @@ int Ctx::solve(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_trace* 
       if (graph) { cudaGraphDestroy(graph); graph = nullptr; }
       device_loop = false;
     } else {
-      if (pg <= 0) {
+      if (!single_kernel) {
         CK(cudaGraphLaunch(exec, st));
         solve_loop = 1;
       }
