@@ -1445,6 +1445,149 @@ __global__ void __launch_bounds__(512) k_pivchol_cl(double* Ag, int n, double to
   if (me == 0 && tid == 0) *rank_out = rank;
 }
 
+// Alg. 1 line 9 in one thread-block cluster with ONE cluster barrier per
+// pivot (k_pivchol_cl needs three plus the physical row / column swaps).  The
+// rows stay in original index order, distributed over the CTAs (row x on CTA
+// x % CL); every CTA keeps a replica of the diagonal and of the position ->
+// index map, so each picks the same pivot itself (max diagonal over the
+// remaining positions, ties to the lowest position), reads the pivot row from
+// its owner over DSMEM, forms the scaled column L_i = A_{x,i} / l and updates
+// its own remaining rows, A_ji -= L_i L_j, and its diagonal replica with the
+// same operation.  These are k_pivchol_cl's values entry for entry (the same
+// division, the same fma per entry in pivot order), so rank, permutation and
+// L are bit-identical; column k of L is written to Ag (original index order)
+// as the pivots go and permuted into place at the end.
+template <int CL>
+__global__ void __launch_bounds__(512) k_pivchol_cl1(double* Ag, int n, double tol, int* perm, int* rank_out,
+                                                     int* status) {
+  namespace cg = cooperative_groups;
+  extern __shared__ double s_dyn[];
+  __shared__ double s_wv[16];
+  __shared__ int s_wi[16];
+  __shared__ double s_bv;
+  __shared__ int s_bp;
+  const int R = (n + CL - 1) / CL;
+  double* A = s_dyn;                                  // R x n own rows, original order
+  double* Lc = A + (size_t)R * n;                     // the current column of L, by original index
+  double* d = Lc + n;                                 // diagonal replica, by original index
+  int* at = reinterpret_cast<int*>(d + n);            // position -> original index
+  unsigned char* done = reinterpret_cast<unsigned char*>(at + n);
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int lane = tid & 31, warp = tid >> 5, nwarp = nt >> 5;
+  int me = 0;
+  if constexpr (CL > 1) me = (int)cg::this_cluster().block_rank();
+  auto csync = [&]() {
+    if constexpr (CL > 1) cg::this_cluster().sync();
+    else __syncthreads();
+  };
+  auto remote = [&](double* p, int r) -> double* {
+    if constexpr (CL > 1) return cg::this_cluster().map_shared_rank(p, r);
+    else return p;
+  };
+  auto better = [](double v, int i, double bv, int bi) { return v > bv || (v == bv && i < bi); };
+  for (int lr = 0; lr < R; ++lr) {
+    const int x = lr * CL + me;
+    if (x < n)
+      for (int i = tid; i < n; i += nt) A[(size_t)lr * n + i] = Ag[(size_t)x * n + i];
+  }
+  double mx = -1e300;
+  for (int i = tid; i < n; i += nt) {
+    d[i] = Ag[(size_t)i * n + i];
+    at[i] = i;
+    done[i] = 0;
+    Lc[i] = 0.0;
+    mx = fmax(mx, d[i]);
+  }
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if (lane == 0) s_wv[warp] = mx;
+  __syncthreads();
+  double scale = -1e300;
+  for (int w = 0; w < nwarp; ++w) scale = fmax(scale, s_wv[w]);
+  const double stop_tol = tol * scale;
+  const double neg_tol = -tol * fmax(scale, 1e-300);
+  csync();   // every CTA has its input before column 0 of L overwrites row 0 of Ag
+  int rank = 0;
+  for (int k = 0; k < n; ++k) {
+    // pivot: the best diagonal over positions p >= k (identical in every CTA)
+    double bv = -1e300;
+    int bp = n;
+    for (int p = k + tid; p < n; p += nt) {
+      const double v = d[at[p]];
+      if (better(v, p, bv, bp)) { bv = v; bp = p; }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int op = __shfl_xor_sync(0xffffffffu, bp, o);
+      if (better(ov, op, bv, bp)) { bv = ov; bp = op; }
+    }
+    if (lane == 0) { s_wv[warp] = bv; s_wi[warp] = bp; }
+    __syncthreads();
+    if (warp == 0) {   // the best of the warp bests (a total order: any tree gives the same pivot)
+      double v = lane < nwarp ? s_wv[lane] : -1e300;
+      int p = lane < nwarp ? s_wi[lane] : n;
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+        const int op = __shfl_xor_sync(0xffffffffu, p, o);
+        if (better(ov, op, v, p)) { v = ov; p = op; }
+      }
+      if (lane == 0) {
+        s_bv = v;
+        s_bp = p;
+        if (v > stop_tol) {   // swap positions k <-> p
+          const int t = at[k];
+          at[k] = at[p];
+          at[p] = t;
+        }
+      }
+    }
+    __syncthreads();
+    if (!(s_bv > stop_tol)) {
+      if (me == 0)
+        for (int p = k + tid; p < n; p += nt)
+          if (d[at[p]] < neg_tol) atomicExch(status, 2 /* IndefiniteInput */);
+      break;
+    }
+    const int x = at[k];
+    const double l = sqrt(d[x]);
+    const double* rx = remote(A, x % CL) + (size_t)(x / CL) * n;
+    const bool writer = me == k % CL;
+    for (int p = k + 1 + tid; p < n; p += nt) {
+      const int i = at[p];
+      const double v = rx[i] / l;
+      Lc[i] = v;
+      if (writer) Ag[(size_t)k * n + i] = v;
+    }
+    if (writer && tid == 0) Ag[(size_t)k * n + x] = l;
+    if (tid == 0) done[x] = 1;
+    __syncthreads();
+    // own remaining rows j: A_ji -= L_i L_j.  Contiguous over ALL columns:
+    // entries at pivoted columns (stale Lc) are never read again, the
+    // remaining ones get exactly the pivot-order operation
+    for (int lr = warp; lr < R; lr += nwarp) {
+      const int j = lr * CL + me;
+      if (j >= n || done[j]) continue;
+      double* row = A + (size_t)lr * n;
+      const double lj = Lc[j];
+      for (int i = lane; i < n; i += 32) row[i] = row[i] - Lc[i] * lj;
+    }
+    for (int i = tid; i < n; i += nt) d[i] = d[i] - Lc[i] * Lc[i];   // the diagonal replica, same operation
+    rank = k + 1;
+    csync();   // step k's updates (and reads of its pivot row) done everywhere
+  }
+  csync();   // all columns of L written
+  // columns of L into the final position order: Ag[c][p] = L_{at[p], c}, p >= c
+  for (int c = me; c < rank; c += CL) {
+    for (int i = tid; i < n; i += nt) Lc[i] = Ag[(size_t)c * n + i];
+    __syncthreads();
+    for (int p = c + tid; p < n; p += nt) Ag[(size_t)c * n + p] = Lc[at[p]];
+    __syncthreads();
+  }
+  if (me == 0) {
+    for (int i = tid; i < n; i += nt) perm[i] = at[i];
+    if (tid == 0) *rank_out = rank;
+  }
+}
+
 // Same algorithm and per-element arithmetic as k_pivchol, spread over a
 // cooperative grid: block 0 selects the pivot, swaps and scales column k; all
 // blocks share the rank-1 trailing update; two grid syncs per pivot.

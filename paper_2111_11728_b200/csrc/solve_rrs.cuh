@@ -259,6 +259,25 @@ static bool pivchol_cluster_try(double* A, int n, double tol, int* perm, int* ra
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = CL > 1 ? 1 : 0;
+  static const bool cl1 = [] {   // FETIGPU_PIVCHOL_CL1=0: the three-barrier kernel with physical swaps
+    const char* e = getenv("FETIGPU_PIVCHOL_CL1");
+    return !(e && e[0] == '0');
+  }();
+  if (cl1) {
+    static std::atomic<int> ok1{-1};
+    if (ok1.load() < 0) {
+      bool good = cudaFuncSetAttribute(k_pivchol_cl1<CL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       225 * 1024) == cudaSuccess;
+      if (good && CL > 8)
+        good = cudaFuncSetAttribute(k_pivchol_cl1<CL>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
+               cudaSuccess;
+      if (!good) cudaGetLastError();
+      ok1.store(good ? 1 : 0);
+    }
+    if (ok1.load() && cudaLaunchKernelEx(&cfg, k_pivchol_cl1<CL>, A, n, tol, perm, rank, status) == cudaSuccess)
+      return true;
+    cudaGetLastError();
+  }
   CK(cudaLaunchKernelEx(&cfg, k_pivchol_cl<CL>, A, n, tol, perm, rank, status, gx));
   return true;
 }
@@ -280,7 +299,11 @@ static bool launch_pivchol_cluster(double* A, int n, double tol, int* perm, int*
 // (FETIGPU_PIVCHOL_COOP0=1 forces it).  Scratch: ctl 4 ints, gx 2n + 64 doubles.
 static void launch_pivchol(double* A, int n, double tol, int* perm, int* rank, int* status, int* ctl, double* gx,
                            cudaStream_t st, double* lc = nullptr) {
-  if (launch_pivchol_cluster(A, n, tol, perm, rank, status, gx, st)) return;
+  static const bool no_cluster = [] {   // FETIGPU_PIVCHOL_CLUSTER=0: blocked / cooperative kernels for every n
+    const char* e = getenv("FETIGPU_PIVCHOL_CLUSTER");
+    return e && e[0] == '0';
+  }();
+  if (!no_cluster && launch_pivchol_cluster(A, n, tol, perm, rank, status, gx, st)) return;
   // blocked (panels of kPcNB pivots, one grid-wide trailing phase per panel;
   // the per-entry arithmetic of k_pivchol_coop1): at[] lives in perm, the
   // running diagonal and the control block in gx (2n + 64 doubles)

@@ -444,6 +444,29 @@ def test_pivoted_cholesky_blocked_bitwise(n, deficit):
     assert out["0"] == out["1"]
 
 
+@pytest.mark.parametrize("n,deficit", [(48, 0), (300, 17), (512, 0), (640, 40)])
+def test_pivoted_cholesky_cluster_one_barrier_bitwise(n, deficit):
+    """k_pivchol_cl1 (one cluster barrier per pivot, rows in original order,
+    replicated diagonal and position map) against k_pivchol_cl (physical
+    swaps, three barriers): rank, permutation and L bit for bit (one process
+    per variant: FETIGPU_PIVCHOL_CL1 is read once)."""
+    import subprocess
+    import sys
+    code = ("import sys, hashlib, numpy as np; sys.path.insert(0, %r);"
+            "from paper_2111_11728_b200 import engine;"
+            "rng = np.random.default_rng(%d); X = rng.standard_normal((%d, %d)) * np.logspace(0, -3, %d);"
+            "A = X @ X.T; p, L, r = engine.pivoted_cholesky(A);"
+            "print(r, hashlib.sha1(p.tobytes() + L.tobytes()).hexdigest())"
+            % (os.path.dirname(os.path.dirname(os.path.abspath(__file__))), n, n, n - deficit, n - deficit))
+    out = {}
+    for v in ("0", "1"):
+        env = dict(os.environ, FETIGPU_PIVCHOL_CL1=v)
+        out[v] = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                                check=True).stdout.split()
+    assert int(out["1"][0]) == n - deficit
+    assert out["0"] == out["1"]
+
+
 @pytest.mark.gpu
 def test_pivoted_cholesky_device_edge_cases(oracle_mod):
     from paper_2111_11728_b200 import engine
