@@ -505,7 +505,8 @@ struct ClusterArgs {
 __host__ __device__ constexpr int even_up(int n) { return (n + 1) & ~1; }
 __host__ __device__ constexpr size_t cluster_smem_doubles(int m, int Ns, int ndot, int fs, int ps, int xs) {
   return (size_t)even_up(fs) + even_up(ps) + 5 * (size_t)even_up(m) + 3 * (size_t)even_up(xs) +
-         3 * (size_t)even_up(3 * Ns) + (size_t)even_up(9 * Ns * Ns) + 4 * (size_t)ndot;
+         3 * (size_t)even_up(3 * Ns) + (size_t)even_up(9 * Ns * Ns) + 4 * (size_t)ndot +
+         15 * (size_t)even_up(xs);   // the CTA's own gather / projector maps (4 x 3 xs doubles, 2 x 3 xs ints)
 }
 
 // g_s = sign R_T^T (B_s^T v) by ONE warp, emulating proj_gather_fn's CTA
@@ -576,10 +577,37 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg_cluster(const ClusterArgs a
   double* h = gall + n3p;
   double* Hs = h + n3p;
   double* part = Hs + even_up(nc3 * nc3);
+  // this CTA's maps, staged once: operator (rows, coefs), preconditioner
+  // (rows, coefs), projector coefs and R_T rows -- every gather reads shared
+  // memory only
+  double* ocf = part + 4 * nd;
+  double* pcf = ocf + 3 * xp;
+  double* pjcf = pcf + 3 * xp;
+  double* RTs = pjcf + 3 * xp;
+  int* orow = reinterpret_cast<int*>(RTs + 3 * xp);
+  int* prow = orow + 3 * xp;
   __shared__ double s_sum[4];
   __shared__ int zoff[16];
+  __shared__ OpSub lpj[16];
   if (tid < 16) zoff[tid] = 0;
   OpSub dop = a.op[s], dpc = a.pc[s];
+  const OpSub dpj = a.pj[s];
+  for (int i = tid; i < dop.ns * 3; i += kThreads) {
+    orow[i] = a.oprows[dop.map_off + i];
+    ocf[i] = a.opcoef[dop.map_off + i];
+  }
+  for (int i = tid; i < dpc.ns * KRP; i += kThreads) {
+    prow[i] = a.pcrows[dpc.map_off + i];
+    pcf[i] = a.pccoef[dpc.map_off + i];
+  }
+  for (int i = tid; i < dpj.ns * 3; i += kThreads) {
+    pjcf[i] = a.pjcoef[dpj.map_off + i];
+    RTs[i] = a.RT[a.rt_off[s] + i];
+  }
+  if (tid == 0) {
+    lpj[s] = dpj;
+    lpj[s].map_off = 0;
+  }
   for (int i = tid; i < dop.ns * dop.ld; i += kThreads) Fs[i] = a.opmat[dop.moff + i];
   for (int i = tid; i < dpc.ns * dpc.ld; i += kThreads) Ps[i] = a.pcmat[dpc.moff + i];
   for (int i = tid; i < nc3 * nc3; i += kThreads) Hs[i] = a.H[i];
@@ -588,9 +616,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg_cluster(const ClusterArgs a
     r[i] = a.r[i];
     lam[i] = a.lam[i];
   }
-  OpSub lop = dop, lpc = dpc;
+  OpSub lop = dop, lpc = dpc;   // local views: matrices and maps in shared memory
   lop.moff = 0;
   lpc.moff = 0;
+  lop.map_off = 0;
+  lpc.map_off = 0;
   double rz = a.sc->rz, rz_old = a.sc->rz_old, breakdown = a.sc->breakdown;
   int it = a.ctl->it;
   const int max_it = a.ctl->max_it, trace_cap = a.ctl->trace_cap;
@@ -608,7 +638,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg_cluster(const ClusterArgs a
   // P-correction: g_s = -R_s^T B_s^T v by this CTA (the projector kernel's
   // CTA reduction), every g_s over DSMEM, then h = H g in every CTA
   auto proj_h = [&](const double* v) {
-    proj_gather_fn(s, 0, a.pj, a.pcrows, a.pjcoef, a.RT, a.rt_off, g, 0, -1.0, [&](int row) { return v[row]; });
+    proj_gather_fn(s, 0, lpj, prow, pjcf, RTs, zoff, g, 0, -1.0, [&](int row) { return v[row]; });
     cl.sync();
     for (int t = tid; t < nc3; t += kThreads) gall[t] = cl.map_shared_rank(g, t / 3)[t];
     __syncthreads();
@@ -660,9 +690,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg_cluster(const ClusterArgs a
       __syncthreads();
     }
     // ---- v_s = F_s B_s^T w
-    gather_xs<3>(dop, a.oprows, a.opcoef, xs, [&](int row, int) { return w[row]; });
+    gather_xs<3>(lop, orow, ocf, xs, [&](int row, int) { return w[row]; });
     __syncthreads();
-    gemv_rows_cta<3, true, true>(s, 0, 0, 1, xs, lop, Fs, a.oprows, a.opcoef, nullptr, nullptr, 0, vop, zoff, 0, 1);
+    gemv_rows_cta<3, true, true>(s, 0, 0, 1, xs, lop, Fs, orow, ocf, nullptr, nullptr, 0, vop, zoff, 0, 1);
     cl.sync();
     pprof_mark();
     // ---- q rows over DSMEM; delta, wr; P-correction of q
@@ -697,9 +727,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg_cluster(const ClusterArgs a
       }
     }
     __syncthreads();
-    gather_xs<KRP>(dpc, a.pcrows, a.pccoef, xs, [&](int row, int) { return r[row]; });
+    gather_xs<KRP>(lpc, prow, pcf, xs, [&](int row, int) { return r[row]; });
     __syncthreads();
-    gemv_rows_cta<KRP, true, true>(s, 0, 0, 1, xs, lpc, Ps, a.pcrows, a.pccoef, nullptr, nullptr, 0, vpc, zoff, 0, 1);
+    gemv_rows_cta<KRP, true, true>(s, 0, 0, 1, xs, lpc, Ps, prow, pcf, nullptr, nullptr, 0, vpc, zoff, 0, 1);
     cl.sync();
     pprof_mark();
     // ---- z = P (M r): rows over DSMEM, P-correction; rz, rr, zz
