@@ -6,6 +6,7 @@
 namespace fg {
 
 // ------------------------------------------- K15: persistent iteration ---
+static std::mutex g_persist_mu;   // one grid-barrier persistent kernel in flight per process
 // Per dual row the (subdomain, local index, coefficient) entries of a map
 // (operator or preconditioner) and one designated storing entry per row;
 // false if some row has more than two entries (or none, unless allowed: the
@@ -430,11 +431,17 @@ int Ctx::solve(const fetigpu_solve_opts& o, double* lambda_host, fetigpu_trace* 
     // to the graph below (kernels_persist.cuh)
     // (a launch that cannot be scheduled falls back to the next loop)
     bool single_kernel = false;
+    // Two grid-barrier persistent kernels from different contexts / host
+    // threads could each end up partly resident and wait on each other: the
+    // process runs one at a time (held until this solve's final sync).
+    // Cluster kernels need no lock (a cluster is co-scheduled as a whole).
+    std::unique_lock<std::mutex> persist_lock(g_persist_mu, std::defer_lock);
     if (cluster_ok(fo) && launch_cluster(lam.p, r.p, w.p, sc.p, dctl.p, dtrace.p)) {
       single_kernel = true;
       solve_loop = 4;
     } else {
       const int pg = persist_grid(fo);
+      if (pg > 0 && !persist_cluster) persist_lock.lock();
       if (pg > 0 && launch_persist(pg, fo, passes, psi_S, lam.p, r.p, z.p, w.p, q.p, sc.p, Wst.p, Qst.p, psi.p,
                                    psi_part.p, cnt.p, dctl.p, dtrace.p)) {
         single_kernel = true;
