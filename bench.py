@@ -524,9 +524,20 @@ def main():
     achieved = st["main_kernel_bytes"] / (t_main_ms * 1e-3) / 1e9
     traffic = None
     sym = st["main_kernel_bytes"] < 0.9 * c4_work()["main_bytes"]
-    kname = ("k_sym_gemv_scatter<1,true> (symmetric-packed F_rr stream + fused coarse pre-pass)" if sym
-             else "k_gather_gemv_scatter<1,true> (F_rr stream + fused coarse pre-pass)")
-    tp = os.path.join(ROOT, "profiles", "traffic_sym_gemv.json" if sym else "traffic_gemv.json")
+    kname = {2: "k_sym_gemv_tma<1,true> (symmetric-packed F_rr tiles by TMA bulk copies into per-warp mbarrier "
+                "rings, persistent grid, fused coarse pre-pass)",
+             1: "k_sym_gemv_scatter<1,true> (symmetric-packed F_rr stream by LDG + fused coarse pre-pass)",
+             0: "k_gather_gemv_scatter<1,true> (F_rr stream + fused coarse pre-pass)"}[st["apply_kernel"]]
+    # the apply only reads its operator: the read-only stream ceiling of this
+    # device, measured here, beside the copy (read + write) figure the driver
+    # wrote to MEASURED_PEAKS.json, which stays the roofline's `peak`
+    try:
+        read_peak = engine.hbm_read_peak(2 << 30, 10)
+    except Exception as e:  # noqa: BLE001
+        log(f"note: hbm_read_peak failed: {e}")
+        read_peak = None
+    tp = os.path.join(ROOT, "profiles", {2: "traffic_sym_gemv_tma.json", 1: "traffic_sym_gemv.json",
+                                         0: "traffic_gemv.json"}[st["apply_kernel"]])
     if os.path.exists(tp):
         try:
             traffic = json.load(open(tp)).get("dram_bytes_per_launch")
@@ -640,7 +651,12 @@ def main():
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": kname,
                          "kernel_ms": t_main_ms, "kernel_share": t_main_ms / t_apply_ms,
-                         "bytes_per_launch": st["main_kernel_bytes"], "peak_kind": peak_kind},
+                         "bytes_per_launch": st["main_kernel_bytes"], "peak_kind": peak_kind,
+                         "peak_note": "peak = copy bandwidth (read + write bytes) from MEASURED_PEAKS.json; the "
+                                      "kernel only reads, so frac can exceed 1 -- read_only_peak is the same "
+                                      "device's read-only stream ceiling measured by fetigpu_hbm_read_peak",
+                         "read_only_peak": read_peak,
+                         "frac_read_only": (achieved / read_peak) if read_peak else None},
             "clocks": clocks,
             "build": {"ms": st["build_ms"], "nd_ms": st["nd_ms"], "slot_ms": st["slot_ms"],
                       "wall_s": build_wall},

@@ -161,6 +161,11 @@ typedef struct fetigpu_stats {
    * lambda read + y written and the gather lists -- the roofline bytes of
    * the apply actually executed (op_bytes counts full F_s storage). */
   double stream_bytes;
+  /* dominant apply kernel: 0 full-matrix GEMV (k_gather_gemv_scatter), 1
+   * symmetric-packed tiles by LDG (k_sym_gemv_scatter), 2 symmetric-packed
+   * tiles by TMA bulk copies into per-warp mbarrier rings on a persistent
+   * grid (k_sym_gemv_tma); apply_ring = ring slots per warp of the latter */
+  int apply_kernel, apply_ring;
 } fetigpu_stats;
 
 /* Select the CUDA device used by contexts built afterwards from this host
@@ -282,6 +287,11 @@ int fetigpu_dla_tri_inv(const double* L, int n, long long ldl, double* X);
 int fetigpu_dla_time_gemm(int ta, int tb, int M, int N, int K, int reps, double* ms);
 /* Measured FP64 issue peaks of this device (DMMA m8n8k4 and DFMA), TFLOP/s. */
 int fetigpu_fp64_peak(double* tflops_dmma, double* tflops_dfma);
+/* Measured read-only HBM bandwidth of this device (GB/s): `bytes` (at least
+ * 256 MB, much larger than L2) streamed `reps` times by 16-byte loads.  The
+ * ceiling of the F-apply's operator stream, which only reads; the copy figure
+ * of MEASURED_PEAKS.json counts read + write bytes and is lower. */
+int fetigpu_hbm_read_peak(size_t bytes, int reps, double* gbs);
 /* DMMA fragment-layout self test: C (8x8 row-major) = A (8x4) B (4x8). */
 int fetigpu_selftest_dmma(const double* A, const double* B, double* C);
 

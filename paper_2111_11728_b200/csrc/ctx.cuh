@@ -65,6 +65,15 @@ struct Ctx {
   DBuf<double> d_pcsymtiles;
   DBuf<SymSub> d_pcsym;
   int pc_sym_smem = 0;
+  // TMA form of the symmetric-packed GEMV (k_sym_gemv_tma, the default;
+  // FETIGPU_SYM_TMA=0 keeps the LDG kernel): ring slots, padded length,
+  // dynamic shared memory, persistent grid (2 CTAs per SM)
+  bool sym_tma = false;
+  int sym_ring = 0, sym_npad = 0, pc_sym_ring = 0, pc_sym_npad = 0, sym_grid = 0;
+  // 1: next x_s gathered inside the tile loop, 2: next A'' prefetched into L2 (measured slower),
+  // 4: coarse arrival count per subdomain instead of once per CTA (FETIGPU_SYM_FLAGS)
+  int sym_flags = 1;
+  size_t sym_tma_bytes = 0, pc_sym_tma_bytes = 0;
   std::vector<std::vector<double>> slot_sign;
   DBuf<int> d_oprows, d_slot_of, d_fac_ne, d_top_pos, d_top_off;
   DBuf<long long> d_fac_off;
@@ -227,6 +236,20 @@ struct Ctx {
   // y_zeroed: the caller already zeroed y (T-FETI scatters into it); lets the
   // solver loop drop the memset node and chain the GEMV with PDL
   void apply_F(const double* x, double* y, int ncols, int ldx, int ldy, bool y_zeroed = false);
+  // one launch of the symmetric-packed GEMV over subdomains [s0, s0 + n)
+  struct SymArgs {
+    bool pc = false;        // preconditioner blocks (else the operator)
+    int kr = 1;             // map entries per local DOF
+    bool store_v = false;   // FETI-DP phase 1: v_s stored (and t_s, g); else scattered into y
+    const double* x = nullptr;
+    double* y = nullptr;
+    int s0 = 0, n = 0;
+    double* zero_y = nullptr;   // FETI-DP phase 1 also zeroes this vector (slices by subdomain)
+    bool coarse_gather = false;
+    bool pdl = false;
+    bool per_cta = false;   // one subdomain per CTA (the host-pipelined chunks)
+  };
+  void launch_sym(cudaStream_t q, const SymArgs& a);
 
   void setup_pipe();
 

@@ -708,6 +708,43 @@ void Ctx::build_ops(const SlotOut& so, std::future<HostMaps>& maps) {
     raise_smem_limit(k_sym_gemv_scatter<3, false>, pc_sym_smem);
     CK(cudaStreamSynchronize(st));
     pc_sym = true;
+    // TMA ring form (k_sym_gemv_tma): persistent grid, a private ring of 8 KB slots per warp
+    {
+      const char* e = getenv("FETIGPU_SYM_TMA");
+      const char* er = getenv("FETIGPU_SYM_RING");
+      int dev = 0, sms = 0, per_sm = 0, optin = 0;
+      CK(cudaGetDevice(&dev));
+      CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+      CK(cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));
+      CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+      // slots per warp: 2 CTAs per SM if one slot per warp fits beside x_s and the partials, else 1 CTA
+      const char* ec = getenv("FETIGPU_SYM_CTAS");
+      int ctas = ec && ec[0] == '1' ? 1 : 2;
+      auto ring_for = [&](int npad) {
+        const long long budget = std::min<long long>(optin, per_sm / ctas - 1024);
+        const long long left = budget - (long long)sym_tma_smem(0, npad);
+        int r = (int)std::max<long long>(0, left / (kSymWarps * kSymTileBytes));
+        r = std::min(r, kSymRingMax);
+        if (er && atoi(er) > 0) r = std::min(r, atoi(er));
+        return r;
+      };
+      if (ring_for(nbmax * 32) < 1 || ring_for(pnbmax * 32) < 1) ctas = 1;
+      if (const char* ef = getenv("FETIGPU_SYM_FLAGS")) sym_flags = atoi(ef);
+      sym_npad = nbmax * 32;
+      pc_sym_npad = pnbmax * 32;
+      sym_ring = ring_for(sym_npad);
+      pc_sym_ring = ring_for(pc_sym_npad);
+      sym_tma = !(e && e[0] == '0') && sym_ring >= 1 && pc_sym_ring >= 1;
+      if (sym_tma) {
+        sym_tma_bytes = sym_tma_smem(sym_ring, sym_npad);
+        pc_sym_tma_bytes = sym_tma_smem(pc_sym_ring, pc_sym_npad);
+        const size_t mx = std::max(sym_tma_bytes, pc_sym_tma_bytes);
+        raise_smem_limit(k_sym_gemv_tma<1, true>, mx);
+        raise_smem_limit(k_sym_gemv_tma<1, false>, mx);
+        raise_smem_limit(k_sym_gemv_tma<3, false>, mx);
+        sym_grid = ctas * sms;
+      }
+    }
   }
   ptimer.mark("symmetric packing", st);
   setup_pipe();

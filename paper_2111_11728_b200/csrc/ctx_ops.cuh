@@ -209,16 +209,57 @@ void Ctx::coarse_solve_packed(bool g_ready, double* zero_y) {
   LAUNCH_CHECK();
 }
 
+// The symmetric-packed GEMV (K4 / K7 at C4 sizes) over subdomains [s0, s0+n):
+// the TMA ring kernel on a persistent grid (default) or the LDG kernel with
+// one CTA per subdomain (FETIGPU_SYM_TMA=0); bit-identical results.
+void Ctx::launch_sym(cudaStream_t q, const SymArgs& a) {
+  if (a.n <= 0) return;
+  const SymSub* subs = a.pc ? d_pcsym.p : d_sym.p;
+  const double* tiles = a.pc ? d_pcsymtiles.p : d_symtiles.p;
+  const int* rows = a.pc ? d_pcrows.p : d_oprows.p;
+  const double* coefs = a.pc ? d_pccoef.p : d_opcoef_apply.p;
+  double* vbuf = a.store_v ? d_vbuf.p : nullptr;
+  const int* voff = a.store_v ? d_voff.p : nullptr;
+  const DpSub* dps = a.store_v ? d_dp.p : nullptr;
+  const double* abc = a.store_v ? d_abc.p : nullptr;
+  double* tbuf = a.store_v ? d_tbuf.p : nullptr;
+  const int ny = a.zero_y ? su.m : 0, nsub = a.zero_y ? su.Ns : 1;
+  const CoarseGather* cgp = a.coarse_gather && su.Nc ? d_cgather.p : nullptr;
+  auto go = [&](auto ktma, auto kldg) {
+    if (sym_tma) {
+      const int ring = a.pc ? pc_sym_ring : sym_ring, npad = a.pc ? pc_sym_npad : sym_npad;
+      const size_t smem = a.pc ? pc_sym_tma_bytes : sym_tma_bytes;
+      const int grid = a.per_cta ? a.n : std::min(a.n, sym_grid);
+      if (a.pdl)
+        launch_pdl(ktma, grid, 256, smem, q, subs, tiles, rows, coefs, a.x, a.y, vbuf, voff, dps, abc, tbuf, a.s0,
+                   a.s0 + a.n, a.zero_y, ny, nsub, cgp, ring, npad, sym_flags);
+      else
+        ktma<<<grid, 256, smem, q>>>(subs, tiles, rows, coefs, a.x, a.y, vbuf, voff, dps, abc, tbuf, a.s0,
+                                     a.s0 + a.n, a.zero_y, ny, nsub, cgp, ring, npad, sym_flags);
+    } else {
+      const int smem = a.pc ? pc_sym_smem : sym_smem;
+      if (a.pdl)
+        launch_pdl(kldg, a.n, 256, smem, q, subs, tiles, rows, coefs, a.x, a.y, vbuf, voff, dps, abc, tbuf, a.s0,
+                   a.zero_y, ny, nsub, cgp);
+      else
+        kldg<<<a.n, 256, smem, q>>>(subs, tiles, rows, coefs, a.x, a.y, vbuf, voff, dps, abc, tbuf, a.s0, a.zero_y,
+                                    ny, nsub, cgp);
+    }
+  };
+  if (a.store_v) go(k_sym_gemv_tma<1, true>, k_sym_gemv_scatter<1, true>);
+  else if (a.kr == 1) go(k_sym_gemv_tma<1, false>, k_sym_gemv_scatter<1, false>);
+  else go(k_sym_gemv_tma<3, false>, k_sym_gemv_scatter<3, false>);
+}
+
 void Ctx::apply_F(const double* x, double* y, int ncols, int ldx, int ldy, bool y_zeroed) {
   const int Ns = su.Ns;
   if (su.method == FETIGPU_TFETI) {
     if (ncols == 1 && y_zeroed) {
-      if (use_sym)
-        launch_pdl(k_sym_gemv_scatter<3, false>, Ns, 256, sym_smem, st, (const SymSub*)d_sym.p,
-                   (const double*)d_symtiles.p, (const int*)d_oprows.p, (const double*)d_opcoef_apply.p, x, y,
-                   (double*)nullptr, (const int*)nullptr, (const DpSub*)nullptr, (const double*)nullptr,
-                   (double*)nullptr, 0, (double*)nullptr, 0, 1, (const CoarseGather*)nullptr);
-      else
+      if (use_sym) {
+        SymArgs sa;
+        sa.kr = 3; sa.x = x; sa.y = y; sa.n = Ns; sa.pdl = true;
+        launch_sym(st, sa);
+      } else
         launch_pdl(k_gather_gemv_scatter<3, false>, dim3(Ns, 1, rsplit), kThreads, max_ld * 8, st,
                    (const OpSub*)d_op.p, (const double*)d_opmat.p, (const int*)d_oprows.p,
                    (const double*)d_opcoef_apply.p, x, y, (double*)nullptr, 0, (double*)nullptr,
@@ -229,10 +270,11 @@ void Ctx::apply_F(const double* x, double* y, int ncols, int ldx, int ldy, bool 
     }
     for (int c = 0; c < ncols; ++c) CK(cudaMemsetAsync(y + (size_t)c * ldy, 0, su.m * 8, st));
     if (use_sym) {
-      for (int c = 0; c < ncols; ++c)
-        k_sym_gemv_scatter<3, false><<<Ns, 256, sym_smem, st>>>(d_sym.p, d_symtiles.p, d_oprows.p,
-                                                                d_opcoef_apply.p, x + (size_t)c * ldx,
-                                                                y + (size_t)c * ldy, nullptr, nullptr);
+      for (int c = 0; c < ncols; ++c) {
+        SymArgs sa;
+        sa.kr = 3; sa.x = x + (size_t)c * ldx; sa.y = y + (size_t)c * ldy; sa.n = Ns;
+        launch_sym(st, sa);
+      }
     } else {
       dim3 grid(Ns, ncols, rsplit);
       k_gather_gemv_scatter<3, false><<<grid, kThreads, max_ld * 8, st>>>(
@@ -245,11 +287,9 @@ void Ctx::apply_F(const double* x, double* y, int ncols, int ldx, int ldy, bool 
       double* yc = y + (size_t)c * ldy;
       // phase 1: v_s = F''_s x_s and t_s = A''^T x_s (one kernel; it also zeroes y)
       if (use_sym) {
-        launch_pdl(k_sym_gemv_scatter<1, true>, Ns, 256, sym_smem, st, (const SymSub*)d_sym.p,
-                   (const double*)d_symtiles.p, (const int*)d_oprows.p, (const double*)d_opcoef_apply.p, xc,
-                   (double*)nullptr, d_vbuf.p, (const int*)d_voff.p, (const DpSub*)d_dp.p,
-                   (const double*)d_abc.p, d_tbuf.p, 0, yc, su.m, Ns,
-                   (const CoarseGather*)(su.Nc ? d_cgather.p : nullptr));
+        SymArgs sa;
+        sa.store_v = true; sa.x = xc; sa.n = Ns; sa.zero_y = yc; sa.coarse_gather = true; sa.pdl = true;
+        launch_sym(st, sa);
       } else {
         launch_pdl(k_gather_gemv_scatter<1, true>, dim3(Ns, 1, rsplit), kThreads, max_ld * 8, st,
                    (const OpSub*)d_op.p, (const double*)d_opmat.p, (const int*)d_oprows.p,
@@ -314,10 +354,10 @@ void Ctx::apply_F_host(const double* xh, double* yh) {
       cudaStream_t q = pipe_st[c];
       CK(cudaStreamWaitEvent(q, pipe_in[c], 0));
       const int nblk = pipe_s0[c + 1] - pipe_s0[c];
-      k_sym_gemv_scatter<1, true><<<nblk, 256, sym_smem, q>>>(d_sym.p, d_symtiles.p, d_oprows.p,
-                                                               d_opcoef_apply.p, x, nullptr, d_vbuf.p, d_voff.p,
-                                                               d_dp.p, d_abc.p, d_tbuf.p, pipe_s0[c], y, m,
-                                                               su.Ns, su.Nc ? d_cgather.p : nullptr);
+      SymArgs sa;
+      sa.store_v = true; sa.x = x; sa.s0 = pipe_s0[c]; sa.n = nblk; sa.zero_y = y; sa.coarse_gather = true;
+      sa.per_cta = true;
+      launch_sym(q, sa);
       LAUNCH_CHECK();
       CK(cudaEventRecord(pipe_done[c], q));
       CK(cudaStreamWaitEvent(st, pipe_done[c], 0));
@@ -336,11 +376,9 @@ void Ctx::apply_precond(const double* r, double* z, double* Zcols, bool row_majo
   if (Zcols) CK(cudaMemsetAsync(Zcols, 0, (size_t)su.m * su.Ns * 8, st));
   const int ldz = row_major ? 1 : su.m, zrs = row_major ? su.Ns : 1;
   if (pc_sym && !Zcols) {
-    auto k = KRp == 1 ? k_sym_gemv_scatter<1, false> : k_sym_gemv_scatter<3, false>;
-    launch_pdl(k, su.Ns, 256, pc_sym_smem, st, (const SymSub*)d_pcsym.p, (const double*)d_pcsymtiles.p,
-               (const int*)d_pcrows.p, (const double*)d_pccoef.p, r, z, (double*)nullptr, (const int*)nullptr,
-               (const DpSub*)nullptr, (const double*)nullptr, (double*)nullptr, 0, (double*)nullptr, 0, 1,
-               (const CoarseGather*)nullptr);
+    SymArgs sa;
+    sa.pc = true; sa.kr = KRp == 1 ? 1 : 3; sa.x = r; sa.y = z; sa.n = su.Ns; sa.pdl = true;
+    launch_sym(st, sa);
     LAUNCH_CHECK();
     return;
   }
@@ -498,9 +536,9 @@ void Ctx::shard_phase1(const double* x, double* y, double* tout, bool precond) {
   if (n <= 0 || su.m == 0) return;
   if (precond) {
     if (pc_sym) {
-      auto k = KRp == 1 ? k_sym_gemv_scatter<1, false> : k_sym_gemv_scatter<3, false>;
-      k<<<n, 256, pc_sym_smem, st>>>(d_pcsym.p, d_pcsymtiles.p, d_pcrows.p, d_pccoef.p, x, y, nullptr, nullptr,
-                                     nullptr, nullptr, nullptr, s0, nullptr, 0, 1, nullptr);
+      SymArgs sa;
+      sa.pc = true; sa.kr = KRp == 1 ? 1 : 3; sa.x = x; sa.y = y; sa.s0 = s0; sa.n = n;
+      launch_sym(st, sa);
     } else {
       auto k = KRp == 1 ? k_gather_gemv_scatter<1, false> : k_gather_gemv_scatter<3, false>;
       k<<<dim3(n, 1, pc_rsplit), kThreads, max_pc_ld * 8, st>>>(d_pc.p + s0, d_pcmat.p, d_pcrows.p, d_pccoef.p, x,
@@ -511,22 +549,22 @@ void Ctx::shard_phase1(const double* x, double* y, double* tout, bool precond) {
     return;
   }
   if (su.method == FETIGPU_TFETI) {
-    if (use_sym)
-      k_sym_gemv_scatter<3, false><<<n, 256, sym_smem, st>>>(d_sym.p, d_symtiles.p, d_oprows.p, d_opcoef_apply.p,
-                                                             x, y, nullptr, nullptr, nullptr, nullptr, nullptr, s0,
-                                                             nullptr, 0, 1, nullptr);
-    else
+    if (use_sym) {
+      SymArgs sa;
+      sa.kr = 3; sa.x = x; sa.y = y; sa.s0 = s0; sa.n = n;
+      launch_sym(st, sa);
+    } else
       k_gather_gemv_scatter<3, false><<<dim3(n, 1, rsplit), kThreads, max_ld * 8, st>>>(
           d_op.p + s0, d_opmat.p, d_oprows.p, d_opcoef_apply.p, x, y, nullptr, 0, nullptr, nullptr, su.m, su.m, 1,
           nullptr, nullptr, nullptr);
     LAUNCH_CHECK();
     return;
   }
-  if (use_sym)
-    k_sym_gemv_scatter<1, true><<<n, 256, sym_smem, st>>>(d_sym.p, d_symtiles.p, d_oprows.p, d_opcoef_apply.p, x,
-                                                          nullptr, d_vbuf.p, d_voff.p, d_dp.p, d_abc.p, d_tbuf.p, s0,
-                                                          nullptr, 0, 1, nullptr);
-  else
+  if (use_sym) {
+    SymArgs sa;
+    sa.store_v = true; sa.x = x; sa.s0 = s0; sa.n = n;
+    launch_sym(st, sa);
+  } else
     k_gather_gemv_scatter<1, true><<<dim3(n, 1, rsplit), kThreads, max_ld * 8, st>>>(
         d_op.p + s0, d_opmat.p, d_oprows.p, d_opcoef_apply.p, x, nullptr, nullptr, 0, d_vbuf.p, d_voff.p + s0,
         su.m, 0, 1, d_dp.p + s0, d_abc.p, d_tbuf.p);

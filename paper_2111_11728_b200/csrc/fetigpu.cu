@@ -103,6 +103,8 @@ int fetigpu_stats_get(const fetigpu_ctx* ctx, fetigpu_stats* s) {
     s->op_bytes = 8 * sn2 + (dp ? 16 * snc + 8.0 * c.su.Nc * c.su.Nc : 0) + 16.0 * c.su.m + 8 * sns;
     s->op_flops_per_col = 2 * sn2 + (dp ? 4 * snc + 2.0 * c.su.Nc * c.su.Nc : 0);
     s->main_kernel_bytes = c.use_sym ? c.sym_bytes : 8 * sn2;
+    s->apply_kernel = c.use_sym ? (c.sym_tma ? 2 : 1) : 0;
+    s->apply_ring = c.use_sym && c.sym_tma ? c.sym_ring : 0;
     double coarse = 0;
     if (dp) {
       const double nbc = (c.su.Nc + 31) / 32;
@@ -428,6 +430,38 @@ int fetigpu_fp64_peak(double* tflops_dmma, double* tflops_dfma) {
   });
 }
 
+int fetigpu_hbm_read_peak(size_t bytes, int reps, double* gbs) {
+  return guarded([&] {
+    if (!gbs || reps < 1) fail(FETIGPU_E_INVALID_ARGUMENT, "hbm_read_peak: bad arguments");
+    int dev = 0, sms = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    bytes = std::max<size_t>(bytes, (size_t)1 << 28) & ~(size_t)4095;
+    DBuf<double> buf, out;
+    buf.alloc(bytes / 8);
+    out.alloc(8);
+    CK(cudaMemset(buf.p, 0, bytes));
+    cudaEvent_t a, b;
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+    double best = 0.0;
+    for (int grid : {4 * sms, 8 * sms, 16 * sms}) {
+      for (int r = 0; r < 3; ++r) k_peak_read<8><<<grid, 256>>>((const double2*)buf.p, bytes / 16, out.p);
+      CK(cudaEventRecord(a));
+      for (int r = 0; r < reps; ++r) k_peak_read<8><<<grid, 256>>>((const double2*)buf.p, bytes / 16, out.p);
+      CK(cudaEventRecord(b));
+      CK(cudaEventSynchronize(b));
+      LAUNCH_CHECK();
+      float t = 0;
+      CK(cudaEventElapsedTime(&t, a, b));
+      best = std::max(best, (double)bytes * reps / (t * 1e-3) / 1e9);
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    *gbs = best;
+  });
+}
+
 // ---- dense algebra hooks (dla.cuh): host-buffer GEMM / triangular inverse
 // for the parity tests, device-resident GEMM timing for the bench
 int fetigpu_dla_gemm(int ta, int tb, int M, int N, int K, double alpha, const double* A, long long lda,
@@ -677,13 +711,11 @@ int fetigpu_time_apply(fetigpu_ctx* ctx, const double* x, double* y, int ncols, 
         const double* xc = x + (size_t)col * c.su.m;
         double* yc = y + (size_t)col * c.su.m;
         if (c.use_sym) {
-          if (c.su.method == FETIGPU_TFETI)
-            k_sym_gemv_scatter<3, false><<<c.su.Ns, 256, c.sym_smem, c.st>>>(
-                c.d_sym.p, c.d_symtiles.p, c.d_oprows.p, c.d_opcoef_apply.p, xc, yc, nullptr, nullptr);
-          else
-            k_sym_gemv_scatter<1, true><<<c.su.Ns, 256, c.sym_smem, c.st>>>(
-                c.d_sym.p, c.d_symtiles.p, c.d_oprows.p, c.d_opcoef_apply.p, xc, nullptr, c.d_vbuf.p, c.d_voff.p,
-                c.d_dp.p, c.d_abc.p, c.d_tbuf.p);
+          Ctx::SymArgs sa;
+          sa.x = xc; sa.n = c.su.Ns;
+          if (c.su.method == FETIGPU_TFETI) { sa.kr = 3; sa.y = yc; }
+          else sa.store_v = true;
+          c.launch_sym(c.st, sa);
         } else if (c.su.method == FETIGPU_TFETI) {
           k_gather_gemv_scatter<3, false><<<dim3(c.su.Ns, 1, c.rsplit), kThreads, c.max_ld * 8, c.st>>>(
               c.d_op.p, c.d_opmat.p, c.d_oprows.p, c.d_opcoef_apply.p, xc, yc, nullptr, 0, nullptr, nullptr,

@@ -332,6 +332,271 @@ __global__ void __launch_bounds__(256) k_sym_gemv_scatter(
   }
 }
 
+// ---- K4 on symmetric-packed F_s, TMA form (the default since round 2) ----
+// The same arithmetic per tile, per warp and per subdomain as
+// k_sym_gemv_scatter (bit-identical results), but the operator stream is
+// moved by the TMA engine and the grid is persistent (CTA b walks subdomains
+// s0 + b, s0 + b + G, ...).  Every warp owns a private ring of R 8 KB
+// shared-memory slots, each with its own mbarrier, and a cursor over ITS
+// stream of tiles (t = warp, warp + 8, ... of each of the CTA's subdomains in
+// turn): one cp.async.bulk per tile, and as soon as the warp has drained a
+// slot into registers it requests its next unrequested tile into that slot --
+// across subdomain boundaries -- so a slot is in flight except for the few
+// cycles between arrival and refill, also while the CTA gathers x_s or
+// reduces its partials; the first tiles are requested before
+// griddepcontrol.wait (the operator does not depend on the predecessor
+// kernel).  A slot is filled and drained by one warp only, in order, so the
+// barrier phase a warp waits for is always the slot's current or next one.
+// A warp of LDG.64 loads keeps its 8 KB in flight only between issue and use
+// and measured 6.35 TB/s; a read-only stream of this shape reaches 7.1-7.3
+// TB/s on a B200 (tools/read_peak.cu).
+__device__ __forceinline__ uint32_t smem_addr32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_parity(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@p bra DONE_%=;\n"
+      "bra WAIT_%=;\n"
+      "DONE_%=:\n"
+      "}\n" ::"r"(smem_addr32(b)),
+      "r"(parity)
+      : "memory");
+}
+// one 1D bulk copy global -> shared, completing `bytes` on the mbarrier; L2 evict-first (read once)
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr32(bar)), "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::
+          "r"(smem_addr32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr32(bar)), "l"(pol)
+      : "memory");
+}
+constexpr int kSymRingMax = 2;                        // slots per warp (the 8 x 2 barriers share one 128-byte line)
+constexpr int kSymTileBytes = 32 * 32 * 8;
+__host__ __device__ constexpr size_t sym_tma_smem(int R, int npad) {
+  return (size_t)R * kSymWarps * kSymTileBytes + 128 + (size_t)npad * (2 + kSymWarps) * 8;
+}
+// L2 prefetch of [p, p + bytes) (16-byte granules inside the range)
+__device__ __forceinline__ void prefetch_l2_bulk(const void* p, size_t bytes) {
+  const uintptr_t a = ((uintptr_t)p + 15) & ~(uintptr_t)15, e = ((uintptr_t)p + bytes) & ~(uintptr_t)15;
+  if (e > a)
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"((const void*)a), "r"((uint32_t)(e - a))
+                 : "memory");
+}
+
+template <int KR, bool STORE_V>
+__global__ void __launch_bounds__(256, 2) k_sym_gemv_tma(
+    const SymSub* __restrict__ subs, const double* __restrict__ tiles, const int* __restrict__ rows,
+    const double* __restrict__ coefs, const double* __restrict__ x, double* __restrict__ y,
+    double* __restrict__ vbuf, const int* __restrict__ voff, const DpSub* __restrict__ dps,
+    const double* __restrict__ abc, double* __restrict__ tbuf, int s0, int s1, double* __restrict__ zero_y, int ny,
+    int nsub, const CoarseGather* cgp, int R, int npad_max, int flags) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  const size_t ring_bytes = (size_t)R * kSymWarps * kSymTileBytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smraw + ring_bytes);     // 8 R barriers
+  double* xs_buf = reinterpret_cast<double*>(smraw + ring_bytes + 128); // 2 x npad (double-buffered x_s)
+  double* part = xs_buf + 2 * npad_max;                                 // kSymWarps x npad
+  const int G = gridDim.x, sfirst = s0 + blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* wring = reinterpret_cast<double*>(smraw) + (size_t)warp * R * 1024;   // this warp's R slots
+  uint64_t* wfull = full + warp * R;
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  // this warp's request cursor: tile ct of subdomain cs (cnt tiles at ctoff)
+  int cs = sfirst, ct = warp, cnt = 0, nreq = 0;
+  long long ctoff = 0;
+  auto cursor_load = [&]() {
+    if (cs < s1) {
+      const SymSub q = subs[cs];
+      cnt = q.nb * (q.nb + 1) / 2;
+      ctoff = q.toff;
+    }
+  };
+  auto request_next = [&]() {   // warp-uniform; lane 0 issues
+    while (cs < s1 && ct >= cnt) {
+      cs += G;
+      ct = warp;
+      cursor_load();
+    }
+    if (cs < s1) {
+      const int slot = nreq % R;
+      if (lane == 0)
+        tma_load_1d(wring + (size_t)slot * 1024, tiles + ctoff + (size_t)ct * 1024, kSymTileBytes, wfull + slot,
+                    pol);
+      ++nreq;
+      ct += kSymWarps;
+    }
+  };
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < R * kSymWarps; ++i) mbar_init(full + i, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  cursor_load();
+  for (int i = 0; i < R; ++i) request_next();
+  pdl_wait();
+  int ncons = 0;   // tiles this warp has drained
+  // x_s of the CTA's NEXT subdomain is gathered inside the tile loop (KR = 1):
+  // chain c covers local DOFs j = 256 c + 32 warp + lane in three of the
+  // warp's iterations -- map entry, then x[row], then the store -- each load
+  // consumed one tile later, so its latency hides behind the tile arithmetic
+  bool have_xs = false;   // the current subdomain's x_s is already in its buffer
+  int xsel = 0;
+  for (int s = sfirst; s < s1; s += G) {
+    const SymSub d = subs[s];
+    double* xs = xs_buf + xsel * npad_max;
+    double* xs_next = xs_buf + (xsel ^ 1) * npad_max;
+    if (STORE_V && zero_y) {  // FETI-DP: phase 1 never writes y, so its slice is zeroed here for phase 2
+      const long long a = (long long)ny * s / nsub, e = (long long)ny * (s + 1) / nsub;
+      for (long long i = a + threadIdx.x; i < e; i += blockDim.x) zero_y[i] = 0.0;
+    }
+    const int npad = d.nb * 32;
+    const int* rw = rows + d.map_off;
+    const double* cf = coefs + d.map_off;
+    if (!have_xs) {
+      for (int j = threadIdx.x; j < npad; j += blockDim.x) {
+        double acc = 0.0;
+        if (j < d.ns) {
+#pragma unroll
+          for (int k = 0; k < KR; ++k) {
+            const int r = rw[j * KR + k];
+            if (r >= 0) acc += cf[j * KR + k] * x[r];
+          }
+        }
+        xs[j] = acc;
+      }
+    }
+    // the next subdomain: its A'' rows into L2 now, its x_s during the tile loop
+    const int sn = s + G;
+    SymSub dn = d;
+    bool pre = false;
+    int nchain = 0;
+    if (sn < s1) {
+      dn = subs[sn];
+      nchain = (dn.nb * 32 + 255) / 256;
+      pre = KR == 1 && (flags & 1) && (d.nb * (d.nb + 1) / 2) / kSymWarps >= 3 * nchain;
+      if (STORE_V && dps && (flags & 2) && threadIdx.x == 0) {
+        const DpSub pn = dps[sn];
+        prefetch_l2_bulk(abc + pn.abc_off, (size_t)dn.ns * pn.nc * 8);
+      }
+    }
+    const int* rwn = rows + dn.map_off;
+    const double* cfn = coefs + dn.map_off;
+    int pr = -1;
+    double pc = 0.0, px = 0.0;
+    for (int j = threadIdx.x; j < kSymWarps * npad; j += blockDim.x) part[j] = 0.0;
+    __syncthreads();
+    if (STORE_V && dps) fused_dp_t(dps[s], abc, xs, d.ns, tbuf, (flags & 4) ? cgp : nullptr);
+    double* pw = part + warp * npad;
+    const int ntiles = d.nb * (d.nb + 1) / 2;
+    int it = 0;
+    for (int t = warp; t < ntiles; t += kSymWarps, ++it) {
+      if (pre && it < 3 * nchain) {
+        const int ch = it / 3, stage = it - 3 * ch, j = ch * 256 + threadIdx.x;
+        if (stage == 0) {
+          pr = -1;
+          if (j < dn.ns) {
+            pr = rwn[j];
+            pc = cfn[j];
+          }
+        } else if (stage == 1) {
+          px = pr >= 0 ? x[pr] : 0.0;
+        } else if (j < dn.nb * 32) {
+          double acc = 0.0;
+          if (pr >= 0) acc += pc * px;
+          xs_next[j] = acc;
+        }
+      }
+      int bi = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+      while (bi * (bi + 1) / 2 > t) --bi;
+      while ((bi + 1) * (bi + 2) / 2 <= t) ++bi;
+      const int bj = t - bi * (bi + 1) / 2;
+      const int slot = ncons % R;
+      mbar_wait_parity(wfull + slot, (uint32_t)(ncons / R) & 1u);
+      ++ncons;
+      const double* T = wring + (size_t)slot * 1024;
+      double f[32];
+#pragma unroll
+      for (int r = 0; r < 32; ++r) f[r] = T[r * 32 + lane];
+      // the slot is drained (every lane holds its 32 values): refill it.  The
+      // generic-proxy reads are ordered before the async-proxy write by the
+      // warp barrier and the proxy fence of the issuing lane
+      __syncwarp();
+      if (lane == 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      request_next();
+      const double xj = xs[bj * 32 + lane];
+      double c = 0.0;
+#pragma unroll
+      for (int r = 0; r < 32; ++r) {
+        c = fma(f[r], xs[bi * 32 + r], c);   // column part: sum_r F[r][lane] x_i[r]
+        f[r] *= xj;                          // row part products
+      }
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) {
+        const bool hi = (lane & o) != 0;
+#pragma unroll
+        for (int q = 0; q < o; ++q) {
+          const double keep = hi ? f[q + o] : f[q];
+          const double send = hi ? f[q] : f[q + o];
+          f[q] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
+      }
+      pw[bi * 32 + lane] += f[0];
+      if (bi != bj) pw[bj * 32 + lane] += c;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < d.ns; i += blockDim.x) {
+      double v = 0.0;
+#pragma unroll
+      for (int w = 0; w < kSymWarps; ++w) v += part[w * npad + i];
+      if (STORE_V) {
+        vbuf[voff[s] + i] = v;
+      } else {
+#pragma unroll
+        for (int k = 0; k < KR; ++k) {
+          const int r = rw[i * KR + k];
+          if (r >= 0) atomicAdd(y + r, cf[i * KR + k] * v);
+        }
+      }
+    }
+    __syncthreads();   // part (and, without the in-loop gather, xs) is rewritten by the next subdomain
+    have_xs = pre;
+    xsel ^= 1;
+  }
+  // Deterministic coarse gather (fused_dp_t's last-arriver pattern), once per
+  // CTA instead of once per subdomain: the fence + atomic round trips of the
+  // arrival count sat on warp 0's critical path in every subdomain (2.6 us
+  // each at C4).  All t_s of this CTA were stored before the barriers above;
+  // one thread per (subdomain, primal DOF) counts the arrival, and the last
+  // owner to arrive sums the owners' entries in the fixed order.
+  if (STORE_V && dps && cgp && !(flags & 4)) {
+    const CoarseGather cg = *cgp;
+    const int nmine = sfirst < s1 ? (s1 - sfirst + G - 1) / G : 0;
+    for (int q = threadIdx.x; q < nmine * 8; q += blockDim.x) {
+      const DpSub p = dps[sfirst + (q >> 3) * G];
+      const int c = q & 7;
+      if (c < p.nc) {
+        const int gid = cg.cmap[p.cmap_off + c];
+        const int k0 = cg.optr[gid], k1 = cg.optr[gid + 1];
+        __threadfence();
+        if (atomicAdd(cg.cnt + gid, 1u) + 1u == (unsigned)(k1 - k0)) {
+          __threadfence();
+          double g = 0.0;
+          for (int k = k0; k < k1; ++k) g += __ldcg(tbuf + cg.oidx[k]);
+          cg.g[gid] = g;
+          cg.cnt[gid] = 0u;
+        }
+      }
+    }
+  }
+}
+
 // pack the lower block-triangle of a row-major symmetric ns x ld matrix
 // Explicit symmetric local operators (F_s, S~_s; row-major ns x ld per slot):
 // the upper triangle is replaced by the lower one.  The elimination computes

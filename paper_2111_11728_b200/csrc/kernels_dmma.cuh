@@ -46,6 +46,25 @@ __global__ void __launch_bounds__(256) k_peak_dmma(double* out, int iters) {
   for (int i = 0; i < 16; ++i) s += acc[i];
   if (s == 12345.678) out[0] = s;
 }
+// Read-only HBM ceiling (fetigpu_hbm_read_peak): every thread keeps U 16-byte
+// streaming loads in flight over a buffer much larger than L2.  The F-apply
+// only reads its operator, and a read-only stream runs faster than the
+// read + write copy MEASURED_PEAKS.json times (no bus turnarounds).
+template <int U>
+__global__ void __launch_bounds__(256) k_peak_read(const double2* __restrict__ p, size_t n, double* out) {
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double acc = 0.0;
+  for (; i + (U - 1) * stride < n; i += U * stride) {
+    double2 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = __ldcs(p + i + u * stride);
+#pragma unroll
+    for (int u = 0; u < U; ++u) acc += v[u].x + v[u].y;
+  }
+  if (acc == 1.2345e-300) out[0] = acc;   // never true on a zeroed buffer: keeps the loads alive
+}
+
 __global__ void __launch_bounds__(256) k_peak_dfma(double* out, int iters) {
   double acc[8];
 #pragma unroll

@@ -78,7 +78,7 @@ EXPORTED = ["fetigpu_set_device", "fetigpu_create", "fetigpu_build", "fetigpu_de
             "fetigpu_local_operator", "fetigpu_device_alloc", "fetigpu_device_free",
             "fetigpu_host_alloc", "fetigpu_host_free", "fetigpu_memcpy", "fetigpu_fill_random",
             "fetigpu_synchronize", "fetigpu_time_apply", "fetigpu_apply_F_block_device",
-            "fetigpu_time_apply_block", "fetigpu_fp64_peak", "fetigpu_selftest_dmma",
+            "fetigpu_time_apply_block", "fetigpu_fp64_peak", "fetigpu_hbm_read_peak", "fetigpu_selftest_dmma",
             "fetigpu_pivoted_cholesky", "fetigpu_pivoted_compress", "fetigpu_time_ops",
             "fetigpu_device_memory", "fetigpu_set_rrs_store", "fetigpu_dla_gemm", "fetigpu_dla_tri_inv",
             "fetigpu_dla_time_gemm", "fetigpu_apply_F_zblock", "fetigpu_set_check", "fetigpu_check_result",
@@ -117,7 +117,8 @@ class FgStats(C.Structure):
                [(k, C.c_double) for k in ("op_bytes", "op_flops_per_col", "main_kernel_bytes",
                                           "build_ms", "nd_ms", "slot_ms", "coarse_ms",
                                           "device_bytes")] + \
-               [("host_pipeline", C.c_int), ("solve_loop", C.c_int), ("stream_bytes", C.c_double)]
+               [("host_pipeline", C.c_int), ("solve_loop", C.c_int), ("stream_bytes", C.c_double),
+                ("apply_kernel", C.c_int), ("apply_ring", C.c_int)]
 
 
 def lib():
@@ -153,6 +154,13 @@ def fp64_peak():
     a, b = C.c_double(), C.c_double()
     check(lib().fetigpu_fp64_peak(C.byref(a), C.byref(b)))
     return a.value, b.value
+
+
+def hbm_read_peak(nbytes: int = 2 << 30, reps: int = 10) -> float:
+    """Read-only HBM stream bandwidth (GB/s) measured on the current device."""
+    g = C.c_double()
+    check(lib().fetigpu_hbm_read_peak(C.c_size_t(nbytes), reps, C.byref(g)))
+    return g.value
 
 
 def device_memory(system=None) -> dict:

@@ -294,6 +294,53 @@ def test_symmetric_packed_apply(name, oracle_mod, monkeypatch):
     gs.close()
 
 
+SYM_TMA_CASES = dict(CASES)
+SYM_TMA_CASES.update({
+    # many small subdomains: one or three tiles each, so the ring runs several
+    # subdomains ahead of the CTA's consumer warps
+    "C4_tiny": lambda: pb.config4(sx=24, sy=20, n=2),
+    "C1_tiny": lambda: pb.config1(sx=20, sy=16, n=3),
+    # more subdomains than the persistent grid holds (2 CTAs per SM): every
+    # CTA walks several subdomains
+    "C4_many": lambda: pb.config4(sx=28, sy=24, n=6),
+})
+
+
+@pytest.mark.parametrize("ring", [None, "2", "1"])
+@pytest.mark.parametrize("name", ["C1", "C2s", "C3tf_s", "C3dp_s", "C5s", "C4s", "C4_tiny", "C1_tiny", "C4_many"])
+def test_symmetric_packed_tma_bitwise(name, ring, monkeypatch):
+    """k_sym_gemv_tma (operator tiles moved by cp.async.bulk into per-warp
+    mbarrier rings, persistent grid, prefetch across subdomain boundaries)
+    against the LDG kernel it replaces: F, the preconditioner and the
+    host-buffer apply must be bit-identical -- with two CTAs per SM and one
+    slot per warp (default), and with one CTA per SM and two or one slots."""
+    from paper_2111_11728_b200 import engine
+    prob = SYM_TMA_CASES[name]()
+    monkeypatch.setenv("FETIGPU_FORCE_SYM", "1")
+    if ring:
+        monkeypatch.setenv("FETIGPU_SYM_CTAS", "1")
+        monkeypatch.setenv("FETIGPU_SYM_RING", ring)
+    gt = engine.FetiSystem(prob)
+    monkeypatch.setenv("FETIGPU_SYM_TMA", "0")
+    gl = engine.FetiSystem(prob)
+    for k in ("FETIGPU_FORCE_SYM", "FETIGPU_SYM_TMA", "FETIGPU_SYM_CTAS", "FETIGPU_SYM_RING"):
+        monkeypatch.delenv(k, raising=False)
+    assert gt.stats()["main_kernel_bytes"] > 0
+    X = np.random.default_rng(33).standard_normal((gt.m, 3))
+    for c in range(3):
+        yt, yl = gt.apply_F(X[:, c]), gl.apply_F(X[:, c])
+        assert np.array_equal(yt, yl), f"{name} F col {c}"
+        assert np.array_equal(gt.apply_precond(X[:, c]), gl.apply_precond(X[:, c])), f"{name} M col {c}"
+    assert np.array_equal(gt.apply_F(X), gl.apply_F(X))
+    for _ in range(3):
+        assert np.array_equal(gt.apply_F(X[:, 0]), gl.apply_F(X[:, 0]))
+    lt, tt = gt.solve(tol=1e-6, max_it=300, directions=0)
+    ll, tl = gl.solve(tol=1e-6, max_it=300, directions=0)
+    assert tt["iterations"] == tl["iterations"] and np.array_equal(lt, ll)
+    gt.close()
+    gl.close()
+
+
 @pytest.mark.parametrize("name", ["C1", "C2s", "C3tf_s", "C3dp_s", "C5s", "C4s"])
 def test_recovered_interface_jump(name, oracle_mod):
     """after convergence at eps 1e-8 the recovered

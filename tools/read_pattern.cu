@@ -1,0 +1,145 @@
+// Which ADDRESS PATTERN of a read-only 2.2 GB stream reaches the HBM ceiling?
+// K4 (k_sym_gemv_tma) has 296 CTAs each streaming its own contiguous 1.07 MB
+// operator (136 tiles of 8 KB, warp w takes tiles w, w+8, ...), and stays at
+// 6.4 TB/s although tools/read_peak.cu reaches 7.1-7.3 TB/s with all CTAs
+// marching through memory together.  Per-warp private slot + mbarrier, one
+// cp.async.bulk of CH bytes per request, as in the kernel.
+//   pattern 0: marching   chunk = (i * G + cta) * 8 + warp
+//   pattern 1: region per CTA (REG chunks of CH bytes), warp w takes chunks w, w+8, ... of its region
+//   pattern 2: region per CTA, warp w takes a contiguous eighth of the region
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o read_pattern read_pattern.cu
+#include <cstdio>
+#include <cstdlib>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("%s: %s\n", #x, cudaGetErrorString(e)); exit(1); } } while (0)
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, int c) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(c));
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t ph) {
+  asm volatile(
+      "{\n.reg .pred p;\nW_%=: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@p bra D_%=;\nbra W_%=;\nD_%=:\n}\n" ::"r"(
+          smem_u32(b)),
+      "r"(ph)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(b))
+               : "memory");
+}
+
+// work: extra dependent FP64 work per chunk (emulates the tile arithmetic's latency chain)
+template <int CH, int R>
+__global__ void __launch_bounds__(256, 2) k_pat(const double* __restrict__ p, size_t nchunks, int pattern, int reg,
+                                                int work, double* out) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* ring = reinterpret_cast<double*>(smem) + (size_t)warp * R * (CH / 8);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)8 * R * CH) + warp * R;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < 8 * R; ++s) mbar_init(reinterpret_cast<uint64_t*>(smem + (size_t)8 * R * CH) + s, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const size_t G = gridDim.x, cta = blockIdx.x;
+  // the warp's n-th chunk -> global chunk index (or >= nchunks when exhausted)
+  auto chunk_of = [&](size_t n) -> size_t {
+    if (pattern == 0) return (n * G + cta) * 8 + warp;
+    const size_t per = (size_t)reg / 8;             // chunks per warp per region
+    const size_t r = n / per, k = n % per;          // region number of this CTA, chunk within
+    const size_t base = (r * G + cta) * (size_t)reg;
+    return pattern == 1 ? base + k * 8 + warp : base + (size_t)warp * per + k;
+  };
+  size_t nreq = 0, ncons = 0;
+  auto request = [&]() {
+    const size_t c = chunk_of(nreq);
+    if (c < nchunks) {
+      if (lane == 0) bulk_g2s(ring + (nreq % R) * (CH / 8), p + c * (CH / 8), CH, full + nreq % R);
+      ++nreq;
+    }
+  };
+  for (int i = 0; i < R; ++i) request();
+  double acc = 0.0;
+  while (ncons < nreq) {
+    const int slot = (int)(ncons % R);
+    mbar_wait(full + slot, (uint32_t)(ncons / R) & 1u);
+    const double* T = ring + (size_t)slot * (CH / 8);
+    constexpr int NR = CH / 256;
+    double f[NR];
+#pragma unroll
+    for (int r = 0; r < NR; ++r) f[r] = T[r * 32 + lane];
+    ++ncons;
+    __syncwarp();
+    if (lane == 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    request();
+    double c = 0.0;
+#pragma unroll
+    for (int r = 0; r < NR; ++r) c = fma(f[r], 1.0000001, c);
+    for (int w = 0; w < work; ++w) c = fma(c, 1.0000001, 1e-9);
+    acc += c;
+  }
+  if (acc == 1.2345e-300) out[0] = acc;
+}
+
+template <class F>
+static double time_gbs(F launch, size_t bytes, int reps) {
+  cudaEvent_t a, b;
+  CK(cudaEventCreate(&a));
+  CK(cudaEventCreate(&b));
+  for (int i = 0; i < 3; ++i) launch();
+  CK(cudaDeviceSynchronize());
+  CK(cudaEventRecord(a));
+  for (int i = 0; i < reps; ++i) launch();
+  CK(cudaEventRecord(b));
+  CK(cudaEventSynchronize(b));
+  CK(cudaGetLastError());
+  float ms;
+  CK(cudaEventElapsedTime(&ms, a, b));
+  return bytes * (double)reps / (ms * 1e-3) / 1e9;
+}
+
+int main() {
+  const size_t bytes = 2190999552ull;
+  double *p, *out;
+  const size_t alloc = 2190999552ull;
+  CK(cudaMalloc(&p, alloc));
+  CK(cudaMalloc(&out, 64));
+  CK(cudaMemset(p, 0, alloc));
+  cudaDeviceProp pr;
+  CK(cudaGetDeviceProperties(&pr, 0));
+  const int sm = pr.multiProcessorCount, G = 2 * sm;
+  printf("device %s, %d SMs, grid %d, buffer %.3f GB (used %.3f)\n", pr.name, sm, G, alloc / 1e9, bytes / 1e9);
+  auto run = [&](auto chc, auto rc, int pattern, int reg_bytes, int work) {
+    constexpr int CH = decltype(chc)::value, R = decltype(rc)::value;
+    const size_t sh = (size_t)8 * R * CH + 128;
+    CK(cudaFuncSetAttribute(k_pat<CH, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
+    const int reg = reg_bytes / CH;
+    // whole regions only, so every pattern reads the same byte count
+    const size_t nreg = bytes / reg_bytes / G * G;
+    const size_t nch = nreg * reg;
+    const double g = time_gbs([&] { k_pat<CH, R><<<G, 256, sh>>>(p, nch, pattern, reg, work, out); },
+                              nch * (size_t)CH, 20);
+    printf("CH=%5d R=%d pattern=%d region=%7d B work=%4d : %.0f GB/s\n", CH, R, pattern, reg_bytes, work, g);
+  };
+  using std::integral_constant;
+  const int REG = 136 * 8192;   // one C4 subdomain's packed operator
+  for (int work : {0, 400}) {
+    run(integral_constant<int, 8192>{}, integral_constant<int, 1>{}, 0, REG, work);
+    run(integral_constant<int, 8192>{}, integral_constant<int, 1>{}, 1, REG, work);
+    run(integral_constant<int, 8192>{}, integral_constant<int, 1>{}, 2, REG, work);
+    run(integral_constant<int, 8192>{}, integral_constant<int, 1>{}, 1, 32 * 8192, work);
+    run(integral_constant<int, 8192>{}, integral_constant<int, 1>{}, 1, 64 * 8192, work);
+    run(integral_constant<int, 8192>{}, integral_constant<int, 1>{}, 1, 8 * 8192, work);
+    run(integral_constant<int, 4096>{}, integral_constant<int, 2>{}, 1, REG, work);
+    run(integral_constant<int, 4096>{}, integral_constant<int, 3>{}, 1, REG, work);
+    run(integral_constant<int, 2048>{}, integral_constant<int, 4>{}, 1, REG, work);
+    run(integral_constant<int, 2048>{}, integral_constant<int, 6>{}, 1, REG, work);
+  }
+  return 0;
+}
