@@ -225,6 +225,8 @@ void Ctx::launch_sym(cudaStream_t q, const SymArgs& a) {
   double* tbuf = a.store_v ? d_tbuf.p : nullptr;
   const int ny = a.zero_y ? su.m : 0, nsub = a.zero_y ? su.Ns : 1;
   const CoarseGather* cgp = a.coarse_gather && su.Nc ? d_cgather.p : nullptr;
+  const int* wflag = a.wait_x ? d_xflag.p : nullptr;
+  const int* wneed = a.wait_x ? d_subneed.p : nullptr;
   auto go = [&](auto ktma, auto kldg) {
     if (sym_tma) {
       const int ring = a.pc ? pc_sym_ring : sym_ring, npad = a.pc ? pc_sym_npad : sym_npad;
@@ -232,10 +234,10 @@ void Ctx::launch_sym(cudaStream_t q, const SymArgs& a) {
       const int grid = a.per_cta ? a.n : std::min(a.n, sym_grid);
       if (a.pdl)
         launch_pdl(ktma, grid, 256, smem, q, subs, tiles, rows, coefs, a.x, a.y, vbuf, voff, dps, abc, tbuf, a.s0,
-                   a.s0 + a.n, a.zero_y, ny, nsub, cgp, ring, npad, sym_flags);
+                   a.s0 + a.n, a.zero_y, ny, nsub, cgp, ring, npad, sym_flags, wflag, wneed);
       else
         ktma<<<grid, 256, smem, q>>>(subs, tiles, rows, coefs, a.x, a.y, vbuf, voff, dps, abc, tbuf, a.s0,
-                                     a.s0 + a.n, a.zero_y, ny, nsub, cgp, ring, npad, sym_flags);
+                                     a.s0 + a.n, a.zero_y, ny, nsub, cgp, ring, npad, sym_flags, wflag, wneed);
     } else {
       const int smem = a.pc ? pc_sym_smem : sym_smem;
       if (a.pdl)
@@ -326,6 +328,23 @@ void Ctx::setup_pipe() {
       CK(cudaEventCreateWithFlags(&pipe_done[c], cudaEventDisableTiming));
     }
     CK(cudaEventCreateWithFlags(&pipe_start, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&pipe_cp_done, cudaEventDisableTiming));
+  }
+  // flag value after chunk c has landed: c + 1
+  {
+    std::vector<int> need(su.Ns);
+    for (int s = 0; s < su.Ns; ++s) {
+      int c = 0;
+      while (c < kPipe - 1 && pipe_need[c] <= sub_maxrow[s]) ++c;
+      need[s] = c + 1;
+    }
+    d_subneed.upload(need, st);
+    d_xflag.alloc(1);
+    d_xflag.zero(st);
+    if (!h_flagvals) {
+      CK(cudaMallocHost(&h_flagvals, kPipe * sizeof(int)));
+      for (int c = 0; c < kPipe; ++c) h_flagvals[c] = c + 1;
+    }
   }
   pipe_ready = true;
 }
@@ -338,6 +357,33 @@ void Ctx::apply_F_host(const double* xh, double* yh) {
   if (!pipe_ready) {
     CK(cudaMemcpyAsync(x, xh, (size_t)m * 8, cudaMemcpyHostToDevice, st));
     apply_F(x, y, 1, m, m);
+  } else if (sym_tma && pipe_flagged()) {
+    // ONE persistent phase-1 kernel, launched before x has arrived: it
+    // requests its first operator tiles at once, and every subdomain's gather
+    // waits until the copy stream has flagged the row prefix it needs
+    CK(cudaMemsetAsync(d_xflag.p, 0, 4, st));
+    CK(cudaEventRecord(pipe_start, st));  // after everything already queued on st
+    CK(cudaStreamWaitEvent(pipe_cp, pipe_start, 0));
+    int done = 0;
+    for (int c = 0; c < kPipe; ++c) {
+      const int need = c == kPipe - 1 ? m : pipe_need[c];
+      if (need > done) {
+        CK(cudaMemcpyAsync(x + done, xh + done, (size_t)(need - done) * 8, cudaMemcpyHostToDevice, pipe_cp));
+        done = need;
+      }
+      // the flag is stored by the copy engine: a memset kernel could not be scheduled beside the
+      // persistent kernel (it holds every SM's registers) and the two would wait on each other
+      CK(cudaMemcpyAsync(d_xflag.p, h_flagvals + c, 4, cudaMemcpyHostToDevice, pipe_cp));
+    }
+    CK(cudaEventRecord(pipe_cp_done, pipe_cp));
+    SymArgs sa;
+    sa.store_v = true; sa.x = x; sa.n = su.Ns; sa.zero_y = y; sa.coarse_gather = true; sa.wait_x = true;
+    launch_sym(st, sa);
+    LAUNCH_CHECK();
+    CK(cudaStreamWaitEvent(st, pipe_cp_done, 0));
+    coarse_solve_packed(true);
+    launch_phase2_csym(y);
+    LAUNCH_CHECK();
   } else {
     CK(cudaEventRecord(pipe_start, st));  // after everything already queued on st
     CK(cudaStreamWaitEvent(pipe_cp, pipe_start, 0));

@@ -396,7 +396,8 @@ __global__ void __launch_bounds__(256, 2) k_sym_gemv_tma(
     const double* __restrict__ coefs, const double* __restrict__ x, double* __restrict__ y,
     double* __restrict__ vbuf, const int* __restrict__ voff, const DpSub* __restrict__ dps,
     const double* __restrict__ abc, double* __restrict__ tbuf, int s0, int s1, double* __restrict__ zero_y, int ny,
-    int nsub, const CoarseGather* cgp, int R, int npad_max, int flags) {
+    int nsub, const CoarseGather* cgp, int R, int npad_max, int flags, const int* wait_flag = nullptr,
+    const int* __restrict__ sub_need = nullptr) {
   extern __shared__ __align__(128) unsigned char smraw[];
   const size_t ring_bytes = (size_t)R * kSymWarps * kSymTileBytes;
   uint64_t* full = reinterpret_cast<uint64_t*>(smraw + ring_bytes);     // 8 R barriers
@@ -408,6 +409,17 @@ __global__ void __launch_bounds__(256, 2) k_sym_gemv_tma(
   uint64_t* wfull = full + warp * R;
   uint64_t pol;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  // Host-buffer apply (fetigpu_apply_F on host pointers): x arrives by row
+  // prefix chunks on a copy stream while this kernel already runs; after each
+  // chunk the stream stores a larger value in *wait_flag, and subdomain s may
+  // gather once the flag has reached sub_need[s].  x is then read through L2
+  // (a line cached in L1 before its chunk landed would be stale).
+  auto flag_now = [&]() {
+    int v;
+    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(wait_flag) : "memory");
+    return v;
+  };
+  auto ldx = [&](int r) { return wait_flag ? __ldcg(x + r) : x[r]; };
   // this warp's request cursor: tile ct of subdomain cs (cnt tiles at ctoff)
   int cs = sfirst, ct = warp, cnt = 0, nreq = 0;
   long long ctoff = 0;
@@ -460,13 +472,22 @@ __global__ void __launch_bounds__(256, 2) k_sym_gemv_tma(
     const int* rw = rows + d.map_off;
     const double* cf = coefs + d.map_off;
     if (!have_xs) {
+      if (wait_flag) {
+        const int need = sub_need[s];
+        // (bounded: the chunks are queued on the copy stream before this kernel is launched and arrive
+        // within ~0.1 ms; a wait of seconds means a broken stream order -- trap rather than hang the device)
+        for (long long spin = 0; flag_now() < need; ++spin) {
+          __nanosleep(200);
+          if (spin > 20000000) __trap();
+        }
+      }
       for (int j = threadIdx.x; j < npad; j += blockDim.x) {
         double acc = 0.0;
         if (j < d.ns) {
 #pragma unroll
           for (int k = 0; k < KR; ++k) {
             const int r = rw[j * KR + k];
-            if (r >= 0) acc += cf[j * KR + k] * x[r];
+            if (r >= 0) acc += cf[j * KR + k] * ldx(r);
           }
         }
         xs[j] = acc;
@@ -481,6 +502,9 @@ __global__ void __launch_bounds__(256, 2) k_sym_gemv_tma(
       dn = subs[sn];
       nchain = (dn.nb * 32 + 255) / 256;
       pre = KR == 1 && (flags & 1) && (d.nb * (d.nb + 1) / 2) / kSymWarps >= 3 * nchain;
+      // (per thread: a thread that finds the next subdomain's rows not landed yet gathers ITS entries
+      // j = tid, tid + 256, ... in the prologue instead -- the same entries its chains would cover)
+      if (pre && wait_flag) pre = flag_now() >= sub_need[sn];
       if (STORE_V && dps && (flags & 2) && threadIdx.x == 0) {
         const DpSub pn = dps[sn];
         prefetch_l2_bulk(abc + pn.abc_off, (size_t)dn.ns * pn.nc * 8);
@@ -506,7 +530,7 @@ __global__ void __launch_bounds__(256, 2) k_sym_gemv_tma(
             pc = cfn[j];
           }
         } else if (stage == 1) {
-          px = pr >= 0 ? x[pr] : 0.0;
+          px = pr >= 0 ? ldx(pr) : 0.0;
         } else if (j < dn.nb * 32) {
           double acc = 0.0;
           if (pr >= 0) acc += pc * px;

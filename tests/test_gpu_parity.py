@@ -562,6 +562,15 @@ def test_host_pipelined_apply(oracle_mod, monkeypatch):
     assert np.array_equal(y_host, y_dev)
     for _ in range(3):                                     # repeated, back to back
         assert np.array_equal(g.apply_F(x), y_host)
+    # FETIGPU_PIPE_FLAG=1: ONE persistent phase-1 kernel gated on the landed row
+    # prefix of lambda instead of a kernel per chunk and stream
+    monkeypatch.setenv("FETIGPU_PIPE_FLAG", "1")
+    for _ in range(2):
+        assert np.array_equal(g.apply_F(x), y_host)
+    monkeypatch.delenv("FETIGPU_PIPE_FLAG")
+    x2 = np.random.default_rng(6).standard_normal(m)
+    y2 = g.apply_F(x2)
+    assert np.array_equal(g.apply_F(x), y_host) and np.array_equal(g.apply_F(x2), y2)
     o = oracle_mod.Oracle(prob)
     assert rel(y_host, o.apply_F(x)) <= 1e-8
     g.close()
