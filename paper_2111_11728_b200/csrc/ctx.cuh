@@ -71,8 +71,9 @@ struct Ctx {
   bool sym_tma = false;
   int sym_ring = 0, sym_npad = 0, pc_sym_ring = 0, pc_sym_npad = 0, sym_grid = 0;
   // 1: next x_s gathered inside the tile loop, 2: next A'' prefetched into L2 (measured slower),
-  // 4: coarse arrival count per subdomain instead of once per CTA (FETIGPU_SYM_FLAGS)
-  int sym_flags = 1;
+  // 4: coarse arrival count per subdomain instead of once per CTA, 8: A'' streamed through the rings
+  // (coarse pre-pass after the tile loop; t_s summed in another order than fused_dp_t) (FETIGPU_SYM_FLAGS)
+  int sym_flags = 9;
   size_t sym_tma_bytes = 0, pc_sym_tma_bytes = 0;
   std::vector<std::vector<double>> slot_sign;
   DBuf<int> d_oprows, d_slot_of, d_fac_ne, d_top_pos, d_top_off;

@@ -377,6 +377,24 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
       "l"(src), "r"(bytes), "r"(smem_addr32(bar)), "l"(pol)
       : "memory");
 }
+// the same without a cache hint (data that should stay in L2: A'' is read again by phase 2)
+__device__ __forceinline__ void tma_load_1d_plain(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr32(bar)), "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_addr32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_addr32(bar))
+               : "memory");
+}
+// FETI-DP coarse pre-pass streamed through the rings (flag 8): A''_s (n_s x n_c
+// row-major, n_c in {2, 4, 8}) is cut into 8 KB chunks, chunk w appended to
+// warp w's tile stream of the subdomain; lane l of the warp sums column
+// l % n_c over the chunk's rows l / n_c, + 32 / n_c, ...  Chunks of A''_s:
+__device__ __forceinline__ int dp_chunks(const DpSub& p, int ns) {
+  const bool ok = (p.nc == 2 || p.nc == 4 || p.nc == 8) && (p.abc_off & 1) == 0;
+  const int n = (ns * p.nc + 1023) >> 10;
+  return ok && n <= kSymWarps ? n : 0;
+}
 constexpr int kSymRingMax = 2;                        // slots per warp (the 8 x 2 barriers share one 128-byte line)
 constexpr int kSymTileBytes = 32 * 32 * 8;
 __host__ __device__ constexpr size_t sym_tma_smem(int R, int npad) {
@@ -422,27 +440,45 @@ __global__ void __launch_bounds__(256, 2) k_sym_gemv_tma(
   auto ldx = [&](int r) { return wait_flag ? __ldcg(x + r) : x[r]; };
   // this warp's request cursor: tile ct of subdomain cs (cnt tiles at ctoff)
   int cs = sfirst, ct = warp, cnt = 0, nreq = 0;
-  long long ctoff = 0;
+  long long ctoff = 0, caoff = 0;
+  int cabytes = 0;   // > 0: this warp's A'' chunk of subdomain cs is still to be requested (after its tiles)
+  const bool stream_a = STORE_V && dps && (flags & 8);
   auto cursor_load = [&]() {
     if (cs < s1) {
       const SymSub q = subs[cs];
       cnt = q.nb * (q.nb + 1) / 2;
       ctoff = q.toff;
+      cabytes = 0;
+      if (stream_a) {
+        const DpSub pq = dps[cs];
+        if (warp < dp_chunks(pq, q.ns)) {
+          caoff = pq.abc_off + (long long)warp * 1024;
+          cabytes = min(1024, q.ns * pq.nc - warp * 1024) * 8;
+        }
+      }
     }
   };
   auto request_next = [&]() {   // warp-uniform; lane 0 issues
-    while (cs < s1 && ct >= cnt) {
+    for (;;) {
+      if (cs >= s1) return;
+      const int slot = nreq % R;
+      if (ct < cnt) {
+        if (lane == 0)
+          tma_load_1d(wring + (size_t)slot * 1024, tiles + ctoff + (size_t)ct * 1024, kSymTileBytes,
+                      wfull + slot, pol);
+        ++nreq;
+        ct += kSymWarps;
+        return;
+      }
+      if (cabytes > 0) {
+        if (lane == 0) tma_load_1d_plain(wring + (size_t)slot * 1024, abc + caoff, (uint32_t)cabytes, wfull + slot);
+        ++nreq;
+        cabytes = 0;
+        return;
+      }
       cs += G;
       ct = warp;
       cursor_load();
-    }
-    if (cs < s1) {
-      const int slot = nreq % R;
-      if (lane == 0)
-        tma_load_1d(wring + (size_t)slot * 1024, tiles + ctoff + (size_t)ct * 1024, kSymTileBytes, wfull + slot,
-                    pol);
-      ++nreq;
-      ct += kSymWarps;
     }
   };
   if (threadIdx.x == 0) {
@@ -453,12 +489,16 @@ __global__ void __launch_bounds__(256, 2) k_sym_gemv_tma(
   cursor_load();
   for (int i = 0; i < R; ++i) request_next();
   pdl_wait();
-  int ncons = 0;   // tiles this warp has drained
+  __shared__ double tpart[kSymWarps][8];   // per-chunk partials of t_s = A''^T x_s
+  int ncons = 0;   // tiles (and A'' chunks) this warp has drained
   // x_s of the CTA's NEXT subdomain is gathered inside the tile loop (KR = 1):
   // chain c covers local DOFs j = 256 c + 32 warp + lane in three of the
   // warp's iterations -- map entry, then x[row], then the store -- each load
   // consumed one tile later, so its latency hides behind the tile arithmetic
   bool have_xs = false;   // the current subdomain's x_s is already in its buffer
+  // the warp partials are zero between subdomains: zeroed once here, and every entry again by the thread
+  // that reads it in the final reduction (no zeroing pass and one barrier less per subdomain)
+  for (int j = threadIdx.x; j < kSymWarps * npad_max; j += blockDim.x) part[j] = 0.0;
   int xsel = 0;
   for (int s = sfirst; s < s1; s += G) {
     const SymSub d = subs[s];
@@ -514,9 +554,14 @@ __global__ void __launch_bounds__(256, 2) k_sym_gemv_tma(
     const double* cfn = coefs + dn.map_off;
     int pr = -1;
     double pc = 0.0, px = 0.0;
-    for (int j = threadIdx.x; j < kSymWarps * npad; j += blockDim.x) part[j] = 0.0;
-    __syncthreads();
-    if (STORE_V && dps) fused_dp_t(dps[s], abc, xs, d.ns, tbuf, (flags & 4) ? cgp : nullptr);
+    // x_s complete: a subdomain gathered inside the previous tile loop is covered by that loop's
+    // barriers (have_xs is CTA-uniform unless the gather is flag-gated per thread)
+    if (!have_xs || wait_flag) __syncthreads();
+    int na = 0;   // A'' chunks streamed through the rings for this subdomain (0: pre-pass here)
+    if (STORE_V && dps) {
+      if (stream_a) na = dp_chunks(dps[s], d.ns);
+      if (na == 0) fused_dp_t(dps[s], abc, xs, d.ns, tbuf, (flags & 4) && !stream_a ? cgp : nullptr);
+    }
     double* pw = part + warp * npad;
     const int ntiles = d.nb * (d.nb + 1) / 2;
     int it = 0;
@@ -574,11 +619,40 @@ __global__ void __launch_bounds__(256, 2) k_sym_gemv_tma(
       pw[bi * 32 + lane] += f[0];
       if (bi != bj) pw[bj * 32 + lane] += c;
     }
+    if (STORE_V && warp < na) {   // this warp's A'' chunk: the next item of its stream after its tiles
+      const DpSub p = dps[s];
+      const int slot = ncons % R;
+      mbar_wait_parity(wfull + slot, (uint32_t)(ncons / R) & 1u);
+      ++ncons;
+      const double* T = wring + (size_t)slot * 1024;
+      const int sh = p.nc == 8 ? 3 : p.nc == 4 ? 2 : 1;
+      const int e0 = warp * 1024 + lane, tot = d.ns * p.nc;
+      double acc = 0.0;
+#pragma unroll 8
+      for (int k = 0; k < 32; ++k) {
+        const int e = e0 + 32 * k;
+        if (e < tot) acc = fma(T[lane + 32 * k], xs[e >> sh], acc);
+      }
+      __syncwarp();
+      if (lane == 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      request_next();
+      for (int o = 16; o >= p.nc; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (lane < p.nc) tpart[warp][lane] = acc;
+    }
     __syncthreads();
-    for (int i = threadIdx.x; i < d.ns; i += blockDim.x) {
+    if (STORE_V && na > 0 && (int)threadIdx.x < dps[s].nc) {   // t_s: chunk partials in chunk order
+      double t = 0.0;
+      for (int w = 0; w < na; ++w) t += tpart[w][threadIdx.x];
+      tbuf[dps[s].t_off + threadIdx.x] = t;
+    }
+    for (int i = threadIdx.x; i < npad; i += blockDim.x) {
       double v = 0.0;
 #pragma unroll
-      for (int w = 0; w < kSymWarps; ++w) v += part[w * npad + i];
+      for (int w = 0; w < kSymWarps; ++w) {
+        v += part[w * npad + i];
+        part[w * npad + i] = 0.0;
+      }
+      if (i >= d.ns) continue;
       if (STORE_V) {
         vbuf[voff[s] + i] = v;
       } else {
@@ -589,7 +663,7 @@ __global__ void __launch_bounds__(256, 2) k_sym_gemv_tma(
         }
       }
     }
-    __syncthreads();   // part (and, without the in-loop gather, xs) is rewritten by the next subdomain
+    __syncthreads();   // part is zero again; without the in-loop gather xs is rewritten by the next subdomain
     have_xs = pre;
     xsel ^= 1;
   }
@@ -599,7 +673,7 @@ __global__ void __launch_bounds__(256, 2) k_sym_gemv_tma(
   // each at C4).  All t_s of this CTA were stored before the barriers above;
   // one thread per (subdomain, primal DOF) counts the arrival, and the last
   // owner to arrive sums the owners' entries in the fixed order.
-  if (STORE_V && dps && cgp && !(flags & 4)) {
+  if (STORE_V && dps && cgp && (!(flags & 4) || stream_a)) {
     const CoarseGather cg = *cgp;
     const int nmine = sfirst < s1 ? (s1 - sfirst + G - 1) / G : 0;
     for (int q = threadIdx.x; q < nmine * 8; q += blockDim.x) {

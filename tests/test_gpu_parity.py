@@ -306,37 +306,55 @@ SYM_TMA_CASES.update({
 })
 
 
+@pytest.mark.parametrize("flags", [None, "1"])
 @pytest.mark.parametrize("ring", [None, "2", "1"])
 @pytest.mark.parametrize("name", ["C1", "C2s", "C3tf_s", "C3dp_s", "C5s", "C4s", "C4_tiny", "C1_tiny", "C4_many"])
-def test_symmetric_packed_tma_bitwise(name, ring, monkeypatch):
+def test_symmetric_packed_tma_vs_ldg(name, ring, flags, monkeypatch):
     """k_sym_gemv_tma (operator tiles moved by cp.async.bulk into per-warp
-    mbarrier rings, persistent grid, prefetch across subdomain boundaries)
-    against the LDG kernel it replaces: F, the preconditioner and the
-    host-buffer apply must be bit-identical -- with two CTAs per SM and one
-    slot per warp (default), and with one CTA per SM and two or one slots."""
+    mbarrier rings, persistent grid, prefetch across subdomain boundaries,
+    next x_s gathered inside the tile loop) against the LDG kernel it
+    replaces -- with two CTAs per SM and one slot per warp (default), and with
+    one CTA per SM and two or one slots.  FETIGPU_SYM_FLAGS=1: the same
+    arithmetic everywhere, so F, the preconditioner and the host-buffer apply
+    must be bit-identical.  Default: FETI-DP's coarse pre-pass t_s = A''^T x_s
+    is streamed through the rings too and summed chunk-wise, so F agrees to
+    rounding (1e-13 of |y|); the preconditioner and T-FETI stay bit-identical."""
     from paper_2111_11728_b200 import engine
     prob = SYM_TMA_CASES[name]()
     monkeypatch.setenv("FETIGPU_FORCE_SYM", "1")
     if ring:
         monkeypatch.setenv("FETIGPU_SYM_CTAS", "1")
         monkeypatch.setenv("FETIGPU_SYM_RING", ring)
+    if flags:
+        monkeypatch.setenv("FETIGPU_SYM_FLAGS", flags)
     gt = engine.FetiSystem(prob)
     monkeypatch.setenv("FETIGPU_SYM_TMA", "0")
     gl = engine.FetiSystem(prob)
-    for k in ("FETIGPU_FORCE_SYM", "FETIGPU_SYM_TMA", "FETIGPU_SYM_CTAS", "FETIGPU_SYM_RING"):
+    for k in ("FETIGPU_FORCE_SYM", "FETIGPU_SYM_TMA", "FETIGPU_SYM_CTAS", "FETIGPU_SYM_RING", "FETIGPU_SYM_FLAGS"):
         monkeypatch.delenv(k, raising=False)
-    assert gt.stats()["main_kernel_bytes"] > 0
+    assert gt.stats()["apply_kernel"] == 2 and gl.stats()["apply_kernel"] == 1
+    exact = flags == "1" or prob.method == 0
+
+    def same(a, b, what):
+        if exact:
+            assert np.array_equal(a, b), what
+        else:
+            assert np.linalg.norm(a - b) <= 1e-13 * np.linalg.norm(b), what
+
     X = np.random.default_rng(33).standard_normal((gt.m, 3))
     for c in range(3):
-        yt, yl = gt.apply_F(X[:, c]), gl.apply_F(X[:, c])
-        assert np.array_equal(yt, yl), f"{name} F col {c}"
+        same(gt.apply_F(X[:, c]), gl.apply_F(X[:, c]), f"{name} F col {c}")
         assert np.array_equal(gt.apply_precond(X[:, c]), gl.apply_precond(X[:, c])), f"{name} M col {c}"
-    assert np.array_equal(gt.apply_F(X), gl.apply_F(X))
-    for _ in range(3):
-        assert np.array_equal(gt.apply_F(X[:, 0]), gl.apply_F(X[:, 0]))
-    lt, tt = gt.solve(tol=1e-6, max_it=300, directions=0)
-    ll, tl = gl.solve(tol=1e-6, max_it=300, directions=0)
-    assert tt["iterations"] == tl["iterations"] and np.array_equal(lt, ll)
+    same(gt.apply_F(X), gl.apply_F(X), f"{name} F block")
+    y0 = gt.apply_F(X[:, 0])
+    for _ in range(3):                       # deterministic
+        assert np.array_equal(gt.apply_F(X[:, 0]), y0)
+    lt, tt = gt.solve(tol=1e-6, max_it=300, directions=1)
+    ll, tl = gl.solve(tol=1e-6, max_it=300, directions=1)
+    if exact:
+        assert tt["iterations"] == tl["iterations"] and np.array_equal(lt, ll)
+    else:
+        assert abs(tt["iterations"] - tl["iterations"]) <= 1
     gt.close()
     gl.close()
 
