@@ -938,11 +938,51 @@ __device__ __forceinline__ void dp_phase2_cta(int s, const OpSub* __restrict__ s
   const OpSub d = subs[s];
   const DpSub p = dps[s];
   __shared__ double uc[8];
-  if (threadIdx.x < 8) uc[threadIdx.x] = threadIdx.x < p.nc ? __ldcg(u + cmap[p.cmap_off + threadIdx.x]) : 0.0;
-  __syncthreads();
   const double* Ab = abc + p.abc_off;
   const bool vec = (p.nc & 1) == 0 && (p.abc_off & 1) == 0;
-  for (int j = threadIdx.x; j < d.ns; j += blockDim.x) {
+  // Rows j = tid and tid + blockDim (all of a C4 subdomain's rows): v, the A''
+  // row, the dual row and its coefficient are requested BEFORE the barrier
+  // that publishes u_s, so their DRAM latency overlaps the cmap -> u chain
+  // instead of following it.  Same fma chain per row as the loop below.
+  const int nh = p.nc >> 1;
+  double2 a[2][4];
+  double vv[2], cc[2];
+  int rr[2];
+  const bool fastp = vec && vbuf != nullptr;
+  if (fastp) {
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int j = threadIdx.x + q * blockDim.x;
+      rr[q] = -1;
+      if (j < d.ns) {
+        vv[q] = __ldcg(vbuf + p.v_off + j);
+        const double2* A2 = reinterpret_cast<const double2*>(Ab + (size_t)j * p.nc);
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          if (c < nh) a[q][c] = __ldcs(A2 + c);
+        rr[q] = rows[d.map_off + j];
+        cc[q] = coefs[d.map_off + j];
+      }
+    }
+  }
+  if (threadIdx.x < 8) uc[threadIdx.x] = threadIdx.x < p.nc ? __ldcg(u + cmap[p.cmap_off + threadIdx.x]) : 0.0;
+  __syncthreads();
+  if (fastp) {
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      if (rr[q] >= 0) {
+        double v = vscale * vv[q];
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          if (c < nh) {
+            v = fma(a[q][c].x, uc[2 * c], v);
+            v = fma(a[q][c].y, uc[2 * c + 1], v);
+          }
+        atomicAdd(y + rr[q], cc[q] * v);
+      }
+    }
+  }
+  for (int j = threadIdx.x + (fastp ? 2 * blockDim.x : 0); j < d.ns; j += blockDim.x) {
     double v = vbuf ? vscale * __ldcg(vbuf + p.v_off + j) : 0.0;
     if (vec) {
       const double2* A2 = reinterpret_cast<const double2*>(Ab + (size_t)j * p.nc);
