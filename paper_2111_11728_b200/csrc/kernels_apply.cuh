@@ -565,6 +565,12 @@ __global__ void __launch_bounds__(256, 2) k_sym_gemv_tma(
     double* pw = part + warp * npad;
     const int ntiles = d.nb * (d.nb + 1) / 2;
     int it = 0;
+    // (bi, bj) of tile t = warp, advanced with t (tile index bi (bi + 1) / 2 + bj, bj <= bi)
+    int bi = 0, bj = warp;
+    while (bj > bi) {
+      bj -= bi + 1;
+      ++bi;
+    }
     for (int t = warp; t < ntiles; t += kSymWarps, ++it) {
       if (pre && it < 3 * nchain) {
         const int ch = it / 3, stage = it - 3 * ch, j = ch * 256 + threadIdx.x;
@@ -582,10 +588,6 @@ __global__ void __launch_bounds__(256, 2) k_sym_gemv_tma(
           xs_next[j] = acc;
         }
       }
-      int bi = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
-      while (bi * (bi + 1) / 2 > t) --bi;
-      while ((bi + 1) * (bi + 2) / 2 <= t) ++bi;
-      const int bj = t - bi * (bi + 1) / 2;
       const int slot = ncons % R;
       mbar_wait_parity(wfull + slot, (uint32_t)(ncons / R) & 1u);
       ++ncons;
@@ -618,6 +620,11 @@ __global__ void __launch_bounds__(256, 2) k_sym_gemv_tma(
       }
       pw[bi * 32 + lane] += f[0];
       if (bi != bj) pw[bj * 32 + lane] += c;
+      bj += kSymWarps;
+      while (bj > bi) {
+        bj -= bi + 1;
+        ++bi;
+      }
     }
     if (STORE_V && warp < na) {   // this warp's A'' chunk: the next item of its stream after its tiles
       const DpSub p = dps[s];
