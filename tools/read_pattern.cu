@@ -117,7 +117,7 @@ int main() {
   printf("device %s, %d SMs, grid %d, buffer %.3f GB (used %.3f)\n", pr.name, sm, G, alloc / 1e9, bytes / 1e9);
   auto run = [&](auto chc, auto rc, int pattern, int reg_bytes, int work) {
     constexpr int CH = decltype(chc)::value, R = decltype(rc)::value;
-    const size_t sh = (size_t)8 * R * CH + 128;
+    const size_t sh = (size_t)8 * R * CH + 8 * R * 8;   // rings + one mbarrier per slot
     CK(cudaFuncSetAttribute(k_pat<CH, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
     const int reg = reg_bytes / CH;
     // whole regions only, so every pattern reads the same byte count
