@@ -462,18 +462,18 @@ __global__ void __launch_bounds__(256, 2) k_sym_gemv_tma(
     for (;;) {
       if (cs >= s1) return;
       const int slot = nreq % R;
+      if (cabytes > 0) {   // the subdomain's A'' chunk first: it lands while the CTA is between tile loops
+        if (lane == 0) tma_load_1d_plain(wring + (size_t)slot * 1024, abc + caoff, (uint32_t)cabytes, wfull + slot);
+        ++nreq;
+        cabytes = 0;
+        return;
+      }
       if (ct < cnt) {
         if (lane == 0)
           tma_load_1d(wring + (size_t)slot * 1024, tiles + ctoff + (size_t)ct * 1024, kSymTileBytes,
                       wfull + slot, pol);
         ++nreq;
         ct += kSymWarps;
-        return;
-      }
-      if (cabytes > 0) {
-        if (lane == 0) tma_load_1d_plain(wring + (size_t)slot * 1024, abc + caoff, (uint32_t)cabytes, wfull + slot);
-        ++nreq;
-        cabytes = 0;
         return;
       }
       cs += G;
@@ -562,6 +562,26 @@ __global__ void __launch_bounds__(256, 2) k_sym_gemv_tma(
       if (stream_a) na = dp_chunks(dps[s], d.ns);
       if (na == 0) fused_dp_t(dps[s], abc, xs, d.ns, tbuf, (flags & 4) && !stream_a ? cgp : nullptr);
     }
+    if (STORE_V && warp < na) {   // this warp's A'' chunk: the first item of its stream for this subdomain
+      const DpSub p = dps[s];
+      const int slot = ncons % R;
+      mbar_wait_parity(wfull + slot, (uint32_t)(ncons / R) & 1u);
+      ++ncons;
+      const double* T = wring + (size_t)slot * 1024;
+      const int sh = p.nc == 8 ? 3 : p.nc == 4 ? 2 : 1;
+      const int e0 = warp * 1024 + lane, tot = d.ns * p.nc;
+      double acc = 0.0;
+#pragma unroll 8
+      for (int k = 0; k < 32; ++k) {
+        const int e = e0 + 32 * k;
+        if (e < tot) acc = fma(T[lane + 32 * k], xs[e >> sh], acc);
+      }
+      __syncwarp();
+      if (lane == 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      request_next();
+      for (int o = 16; o >= p.nc; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (lane < p.nc) tpart[warp][lane] = acc;
+    }
     double* pw = part + warp * npad;
     const int ntiles = d.nb * (d.nb + 1) / 2;
     int it = 0;
@@ -625,26 +645,6 @@ __global__ void __launch_bounds__(256, 2) k_sym_gemv_tma(
         bj -= bi + 1;
         ++bi;
       }
-    }
-    if (STORE_V && warp < na) {   // this warp's A'' chunk: the next item of its stream after its tiles
-      const DpSub p = dps[s];
-      const int slot = ncons % R;
-      mbar_wait_parity(wfull + slot, (uint32_t)(ncons / R) & 1u);
-      ++ncons;
-      const double* T = wring + (size_t)slot * 1024;
-      const int sh = p.nc == 8 ? 3 : p.nc == 4 ? 2 : 1;
-      const int e0 = warp * 1024 + lane, tot = d.ns * p.nc;
-      double acc = 0.0;
-#pragma unroll 8
-      for (int k = 0; k < 32; ++k) {
-        const int e = e0 + 32 * k;
-        if (e < tot) acc = fma(T[lane + 32 * k], xs[e >> sh], acc);
-      }
-      __syncwarp();
-      if (lane == 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      request_next();
-      for (int o = 16; o >= p.nc; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-      if (lane < p.nc) tpart[warp][lane] = acc;
     }
     __syncthreads();
     if (STORE_V && na > 0 && (int)threadIdx.x < dps[s].nc) {   // t_s: chunk partials in chunk order
